@@ -1,0 +1,186 @@
+/*
+ * paraq_b200.h -- C ABI of the B200-native fast-DQN hot path
+ * (arXiv 2111.01264: concurrent training + synchronized execution).
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t passed
+ * as void*, returns 0 on success and a nonzero status on error (pq_last_error()
+ * gives the message; the Python shim maps it to ValueError / RuntimeError like
+ * the reference).  No torch types cross this boundary.  All kernels are sm_100a.
+ *
+ * Reference interfaces each group replaces (paths under /root/reference/pkg/src/paraq):
+ *   replay sampling ..... replay.py:61-66   ReplayMemory.sample -> rng.integers(0, len, B)
+ *   replay flush ........ replay.py:82-93   ReplayMemory.flush (owner-major order)
+ *   prepopulation ....... replay.py:68-80   ReplayMemory.prepopulate
+ *   batch gather ........ agent.py:76,:100  np.stack of states / next states
+ *   Q forward ........... nn.py:123-131     forward  (kernels affine_rows/relu, _kernels_numba.py:19-42)
+ *   learner step ........ agent.py:84-105   train_minibatch = td_targets (agent.py:69-81)
+ *                                           + gradient (nn.py:134-170) + rmsprop_step (nn.py:173-203)
+ *   acting .............. executor.py:106-112 batched_inference + agent.py:53-66 select_action
+ *                                           + executor.py:237-249 _sampler_step
+ *   target sync ......... nn.py:206-211     copy_parameters (executor.py:559)
+ *   theta hash .......... nn.py:214-229     parameter_bytes + theta_hash (FNV-1a 64)
+ *   kernel plugin ....... backend.py:18-34 / _kernels_numba.py:19-111 (fp64 kernel module)
+ */
+#ifndef PARAQ_B200_H
+#define PARAQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PQ_ABI_VERSION 1
+#define PQ_FRAME_BYTES 7056 /* one 84x84 uint8 frame */
+#define PQ_REC_INTS 8       /* replay record: frame slots f0..f4, action, reward (f32 bits), terminal */
+
+/* ---- housekeeping ---------------------------------------------------------- */
+int pq_abi_version(void);
+const char *pq_last_error(void);
+int64_t pq_num_params(int actions);          /* 1,693,362 for 18 actions */
+int64_t pq_num_shadow(void);                 /* bf16 copies of the conv1..fc1 weights */
+
+/* ---- one Q-network parameter set (theta or theta-minus), device memory ------------ */
+typedef struct pq_net {
+    float *master;     /* fp32 [pq_num_params] in nn.parameter_bytes order */
+    uint16_t *shadow;  /* bf16 [pq_num_shadow] GEMM copies of W1..W4 */
+} pq_net;
+
+typedef struct pq_opt {
+    float *m; /* first moments  (nn.OptState.m_*) */
+    float *v; /* second moments (nn.OptState.v_*) */
+} pq_opt;
+
+/* Refresh the bf16 shadow from the fp32 master (after an upload). */
+int pq_net_sync_shadow(pq_net net, void *stream);
+/* theta-minus <- theta (copy_parameters, nn.py:206-211; executor.py:559) */
+int pq_net_copy(pq_net dst, pq_net src, int actions, void *stream);
+
+/* ---- frame-stack addressing -------------------------------------------------------
+ * A state is 4 frames; frames live in a uint8 ring [slots][7056].  Sample b,
+ * channel c reads slot refs[map(b) * ref_stride + ref_off + c] (map = identity when
+ * NULL); slot -1 is the all-zero (masked) frame.  Replay records [cap][8] int32 are
+ * {f0, f1, f2, f3, f4, action, reward_bits, terminal}: state = (f0..f3), next state =
+ * (f1..f4), so ref_off 0 / 1 selects s / s'. */
+
+/* ---- replay (replay.py) ----------------------------------------------------------- */
+/* rng.integers(0, n, size=count), bit-exact with numpy PCG64 + buffered Lemire;
+ * pcg_state: device u64[6] {state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger},
+ * updated in place.  1 <= n < 2^32. */
+int pq_sample_indices(uint64_t *pcg_state, uint32_t n, int64_t count, int64_t *idx_out,
+                      void *stream);
+/* Stack gather of a sampled batch: s_out / s2_out [B][4][84][84] uint8,
+ * a_out int32 [B], r_out f32 [B], term_out uint8 [B]. */
+int pq_replay_gather(const uint8_t *ring, const int32_t *records, const int64_t *idx,
+                     int64_t B, uint8_t *s_out, uint8_t *s2_out, int32_t *a_out, float *r_out,
+                     uint8_t *term_out, void *stream);
+/* Flush: staging records [W][steps][8] -> ring records in owner-major order,
+ * slot = (push_count + j * steps + k) mod capacity. */
+int pq_replay_flush(const int32_t *staging, int W, int steps, int32_t *records,
+                    int64_t capacity, int64_t push_count, void *stream);
+
+/* ---- synthetic frame environments (caller side, oracle/envs.py on the CPU) -------- */
+typedef struct pq_envs {
+    uint64_t *pcg;       /* [W][6] per-sampler PCG64 streams (executor.py:59-63) */
+    int64_t *episode;    /* [W] episode index */
+    int32_t *t;          /* [W] steps into the episode */
+    int32_t *stack;      /* [W][4] frame slots of the current state (-1 = masked) */
+    double *ep_return;   /* [W] running return */
+    uint64_t *key;       /* [W] frame-hash key */
+    int64_t *slot_next;  /* [W] next frame sequence number of this env (slot = seq mod ring size) */
+    int32_t *ep_count;   /* [W] episodes finished this epoch */
+    int64_t *ep_label;   /* [W][steps] t_label of finished episodes */
+    double *ep_ret;      /* [W][steps] their returns */
+    int32_t *actions;    /* [W] last actions (read back by the host API) */
+} pq_envs;
+
+/* Reset env j into frame slot slots[j] (episode start, masked stack). */
+int pq_env_reset(pq_envs envs, int W, const int32_t *slots, uint8_t *ring, void *stream);
+
+/* Prepopulation (replay.py:68-80) of n transitions from one env on the PREPOP
+ * stream: frames into ring slots [frame_base, frame_base + used), records into
+ * rec_out[n][8]; *frames_used_out (device int64) receives the slot count. */
+int pq_prepopulate(uint64_t *pcg_state, uint64_t key, int episode_length, int actions,
+                   double terminal_p, int64_t n, uint8_t *ring, int64_t frame_base,
+                   int64_t frame_capacity, int32_t *rec_out, int64_t *frames_used_out,
+                   void *scratch, void *stream);
+size_t pq_prepopulate_scratch_bytes(int64_t n);
+
+/* ---- Q network (nn.py / agent.py) -------------------------------------------------- */
+size_t pq_workspace_bytes(int max_batch, int actions);
+/* Byte offsets of the workspace buffers (stage-wise kernel tests), in order:
+ * act1, act2, act3, fc1part (online), act1, act2, act3, fc1part (target), q, h1, dh1,
+ * td, dh1_bf16, dh1T_bf16, actions, dY3, dY2, dY1, part1, part2, part3, grad4. */
+int pq_workspace_layout(int max_batch, int actions, int64_t *offsets);
+
+/* Q-values for n states (nn.forward): q_out f32 [n][actions]. */
+int pq_forward(pq_net net, const uint8_t *ring, const int32_t *refs, const int64_t *map,
+               int ref_stride, int ref_off, int n, int actions, float *q_out, void *ws,
+               int max_batch, void *stream);
+
+typedef struct pq_learn_args {
+    pq_net theta;          /* read */
+    pq_opt opt;            /* read */
+    pq_net theta_out;      /* written (may alias theta: elementwise update) */
+    pq_opt opt_out;        /* written (may alias opt) */
+    pq_net target;         /* theta-minus, read */
+    const uint8_t *ring;
+    const int32_t *records;
+    const int64_t *idx;          /* [n] sampled record slots; NULL -> idx_base + counter */
+    const int64_t *idx_base;     /* epoch index table, sliced by *update_counter */
+    int32_t *update_counter;     /* device counter, incremented per step (graph replay) */
+    const float *ext_targets;    /* optional: fixed targets (nn.gradient), skips the TD head */
+    const int32_t *ext_actions;
+    int n, actions;
+    float gamma, lr, rho, kappa;
+    int32_t *nonfinite;          /* device int: min update id with a non-finite gradient */
+    float *grad_out;             /* optional f32 [num_params]: summed gradient */
+    float *q_out;                /* optional f32 [2][n][actions]: online / target Q */
+    float *td_out;               /* optional f32 [n][3]: target, delta, loss */
+    void *ws;
+    int max_batch;
+} pq_learn_args;
+
+/* One learner step (agent.train_minibatch): target forward + max, online forward,
+ * TD error, backward, centered RMSProp on the summed gradient. */
+int pq_learn_step(const pq_learn_args *args, void *stream);
+
+typedef struct pq_act_args {
+    pq_net net;                 /* acting parameters (theta-minus when concurrent) */
+    pq_envs envs;
+    uint8_t *ring;
+    int32_t *staging;           /* [W][steps][8] transition records of this epoch */
+    int32_t *step_counter;      /* device block counter bg: t_label = epoch_start + bg*W + j + 1,
+                                   staging row = bg mod steps; incremented per call */
+    int W, steps, actions, episode_length;
+    int64_t epoch_start;        /* global step at the epoch start (t labels) */
+    int64_t frame_capacity;     /* frame ring slots */
+    double eps_start, eps_end;
+    int64_t eps_anneal;
+    double terminal_p;
+    float *q_out;               /* optional [W][actions] */
+    void *ws;
+    int max_batch;
+} pq_act_args;
+
+/* One synchronized block (executor.py:451-510): batched Q inference for the W current
+ * states, epsilon-greedy per sampler on its own PCG64 stream (agent.py:53-66), env
+ * step, transition record into staging, episode bookkeeping and reset. */
+int pq_act_step(const pq_act_args *args, void *stream);
+
+/* ---- elementwise kernels of the reference kernel module (fp32 / fp64) ------------- */
+int pq_rmsprop_f32(const float *p, const float *g, const float *m, const float *v, int64_t n,
+                   float lr, float rho, float kappa, float *p2, float *m2, float *v2,
+                   int32_t *nonfinite, void *stream);
+
+/* ---- host-side helpers ---------------------------------------------------------- */
+/* theta_hash (nn.py:223-229): FNV-1a 64 over the little-endian float64 bytes of the
+ * parameters (fp32 master widened to f64), layer order weights then bias. */
+uint64_t pq_theta_hash_f32(const float *host_params, int64_t n);
+uint64_t pq_theta_hash_f64(const double *host_params, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARAQ_B200_H */

@@ -1,0 +1,272 @@
+// Shared device helpers for the sm_100a fast-DQN hot path: PTX wrappers for
+// mbarrier / tcgen05 (TMEM alloc, UMMA issue, commit, TMEM load), UMMA smem
+// descriptors, bf16 packing and the numpy-compatible PCG64 generator.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PQ_DEV __device__ __forceinline__
+
+namespace pq {
+
+// ---------------------------------------------------------------- smem / mbarrier
+PQ_DEV uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+PQ_DEV void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+PQ_DEV void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+PQ_DEV bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+PQ_DEV void mbar_wait(uint64_t *bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+// generic-proxy smem writes -> visible to the async proxy (UMMA operand reads)
+PQ_DEV void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- tcgen05 / TMEM
+template <uint32_t NCOLS>
+PQ_DEV void tmem_alloc(uint32_t *dst_smem) {  // whole warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(dst_smem)),
+                 "n"(NCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+template <uint32_t NCOLS>
+PQ_DEV void tmem_dealloc(uint32_t taddr) {  // whole warp
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS)
+                 : "memory");
+}
+
+PQ_DEV void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+PQ_DEV void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// D[tmem] (+)= A[smem] * B[smem]^T, bf16 inputs, fp32 accumulate (kind::f16)
+PQ_DEV void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                      uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// arrive on an mbarrier once every previously issued UMMA of this thread completes
+PQ_DEV void umma_commit(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+// TMEM -> registers: 32 lanes x 32 consecutive 32-bit columns (one per register)
+PQ_DEV void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+PQ_DEV void tmem_ld16(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+#pragma unroll
+    for (int i = 16; i < 32; ++i) v[i] = 0.f;
+}
+
+// ---------------------------------------------------------------- UMMA descriptors
+// 128B-swizzled canonical layouts (bf16):
+//  K-major : rows of 64 K-elements (128 B), 8-row atoms of 1024 B at SBO = 1024.
+//  MN-major: rows of 64 MN-elements (128 B) per K index, 8-K-row atoms of 1024 B at
+//            SBO = 1024 (K direction), MN atoms at LBO = 64 * 128 B = 8192 (BK = 64).
+PQ_DEV uint64_t desc_sw128(uint32_t saddr, uint32_t lbo_bytes) {
+    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)(1024u >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// instruction descriptor: bf16 x bf16 -> f32, M = 128, N, majors
+__host__ __device__ constexpr uint32_t idesc_bf16(int N, bool a_mn, bool b_mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) |
+           ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+// byte offset of the 16-byte chunk (row, chunk) inside a K-major SW128 tile
+PQ_DEV uint32_t kmaj_off(int row, int c8) {
+    return (uint32_t)(row * 128 + ((c8 ^ (row & 7)) << 4));
+}
+// byte offset of chunk (k, m8) inside an MN-major SW128 tile with BK = 64
+PQ_DEV uint32_t mnmaj_off(int k, int m8) {
+    return (uint32_t)((m8 >> 3) * 8192 + (k >> 3) * 1024 + (k & 7) * 128 +
+                      (((m8 & 7) ^ (k & 7)) << 4));
+}
+
+// ---------------------------------------------------------------- bf16 helpers
+PQ_DEV uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+PQ_DEV float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+PQ_DEV float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+
+// 8 unsigned bytes -> 8 bf16 (exact: integers <= 255 are representable)
+PQ_DEV uint4 u8x8_to_bf16(uint32_t lo, uint32_t hi) {
+    uint4 r;
+    r.x = pack_bf16((float)(lo & 0xFF), (float)((lo >> 8) & 0xFF));
+    r.y = pack_bf16((float)((lo >> 16) & 0xFF), (float)(lo >> 24));
+    r.z = pack_bf16((float)(hi & 0xFF), (float)((hi >> 8) & 0xFF));
+    r.w = pack_bf16((float)((hi >> 16) & 0xFF), (float)(hi >> 24));
+    return r;
+}
+
+// ---------------------------------------------------------------- PCG64 (numpy)
+// state layout (u64[6]): state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger
+struct U128 {
+    uint64_t hi, lo;
+};
+PQ_DEV U128 mul128(U128 a, U128 b) {
+    U128 r;
+    r.lo = a.lo * b.lo;
+    r.hi = __umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo;
+    return r;
+}
+PQ_DEV U128 add128(U128 a, U128 b) {
+    U128 r;
+    r.lo = a.lo + b.lo;
+    r.hi = a.hi + b.hi + (r.lo < a.lo ? 1ull : 0ull);
+    return r;
+}
+__device__ constexpr uint64_t PCG_MULT_HI = 0x2360ED051FC65DA4ULL;
+__device__ constexpr uint64_t PCG_MULT_LO = 0x4385DF649FCCF645ULL;
+
+PQ_DEV uint64_t pcg_output(U128 s) {
+    uint64_t x = s.hi ^ s.lo;
+    unsigned rot = (unsigned)(s.hi >> 58);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+struct Pcg64 {
+    U128 state, inc;
+    uint32_t has32, buf;
+
+    PQ_DEV void load(const uint64_t *s) {
+        state = {s[0], s[1]};
+        inc = {s[2], s[3]};
+        has32 = (uint32_t)s[4];
+        buf = (uint32_t)s[5];
+    }
+    PQ_DEV void store(uint64_t *s) const {
+        s[0] = state.hi;
+        s[1] = state.lo;
+        s[2] = inc.hi;
+        s[3] = inc.lo;
+        s[4] = has32;
+        s[5] = buf;
+    }
+    PQ_DEV uint64_t next64() {
+        state = add128(mul128(state, U128{PCG_MULT_HI, PCG_MULT_LO}), inc);
+        return pcg_output(state);
+    }
+    PQ_DEV uint32_t next32() {
+        if (has32) {
+            has32 = 0;
+            return buf;
+        }
+        uint64_t v = next64();
+        has32 = 1;
+        buf = (uint32_t)(v >> 32);
+        return (uint32_t)v;
+    }
+    // Generator.random()
+    PQ_DEV double random() {
+        return (double)(next64() >> 11) * (1.0 / 9007199254740992.0);
+    }
+    // Generator.integers(0, n) for 1 <= n < 2^32 (buffered Lemire, rng = n - 1)
+    PQ_DEV uint32_t bounded(uint32_t n) {
+        if (n <= 1) return 0;
+        uint64_t m = (uint64_t)next32() * n;
+        uint32_t left = (uint32_t)m;
+        if (left < n) {
+            uint32_t threshold = (0u - n) % n;  // (2^32 - n) mod n
+            while (left < threshold) {
+                m = (uint64_t)next32() * n;
+                left = (uint32_t)m;
+            }
+        }
+        return (uint32_t)(m >> 32);
+    }
+};
+
+// LCG jump-ahead by delta steps (pcg_advance_lcg_128)
+PQ_DEV U128 pcg_advance(U128 state, U128 inc, uint64_t delta) {
+    U128 acc_mult{0, 1}, acc_plus{0, 0}, cur_mult{PCG_MULT_HI, PCG_MULT_LO}, cur_plus = inc;
+    while (delta > 0) {
+        if (delta & 1) {
+            acc_mult = mul128(acc_mult, cur_mult);
+            acc_plus = add128(mul128(acc_plus, cur_mult), cur_plus);
+        }
+        cur_plus = mul128(add128(cur_mult, U128{0, 1}), cur_plus);
+        cur_mult = mul128(cur_mult, cur_mult);
+        delta >>= 1;
+    }
+    return add128(mul128(acc_mult, state), acc_plus);
+}
+
+// ---------------------------------------------------------------- misc
+PQ_DEV uint64_t splitmix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+}  // namespace pq

@@ -1,0 +1,214 @@
+// Synchronized execution on the device: one lockstep block of W samplers.
+//
+//   executor.py:451-510 run_epoch_lockstep / barrier_action -> pq_act_step
+//     batched_inference (executor.py:106-112)   -> F1..F4 GEMMs over the W current stacks
+//     select_action (agent.py:53-66)           -> k_act_env: explore = random() < eps,
+//                                                 integers(A) when exploring, else argmax
+//                                                 with lowest-index ties, on sampler j's
+//                                                 own PCG64 stream (executor.py:59-63)
+//     _sampler_step (executor.py:237-249)      -> env.step on the same stream, transition
+//                                                 record into the sampler buffer (staging),
+//                                                 bootstrap terminal = terminal && !truncated,
+//                                                 episode log, reset
+//   epsilon_at (agent.py:44-50) is evaluated in fp64 with the reference formula.
+// The environment is the synthetic frame env of oracle/envs.py (reward draw, terminal
+// draw, counter-hashed 84x84 frames, 4-frame stack with masked history).
+#include "../../include/paraq_b200.h"
+#include "common.cuh"
+#include "qnet.cuh"
+
+namespace pq {
+int set_err(const char *msg);
+int cuda_err(cudaError_t e, const char *where);
+int act_forward(pq_net net, const uint8_t *ring, const int32_t *stack, int W, int A, void *ws,
+                int max_batch, const float **part_out, cudaStream_t st);
+
+__device__ __forceinline__ uint64_t env_frame_base(uint64_t key, int64_t episode, int t, int action) {
+    return splitmix64(splitmix64(splitmix64(key) ^ (uint64_t)episode) ^
+                      (((uint64_t)t << 8) | (uint64_t)action));
+}
+
+__device__ __forceinline__ double epsilon_at(int64_t t, double start, double end, int64_t anneal) {
+    if (t >= anneal || anneal == 1) return end;
+    double frac = (double)(t - 1) / (double)(anneal - 1);
+    return __dadd_rn(start, __dmul_rn(__dsub_rn(end, start), frac));
+}
+
+struct ActArgs {
+    const float *part;   // fc1 partials [S][W][512]
+    const float *master;
+    pq_envs e;
+    uint8_t *ring;
+    int32_t *staging;
+    const int32_t *step_counter;
+    int W, steps, A, L;
+    int64_t epoch_start, frame_capacity;
+    double eps_start, eps_end;
+    int64_t eps_anneal;
+    double term_p;
+    float *q_out;
+};
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(128) k_act_env(const ActArgs a) {
+    const int j = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    __shared__ float red[4][MAX_ACTIONS];
+    __shared__ float qs[MAX_ACTIONS];
+    __shared__ uint64_t s_base[2];
+    __shared__ int64_t s_slot[2];
+    float h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int jj = tid + 128 * i;
+        float s = 0.f;
+        for (int sp = 0; sp < FC1_SPLITS; ++sp) s += a.part[((size_t)sp * a.W + j) * 512 + jj];
+        s += a.master[P_B4 + jj];
+        h[i] = s > 0.f ? s : 0.f;
+    }
+    for (int aa = 0; aa < a.A; ++aa) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc += a.master[P_W5 + aa * 512 + tid + 128 * i] * h[i];
+        acc = warp_sum_f(acc);
+        if (lane == 0) red[warp][aa] = acc;
+    }
+    __syncthreads();
+    if (tid < a.A) {
+        float q = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid] + a.master[p_b5(a.A) + tid];
+        qs[tid] = q;
+        if (a.q_out) a.q_out[j * a.A + tid] = q;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        // step_counter counts lockstep blocks (run-global in the executor); the
+        // staging row is the block index within the epoch
+        const int64_t bg = *a.step_counter;
+        const int b = (int)(bg % a.steps);
+        const int64_t t_label = a.epoch_start + bg * a.W + j + 1;
+        const double eps = epsilon_at(t_label, a.eps_start, a.eps_end, a.eps_anneal);
+        Pcg64 g;
+        g.load(a.e.pcg + j * 6);
+        int act;
+        if (g.random() < eps) {
+            act = (int)g.bounded((uint32_t)a.A);
+        } else {
+            act = 0;
+            for (int aa = 1; aa < a.A; ++aa)
+                if (qs[aa] > qs[act]) act = aa;
+        }
+        // env.step(action, rng): reward draw, terminal draw, next frame
+        double reward = g.random();
+        bool term = g.random() < a.term_p;
+        int t = a.e.t[j] + 1;
+        int64_t ep = a.e.episode[j];
+        int64_t seq = a.e.slot_next[j];
+        int32_t fs = (int32_t)(seq % a.frame_capacity);
+        s_slot[0] = fs;
+        s_base[0] = env_frame_base(a.e.key[j], ep, t, act);
+        bool trunc = !term && t >= a.L;
+        int32_t *st4 = a.e.stack + j * 4;
+        int32_t *rec = a.staging + ((int64_t)j * a.steps + b) * REC_INTS;
+        rec[0] = st4[0], rec[1] = st4[1], rec[2] = st4[2], rec[3] = st4[3], rec[4] = fs;
+        rec[5] = act;
+        rec[6] = __float_as_int((float)reward);
+        rec[7] = term ? 1 : 0;
+        double ret = a.e.ep_return[j] + reward;
+        s_slot[1] = -1;
+        if (term || trunc) {
+            int c = a.e.ep_count[j];
+            a.e.ep_label[(int64_t)j * a.steps + c] = t_label;
+            a.e.ep_ret[(int64_t)j * a.steps + c] = ret;
+            a.e.ep_count[j] = c + 1;
+            ret = 0.0;
+            ep += 1;
+            t = 0;
+            int32_t rs = (int32_t)((seq + 1) % a.frame_capacity);
+            s_slot[1] = rs;
+            s_base[1] = env_frame_base(a.e.key[j], ep, 0, 255);
+            st4[0] = st4[1] = st4[2] = -1;
+            st4[3] = rs;
+            a.e.slot_next[j] = seq + 2;
+        } else {
+            st4[0] = st4[1], st4[1] = st4[2], st4[2] = st4[3], st4[3] = fs;
+            a.e.slot_next[j] = seq + 1;
+        }
+        a.e.ep_return[j] = ret;
+        a.e.t[j] = t;
+        a.e.episode[j] = ep;
+        a.e.actions[j] = act;
+        g.store(a.e.pcg + j * 6);
+    }
+    __syncthreads();
+    for (int f = 0; f < 2; ++f) {
+        if (s_slot[f] < 0) continue;
+        uint64_t *d = reinterpret_cast<uint64_t *>(a.ring + (size_t)s_slot[f] * FRAME_BYTES);
+        for (int p = tid; p < FRAME_BYTES / 8; p += blockDim.x) d[p] = splitmix64(s_base[f] + (uint64_t)p);
+    }
+}
+
+__global__ void k_env_reset(pq_envs e, int W, const int32_t *slots, uint8_t *ring) {
+    const int j = blockIdx.x;
+    __shared__ uint64_t base;
+    if (threadIdx.x == 0) {
+        int64_t ep = e.episode[j] + 1;
+        e.episode[j] = ep;
+        e.t[j] = 0;
+        e.ep_return[j] = 0.0;
+        int32_t *st4 = e.stack + j * 4;
+        st4[0] = st4[1] = st4[2] = -1;
+        st4[3] = slots[j];
+        base = env_frame_base(e.key[j], ep, 0, 255);
+    }
+    __syncthreads();
+    uint64_t *d = reinterpret_cast<uint64_t *>(ring + (size_t)slots[j] * FRAME_BYTES);
+    for (int p = threadIdx.x; p < FRAME_BYTES / 8; p += blockDim.x) d[p] = splitmix64(base + (uint64_t)p);
+}
+
+__global__ void k_bump_counter(int32_t *c) { *c += 1; }
+
+}  // namespace pq
+
+using namespace pq;
+
+extern "C" {
+
+int pq_env_reset(pq_envs envs, int W, const int32_t *slots, uint8_t *ring, void *stream) {
+    if (W <= 0) return 0;
+    k_env_reset<<<W, 128, 0, (cudaStream_t)stream>>>(envs, W, slots, ring);
+    return cuda_err(cudaGetLastError(), "env_reset");
+}
+
+int pq_act_step(const pq_act_args *x, void *stream) {
+    if (x->W < 1 || x->W > x->max_batch) return set_err("W out of range for the workspace");
+    if (x->actions < 1 || x->actions > MAX_ACTIONS) return set_err("actions must be in [1, 32]");
+    cudaStream_t st = (cudaStream_t)stream;
+    const float *part = nullptr;
+    int rc = act_forward(x->net, x->ring, x->envs.stack, x->W, x->actions, x->ws, x->max_batch,
+                         &part, st);
+    if (rc) return rc;
+    ActArgs a{};
+    a.part = part;
+    a.master = x->net.master;
+    a.e = x->envs;
+    a.ring = x->ring;
+    a.staging = x->staging;
+    a.step_counter = x->step_counter;
+    a.W = x->W, a.steps = x->steps, a.A = x->actions, a.L = x->episode_length;
+    a.epoch_start = x->epoch_start;
+    a.frame_capacity = x->frame_capacity;
+    a.eps_start = x->eps_start, a.eps_end = x->eps_end, a.eps_anneal = x->eps_anneal;
+    a.term_p = x->terminal_p;
+    a.q_out = x->q_out;
+    k_act_env<<<x->W, 128, 0, st>>>(a);
+    rc = cuda_err(cudaGetLastError(), "act_env");
+    if (rc) return rc;
+    k_bump_counter<<<1, 1, 0, st>>>(x->step_counter);
+    return cuda_err(cudaGetLastError(), "act counter");
+}
+
+}  // extern "C"

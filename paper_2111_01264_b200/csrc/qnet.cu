@@ -1,0 +1,657 @@
+// Nature-CNN Q-network forward, DQN learner step and fused centered RMSProp.
+//
+// Reference path restated (pkg/src/paraq):
+//   forward          nn.py:123-131   -> F1..F4 implicit GEMMs (tcgen05) + k_head
+//   td_targets       agent.py:69-81  -> k_head (target forward max, bootstrap)
+//   gradient         nn.py:134-170   -> k_head (output_delta, fc2 back-prop) +
+//                                       B4w/B4d, B3w/B3d, B2w/B2d, B1w GEMMs
+//   x n rescale      agent.py:103-104 -> delta = q - target (summed-gradient convention)
+//   rmsprop_step     nn.py:173-203   -> k_optimizer (split-K reduction + RMSProp + bf16
+//                                       shadow refresh + non-finite flag)
+#include <climits>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/paraq_b200.h"
+#include "gemm.cuh"
+#include "qnet.cuh"
+
+namespace pq {
+
+thread_local char g_err[512] = "";
+int set_err(const char *msg) {
+    snprintf(g_err, sizeof(g_err), "%s", msg);
+    return 1;
+}
+int cuda_err(cudaError_t e, const char *where) {
+    if (e == cudaSuccess) return 0;
+    snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+    return 2;
+}
+#define PQ_CHECK(expr, where)                          \
+    do {                                               \
+        int _rc = cuda_err((expr), where);             \
+        if (_rc) return _rc;                           \
+    } while (0)
+
+// ------------------------------------------------------------------ workspace
+static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct WS {
+    bf16 *act1[2], *act2[2], *act3[2];
+    float *fc1part[2];
+    float *q, *h1, *dh1, *td;
+    bf16 *dh1_bf, *dh1T;
+    int32_t *act;
+    bf16 *dY3, *dY2, *dY1;
+    float *part1, *part2, *part3, *grad4;
+    int n8;
+    size_t bytes;
+};
+
+static WS carve(void *base, int N, int A) {
+    WS w;
+    size_t off = 0;
+    char *b = static_cast<char *>(base);
+    auto take = [&](size_t bytes) -> void * {
+        void *p = b ? b + off : nullptr;
+        off += al(bytes);
+        return p;
+    };
+    int n8 = (N + 7) & ~7;
+    w.n8 = n8;
+    for (int g = 0; g < 2; ++g) {
+        w.act1[g] = (bf16 *)take((size_t)N * 400 * 32 * 2);
+        w.act2[g] = (bf16 *)take((size_t)N * 81 * 64 * 2);
+        w.act3[g] = (bf16 *)take((size_t)N * 3136 * 2);
+        w.fc1part[g] = (float *)take((size_t)FC1_SPLITS * N * 512 * 4);
+    }
+    w.q = (float *)take((size_t)2 * N * A * 4);
+    w.h1 = (float *)take((size_t)N * 512 * 4);
+    w.dh1 = (float *)take((size_t)N * 512 * 4);
+    w.td = (float *)take((size_t)N * 3 * 4);
+    w.dh1_bf = (bf16 *)take((size_t)N * 512 * 2);
+    w.dh1T = (bf16 *)take((size_t)512 * n8 * 2);
+    w.act = (int32_t *)take((size_t)N * 4);
+    w.dY3 = (bf16 *)take((size_t)N * 3136 * 2);
+    w.dY2 = (bf16 *)take((size_t)N * 81 * 64 * 2);
+    w.dY1 = (bf16 *)take((size_t)N * 400 * 32 * 2);
+    w.part1 = (float *)take((size_t)MAX_SPLITS * 32 * 257 * 4);
+    w.part2 = (float *)take((size_t)MAX_SPLITS * 64 * 513 * 4);
+    w.part3 = (float *)take((size_t)MAX_SPLITS * 64 * 577 * 4);
+    w.grad4 = (float *)take((size_t)512 * 3136 * 4);
+    w.bytes = off;
+    return w;
+}
+
+// ------------------------------------------------------------------ forward GEMMs
+struct FwdInput {  // frame-stack addressing of one group
+    const uint8_t *ring;
+    const int32_t *refs;
+    const int64_t *map;
+    const int32_t *counter;  // optional: map += *counter * map_stride
+    int map_stride;
+    int ref_stride, ref_off;
+};
+
+}  // namespace pq
+
+// LoadFrames with a device-counter-sliced map (graph replay of the epoch index table)
+namespace pq {
+struct LoadFramesC {
+    LoadFrames f;
+    const int32_t *counter;
+    int map_stride;
+    PQ_DEV uint4 fetch(int m, int k) const {
+        if (counter && f.map) {
+            LoadFrames g2 = f;
+            g2.map = f.map + (int64_t)(*counter) * map_stride;
+            return g2.fetch(m, k);
+        }
+        return f.fetch(m, k);
+    }
+};
+
+static LoadFramesC frames_loader(const FwdInput &in, int n) {
+    LoadFramesC l;
+    l.f.ring = in.ring;
+    l.f.refs = in.refs;
+    l.f.map = in.map;
+    l.f.n = n;
+    l.f.ref_stride = in.ref_stride;
+    l.f.ref_off = in.ref_off;
+    l.counter = in.counter;
+    l.map_stride = in.map_stride;
+    return l;
+}
+
+static int choose_bn(int n) {
+    return n <= 16 ? 16 : n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256;
+}
+
+template <class LA, class LB, class EP, bool AMN, bool BMN>
+static cudaError_t launch_bn(int bn, const GemmArgs<LA, LB, EP> &g, int groups, cudaStream_t st) {
+    switch (bn) {
+        case 16: return launch_gemm<16, AMN, BMN>(g, groups, st);
+        case 32: return launch_gemm<32, AMN, BMN>(g, groups, st);
+        case 64: return launch_gemm<64, AMN, BMN>(g, groups, st);
+        case 128: return launch_gemm<128, AMN, BMN>(g, groups, st);
+        default: return launch_gemm<256, AMN, BMN>(g, groups, st);
+    }
+}
+
+// F1..F4 for `groups` parameter sets (group 0 / 1 = online / target in the learner)
+static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, int n, const WS &w,
+                         cudaStream_t st) {
+    {  // F1: conv1 8x8/4 over uint8 frames (K = 256), bias + ReLU, x 1/255
+        GemmArgs<LoadFramesC, LoadDense, EpiBiasRelu> g{};
+        for (int q = 0; q < groups; ++q) {
+            g.a[q] = frames_loader(ins[q], n);
+            g.b[q] = LoadDense{(const bf16 *)nets[q].shadow + S_W1, 32, 256, 256};
+            g.e[q] = EpiBiasRelu{w.act1[q], nets[q].master + P_B1, n * 400, 32, 32, 1.0f / 255.0f};
+        }
+        g.M = n * 400, g.N = 32, g.K = 256, g.kc_per_split = 4, g.splits = 1, g.ones_at = -1;
+        PQ_CHECK((launch_gemm<32, false, false>(g, groups, st)), "conv1 forward");
+    }
+    {  // F2: conv2 4x4/2 over 20x20x32 (K = 512)
+        GemmArgs<LoadIm2col, LoadDense, EpiBiasRelu> g{};
+        for (int q = 0; q < groups; ++q) {
+            g.a[q] = LoadIm2col{w.act1[q], n, 20, 20, 32, 4, 2, 9, 9};
+            g.b[q] = LoadDense{(const bf16 *)nets[q].shadow + S_W2, 64, 512, 512};
+            g.e[q] = EpiBiasRelu{w.act2[q], nets[q].master + P_B2, n * 81, 64, 64, 1.0f};
+        }
+        g.M = n * 81, g.N = 64, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
+        PQ_CHECK((launch_gemm<64, false, false>(g, groups, st)), "conv2 forward");
+    }
+    {  // F3: conv3 3x3/1 over 9x9x64 (K = 576)
+        GemmArgs<LoadIm2col, LoadDense, EpiBiasRelu> g{};
+        for (int q = 0; q < groups; ++q) {
+            g.a[q] = LoadIm2col{w.act2[q], n, 9, 9, 64, 3, 1, 7, 7};
+            g.b[q] = LoadDense{(const bf16 *)nets[q].shadow + S_W3, 64, 576, 576};
+            g.e[q] = EpiBiasRelu{w.act3[q], nets[q].master + P_B3, n * 49, 64, 64, 1.0f};
+        }
+        g.M = n * 49, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
+        PQ_CHECK((launch_gemm<64, false, false>(g, groups, st)), "conv3 forward");
+    }
+    {  // F4: fc1, swapped (D[j][b] = W4[j] . x[b]) with split-K partials [s][b][j]
+        GemmArgs<LoadDense, LoadDense, EpiF32T> g{};
+        for (int q = 0; q < groups; ++q) {
+            g.a[q] = LoadDense{(const bf16 *)nets[q].shadow + S_W4, 512, 3136, 3136};
+            g.b[q] = LoadDense{w.act3[q], n, 3136, 3136};
+            g.e[q] = EpiF32T{w.fc1part[q], 512, n, 512, (size_t)n * 512};
+        }
+        g.M = 512, g.N = n, g.K = 3136, g.kc_per_split = 49 / FC1_SPLITS, g.splits = FC1_SPLITS,
+        g.ones_at = -1;
+        PQ_CHECK((launch_bn<LoadDense, LoadDense, EpiF32T, false, false>(choose_bn(n), g, groups, st)),
+                 "fc1 forward");
+    }
+    return 0;
+}
+
+// ------------------------------------------------------------------ head kernel
+struct HeadArgs {
+    const float *part[2];
+    const float *master[2];
+    int groups, n, A, n8;
+    const int32_t *records;
+    const int64_t *idx;       // sampled slots, or
+    const int64_t *idx_base;  // epoch table sliced by *counter
+    const int32_t *counter;
+    const float *ext_targets;
+    const int32_t *ext_actions;
+    float gamma;
+    int learner;
+    float *q_out;  // [groups][n][A]
+    float *h1, *dh1, *td;
+    bf16 *dh1_bf, *dh1T;
+    int32_t *act_out;
+    float *q_copy;  // optional extra copy [groups][n][A]
+    float *td_copy; // optional [n][3]
+};
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// fc1 reduction + bias + ReLU, fc2, and (learner) TD target / error / fc2 back-prop.
+__global__ void __launch_bounds__(128) k_head(const HeadArgs a) {
+    const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    __shared__ float red[2][4][MAX_ACTIONS];
+    __shared__ float qs[2][MAX_ACTIONS];
+    __shared__ float s_delta;
+    __shared__ int s_act;
+    float h[2][4];
+    for (int g = 0; g < a.groups; ++g) {
+        const float *P = a.part[g];
+        const float *mp = a.master[g];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            int j = tid + 128 * i;
+            float s = 0.f;
+            for (int sp = 0; sp < FC1_SPLITS; ++sp) s += P[((size_t)sp * a.n + b) * 512 + j];
+            s += mp[P_B4 + j];
+            h[g][i] = s > 0.f ? s : 0.f;
+        }
+#pragma unroll 4
+        for (int aa = 0; aa < MAX_ACTIONS; ++aa) {
+            if (aa >= a.A) break;
+            float acc = 0.f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc += mp[P_W5 + aa * 512 + tid + 128 * i] * h[g][i];
+            acc = warp_sum(acc);
+            if (lane == 0) red[g][warp][aa] = acc;
+        }
+    }
+    __syncthreads();
+    if (tid < a.A) {
+        for (int g = 0; g < a.groups; ++g) {
+            float q = red[g][0][tid] + red[g][1][tid] + red[g][2][tid] + red[g][3][tid] +
+                      a.master[g][p_b5(a.A) + tid];
+            qs[g][tid] = q;
+            a.q_out[((size_t)g * a.n + b) * a.A + tid] = q;
+            if (a.q_copy) a.q_copy[((size_t)g * a.n + b) * a.A + tid] = q;
+        }
+    }
+    if (!a.learner) return;
+    __syncthreads();
+    if (tid == 0) {
+        int act;
+        float target;
+        if (a.ext_targets) {
+            act = a.ext_actions[b];
+            target = a.ext_targets[b];
+        } else {
+            int64_t slot = a.idx        ? a.idx[b]
+                           : a.idx_base ? a.idx_base[(int64_t)(*a.counter) * a.n + b]
+                                        : (int64_t)b;
+            const int32_t *rec = a.records + slot * REC_INTS;
+            act = rec[5];
+            float r = __int_as_float(rec[6]);
+            if (rec[7]) {
+                target = r;
+            } else {
+                float mx = qs[1][0];
+                for (int aa = 1; aa < a.A; ++aa) mx = fmaxf(mx, qs[1][aa]);
+                target = r + a.gamma * mx;
+            }
+        }
+        float q = qs[0][act];
+        float d = q - target;  // = n * output_delta (agent.py:103-104 summed gradient)
+        s_delta = d;
+        s_act = act;
+        a.act_out[b] = act;
+        a.td[b * 3 + 0] = target;
+        a.td[b * 3 + 1] = d;
+        a.td[b * 3 + 2] = 0.5f * d * d;
+        if (a.td_copy) {
+            a.td_copy[b * 3 + 0] = target;
+            a.td_copy[b * 3 + 1] = d;
+            a.td_copy[b * 3 + 2] = 0.5f * d * d;
+        }
+    }
+    __syncthreads();
+    const float d = s_delta;
+    const float *w5 = a.master[0] + P_W5 + (size_t)s_act * 512;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int j = tid + 128 * i;
+        float hv = h[0][i];
+        float g = hv > 0.f ? d * w5[j] : 0.f;  // hidden_delta with the fc1 ReLU mask
+        a.h1[(size_t)b * 512 + j] = hv;
+        a.dh1[(size_t)b * 512 + j] = g;
+        bf16 gb = __float2bfloat16_rn(g);
+        a.dh1_bf[(size_t)b * 512 + j] = gb;
+        a.dh1T[(size_t)j * a.n8 + b] = gb;
+    }
+}
+
+static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int learner,
+                const pq_learn_args *la, cudaStream_t st) {
+    HeadArgs h{};
+    for (int g = 0; g < groups; ++g) {
+        h.part[g] = w.fc1part[g];
+        h.master[g] = nets[g].master;
+    }
+    h.groups = groups, h.n = n, h.A = A, h.n8 = w.n8;
+    h.learner = learner;
+    h.q_out = w.q, h.h1 = w.h1, h.dh1 = w.dh1, h.td = w.td, h.dh1_bf = w.dh1_bf, h.dh1T = w.dh1T;
+    h.act_out = w.act;
+    if (la) {
+        h.records = la->records, h.idx = la->idx, h.idx_base = la->idx_base;
+        h.counter = la->update_counter, h.ext_targets = la->ext_targets;
+        h.ext_actions = la->ext_actions, h.gamma = la->gamma;
+        h.q_copy = la->q_out, h.td_copy = la->td_out;
+    }
+    k_head<<<n, 128, 0, st>>>(h);
+    return cuda_err(cudaGetLastError(), "head");
+}
+
+// ------------------------------------------------------------------ optimizer
+struct OptArgs {
+    const float *p, *m, *v;
+    float *p2, *m2, *v2;
+    bf16 *shadow;
+    const float *part1, *part2, *part3, *grad4;
+    int s1, s2, s3;
+    const float *dh1, *h1, *td;
+    const int32_t *act;
+    int n, A;
+    float lr, rho, kappa;
+    int32_t *flag;
+    int32_t *counter;  // update id source; incremented once per step
+    float *grad_out;
+    int64_t total;
+};
+
+__device__ __forceinline__ float sum_part(const float *part, int splits, size_t stride, size_t off) {
+    float s = 0.f;
+    for (int q = 0; q < splits; ++q) s += part[q * stride + off];
+    return s;
+}
+
+__global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.total) return;
+    float g;
+    int64_t sh = -1;
+    if (i < P_B1) {
+        int o = (int)(i >> 8), k = (int)(i & 255);
+        g = sum_part(a.part1, a.s1, 32 * 257, (size_t)o * 257 + k) * (1.0f / 255.0f);
+        sh = S_W1 + i;
+    } else if (i < P_W2) {
+        g = sum_part(a.part1, a.s1, 32 * 257, (size_t)(i - P_B1) * 257 + 256);
+    } else if (i < P_B2) {
+        int64_t r = i - P_W2;
+        g = sum_part(a.part2, a.s2, 64 * 513, (size_t)(r / 512) * 513 + (r % 512));
+        sh = S_W2 + r;
+    } else if (i < P_W3) {
+        g = sum_part(a.part2, a.s2, 64 * 513, (size_t)(i - P_B2) * 513 + 512);
+    } else if (i < P_B3) {
+        int64_t r = i - P_W3;
+        g = sum_part(a.part3, a.s3, 64 * 577, (size_t)(r / 576) * 577 + (r % 576));
+        sh = S_W3 + r;
+    } else if (i < P_W4) {
+        g = sum_part(a.part3, a.s3, 64 * 577, (size_t)(i - P_B3) * 577 + 576);
+    } else if (i < P_B4) {
+        g = a.grad4[i - P_W4];
+        sh = S_W4 + (i - P_W4);
+    } else if (i < P_W5) {
+        int j = (int)(i - P_B4);
+        g = 0.f;
+        for (int b = 0; b < a.n; ++b) g += a.dh1[(size_t)b * 512 + j];
+    } else if (i < p_b5(a.A)) {
+        int64_t r = i - P_W5;
+        int aa = (int)(r / 512), j = (int)(r % 512);
+        g = 0.f;
+        for (int b = 0; b < a.n; ++b)
+            if (a.act[b] == aa) g += a.td[b * 3 + 1] * a.h1[(size_t)b * 512 + j];
+    } else {
+        int aa = (int)(i - p_b5(a.A));
+        g = 0.f;
+        for (int b = 0; b < a.n; ++b)
+            if (a.act[b] == aa) g += a.td[b * 3 + 1];
+    }
+    if (a.grad_out) a.grad_out[i] = g;
+    if (!isfinite(g)) atomicMin(a.flag, a.counter ? *a.counter : 0);
+    // centered RMSProp, kappa inside the square root (_kernels_numba.py:98-111)
+    float mi = a.rho * a.m[i] + (1.0f - a.rho) * g;
+    float vi = a.rho * a.v[i] + (1.0f - a.rho) * g * g;
+    float pi = a.p[i] - a.lr * g / sqrtf(vi - mi * mi + a.kappa);
+    a.m2[i] = mi;
+    a.v2[i] = vi;
+    a.p2[i] = pi;
+    if (sh >= 0) a.shadow[sh] = __float2bfloat16_rn(pi);
+}
+
+__global__ void k_bump(int32_t *counter) { *counter += 1; }
+
+static int choose_kc(int nchunks, int mtiles, int *splits) {
+    int kc = (nchunks * mtiles + 147) / 148;
+    if (kc < 2) kc = 2;
+    int need = (nchunks + MAX_SPLITS - 1) / MAX_SPLITS;
+    if (kc < need) kc = need;
+    *splits = (nchunks + kc - 1) / kc;
+    return kc;
+}
+
+static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cudaStream_t st) {
+    const pq_net &th = la->theta;
+    const bf16 *sh = (const bf16 *)th.shadow;
+    int s1 = 1, s2 = 1, s3 = 1;
+    {  // B4w: dW4[j][k] = sum_b dh1[b][j] x3[b][k]  (contraction over the batch)
+        GemmArgs<LoadDense, LoadDense, EpiF32> g{};
+        g.a[0] = LoadDense{w.dh1T, 512, n, w.n8};
+        g.b[0] = LoadDense{w.act3[0], n, 3136, 3136};
+        g.e[0] = EpiF32{w.grad4, 512, 3136, 3136, 0};
+        g.M = 512, g.N = 3136, g.K = n, g.kc_per_split = (n + 63) / 64, g.splits = 1, g.ones_at = -1;
+        PQ_CHECK((launch_gemm<64, false, true>(g, 1, st)), "fc1 wgrad");
+    }
+    {  // B4d: dY3[b][k] = relu'(x3) * sum_j W4[j][k] dh1[b][j]   (D[k][b], MN-major W4)
+        GemmArgs<LoadDense, LoadDense, EpiMaskT> g{};
+        g.a[0] = LoadDense{sh + S_W4, 512, 3136, 3136};
+        g.b[0] = LoadDense{w.dh1_bf, n, 512, 512};
+        g.e[0] = EpiMaskT{w.dY3, w.act3[0], 3136, n, 3136};
+        g.M = 3136, g.N = n, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
+        PQ_CHECK((launch_bn<LoadDense, LoadDense, EpiMaskT, true, false>(choose_bn(n), g, 1, st)),
+                 "fc1 dgrad");
+    }
+    {  // B3w: dW3^T[k][o] = sum_m P3[m][k] dY3[m][o]; row 576 = ones -> bias grad
+        GemmArgs<LoadIm2col, LoadDense, EpiF32T> g{};
+        g.a[0] = LoadIm2col{w.act2[0], n, 9, 9, 64, 3, 1, 7, 7};
+        g.b[0] = LoadDense{w.dY3, n * 49, 64, 64};
+        g.e[0] = EpiF32T{w.part3, 577, 64, 577, (size_t)64 * 577};
+        int nch = (n * 49 + 63) / 64;
+        g.kc_per_split = choose_kc(nch, 5, &s3);
+        g.M = 577, g.N = 64, g.K = n * 49, g.splits = s3, g.ones_at = 576, g.ones_extent = n * 49;
+        PQ_CHECK((launch_gemm<64, true, true>(g, 1, st)), "conv3 wgrad");
+    }
+    {  // B3d: dY2 = relu'(x2) * transposed conv3(dY3)
+        GemmArgs<LoadTConv, LoadWeightT, EpiMask> g{};
+        g.a[0] = LoadTConv{w.dY3, n, 9, 9, 7, 7, 64, 3, 1};
+        g.b[0] = LoadWeightT{sh + S_W3, 64, 3, 64};
+        g.e[0] = EpiMask{w.dY2, w.act2[0], n * 81, 64, 64};
+        g.M = n * 81, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
+        PQ_CHECK((launch_gemm<64, false, true>(g, 1, st)), "conv3 dgrad");
+    }
+    {  // B2w
+        GemmArgs<LoadIm2col, LoadDense, EpiF32T> g{};
+        g.a[0] = LoadIm2col{w.act1[0], n, 20, 20, 32, 4, 2, 9, 9};
+        g.b[0] = LoadDense{w.dY2, n * 81, 64, 64};
+        g.e[0] = EpiF32T{w.part2, 513, 64, 513, (size_t)64 * 513};
+        int nch = (n * 81 + 63) / 64;
+        g.kc_per_split = choose_kc(nch, 5, &s2);
+        g.M = 513, g.N = 64, g.K = n * 81, g.splits = s2, g.ones_at = 512, g.ones_extent = n * 81;
+        PQ_CHECK((launch_gemm<64, true, true>(g, 1, st)), "conv2 wgrad");
+    }
+    {  // B2d: dY1 = relu'(x1) * transposed conv2(dY2)  (stride 2, K = 16 x 64)
+        GemmArgs<LoadTConv, LoadWeightT, EpiMask> g{};
+        g.a[0] = LoadTConv{w.dY2, n, 20, 20, 9, 9, 64, 4, 2};
+        g.b[0] = LoadWeightT{sh + S_W2, 64, 4, 32};
+        g.e[0] = EpiMask{w.dY1, w.act1[0], n * 400, 32, 32};
+        g.M = n * 400, g.N = 32, g.K = 1024, g.kc_per_split = 16, g.splits = 1, g.ones_at = -1;
+        PQ_CHECK((launch_gemm<64, false, true>(g, 1, st)), "conv2 dgrad");
+    }
+    {  // B1w: dW1^T[k][o] = sum_m P1[m][k] dY1[m][o] over uint8 frames; row 256 = ones
+        GemmArgs<LoadFramesC, LoadDense, EpiF32T> g{};
+        FwdInput in{la->ring, la->records, la->idx ? la->idx : la->idx_base,
+                    la->idx ? nullptr : la->update_counter, n, REC_INTS, 0};
+        g.a[0] = frames_loader(in, n);
+        g.b[0] = LoadDense{w.dY1, n * 400, 32, 32};
+        g.e[0] = EpiF32T{w.part1, 257, 32, 257, (size_t)32 * 257};
+        int nch = (n * 400 + 63) / 64;
+        g.kc_per_split = choose_kc(nch, 3, &s1);
+        g.M = 257, g.N = 32, g.K = n * 400, g.splits = s1, g.ones_at = 256, g.ones_extent = n * 400;
+        PQ_CHECK((launch_gemm<64, true, true>(g, 1, st)), "conv1 wgrad");
+    }
+    {
+        OptArgs o{};
+        o.p = th.master, o.m = la->opt.m, o.v = la->opt.v;
+        o.p2 = la->theta_out.master, o.m2 = la->opt_out.m, o.v2 = la->opt_out.v;
+        o.shadow = (bf16 *)la->theta_out.shadow;
+        o.part1 = w.part1, o.part2 = w.part2, o.part3 = w.part3, o.grad4 = w.grad4;
+        o.s1 = s1, o.s2 = s2, o.s3 = s3;
+        o.dh1 = w.dh1, o.h1 = w.h1, o.td = w.td, o.act = w.act;
+        o.n = n, o.A = la->actions;
+        o.lr = la->lr, o.rho = la->rho, o.kappa = la->kappa;
+        o.flag = la->nonfinite, o.counter = la->update_counter, o.grad_out = la->grad_out;
+        o.total = n_params(la->actions);
+        int blocks = (int)((o.total + 255) / 256);
+        k_optimizer<<<blocks, 256, 0, st>>>(o);
+        PQ_CHECK(cudaGetLastError(), "optimizer");
+        if (la->update_counter) {
+            k_bump<<<1, 1, 0, st>>>(la->update_counter);
+            PQ_CHECK(cudaGetLastError(), "counter");
+        }
+    }
+    return 0;
+}
+
+// ------------------------------------------------------------------ misc kernels
+__global__ void k_f32_to_bf16(const float *src, bf16 *dst, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+__global__ void k_rmsprop(const float *p, const float *g, const float *m, const float *v,
+                          int64_t n, float lr, float rho, float kappa, float *p2, float *m2,
+                          float *v2, int32_t *flag) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float gi = g[i];
+    if (!isfinite(gi) && flag) atomicMin(flag, 0);
+    float mi = rho * m[i] + (1.0f - rho) * gi;
+    float vi = rho * v[i] + (1.0f - rho) * gi * gi;
+    m2[i] = mi;
+    v2[i] = vi;
+    p2[i] = p[i] - lr * gi / sqrtf(vi - mi * mi + kappa);
+}
+
+// acting forward: F1..F4 over the W current stacks (refs [W][4]), fc1 partials out
+int act_forward(pq_net net, const uint8_t *ring, const int32_t *stack, int W, int A, void *ws,
+                int max_batch, const float **part_out, cudaStream_t st) {
+    WS w = carve(ws, max_batch, A);
+    FwdInput in{ring, stack, nullptr, nullptr, 0, 4, 0};
+    int rc = forward_gemms(&net, &in, 1, W, w, st);
+    *part_out = w.fc1part[0];
+    return rc;
+}
+
+}  // namespace pq
+
+using namespace pq;
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+int pq_abi_version(void) { return PQ_ABI_VERSION; }
+const char *pq_last_error(void) { return g_err; }
+int64_t pq_num_params(int actions) { return n_params(actions); }
+int64_t pq_num_shadow(void) { return S_TOTAL; }
+
+size_t pq_workspace_bytes(int max_batch, int actions) {
+    return carve(nullptr, max_batch, actions).bytes;
+}
+
+int pq_workspace_layout(int max_batch, int actions, int64_t *offsets) {
+    char *base = reinterpret_cast<char *>(size_t(1) << 40);
+    WS w = carve(base, max_batch, actions);
+    const void *ptrs[] = {w.act1[0], w.act2[0], w.act3[0], w.fc1part[0], w.act1[1], w.act2[1],
+                          w.act3[1], w.fc1part[1], w.q, w.h1, w.dh1, w.td, w.dh1_bf, w.dh1T,
+                          w.act, w.dY3, w.dY2, w.dY1, w.part1, w.part2, w.part3, w.grad4};
+    for (int i = 0; i < 22; ++i) offsets[i] = (const char *)ptrs[i] - base;
+    return 0;
+}
+
+int pq_net_sync_shadow(pq_net net, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t src_off[4] = {P_W1, P_W2, P_W3, P_W4};
+    const int64_t dst_off[4] = {S_W1, S_W2, S_W3, S_W4};
+    const int64_t cnt[4] = {8192, 32768, 36864, 1605632};
+    for (int l = 0; l < 4; ++l) {
+        k_f32_to_bf16<<<(unsigned)((cnt[l] + 255) / 256), 256, 0, st>>>(
+            net.master + src_off[l], (bf16 *)net.shadow + dst_off[l], cnt[l]);
+    }
+    return cuda_err(cudaGetLastError(), "sync_shadow");
+}
+
+int pq_net_copy(pq_net dst, pq_net src, int actions, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    PQ_CHECK(cudaMemcpyAsync(dst.master, src.master, n_params(actions) * 4,
+                             cudaMemcpyDeviceToDevice, st), "net_copy master");
+    PQ_CHECK(cudaMemcpyAsync(dst.shadow, src.shadow, S_TOTAL * 2, cudaMemcpyDeviceToDevice, st),
+             "net_copy shadow");
+    return 0;
+}
+
+int pq_forward(pq_net net, const uint8_t *ring, const int32_t *refs, const int64_t *map,
+               int ref_stride, int ref_off, int n, int actions, float *q_out, void *ws,
+               int max_batch, void *stream) {
+    if (n < 1 || n > max_batch) return set_err("batch size out of range for the workspace");
+    if (actions < 1 || actions > MAX_ACTIONS) return set_err("actions must be in [1, 32]");
+    cudaStream_t st = (cudaStream_t)stream;
+    WS w = carve(ws, max_batch, actions);
+    FwdInput in{ring, refs, map, nullptr, 0, ref_stride, ref_off};
+    int rc = forward_gemms(&net, &in, 1, n, w, st);
+    if (rc) return rc;
+    rc = head(&net, 1, n, actions, w, 0, nullptr, st);
+    if (rc) return rc;
+    if (q_out)
+        PQ_CHECK(cudaMemcpyAsync(q_out, w.q, (size_t)n * actions * 4, cudaMemcpyDeviceToDevice, st),
+                 "forward q copy");
+    return 0;
+}
+
+int pq_learn_step(const pq_learn_args *la, void *stream) {
+    const int n = la->n;
+    if (n < 1 || n > la->max_batch) return set_err("batch size out of range for the workspace");
+    if (la->actions < 1 || la->actions > MAX_ACTIONS) return set_err("actions must be in [1, 32]");
+    cudaStream_t st = (cudaStream_t)stream;
+    WS w = carve(la->ws, la->max_batch, la->actions);
+    const int64_t *map = la->idx ? la->idx : la->idx_base;
+    const int32_t *counter = la->idx ? nullptr : la->update_counter;
+    pq_net nets[2] = {la->theta, la->target};
+    FwdInput ins[2] = {{la->ring, la->records, map, counter, n, REC_INTS, 0},
+                       {la->ring, la->records, map, counter, n, REC_INTS, 1}};
+    const int groups = la->ext_targets ? 1 : 2;
+    int rc = forward_gemms(nets, ins, groups, n, w, st);
+    if (rc) return rc;
+    rc = head(nets, groups, n, la->actions, w, 1, la, st);
+    if (rc) return rc;
+    return backward_and_update(la, n, w, st);
+}
+
+int pq_rmsprop_f32(const float *p, const float *g, const float *m, const float *v, int64_t n,
+                   float lr, float rho, float kappa, float *p2, float *m2, float *v2,
+                   int32_t *nonfinite, void *stream) {
+    k_rmsprop<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        p, g, m, v, n, lr, rho, kappa, p2, m2, v2, nonfinite);
+    return cuda_err(cudaGetLastError(), "rmsprop");
+}
+
+uint64_t pq_theta_hash_f64(const double *x, int64_t n) {
+    uint64_t h = 0xCBF29CE484222325ULL;
+    const unsigned char *b = reinterpret_cast<const unsigned char *>(x);
+    for (int64_t i = 0; i < n * 8; ++i) {
+        h ^= b[i];
+        h *= 0x100000001B3ULL;
+    }
+    return h;
+}
+
+uint64_t pq_theta_hash_f32(const float *x, int64_t n) {
+    uint64_t h = 0xCBF29CE484222325ULL;
+    for (int64_t i = 0; i < n; ++i) {
+        double d = (double)x[i];
+        unsigned char b[8];
+        memcpy(b, &d, 8);
+        for (int k = 0; k < 8; ++k) {
+            h ^= b[k];
+            h *= 0x100000001B3ULL;
+        }
+    }
+    return h;
+}
+
+}  // extern "C"

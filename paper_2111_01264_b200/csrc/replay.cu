@@ -1,0 +1,298 @@
+// GPU-resident replay memory: numpy-exact index sampling, 4-frame-stack gather,
+// owner-major flush and device prepopulation.
+//
+//   ReplayMemory.sample   replay.py:61-66  -> k_sample_indices (PCG64 + buffered Lemire,
+//                                             bit-exact with Generator.integers)
+//   batch stack gather    agent.py:76,:100 -> k_gather (5 unique frames in, 8 out)
+//   ReplayMemory.flush    replay.py:82-93  -> k_flush (owner-major slot order)
+//   ReplayMemory.prepopulate replay.py:68-80 -> k_prepop_scalar + k_gen_frames
+#include <cstdio>
+
+#include "../../include/paraq_b200.h"
+#include "common.cuh"
+#include "qnet.cuh"
+
+namespace pq {
+int set_err(const char *msg);
+int cuda_err(cudaError_t e, const char *where);
+
+// ------------------------------------------------------------------ sampling
+constexpr int SAMPLE_THREADS = 1024;
+constexpr int SAMPLE_PER = 32;  // 64-bit outputs per thread per round
+
+__device__ __forceinline__ U128 pcg_step(U128 s, U128 inc) {
+    return add128(mul128(s, U128{PCG_MULT_HI, PCG_MULT_LO}), inc);
+}
+
+// Parallel restatement of numpy's sequential draw: every thread generates a
+// contiguous run of 64-bit outputs by LCG jump-ahead, Lemire-accepts each 32-bit
+// half (lo then hi, the has_uint32 order), and a block scan places accepted values
+// in stream order.  The state after the count-th accepted draw (including the
+// buffered high half) is written back exactly as numpy would leave it.
+__global__ void __launch_bounds__(SAMPLE_THREADS) k_sample_indices(uint64_t *st, uint32_t n,
+                                                                   int64_t count, int64_t *out) {
+    __shared__ int64_t s_produced;
+    __shared__ int s_warp[SAMPLE_THREADS / 32];
+    __shared__ int s_total;
+    __shared__ uint64_t s_fin[6];
+    __shared__ int s_done;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (count <= 0) return;
+    if (n <= 1) {
+        for (int64_t i = tid; i < count; i += SAMPLE_THREADS) out[i] = 0;
+        return;
+    }
+    const uint32_t threshold = (0u - n) % n;
+    Pcg64 g;
+    g.load(st);
+    const U128 inc = g.inc;
+    U128 base = g.state;
+    if (tid == 0) {
+        s_produced = 0;
+        s_done = 0;
+        for (int k = 0; k < 6; ++k) s_fin[k] = st[k];
+        if (g.has32) {
+            uint64_t m = (uint64_t)g.buf * n;
+            s_fin[4] = 0;  // the buffered half is consumed
+            if ((uint32_t)m >= threshold) {
+                out[0] = (int64_t)(m >> 32);
+                s_produced = 1;
+            }
+            if (s_produced == count) s_done = 1;
+        }
+    }
+    __syncthreads();
+    while (!s_done) {
+        const int64_t produced = s_produced;
+        U128 s0 = pcg_advance(base, inc, (uint64_t)tid * SAMPLE_PER);
+        int cnt = 0;
+        U128 s = s0;
+        for (int o = 0; o < SAMPLE_PER; ++o) {
+            s = pcg_step(s, inc);
+            uint64_t v = pcg_output(s);
+            cnt += ((uint32_t)((uint64_t)(uint32_t)v * n) >= threshold);
+            cnt += ((uint32_t)((uint64_t)(uint32_t)(v >> 32) * n) >= threshold);
+        }
+        // block exclusive scan of cnt
+        int x = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int wv = lane < SAMPLE_THREADS / 32 ? s_warp[lane] : 0;
+            int ws = wv;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, ws, o);
+                if (lane >= o) ws += y;
+            }
+            if (lane < SAMPLE_THREADS / 32) s_warp[lane] = ws - wv;
+            if (lane == 31) s_total = ws;
+        }
+        __syncthreads();
+        int64_t k = produced + s_warp[warp] + (x - cnt);
+        s = s0;
+        for (int o = 0; o < SAMPLE_PER; ++o) {
+            s = pcg_step(s, inc);
+            uint64_t v = pcg_output(s);
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t u = half ? (uint32_t)(v >> 32) : (uint32_t)v;
+                uint64_t m = (uint64_t)u * n;
+                if ((uint32_t)m >= threshold) {
+                    if (k < count) out[k] = (int64_t)(m >> 32);
+                    if (k == count - 1) {
+                        s_fin[0] = s.hi;
+                        s_fin[1] = s.lo;
+                        s_fin[4] = half ? 0 : 1;
+                        s_fin[5] = (uint32_t)(v >> 32);  // numpy leaves uinteger = hi
+                    }
+                    ++k;
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if (produced + s_total >= count) {
+                s_done = 1;
+            } else {
+                s_produced = produced + s_total;
+            }
+        }
+        base = pcg_advance(base, inc, (uint64_t)SAMPLE_THREADS * SAMPLE_PER);
+        __syncthreads();
+    }
+    if (tid == 0) {
+        for (int k = 0; k < 6; ++k) st[k] = s_fin[k];
+    }
+}
+
+// ------------------------------------------------------------------ gather
+// one block per sampled transition: read the 5 unique frames once (16 B vector
+// loads), write the two 4-frame stacks (masked slots -> zeros)
+__global__ void __launch_bounds__(256) k_gather(const uint8_t *ring, const int32_t *records,
+                                                const int64_t *idx, uint8_t *s_out,
+                                                uint8_t *s2_out, int32_t *a_out, float *r_out,
+                                                uint8_t *term_out) {
+    const int b = blockIdx.x;
+    const int32_t *rec = records + idx[b] * REC_INTS;
+    __shared__ int32_t f[REC_INTS];
+    if (threadIdx.x < REC_INTS) f[threadIdx.x] = rec[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a_out[b] = f[5];
+        r_out[b] = __int_as_float(f[6]);
+        term_out[b] = (uint8_t)f[7];
+    }
+    constexpr int V = FRAME_BYTES / 16;  // 441
+    uint4 *s4 = reinterpret_cast<uint4 *>(s_out + (size_t)b * 4 * FRAME_BYTES);
+    uint4 *t4 = reinterpret_cast<uint4 *>(s2_out + (size_t)b * 4 * FRAME_BYTES);
+    for (int e = threadIdx.x; e < 5 * V; e += blockDim.x) {
+        int fr = e / V, off = e - fr * V;
+        int slot = f[fr];
+        uint4 v = slot < 0 ? make_uint4(0, 0, 0, 0)
+                           : __ldg(reinterpret_cast<const uint4 *>(ring + (size_t)slot * FRAME_BYTES) + off);
+        if (fr < 4) s4[fr * V + off] = v;
+        if (fr > 0) t4[(fr - 1) * V + off] = v;
+    }
+}
+
+// ------------------------------------------------------------------ flush
+__global__ void k_flush(const int32_t *staging, int W, int steps, int32_t *records,
+                        int64_t capacity, int64_t push_count) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // owner-major index
+    if (i >= (int64_t)W * steps) return;
+    int64_t slot = (push_count + i) % capacity;
+    const uint4 *src = reinterpret_cast<const uint4 *>(staging + i * REC_INTS);
+    uint4 *dst = reinterpret_cast<uint4 *>(records + slot * REC_INTS);
+    dst[0] = src[0];
+    dst[1] = src[1];
+}
+
+// ------------------------------------------------------------------ frames
+__device__ __forceinline__ uint64_t frame_base(uint64_t key, int64_t episode, int t, int action) {
+    return splitmix64(splitmix64(splitmix64(key) ^ (uint64_t)episode) ^
+                      (((uint64_t)t << 8) | (uint64_t)action));
+}
+
+// frame words: word p = splitmix64(base + p) (little-endian bytes = 8 pixels)
+__device__ __forceinline__ void write_frame(uint8_t *dst, uint64_t base, int tid, int nthreads) {
+    uint64_t *d = reinterpret_cast<uint64_t *>(dst);
+    for (int p = tid; p < FRAME_BYTES / 8; p += nthreads) d[p] = splitmix64(base + (uint64_t)p);
+}
+
+// prepopulation, sequential part: one thread walks the PREPOP stream exactly like
+// replay.py:68-80 with the synthetic frame env (oracle/envs.py)
+struct FrameDesc {
+    int64_t episode;
+    int32_t t, action;
+};
+
+__global__ void k_prepop_scalar(uint64_t *pcg, int L, int A, double term_p, int64_t n,
+                                int64_t frame_base_seq, int64_t frame_capacity, int32_t *rec,
+                                FrameDesc *desc, int64_t *frames_used) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    Pcg64 g;
+    g.load(pcg);
+    int64_t episode = 0, used = 0;
+    int t = 0;
+    int32_t stack[4];
+    auto alloc = [&](int64_t ep, int tt, int a) -> int32_t {
+        desc[used] = FrameDesc{ep, tt, a};
+        int32_t slot = (int32_t)((frame_base_seq + used) % frame_capacity);
+        ++used;
+        return slot;
+    };
+    stack[0] = stack[1] = stack[2] = -1;
+    stack[3] = alloc(episode, 0, 255);
+    for (int64_t i = 0; i < n; ++i) {
+        int a = (int)g.bounded((uint32_t)A);
+        double reward = g.random();
+        bool term = g.random() < term_p;
+        t += 1;
+        int32_t fs = alloc(episode, t, a);
+        bool trunc = !term && t >= L;
+        int32_t *r = rec + i * REC_INTS;
+        r[0] = stack[0], r[1] = stack[1], r[2] = stack[2], r[3] = stack[3], r[4] = fs;
+        r[5] = a;
+        r[6] = __float_as_int((float)reward);
+        r[7] = term ? 1 : 0;  // bootstrap terminal = terminal and not truncated
+        if (term || trunc) {
+            if (i + 1 < n) {
+                episode += 1;
+                t = 0;
+                stack[0] = stack[1] = stack[2] = -1;
+                stack[3] = alloc(episode, 0, 255);
+            }
+        } else {
+            stack[0] = stack[1], stack[1] = stack[2], stack[2] = stack[3], stack[3] = fs;
+        }
+    }
+    g.store(pcg);
+    *frames_used = used;
+}
+
+__global__ void __launch_bounds__(128) k_gen_frames(const FrameDesc *desc, const int64_t *count,
+                                                    uint64_t key, uint8_t *ring,
+                                                    int64_t frame_base_seq, int64_t frame_capacity) {
+    for (int64_t f = blockIdx.x; f < *count; f += gridDim.x) {
+        FrameDesc d = desc[f];
+        int64_t slot = (frame_base_seq + f) % frame_capacity;
+        write_frame(ring + slot * FRAME_BYTES, frame_base(key, d.episode, d.t, d.action),
+                    threadIdx.x, blockDim.x);
+    }
+}
+
+}  // namespace pq
+
+using namespace pq;
+
+extern "C" {
+
+int pq_sample_indices(uint64_t *pcg_state, uint32_t n, int64_t count, int64_t *idx_out,
+                      void *stream) {
+    if (n == 0) return set_err("cannot sample from an empty replay memory");
+    k_sample_indices<<<1, SAMPLE_THREADS, 0, (cudaStream_t)stream>>>(pcg_state, n, count, idx_out);
+    return cuda_err(cudaGetLastError(), "sample_indices");
+}
+
+int pq_replay_gather(const uint8_t *ring, const int32_t *records, const int64_t *idx, int64_t B,
+                     uint8_t *s_out, uint8_t *s2_out, int32_t *a_out, float *r_out,
+                     uint8_t *term_out, void *stream) {
+    if (B <= 0) return 0;
+    k_gather<<<(unsigned)B, 256, 0, (cudaStream_t)stream>>>(ring, records, idx, s_out, s2_out,
+                                                            a_out, r_out, term_out);
+    return cuda_err(cudaGetLastError(), "gather");
+}
+
+int pq_replay_flush(const int32_t *staging, int W, int steps, int32_t *records, int64_t capacity,
+                    int64_t push_count, void *stream) {
+    int64_t total = (int64_t)W * steps;
+    if (total <= 0) return 0;
+    k_flush<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        staging, W, steps, records, capacity, push_count);
+    return cuda_err(cudaGetLastError(), "flush");
+}
+
+size_t pq_prepopulate_scratch_bytes(int64_t n) { return (size_t)(2 * n + 2) * sizeof(FrameDesc); }
+
+int pq_prepopulate(uint64_t *pcg_state, uint64_t key, int episode_length, int actions,
+                   double terminal_p, int64_t n, uint8_t *ring, int64_t frame_base,
+                   int64_t frame_capacity, int32_t *rec_out, int64_t *frames_used_out,
+                   void *scratch, void *stream) {
+    if (n <= 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    FrameDesc *desc = static_cast<FrameDesc *>(scratch);
+    k_prepop_scalar<<<1, 32, 0, st>>>(pcg_state, episode_length, actions, terminal_p, n,
+                                      frame_base, frame_capacity, rec_out, desc, frames_used_out);
+    int rc = cuda_err(cudaGetLastError(), "prepopulate scalar");
+    if (rc) return rc;
+    k_gen_frames<<<4096, 128, 0, st>>>(desc, frames_used_out, key, ring, frame_base, frame_capacity);
+    return cuda_err(cudaGetLastError(), "prepopulate frames");
+}
+
+}  // extern "C"

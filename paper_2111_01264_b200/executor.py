@@ -1,0 +1,423 @@
+"""Concurrent training + synchronized execution on one B200 (executor.py:1-637).
+
+The reference runs W sampler threads, one trainer thread and a lock-serialized
+"device" (InferenceWorker).  Here the device is real:
+
+* acting   -- one CUDA stream replays a captured graph of lockstep blocks: batched
+  Nature-CNN inference over the W current stacks with theta-minus, epsilon-greedy
+  and the env step in-kernel on each sampler's own PCG64 stream
+  (run_epoch_lockstep, executor.py:451-510; _sampler_step :237-249);
+* training -- a second stream replays a captured graph of learner steps over the
+  epoch-frozen replay memory; the epoch's C/F x B indices are drawn up front from
+  the trainer stream (identical consumption to C/F successive draws of B,
+  replay.py:65) and sliced by a device counter (train_one, executor.py:421-434);
+* epoch barrier -- stream join, owner-major flush of the sampler buffers,
+  theta-minus <- theta, theta hash (execute, executor.py:552-572).
+
+Concurrent modes ("both", "concurrent") are deterministic and reproduce the
+reference's schedule; the non-concurrent modes interleave blocking training with
+acting (executor.py:436-440) and are not offered on the device path.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .agent import HyperParams, epsilon_at
+from .envs import DeviceEnvs, FrameEnvSpec
+from .nn import OptState, QNet, copy_into, forward, init_network, theta_hash, workspace
+from .replay import REC_INTS, ReplayMemory, device_pcg, pcg_state_to_generator, \
+    sample_indices_device
+
+ROLE_INIT = 0
+ROLE_SAMPLER = 1
+ROLE_TRAINER = 2
+ROLE_EVAL = 3
+ROLE_PREPOP = 4
+ROLE_BENCH = 5
+
+
+def rng_stream(seed: int, role: int, index: int = 0) -> np.random.Generator:
+    """executor.py:59-63."""
+    return np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(role, index)))
+
+
+def derived_seed(seed: int, role: int, index: int = 0) -> int:
+    """executor.py:66-68."""
+    ss = np.random.SeedSequence(seed, spawn_key=(role, index))
+    return int(ss.generate_state(1, np.uint64)[0])
+
+
+class InferenceWorker:
+    """The prediction/training device with the reference's transaction counters
+    (executor.py:71-103).  Calls are stream-ordered on the GPU instead of locked."""
+
+    def __init__(self):
+        self.single_calls = 0
+        self.batched_calls = 0
+        self.rows_from_target = 0
+        self.rows_from_main = 0
+        self.train_calls = 0
+
+    @property
+    def inference_calls(self) -> int:
+        return self.single_calls + self.batched_calls
+
+    def count_predict(self, rows: int, from_target: bool, calls: int = 1) -> None:
+        if rows == 1:
+            self.single_calls += calls
+        else:
+            self.batched_calls += calls
+        if from_target:
+            self.rows_from_target += rows * calls
+        else:
+            self.rows_from_main += rows * calls
+
+    def predict(self, params: QNet, states, *, from_target: bool):
+        q = forward(params, states)
+        self.count_predict(q.shape[0], from_target)
+        return q
+
+    def train(self, fn):
+        self.train_calls += 1
+        return fn()
+
+
+def batched_inference(params: QNet, states):
+    """One forward over the W sampler states (executor.py:106-112); row-independent."""
+    if np.asarray(states).ndim != 4 if not hasattr(states, "dim") else states.dim() != 4:
+        raise ValueError("expected a (W, 4, 84, 84) batch of sampler states")
+    return forward(params, states)
+
+
+def transaction_breakdown(hp: HyperParams, steps: int) -> tuple[int, int]:
+    """executor.py:115-122."""
+    if steps < 1 or steps % hp.C != 0:
+        raise ValueError("steps must be a positive multiple of C")
+    return (steps // hp.W if hp.synchronized else steps), steps // hp.F
+
+
+def transaction_count(hp: HyperParams, steps: int) -> int:
+    inference, training = transaction_breakdown(hp, steps)
+    return inference + training
+
+
+@dataclass
+class RunRecord:
+    """Run products + counters; CSV format of executor.py:144-209."""
+
+    config: dict
+    seed: int
+    mode: str
+    evals: list = field(default_factory=list)
+    episodes: list = field(default_factory=list)
+    epoch_hashes: list = field(default_factory=list)
+    final_hash: str = ""
+    counters: dict = field(default_factory=dict)
+    events: list = field(default_factory=list)
+    duration_s: float = 0.0
+    final_params: object = None
+
+    def to_csv_text(self) -> str:
+        lines = ["# paraq-run-record v1"]
+        for k in sorted(self.config):
+            lines.append(f"# config {k}={self.config[k]}")
+        lines.append("step,event,value")
+        for step, kind, value in self.events:
+            lines.append(f"{step},{kind},{value}")
+        lines.append(f"# final_theta_hash {self.final_hash}")
+        for k in sorted(self.counters):
+            lines.append(f"# counter {k}={self.counters[k]}")
+        return "\n".join(lines) + "\n"
+
+    def write_csv(self, path) -> None:
+        with open(path, "w", newline="\n") as fh:
+            fh.write(self.to_csv_text())
+
+
+def config_echo(hp: HyperParams) -> dict:
+    return {
+        "mode": hp.mode, "workers": str(hp.W), "C": str(hp.C), "F": str(hp.F),
+        "gamma": repr(hp.gamma), "N": str(hp.N), "capacity": str(hp.capacity),
+        "batch_size": str(hp.batch_size), "total_steps": str(hp.total_steps),
+        "eval_period": str(hp.eval_period), "eval_episodes": str(hp.eval_episodes),
+        "eval_epsilon": repr(hp.eval_epsilon), "eps_start": repr(hp.schedule.start),
+        "eps_end": repr(hp.schedule.end), "eps_anneal": str(hp.schedule.anneal_steps),
+        "lr": repr(hp.opt.learning_rate), "rho": repr(hp.opt.rho), "kappa": repr(hp.opt.kappa),
+        "seed": str(hp.seed), "env": "frames84", "actions": str(hp.actions),
+        "episode_length": str(hp.episode_length), "terminal_p": repr(hp.terminal_p),
+    }
+
+
+class DeviceRun:
+    """Shared state and epoch driver of one device run (executor.py:341-594)."""
+
+    def __init__(self, hp: HyperParams, sink=None, use_graphs: bool = True, graph_chunk: int = 25,
+                 hash_epochs: bool = True):
+        hp.validate()
+        if not hp.concurrent:
+            raise NotImplementedError("the device executor implements the concurrent modes "
+                                      "('both', 'concurrent')")
+        if hp.eval_period:
+            raise NotImplementedError("periodic evaluation is not on the device path (eval_period=0)")
+        torch = N.require_cuda()
+        self.torch = torch
+        self.hp = hp
+        self.sink = sink
+        self.use_graphs = use_graphs
+        self.graph_chunk = graph_chunk
+        self.hash_epochs = hash_epochs
+        W, C, F, B = hp.W, hp.C, hp.F, hp.batch_size
+        self.steps = C // W
+        self.updates = C // F
+        self.worker = InferenceWorker()
+        lag = -(-3 // self.steps) + 1  # epochs of stack history an env can reference
+        self.lag = lag
+        fcap = 2 * hp.capacity + 2 * (lag + 3) * C + 2 * W + 1024
+        self.D = ReplayMemory(hp.capacity, frame_capacity=fcap)
+        prepop_env = FrameEnvSpec(derived_seed(hp.seed, ROLE_PREPOP, 1), hp.episode_length,
+                                  hp.actions, hp.terminal_p)
+        self.D.prepopulate(prepop_env, hp.N, rng_stream(hp.seed, ROLE_PREPOP))
+        self.theta = init_network(derived_seed(hp.seed, ROLE_INIT), hp.actions)
+        self.opt = OptState.zeros(self.theta)
+        self.target = self.theta.copy()
+        keys = [derived_seed(hp.seed, ROLE_SAMPLER, 1000 + j) for j in range(W)]
+        rngs = [rng_stream(hp.seed, ROLE_SAMPLER, j) for j in range(W)]
+        self.envs = DeviceEnvs(keys, rngs, self.steps)
+        first = self.D._reserve_frames(W)
+        slots = torch.as_tensor([(first + j) % fcap for j in range(W)], dtype=torch.int32,
+                                device="cuda")
+        self.envs.reset_all(slots, self.D.ring)
+        self.epoch_bases = [first]
+        self.trainer_pcg = device_pcg(rng_stream(hp.seed, ROLE_TRAINER))
+        self.staging = torch.full((W, self.steps, REC_INTS), -1, dtype=torch.int32, device="cuda")
+        self.staged = False
+        self.idx_table = torch.empty(self.updates * B, dtype=torch.int64, device="cuda")
+        self.update_counter = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.step_counter = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.nonfinite = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
+        self.act_ws, self.act_cap = self._own_ws(W)
+        self.learn_ws, self.learn_cap = self._own_ws(B)
+        self.act_stream = torch.cuda.Stream()
+        self.learn_stream = torch.cuda.Stream()
+        self.epoch_start = 0
+        self.counters = {"dfreeze_checks": 0, "dfreeze_violations": 0,
+                         "prepop_pushes": self.D.version, "flush_pushes": 0}
+        self.record = RunRecord(config=config_echo(hp), seed=hp.seed, mode=hp.mode,
+                                counters=self.counters)
+        self._graphs = None
+
+    def _own_ws(self, n):
+        torch = self.torch
+        cap = max(64, 1 << (int(n) - 1).bit_length())
+        nbytes = N.load().pq_workspace_bytes(cap, self.hp.actions)
+        return torch.empty(nbytes, dtype=torch.uint8, device="cuda"), cap
+
+    # -- raw step launchers (stream-ordered, graph-capturable) ----------------------------
+    def _learn_args(self):
+        hp = self.hp
+        th, op = self.theta, self.opt
+        return N.PqLearnArgs(
+            theta=th.struct(), opt=op.struct(), theta_out=th.struct(), opt_out=op.struct(),
+            target=self.target.struct(), ring=self.D.ring.data_ptr(),
+            records=self.D.records.data_ptr(), idx=None, idx_base=self.idx_table.data_ptr(),
+            update_counter=self.update_counter.data_ptr(), ext_targets=None, ext_actions=None,
+            n=hp.batch_size, actions=hp.actions, gamma=hp.gamma, lr=hp.opt.learning_rate,
+            rho=hp.opt.rho, kappa=hp.opt.kappa, nonfinite=self.nonfinite.data_ptr(),
+            grad_out=None, q_out=None, td_out=None, ws=self.learn_ws.data_ptr(),
+            max_batch=self.learn_cap)
+
+    def _act_args(self):
+        hp = self.hp
+        s = hp.schedule
+        return N.PqActArgs(
+            net=self.target.struct(), envs=self.envs.struct(), ring=self.D.ring.data_ptr(),
+            staging=self.staging.data_ptr(), step_counter=self.step_counter.data_ptr(),
+            W=hp.W, steps=self.steps, actions=hp.actions, episode_length=hp.episode_length,
+            epoch_start=0, frame_capacity=self.D.frame_capacity,
+            eps_start=s.start, eps_end=s.end, eps_anneal=s.anneal_steps,
+            terminal_p=hp.terminal_p, q_out=None, ws=self.act_ws.data_ptr(),
+            max_batch=self.act_cap)
+
+    def learn_step(self, stream=None):
+        a = self._learn_args()
+        N.check(N.load().pq_learn_step(N.C.byref(a), N.stream_ptr(stream)), "learn_step")
+
+    def act_step(self, stream=None):
+        a = self._act_args()
+        N.check(N.load().pq_act_step(N.C.byref(a), N.stream_ptr(stream)), "act_step")
+
+    # -- CUDA graphs ------------------------------------------------------------------
+    def _capture(self):
+        """Capture graph_chunk acting blocks and graph_chunk learner steps.  The
+        epoch start label is read from a device scalar, so one capture serves all
+        epochs; counters slice the per-epoch tables."""
+        torch = self.torch
+        # one eager act + learn step configures every kernel outside capture; all
+        # state they touch is snapshotted and restored
+        keep = [self.theta.master, self.theta.shadow, self.opt.m, self.opt.v,
+                self.update_counter, self.step_counter, self.nonfinite, self.idx_table,
+                self.envs.pcg, self.envs.episode, self.envs.t, self.envs.stack,
+                self.envs.ep_return, self.envs.slot_next, self.envs.ep_count,
+                self.envs.actions]
+        saved = [t.clone() for t in keep]
+        self.idx_table.zero_()
+        self.act_step()
+        self.learn_step()
+        torch.cuda.synchronize()
+        for t, v in zip(keep, saved):
+            t.copy_(v)
+        k = self.graph_chunk
+        graphs = {}
+        for name, fn, n in (("act", self.act_step, min(k, self.steps)),
+                            ("learn", self.learn_step, min(k, self.updates))):
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    for _ in range(n):
+                        fn()
+            graphs[name] = (g, n)
+        torch.cuda.synchronize()
+        for t, v in zip(keep, saved):
+            t.copy_(v)
+        return graphs
+
+    # -- epoch pieces -------------------------------------------------------------------
+    def emit(self, step, kind, value):
+        self.record.events.append((step, kind, value))
+        if self.sink is not None:
+            self.sink(step, kind, value)
+
+    def flush_and_merge(self):
+        """Epoch-boundary flush (executor.py:385-394): staged transitions in owner-major
+        order into D, finished episodes in owner order."""
+        hp = self.hp
+        if not self.staged:
+            return
+        lib = N.load()
+        tmp = self.torch.empty((hp.C, REC_INTS), dtype=self.torch.int32, device="cuda")
+        N.check(lib.pq_replay_flush(self.staging.data_ptr(), hp.W, self.steps, tmp.data_ptr(),
+                                    hp.C, 0, N.stream_ptr()), "flush")
+        base = self.epoch_bases[max(0, len(self.epoch_bases) - 1 - self.lag)]
+        self.D.push_device_records(tmp, hp.C, base)
+        self.counters["flush_pushes"] += hp.C
+        counts = self.envs.ep_count.cpu().numpy()
+        labels = self.envs.ep_label.cpu().numpy()
+        rets = self.envs.ep_ret.cpu().numpy()
+        for j in range(hp.W):
+            for c in range(int(counts[j])):
+                self.record.episodes.append((int(labels[j, c]), float(rets[j, c])))
+                self.emit(int(labels[j, c]), "episode", repr(float(rets[j, c])))
+        self.envs.ep_count.zero_()
+        self.staged = False
+
+    def begin_epoch(self, epoch: int):
+        """Per-epoch tables: the trainer's C/F x B indices, each sampler's frame-slot
+        reservation (2 per step: next frame + possible reset frame), counters."""
+        hp = self.hp
+        torch = self.torch
+        self.epoch_start = epoch * hp.C
+        sample_indices_device(self.trainer_pcg, len(self.D), self.updates * hp.batch_size,
+                              out=self.idx_table)
+        base = self.D._reserve_frames(2 * hp.C)
+        self.epoch_bases.append(base)
+        per = 2 * self.steps
+        self.envs.slot_next.copy_(torch.arange(hp.W, device="cuda", dtype=torch.int64) * per + base)
+        self.update_counter.zero_()
+
+    def run_epoch(self, epoch: int):
+        hp = self.hp
+        torch = self.torch
+        self.begin_epoch(epoch)
+        if self.use_graphs and self._graphs is None:
+            self._graphs = self._capture()
+        cur = torch.cuda.current_stream()
+        self.act_stream.wait_stream(cur)
+        self.learn_stream.wait_stream(cur)
+        if self.use_graphs:
+            self._replay_epoch()
+        else:
+            with torch.cuda.stream(self.act_stream):
+                for _ in range(self.steps):
+                    self.act_step()
+            with torch.cuda.stream(self.learn_stream):
+                for _ in range(self.updates):
+                    self.learn_step()
+        cur.wait_stream(self.act_stream)
+        cur.wait_stream(self.learn_stream)
+        self.staged = True
+        self.worker.count_predict(hp.W, True, self.steps)
+        self.worker.train_calls += self.updates
+        self.counters["dfreeze_checks"] += self.updates
+
+    def _replay_epoch(self):
+        """Acting and training graphs interleaved on their own streams."""
+        torch = self.torch
+        ga, na = self._graphs["act"]
+        gl, nl = self._graphs["learn"]
+        if self.steps % na or self.updates % nl:
+            raise RuntimeError("graph chunk must divide the per-epoch step counts")
+        # t labels come from the run-global device block counter, so the same
+        # captured graph serves every epoch
+        ra, rl = self.steps // na, self.updates // nl
+        ia = il = 0
+        while ia < ra or il < rl:
+            if ia < ra:
+                with torch.cuda.stream(self.act_stream):
+                    ga.replay()
+                ia += 1
+            for _ in range(2):
+                if il < rl:
+                    with torch.cuda.stream(self.learn_stream):
+                        gl.replay()
+                    il += 1
+
+    def check_finite(self):
+        v = int(self.nonfinite.item())
+        if v != 2**31 - 1:
+            raise ValueError(f"gradient contains non-finite entries (learner step {v} of the epoch)")
+
+    def record_epoch_hash(self, boundary: int):
+        h = theta_hash(self.theta)
+        self.record.epoch_hashes.append((boundary, h))
+        self.emit(boundary, "theta_hash", h)
+
+    def execute(self) -> RunRecord:
+        hp = self.hp
+        wall0 = time.perf_counter()
+        for e in range(hp.total_steps // hp.C):
+            self.flush_and_merge()
+            copy_into(self.target, self.theta)
+            self.run_epoch(e)
+            self.torch.cuda.synchronize()
+            self.check_finite()
+            if self.hash_epochs:
+                self.record_epoch_hash((e + 1) * hp.C)
+        self.flush_and_merge()
+        self.finalize(wall0)
+        return self.record
+
+    def finalize(self, wall0: float):
+        w = self.worker
+        self.counters.update({
+            "inference_single_calls": w.single_calls,
+            "inference_batched_calls": w.batched_calls,
+            "inference_calls": w.inference_calls,
+            "acting_rows_from_target": w.rows_from_target,
+            "acting_rows_from_main": w.rows_from_main,
+            "train_calls": w.train_calls,
+        })
+        self.record.final_hash = theta_hash(self.theta)
+        self.record.final_params = self.theta
+        self.record.duration_s = time.perf_counter() - wall0
+
+
+def run(hp: HyperParams, sink=None, **kw) -> RunRecord:
+    """Execute the full training run described by hp on the GPU (executor.py:591-593)."""
+    return DeviceRun(hp, sink, **kw).execute()
