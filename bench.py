@@ -1,0 +1,384 @@
+"""Benchmark of the fast-DQN hot path (BASELINE.json metric: env frames/sec + learner
+updates/sec at batch 32).
+
+Workload (BASELINE.json configs[1]): Nature-CNN DQN on synthetic 84x84x4 uint8
+frames, 18 actions, W = 8 synchronized envs, batch 32, F = 4, 1M-transition replay
+memory resident in HBM (prefilled by device prepopulation before timing), concurrent
+training, target sync every C = 10,000 steps.  One bench step = one epoch: C env
+frames (C/W lockstep acting blocks on one stream) + C/F learner updates (second
+stream) + the epoch barrier (flush, theta-minus sync, theta hash).
+
+  python bench.py [--gpus N --steps K --warmup W]          # the B200 arm
+  python bench.py --impl reference [...]                    # the CPU reference arm
+
+Multi-GPU (torchrun, one rank per GPU): independent agent replicas (configs[3]),
+distinct seeds, no data-path collective ("replicas only" / weak scaling); the job
+value is all ranks' frames over the max-over-ranks time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "env frames/sec + learner updates/sec (batch 32)"
+UNIT = "env frames/s"
+FLOP_PER_SAMPLE_LEARN = 68.26e6
+FLOP_PER_STATE_ACT = 18.70e6
+GATHER_BYTES_PER_TRANSITION = 91_728  # 5 unique frames read + 8 written
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--capacity", type=int, default=1_000_000)
+    ap.add_argument("--prefill", type=int, default=1_000_000)
+    ap.add_argument("--C", type=int, default=10_000)
+    ap.add_argument("--W", type=int, default=8)
+    ap.add_argument("--B", type=int, default=32)
+    ap.add_argument("--F", type=int, default=4)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), \
+            d.get("bf16_tflops_sustained", 1400.0), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- CPU arm
+def cpu_sample(args, seconds: float, threads: int):
+    """The oracle port (C restatement of the reference kernels, composed like
+    nn.py / agent.py) on the host cores: lockstep acting blocks (W forwards +
+    select_action + env step) and learner updates at batch B, in the concurrent
+    schedule's W : W/F proportion.  Returns (frames/s, updates/s, sample text)."""
+    from oracle import _lib as OK
+    from oracle import natcnn, replay as oreplay
+    from oracle.envs import SyntheticFrameEnv
+
+    OK.set_threads(threads)
+    spec = natcnn.nature_cnn(18)
+    theta = natcnn.init_params(spec, 1)
+    target = natcnn.copy_params(theta)
+    opt = natcnn.Opt.zeros(theta)
+    mem = oreplay.ReplayMemory(10_000)
+    mem.prepopulate(SyntheticFrameEnv(3, action_count=18), 2000, np.random.default_rng(0))
+    envs = [SyntheticFrameEnv(100 + j, action_count=18) for j in range(args.W)]
+    rngs = [np.random.default_rng(j) for j in range(args.W)]
+    states = [e.reset(r) for e, r in zip(envs, rngs)]
+    trng = np.random.default_rng(9)
+    t_act, n_act, t_upd, n_upd = 0.0, 0, 0.0, 0
+    t_begin = time.perf_counter()
+    while time.perf_counter() - t_begin < seconds or n_upd < 1:
+        t0 = time.perf_counter()
+        q = natcnn.forward(spec, target, np.stack(states))
+        for j in range(args.W):
+            st = OK.pcg_state_from_generator(rngs[j])
+            a = OK.select_action(st, q[j], 0.1)
+            OK.pcg_state_to_generator(st, rngs[j])
+            nxt, rew, done = envs[j].step(a, rngs[j])
+            states[j] = envs[j].reset(rngs[j]) if done else nxt
+        t_act += time.perf_counter() - t0
+        n_act += 1
+        for _ in range(max(1, args.W // args.F)):
+            t0 = time.perf_counter()
+            batch = oreplay.gather(mem.sample(args.B, trng))
+            theta, opt = natcnn.train_minibatch(spec, theta, opt, batch, target, 0.99)
+            t_upd += time.perf_counter() - t0
+            n_upd += 1
+    OK.set_threads(1)
+    per_frame = t_act / (n_act * args.W) + (t_upd / n_upd) / args.F
+    frames_s = 1.0 / per_frame
+    sample = (f"{n_act} acting blocks (W={args.W}) + {n_upd} learner updates (B={args.B}) of the "
+              f"Nature-CNN oracle in {t_act + t_upd:.1f} s; frames/s = 1/(t_act/W + t_update/F)")
+    return frames_s, frames_s / args.F, sample
+
+
+def run_reference(args, rank: int):
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    t_total = 0.0
+    frames = 0.0
+    vals = []
+    for k in range(args.warmup + args.steps):
+        fs, us, sample = cpu_sample(args, seconds=0.0, threads=threads)  # 1 block + W/F updates
+        if k >= args.warmup:
+            vals.append(fs)
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * args.W / value, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "learner_updates_per_s": value / args.F,
+        "config": {"workload": "configs[1]: Nature-CNN DQN, 84x84x4 uint8 frames, 18 actions, "
+                               "W=8 synchronized envs, batch 32, F=4 (CPU sample: one lockstep "
+                               "block + W/F updates per step)",
+                   "global_batch": args.B, "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- B200 arm
+def time_kernel_isolated(runner, reps: int = 200):
+    """Average device time of one learner step and of its dominant GEMM, eager
+    launches bracketed by CUDA events on the launching stream."""
+    import torch
+
+    s = torch.cuda.current_stream()
+    saved = [t.clone() for t in (runner.theta.master, runner.theta.shadow, runner.opt.m,
+                                 runner.opt.v, runner.update_counter)]
+    runner.update_counter.zero_()
+    for _ in range(10):
+        runner.learn_step()
+        runner.update_counter.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(reps):
+        runner.learn_step()
+        runner.update_counter.zero_()
+    e1.record(s)
+    torch.cuda.synchronize()
+    learn_ms = e0.elapsed_time(e1) / reps
+    for t, v in zip((runner.theta.master, runner.theta.shadow, runner.opt.m, runner.opt.v,
+                     runner.update_counter), saved):
+        t.copy_(v)
+    return learn_ms
+
+
+def time_gather(runner, transitions: int = 80_000, reps: int = 10):
+    """Replay sample + stack gather over an epoch-sized batch (HBM-bound)."""
+    import torch
+    from paper_2111_01264_b200.replay import device_pcg, sample_indices_device
+
+    st = device_pcg(np.random.default_rng(123))
+    idx = sample_indices_device(st, len(runner.D), transitions)
+    B = transitions
+    s = torch.empty((B, 4, 84, 84), dtype=torch.uint8, device="cuda")
+    s2 = torch.empty_like(s)
+    a = torch.empty(B, dtype=torch.int32, device="cuda")
+    r = torch.empty(B, dtype=torch.float32, device="cuda")
+    t = torch.empty(B, dtype=torch.uint8, device="cuda")
+    from paper_2111_01264_b200 import _native as N
+
+    lib = N.load()
+
+    def go():
+        N.check(lib.pq_replay_gather(runner.D.ring.data_ptr(), runner.D.records.data_ptr(),
+                                     idx.data_ptr(), B, s.data_ptr(), s2.data_ptr(), a.data_ptr(),
+                                     r.data_ptr(), t.data_ptr(), N.stream_ptr()), "gather")
+    go()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        go()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    del s, s2
+    return ms
+
+
+def run_b200(args, rank: int, world: int, local_rank: int):
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    from paper_2111_01264_b200.agent import EpsilonSchedule, HyperParams
+    from paper_2111_01264_b200.executor import ROLE_BENCH, DeviceRun, derived_seed
+    from paper_2111_01264_b200.nn import copy_into
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    seed = derived_seed(args.seed, ROLE_BENCH, rank) % (2**31)
+    total_epochs = args.warmup + args.steps
+    hp = HyperParams(C=args.C, F=args.F, N=args.prefill, W=args.W, batch_size=args.B,
+                     total_steps=args.C * total_epochs, capacity=args.capacity, seed=seed,
+                     schedule=EpsilonSchedule(0.1, 0.1, 1))
+    t_setup = time.perf_counter()
+    runner = DeviceRun(hp, use_graphs=True, graph_chunk=25)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+
+    def epoch(e):
+        runner.flush_and_merge()
+        copy_into(runner.target, runner.theta)
+        runner.run_epoch(e)
+        torch.cuda.synchronize()
+        runner.check_finite()
+        runner.record_epoch_hash((e + 1) * hp.C)
+
+    for e in range(args.warmup):
+        epoch(e)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for e in range(args.warmup, total_epochs):
+        epoch(e)
+    e1.record()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    secs = ms / 1000.0
+    frames = world * args.steps * hp.C
+    value = frames / secs
+    updates_s = world * args.steps * (hp.C // hp.F) / secs
+    # kernel-level measurements (outside the timed region; same inputs)
+    learn_ms = time_kernel_isolated(runner)
+    gather_ms = time_gather(runner)
+    if dist:
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    hbm, bf16_burst, bf16_sus, peak_src = measured_peaks()
+    learn_flop = FLOP_PER_SAMPLE_LEARN * hp.batch_size
+    achieved_tf = learn_flop / (learn_ms * 1e-3) / 1e12
+    gather_gbs = 80_000 * GATHER_BYTES_PER_TRANSITION / (gather_ms * 1e-3) / 1e9
+    per_epoch_launches = (hp.C // hp.W) * 6 + (hp.C // hp.F) * 14 + 2
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        threads = len(os.sched_getaffinity(0))
+        fs, us, sample = cpu_sample(args, seconds=args.cpu_seconds, threads=threads)
+        cpu = {"value": fs, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+               "updates_per_s": us}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "learner_updates_per_s": updates_s,
+        "config": {
+            "workload": "configs[1]: Nature-CNN DQN, synthetic 84x84x4 uint8 frames, 18 actions, "
+                        "W=8 synchronized envs, batch 32, F=4, 1M-transition replay in HBM "
+                        "(prefilled), concurrent training, target sync every 10k steps; "
+                        "1 step = 1 epoch (10k frames + 2.5k updates)",
+            "global_batch": hp.batch_size * world, "W": hp.W, "C": hp.C, "F": hp.F,
+            "capacity": hp.capacity, "prefill": hp.N,
+            "parallelism": f"replicas x{world}" if world > 1 else "single agent",
+            "l2": "inputs larger than L2 (7 GB replay ring sampled uniformly)",
+            "setup_s": round(setup_s, 2),
+        },
+        "roofline": {
+            "kernel": "learner step (15 tcgen05 GEMM/head/optimizer launches, batch 32)",
+            "bound": "tensor", "achieved": achieved_tf, "peak": bf16_burst, "unit": "TFLOP/s",
+            "frac": achieved_tf / bf16_burst, "traffic": None,
+            "per_launch": f"{learn_flop / 1e9:.3f} GFLOP (68.26 MFLOP/sample x {hp.batch_size}) "
+                          f"in {learn_ms * 1e3:.1f} us", "peak_source": peak_src,
+        },
+        "gather_roofline": {
+            "kernel": "k_gather (80k-transition sample, 91,728 B each)", "bound": "hbm",
+            "achieved": gather_gbs, "peak": hbm, "unit": "GB/s", "frac": gather_gbs / hbm,
+            "ms": gather_ms,
+        },
+        "gpu_launches": per_epoch_launches * args.steps,
+        "clocks": clk,
+        "cpu_baseline": cpu,
+        "e2e": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    run_b200(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()
