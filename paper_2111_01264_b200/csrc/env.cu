@@ -21,7 +21,7 @@ namespace pq {
 int set_err(const char *msg);
 int cuda_err(cudaError_t e, const char *where);
 int act_forward(pq_net net, const uint8_t *ring, const int32_t *stack, int W, int A, void *ws,
-                int max_batch, const float **part_out, cudaStream_t st);
+                int max_batch, const float **part_out, uint32_t **done_out, cudaStream_t st);
 
 __device__ __forceinline__ uint64_t env_frame_base(uint64_t key, int64_t episode, int t, int action) {
     return splitmix64(splitmix64(splitmix64(key) ^ (uint64_t)episode) ^
@@ -40,7 +40,8 @@ struct ActArgs {
     pq_envs e;
     uint8_t *ring;
     int32_t *staging;
-    const int32_t *step_counter;
+    int32_t *step_counter;
+    uint32_t *done;
     int W, steps, A, L;
     int64_t epoch_start, frame_capacity;
     double eps_start, eps_end;
@@ -55,44 +56,81 @@ __device__ __forceinline__ float warp_sum_f(float v) {
     return v;
 }
 
-__global__ void __launch_bounds__(128) k_act_env(const ActArgs a) {
+__global__ void __launch_bounds__(256) k_act_env(const ActArgs a) {
     const int j = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    __shared__ float red[4][MAX_ACTIONS];
+    __shared__ float hs[512];
     __shared__ float qs[MAX_ACTIONS];
     __shared__ uint64_t s_base[2];
     __shared__ int64_t s_slot[2];
-    float h[4];
+    // sampler state: every load issued up front by thread 0 (independent, in flight
+    // together with the fc1 reduction below)
+    uint64_t pcg[6] = {}, key = 0;
+    int32_t st4[4] = {}, t0 = 0, epc = 0;
+    int64_t ep0 = 0, seq = 0, bg = 0;
+    double ret0 = 0.0;
+    if (tid == 0) {
+        bg = *a.step_counter;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        int jj = tid + 128 * i;
-        float s = 0.f;
-        for (int sp = 0; sp < FC1_SPLITS; ++sp) s += a.part[((size_t)sp * a.W + j) * 512 + jj];
-        s += a.master[P_B4 + jj];
-        h[i] = s > 0.f ? s : 0.f;
+        for (int k = 0; k < 6; ++k) pcg[k] = a.e.pcg[j * 6 + k];
+        const int4 sv = *reinterpret_cast<const int4 *>(a.e.stack + j * 4);
+        st4[0] = sv.x, st4[1] = sv.y, st4[2] = sv.z, st4[3] = sv.w;
+        t0 = a.e.t[j];
+        ep0 = a.e.episode[j];
+        seq = a.e.slot_next[j];
+        key = a.e.key[j];
+        ret0 = a.e.ep_return[j];
+        epc = a.e.ep_count[j];
     }
-    for (int aa = 0; aa < a.A; ++aa) {
-        float acc = 0.f;
+    {
+        float v[2][FC1_SPLITS + 1];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc += a.master[P_W5 + aa * 512 + tid + 128 * i] * h[i];
-        acc = warp_sum_f(acc);
-        if (lane == 0) red[warp][aa] = acc;
+        for (int i = 0; i < 2; ++i) {
+            const int jj = tid + 256 * i;
+#pragma unroll
+            for (int sp = 0; sp < FC1_SPLITS; ++sp) v[i][sp] = a.part[((size_t)sp * a.W + j) * 512 + jj];
+            v[i][FC1_SPLITS] = a.master[P_B4 + jj];
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            float s = 0.f;
+#pragma unroll
+            for (int sp = 0; sp < FC1_SPLITS; ++sp) s += v[i][sp];
+            s += v[i][FC1_SPLITS];
+            hs[tid + 256 * i] = s > 0.f ? s : 0.f;
+        }
     }
     __syncthreads();
-    if (tid < a.A) {
-        float q = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid] + a.master[p_b5(a.A) + tid];
-        qs[tid] = q;
-        if (a.q_out) a.q_out[j * a.A + tid] = q;
+    {
+        float wv[4][16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int aa = min(warp + 8 * u, a.A - 1);
+#pragma unroll
+            for (int t = 0; t < 16; ++t) wv[u][t] = a.master[P_W5 + aa * 512 + lane + 32 * t];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int aa = warp + 8 * u;
+            float acc = 0.f;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) acc += wv[u][t] * hs[lane + 32 * t];
+            acc = warp_sum_f(acc);
+            if (lane == 0 && aa < a.A) {
+                const float q = acc + a.master[p_b5(a.A) + aa];
+                qs[aa] = q;
+                if (a.q_out) a.q_out[j * a.A + aa] = q;
+            }
+        }
     }
     __syncthreads();
     if (tid == 0) {
         // step_counter counts lockstep blocks (run-global in the executor); the
         // staging row is the block index within the epoch
-        const int64_t bg = *a.step_counter;
         const int b = (int)(bg % a.steps);
         const int64_t t_label = a.epoch_start + bg * a.W + j + 1;
         const double eps = epsilon_at(t_label, a.eps_start, a.eps_end, a.eps_anneal);
         Pcg64 g;
-        g.load(a.e.pcg + j * 6);
+        g.load(pcg);
         int act;
         if (g.random() < eps) {
             act = (int)g.bounded((uint32_t)a.A);
@@ -102,52 +140,64 @@ __global__ void __launch_bounds__(128) k_act_env(const ActArgs a) {
                 if (qs[aa] > qs[act]) act = aa;
         }
         // env.step(action, rng): reward draw, terminal draw, next frame
-        double reward = g.random();
-        bool term = g.random() < a.term_p;
-        int t = a.e.t[j] + 1;
-        int64_t ep = a.e.episode[j];
-        int64_t seq = a.e.slot_next[j];
-        int32_t fs = (int32_t)(seq % a.frame_capacity);
+        const double reward = g.random();
+        const bool term = g.random() < a.term_p;
+        int t = t0 + 1;
+        int64_t ep = ep0;
+        const int32_t fs = (int32_t)(seq % a.frame_capacity);
         s_slot[0] = fs;
-        s_base[0] = env_frame_base(a.e.key[j], ep, t, act);
-        bool trunc = !term && t >= a.L;
-        int32_t *st4 = a.e.stack + j * 4;
-        int32_t *rec = a.staging + ((int64_t)j * a.steps + b) * REC_INTS;
-        rec[0] = st4[0], rec[1] = st4[1], rec[2] = st4[2], rec[3] = st4[3], rec[4] = fs;
-        rec[5] = act;
-        rec[6] = __float_as_int((float)reward);
-        rec[7] = term ? 1 : 0;
-        double ret = a.e.ep_return[j] + reward;
+        s_base[0] = env_frame_base(key, ep, t, act);
+        const bool trunc = !term && t >= a.L;
+        int4 *rec = reinterpret_cast<int4 *>(a.staging + ((int64_t)j * a.steps + b) * REC_INTS);
+        rec[0] = make_int4(st4[0], st4[1], st4[2], st4[3]);
+        rec[1] = make_int4(fs, act, __float_as_int((float)reward), term ? 1 : 0);
+        double ret = ret0 + reward;
         s_slot[1] = -1;
+        int4 nst;
         if (term || trunc) {
-            int c = a.e.ep_count[j];
-            a.e.ep_label[(int64_t)j * a.steps + c] = t_label;
-            a.e.ep_ret[(int64_t)j * a.steps + c] = ret;
-            a.e.ep_count[j] = c + 1;
+            a.e.ep_label[(int64_t)j * a.steps + epc] = t_label;
+            a.e.ep_ret[(int64_t)j * a.steps + epc] = ret;
+            a.e.ep_count[j] = epc + 1;
             ret = 0.0;
             ep += 1;
             t = 0;
-            int32_t rs = (int32_t)((seq + 1) % a.frame_capacity);
+            const int32_t rs = (int32_t)((seq + 1) % a.frame_capacity);
             s_slot[1] = rs;
-            s_base[1] = env_frame_base(a.e.key[j], ep, 0, 255);
-            st4[0] = st4[1] = st4[2] = -1;
-            st4[3] = rs;
+            s_base[1] = env_frame_base(key, ep, 0, 255);
+            nst = make_int4(-1, -1, -1, rs);
             a.e.slot_next[j] = seq + 2;
         } else {
-            st4[0] = st4[1], st4[1] = st4[2], st4[2] = st4[3], st4[3] = fs;
+            nst = make_int4(st4[1], st4[2], st4[3], fs);
             a.e.slot_next[j] = seq + 1;
         }
+        *reinterpret_cast<int4 *>(a.e.stack + j * 4) = nst;
         a.e.ep_return[j] = ret;
         a.e.t[j] = t;
         a.e.episode[j] = ep;
         a.e.actions[j] = act;
-        g.store(a.e.pcg + j * 6);
+        uint64_t out[6];
+        g.store(out);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) a.e.pcg[j * 6 + k] = out[k];
     }
     __syncthreads();
     for (int f = 0; f < 2; ++f) {
         if (s_slot[f] < 0) continue;
         uint64_t *d = reinterpret_cast<uint64_t *>(a.ring + (size_t)s_slot[f] * FRAME_BYTES);
         for (int p = tid; p < FRAME_BYTES / 8; p += blockDim.x) d[p] = splitmix64(s_base[f] + (uint64_t)p);
+    }
+    // the last CTA advances the block counter (every CTA has read it by then)
+    __shared__ bool s_last;
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && tid == 0) {
+        *a.step_counter += 1;
+        *a.done = 0;
+        __threadfence();
     }
 }
 
@@ -169,8 +219,6 @@ __global__ void k_env_reset(pq_envs e, int W, const int32_t *slots, uint8_t *rin
     for (int p = threadIdx.x; p < FRAME_BYTES / 8; p += blockDim.x) d[p] = splitmix64(base + (uint64_t)p);
 }
 
-__global__ void k_bump_counter(int32_t *c) { *c += 1; }
-
 }  // namespace pq
 
 using namespace pq;
@@ -188,8 +236,9 @@ int pq_act_step(const pq_act_args *x, void *stream) {
     if (x->actions < 1 || x->actions > MAX_ACTIONS) return set_err("actions must be in [1, 32]");
     cudaStream_t st = (cudaStream_t)stream;
     const float *part = nullptr;
+    uint32_t *done = nullptr;
     int rc = act_forward(x->net, x->ring, x->envs.stack, x->W, x->actions, x->ws, x->max_batch,
-                         &part, st);
+                         &part, &done, st);
     if (rc) return rc;
     ActArgs a{};
     a.part = part;
@@ -198,17 +247,15 @@ int pq_act_step(const pq_act_args *x, void *stream) {
     a.ring = x->ring;
     a.staging = x->staging;
     a.step_counter = x->step_counter;
+    a.done = done;
     a.W = x->W, a.steps = x->steps, a.A = x->actions, a.L = x->episode_length;
     a.epoch_start = x->epoch_start;
     a.frame_capacity = x->frame_capacity;
     a.eps_start = x->eps_start, a.eps_end = x->eps_end, a.eps_anneal = x->eps_anneal;
     a.term_p = x->terminal_p;
     a.q_out = x->q_out;
-    k_act_env<<<x->W, 128, 0, st>>>(a);
-    rc = cuda_err(cudaGetLastError(), "act_env");
-    if (rc) return rc;
-    k_bump_counter<<<1, 1, 0, st>>>(x->step_counter);
-    return cuda_err(cudaGetLastError(), "act counter");
+    k_act_env<<<x->W, 256, 0, st>>>(a);
+    return cuda_err(cudaGetLastError(), "act_env");
 }
 
 }  // extern "C"

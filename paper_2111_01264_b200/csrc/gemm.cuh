@@ -3,21 +3,23 @@
 //   D[m, n] = sum_k A[m, k] * B[n, k]      (bf16 operands, fp32 accumulate in TMEM)
 //
 // One CTA = 128 threads computes a 128 x BN tile.  Operand tiles (BK = 64) are
-// gathered by all threads with 16-byte loads straight from the producing layout
-// (im2col of uint8 frames through the replay ring's frame table, im2col of NHWC
-// activations, transposed-conv windows, plain matrices) and written to shared
-// memory in the UMMA 128B-swizzled canonical layout, K-major or MN-major -- so no
-// im2col or transpose is ever materialised in HBM.  Thread 0 issues 4 x
-// tcgen05.mma (K = 16) per stage and commits to the stage's mbarrier; a 4-stage
-// ring lets the next stage's loads overlap the running MMAs.  The epilogue reads
-// the accumulator with tcgen05.ld (warp w owns TMEM lanes 32w..32w+31, i.e. tile
-// rows) and applies a fused operator (bias / 255-scale / ReLU / ReLU-mask /
-// split-K partial / transposed store).
+// gathered straight from the producing layout -- im2col of uint8 frames through the
+// replay ring's frame table, im2col of NHWC activations, transposed-conv windows,
+// plain matrices -- by cp.async (LDGSTS) into shared memory in the UMMA 128B-swizzled
+// canonical layout, K-major or MN-major, so no im2col or transpose is materialised in
+// HBM.  The mainloop is a STAGES-deep ring: loads for K-chunk i+STAGES-1 are in flight
+// while thread 0 issues the 4 x tcgen05.mma (K = 16) of chunk i and commits them to
+// the chunk's mbarrier, which releases the slot for reuse.  Ragged edges zero-fill
+// through the cp.async src-size operand.  uint8 frame tiles are copied raw and widened
+// to bf16 in shared memory by the thread that loaded them (0..255 is exact in bf16).
+// The epilogue reads the accumulator with tcgen05.ld (warp w owns TMEM lanes
+// 32w..32w+31 = tile rows) and applies a fused operator (bias / 1/255 scale / ReLU /
+// ReLU-mask / split-K partial / transposed store).
 //
-// A loader exposes fetch(outer, inner) -> 8 consecutive bf16 of its natural
-// row-major view (inner is the contiguous index, inner % 8 == 0); out-of-range
-// chunks read as zero.  K-major operands use (outer, inner) = (mn, k); MN-major
-// operands use (outer, inner) = (k, mn).
+// A loader exposes src(outer, inner, bytes) -> address of 8 consecutive elements of its
+// natural row-major view (inner % 8 == 0), bytes = how many of them exist (0 = zero
+// chunk).  K-major operands use (outer, inner) = (mn, k); MN-major operands use
+// (outer, inner) = (k, mn).
 #pragma once
 
 #include "common.cuh"
@@ -26,99 +28,274 @@ namespace pq {
 
 typedef __nv_bfloat16 bf16;
 
+// ------------------------------------------------------------------------ cp.async
+PQ_DEV void cp_async16(uint32_t dst, const void *src, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes)
+                 : "memory");
+}
+PQ_DEV void cp_async4(uint32_t dst, const void *src, int bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(bytes)
+                 : "memory");
+}
+PQ_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+PQ_DEV void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ------------------------------------------------------------------------ loaders
+// Exact x / d for 0 <= x < 2^24, 1 <= d < 4096 by one 64-bit multiply-high.
+struct FastDiv {
+    uint64_t m;
+    int d;
+    FastDiv() = default;
+    __host__ FastDiv(int dd) : m(((1ull << 40) + (uint64_t)dd - 1) / (uint64_t)dd), d(dd) {}
+    PQ_DEV int div(int x) const { return (int)(((uint64_t)(uint32_t)x * m) >> 40); }
+};
+
+// Per-CTA context handed to the loaders (frame-slot table in shared memory).
+struct LoadCtx {
+    const int32_t *table;  // [samples][4] frame slots of the CTA's sample window
+    int tb;                // first sample of the window
+};
+
+// Addresses are separable into a row part (outer index) and a column part (inner
+// index): row(outer) and col(inner) are computed once per thread per row / per
+// K-chunk, addr() combines them.  K-major operands keep their rows for the whole
+// K loop; MN-major operands keep their column.
 struct LoadDense {  // bf16 row-major [rows][cols] with row stride ld (elements)
+    static constexpr bool U8 = false, TABLE = false;
     const bf16 *p;
     int rows, cols, ld;
-    PQ_DEV uint4 fetch(int r, int c) const {
-        if (r >= rows || c >= cols) return make_uint4(0, 0, 0, 0);
-        const bf16 *src = p + (size_t)r * ld + c;
-        if (c + 8 <= cols) return __ldg(reinterpret_cast<const uint4 *>(src));
-        uint16_t e[8];  // ragged tail: elements >= cols read as zero
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            e[i] = (c + i < cols) ? __ldg(reinterpret_cast<const uint16_t *>(src) + i) : (uint16_t)0;
-        return make_uint4(e[0] | (e[1] << 16), e[2] | (e[3] << 16), e[4] | (e[5] << 16),
-                          e[6] | (e[7] << 16));
+    struct Row {
+        const bf16 *p;
+        bool ok;
+    };
+    struct Col {
+        int c, bytes;
+    };
+    PQ_DEV Row row(int r) const { return {p + (size_t)r * ld, r < rows}; }
+    PQ_DEV Col col(int c) const {
+        int rem = cols - c;
+        return {c, rem <= 0 ? 0 : (rem >= 8 ? 16 : rem * 2)};
+    }
+    PQ_DEV const void *addr(const Row &R, const Col &Cc, int &bytes, const LoadCtx &) const {
+        bytes = R.ok ? Cc.bytes : 0;
+        return bytes ? (const void *)(R.p + Cc.c) : (const void *)p;
     }
 };
 
 // im2col over NHWC bf16 activations: row m = (b, oy, ox), col k = (kh, kw, c)
 struct LoadIm2col {
+    static constexpr bool U8 = false, TABLE = false;
     const bf16 *x;
     int n, H, W, C, KS, S, OH, OW;
-    PQ_DEV uint4 fetch(int m, int k) const {
-        int npix = OH * OW;
-        if (m >= n * npix || k >= KS * KS * C) return make_uint4(0, 0, 0, 0);
-        int b = m / npix, rem = m - b * npix;
-        int oy = rem / OW, ox = rem - oy * OW;
-        int kc = KS * C;
-        int kh = k / kc, r2 = k - kh * kc;
-        int kw = r2 / C, c = r2 - kw * C;
-        const bf16 *src = x + ((size_t)(b * H + oy * S + kh) * W + (ox * S + kw)) * C + c;
-        return __ldg(reinterpret_cast<const uint4 *>(src));
+    FastDiv f_npix, f_ow, f_kc, f_c;
+    struct Row {
+        int off;
+        bool ok;
+    };
+    struct Col {
+        int off;
+        bool ok;
+    };
+    PQ_DEV Row row(int m) const {
+        if (m >= n * OH * OW) return {0, false};
+        int b = f_npix.div(m), rem = m - b * OH * OW;
+        int oy = f_ow.div(rem), ox = rem - oy * OW;
+        return {((b * H + oy * S) * W + ox * S) * C, true};
+    }
+    PQ_DEV Col col(int k) const {
+        if (k >= KS * KS * C) return {0, false};
+        int kh = f_kc.div(k), r2 = k - kh * KS * C;
+        int kw = f_c.div(r2), c = r2 - kw * C;
+        return {(kh * W + kw) * C + c, true};
+    }
+    PQ_DEV const void *addr(const Row &R, const Col &Cc, int &bytes, const LoadCtx &) const {
+        bytes = (R.ok && Cc.ok) ? 16 : 0;
+        return bytes ? (const void *)(x + R.off + Cc.off) : (const void *)x;
     }
 };
 
 // im2col over uint8 frame stacks addressed through a frame table:
 // sample b, channel c -> frame slot refs[map(b) * ref_stride + ref_off + c] (-1 = zero
 // frame) inside the frame ring; row m = (b, oy, ox) of the 20x20 conv1 output, col
-// k = (c, kh, kw) with kw = 0..7 being one 8-byte run.  Values are the raw bytes
-// 0..255 (exact in bf16); the 1/255 input scale is applied in the epilogue.
+// k = (c, kh, kw) with kw = 0..7 being one 8-byte run (4-byte aligned).  Values are the
+// raw bytes 0..255 (exact in bf16); the 1/255 input scale is applied in the epilogue.
+// The CTA first stages the slots of its sample window in shared memory (fill()); an
+// optional device counter slices the map (graph replay of the epoch index table).
 struct LoadFrames {
+    static constexpr bool U8 = true, TABLE = true;
     const uint8_t *ring;
     const int32_t *refs;
-    const int64_t *map;  // optional sample -> record index (replay sample)
+    const int64_t *map;
+    const int32_t *counter;
+    int map_stride;
     int n, ref_stride, ref_off;
-    PQ_DEV uint4 fetch(int m, int k) const {
-        if (m >= n * 400 || k >= 256) return make_uint4(0, 0, 0, 0);
-        int b = m / 400, rem = m - b * 400;
-        int oy = rem / 20, ox = rem - oy * 20;
-        int c = k >> 6, kh = (k >> 3) & 7;
-        int64_t rec = map ? map[b] : (int64_t)b;
-        int slot = __ldg(refs + rec * ref_stride + ref_off + c);
-        if (slot < 0) return make_uint4(0, 0, 0, 0);
-        const uint8_t *src = ring + (size_t)slot * 7056 + (oy * 4 + kh) * 84 + ox * 4;
-        uint32_t lo = __ldg(reinterpret_cast<const uint32_t *>(src));
-        uint32_t hi = __ldg(reinterpret_cast<const uint32_t *>(src + 4));
-        return u8x8_to_bf16(lo, hi);
+    FastDiv f400, f20;
+    struct Row {
+        int pix, b;
+        bool ok;
+    };
+    struct Col {
+        int c, kh;
+        bool ok;
+    };
+    PQ_DEV Row row(int m) const {
+        if (m >= n * 400) return {0, 0, false};
+        int b = f400.div(m), rem = m - b * 400;
+        int oy = f20.div(rem), ox = rem - oy * 20;
+        return {oy * 336 + ox * 4, b, true};
+    }
+    PQ_DEV Col col(int k) const { return {k >> 6, (k >> 3) & 7, k < 256}; }
+    PQ_DEV const void *addr(const Row &R, const Col &Cc, int &bytes, const LoadCtx &cx) const {
+        bytes = 0;
+        if (!R.ok || !Cc.ok) return ring;
+        int slot = cx.table[(R.b - cx.tb) * 4 + Cc.c];
+        if (slot < 0) return ring;
+        bytes = 8;
+        return ring + (size_t)slot * 7056 + R.pix + Cc.kh * 84;
+    }
+    // stage frame slots of samples [b_lo, b_hi] (all threads of the CTA)
+    PQ_DEV void fill(int b_lo, int b_hi, int32_t *table) const {
+        const int64_t base = (map && counter) ? (int64_t)(*counter) * map_stride : 0;
+        for (int e = threadIdx.x; e < (b_hi - b_lo + 1) * 4; e += blockDim.x) {
+            int b = b_lo + (e >> 2), c = e & 3;
+            int32_t v = -1;
+            if (b < n) {
+                int64_t rec = map ? map[base + b] : (int64_t)b;
+                v = refs[rec * ref_stride + ref_off + c];
+            }
+            table[e] = v;
+        }
     }
 };
 
-// transposed-conv window (data gradient): row m = input pixel (b, iy, ix) of an
-// H x W x C layer input, col t = (kh, kw, o); reads dY[b, (iy-kh)/S, (ix-kw)/S, o]
-// when the division is exact and in range.
+// transposed-conv window (data gradient, stride 1): row m = input pixel (b, iy, ix) of an
+// H x W layer input, col t = (kh, kw, o); reads dY[b, iy-kh, ix-kw, o] when in range.
 struct LoadTConv {
+    static constexpr bool U8 = false, TABLE = false;
     const bf16 *dy;
-    int n, H, W, OH, OW, O, KS, S;
-    PQ_DEV uint4 fetch(int m, int t) const {
-        int npix = H * W;
-        if (m >= n * npix || t >= KS * KS * O) return make_uint4(0, 0, 0, 0);
-        int b = m / npix, rem = m - b * npix;
-        int iy = rem / W, ix = rem - iy * W;
-        int ko = KS * O;
-        int kh = t / ko, r2 = t - kh * ko;
-        int kw = r2 / O, o = r2 - kw * O;
-        int ty = iy - kh, tx = ix - kw;
-        if (ty < 0 || tx < 0) return make_uint4(0, 0, 0, 0);
-        int oy = ty / S, ox = tx / S;
-        if (oy * S != ty || ox * S != tx || oy >= OH || ox >= OW) return make_uint4(0, 0, 0, 0);
-        const bf16 *src = dy + ((size_t)(b * OH + oy) * OW + ox) * O + o;
-        return __ldg(reinterpret_cast<const uint4 *>(src));
+    int n, H, W, OH, OW, O, KS;
+    FastDiv f_npix, f_w, f_ko, f_o;
+    struct Row {
+        int b, iy, ix;
+        bool ok;
+    };
+    struct Col {
+        int kh, kw, o;
+        bool ok;
+    };
+    PQ_DEV Row row(int m) const {
+        if (m >= n * H * W) return {0, 0, 0, false};
+        int b = f_npix.div(m), rem = m - b * H * W;
+        int iy = f_w.div(rem);
+        return {b, iy, rem - iy * W, true};
+    }
+    PQ_DEV Col col(int t) const {
+        if (t >= KS * KS * O) return {0, 0, 0, false};
+        int kh = f_ko.div(t), r2 = t - kh * KS * O;
+        int kw = f_o.div(r2);
+        return {kh, kw, r2 - kw * O, true};
+    }
+    PQ_DEV const void *addr(const Row &R, const Col &Cc, int &bytes, const LoadCtx &) const {
+        int oy = R.iy - Cc.kh, ox = R.ix - Cc.kw;
+        bytes = (R.ok && Cc.ok && oy >= 0 && ox >= 0 && oy < OH && ox < OW) ? 16 : 0;
+        return bytes ? (const void *)(dy + ((size_t)(R.b * OH + oy) * OW + ox) * O + Cc.o)
+                     : (const void *)dy;
     }
 };
 
 // conv weight W[o][kh][kw][c] viewed as [t = (kh, kw, o)][c] (rows t, contiguous c)
 struct LoadWeightT {
+    static constexpr bool U8 = false, TABLE = false;
     const bf16 *w;
     int O, KS, C;
-    PQ_DEV uint4 fetch(int t, int c) const {
-        if (t >= KS * KS * O || c >= C) return make_uint4(0, 0, 0, 0);
-        int ko = KS * O;
-        int kh = t / ko, r2 = t - kh * ko;
-        int kw = r2 / O, o = r2 - kw * O;
-        const bf16 *src = w + (size_t)o * (KS * KS * C) + (kh * KS + kw) * C + c;
-        return __ldg(reinterpret_cast<const uint4 *>(src));
+    FastDiv f_ko, f_o;
+    struct Row {
+        int off;
+        bool ok;
+    };
+    struct Col {
+        int c;
+        bool ok;
+    };
+    PQ_DEV Row row(int t) const {
+        if (t >= KS * KS * O) return {0, false};
+        int kh = f_ko.div(t), r2 = t - kh * KS * O;
+        int kw = f_o.div(r2), o = r2 - kw * O;
+        return {o * (KS * KS * C) + (kh * KS + kw) * C, true};
+    }
+    PQ_DEV Col col(int c) const { return {c, c < C}; }
+    PQ_DEV const void *addr(const Row &R, const Col &Cc, int &bytes, const LoadCtx &) const {
+        bytes = (R.ok && Cc.ok) ? 16 : 0;
+        return bytes ? (const void *)(w + R.off + Cc.c) : (const void *)w;
+    }
+};
+
+// Stride-2 transposed conv split into the 4 parity classes (py, px) of the input pixel:
+// a class sees only taps kh = py + 2i, kw = px + 2j (i, j in {0,1}), so the contraction
+// is 4 taps x O instead of 16 taps x O.  Grid rows are class-major, tpc tiles per class:
+// row m -> class = m / (tpc*128), local row = (b, iy', ix') with iy = 2 iy' + py.
+struct LoadTConvP {
+    static constexpr bool U8 = false, TABLE = false;
+    const bf16 *dy;
+    int n, H2, W2, OH, OW, O, tpc;  // H2 = H / 2
+    FastDiv f_per, f_npix, f_w2, f_o;
+    struct Row {
+        int b, iy2, ix2;
+        bool ok;
+    };
+    struct Col {
+        int ty, tx, o;
+        bool ok;
+    };
+    PQ_DEV Row row(int m) const {
+        int cls = f_per.div(m), loc = m - cls * tpc * 128;
+        if (loc >= n * H2 * W2) return {0, 0, 0, false};
+        int b = f_npix.div(loc), rem = loc - b * H2 * W2;
+        int iy2 = f_w2.div(rem);
+        return {b, iy2, rem - iy2 * W2, true};
+    }
+    PQ_DEV Col col(int t) const {
+        if (t >= 4 * O) return {0, 0, 0, false};
+        int tap = f_o.div(t);
+        return {tap >> 1, tap & 1, t - tap * O, true};
+    }
+    PQ_DEV const void *addr(const Row &R, const Col &Cc, int &bytes, const LoadCtx &) const {
+        int oy = R.iy2 - Cc.ty, ox = R.ix2 - Cc.tx;
+        bytes = (R.ok && Cc.ok && oy >= 0 && ox >= 0 && oy < OH && ox < OW) ? 16 : 0;
+        return bytes ? (const void *)(dy + ((size_t)(R.b * OH + oy) * OW + ox) * O + Cc.o)
+                     : (const void *)dy;
+    }
+};
+
+// weight operand of LoadTConvP: rows t = (tap, o) of the CTA's parity class
+struct LoadWeightTP {
+    static constexpr bool U8 = false, TABLE = false;
+    const bf16 *w;
+    int O, KS, C, tpc;
+    FastDiv f_o;
+    struct Row {
+        int off;
+        bool ok;
+    };
+    struct Col {
+        int c;
+        bool ok;
+    };
+    PQ_DEV Row row(int t) const {
+        if (t >= 4 * O) return {0, false};
+        int cls = blockIdx.x / tpc;
+        int py = cls >> 1, px = cls & 1;
+        int tap = f_o.div(t), o = t - tap * O;
+        int kh = py + 2 * (tap >> 1), kw = px + 2 * (tap & 1);
+        return {o * (KS * KS * C) + (kh * KS + kw) * C, true};
+    }
+    PQ_DEV Col col(int c) const { return {c, c < C}; }
+    PQ_DEV const void *addr(const Row &R, const Col &Cc, int &bytes, const LoadCtx &) const {
+        bytes = (R.ok && Cc.ok) ? 16 : 0;
+        return bytes ? (const void *)(w + R.off + Cc.c) : (const void *)w;
     }
 };
 
@@ -173,10 +350,29 @@ struct EpiF32 {
     PQ_DEV void apply(int m, int n0, const float *v, int cnt, int split) const {
         if (m >= M) return;
         float *dst = out + split * split_stride + (size_t)m * ld;
+        if (n0 + cnt <= N && (ld & 3) == 0) {
+            for (int j = 0; j < cnt; j += 4)
+                *reinterpret_cast<float4 *>(dst + n0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            return;
+        }
         for (int j = 0; j < cnt; ++j)
             if (n0 + j < N) dst[n0 + j] = v[j];
     }
 };
+
+// masked bf16 store of 8 values at dst (mask = forward activation at the same place)
+PQ_DEV void store_masked8(bf16 *dst, const bf16 *mask, const float *v) {
+    uint4 mk = *reinterpret_cast<const uint4 *>(mask);
+    uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
+    float y[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        y[2 * e] = bf16_lo(mw[e]) > 0.f ? v[2 * e] : 0.f;
+        y[2 * e + 1] = bf16_hi(mw[e]) > 0.f ? v[2 * e + 1] : 0.f;
+    }
+    *reinterpret_cast<uint4 *>(dst) = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]),
+                                                 pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
+}
 
 // data gradient: bf16 out[m][n] = acc * (mask[m][n] > 0), mask = forward activation
 struct EpiMask {
@@ -188,17 +384,29 @@ struct EpiMask {
         for (int j = 0; j < cnt; j += 8) {
             int n = n0 + j;
             if (n >= N) break;
-            uint4 mk = *reinterpret_cast<const uint4 *>(mask + (size_t)m * ld + n);
-            uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
-            float y[8];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                y[2 * e] = bf16_lo(mw[e]) > 0.f ? v[j + 2 * e] : 0.f;
-                y[2 * e + 1] = bf16_hi(mw[e]) > 0.f ? v[j + 2 * e + 1] : 0.f;
-            }
-            *reinterpret_cast<uint4 *>(out + (size_t)m * ld + n) =
-                make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]),
-                           pack_bf16(y[6], y[7]));
+            store_masked8(out + (size_t)m * ld + n, mask + (size_t)m * ld + n, v + j);
+        }
+    }
+};
+
+// EpiMask for LoadTConvP rows (class-major) -> NHWC position of the H x W input
+struct EpiMaskP {
+    bf16 *out;
+    const bf16 *mask;
+    int n, H2, W2, C, tpc;
+    FastDiv f_per, f_npix, f_w2;
+    PQ_DEV void apply(int m, int n0, const float *v, int cnt, int) const {
+        int cls = f_per.div(m), loc = m - cls * tpc * 128;
+        int npix = H2 * W2;
+        if (loc >= n * npix) return;
+        int b = f_npix.div(loc), rem = loc - b * npix;
+        int ry = f_w2.div(rem);
+        int iy = 2 * ry + (cls >> 1), ix = 2 * (rem - ry * W2) + (cls & 1);
+        size_t o = ((size_t)(b * 2 * H2 + iy) * (2 * W2) + ix) * C;
+        for (int j = 0; j < cnt; j += 8) {
+            int c = n0 + j;
+            if (c >= C) break;
+            store_masked8(out + o + c, mask + o + c, v + j);
         }
     }
 };
@@ -233,35 +441,48 @@ struct GemmArgs {
     int ones_extent;  // ... for contraction indices < ones_extent
 };
 
-constexpr int GEMM_STAGES = 4;
+constexpr int GEMM_THREADS = 256;
 constexpr int GEMM_A_BYTES = 128 * 64 * 2;
+constexpr int TABLE_SAMPLES = 64;
 
-template <int BN>
-constexpr int gemm_smem_bytes() {
-    return GEMM_STAGES * (GEMM_A_BYTES + BN * 128) + 1024;
-}
+template <int BN, bool U8A>
+struct GemmCfg {
+    static constexpr int B_BYTES = BN * 128;
+    static constexpr int U8_BYTES = U8A ? 128 * 64 : 0;  // raw uint8 staging of the A tile
+    static constexpr int STAGE = GEMM_A_BYTES + B_BYTES + U8_BYTES;
+    static constexpr int STAGES = (200 * 1024 / STAGE) < 6 ? (200 * 1024 / STAGE) : 6;
+    static constexpr int SMEM = STAGES * STAGE + 1024;
+};
 
 template <int BN, bool AMN, bool BMN, class LA, class LB, class EP>
-__global__ void __launch_bounds__(128, 1) k_gemm(const __grid_constant__ GemmArgs<LA, LB, EP> g) {
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    k_gemm(const __grid_constant__ GemmArgs<LA, LB, EP> g) {
     static_assert(BN == 16 || BN == 32 || BN == 64 || BN == 128 || BN == 256, "BN");
     static_assert(!BMN || BN >= 64, "MN-major B needs 64-wide swizzle atoms");
-    constexpr int B_BYTES = BN * 128;
-    constexpr int STAGE_BYTES = GEMM_A_BYTES + B_BYTES;
+    static_assert(!LB::TABLE, "frame tables are A-operand only");
+    using Cfg = GemmCfg<BN, LA::U8>;
+    constexpr int STAGES = Cfg::STAGES;
+    constexpr int PRE = STAGES - 1;
     constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
     constexpr uint32_t IDESC = idesc_bf16(BN, AMN, BMN);
-    constexpr int NB = BN * 8 / 128;  // B chunks per thread (BN=16 -> 1)
+    constexpr int NA = 1024 / GEMM_THREADS;                   // A chunks per thread (4)
+    constexpr int BCH = BN * 8;                               // B chunks per stage
+    constexpr int NB = BCH >= GEMM_THREADS ? BCH / GEMM_THREADS : 1;
+    constexpr int CPR = BN / 8;                               // MN-major B chunks per K row
+    constexpr int BSTEP = BMN ? GEMM_THREADS / CPR : GEMM_THREADS / 8;  // K (resp. MN) rows per i
 
     extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t bars[GEMM_STAGES];
+    __shared__ uint64_t bars[STAGES];
     __shared__ uint32_t tmem_base_s;
+    __shared__ int32_t table[LA::TABLE ? TABLE_SAMPLES * 4 : 1];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t smem_s = smem_u32(smem);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int grp = blockIdx.z / g.splits, split = blockIdx.z - grp * g.splits;
-    const LA &la = g.a[grp];
-    const LB &lb = g.b[grp];
-    const EP &ep = g.e[grp];
+    const LA la = g.a[grp];
+    const LB lb = g.b[grp];
     const int m0 = blockIdx.x * 128, n0 = blockIdx.y * BN;
     const int nk_total = (g.K + 63) >> 6;
     const int kb0 = split * g.kc_per_split;
@@ -269,74 +490,122 @@ __global__ void __launch_bounds__(128, 1) k_gemm(const __grid_constant__ GemmArg
     const int nk = kb1 > kb0 ? kb1 - kb0 : 0;
 
     if (tid == 0) {
-        for (int s = 0; s < GEMM_STAGES; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc<TMEM_COLS>(&tmem_base_s);
+    LoadCtx cx{table, 0};
+    if constexpr (LA::TABLE) {
+        // sample window of the rows this CTA reads: MN rows (K-major) or the split's
+        // contraction range (MN-major)
+        const int lo = AMN ? kb0 * 64 : m0;
+        const int hi = AMN ? max(lo, kb1 * 64 - 1) : m0 + 127;
+        cx.tb = lo / 400;
+        int last = min(hi / 400, cx.tb + TABLE_SAMPLES - 1);
+        la.fill(cx.tb, last, table);
+    }
+
+    // fixed per-thread operand contexts
+    const int a_c8 = AMN ? (tid & 15) : (tid & 7);      // fixed inner chunk
+    const int a_r0 = AMN ? (tid >> 4) : (tid >> 3);     // first outer row
+    const int a_rs = AMN ? 16 : 32;                     // outer step per i
+    const int b_c8 = BMN ? (tid % CPR) : (tid & 7);
+    const int b_r0 = BMN ? (tid / CPR) : (tid >> 3);
+    typename LA::Row ra[NA];
+    typename LA::Col ca{};
+    typename LB::Row rb[NB];
+    typename LB::Col cb{};
+    if (!AMN) {
+#pragma unroll
+        for (int i = 0; i < NA; ++i) ra[i] = la.row(m0 + a_r0 + i * a_rs);
+    } else {
+        ca = la.col(m0 + a_c8 * 8);
+    }
+    const bool b_live = BCH >= GEMM_THREADS || tid < BCH;
+    if (!BMN) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) rb[i] = lb.row(n0 + b_r0 + i * BSTEP);
+    } else {
+        cb = lb.col(n0 + b_c8 * 8);
+    }
+    const bool has_ones = AMN && g.ones_at >= m0 + a_c8 * 8 && g.ones_at < m0 + a_c8 * 8 + 8;
+
+    // issue the cp.async copies of K-chunk kb into ring slot s
+    auto issue = [&](int kb, int s) {
+        const int k0 = kb * 64;
+        const uint32_t a_s = smem_s + s * Cfg::STAGE;
+        const uint32_t b_s = a_s + GEMM_A_BYTES;
+        const uint32_t u_s = b_s + Cfg::B_BYTES;
+        typename LA::Col cak = AMN ? ca : la.col(k0 + a_c8 * 8);
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+            const int r = a_r0 + i * a_rs;  // outer row within the tile
+            const int q = AMN ? (r * 16 + a_c8) : (r * 8 + a_c8);
+            typename LA::Row rr = AMN ? la.row(k0 + r) : ra[i];
+            int bytes;
+            const void *src = la.addr(rr, cak, bytes, cx);
+            if (LA::U8) {
+                const uint8_t *p = static_cast<const uint8_t *>(src);
+                cp_async4(u_s + q * 8, p, bytes > 0 ? 4 : 0);
+                cp_async4(u_s + q * 8 + 4, bytes > 0 ? p + 4 : p, bytes > 0 ? 4 : 0);
+            } else {
+                const uint32_t off = AMN ? mnmaj_off(r, a_c8) : kmaj_off(r, a_c8);
+                cp_async16(a_s + off, src, bytes);
+            }
+        }
+        if (b_live) {
+            typename LB::Col cbk = BMN ? cb : lb.col(k0 + b_c8 * 8);
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                const int r = b_r0 + i * BSTEP;
+                typename LB::Row rr = BMN ? lb.row(k0 + r) : rb[i];
+                int bytes;
+                const void *src = lb.addr(rr, cbk, bytes, cx);
+                const uint32_t off = BMN ? mnmaj_off(r, b_c8) : kmaj_off(r, b_c8);
+                cp_async16(b_s + off, src, bytes);
+            }
+        }
+    };
+    // after this thread's copies of chunk kb landed: widen its own uint8 chunks to
+    // bf16 and write the bias-gradient "ones" element into its own chunk (if any)
+    auto post = [&](int kb, int s) {
+        if (!LA::U8 && !has_ones) return;
+        uint8_t *a_p = smem + s * Cfg::STAGE;
+        const uint8_t *u_p = a_p + GEMM_A_BYTES + Cfg::B_BYTES;
+        const int k0 = kb * 64;
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+            const int r = a_r0 + i * a_rs;
+            const int q = AMN ? (r * 16 + a_c8) : (r * 8 + a_c8);
+            const uint32_t off = AMN ? mnmaj_off(r, a_c8) : kmaj_off(r, a_c8);
+            if (LA::U8) {
+                uint2 raw = *reinterpret_cast<const uint2 *>(u_p + q * 8);
+                *reinterpret_cast<uint4 *>(a_p + off) = u8x8_to_bf16(raw.x, raw.y);
+            }
+            if (has_ones && k0 + r < g.ones_extent)
+                *reinterpret_cast<uint16_t *>(a_p + off + (g.ones_at - m0 - a_c8 * 8) * 2) = 0x3F80;
+        }
+    };
+
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
 
-    uint4 ra[8], rb[NB];
-    auto fetch = [&](int kb) {
-        const int k0 = kb * 64;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            int q = tid + i * 128;
-            if (!AMN) {
-                ra[i] = la.fetch(m0 + (q >> 3), k0 + (q & 7) * 8);
-            } else {
-                int kk = q >> 4, inner = m0 + (q & 15) * 8;
-                uint4 v = la.fetch(k0 + kk, inner);
-                if (g.ones_at >= inner && g.ones_at < inner + 8 && k0 + kk < g.ones_extent) {
-                    int e = g.ones_at - inner;
-                    uint32_t *w = reinterpret_cast<uint32_t *>(&v) + (e >> 1);
-                    *w = (e & 1) ? ((*w & 0x0000FFFFu) | 0x3F800000u) : ((*w & 0xFFFF0000u) | 0x3F80u);
-                }
-                ra[i] = v;
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            int q = tid + i * 128;
-            if (!BMN) {
-                rb[i] = lb.fetch(n0 + (q >> 3), k0 + (q & 7) * 8);
-            } else {
-                constexpr int CPR = BN / 8;  // chunks per K row
-                rb[i] = lb.fetch(k0 + q / CPR, n0 + (q % CPR) * 8);
-            }
-        }
-    };
-    auto store = [&](int s) {
-        uint8_t *a_s = smem + s * STAGE_BYTES;
-        uint8_t *b_s = a_s + GEMM_A_BYTES;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            int q = tid + i * 128;
-            uint32_t off = AMN ? mnmaj_off(q >> 4, q & 15) : kmaj_off(q >> 3, q & 7);
-            *reinterpret_cast<uint4 *>(a_s + off) = ra[i];
-        }
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            int q = tid + i * 128;
-            constexpr int CPR = BN / 8;
-            uint32_t off = BMN ? mnmaj_off(q / CPR, q % CPR) : kmaj_off(q >> 3, q & 7);
-            *reinterpret_cast<uint4 *>(b_s + off) = rb[i];
-        }
-    };
-
-    if (nk > 0) fetch(kb0);
+    for (int s = 0; s < PRE; ++s) {
+        if (s < nk) issue(kb0 + s, s);
+        cp_async_commit();
+    }
     for (int i = 0; i < nk; ++i) {
-        const int s = i % GEMM_STAGES;
-        if (i >= GEMM_STAGES) mbar_wait(&bars[s], ((i / GEMM_STAGES) - 1) & 1);
-        store(s);
-        if (i + 1 < nk) fetch(kb0 + i + 1);
+        const int s = i % STAGES;
+        cp_async_wait<PRE - 1>();
+        post(kb0 + i, s);
         fence_proxy_async_smem();
         __syncthreads();
         if (tid == 0) {
             tc_fence_after();
-            const uint32_t a_addr = smem_u32(smem + s * STAGE_BYTES);
+            const uint32_t a_addr = smem_s + s * Cfg::STAGE;
             const uint32_t b_addr = a_addr + GEMM_A_BYTES;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -346,28 +615,43 @@ __global__ void __launch_bounds__(128, 1) k_gemm(const __grid_constant__ GemmArg
             }
             umma_commit(&bars[s]);
         }
+        const int jn = i + PRE;
+        if (jn < nk) {
+            const int sl = jn % STAGES;
+            if (jn >= STAGES) mbar_wait(&bars[sl], ((jn / STAGES) - 1) & 1);
+            issue(kb0 + jn, sl);
+        }
+        cp_async_commit();
     }
     if (nk > 0) {
         const int last = nk - 1;
-        mbar_wait(&bars[last % GEMM_STAGES], (last / GEMM_STAGES) & 1);
+        mbar_wait(&bars[last % STAGES], (last / STAGES) & 1);
     }
     tc_fence_after();
 
-    const int row = m0 + warp * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    // epilogue: warp w reads TMEM lanes 32*(w%4).. (tile rows); the two warpgroups
+    // split the columns
+    const EP &ep = g.e[grp];
+    const int wq = warp & 3, half = warp >> 2;
+    const int row = m0 + wq * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
+    constexpr int CW = BN >= 64 ? BN / 2 : BN;  // columns per warpgroup
+    if (BN >= 64 || half == 0) {
+        const int cbeg = BN >= 64 ? half * CW : 0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        if (nk > 0) {
-            if (BN >= 32)
-                tmem_ld32(trow + c0, v);
-            else
-                tmem_ld16(trow + c0, v);
-        } else {
+        for (int c0 = cbeg; c0 < cbeg + CW; c0 += 32) {
+            float v[32];
+            if (nk > 0) {
+                if (BN >= 32)
+                    tmem_ld32(trow + c0, v);
+                else
+                    tmem_ld16(trow + c0, v);
+            } else {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = 0.f;
+                for (int e = 0; e < 32; ++e) v[e] = 0.f;
+            }
+            ep.apply(row, n0 + c0, v, BN < 32 ? BN : 32, split);
         }
-        ep.apply(row, n0 + c0, v, BN < 32 ? BN : 32, split);
     }
     tc_fence_before();
     __syncthreads();
@@ -375,17 +659,17 @@ __global__ void __launch_bounds__(128, 1) k_gemm(const __grid_constant__ GemmArg
 }
 
 template <int BN, bool AMN, bool BMN, class LA, class LB, class EP>
-cudaError_t launch_gemm(const GemmArgs<LA, LB, EP> &g, int groups, cudaStream_t st) {
+cudaError_t launch_gemm(const GemmArgs<LA, LB, EP> &g, int groups, cudaStream_t st, int grid_x = 0) {
     auto kern = k_gemm<BN, AMN, BMN, LA, LB, EP>;
-    constexpr int smem = gemm_smem_bytes<BN>();
+    constexpr int smem = GemmCfg<BN, LA::U8>::SMEM;
     static bool configured = false;  // per instantiation
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    dim3 grid((g.M + 127) / 128, (g.N + BN - 1) / BN, groups * g.splits);
-    kern<<<grid, 128, smem, st>>>(g);
+    dim3 grid(grid_x ? grid_x : (g.M + 127) / 128, (g.N + BN - 1) / BN, groups * g.splits);
+    kern<<<grid, GEMM_THREADS, smem, st>>>(g);
     return cudaGetLastError();
 }
 

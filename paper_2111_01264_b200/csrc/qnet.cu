@@ -45,6 +45,7 @@ struct WS {
     int32_t *act;
     bf16 *dY3, *dY2, *dY1;
     float *part1, *part2, *part3, *grad4;
+    uint32_t *done;  // [2] CTA completion counters (optimizer, acting)
     int n8;
     size_t bytes;
 };
@@ -80,6 +81,7 @@ static WS carve(void *base, int N, int A) {
     w.part2 = (float *)take((size_t)MAX_SPLITS * 64 * 513 * 4);
     w.part3 = (float *)take((size_t)MAX_SPLITS * 64 * 577 * 4);
     w.grad4 = (float *)take((size_t)512 * 3136 * 4);
+    w.done = (uint32_t *)take(2 * sizeof(uint32_t));
     w.bytes = off;
     return w;
 }
@@ -94,34 +96,50 @@ struct FwdInput {  // frame-stack addressing of one group
     int ref_stride, ref_off;
 };
 
-}  // namespace pq
 
-// LoadFrames with a device-counter-sliced map (graph replay of the epoch index table)
-namespace pq {
-struct LoadFramesC {
-    LoadFrames f;
-    const int32_t *counter;
-    int map_stride;
-    PQ_DEV uint4 fetch(int m, int k) const {
-        if (counter && f.map) {
-            LoadFrames g2 = f;
-            g2.map = f.map + (int64_t)(*counter) * map_stride;
-            return g2.fetch(m, k);
-        }
-        return f.fetch(m, k);
-    }
-};
+// loader / epilogue constructors (host side precomputes the multiply-shift divisors)
+static LoadIm2col im2col(const bf16 *x, int n, int H, int W, int C, int KS, int S, int OH, int OW) {
+    LoadIm2col l{x, n, H, W, C, KS, S, OH, OW};
+    l.f_npix = FastDiv(OH * OW), l.f_ow = FastDiv(OW), l.f_kc = FastDiv(KS * C), l.f_c = FastDiv(C);
+    return l;
+}
+static LoadTConv tconv(const bf16 *dy, int n, int H, int W, int OH, int OW, int O, int KS) {
+    LoadTConv l{dy, n, H, W, OH, OW, O, KS};
+    l.f_npix = FastDiv(H * W), l.f_w = FastDiv(W), l.f_ko = FastDiv(KS * O), l.f_o = FastDiv(O);
+    return l;
+}
+static LoadWeightT weight_t(const bf16 *w, int O, int KS, int C) {
+    LoadWeightT l{w, O, KS, C};
+    l.f_ko = FastDiv(KS * O), l.f_o = FastDiv(O);
+    return l;
+}
+static LoadTConvP tconv_p(const bf16 *dy, int n, int H2, int W2, int OH, int OW, int O, int tpc) {
+    LoadTConvP l{dy, n, H2, W2, OH, OW, O, tpc};
+    l.f_per = FastDiv(tpc * 128), l.f_npix = FastDiv(H2 * W2), l.f_w2 = FastDiv(W2), l.f_o = FastDiv(O);
+    return l;
+}
+static LoadWeightTP weight_tp(const bf16 *w, int O, int KS, int C, int tpc) {
+    LoadWeightTP l{w, O, KS, C, tpc};
+    l.f_o = FastDiv(O);
+    return l;
+}
+static EpiMaskP epi_mask_p(bf16 *out, const bf16 *mask, int n, int H2, int W2, int C, int tpc) {
+    EpiMaskP e{out, mask, n, H2, W2, C, tpc};
+    e.f_per = FastDiv(tpc * 128), e.f_npix = FastDiv(H2 * W2), e.f_w2 = FastDiv(W2);
+    return e;
+}
 
-static LoadFramesC frames_loader(const FwdInput &in, int n) {
-    LoadFramesC l;
-    l.f.ring = in.ring;
-    l.f.refs = in.refs;
-    l.f.map = in.map;
-    l.f.n = n;
-    l.f.ref_stride = in.ref_stride;
-    l.f.ref_off = in.ref_off;
+static LoadFrames frames_loader(const FwdInput &in, int n) {
+    LoadFrames l;
+    l.ring = in.ring;
+    l.refs = in.refs;
+    l.map = in.map;
     l.counter = in.counter;
     l.map_stride = in.map_stride;
+    l.n = n;
+    l.ref_stride = in.ref_stride;
+    l.ref_off = in.ref_off;
+    l.f400 = FastDiv(400), l.f20 = FastDiv(20);
     return l;
 }
 
@@ -144,7 +162,7 @@ static cudaError_t launch_bn(int bn, const GemmArgs<LA, LB, EP> &g, int groups, 
 static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, int n, const WS &w,
                          cudaStream_t st) {
     {  // F1: conv1 8x8/4 over uint8 frames (K = 256), bias + ReLU, x 1/255
-        GemmArgs<LoadFramesC, LoadDense, EpiBiasRelu> g{};
+        GemmArgs<LoadFrames, LoadDense, EpiBiasRelu> g{};
         for (int q = 0; q < groups; ++q) {
             g.a[q] = frames_loader(ins[q], n);
             g.b[q] = LoadDense{(const bf16 *)nets[q].shadow + S_W1, 32, 256, 256};
@@ -156,7 +174,7 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
     {  // F2: conv2 4x4/2 over 20x20x32 (K = 512)
         GemmArgs<LoadIm2col, LoadDense, EpiBiasRelu> g{};
         for (int q = 0; q < groups; ++q) {
-            g.a[q] = LoadIm2col{w.act1[q], n, 20, 20, 32, 4, 2, 9, 9};
+            g.a[q] = im2col(w.act1[q], n, 20, 20, 32, 4, 2, 9, 9);
             g.b[q] = LoadDense{(const bf16 *)nets[q].shadow + S_W2, 64, 512, 512};
             g.e[q] = EpiBiasRelu{w.act2[q], nets[q].master + P_B2, n * 81, 64, 64, 1.0f};
         }
@@ -166,7 +184,7 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
     {  // F3: conv3 3x3/1 over 9x9x64 (K = 576)
         GemmArgs<LoadIm2col, LoadDense, EpiBiasRelu> g{};
         for (int q = 0; q < groups; ++q) {
-            g.a[q] = LoadIm2col{w.act2[q], n, 9, 9, 64, 3, 1, 7, 7};
+            g.a[q] = im2col(w.act2[q], n, 9, 9, 64, 3, 1, 7, 7);
             g.b[q] = LoadDense{(const bf16 *)nets[q].shadow + S_W3, 64, 576, 576};
             g.e[q] = EpiBiasRelu{w.act3[q], nets[q].master + P_B3, n * 49, 64, 64, 1.0f};
         }
@@ -215,43 +233,72 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// fc1 reduction + bias + ReLU, fc2, and (learner) TD target / error / fc2 back-prop.
-__global__ void __launch_bounds__(128) k_head(const HeadArgs a) {
+// fc1 split-K reduction + bias + ReLU into shared memory, fc2 with one warp per action,
+// and (learner) the TD target / error (agent.py:69-81, output_delta) and the fc2
+// back-prop through the fc1 ReLU mask (hidden_delta).  One 256-thread CTA per sample;
+// every global load of a phase is independent so they are all in flight together.
+constexpr int HEAD_THREADS = 256;
+__global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
     const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    __shared__ float red[2][4][MAX_ACTIONS];
+    __shared__ float hs[2][512];
     __shared__ float qs[2][MAX_ACTIONS];
     __shared__ float s_delta;
     __shared__ int s_act;
-    float h[2][4];
-    for (int g = 0; g < a.groups; ++g) {
-        const float *P = a.part[g];
-        const float *mp = a.master[g];
+    // the sampled record (action, reward, terminal) is fetched early by thread 0
+    int4 rec_hi = make_int4(0, 0, 0, 0);
+    if (a.learner && tid == 0 && !a.ext_targets) {
+        int64_t slot = a.idx        ? a.idx[b]
+                       : a.idx_base ? a.idx_base[(int64_t)(*a.counter) * a.n + b]
+                                    : (int64_t)b;
+        rec_hi = *reinterpret_cast<const int4 *>(a.records + slot * REC_INTS + 4);
+    }
+    {
+        float v[2][2][FC1_SPLITS + 1];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            int j = tid + 128 * i;
-            float s = 0.f;
-            for (int sp = 0; sp < FC1_SPLITS; ++sp) s += P[((size_t)sp * a.n + b) * 512 + j];
-            s += mp[P_B4 + j];
-            h[g][i] = s > 0.f ? s : 0.f;
-        }
-#pragma unroll 4
-        for (int aa = 0; aa < MAX_ACTIONS; ++aa) {
-            if (aa >= a.A) break;
-            float acc = 0.f;
+        for (int g = 0; g < 2; ++g)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) acc += mp[P_W5 + aa * 512 + tid + 128 * i] * h[g][i];
-            acc = warp_sum(acc);
-            if (lane == 0) red[g][warp][aa] = acc;
-        }
+            for (int i = 0; i < 2; ++i) {
+                const int j = tid + HEAD_THREADS * i;
+                const int gg = g < a.groups ? g : 0;
+                const float *P = a.part[gg] + (size_t)b * 512 + j;
+#pragma unroll
+                for (int sp = 0; sp < FC1_SPLITS; ++sp) v[g][i][sp] = P[(size_t)sp * a.n * 512];
+                v[g][i][FC1_SPLITS] = a.master[gg][P_B4 + j];
+            }
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                float s = 0.f;
+#pragma unroll
+                for (int sp = 0; sp < FC1_SPLITS; ++sp) s += v[g][i][sp];
+                s += v[g][i][FC1_SPLITS];
+                hs[g][tid + HEAD_THREADS * i] = s > 0.f ? s : 0.f;
+            }
     }
     __syncthreads();
-    if (tid < a.A) {
-        for (int g = 0; g < a.groups; ++g) {
-            float q = red[g][0][tid] + red[g][1][tid] + red[g][2][tid] + red[g][3][tid] +
-                      a.master[g][p_b5(a.A) + tid];
-            qs[g][tid] = q;
-            a.q_out[((size_t)g * a.n + b) * a.A + tid] = q;
-            if (a.q_copy) a.q_copy[((size_t)g * a.n + b) * a.A + tid] = q;
+    for (int g = 0; g < a.groups; ++g) {
+        const float *w5 = a.master[g] + P_W5;
+        float wv[4][16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int aa = min(warp + 8 * u, a.A - 1);
+#pragma unroll
+            for (int t = 0; t < 16; ++t) wv[u][t] = w5[aa * 512 + lane + 32 * t];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int aa = warp + 8 * u;
+            float acc = 0.f;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) acc += wv[u][t] * hs[g][lane + 32 * t];
+            acc = warp_sum(acc);
+            if (lane == 0 && aa < a.A) {
+                float q = acc + a.master[g][p_b5(a.A) + aa];
+                qs[g][aa] = q;
+                a.q_out[((size_t)g * a.n + b) * a.A + aa] = q;
+                if (a.q_copy) a.q_copy[((size_t)g * a.n + b) * a.A + aa] = q;
+            }
         }
     }
     if (!a.learner) return;
@@ -263,13 +310,9 @@ __global__ void __launch_bounds__(128) k_head(const HeadArgs a) {
             act = a.ext_actions[b];
             target = a.ext_targets[b];
         } else {
-            int64_t slot = a.idx        ? a.idx[b]
-                           : a.idx_base ? a.idx_base[(int64_t)(*a.counter) * a.n + b]
-                                        : (int64_t)b;
-            const int32_t *rec = a.records + slot * REC_INTS;
-            act = rec[5];
-            float r = __int_as_float(rec[6]);
-            if (rec[7]) {
+            act = rec_hi.y;
+            const float r = __int_as_float(rec_hi.z);
+            if (rec_hi.w) {
                 target = r;
             } else {
                 float mx = qs[1][0];
@@ -277,8 +320,7 @@ __global__ void __launch_bounds__(128) k_head(const HeadArgs a) {
                 target = r + a.gamma * mx;
             }
         }
-        float q = qs[0][act];
-        float d = q - target;  // = n * output_delta (agent.py:103-104 summed gradient)
+        float d = qs[0][act] - target;  // = n * output_delta (agent.py:103-104 summed gradient)
         s_delta = d;
         s_act = act;
         a.act_out[b] = act;
@@ -295,13 +337,13 @@ __global__ void __launch_bounds__(128) k_head(const HeadArgs a) {
     const float d = s_delta;
     const float *w5 = a.master[0] + P_W5 + (size_t)s_act * 512;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        int j = tid + 128 * i;
-        float hv = h[0][i];
-        float g = hv > 0.f ? d * w5[j] : 0.f;  // hidden_delta with the fc1 ReLU mask
+    for (int i = 0; i < 2; ++i) {
+        const int j = tid + HEAD_THREADS * i;
+        const float hv = hs[0][j];
+        const float g = hv > 0.f ? d * w5[j] : 0.f;  // hidden_delta with the fc1 ReLU mask
         a.h1[(size_t)b * 512 + j] = hv;
         a.dh1[(size_t)b * 512 + j] = g;
-        bf16 gb = __float2bfloat16_rn(g);
+        const bf16 gb = __float2bfloat16_rn(g);
         a.dh1_bf[(size_t)b * 512 + j] = gb;
         a.dh1T[(size_t)j * a.n8 + b] = gb;
     }
@@ -324,7 +366,7 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
         h.ext_actions = la->ext_actions, h.gamma = la->gamma;
         h.q_copy = la->q_out, h.td_copy = la->td_out;
     }
-    k_head<<<n, 128, 0, st>>>(h);
+    k_head<<<n, HEAD_THREADS, 0, st>>>(h);
     return cuda_err(cudaGetLastError(), "head");
 }
 
@@ -340,7 +382,8 @@ struct OptArgs {
     int n, A;
     float lr, rho, kappa;
     int32_t *flag;
-    int32_t *counter;  // update id source; incremented once per step
+    int32_t *counter;  // update id source; incremented once per step by the last CTA
+    uint32_t *done;    // CTA completion counter for that increment
     float *grad_out;
     int64_t total;
 };
@@ -351,82 +394,160 @@ __device__ __forceinline__ float sum_part(const float *part, int splits, size_t 
     return s;
 }
 
-__global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.total) return;
-    float g;
-    int64_t sh = -1;
+// last CTA of a grid bumps a device step counter (replaces a separate launch)
+__device__ __forceinline__ void last_block_bump(int32_t *counter, uint32_t *done) {
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(done, 1u) == gridDim.x * gridDim.y * gridDim.z - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        *counter += 1;
+        *done = 0;
+        __threadfence();
+    }
+}
+
+__device__ __forceinline__ float grad_of(const OptArgs &a, int64_t i, int64_t &sh) {
+    sh = -1;
     if (i < P_B1) {
         int o = (int)(i >> 8), k = (int)(i & 255);
-        g = sum_part(a.part1, a.s1, 32 * 257, (size_t)o * 257 + k) * (1.0f / 255.0f);
         sh = S_W1 + i;
-    } else if (i < P_W2) {
-        g = sum_part(a.part1, a.s1, 32 * 257, (size_t)(i - P_B1) * 257 + 256);
-    } else if (i < P_B2) {
+        return sum_part(a.part1, a.s1, 32 * 257, (size_t)o * 257 + k) * (1.0f / 255.0f);
+    }
+    if (i < P_W2) return sum_part(a.part1, a.s1, 32 * 257, (size_t)(i - P_B1) * 257 + 256);
+    if (i < P_B2) {
         int64_t r = i - P_W2;
-        g = sum_part(a.part2, a.s2, 64 * 513, (size_t)(r / 512) * 513 + (r % 512));
         sh = S_W2 + r;
-    } else if (i < P_W3) {
-        g = sum_part(a.part2, a.s2, 64 * 513, (size_t)(i - P_B2) * 513 + 512);
-    } else if (i < P_B3) {
+        return sum_part(a.part2, a.s2, 64 * 513, (size_t)(r >> 9) * 513 + (r & 511));
+    }
+    if (i < P_W3) return sum_part(a.part2, a.s2, 64 * 513, (size_t)(i - P_B2) * 513 + 512);
+    if (i < P_B3) {
         int64_t r = i - P_W3;
-        g = sum_part(a.part3, a.s3, 64 * 577, (size_t)(r / 576) * 577 + (r % 576));
         sh = S_W3 + r;
-    } else if (i < P_W4) {
-        g = sum_part(a.part3, a.s3, 64 * 577, (size_t)(i - P_B3) * 577 + 576);
-    } else if (i < P_B4) {
-        g = a.grad4[i - P_W4];
+        return sum_part(a.part3, a.s3, 64 * 577, (size_t)(r / 576) * 577 + (r % 576));
+    }
+    if (i < P_W4) return sum_part(a.part3, a.s3, 64 * 577, (size_t)(i - P_B3) * 577 + 576);
+    if (i < P_B4) {
         sh = S_W4 + (i - P_W4);
-    } else if (i < P_W5) {
+        return a.grad4[i - P_W4];
+    }
+    float g = 0.f;
+    if (i < P_W5) {
         int j = (int)(i - P_B4);
-        g = 0.f;
         for (int b = 0; b < a.n; ++b) g += a.dh1[(size_t)b * 512 + j];
     } else if (i < p_b5(a.A)) {
         int64_t r = i - P_W5;
-        int aa = (int)(r / 512), j = (int)(r % 512);
-        g = 0.f;
+        int aa = (int)(r >> 9), j = (int)(r & 511);
         for (int b = 0; b < a.n; ++b)
             if (a.act[b] == aa) g += a.td[b * 3 + 1] * a.h1[(size_t)b * 512 + j];
     } else {
         int aa = (int)(i - p_b5(a.A));
-        g = 0.f;
         for (int b = 0; b < a.n; ++b)
             if (a.act[b] == aa) g += a.td[b * 3 + 1];
     }
-    if (a.grad_out) a.grad_out[i] = g;
-    if (!isfinite(g)) atomicMin(a.flag, a.counter ? *a.counter : 0);
-    // centered RMSProp, kappa inside the square root (_kernels_numba.py:98-111)
-    float mi = a.rho * a.m[i] + (1.0f - a.rho) * g;
-    float vi = a.rho * a.v[i] + (1.0f - a.rho) * g * g;
-    float pi = a.p[i] - a.lr * g / sqrtf(vi - mi * mi + a.kappa);
-    a.m2[i] = mi;
-    a.v2[i] = vi;
-    a.p2[i] = pi;
-    if (sh >= 0) a.shadow[sh] = __float2bfloat16_rn(pi);
+    return g;
 }
 
-__global__ void k_bump(int32_t *counter) { *counter += 1; }
+// centered RMSProp, kappa inside the square root (_kernels_numba.py:98-111)
+__device__ __forceinline__ void rms(const OptArgs &a, float g, float m, float v, float p,
+                                    float &m2, float &v2, float &p2) {
+    m2 = a.rho * m + (1.0f - a.rho) * g;
+    v2 = a.rho * v + (1.0f - a.rho) * g * g;
+    p2 = p - a.lr * g / sqrtf(v2 - m2 * m2 + a.kappa);
+}
 
-static int choose_kc(int nchunks, int mtiles, int *splits) {
+__global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
+    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    const int upd = a.counter ? *a.counter : 0;
+    bool bad = false;
+    if (i0 >= P_W4 && i0 + 4 <= P_B4) {  // fc1 weight: 16-byte vector path
+        const int64_t r = i0 - P_W4;
+        const float4 g = *reinterpret_cast<const float4 *>(a.grad4 + r);
+        const float4 m = *reinterpret_cast<const float4 *>(a.m + i0);
+        const float4 v = *reinterpret_cast<const float4 *>(a.v + i0);
+        const float4 p = *reinterpret_cast<const float4 *>(a.p + i0);
+        float4 m2, v2, p2;
+        rms(a, g.x, m.x, v.x, p.x, m2.x, v2.x, p2.x);
+        rms(a, g.y, m.y, v.y, p.y, m2.y, v2.y, p2.y);
+        rms(a, g.z, m.z, v.z, p.z, m2.z, v2.z, p2.z);
+        rms(a, g.w, m.w, v.w, p.w, m2.w, v2.w, p2.w);
+        *reinterpret_cast<float4 *>(a.m2 + i0) = m2;
+        *reinterpret_cast<float4 *>(a.v2 + i0) = v2;
+        *reinterpret_cast<float4 *>(a.p2 + i0) = p2;
+        *reinterpret_cast<uint2 *>(a.shadow + S_W4 + r) =
+            make_uint2(pack_bf16(p2.x, p2.y), pack_bf16(p2.z, p2.w));
+        if (a.grad_out) *reinterpret_cast<float4 *>(a.grad_out + i0) = g;
+        bad = !(isfinite(g.x) && isfinite(g.y) && isfinite(g.z) && isfinite(g.w));
+    } else {
+        for (int e = 0; e < 4; ++e) {
+            const int64_t i = i0 + e;
+            if (i >= a.total) break;
+            int64_t sh;
+            const float g = grad_of(a, i, sh);
+            float m2, v2, p2;
+            rms(a, g, a.m[i], a.v[i], a.p[i], m2, v2, p2);
+            a.m2[i] = m2;
+            a.v2[i] = v2;
+            a.p2[i] = p2;
+            if (sh >= 0) a.shadow[sh] = __float2bfloat16_rn(p2);
+            if (a.grad_out) a.grad_out[i] = g;
+            bad |= !isfinite(g);
+        }
+    }
+    if (bad) atomicMin(a.flag, upd);
+    if (a.counter) last_block_bump(a.counter, a.done);
+}
+
+static int choose_kc(int nchunks, int mtiles, int *splits, int kc_max = 1 << 30) {
     int kc = (nchunks * mtiles + 147) / 148;
     if (kc < 2) kc = 2;
     int need = (nchunks + MAX_SPLITS - 1) / MAX_SPLITS;
     if (kc < need) kc = need;
+    if (kc > kc_max) kc = kc_max;
     *splits = (nchunks + kc - 1) / kc;
     return kc;
+}
+
+// side stream + events for the weight-gradient branch (fork after each data
+// gradient, join before the optimizer); also captured into CUDA graphs as branches
+struct Fork {
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev[4] = {};
+};
+static Fork g_fork[16];
+
+static int get_fork(Fork **out) {
+    int dev = 0;
+    PQ_CHECK(cudaGetDevice(&dev), "get device");
+    Fork &f = g_fork[dev & 15];
+    if (!f.side) {
+        PQ_CHECK(cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking), "side stream");
+        for (auto &e : f.ev) PQ_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    *out = &f;
+    return 0;
 }
 
 static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cudaStream_t st) {
     const pq_net &th = la->theta;
     const bf16 *sh = (const bf16 *)th.shadow;
     int s1 = 1, s2 = 1, s3 = 1;
+    Fork *fk = nullptr;
+    if (int rc = get_fork(&fk)) return rc;
+    cudaStream_t side = fk->side;
+    // fork: fc1 wgrad needs only the head outputs
+    PQ_CHECK(cudaEventRecord(fk->ev[0], st), "fork0");
+    PQ_CHECK(cudaStreamWaitEvent(side, fk->ev[0], 0), "fork0 wait");
     {  // B4w: dW4[j][k] = sum_b dh1[b][j] x3[b][k]  (contraction over the batch)
         GemmArgs<LoadDense, LoadDense, EpiF32> g{};
         g.a[0] = LoadDense{w.dh1T, 512, n, w.n8};
         g.b[0] = LoadDense{w.act3[0], n, 3136, 3136};
         g.e[0] = EpiF32{w.grad4, 512, 3136, 3136, 0};
         g.M = 512, g.N = 3136, g.K = n, g.kc_per_split = (n + 63) / 64, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<64, false, true>(g, 1, st)), "fc1 wgrad");
+        PQ_CHECK((launch_gemm<64, false, true>(g, 1, side)), "fc1 wgrad");
     }
     {  // B4d: dY3[b][k] = relu'(x3) * sum_j W4[j][k] dh1[b][j]   (D[k][b], MN-major W4)
         GemmArgs<LoadDense, LoadDense, EpiMaskT> g{};
@@ -437,54 +558,63 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         PQ_CHECK((launch_bn<LoadDense, LoadDense, EpiMaskT, true, false>(choose_bn(n), g, 1, st)),
                  "fc1 dgrad");
     }
+    PQ_CHECK(cudaEventRecord(fk->ev[1], st), "fork1");
+    PQ_CHECK(cudaStreamWaitEvent(side, fk->ev[1], 0), "fork1 wait");
     {  // B3w: dW3^T[k][o] = sum_m P3[m][k] dY3[m][o]; row 576 = ones -> bias grad
         GemmArgs<LoadIm2col, LoadDense, EpiF32T> g{};
-        g.a[0] = LoadIm2col{w.act2[0], n, 9, 9, 64, 3, 1, 7, 7};
+        g.a[0] = im2col(w.act2[0], n, 9, 9, 64, 3, 1, 7, 7);
         g.b[0] = LoadDense{w.dY3, n * 49, 64, 64};
         g.e[0] = EpiF32T{w.part3, 577, 64, 577, (size_t)64 * 577};
         int nch = (n * 49 + 63) / 64;
         g.kc_per_split = choose_kc(nch, 5, &s3);
         g.M = 577, g.N = 64, g.K = n * 49, g.splits = s3, g.ones_at = 576, g.ones_extent = n * 49;
-        PQ_CHECK((launch_gemm<64, true, true>(g, 1, st)), "conv3 wgrad");
+        PQ_CHECK((launch_gemm<64, true, true>(g, 1, side)), "conv3 wgrad");
     }
     {  // B3d: dY2 = relu'(x2) * transposed conv3(dY3)
         GemmArgs<LoadTConv, LoadWeightT, EpiMask> g{};
-        g.a[0] = LoadTConv{w.dY3, n, 9, 9, 7, 7, 64, 3, 1};
-        g.b[0] = LoadWeightT{sh + S_W3, 64, 3, 64};
+        g.a[0] = tconv(w.dY3, n, 9, 9, 7, 7, 64, 3);
+        g.b[0] = weight_t(sh + S_W3, 64, 3, 64);
         g.e[0] = EpiMask{w.dY2, w.act2[0], n * 81, 64, 64};
         g.M = n * 81, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
         PQ_CHECK((launch_gemm<64, false, true>(g, 1, st)), "conv3 dgrad");
     }
+    PQ_CHECK(cudaEventRecord(fk->ev[2], st), "fork2");
+    PQ_CHECK(cudaStreamWaitEvent(side, fk->ev[2], 0), "fork2 wait");
     {  // B2w
         GemmArgs<LoadIm2col, LoadDense, EpiF32T> g{};
-        g.a[0] = LoadIm2col{w.act1[0], n, 20, 20, 32, 4, 2, 9, 9};
+        g.a[0] = im2col(w.act1[0], n, 20, 20, 32, 4, 2, 9, 9);
         g.b[0] = LoadDense{w.dY2, n * 81, 64, 64};
         g.e[0] = EpiF32T{w.part2, 513, 64, 513, (size_t)64 * 513};
         int nch = (n * 81 + 63) / 64;
         g.kc_per_split = choose_kc(nch, 5, &s2);
         g.M = 513, g.N = 64, g.K = n * 81, g.splits = s2, g.ones_at = 512, g.ones_extent = n * 81;
-        PQ_CHECK((launch_gemm<64, true, true>(g, 1, st)), "conv2 wgrad");
+        PQ_CHECK((launch_gemm<64, true, true>(g, 1, side)), "conv2 wgrad");
     }
-    {  // B2d: dY1 = relu'(x1) * transposed conv2(dY2)  (stride 2, K = 16 x 64)
-        GemmArgs<LoadTConv, LoadWeightT, EpiMask> g{};
-        g.a[0] = LoadTConv{w.dY2, n, 20, 20, 9, 9, 64, 4, 2};
-        g.b[0] = LoadWeightT{sh + S_W2, 64, 4, 32};
-        g.e[0] = EpiMask{w.dY1, w.act1[0], n * 400, 32, 32};
-        g.M = n * 400, g.N = 32, g.K = 1024, g.kc_per_split = 16, g.splits = 1, g.ones_at = -1;
+    {  // B2d: dY1 = relu'(x1) * transposed conv2(dY2), stride 2 split into the 4 input
+       // parity classes -> K = 4 taps x 64 per class instead of 16 x 64
+        const int tpc = (n * 100 + 127) / 128;
+        GemmArgs<LoadTConvP, LoadWeightTP, EpiMaskP> g{};
+        g.a[0] = tconv_p(w.dY2, n, 10, 10, 9, 9, 64, tpc);
+        g.b[0] = weight_tp(sh + S_W2, 64, 4, 32, tpc);
+        g.e[0] = epi_mask_p(w.dY1, w.act1[0], n, 10, 10, 32, tpc);
+        g.M = 4 * tpc * 128, g.N = 32, g.K = 256, g.kc_per_split = 4, g.splits = 1, g.ones_at = -1;
         PQ_CHECK((launch_gemm<64, false, true>(g, 1, st)), "conv2 dgrad");
     }
     {  // B1w: dW1^T[k][o] = sum_m P1[m][k] dY1[m][o] over uint8 frames; row 256 = ones
-        GemmArgs<LoadFramesC, LoadDense, EpiF32T> g{};
+        GemmArgs<LoadFrames, LoadDense, EpiF32T> g{};
         FwdInput in{la->ring, la->records, la->idx ? la->idx : la->idx_base,
                     la->idx ? nullptr : la->update_counter, n, REC_INTS, 0};
         g.a[0] = frames_loader(in, n);
         g.b[0] = LoadDense{w.dY1, n * 400, 32, 32};
         g.e[0] = EpiF32T{w.part1, 257, 32, 257, (size_t)32 * 257};
         int nch = (n * 400 + 63) / 64;
-        g.kc_per_split = choose_kc(nch, 3, &s1);
+        g.kc_per_split = choose_kc(nch, 3, &s1, (TABLE_SAMPLES - 2) * 400 / 64);
         g.M = 257, g.N = 32, g.K = n * 400, g.splits = s1, g.ones_at = 256, g.ones_extent = n * 400;
         PQ_CHECK((launch_gemm<64, true, true>(g, 1, st)), "conv1 wgrad");
     }
+    // join the weight-gradient branch
+    PQ_CHECK(cudaEventRecord(fk->ev[3], side), "join");
+    PQ_CHECK(cudaStreamWaitEvent(st, fk->ev[3], 0), "join wait");
     {
         OptArgs o{};
         o.p = th.master, o.m = la->opt.m, o.v = la->opt.v;
@@ -495,15 +625,12 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         o.dh1 = w.dh1, o.h1 = w.h1, o.td = w.td, o.act = w.act;
         o.n = n, o.A = la->actions;
         o.lr = la->lr, o.rho = la->rho, o.kappa = la->kappa;
-        o.flag = la->nonfinite, o.counter = la->update_counter, o.grad_out = la->grad_out;
+        o.flag = la->nonfinite, o.counter = la->update_counter, o.done = w.done;
+        o.grad_out = la->grad_out;
         o.total = n_params(la->actions);
-        int blocks = (int)((o.total + 255) / 256);
+        int blocks = (int)((o.total + 1023) / 1024);
         k_optimizer<<<blocks, 256, 0, st>>>(o);
         PQ_CHECK(cudaGetLastError(), "optimizer");
-        if (la->update_counter) {
-            k_bump<<<1, 1, 0, st>>>(la->update_counter);
-            PQ_CHECK(cudaGetLastError(), "counter");
-        }
     }
     return 0;
 }
@@ -530,11 +657,12 @@ __global__ void k_rmsprop(const float *p, const float *g, const float *m, const 
 
 // acting forward: F1..F4 over the W current stacks (refs [W][4]), fc1 partials out
 int act_forward(pq_net net, const uint8_t *ring, const int32_t *stack, int W, int A, void *ws,
-                int max_batch, const float **part_out, cudaStream_t st) {
+                int max_batch, const float **part_out, uint32_t **done_out, cudaStream_t st) {
     WS w = carve(ws, max_batch, A);
     FwdInput in{ring, stack, nullptr, nullptr, 0, 4, 0};
     int rc = forward_gemms(&net, &in, 1, W, w, st);
     *part_out = w.fc1part[0];
+    *done_out = w.done + 1;
     return rc;
 }
 

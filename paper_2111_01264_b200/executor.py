@@ -215,7 +215,7 @@ class DeviceRun:
         torch = self.torch
         cap = max(64, 1 << (int(n) - 1).bit_length())
         nbytes = N.load().pq_workspace_bytes(cap, self.hp.actions)
-        return torch.empty(nbytes, dtype=torch.uint8, device="cuda"), cap
+        return torch.zeros(nbytes, dtype=torch.uint8, device="cuda"), cap
 
     # -- raw step launchers (stream-ordered, graph-capturable) ----------------------------
     def _learn_args(self):

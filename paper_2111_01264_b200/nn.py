@@ -202,7 +202,7 @@ def workspace(max_batch: int, actions: int):
     key = (cap, actions, torch.cuda.current_device())
     if key not in _WS:
         nbytes = N.load().pq_workspace_bytes(cap, actions)
-        _WS[key] = (torch.empty(nbytes, dtype=torch.uint8, device="cuda"), cap)
+        _WS[key] = (torch.zeros(nbytes, dtype=torch.uint8, device="cuda"), cap)
     return _WS[key]
 
 
