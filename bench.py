@@ -318,6 +318,46 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     # kernel-level measurements (outside the timed region; same inputs)
     learn_ms = time_kernel_isolated(runner)
     gather_ms = time_gather(runner)
+    del runner
+    torch.cuda.empty_cache()
+    # end to end through the public API with host envs: H2D frames + D2H Q-rows per
+    # lockstep block, theta hash D2H per epoch (the paper's CPU-env / GPU setting)
+    from paper_2111_01264_b200.executor import HostEnvRun
+
+    erun = HostEnvRun(hp, use_graphs=True, graph_chunk=25)
+
+    def e_epoch(e):
+        erun.flush_and_merge()
+        copy_into(erun.target, erun.theta)
+        erun.run_epoch(e)
+        torch.cuda.synchronize()
+        erun.check_finite()
+        erun.record_epoch_hash((e + 1) * hp.C)
+
+    for e in range(args.warmup):
+        e_epoch(e)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    h2d0, d2h0 = erun.h2d_bytes, erun.d2h_bytes
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for e in range(args.warmup, total_epochs):
+        e_epoch(e)
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": world * args.steps * hp.C / (e2e_ms / 1000.0), "unit": UNIT,
+           "h2d_bytes_per_step": (erun.h2d_bytes - h2d0) // args.steps,
+           "d2h_bytes_per_step": (erun.d2h_bytes - d2h0) // args.steps,
+           "path": "executor.run(host_envs=True): CPU samplers (select_action + env.step in C), "
+                   "per lockstep block H2D stacks + new frames from pinned memory and D2H of the "
+                   "W Q-rows; per epoch H2D staging, D2H theta for the hash"}
+    del erun
     if dist:
         dist.destroy_process_group()
     if rank != 0:
@@ -364,7 +404,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "gpu_launches": per_epoch_launches * args.steps,
         "clocks": clk,
         "cpu_baseline": cpu,
-        "e2e": None,
+        "e2e": e2e,
     }
     print(json.dumps(line), flush=True)
 

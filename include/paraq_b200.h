@@ -169,6 +169,23 @@ typedef struct pq_act_args {
  * step, transition record into staging, episode bookkeeping and reset. */
 int pq_act_step(const pq_act_args *args, void *stream);
 
+/* ---- host-side samplers (end-to-end path: CPU envs, GPU inference) ---------------- */
+typedef struct pq_henv {
+    uint64_t pcg[6];   /* the sampler's PCG64 stream (shared by select_action and env.step) */
+    uint64_t key;      /* frame-hash key */
+    int64_t episode;
+    int32_t t, pad;
+    double ep_return;
+} pq_henv;
+
+int pq_henv_reset(pq_henv *envs, int W, int64_t *seq, int64_t frame_capacity, uint8_t *frames_out,
+                  int32_t *stacks);
+int pq_henv_step(pq_henv *envs, int W, const float *q, int A, int episode_length,
+                 double terminal_p, int64_t t_label0, double eps_start, double eps_end,
+                 int64_t eps_anneal, int64_t *seq, int64_t frame_capacity, uint8_t *frames_out,
+                 int *nframes, int32_t *stacks, int32_t *records, int64_t *ep_labels,
+                 double *ep_rets, int *n_eps);
+
 /* ---- elementwise kernels of the reference kernel module (fp32 / fp64) ------------- */
 int pq_rmsprop_f32(const float *p, const float *g, const float *m, const float *v, int64_t n,
                    float lr, float rho, float kappa, float *p2, float *m2, float *v2,

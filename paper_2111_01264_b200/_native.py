@@ -32,6 +32,11 @@ class PqEnvs(C.Structure):
                                   "slot_next", "ep_count", "ep_label", "ep_ret", "actions")]
 
 
+class PqHenv(C.Structure):
+    _fields_ = [("pcg", C.c_uint64 * 6), ("key", C.c_uint64), ("episode", C.c_int64),
+                ("t", C.c_int32), ("pad", C.c_int32), ("ep_return", C.c_double)]
+
+
 class PqLearnArgs(C.Structure):
     _fields_ = [
         ("theta", PqNet), ("opt", PqOpt), ("theta_out", PqNet), ("opt_out", PqOpt),
@@ -77,6 +82,9 @@ EXPORTS = {
     "pq_act_step": ([C.POINTER(PqActArgs), vp], C.c_int),
     "pq_rmsprop_f32": ([vp, vp, vp, vp, C.c_int64, C.c_float, C.c_float, C.c_float, vp, vp, vp,
                         vp, vp], C.c_int),
+    "pq_henv_reset": ([vp, C.c_int, vp, C.c_int64, vp, vp], C.c_int),
+    "pq_henv_step": ([vp, C.c_int, vp, C.c_int, C.c_int, C.c_double, C.c_int64, C.c_double,
+                      C.c_double, C.c_int64, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "pq_theta_hash_f32": ([vp, C.c_int64], C.c_uint64),
     "pq_theta_hash_f64": ([vp, C.c_int64], C.c_uint64),
 }

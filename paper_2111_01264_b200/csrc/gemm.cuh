@@ -309,20 +309,23 @@ struct EpiBiasRelu {
     int M, N, ld;
     float scale;
     PQ_DEV void apply(int m, int n0, const float *v, int cnt, int) const {
+        float bv[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) bv[e] = (e < cnt && n0 + e < N) ? __ldg(bias + n0 + e) : 0.f;
         if (m >= M) return;
         bf16 *dst = out + (size_t)m * ld;
-        for (int j = 0; j < cnt; j += 8) {
-            int n = n0 + j;
-            if (n >= N) break;
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+            const int n = n0 + j;
+            if (j >= cnt || n >= N) break;
             float y[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                float t = v[j + e] * scale + (n + e < N ? bias[n + e] : 0.f);
+                const float t = v[j + e] * scale + bv[j + e];
                 y[e] = t > 0.f ? t : 0.f;
             }
-            uint4 pk = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]),
-                                  pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
-            *reinterpret_cast<uint4 *>(dst + n) = pk;
+            *reinterpret_cast<uint4 *>(dst + n) = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]),
+                                                           pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
         }
     }
 };
@@ -360,18 +363,26 @@ struct EpiF32 {
     }
 };
 
-// masked bf16 store of 8 values at dst (mask = forward activation at the same place)
-PQ_DEV void store_masked8(bf16 *dst, const bf16 *mask, const float *v) {
-    uint4 mk = *reinterpret_cast<const uint4 *>(mask);
-    uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
-    float y[8];
+// masked bf16 store of up to 32 values (4 x 8) at dst; all mask loads are issued
+// before any store (mask = forward activation at the same place)
+PQ_DEV void store_masked32(bf16 *dst, const bf16 *mask, const float *v, int nvalid) {
+    uint4 mk[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        y[2 * e] = bf16_lo(mw[e]) > 0.f ? v[2 * e] : 0.f;
-        y[2 * e + 1] = bf16_hi(mw[e]) > 0.f ? v[2 * e + 1] : 0.f;
+    for (int c = 0; c < 4; ++c)
+        mk[c] = c * 8 < nvalid ? __ldg(reinterpret_cast<const uint4 *>(mask + c * 8)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        if (c * 8 >= nvalid) break;
+        const uint32_t mw[4] = {mk[c].x, mk[c].y, mk[c].z, mk[c].w};
+        float y[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            y[2 * e] = bf16_lo(mw[e]) > 0.f ? v[c * 8 + 2 * e] : 0.f;
+            y[2 * e + 1] = bf16_hi(mw[e]) > 0.f ? v[c * 8 + 2 * e + 1] : 0.f;
+        }
+        *reinterpret_cast<uint4 *>(dst + c * 8) = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]),
+                                                           pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
     }
-    *reinterpret_cast<uint4 *>(dst) = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]),
-                                                 pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7]));
 }
 
 // data gradient: bf16 out[m][n] = acc * (mask[m][n] > 0), mask = forward activation
@@ -380,12 +391,9 @@ struct EpiMask {
     const bf16 *mask;
     int M, N, ld;
     PQ_DEV void apply(int m, int n0, const float *v, int cnt, int) const {
-        if (m >= M) return;
-        for (int j = 0; j < cnt; j += 8) {
-            int n = n0 + j;
-            if (n >= N) break;
-            store_masked8(out + (size_t)m * ld + n, mask + (size_t)m * ld + n, v + j);
-        }
+        if (m >= M || n0 >= N) return;
+        const int nv = min(cnt, N - n0);
+        store_masked32(out + (size_t)m * ld + n0, mask + (size_t)m * ld + n0, v, nv);
     }
 };
 
@@ -398,16 +406,12 @@ struct EpiMaskP {
     PQ_DEV void apply(int m, int n0, const float *v, int cnt, int) const {
         int cls = f_per.div(m), loc = m - cls * tpc * 128;
         int npix = H2 * W2;
-        if (loc >= n * npix) return;
+        if (loc >= n * npix || n0 >= C) return;
         int b = f_npix.div(loc), rem = loc - b * npix;
         int ry = f_w2.div(rem);
         int iy = 2 * ry + (cls >> 1), ix = 2 * (rem - ry * W2) + (cls & 1);
-        size_t o = ((size_t)(b * 2 * H2 + iy) * (2 * W2) + ix) * C;
-        for (int j = 0; j < cnt; j += 8) {
-            int c = n0 + j;
-            if (c >= C) break;
-            store_masked8(out + o + c, mask + o + c, v + j);
-        }
+        size_t o = ((size_t)(b * 2 * H2 + iy) * (2 * W2) + ix) * C + n0;
+        store_masked32(out + o, mask + o, v, min(cnt, C - n0));
     }
 };
 
@@ -418,14 +422,89 @@ struct EpiMaskT {
     int M, N, ld;
     PQ_DEV void apply(int m, int n0, const float *v, int cnt, int) const {
         if (m >= M) return;
-        for (int j = 0; j < cnt; ++j) {
-            int n = n0 + j;
-            if (n >= N) break;
-            size_t o = (size_t)n * ld + m;
-            float mk = __bfloat162float(mask[o]);
-            out[o] = __float2bfloat16_rn(mk > 0.f ? v[j] : 0.f);
+        bf16 mk[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            mk[j] = (j < cnt && n0 + j < N) ? mask[(size_t)(n0 + j) * ld + m] : __float2bfloat16_rn(0.f);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (j >= cnt || n0 + j >= N) break;
+            out[(size_t)(n0 + j) * ld + m] = __float2bfloat16_rn(__bfloat162float(mk[j]) > 0.f ? v[j] : 0.f);
         }
     }
+};
+
+// fc1 weight gradient fused with its centered RMSProp update (the contraction over the
+// batch is complete in one CTA): D[j][k] = dW4[j][k]; parameter i = base + j*N + k.
+// STAGED: the kernel parks the fp32 accumulator tile in shared memory so the update
+// walks rows with lanes over consecutive parameters (coalesced p / m / v traffic).
+struct EpiRms {
+    static constexpr bool STAGED = true;
+    const float *p, *m, *v;
+    float *p2, *m2, *v2;
+    bf16 *shadow;
+    float *grad_out;
+    int32_t *flag;
+    const int32_t *counter;
+    float lr, rho, kappa;
+    int M, N;
+    int64_t pbase, sbase;
+    PQ_DEV void apply(int, int, const float *, int, int) const {}
+    // tile: [128][ld] fp32, rows m0.., cols n0.. (width BN); 256 threads
+    template <int BN>
+    PQ_DEV void apply_tile(const float *tile, int ld, int m0, int n0) const {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        bool bad = false;
+        for (int r0 = warp; r0 < 128; r0 += 32) {
+            float gg[4][BN / 32], mm[4][BN / 32], vv[4][BN / 32], pp[4][BN / 32];
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                const int r = r0 + rr * 8;
+                const bool rok = m0 + r < M;
+#pragma unroll
+                for (int u = 0; u < BN / 32; ++u) {
+                    const int col = lane + 32 * u;
+                    const bool ok = rok && n0 + col < N;
+                    const int64_t i = pbase + (int64_t)(m0 + r) * N + n0 + col;
+                    gg[rr][u] = tile[r * ld + col];
+                    mm[rr][u] = ok ? m[i] : 0.f;
+                    vv[rr][u] = ok ? v[i] : 0.f;
+                    pp[rr][u] = ok ? p[i] : 0.f;
+                }
+            }
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                const int r = r0 + rr * 8;
+                if (m0 + r >= M) continue;
+#pragma unroll
+                for (int u = 0; u < BN / 32; ++u) {
+                    const int col = lane + 32 * u;
+                    if (n0 + col >= N) continue;
+                    const int64_t off = (int64_t)(m0 + r) * N + n0 + col;
+                    const float g = gg[rr][u];
+                    bad |= !isfinite(g);
+                    const float mi = rho * mm[rr][u] + (1.0f - rho) * g;
+                    const float vi = rho * vv[rr][u] + (1.0f - rho) * g * g;
+                    const float pi = pp[rr][u] - lr * g / sqrtf(vi - mi * mi + kappa);
+                    m2[pbase + off] = mi;
+                    v2[pbase + off] = vi;
+                    p2[pbase + off] = pi;
+                    shadow[sbase + off] = __float2bfloat16_rn(pi);
+                    if (grad_out) grad_out[pbase + off] = g;
+                }
+            }
+        }
+        if (bad) atomicMin(flag, counter ? *counter : 0);
+    }
+};
+
+template <class EP, class = void>
+struct is_staged {
+    static constexpr bool value = false;
+};
+template <class EP>
+struct is_staged<EP, decltype((void)EP::STAGED)> {
+    static constexpr bool value = EP::STAGED;
 };
 
 // ------------------------------------------------------------------------ kernel
@@ -445,23 +524,25 @@ constexpr int GEMM_THREADS = 256;
 constexpr int GEMM_A_BYTES = 128 * 64 * 2;
 constexpr int TABLE_SAMPLES = 64;
 
-template <int BN, bool U8A>
+template <int BN, bool U8A, int ST = 0>
 struct GemmCfg {
     static constexpr int B_BYTES = BN * 128;
     static constexpr int U8_BYTES = U8A ? 128 * 64 : 0;  // raw uint8 staging of the A tile
     static constexpr int STAGE = GEMM_A_BYTES + B_BYTES + U8_BYTES;
-    static constexpr int STAGES = (200 * 1024 / STAGE) < 6 ? (200 * 1024 / STAGE) : 6;
+    static constexpr int AUTO = (200 * 1024 / STAGE) < 6 ? (200 * 1024 / STAGE) : 6;
+    static constexpr int STAGES = ST > 0 ? ST : AUTO;
     static constexpr int SMEM = STAGES * STAGE + 1024;
 };
 
-template <int BN, bool AMN, bool BMN, class LA, class LB, class EP>
+template <int BN, bool AMN, bool BMN, int ST, class LA, class LB, class EP>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm(const __grid_constant__ GemmArgs<LA, LB, EP> g) {
     static_assert(BN == 16 || BN == 32 || BN == 64 || BN == 128 || BN == 256, "BN");
     static_assert(!BMN || BN >= 64, "MN-major B needs 64-wide swizzle atoms");
     static_assert(!LB::TABLE, "frame tables are A-operand only");
-    using Cfg = GemmCfg<BN, LA::U8>;
+    using Cfg = GemmCfg<BN, LA::U8, ST>;
     constexpr int STAGES = Cfg::STAGES;
+    static_assert(STAGES >= 2, "stages");
     constexpr int PRE = STAGES - 1;
     constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
     constexpr uint32_t IDESC = idesc_bf16(BN, AMN, BMN);
@@ -636,7 +717,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int row = m0 + wq * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
     constexpr int CW = BN >= 64 ? BN / 2 : BN;  // columns per warpgroup
-    if (BN >= 64 || half == 0) {
+    if constexpr (is_staged<EP>::value) {
+        // park the accumulator tile in the (now idle) operand ring, then let the
+        // epilogue walk it row-wise; row stride BN+1 keeps both passes conflict-free
+        static_assert(128 * (BN + 1) * 4 <= Cfg::STAGES * Cfg::STAGE, "staging tile");
+        float *tile = reinterpret_cast<float *>(smem);
+        if (BN >= 64 || half == 0) {
+            const int cbeg = BN >= 64 ? half * CW : 0;
+            for (int c0 = cbeg; c0 < cbeg + CW; c0 += 32) {
+                float v[32];
+                if (nk > 0) {
+                    tmem_ld32(trow + c0, v);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
+                }
+#pragma unroll
+                for (int e = 0; e < 32; ++e) tile[(wq * 32 + lane) * (BN + 1) + c0 + e] = v[e];
+            }
+        }
+        __syncthreads();
+        ep.template apply_tile<BN>(tile, BN + 1, m0, n0);
+    } else if (BN >= 64 || half == 0) {
         const int cbeg = BN >= 64 ? half * CW : 0;
 #pragma unroll 1
         for (int c0 = cbeg; c0 < cbeg + CW; c0 += 32) {
@@ -658,10 +760,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (warp == 0) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
-template <int BN, bool AMN, bool BMN, class LA, class LB, class EP>
+template <int BN, bool AMN, bool BMN, int ST = 0, class LA, class LB, class EP>
 cudaError_t launch_gemm(const GemmArgs<LA, LB, EP> &g, int groups, cudaStream_t st, int grid_x = 0) {
-    auto kern = k_gemm<BN, AMN, BMN, LA, LB, EP>;
-    constexpr int smem = GemmCfg<BN, LA::U8>::SMEM;
+    auto kern = k_gemm<BN, AMN, BMN, ST, LA, LB, EP>;
+    constexpr int smem = GemmCfg<BN, LA::U8, ST>::SMEM;
     static bool configured = false;  // per instantiation
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

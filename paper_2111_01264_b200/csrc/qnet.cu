@@ -169,7 +169,7 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
             g.e[q] = EpiBiasRelu{w.act1[q], nets[q].master + P_B1, n * 400, 32, 32, 1.0f / 255.0f};
         }
         g.M = n * 400, g.N = 32, g.K = 256, g.kc_per_split = 4, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<32, false, false>(g, groups, st)), "conv1 forward");
+        PQ_CHECK((launch_gemm<32, false, false, 3>(g, groups, st)), "conv1 forward");
     }
     {  // F2: conv2 4x4/2 over 20x20x32 (K = 512)
         GemmArgs<LoadIm2col, LoadDense, EpiBiasRelu> g{};
@@ -389,8 +389,15 @@ struct OptArgs {
 };
 
 __device__ __forceinline__ float sum_part(const float *part, int splits, size_t stride, size_t off) {
+    // up to 32 independent loads in flight per round; fixed (split-ascending) add order
     float s = 0.f;
-    for (int q = 0; q < splits; ++q) s += part[q * stride + off];
+    for (int q = 0; q < splits; q += 32) {
+        float v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) v[u] = q + u < splits ? part[(q + u) * stride + off] : 0.f;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) s += v[u];
+    }
     return s;
 }
 
@@ -408,6 +415,20 @@ __device__ __forceinline__ void last_block_bump(int32_t *counter, uint32_t *done
         *done = 0;
         __threadfence();
     }
+}
+
+// sum over the batch of f(b) with 8 samples' loads in flight (fixed add order)
+template <class F>
+__device__ __forceinline__ float batch_sum(int n, F f) {
+    float s = 0.f;
+    for (int b0 = 0; b0 < n; b0 += 16) {
+        float v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = b0 + u < n ? f(b0 + u) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) s += v[u];
+    }
+    return s;
 }
 
 __device__ __forceinline__ float grad_of(const OptArgs &a, int64_t i, int64_t &sh) {
@@ -434,21 +455,20 @@ __device__ __forceinline__ float grad_of(const OptArgs &a, int64_t i, int64_t &s
         sh = S_W4 + (i - P_W4);
         return a.grad4[i - P_W4];
     }
-    float g = 0.f;
     if (i < P_W5) {
-        int j = (int)(i - P_B4);
-        for (int b = 0; b < a.n; ++b) g += a.dh1[(size_t)b * 512 + j];
-    } else if (i < p_b5(a.A)) {
-        int64_t r = i - P_W5;
-        int aa = (int)(r >> 9), j = (int)(r & 511);
-        for (int b = 0; b < a.n; ++b)
-            if (a.act[b] == aa) g += a.td[b * 3 + 1] * a.h1[(size_t)b * 512 + j];
-    } else {
-        int aa = (int)(i - p_b5(a.A));
-        for (int b = 0; b < a.n; ++b)
-            if (a.act[b] == aa) g += a.td[b * 3 + 1];
+        const int j = (int)(i - P_B4);
+        return batch_sum(a.n, [&](int b) { return a.dh1[(size_t)b * 512 + j]; });
     }
-    return g;
+    if (i < p_b5(a.A)) {
+        const int64_t r = i - P_W5;
+        const int aa = (int)(r >> 9), j = (int)(r & 511);
+        return batch_sum(a.n, [&](int b) {
+            const float x = a.td[b * 3 + 1] * a.h1[(size_t)b * 512 + j];
+            return a.act[b] == aa ? x : 0.f;
+        });
+    }
+    const int aa = (int)(i - p_b5(a.A));
+    return batch_sum(a.n, [&](int b) { return a.act[b] == aa ? a.td[b * 3 + 1] : 0.f; });
 }
 
 // centered RMSProp, kappa inside the square root (_kernels_numba.py:98-111)
@@ -459,45 +479,25 @@ __device__ __forceinline__ void rms(const OptArgs &a, float g, float m, float v,
     p2 = p - a.lr * g / sqrtf(v2 - m2 * m2 + a.kappa);
 }
 
+// every parameter except fc1's weight (updated in the fc1 wgrad epilogue unless
+// a.grad4 is given), one parameter per thread
 __global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
-    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-    const int upd = a.counter ? *a.counter : 0;
-    bool bad = false;
-    if (i0 >= P_W4 && i0 + 4 <= P_B4) {  // fc1 weight: 16-byte vector path
-        const int64_t r = i0 - P_W4;
-        const float4 g = *reinterpret_cast<const float4 *>(a.grad4 + r);
-        const float4 m = *reinterpret_cast<const float4 *>(a.m + i0);
-        const float4 v = *reinterpret_cast<const float4 *>(a.v + i0);
-        const float4 p = *reinterpret_cast<const float4 *>(a.p + i0);
-        float4 m2, v2, p2;
-        rms(a, g.x, m.x, v.x, p.x, m2.x, v2.x, p2.x);
-        rms(a, g.y, m.y, v.y, p.y, m2.y, v2.y, p2.y);
-        rms(a, g.z, m.z, v.z, p.z, m2.z, v2.z, p2.z);
-        rms(a, g.w, m.w, v.w, p.w, m2.w, v2.w, p2.w);
-        *reinterpret_cast<float4 *>(a.m2 + i0) = m2;
-        *reinterpret_cast<float4 *>(a.v2 + i0) = v2;
-        *reinterpret_cast<float4 *>(a.p2 + i0) = p2;
-        *reinterpret_cast<uint2 *>(a.shadow + S_W4 + r) =
-            make_uint2(pack_bf16(p2.x, p2.y), pack_bf16(p2.z, p2.w));
-        if (a.grad_out) *reinterpret_cast<float4 *>(a.grad_out + i0) = g;
-        bad = !(isfinite(g.x) && isfinite(g.y) && isfinite(g.z) && isfinite(g.w));
-    } else {
-        for (int e = 0; e < 4; ++e) {
-            const int64_t i = i0 + e;
-            if (i >= a.total) break;
-            int64_t sh;
-            const float g = grad_of(a, i, sh);
-            float m2, v2, p2;
-            rms(a, g, a.m[i], a.v[i], a.p[i], m2, v2, p2);
-            a.m2[i] = m2;
-            a.v2[i] = v2;
-            a.p2[i] = p2;
-            if (sh >= 0) a.shadow[sh] = __float2bfloat16_rn(p2);
-            if (a.grad_out) a.grad_out[i] = g;
-            bad |= !isfinite(g);
-        }
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = a.grad4 ? t : (t < P_W4 ? t : P_B4 + (t - P_W4));
+    if (i < a.total) {
+        const int upd = a.counter ? *a.counter : 0;
+        const float m = a.m[i], v = a.v[i], p = a.p[i];
+        int64_t sh;
+        const float g = grad_of(a, i, sh);
+        float m2, v2, p2;
+        rms(a, g, m, v, p, m2, v2, p2);
+        a.m2[i] = m2;
+        a.v2[i] = v2;
+        a.p2[i] = p2;
+        if (sh >= 0) a.shadow[sh] = __float2bfloat16_rn(p2);
+        if (a.grad_out) a.grad_out[i] = g;
+        if (!isfinite(g)) atomicMin(a.flag, upd);
     }
-    if (bad) atomicMin(a.flag, upd);
     if (a.counter) last_block_bump(a.counter, a.done);
 }
 
@@ -538,17 +538,6 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     Fork *fk = nullptr;
     if (int rc = get_fork(&fk)) return rc;
     cudaStream_t side = fk->side;
-    // fork: fc1 wgrad needs only the head outputs
-    PQ_CHECK(cudaEventRecord(fk->ev[0], st), "fork0");
-    PQ_CHECK(cudaStreamWaitEvent(side, fk->ev[0], 0), "fork0 wait");
-    {  // B4w: dW4[j][k] = sum_b dh1[b][j] x3[b][k]  (contraction over the batch)
-        GemmArgs<LoadDense, LoadDense, EpiF32> g{};
-        g.a[0] = LoadDense{w.dh1T, 512, n, w.n8};
-        g.b[0] = LoadDense{w.act3[0], n, 3136, 3136};
-        g.e[0] = EpiF32{w.grad4, 512, 3136, 3136, 0};
-        g.M = 512, g.N = 3136, g.K = n, g.kc_per_split = (n + 63) / 64, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<64, false, true>(g, 1, side)), "fc1 wgrad");
-    }
     {  // B4d: dY3[b][k] = relu'(x3) * sum_j W4[j][k] dh1[b][j]   (D[k][b], MN-major W4)
         GemmArgs<LoadDense, LoadDense, EpiMaskT> g{};
         g.a[0] = LoadDense{sh + S_W4, 512, 3136, 3136};
@@ -558,8 +547,26 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         PQ_CHECK((launch_bn<LoadDense, LoadDense, EpiMaskT, true, false>(choose_bn(n), g, 1, st)),
                  "fc1 dgrad");
     }
+    // fork after the fc1 data gradient: the fused fc1 update below rewrites the W4
+    // shadow that B4d reads, so it must not start earlier
     PQ_CHECK(cudaEventRecord(fk->ev[1], st), "fork1");
     PQ_CHECK(cudaStreamWaitEvent(side, fk->ev[1], 0), "fork1 wait");
+    {  // B4w + RMSProp: dW4[j][k] = sum_b dh1[b][j] x3[b][k] (contraction over the batch),
+       // centered RMSProp applied in the epilogue (no fp32 gradient round trip)
+        GemmArgs<LoadDense, LoadDense, EpiRms> g{};
+        g.a[0] = LoadDense{w.dh1T, 512, n, w.n8};
+        g.b[0] = LoadDense{w.act3[0], n, 3136, 3136};
+        EpiRms e{};
+        e.p = th.master, e.m = la->opt.m, e.v = la->opt.v;
+        e.p2 = la->theta_out.master, e.m2 = la->opt_out.m, e.v2 = la->opt_out.v;
+        e.shadow = (bf16 *)la->theta_out.shadow;
+        e.grad_out = la->grad_out, e.flag = la->nonfinite, e.counter = la->update_counter;
+        e.lr = la->lr, e.rho = la->rho, e.kappa = la->kappa;
+        e.M = 512, e.N = 3136, e.pbase = P_W4, e.sbase = S_W4;
+        g.e[0] = e;
+        g.M = 512, g.N = 3136, g.K = n, g.kc_per_split = (n + 63) / 64, g.splits = 1, g.ones_at = -1;
+        PQ_CHECK((launch_gemm<128, false, true, 4>(g, 1, side)), "fc1 wgrad+rmsprop");
+    }
     {  // B3w: dW3^T[k][o] = sum_m P3[m][k] dY3[m][o]; row 576 = ones -> bias grad
         GemmArgs<LoadIm2col, LoadDense, EpiF32T> g{};
         g.a[0] = im2col(w.act2[0], n, 9, 9, 64, 3, 1, 7, 7);
@@ -620,7 +627,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         o.p = th.master, o.m = la->opt.m, o.v = la->opt.v;
         o.p2 = la->theta_out.master, o.m2 = la->opt_out.m, o.v2 = la->opt_out.v;
         o.shadow = (bf16 *)la->theta_out.shadow;
-        o.part1 = w.part1, o.part2 = w.part2, o.part3 = w.part3, o.grad4 = w.grad4;
+        o.part1 = w.part1, o.part2 = w.part2, o.part3 = w.part3, o.grad4 = nullptr;
         o.s1 = s1, o.s2 = s2, o.s3 = s3;
         o.dh1 = w.dh1, o.h1 = w.h1, o.td = w.td, o.act = w.act;
         o.n = n, o.A = la->actions;
@@ -628,8 +635,8 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         o.flag = la->nonfinite, o.counter = la->update_counter, o.done = w.done;
         o.grad_out = la->grad_out;
         o.total = n_params(la->actions);
-        int blocks = (int)((o.total + 1023) / 1024);
-        k_optimizer<<<blocks, 256, 0, st>>>(o);
+        const int64_t cnt = P_W4 + (o.total - P_B4);
+        k_optimizer<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(o);
         PQ_CHECK(cudaGetLastError(), "optimizer");
     }
     return 0;

@@ -418,6 +418,141 @@ class DeviceRun:
         self.record.duration_s = time.perf_counter() - wall0
 
 
-def run(hp: HyperParams, sink=None, **kw) -> RunRecord:
-    """Execute the full training run described by hp on the GPU (executor.py:591-593)."""
-    return DeviceRun(hp, sink, **kw).execute()
+def run(hp: HyperParams, sink=None, host_envs: bool = False, **kw) -> RunRecord:
+    """Execute the full training run described by hp on the GPU (executor.py:591-593).
+    host_envs=True keeps the samplers' envs on the CPU (end-to-end path)."""
+    cls = HostEnvRun if host_envs else DeviceRun
+    return cls(hp, sink, **kw).execute()
+
+
+class HostEnvRun(DeviceRun):
+    """End-to-end variant: the W samplers' envs and epsilon-greedy live on the host (the
+    reference's CPU sampler threads), the GPU serves batched Q-rows (InferenceWorker)
+    and trains concurrently.  Every lockstep block: H2D of the current stacks' frame
+    table, one batched forward on theta-minus, D2H of the W Q-rows, host select_action +
+    env.step (csrc/host_env.cpp), H2D of the new frames into their ring slots.  The
+    learner's graphs are enqueued for the whole epoch first and run concurrently."""
+
+    def __init__(self, hp: HyperParams, sink=None, **kw):
+        super().__init__(hp, sink, **kw)
+        torch = self.torch
+        W = hp.W
+        lib = N.load()
+        self.henv = (N.PqHenv * W)()
+        for j in range(W):
+            st = self.envs.pcg_states()[j]
+            for k in range(6):
+                self.henv[j].pcg[k] = int(st[k])
+            self.henv[j].key = int(self.envs.key[j].item()) & ((1 << 64) - 1)
+            self.henv[j].episode = -1
+        pin = dict(pin_memory=True)
+        self.h_frames = torch.empty((2 * W, 7056), dtype=torch.uint8, **pin)
+        self.h_stacks = torch.empty((W, 4), dtype=torch.int32, **pin)
+        self.h_q = torch.empty((W, hp.actions), dtype=torch.float32, **pin)
+        self.h_staging = torch.empty((W, self.steps, REC_INTS), dtype=torch.int32, **pin)
+        self.h_rec = torch.empty((W, REC_INTS), dtype=torch.int32, **pin)
+        self.d_stacks = torch.empty((W, 4), dtype=torch.int32, device="cuda")
+        self.d_q = torch.empty((W, hp.actions), dtype=torch.float32, device="cuda")
+        self.ep_labels = np.zeros(2 * W, dtype=np.int64)
+        self.ep_rets = np.zeros(2 * W, dtype=np.float64)
+        self.host_episodes = [[] for _ in range(W)]
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+        # initial resets (the device env state built by DeviceRun is not used)
+        seq = np.array([self.D._reserve_frames(W)], dtype=np.int64)
+        lib.pq_henv_reset(N.C.addressof(self.henv), W, seq.ctypes.data, self.D.frame_capacity,
+                          self.h_frames.data_ptr(), self.h_stacks.data_ptr())
+        self._h2d_frames(int(seq[0]) - W, W)
+        torch.cuda.synchronize()
+
+    def _h2d_frames(self, first_seq: int, count: int, stream=None):
+        """Copy count new frames (consecutive sequence numbers) into their ring slots."""
+        fc = self.D.frame_capacity
+        s0 = first_seq % fc
+        n1 = min(count, fc - s0)
+        self.D.ring[s0:s0 + n1].copy_(self.h_frames[:n1], non_blocking=True)
+        if n1 < count:
+            self.D.ring[:count - n1].copy_(self.h_frames[n1:count], non_blocking=True)
+        self.h2d_bytes += count * 7056
+
+    def run_epoch(self, epoch: int):
+        hp = self.hp
+        torch = self.torch
+        lib = N.load()
+        self.begin_epoch(epoch)
+        if self.use_graphs and self._graphs is None:
+            self._graphs = self._capture()
+        cur = torch.cuda.current_stream()
+        self.act_stream.wait_stream(cur)
+        self.learn_stream.wait_stream(cur)
+        # the learner's whole epoch is enqueued first
+        if self.use_graphs:
+            gl, nl = self._graphs["learn"]
+            with torch.cuda.stream(self.learn_stream):
+                for _ in range(self.updates // nl):
+                    gl.replay()
+        else:
+            with torch.cuda.stream(self.learn_stream):
+                for _ in range(self.updates):
+                    self.learn_step()
+        seq = np.array([self.epoch_bases[-1]], dtype=np.int64)
+        nf = np.zeros(1, dtype=np.int32)
+        neps = np.zeros(1, dtype=np.int32)
+        s = hp.schedule
+        net = self.target.struct()
+        ws, cap = self.act_ws.data_ptr(), self.act_cap
+        with torch.cuda.stream(self.act_stream):
+            st = N.stream_ptr()
+            for b in range(self.steps):
+                self.d_stacks.copy_(self.h_stacks, non_blocking=True)
+                self.h2d_bytes += self.h_stacks.numel() * 4
+                N.check(lib.pq_forward(net, self.D.ring.data_ptr(), self.d_stacks.data_ptr(), None, 4,
+                                       0, hp.W, hp.actions, self.d_q.data_ptr(), ws, cap, st),
+                        "forward")
+                self.h_q.copy_(self.d_q, non_blocking=True)
+                self.d2h_bytes += self.h_q.numel() * 4
+                self.act_stream.synchronize()
+                t_label0 = epoch * hp.C + b * hp.W + 1
+                first = int(seq[0])
+                neps[0] = 0
+                lib.pq_henv_step(N.C.addressof(self.henv), hp.W, self.h_q.data_ptr(), hp.actions,
+                                 hp.episode_length, hp.terminal_p, t_label0, s.start, s.end,
+                                 s.anneal_steps, seq.ctypes.data, self.D.frame_capacity,
+                                 self.h_frames.data_ptr(), nf.ctypes.data, self.h_stacks.data_ptr(),
+                                 self.h_rec.data_ptr(), self.ep_labels.ctypes.data,
+                                 self.ep_rets.ctypes.data, neps.ctypes.data)
+                self.h_staging[:, b].copy_(self.h_rec)
+                for k in range(int(neps[0])):
+                    lab = int(self.ep_labels[k])
+                    self.host_episodes[lab - t_label0].append((lab, float(self.ep_rets[k])))
+                self._h2d_frames(first, int(nf[0]))
+            self.staging.copy_(self.h_staging, non_blocking=True)
+            self.h2d_bytes += self.h_staging.numel() * 4
+        cur.wait_stream(self.act_stream)
+        cur.wait_stream(self.learn_stream)
+        self.staged = True
+        self.worker.count_predict(hp.W, True, self.steps)
+        self.worker.train_calls += self.updates
+        self.counters["dfreeze_checks"] += self.updates
+
+    def flush_and_merge(self):
+        hp = self.hp
+        if not self.staged:
+            return
+        lib = N.load()
+        tmp = self.torch.empty((hp.C, REC_INTS), dtype=self.torch.int32, device="cuda")
+        N.check(lib.pq_replay_flush(self.staging.data_ptr(), hp.W, self.steps, tmp.data_ptr(),
+                                    hp.C, 0, N.stream_ptr()), "flush")
+        base = self.epoch_bases[max(0, len(self.epoch_bases) - 1 - self.lag)]
+        self.D.push_device_records(tmp, hp.C, base)
+        self.counters["flush_pushes"] += hp.C
+        for j in range(hp.W):
+            for lab, ret in self.host_episodes[j]:
+                self.record.episodes.append((lab, ret))
+                self.emit(lab, "episode", repr(ret))
+            self.host_episodes[j] = []
+        self.staged = False
+
+    def record_epoch_hash(self, boundary: int):
+        super().record_epoch_hash(boundary)
+        self.d2h_bytes += self.theta.master.numel() * 4

@@ -11,3 +11,8 @@ timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -s 3000 -c
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 1 --warmup 0 --prefill 50000 \
   --capacity 100000 --no-cpu-baseline > gpurun_out/ncu_$TAG.log 2>&1
 python profiles/summarize_launches.py gpurun_out/launches_$TAG.csv
+if [ -n "$PROFILE_FULL" ]; then
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_gemm|k_optimizer|k_head" \
+    -s 60 -c 14 -o gpurun_out/full_$TAG python profiles/one_step.py > gpurun_out/ncufull_$TAG.log 2>&1
+  tail -1 gpurun_out/ncufull_$TAG.log
+fi

@@ -141,7 +141,7 @@ def test_learner_step_stagewise(B):
     ref = ((dh1_bf @ S["W4"]).view(B, 7, 7, 64)) * (act3 > 0)
     assert rel(dY3, ref) < 2e-3, "fc1 dgrad"
     # fc1 weight gradient (contraction over the batch)
-    g4 = view(ws, L["grad4"], (512, 3136), torch.float32)
+    g4 = grad[77984:1683616].view(512, 3136)   # fused fc1 wgrad + RMSProp epilogue
     assert rel(g4, dh1_bf.T @ act3.reshape(B, 3136)) < 1e-4, "fc1 wgrad"
     # conv3 wgrad (+ bias row) and dgrad
     x2 = act2.permute(0, 3, 1, 2)

@@ -293,3 +293,14 @@ def test_run_is_deterministic_and_counts_transactions():
     assert c["train_calls"] == 128 // 4
     assert c["flush_pushes"] == 128 and c["dfreeze_violations"] == 0
     assert any(kind == "episode" for _, kind, _ in r1.events)
+
+
+def test_host_env_run_matches_device_env_run():
+    """End-to-end path (CPU envs + select_action, H2D frames / D2H Q-rows per block)
+    reproduces the all-device executor bit-exactly."""
+    hp = HyperParams(C=64, F=4, N=200, W=8, batch_size=32, total_steps=128, capacity=2000,
+                     schedule=EpsilonSchedule(1.0, 0.1, 100), episode_length=7, seed=5)
+    r_dev = run(hp, graph_chunk=8)
+    r_host = run(hp, host_envs=True, graph_chunk=8)
+    assert r_dev.epoch_hashes == r_host.epoch_hashes
+    assert r_dev.to_csv_text() == r_host.to_csv_text()
