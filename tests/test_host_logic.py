@@ -1,0 +1,133 @@
+"""Host-side logic of the package (no GPU): configuration validation, the epsilon
+schedule and select_action discipline, parameter files, run-record format, and the
+multi-process plumbing (gloo, world_size 2)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_2111_01264_b200 import dist as pdist
+from paper_2111_01264_b200.agent import EpsilonSchedule, HyperParams, epsilon_at, select_action
+from paper_2111_01264_b200.executor import RunRecord, transaction_count
+from paper_2111_01264_b200.nn import Parameters, layer_shapes, load_parameters, num_params, \
+    save_parameters, theta_hash
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_select_action_matches_reference_golden():
+    """agent.py:53-66 draw discipline, against the reference's recorded sequence."""
+    g = np.load(os.path.join(GOLD, "pcg64.npz"))
+    from paper_2111_01264_b200.replay import pcg_state_to_generator, pcg_state_from_generator
+
+    rng = np.random.default_rng(0)
+    pcg_state_to_generator(g["sel_s0"], rng)
+    acts = [select_action(g["sel_q"][i], float(g["sel_eps"][i]), rng) for i in range(500)]
+    assert np.array_equal(acts, g["sel_out"])
+    assert np.array_equal(pcg_state_from_generator(rng), g["sel_s1"])
+
+
+def test_epsilon_schedule():
+    """pkg/tests/test_agent.py epsilon cases."""
+    s = EpsilonSchedule(1.0, 0.1, 10)
+    assert epsilon_at(1, s) == 1.0
+    assert epsilon_at(10, s) == 0.1 and epsilon_at(1000, s) == 0.1
+    assert abs(epsilon_at(5, s) - (1.0 + (0.1 - 1.0) * 4 / 9)) < 1e-15
+    with pytest.raises(ValueError):
+        epsilon_at(0, s)
+    assert epsilon_at(3, EpsilonSchedule(0.5, 0.5, 1)) == 0.5
+
+
+@pytest.mark.parametrize("kw", [dict(C=10, F=3), dict(C=10, W=3), dict(W=1),
+                                dict(N=11, capacity=10), dict(total_steps=15, C=10),
+                                dict(gamma=1.5), dict(actions=40), dict(batch_size=0)])
+def test_hyperparams_validate_rejects(kw):
+    base = dict(C=10, F=2, W=2, N=5, capacity=10, total_steps=20)
+    base.update(kw)
+    with pytest.raises(ValueError):
+        HyperParams(**base).validate()
+
+
+def test_hyperparams_modes_and_transactions():
+    hp = HyperParams(C=40, F=4, W=4, total_steps=200, N=10, capacity=100)
+    assert hp.mode == "both"
+    assert hp.with_mode("concurrent").mode == "concurrent"
+    assert transaction_count(hp, 200) == 200 // 4 + 200 // 4
+    assert transaction_count(hp.with_mode("concurrent"), 200) == 200 + 50
+
+
+def test_parameter_file_roundtrip_and_layout(tmp_path):
+    rng = np.random.default_rng(0)
+    flat = rng.normal(size=num_params(18))
+    p = Parameters.from_flat(flat, 18)
+    assert [w.shape for w in p.weights] == [(o, i) for o, i in layer_shapes(18)]
+    path = tmp_path / "net.params"
+    save_parameters(path, p)
+    q = load_parameters(path)
+    assert np.array_equal(q.flat(), flat)
+    assert theta_hash(p) == theta_hash(q)
+
+
+def test_parameter_file_readable_by_reference(tmp_path, reference_paraq):
+    """The PQNET1 file format is the reference's (nn.py:232-259)."""
+    from paraq.nn import load_parameters as ref_load, theta_hash as ref_hash
+
+    flat = np.random.default_rng(1).normal(size=num_params(4))
+    p = Parameters.from_flat(flat, 4)
+    path = tmp_path / "x.params"
+    save_parameters(path, p)
+    r = ref_load(path)
+    assert ref_hash(r) == theta_hash(p)
+
+
+def test_run_record_csv_format_matches_reference(reference_paraq):
+    from paraq.executor import RunRecord as RefRecord
+
+    kw = dict(config={"b": "2", "a": "1"}, seed=3, mode="both",
+              events=[(40, "episode", "0.5"), (40, "theta_hash", "abcd")],
+              final_hash="ffff", counters={"train_calls": 5, "flush_pushes": 7})
+    assert RunRecord(**kw).to_csv_text() == RefRecord(**kw).to_csv_text()
+
+
+def test_shard_covers_batch():
+    for B in (32, 33, 1024):
+        for G in (1, 2, 3, 8):
+            parts = [pdist.shard(B, r, G) for r in range(G)]
+            assert parts[0][0] == 0 and parts[-1][1] == B
+            assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+
+
+def _worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    seed = pdist.replica_seed(0, rank)
+    mx = pdist.reduce_max(float(rank + 1.5))
+    g = torch.full((8,), float(rank + 1))
+    pdist.allreduce_sum_(g)
+    seeds = [None] * world
+    dist.all_gather_object(seeds, seed)
+    out.put((rank, seeds, mx, g.tolist()))
+    dist.destroy_process_group()
+
+
+def test_multiprocess_replicas_and_gradient_allreduce_gloo():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() % 2000)
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, seeds, mx, g in res:
+        assert len(set(seeds)) == 2          # distinct replica seeds
+        assert mx == 2.5                     # max over ranks
+        assert g == [3.0] * 8                # sum all-reduce of per-rank gradient shards
