@@ -1,7 +1,7 @@
 # Builds the sm_100a C-ABI library of the fast-DQN hot path.
 NVCC ?= nvcc
 ARCH = -gencode arch=compute_100a,code=sm_100a
-NVFLAGS = -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+NVFLAGS = -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr -rdc=false
 SRC = $(wildcard paper_2111_01264_b200/csrc/*.cu)
 CSRC = $(wildcard paper_2111_01264_b200/csrc/*.cpp)
 HDR = $(wildcard paper_2111_01264_b200/csrc/*.cuh) include/paraq_b200.h

@@ -40,6 +40,8 @@ int pq_abi_version(void);
 const char *pq_last_error(void);
 int64_t pq_num_params(int actions);          /* 1,693,362 for 18 actions */
 int64_t pq_num_shadow(void);                 /* bf16 copies of the conv1..fc1 weights */
+/* Latency probes: enable/disable and read GEMM phase timestamps (out [256][12] ns). */
+int pq_timeline(int on, unsigned long long *out, int *count);
 
 /* ---- one Q-network parameter set (theta or theta-minus), device memory ------------ */
 typedef struct pq_net {

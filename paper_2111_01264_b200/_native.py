@@ -65,6 +65,7 @@ EXPORTS = {
     "pq_last_error": ([], C.c_char_p),
     "pq_num_params": ([C.c_int], C.c_int64),
     "pq_num_shadow": ([], C.c_int64),
+    "pq_timeline": ([C.c_int, vp, vp], C.c_int),
     "pq_net_sync_shadow": ([PqNet, vp], C.c_int),
     "pq_net_copy": ([PqNet, PqNet, C.c_int, vp], C.c_int),
     "pq_sample_indices": ([vp, C.c_uint32, C.c_int64, vp, vp], C.c_int),

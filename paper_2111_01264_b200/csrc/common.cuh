@@ -6,10 +6,40 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #define PQ_DEV __device__ __forceinline__
 
 namespace pq {
+
+// Kernel launch with the programmatic-stream-serialization attribute (PDL) unless
+// PQ_PDL=0 is set in the environment.
+inline bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("PQ_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on != 0;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------- smem / mbarrier
 PQ_DEV uint32_t smem_u32(const void *p) {
@@ -260,6 +290,32 @@ PQ_DEV U128 pcg_advance(U128 state, U128 inc, uint64_t delta) {
     }
     return add128(mul128(acc_mult, state), acc_plus);
 }
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// wait: block until the predecessor grid in the stream has completed (no-op when the
+// kernel was launched without the PDL attribute); launch: let the dependent grid start
+// its prologue now.  Every kernel triggers right after its own wait, so a dependent
+// that starts early may read anything produced two or more kernels back.
+PQ_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+PQ_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ---------------------------------------------------------------- timeline probes
+// Runtime-gated phase timestamps (%globaltimer, ns) of CTA 0 of each launch plus the
+// last CTA's end, for latency analysis (pq_timeline_*).  Off by default.
+struct Timeline {
+    int on;
+    int n;
+    unsigned long long t[256][12];
+    char tag[256];
+};
+static __device__ Timeline g_tl;  // one copy per translation unit (GEMMs live in qnet.cu)
+
+PQ_DEV unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+PQ_DEV bool tl_cta0() { return blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0; }
 
 // ---------------------------------------------------------------- misc
 PQ_DEV uint64_t splitmix64(uint64_t z) {

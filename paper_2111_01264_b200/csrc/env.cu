@@ -58,6 +58,8 @@ __device__ __forceinline__ float warp_sum_f(float v) {
 
 __global__ void __launch_bounds__(256) k_act_env(const ActArgs a) {
     const int j = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    griddep_wait();
+    griddep_launch();
     __shared__ float hs[512];
     __shared__ float qs[MAX_ACTIONS];
     __shared__ uint64_t s_base[2];
@@ -254,8 +256,7 @@ int pq_act_step(const pq_act_args *x, void *stream) {
     a.eps_start = x->eps_start, a.eps_end = x->eps_end, a.eps_anneal = x->eps_anneal;
     a.term_p = x->terminal_p;
     a.q_out = x->q_out;
-    k_act_env<<<x->W, 256, 0, st>>>(a);
-    return cuda_err(cudaGetLastError(), "act_env");
+    return cuda_err(launch_k(k_act_env, dim3(x->W), dim3(256), 0, st, a), "act_env");
 }
 
 }  // extern "C"

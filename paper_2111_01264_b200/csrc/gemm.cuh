@@ -450,47 +450,48 @@ struct EpiRms {
     int M, N;
     int64_t pbase, sbase;
     PQ_DEV void apply(int, int, const float *, int, int) const {}
-    // tile: [128][ld] fp32, rows m0.., cols n0.. (width BN); 256 threads
+    // tile: [128][ld] fp32, rows m0.., cols n0.. (width BN); 256 threads.  Rows are
+    // walked by warps, lanes cover consecutive parameters (coalesced); 4 rows per
+    // round keep 3 x 4 x BN/32 loads in flight per thread.
     template <int BN>
     PQ_DEV void apply_tile(const float *tile, int ld, int m0, int n0) const {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        constexpr int U = BN / 32;
+        const float one_m_rho = 1.0f - rho;
         bool bad = false;
         for (int r0 = warp; r0 < 128; r0 += 32) {
-            float gg[4][BN / 32], mm[4][BN / 32], vv[4][BN / 32], pp[4][BN / 32];
+            float mm[4][U], vv[4][U], pp[4][U];
+            int off[4][U];
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr) {
                 const int r = r0 + rr * 8;
-                const bool rok = m0 + r < M;
 #pragma unroll
-                for (int u = 0; u < BN / 32; ++u) {
+                for (int u = 0; u < U; ++u) {
                     const int col = lane + 32 * u;
-                    const bool ok = rok && n0 + col < N;
-                    const int64_t i = pbase + (int64_t)(m0 + r) * N + n0 + col;
-                    gg[rr][u] = tile[r * ld + col];
-                    mm[rr][u] = ok ? m[i] : 0.f;
-                    vv[rr][u] = ok ? v[i] : 0.f;
-                    pp[rr][u] = ok ? p[i] : 0.f;
+                    const bool ok = m0 + r < M && n0 + col < N;
+                    off[rr][u] = ok ? (m0 + r) * N + n0 + col : -1;  // < 2^31 for fc1
+                    mm[rr][u] = ok ? m[pbase + off[rr][u]] : 0.f;
+                    vv[rr][u] = ok ? v[pbase + off[rr][u]] : 0.f;
+                    pp[rr][u] = ok ? p[pbase + off[rr][u]] : 0.f;
                 }
             }
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr) {
                 const int r = r0 + rr * 8;
-                if (m0 + r >= M) continue;
 #pragma unroll
-                for (int u = 0; u < BN / 32; ++u) {
-                    const int col = lane + 32 * u;
-                    if (n0 + col >= N) continue;
-                    const int64_t off = (int64_t)(m0 + r) * N + n0 + col;
-                    const float g = gg[rr][u];
+                for (int u = 0; u < U; ++u) {
+                    const int o = off[rr][u];
+                    if (o < 0) continue;
+                    const float g = tile[r * ld + lane + 32 * u];
                     bad |= !isfinite(g);
-                    const float mi = rho * mm[rr][u] + (1.0f - rho) * g;
-                    const float vi = rho * vv[rr][u] + (1.0f - rho) * g * g;
-                    const float pi = pp[rr][u] - lr * g / sqrtf(vi - mi * mi + kappa);
-                    m2[pbase + off] = mi;
-                    v2[pbase + off] = vi;
-                    p2[pbase + off] = pi;
-                    shadow[sbase + off] = __float2bfloat16_rn(pi);
-                    if (grad_out) grad_out[pbase + off] = g;
+                    const float mi = rho * mm[rr][u] + one_m_rho * g;
+                    const float vi = rho * vv[rr][u] + one_m_rho * g * g;
+                    const float pi = pp[rr][u] - lr * g * rsqrtf(vi - mi * mi + kappa);
+                    m2[pbase + o] = mi;
+                    v2[pbase + o] = vi;
+                    p2[pbase + o] = pi;
+                    shadow[sbase + o] = __float2bfloat16_rn(pi);
+                    if (grad_out) grad_out[pbase + o] = g;
                 }
             }
         }
@@ -561,6 +562,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const uint32_t smem_s = smem_u32(smem);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool tl = g_tl.on && tl_cta0() && tid == 0;
+    int tl_i = 0;
+    unsigned long long tl_t[12];
+    if (tl) tl_t[tl_i++] = gtime();
     const int grp = blockIdx.z / g.splits, split = blockIdx.z - grp * g.splits;
     const LA la = g.a[grp];
     const LB lb = g.b[grp];
@@ -575,6 +580,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc<TMEM_COLS>(&tmem_base_s);
+    if (tl) tl_t[tl_i++] = gtime();  // 1: barriers + TMEM
+    griddep_wait();
+    griddep_launch();
+    if (tl) tl_t[tl_i++] = gtime();  // 2: predecessor done
     LoadCtx cx{table, 0};
     if constexpr (LA::TABLE) {
         // sample window of the rows this CTA reads: MN rows (K-major) or the split's
@@ -673,11 +682,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
 
+    if (tl) tl_t[tl_i++] = gtime();  // 3: contexts ready
 #pragma unroll
     for (int s = 0; s < PRE; ++s) {
         if (s < nk) issue(kb0 + s, s);
         cp_async_commit();
     }
+    if (tl) tl_t[tl_i++] = gtime();  // 4: prologue issued
     for (int i = 0; i < nk; ++i) {
         const int s = i % STAGES;
         cp_async_wait<PRE - 1>();
@@ -695,6 +706,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 umma_bf16(tmem, ad, bd, IDESC, (i > 0 || j > 0) ? 1u : 0u);
             }
             umma_commit(&bars[s]);
+            if (tl && (i == 0 || i == nk - 1)) tl_t[tl_i++] = gtime();  // 5, 6: first / last MMA issued
         }
         const int jn = i + PRE;
         if (jn < nk) {
@@ -709,6 +721,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(&bars[last % STAGES], (last / STAGES) & 1);
     }
     tc_fence_after();
+    if (tl) tl_t[tl_i++] = gtime();  // 7: accumulator ready
 
     // epilogue: warp w reads TMEM lanes 32*(w%4).. (tile rows); the two warpgroups
     // split the columns
@@ -758,6 +771,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc<TMEM_COLS>(tmem);
+    if (tl) {
+        tl_t[tl_i++] = gtime();  // 8: epilogue done
+        const int slot = atomicAdd(&g_tl.n, 1);
+        if (slot < 256) {
+            for (int k = 0; k < 12; ++k) g_tl.t[slot][k] = k < tl_i ? tl_t[k] : 0ull;
+            g_tl.tag[slot] = (char)('a' + (BN >> 4) % 26);
+        }
+    }
 }
 
 template <int BN, bool AMN, bool BMN, int ST = 0, class LA, class LB, class EP>
@@ -771,8 +792,7 @@ cudaError_t launch_gemm(const GemmArgs<LA, LB, EP> &g, int groups, cudaStream_t 
         configured = true;
     }
     dim3 grid(grid_x ? grid_x : (g.M + 127) / 128, (g.N + BN - 1) / BN, groups * g.splits);
-    kern<<<grid, GEMM_THREADS, smem, st>>>(g);
-    return cudaGetLastError();
+    return launch_k(kern, grid, dim3(GEMM_THREADS), smem, st, g);
 }
 
 }  // namespace pq

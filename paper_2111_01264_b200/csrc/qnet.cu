@@ -18,6 +18,8 @@
 
 namespace pq {
 
+
+
 thread_local char g_err[512] = "";
 int set_err(const char *msg) {
     snprintf(g_err, sizeof(g_err), "%s", msg);
@@ -240,6 +242,8 @@ __device__ __forceinline__ float warp_sum(float v) {
 constexpr int HEAD_THREADS = 256;
 __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
     const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    griddep_wait();
+    griddep_launch();
     __shared__ float hs[2][512];
     __shared__ float qs[2][MAX_ACTIONS];
     __shared__ float s_delta;
@@ -366,8 +370,7 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
         h.ext_actions = la->ext_actions, h.gamma = la->gamma;
         h.q_copy = la->q_out, h.td_copy = la->td_out;
     }
-    k_head<<<n, HEAD_THREADS, 0, st>>>(h);
-    return cuda_err(cudaGetLastError(), "head");
+    return cuda_err(launch_k(k_head, dim3(n), dim3(HEAD_THREADS), 0, st, h), "head");
 }
 
 // ------------------------------------------------------------------ optimizer
@@ -476,12 +479,14 @@ __device__ __forceinline__ void rms(const OptArgs &a, float g, float m, float v,
                                     float &m2, float &v2, float &p2) {
     m2 = a.rho * m + (1.0f - a.rho) * g;
     v2 = a.rho * v + (1.0f - a.rho) * g * g;
-    p2 = p - a.lr * g / sqrtf(v2 - m2 * m2 + a.kappa);
+    p2 = p - a.lr * g * rsqrtf(v2 - m2 * m2 + a.kappa);
 }
 
 // every parameter except fc1's weight (updated in the fc1 wgrad epilogue unless
 // a.grad4 is given), one parameter per thread
 __global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
+    griddep_wait();
+    griddep_launch();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t i = a.grad4 ? t : (t < P_W4 ? t : P_B4 + (t - P_W4));
     if (i < a.total) {
@@ -514,8 +519,8 @@ static int choose_kc(int nchunks, int mtiles, int *splits, int kc_max = 1 << 30)
 // side stream + events for the weight-gradient branch (fork after each data
 // gradient, join before the optimizer); also captured into CUDA graphs as branches
 struct Fork {
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev[4] = {};
+    cudaStream_t side = nullptr, side2 = nullptr;
+    cudaEvent_t ev[6] = {};
 };
 static Fork g_fork[16];
 
@@ -525,6 +530,7 @@ static int get_fork(Fork **out) {
     Fork &f = g_fork[dev & 15];
     if (!f.side) {
         PQ_CHECK(cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking), "side stream");
+        PQ_CHECK(cudaStreamCreateWithFlags(&f.side2, cudaStreamNonBlocking), "side stream 2");
         for (auto &e : f.ev) PQ_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     }
     *out = &f;
@@ -537,7 +543,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     int s1 = 1, s2 = 1, s3 = 1;
     Fork *fk = nullptr;
     if (int rc = get_fork(&fk)) return rc;
-    cudaStream_t side = fk->side;
+    cudaStream_t side = fk->side, side2 = fk->side2;
     {  // B4d: dY3[b][k] = relu'(x3) * sum_j W4[j][k] dh1[b][j]   (D[k][b], MN-major W4)
         GemmArgs<LoadDense, LoadDense, EpiMaskT> g{};
         g.a[0] = LoadDense{sh + S_W4, 512, 3136, 3136};
@@ -551,6 +557,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     // shadow that B4d reads, so it must not start earlier
     PQ_CHECK(cudaEventRecord(fk->ev[1], st), "fork1");
     PQ_CHECK(cudaStreamWaitEvent(side, fk->ev[1], 0), "fork1 wait");
+    PQ_CHECK(cudaStreamWaitEvent(side2, fk->ev[1], 0), "fork1 wait 2");
     {  // B4w + RMSProp: dW4[j][k] = sum_b dh1[b][j] x3[b][k] (contraction over the batch),
        // centered RMSProp applied in the epilogue (no fp32 gradient round trip)
         GemmArgs<LoadDense, LoadDense, EpiRms> g{};
@@ -565,7 +572,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         e.M = 512, e.N = 3136, e.pbase = P_W4, e.sbase = S_W4;
         g.e[0] = e;
         g.M = 512, g.N = 3136, g.K = n, g.kc_per_split = (n + 63) / 64, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<128, false, true, 4>(g, 1, side)), "fc1 wgrad+rmsprop");
+        PQ_CHECK((launch_gemm<64, false, true, 4>(g, 1, side)), "fc1 wgrad+rmsprop");
     }
     {  // B3w: dW3^T[k][o] = sum_m P3[m][k] dY3[m][o]; row 576 = ones -> bias grad
         GemmArgs<LoadIm2col, LoadDense, EpiF32T> g{};
@@ -575,7 +582,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         int nch = (n * 49 + 63) / 64;
         g.kc_per_split = choose_kc(nch, 5, &s3);
         g.M = 577, g.N = 64, g.K = n * 49, g.splits = s3, g.ones_at = 576, g.ones_extent = n * 49;
-        PQ_CHECK((launch_gemm<64, true, true>(g, 1, side)), "conv3 wgrad");
+        PQ_CHECK((launch_gemm<64, true, true>(g, 1, side2)), "conv3 wgrad");
     }
     {  // B3d: dY2 = relu'(x2) * transposed conv3(dY3)
         GemmArgs<LoadTConv, LoadWeightT, EpiMask> g{};
@@ -586,7 +593,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         PQ_CHECK((launch_gemm<64, false, true>(g, 1, st)), "conv3 dgrad");
     }
     PQ_CHECK(cudaEventRecord(fk->ev[2], st), "fork2");
-    PQ_CHECK(cudaStreamWaitEvent(side, fk->ev[2], 0), "fork2 wait");
+    PQ_CHECK(cudaStreamWaitEvent(side2, fk->ev[2], 0), "fork2 wait");
     {  // B2w
         GemmArgs<LoadIm2col, LoadDense, EpiF32T> g{};
         g.a[0] = im2col(w.act1[0], n, 20, 20, 32, 4, 2, 9, 9);
@@ -595,7 +602,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         int nch = (n * 81 + 63) / 64;
         g.kc_per_split = choose_kc(nch, 5, &s2);
         g.M = 513, g.N = 64, g.K = n * 81, g.splits = s2, g.ones_at = 512, g.ones_extent = n * 81;
-        PQ_CHECK((launch_gemm<64, true, true>(g, 1, side)), "conv2 wgrad");
+        PQ_CHECK((launch_gemm<64, true, true>(g, 1, side2)), "conv2 wgrad");
     }
     {  // B2d: dY1 = relu'(x1) * transposed conv2(dY2), stride 2 split into the 4 input
        // parity classes -> K = 4 taps x 64 per class instead of 16 x 64
@@ -621,7 +628,9 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     }
     // join the weight-gradient branch
     PQ_CHECK(cudaEventRecord(fk->ev[3], side), "join");
+    PQ_CHECK(cudaEventRecord(fk->ev[4], side2), "join 2");
     PQ_CHECK(cudaStreamWaitEvent(st, fk->ev[3], 0), "join wait");
+    PQ_CHECK(cudaStreamWaitEvent(st, fk->ev[4], 0), "join wait 2");
     {
         OptArgs o{};
         o.p = th.master, o.m = la->opt.m, o.v = la->opt.v;
@@ -636,8 +645,8 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         o.grad_out = la->grad_out;
         o.total = n_params(la->actions);
         const int64_t cnt = P_W4 + (o.total - P_B4);
-        k_optimizer<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(o);
-        PQ_CHECK(cudaGetLastError(), "optimizer");
+        PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((cnt + 255) / 256)), dim3(256), 0, st, o),
+                 "optimizer");
     }
     return 0;
 }
@@ -681,6 +690,19 @@ using namespace pq;
 extern "C" {
 
 int pq_abi_version(void) { return PQ_ABI_VERSION; }
+
+int pq_timeline(int on, unsigned long long *out, int *count) {
+    if (out) {
+        static Timeline h;
+        PQ_CHECK(cudaMemcpyFromSymbol(&h, g_tl, sizeof(Timeline)), "timeline read");
+        *count = h.n < 256 ? h.n : 256;
+        memcpy(out, h.t, sizeof(h.t));
+    }
+    Timeline z{};
+    z.on = on;
+    PQ_CHECK(cudaMemcpyToSymbol(g_tl, &z, sizeof(int) * 2), "timeline reset");
+    return 0;
+}
 const char *pq_last_error(void) { return g_err; }
 int64_t pq_num_params(int actions) { return n_params(actions); }
 int64_t pq_num_shadow(void) { return S_TOTAL; }
