@@ -83,7 +83,7 @@ def unpack(net):
     return P, S
 
 
-@pytest.mark.parametrize("B", [32, 8, 40])
+@pytest.mark.parametrize("B", [32, 8, 40, 256, 1024])
 def test_learner_step_stagewise(B):
     rng = np.random.default_rng(B)
     mem = make_memory(rng)
@@ -199,3 +199,14 @@ def test_forward_zero_network_gives_zero_rows():
     net = dnn.QNet.from_flat(np.zeros(dnn.num_params(A)), A)
     q = dnn.forward(net, np.ones((5, 4, 84, 84), dtype=np.uint8))
     assert q.shape == (5, A) and (q == 0).all()
+
+
+@pytest.mark.parametrize("W", [128, 512])
+def test_wide_acting_batch_rows_match_small_batches(W):
+    """Synchronized-execution sweep (configs[2]): a W-row batched forward equals the
+    forwards of its 8-row slices (row independence across tile / N-shape choices)."""
+    _, _, net = net_from(12)
+    x = np.random.default_rng(W).integers(0, 256, size=(W, 4, 84, 84), dtype=np.uint8)
+    big = dnn.forward(net, x)
+    small = np.concatenate([dnn.forward(net, x[i:i + 8]) for i in range(0, W, 8)])
+    assert np.array_equal(big, small)
