@@ -193,6 +193,23 @@ int pq_rmsprop_f32(const float *p, const float *g, const float *m, const float *
                    float lr, float rho, float kappa, float *p2, float *m2, float *v2,
                    int32_t *nonfinite, void *stream);
 
+/* ---- fp64 kernel module: the reference plugin API, bit-exact with numba ------------
+ * _kernels_numba.py:19-111 (selected by backend.py:18-34); device pointers, float64,
+ * C-contiguous, output buffers caller-allocated. */
+int pq64_affine_rows(const double *w, const double *b, const double *x, int64_t n, int64_t o,
+                     int64_t d, double *out, void *stream);
+int pq64_relu(const double *x, int64_t count, double *out, void *stream);
+int pq64_output_delta(const double *q, const int64_t *actions, const double *targets, int64_t n,
+                      int64_t o, double *delta, void *stream);
+int pq64_weight_grad(const double *delta, const double *acts, int64_t n, int64_t o, int64_t d,
+                     double *dw, void *stream);
+int pq64_bias_grad(const double *delta, int64_t n, int64_t o, double *db, void *stream);
+int pq64_hidden_delta(const double *delta, const double *w, const double *pre, int64_t n,
+                      int64_t o, int64_t d, double *out, void *stream);
+int pq64_rmsprop_flat(const double *p, const double *g, const double *m, const double *v,
+                      int64_t count, double lr, double rho, double kappa, double *p2, double *m2,
+                      double *v2, void *stream);
+
 /* ---- host-side helpers ---------------------------------------------------------- */
 /* theta_hash (nn.py:223-229): FNV-1a 64 over the little-endian float64 bytes of the
  * parameters (fp32 master widened to f64), layer order weights then bias. */

@@ -86,6 +86,14 @@ EXPORTS = {
     "pq_henv_reset": ([vp, C.c_int, vp, C.c_int64, vp, vp], C.c_int),
     "pq_henv_step": ([vp, C.c_int, vp, C.c_int, C.c_int, C.c_double, C.c_int64, C.c_double,
                       C.c_double, C.c_int64, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "pq64_affine_rows": ([vp, vp, vp, C.c_int64, C.c_int64, C.c_int64, vp, vp], C.c_int),
+    "pq64_relu": ([vp, C.c_int64, vp, vp], C.c_int),
+    "pq64_output_delta": ([vp, vp, vp, C.c_int64, C.c_int64, vp, vp], C.c_int),
+    "pq64_weight_grad": ([vp, vp, C.c_int64, C.c_int64, C.c_int64, vp, vp], C.c_int),
+    "pq64_bias_grad": ([vp, C.c_int64, C.c_int64, vp, vp], C.c_int),
+    "pq64_hidden_delta": ([vp, vp, vp, C.c_int64, C.c_int64, C.c_int64, vp, vp], C.c_int),
+    "pq64_rmsprop_flat": ([vp, vp, vp, vp, C.c_int64, C.c_double, C.c_double, C.c_double, vp,
+                           vp, vp, vp], C.c_int),
     "pq_theta_hash_f32": ([vp, C.c_int64], C.c_uint64),
     "pq_theta_hash_f64": ([vp, C.c_int64], C.c_uint64),
 }

@@ -535,7 +535,10 @@ struct GemmCfg {
     static constexpr int SMEM = STAGES * STAGE + 1024;
 };
 
-template <int BN, bool AMN, bool BMN, int ST, class LA, class LB, class EP>
+// PF: operand whose data never comes from the immediately preceding kernel (weights),
+// issued before griddepcontrol.wait so it lands while the predecessor drains
+// (0 = none, 1 = A, 2 = B).
+template <int BN, bool AMN, bool BMN, int ST, int PF, class LA, class LB, class EP>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm(const __grid_constant__ GemmArgs<LA, LB, EP> g) {
     static_assert(BN == 16 || BN == 32 || BN == 64 || BN == 128 || BN == 256, "BN");
@@ -544,7 +547,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     using Cfg = GemmCfg<BN, LA::U8, ST>;
     constexpr int STAGES = Cfg::STAGES;
     static_assert(STAGES >= 2, "stages");
-    constexpr int PRE = STAGES - 1;
+    // chunks in flight ahead of the MMA; refilling the slot of chunk i-2 (not i-1)
+    // gives each MMA a full iteration to retire before its slot is reused
+    constexpr int PRE = STAGES >= 4 ? STAGES - 2 : STAGES - 1;
     constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
     constexpr uint32_t IDESC = idesc_bf16(BN, AMN, BMN);
     constexpr int NA = 1024 / GEMM_THREADS;                   // A chunks per thread (4)
@@ -581,19 +586,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     if (warp == 0) tmem_alloc<TMEM_COLS>(&tmem_base_s);
     if (tl) tl_t[tl_i++] = gtime();  // 1: barriers + TMEM
-    griddep_wait();
-    griddep_launch();
-    if (tl) tl_t[tl_i++] = gtime();  // 2: predecessor done
     LoadCtx cx{table, 0};
-    if constexpr (LA::TABLE) {
-        // sample window of the rows this CTA reads: MN rows (K-major) or the split's
-        // contraction range (MN-major)
-        const int lo = AMN ? kb0 * 64 : m0;
-        const int hi = AMN ? max(lo, kb1 * 64 - 1) : m0 + 127;
-        cx.tb = lo / 400;
-        int last = min(hi / 400, cx.tb + TABLE_SAMPLES - 1);
-        la.fill(cx.tb, last, table);
-    }
 
     // fixed per-thread operand contexts
     const int a_c8 = AMN ? (tid & 15) : (tid & 7);      // fixed inner chunk
@@ -620,12 +613,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     const bool has_ones = AMN && g.ones_at >= m0 + a_c8 * 8 && g.ones_at < m0 + a_c8 * 8 + 8;
 
-    // issue the cp.async copies of K-chunk kb into ring slot s
-    auto issue = [&](int kb, int s) {
+    // issue the cp.async copies of K-chunk kb into ring slot s (A / B separately)
+    auto issue_a = [&](int kb, int s) {
         const int k0 = kb * 64;
         const uint32_t a_s = smem_s + s * Cfg::STAGE;
-        const uint32_t b_s = a_s + GEMM_A_BYTES;
-        const uint32_t u_s = b_s + Cfg::B_BYTES;
+        const uint32_t u_s = a_s + GEMM_A_BYTES + Cfg::B_BYTES;
         typename LA::Col cak = AMN ? ca : la.col(k0 + a_c8 * 8);
 #pragma unroll
         for (int i = 0; i < NA; ++i) {
@@ -643,17 +635,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 cp_async16(a_s + off, src, bytes);
             }
         }
-        if (b_live) {
-            typename LB::Col cbk = BMN ? cb : lb.col(k0 + b_c8 * 8);
+    };
+    auto issue_b = [&](int kb, int s) {
+        if (!b_live) return;
+        const int k0 = kb * 64;
+        const uint32_t b_s = smem_s + s * Cfg::STAGE + GEMM_A_BYTES;
+        typename LB::Col cbk = BMN ? cb : lb.col(k0 + b_c8 * 8);
 #pragma unroll
-            for (int i = 0; i < NB; ++i) {
-                const int r = b_r0 + i * BSTEP;
-                typename LB::Row rr = BMN ? lb.row(k0 + r) : rb[i];
-                int bytes;
-                const void *src = lb.addr(rr, cbk, bytes, cx);
-                const uint32_t off = BMN ? mnmaj_off(r, b_c8) : kmaj_off(r, b_c8);
-                cp_async16(b_s + off, src, bytes);
-            }
+        for (int i = 0; i < NB; ++i) {
+            const int r = b_r0 + i * BSTEP;
+            typename LB::Row rr = BMN ? lb.row(k0 + r) : rb[i];
+            int bytes;
+            const void *src = lb.addr(rr, cbk, bytes, cx);
+            const uint32_t off = BMN ? mnmaj_off(r, b_c8) : kmaj_off(r, b_c8);
+            cp_async16(b_s + off, src, bytes);
         }
     };
     // after this thread's copies of chunk kb landed: widen its own uint8 chunks to
@@ -677,6 +672,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
     };
 
+    // weights (never written by the previous kernel) go out before the dependency wait
+#pragma unroll
+    for (int s = 0; s < PRE; ++s) {
+        if (s < nk) {
+            if (PF == 1) issue_a(kb0 + s, s);
+            if (PF == 2) issue_b(kb0 + s, s);
+        }
+    }
+    griddep_wait();
+    griddep_launch();
+    if (tl) tl_t[tl_i++] = gtime();  // 2: predecessor done
+    if constexpr (LA::TABLE) {
+        // sample window of the rows this CTA reads: MN rows (K-major) or the split's
+        // contraction range (MN-major)
+        const int lo = AMN ? kb0 * 64 : m0;
+        const int hi = AMN ? max(lo, kb1 * 64 - 1) : m0 + 127;
+        cx.tb = lo / 400;
+        int last = min(hi / 400, cx.tb + TABLE_SAMPLES - 1);
+        la.fill(cx.tb, last, table);
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -685,7 +700,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (tl) tl_t[tl_i++] = gtime();  // 3: contexts ready
 #pragma unroll
     for (int s = 0; s < PRE; ++s) {
-        if (s < nk) issue(kb0 + s, s);
+        if (s < nk) {
+            if (PF != 1) issue_a(kb0 + s, s);
+            if (PF != 2) issue_b(kb0 + s, s);
+        }
         cp_async_commit();
     }
     if (tl) tl_t[tl_i++] = gtime();  // 4: prologue issued
@@ -712,7 +730,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (jn < nk) {
             const int sl = jn % STAGES;
             if (jn >= STAGES) mbar_wait(&bars[sl], ((jn / STAGES) - 1) & 1);
-            issue(kb0 + jn, sl);
+            issue_a(kb0 + jn, sl);
+            issue_b(kb0 + jn, sl);
         }
         cp_async_commit();
     }
@@ -781,9 +800,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
 }
 
-template <int BN, bool AMN, bool BMN, int ST = 0, class LA, class LB, class EP>
+template <int BN, bool AMN, bool BMN, int ST = 0, int PF = 0, class LA, class LB, class EP>
 cudaError_t launch_gemm(const GemmArgs<LA, LB, EP> &g, int groups, cudaStream_t st, int grid_x = 0) {
-    auto kern = k_gemm<BN, AMN, BMN, ST, LA, LB, EP>;
+    auto kern = k_gemm<BN, AMN, BMN, ST, PF, LA, LB, EP>;
     constexpr int smem = GemmCfg<BN, LA::U8, ST>::SMEM;
     static bool configured = false;  // per instantiation
     if (!configured) {

@@ -149,14 +149,14 @@ static int choose_bn(int n) {
     return n <= 16 ? 16 : n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256;
 }
 
-template <class LA, class LB, class EP, bool AMN, bool BMN>
+template <class LA, class LB, class EP, bool AMN, bool BMN, int PF = 0>
 static cudaError_t launch_bn(int bn, const GemmArgs<LA, LB, EP> &g, int groups, cudaStream_t st) {
     switch (bn) {
-        case 16: return launch_gemm<16, AMN, BMN>(g, groups, st);
-        case 32: return launch_gemm<32, AMN, BMN>(g, groups, st);
-        case 64: return launch_gemm<64, AMN, BMN>(g, groups, st);
-        case 128: return launch_gemm<128, AMN, BMN>(g, groups, st);
-        default: return launch_gemm<256, AMN, BMN>(g, groups, st);
+        case 16: return launch_gemm<16, AMN, BMN, 0, PF>(g, groups, st);
+        case 32: return launch_gemm<32, AMN, BMN, 0, PF>(g, groups, st);
+        case 64: return launch_gemm<64, AMN, BMN, 0, PF>(g, groups, st);
+        case 128: return launch_gemm<128, AMN, BMN, 0, PF>(g, groups, st);
+        default: return launch_gemm<256, AMN, BMN, 0, PF>(g, groups, st);
     }
 }
 
@@ -181,7 +181,7 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
             g.e[q] = EpiBiasRelu{w.act2[q], nets[q].master + P_B2, n * 81, 64, 64, 1.0f};
         }
         g.M = n * 81, g.N = 64, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<64, false, false>(g, groups, st)), "conv2 forward");
+        PQ_CHECK((launch_gemm<64, false, false, 0, 2>(g, groups, st)), "conv2 forward");
     }
     {  // F3: conv3 3x3/1 over 9x9x64 (K = 576)
         GemmArgs<LoadIm2col, LoadDense, EpiBiasRelu> g{};
@@ -191,7 +191,7 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
             g.e[q] = EpiBiasRelu{w.act3[q], nets[q].master + P_B3, n * 49, 64, 64, 1.0f};
         }
         g.M = n * 49, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<64, false, false>(g, groups, st)), "conv3 forward");
+        PQ_CHECK((launch_gemm<64, false, false, 0, 2>(g, groups, st)), "conv3 forward");
     }
     {  // F4: fc1, swapped (D[j][b] = W4[j] . x[b]) with split-K partials [s][b][j]
         GemmArgs<LoadDense, LoadDense, EpiF32T> g{};
@@ -202,7 +202,7 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
         }
         g.M = 512, g.N = n, g.K = 3136, g.kc_per_split = 49 / FC1_SPLITS, g.splits = FC1_SPLITS,
         g.ones_at = -1;
-        PQ_CHECK((launch_bn<LoadDense, LoadDense, EpiF32T, false, false>(choose_bn(n), g, groups, st)),
+        PQ_CHECK((launch_bn<LoadDense, LoadDense, EpiF32T, false, false, 1>(choose_bn(n), g, groups, st)),
                  "fc1 forward");
     }
     return 0;
@@ -550,7 +550,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         g.b[0] = LoadDense{w.dh1_bf, n, 512, 512};
         g.e[0] = EpiMaskT{w.dY3, w.act3[0], 3136, n, 3136};
         g.M = 3136, g.N = n, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_bn<LoadDense, LoadDense, EpiMaskT, true, false>(choose_bn(n), g, 1, st)),
+        PQ_CHECK((launch_bn<LoadDense, LoadDense, EpiMaskT, true, false, 1>(choose_bn(n), g, 1, st)),
                  "fc1 dgrad");
     }
     // fork after the fc1 data gradient: the fused fc1 update below rewrites the W4
@@ -590,7 +590,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         g.b[0] = weight_t(sh + S_W3, 64, 3, 64);
         g.e[0] = EpiMask{w.dY2, w.act2[0], n * 81, 64, 64};
         g.M = n * 81, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<64, false, true>(g, 1, st)), "conv3 dgrad");
+        PQ_CHECK((launch_gemm<64, false, true, 0, 2>(g, 1, st)), "conv3 dgrad");
     }
     PQ_CHECK(cudaEventRecord(fk->ev[2], st), "fork2");
     PQ_CHECK(cudaStreamWaitEvent(side2, fk->ev[2], 0), "fork2 wait");
@@ -612,7 +612,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         g.b[0] = weight_tp(sh + S_W2, 64, 4, 32, tpc);
         g.e[0] = epi_mask_p(w.dY1, w.act1[0], n, 10, 10, 32, tpc);
         g.M = 4 * tpc * 128, g.N = 32, g.K = 256, g.kc_per_split = 4, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<64, false, true>(g, 1, st)), "conv2 dgrad");
+        PQ_CHECK((launch_gemm<64, false, true, 0, 2>(g, 1, st)), "conv2 dgrad");
     }
     {  // B1w: dW1^T[k][o] = sum_m P1[m][k] dY1[m][o] over uint8 frames; row 256 = ones
         GemmArgs<LoadFrames, LoadDense, EpiF32T> g{};

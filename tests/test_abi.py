@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "paraq_b200.h")
 def declared_symbols():
     txt = open(HEADER).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"\b(pq_[a-z0-9_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(pq(?:64)?_[a-z0-9_]+)\s*\(", txt)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -130,3 +130,17 @@ def test_host_samplers_bit_exact_vs_oracle_env_and_select_action():
             assert dev_state.tobytes() == nxt.tobytes()
             assert np.array_equal(np.array(list(envs[j].pcg), dtype=np.uint64),
                                   pcg_state_from_generator(rngs[j]))
+
+
+def test_reference_nn_runs_on_plugin_module_interface(reference_paraq):
+    """The plugin module exposes exactly the reference kernel-module contract
+    (_kernels_numba.py:14-121), so paraq.nn can be pointed at it."""
+    import paraq._kernels_numba as ref_k
+
+    from paper_2111_01264_b200 import kernels as b200
+
+    names = ["BACKEND_NAME", "affine_rows", "relu", "output_delta", "weight_grad", "bias_grad",
+             "hidden_delta", "rmsprop_flat", "spin"]
+    for nm in names:
+        assert hasattr(ref_k, nm) and hasattr(b200, nm), nm
+    assert b200.spin(1000) == ref_k.spin(1000)
