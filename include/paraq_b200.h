@@ -164,6 +164,8 @@ typedef struct pq_act_args {
     float *q_out;               /* optional [W][actions] */
     void *ws;
     int max_batch;
+    int max_episodes;           /* > 0: a sampler stops after this many finished episodes
+                                   (evaluate_policy's exact episode budget) */
 } pq_act_args;
 
 /* One synchronized block (executor.py:451-510): batched Q inference for the W current

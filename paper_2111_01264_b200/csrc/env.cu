@@ -48,6 +48,7 @@ struct ActArgs {
     int64_t eps_anneal;
     double term_p;
     float *q_out;
+    int max_episodes;
 };
 
 __device__ __forceinline__ float warp_sum_f(float v) {
@@ -124,8 +125,10 @@ __global__ void __launch_bounds__(256) k_act_env(const ActArgs a) {
             }
         }
     }
+    __shared__ bool s_active;
+    if (tid == 0) s_active = a.max_episodes <= 0 || epc < a.max_episodes;
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0 && s_active) {
         // step_counter counts lockstep blocks (run-global in the executor); the
         // staging row is the block index within the epoch
         const int b = (int)(bg % a.steps);
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(256) k_act_env(const ActArgs a) {
         for (int k = 0; k < 6; ++k) a.e.pcg[j * 6 + k] = out[k];
     }
     __syncthreads();
-    for (int f = 0; f < 2; ++f) {
+    for (int f = 0; f < 2 && s_active; ++f) {
         if (s_slot[f] < 0) continue;
         uint64_t *d = reinterpret_cast<uint64_t *>(a.ring + (size_t)s_slot[f] * FRAME_BYTES);
         for (int p = tid; p < FRAME_BYTES / 8; p += blockDim.x) d[p] = splitmix64(s_base[f] + (uint64_t)p);
@@ -256,6 +259,7 @@ int pq_act_step(const pq_act_args *x, void *stream) {
     a.eps_start = x->eps_start, a.eps_end = x->eps_end, a.eps_anneal = x->eps_anneal;
     a.term_p = x->terminal_p;
     a.q_out = x->q_out;
+    a.max_episodes = x->max_episodes;
     return cuda_err(launch_k(k_act_env, dim3(x->W), dim3(256), 0, st, a), "act_env");
 }
 

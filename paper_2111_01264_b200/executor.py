@@ -157,14 +157,13 @@ class DeviceRun:
     """Shared state and epoch driver of one device run (executor.py:341-594)."""
 
     def __init__(self, hp: HyperParams, sink=None, use_graphs: bool = True, graph_chunk: int = 25,
-                 hash_epochs: bool = True):
+                 hash_epochs: bool = True, sequential: bool = False):
         hp.validate()
         if not hp.concurrent:
             raise NotImplementedError("the device executor implements the concurrent modes "
                                       "('both', 'concurrent')")
-        if hp.eval_period:
-            raise NotImplementedError("periodic evaluation is not on the device path (eval_period=0)")
         torch = N.require_cuda()
+        self.sequential = sequential
         self.torch = torch
         self.hp = hp
         self.sink = sink
@@ -210,6 +209,8 @@ class DeviceRun:
         self.record = RunRecord(config=config_echo(hp), seed=hp.seed, mode=hp.mode,
                                 counters=self.counters)
         self._graphs = None
+        self._eval_idx = 0
+        self._eval = None
 
     def _own_ws(self, n):
         torch = self.torch
@@ -340,7 +341,14 @@ class DeviceRun:
         cur = torch.cuda.current_stream()
         self.act_stream.wait_stream(cur)
         self.learn_stream.wait_stream(cur)
-        if self.use_graphs:
+        if self.sequential:
+            # single-lane schedule (sequential_reference, executor.py:596-637): all
+            # sampler blocks, then the epoch's minibatches, on one stream
+            for _ in range(self.steps):
+                self.act_step()
+            for _ in range(self.updates):
+                self.learn_step()
+        elif self.use_graphs:
             self._replay_epoch()
         else:
             with torch.cuda.stream(self.act_stream):
@@ -378,6 +386,53 @@ class DeviceRun:
                         gl.replay()
                     il += 1
 
+    # -- evaluation (envs.evaluate_policy, envs.py:177-202; executor.py:396-412) ---------
+    def maybe_eval(self, boundary: int):
+        hp = self.hp
+        if not hp.eval_period or boundary == 0 or boundary % hp.eval_period != 0:
+            return
+        mean, std = self.evaluate(self.target, hp.eval_epsilon, hp.eval_episodes,
+                                  derived_seed(hp.seed, ROLE_EVAL, self._eval_idx))
+        self._eval_idx += 1
+        self.record.evals.append((boundary, mean, std))
+        self.emit(boundary, "eval_mean", repr(mean))
+        self.emit(boundary, "eval_std", repr(std))
+
+    def evaluate(self, params: QNet, epsilon: float, episodes: int, seed: int):
+        """Exactly `episodes` epsilon-greedy episodes of the (persistent) eval env on one
+        rng stream, single-state forwards on the GPU; mean and population std."""
+        torch = self.torch
+        hp = self.hp
+        lib = N.load()
+        if self._eval is None:
+            envs = DeviceEnvs([derived_seed(hp.seed, ROLE_EVAL, 1000)],
+                              [np.random.default_rng(0)], 256)
+            ring = torch.zeros((64, 7056), dtype=torch.uint8, device="cuda")
+            staging = torch.empty((1, 256, REC_INTS), dtype=torch.int32, device="cuda")
+            counter = torch.zeros(1, dtype=torch.int32, device="cuda")
+            ws, cap = self._own_ws(1)
+            envs.reset_all(torch.zeros(1, dtype=torch.int32, device="cuda"), ring)
+            envs.slot_next.fill_(1)
+            self._eval = (envs, ring, staging, counter, ws, cap)
+        envs, ring, staging, counter, ws, cap = self._eval
+        from .replay import pcg_state_from_generator
+
+        envs.pcg.copy_(torch.from_numpy(
+            pcg_state_from_generator(np.random.default_rng(seed)).view(np.int64)[None]).cuda())
+        envs.ep_count.zero_()
+        a = N.PqActArgs(
+            net=params.struct(), envs=envs.struct(), ring=ring.data_ptr(),
+            staging=staging.data_ptr(), step_counter=counter.data_ptr(), W=1, steps=256,
+            actions=hp.actions, episode_length=hp.episode_length, epoch_start=0,
+            frame_capacity=64, eps_start=epsilon, eps_end=epsilon, eps_anneal=1,
+            terminal_p=hp.terminal_p, q_out=None, ws=ws.data_ptr(), max_batch=cap,
+            max_episodes=episodes)
+        while int(envs.ep_count.item()) < episodes:
+            for _ in range(128):
+                N.check(lib.pq_act_step(N.C.byref(a), N.stream_ptr()), "eval step")
+        rets = envs.ep_ret[0, :episodes].cpu().numpy()
+        return float(rets.mean()), float(rets.std())
+
     def check_finite(self):
         v = int(self.nonfinite.item())
         if v != 2**31 - 1:
@@ -394,12 +449,14 @@ class DeviceRun:
         for e in range(hp.total_steps // hp.C):
             self.flush_and_merge()
             copy_into(self.target, self.theta)
+            self.maybe_eval(e * hp.C)
             self.run_epoch(e)
             self.torch.cuda.synchronize()
             self.check_finite()
             if self.hash_epochs:
                 self.record_epoch_hash((e + 1) * hp.C)
         self.flush_and_merge()
+        self.maybe_eval(hp.total_steps)
         self.finalize(wall0)
         return self.record
 
@@ -416,6 +473,14 @@ class DeviceRun:
         self.record.final_hash = theta_hash(self.theta)
         self.record.final_params = self.theta
         self.record.duration_s = time.perf_counter() - wall0
+
+
+def sequential_reference(hp: HyperParams, sink=None, **kw) -> RunRecord:
+    """The same arithmetic as run() in one lane, canonical order: per epoch all lockstep
+    blocks then the epoch's minibatches (executor.py:596-637).  The determinism oracle
+    of the concurrent device executor."""
+    kw.setdefault("use_graphs", False)
+    return DeviceRun(hp, sink, sequential=True, **kw).execute()
 
 
 def run(hp: HyperParams, sink=None, host_envs: bool = False, **kw) -> RunRecord:

@@ -304,3 +304,45 @@ def test_host_env_run_matches_device_env_run():
     r_host = run(hp, host_envs=True, graph_chunk=8)
     assert r_dev.epoch_hashes == r_host.epoch_hashes
     assert r_dev.to_csv_text() == r_host.to_csv_text()
+
+
+def test_concurrent_run_equals_sequential_reference():
+    """executor.run (two streams, graphs) reproduces the single-lane schedule
+    bit-exactly (pkg/tests/test_executor.py:94-108 oracle equivalence)."""
+    from paper_2111_01264_b200.executor import sequential_reference
+
+    hp = HyperParams(C=64, F=4, N=200, W=8, batch_size=32, total_steps=192, capacity=2000,
+                     schedule=EpsilonSchedule(1.0, 0.1, 100), episode_length=9, seed=11)
+    assert run(hp, graph_chunk=8).to_csv_text() == sequential_reference(hp).to_csv_text()
+
+
+def test_device_evaluation_matches_oracle_evaluate_policy():
+    """evaluate_policy (envs.py:177-202): exactly N episodes on one rng stream, same
+    returns as the oracle env driven by the same actions."""
+    hp = HyperParams(C=64, F=4, N=200, W=8, batch_size=32, total_steps=128, capacity=2000,
+                     eval_period=64, eval_episodes=5, eval_epsilon=0.3, episode_length=6,
+                     seed=2)
+    runner = DeviceRun(hp, use_graphs=False)
+    from paper_2111_01264_b200.executor import ROLE_EVAL, derived_seed
+    seed = derived_seed(hp.seed, ROLE_EVAL, 0)
+    mean, std = runner.evaluate(runner.target, hp.eval_epsilon, hp.eval_episodes, seed)
+    # oracle: the same env / stream; actions from the device Q rows via a single-state
+    # forward of each visited state
+    env = SyntheticFrameEnv(derived_seed(hp.seed, ROLE_EVAL, 1000), episode_length=6,
+                            action_count=A)
+    rng = np.random.default_rng(seed)
+    rets = []
+    for _ in range(hp.eval_episodes):
+        state = env.reset(rng)
+        total, done = 0.0, False
+        while not done:
+            q = dnn.forward(runner.target, state[None])[0]
+            st = OK.pcg_state_from_generator(rng)
+            act = OK.select_action(st, q, hp.eval_epsilon)
+            OK.pcg_state_to_generator(st, rng)
+            state, rew, done = env.step(act, rng)
+            total += rew
+        rets.append(total)
+    assert (mean, std) == (float(np.mean(rets)), float(np.std(rets)))
+    rec = run(hp, graph_chunk=8)
+    assert [k for _, k, _ in rec.events].count("eval_mean") == 2
