@@ -291,6 +291,35 @@ PQ_DEV U128 pcg_advance(U128 state, U128 inc, uint64_t delta) {
     return add128(mul128(acc_mult, state), acc_plus);
 }
 
+// ---------------------------------------------------------------- TMA (cp.async.bulk.tensor)
+// Tiled tensor loads into shared memory, completion counted in bytes on an mbarrier.
+// `map` is the generic address of a CUtensorMap in parameter / constant / global memory.
+PQ_DEV void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+PQ_DEV void tma_load_2d(uint32_t dst, const void *map, uint64_t *bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            dst),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+PQ_DEV void tma_load_3d(uint32_t dst, const void *map, uint64_t *bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            dst),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+PQ_DEV void tma_load_4d(uint32_t dst, const void *map, uint64_t *bar, int c0, int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+            dst),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+
 // ---------------------------------------------------------------- programmatic dependent launch
 // wait: block until the predecessor grid in the stream has completed (no-op when the
 // kernel was launched without the PDL attribute); launch: let the dependent grid start

@@ -49,7 +49,7 @@ struct FastDiv {
     uint64_t m;
     int d;
     FastDiv() = default;
-    __host__ FastDiv(int dd) : m(((1ull << 40) + (uint64_t)dd - 1) / (uint64_t)dd), d(dd) {}
+    __host__ __device__ FastDiv(int dd) : m(((1ull << 40) + (uint64_t)dd - 1) / (uint64_t)dd), d(dd) {}
     PQ_DEV int div(int x) const { return (int)(((uint64_t)(uint32_t)x * m) >> 40); }
 };
 
@@ -65,6 +65,7 @@ struct LoadCtx {
 // K loop; MN-major operands keep their column.
 struct LoadDense {  // bf16 row-major [rows][cols] with row stride ld (elements)
     static constexpr bool U8 = false, TABLE = false;
+    PQ_DEV void at_tile(int) {}
     const bf16 *p;
     int rows, cols, ld;
     struct Row {
@@ -88,6 +89,7 @@ struct LoadDense {  // bf16 row-major [rows][cols] with row stride ld (elements)
 // im2col over NHWC bf16 activations: row m = (b, oy, ox), col k = (kh, kw, c)
 struct LoadIm2col {
     static constexpr bool U8 = false, TABLE = false;
+    PQ_DEV void at_tile(int) {}
     const bf16 *x;
     int n, H, W, C, KS, S, OH, OW;
     FastDiv f_npix, f_ow, f_kc, f_c;
@@ -126,6 +128,7 @@ struct LoadIm2col {
 // optional device counter slices the map (graph replay of the epoch index table).
 struct LoadFrames {
     static constexpr bool U8 = true, TABLE = true;
+    PQ_DEV void at_tile(int) {}
     const uint8_t *ring;
     const int32_t *refs;
     const int64_t *map;
@@ -175,6 +178,7 @@ struct LoadFrames {
 // H x W layer input, col t = (kh, kw, o); reads dY[b, iy-kh, ix-kw, o] when in range.
 struct LoadTConv {
     static constexpr bool U8 = false, TABLE = false;
+    PQ_DEV void at_tile(int) {}
     const bf16 *dy;
     int n, H, W, OH, OW, O, KS;
     FastDiv f_npix, f_w, f_ko, f_o;
@@ -209,6 +213,7 @@ struct LoadTConv {
 // conv weight W[o][kh][kw][c] viewed as [t = (kh, kw, o)][c] (rows t, contiguous c)
 struct LoadWeightT {
     static constexpr bool U8 = false, TABLE = false;
+    PQ_DEV void at_tile(int) {}
     const bf16 *w;
     int O, KS, C;
     FastDiv f_ko, f_o;
@@ -239,6 +244,7 @@ struct LoadWeightT {
 // row m -> class = m / (tpc*128), local row = (b, iy', ix') with iy = 2 iy' + py.
 struct LoadTConvP {
     static constexpr bool U8 = false, TABLE = false;
+    PQ_DEV void at_tile(int) {}
     const bf16 *dy;
     int n, H2, W2, OH, OW, O, tpc;  // H2 = H / 2
     FastDiv f_per, f_npix, f_w2, f_o;
@@ -276,6 +282,8 @@ struct LoadWeightTP {
     const bf16 *w;
     int O, KS, C, tpc;
     FastDiv f_o;
+    int cls;  // parity class of the current tile (bound by at_tile)
+    PQ_DEV void at_tile(int m0) { cls = (m0 >> 7) / tpc; }
     struct Row {
         int off;
         bool ok;
@@ -286,7 +294,6 @@ struct LoadWeightTP {
     };
     PQ_DEV Row row(int t) const {
         if (t >= 4 * O) return {0, false};
-        int cls = blockIdx.x / tpc;
         int py = cls >> 1, px = cls & 1;
         int tap = f_o.div(t), o = t - tap * O;
         int kh = py + 2 * (tap >> 1), kw = px + 2 * (tap & 1);
@@ -298,6 +305,43 @@ struct LoadWeightTP {
         return bytes ? (const void *)(w + R.off + Cc.c) : (const void *)w;
     }
 };
+
+// loader factories (host or device: the multiply-shift divisors are computed here)
+#define PQ_HD __host__ __device__ inline
+PQ_HD LoadIm2col im2col(const bf16 *x, int n, int H, int W, int C, int KS, int S, int OH, int OW) {
+    LoadIm2col l{x, n, H, W, C, KS, S, OH, OW};
+    l.f_npix = FastDiv(OH * OW), l.f_ow = FastDiv(OW), l.f_kc = FastDiv(KS * C), l.f_c = FastDiv(C);
+    return l;
+}
+PQ_HD LoadTConv tconv(const bf16 *dy, int n, int H, int W, int OH, int OW, int O, int KS) {
+    LoadTConv l{dy, n, H, W, OH, OW, O, KS};
+    l.f_npix = FastDiv(H * W), l.f_w = FastDiv(W), l.f_ko = FastDiv(KS * O), l.f_o = FastDiv(O);
+    return l;
+}
+PQ_HD LoadWeightT weight_t(const bf16 *w, int O, int KS, int C) {
+    LoadWeightT l{w, O, KS, C};
+    l.f_ko = FastDiv(KS * O), l.f_o = FastDiv(O);
+    return l;
+}
+PQ_HD LoadTConvP tconv_p(const bf16 *dy, int n, int H2, int W2, int OH, int OW, int O, int tpc) {
+    LoadTConvP l{dy, n, H2, W2, OH, OW, O, tpc};
+    l.f_per = FastDiv(tpc * 128), l.f_npix = FastDiv(H2 * W2), l.f_w2 = FastDiv(W2), l.f_o = FastDiv(O);
+    return l;
+}
+PQ_HD LoadWeightTP weight_tp(const bf16 *w, int O, int KS, int C, int tpc) {
+    LoadWeightTP l{w, O, KS, C, tpc};
+    l.f_o = FastDiv(O);
+    l.cls = 0;
+    return l;
+}
+PQ_HD LoadFrames frames(const uint8_t *ring, const int32_t *refs, const int64_t *map,
+                        const int32_t *counter, int map_stride, int n, int ref_stride, int ref_off) {
+    LoadFrames l;
+    l.ring = ring, l.refs = refs, l.map = map, l.counter = counter, l.map_stride = map_stride;
+    l.n = n, l.ref_stride = ref_stride, l.ref_off = ref_off;
+    l.f400 = FastDiv(400), l.f20 = FastDiv(20);
+    return l;
+}
 
 // ------------------------------------------------------------------------ epilogues
 // apply(m, n0, v, cnt, split): tile row m (global), columns n0 .. n0+cnt-1
@@ -311,7 +355,7 @@ struct EpiBiasRelu {
     PQ_DEV void apply(int m, int n0, const float *v, int cnt, int) const {
         float bv[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) bv[e] = (e < cnt && n0 + e < N) ? __ldg(bias + n0 + e) : 0.f;
+        for (int e = 0; e < 32; ++e) bv[e] = (e < cnt && n0 + e < N) ? __ldcg(bias + n0 + e) : 0.f;
         if (m >= M) return;
         bf16 *dst = out + (size_t)m * ld;
 #pragma unroll
@@ -369,7 +413,7 @@ PQ_DEV void store_masked32(bf16 *dst, const bf16 *mask, const float *v, int nval
     uint4 mk[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-        mk[c] = c * 8 < nvalid ? __ldg(reinterpret_cast<const uint4 *>(mask + c * 8)) : make_uint4(0, 0, 0, 0);
+        mk[c] = c * 8 < nvalid ? __ldcg(reinterpret_cast<const uint4 *>(mask + c * 8)) : make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         if (c * 8 >= nvalid) break;
@@ -414,6 +458,11 @@ struct EpiMaskP {
         store_masked32(out + o, mask + o, v, min(cnt, C - n0));
     }
 };
+PQ_HD EpiMaskP epi_mask_p(bf16 *out, const bf16 *mask, int n, int H2, int W2, int C, int tpc) {
+    EpiMaskP e{out, mask, n, H2, W2, C, tpc};
+    e.f_per = FastDiv(tpc * 128), e.f_npix = FastDiv(H2 * W2), e.f_w2 = FastDiv(W2);
+    return e;
+}
 
 // data gradient of a swapped GEMM (D[feature][sample]): out[n][m] = acc * (mask[n][m] > 0)
 struct EpiMaskT {
@@ -449,6 +498,7 @@ struct EpiRms {
     float lr, rho, kappa;
     int M, N;
     int64_t pbase, sbase;
+    int upd;  // update id reported on a non-finite gradient when counter is NULL
     PQ_DEV void apply(int, int, const float *, int, int) const {}
     // tile: [128][ld] fp32, rows m0.., cols n0.. (width BN); 256 threads.  Rows are
     // walked by warps, lanes cover consecutive parameters (coalesced); 4 rows per
@@ -495,7 +545,7 @@ struct EpiRms {
                 }
             }
         }
-        if (bad) atomicMin(flag, counter ? *counter : 0);
+        if (bad) atomicMin(flag, counter ? *counter : upd);
     }
 };
 
@@ -535,22 +585,43 @@ struct GemmCfg {
     static constexpr int SMEM = STAGES * STAGE + 1024;
 };
 
-// PF: operand whose data never comes from the immediately preceding kernel (weights),
-// issued before griddepcontrol.wait so it lands while the predecessor drains
-// (0 = none, 1 = A, 2 = B).
-template <int BN, bool AMN, bool BMN, int ST, int PF, class LA, class LB, class EP>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
-    k_gemm(const __grid_constant__ GemmArgs<LA, LB, EP> g) {
+// Pipeline state a CTA carries from tile to tile: the operand ring (STAGES slots of
+// SLOT bytes at a 1024-aligned base), one MMA-completion mbarrier per slot and the
+// running K-chunk sequence number (chunk q lives in slot q % STAGES; its slot was last
+// used by chunk q - STAGES, whose barrier phase is (q / STAGES - 1) & 1).  A one-shot
+// kernel starts at seq 0; the persistent learner keeps counting across tiles, phases
+// and updates, so barriers are initialised once per launch.
+struct TileRing {
+    uint8_t *smem;
+    uint32_t smem_s;
+    uint64_t *bars;
+    uint32_t seq;
+    const uint32_t *tmem_s;  // TMEM accumulator base (shared memory, valid after a CTA sync)
+    int32_t *table;          // frame-slot table (LoadFrames operands)
+};
+
+struct NoHook {
+    PQ_DEV void operator()() const {}
+};
+
+// One 128 x BN output tile over K-chunks [kb0, kb1): operand gathers into the ring,
+// tcgen05.mma into TMEM, fused epilogue.  PF: operand whose data never comes from the
+// immediately preceding producer (weights), issued before hook() -- the one-shot
+// kernel's griddepcontrol.wait -- so it lands while the predecessor drains
+// (0 = none, 1 = A, 2 = B).  All 256 threads enter; returns with TMEM and the ring free.
+template <int BN, bool AMN, bool BMN, int STAGES, int SLOT, int PF, class LA, class LB, class EP,
+          class Hook>
+PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, int kb1, int m0, int n0,
+                      int split, int ones_at, int ones_extent, TileRing &R, const Hook &hook) {
     static_assert(BN == 16 || BN == 32 || BN == 64 || BN == 128 || BN == 256, "BN");
     static_assert(!BMN || BN >= 64, "MN-major B needs 64-wide swizzle atoms");
     static_assert(!LB::TABLE, "frame tables are A-operand only");
-    using Cfg = GemmCfg<BN, LA::U8, ST>;
-    constexpr int STAGES = Cfg::STAGES;
     static_assert(STAGES >= 2, "stages");
+    static_assert(GEMM_A_BYTES + BN * 128 + (LA::U8 ? 128 * 64 : 0) <= SLOT, "slot size");
+    constexpr int B_BYTES = BN * 128;
     // chunks in flight ahead of the MMA; refilling the slot of chunk i-2 (not i-1)
     // gives each MMA a full iteration to retire before its slot is reused
     constexpr int PRE = STAGES >= 4 ? STAGES - 2 : STAGES - 1;
-    constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
     constexpr uint32_t IDESC = idesc_bf16(BN, AMN, BMN);
     constexpr int NA = 1024 / GEMM_THREADS;                   // A chunks per thread (4)
     constexpr int BCH = BN * 8;                               // B chunks per stage
@@ -558,35 +629,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     constexpr int CPR = BN / 8;                               // MN-major B chunks per K row
     constexpr int BSTEP = BMN ? GEMM_THREADS / CPR : GEMM_THREADS / 8;  // K (resp. MN) rows per i
 
-    extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t bars[STAGES];
-    __shared__ uint32_t tmem_base_s;
-    __shared__ int32_t table[LA::TABLE ? TABLE_SAMPLES * 4 : 1];
-    uint8_t *smem = reinterpret_cast<uint8_t *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t smem_s = smem_u32(smem);
-
+    LA la = la_in;
+    LB lb = lb_in;
+    la.at_tile(m0);
+    lb.at_tile(m0);
+    uint8_t *smem = R.smem;
+    const uint32_t smem_s = R.smem_s;
+    const uint32_t seq0 = R.seq;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool tl = g_tl.on && tl_cta0() && tid == 0;
     int tl_i = 0;
     unsigned long long tl_t[12];
     if (tl) tl_t[tl_i++] = gtime();
-    const int grp = blockIdx.z / g.splits, split = blockIdx.z - grp * g.splits;
-    const LA la = g.a[grp];
-    const LB lb = g.b[grp];
-    const int m0 = blockIdx.x * 128, n0 = blockIdx.y * BN;
-    const int nk_total = (g.K + 63) >> 6;
-    const int kb0 = split * g.kc_per_split;
-    const int kb1 = min(nk_total, kb0 + g.kc_per_split);
     const int nk = kb1 > kb0 ? kb1 - kb0 : 0;
-
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
-        fence_mbar_init();
-    }
-    if (warp == 0) tmem_alloc<TMEM_COLS>(&tmem_base_s);
-    if (tl) tl_t[tl_i++] = gtime();  // 1: barriers + TMEM
-    LoadCtx cx{table, 0};
+    LoadCtx cx{R.table, 0};
 
     // fixed per-thread operand contexts
     const int a_c8 = AMN ? (tid & 15) : (tid & 7);      // fixed inner chunk
@@ -611,13 +667,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     } else {
         cb = lb.col(n0 + b_c8 * 8);
     }
-    const bool has_ones = AMN && g.ones_at >= m0 + a_c8 * 8 && g.ones_at < m0 + a_c8 * 8 + 8;
+    const bool has_ones = AMN && ones_at >= m0 + a_c8 * 8 && ones_at < m0 + a_c8 * 8 + 8;
 
+    // slot of local chunk i; before reuse, wait for the MMA of its previous occupant
+    auto slot_of = [&](int i) -> int { return (int)((seq0 + (uint32_t)i) % STAGES); };
+    auto slot_free = [&](int i) {
+        const uint32_t q = seq0 + (uint32_t)i;
+        if (q >= STAGES) mbar_wait(&R.bars[q % STAGES], ((q / STAGES) - 1) & 1);
+    };
     // issue the cp.async copies of K-chunk kb into ring slot s (A / B separately)
     auto issue_a = [&](int kb, int s) {
         const int k0 = kb * 64;
-        const uint32_t a_s = smem_s + s * Cfg::STAGE;
-        const uint32_t u_s = a_s + GEMM_A_BYTES + Cfg::B_BYTES;
+        const uint32_t a_s = smem_s + s * SLOT;
+        const uint32_t u_s = a_s + GEMM_A_BYTES + B_BYTES;
         typename LA::Col cak = AMN ? ca : la.col(k0 + a_c8 * 8);
 #pragma unroll
         for (int i = 0; i < NA; ++i) {
@@ -639,7 +701,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     auto issue_b = [&](int kb, int s) {
         if (!b_live) return;
         const int k0 = kb * 64;
-        const uint32_t b_s = smem_s + s * Cfg::STAGE + GEMM_A_BYTES;
+        const uint32_t b_s = smem_s + s * SLOT + GEMM_A_BYTES;
         typename LB::Col cbk = BMN ? cb : lb.col(k0 + b_c8 * 8);
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
@@ -655,8 +717,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // bf16 and write the bias-gradient "ones" element into its own chunk (if any)
     auto post = [&](int kb, int s) {
         if (!LA::U8 && !has_ones) return;
-        uint8_t *a_p = smem + s * Cfg::STAGE;
-        const uint8_t *u_p = a_p + GEMM_A_BYTES + Cfg::B_BYTES;
+        uint8_t *a_p = smem + s * SLOT;
+        const uint8_t *u_p = a_p + GEMM_A_BYTES + B_BYTES;
         const int k0 = kb * 64;
 #pragma unroll
         for (int i = 0; i < NA; ++i) {
@@ -667,22 +729,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 uint2 raw = *reinterpret_cast<const uint2 *>(u_p + q * 8);
                 *reinterpret_cast<uint4 *>(a_p + off) = u8x8_to_bf16(raw.x, raw.y);
             }
-            if (has_ones && k0 + r < g.ones_extent)
-                *reinterpret_cast<uint16_t *>(a_p + off + (g.ones_at - m0 - a_c8 * 8) * 2) = 0x3F80;
+            if (has_ones && k0 + r < ones_extent)
+                *reinterpret_cast<uint16_t *>(a_p + off + (ones_at - m0 - a_c8 * 8) * 2) = 0x3F80;
         }
     };
 
-    // weights (never written by the previous kernel) go out before the dependency wait
+    // weights (never written by the previous producer) go out before the dependency wait
 #pragma unroll
     for (int s = 0; s < PRE; ++s) {
-        if (s < nk) {
-            if (PF == 1) issue_a(kb0 + s, s);
-            if (PF == 2) issue_b(kb0 + s, s);
+        if (s < nk && PF != 0) {
+            slot_free(s);
+            if (PF == 1) issue_a(kb0 + s, slot_of(s));
+            if (PF == 2) issue_b(kb0 + s, slot_of(s));
         }
     }
-    griddep_wait();
-    griddep_launch();
-    if (tl) tl_t[tl_i++] = gtime();  // 2: predecessor done
+    hook();
+    if (tl) tl_t[tl_i++] = gtime();  // 1: predecessor done
     if constexpr (LA::TABLE) {
         // sample window of the rows this CTA reads: MN rows (K-major) or the split's
         // contraction range (MN-major)
@@ -690,32 +752,33 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int hi = AMN ? max(lo, kb1 * 64 - 1) : m0 + 127;
         cx.tb = lo / 400;
         int last = min(hi / 400, cx.tb + TABLE_SAMPLES - 1);
-        la.fill(cx.tb, last, table);
+        la.fill(cx.tb, last, R.table);
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = tmem_base_s;
+    const uint32_t tmem = *R.tmem_s;
 
-    if (tl) tl_t[tl_i++] = gtime();  // 3: contexts ready
+    if (tl) tl_t[tl_i++] = gtime();  // 2: contexts ready
 #pragma unroll
     for (int s = 0; s < PRE; ++s) {
         if (s < nk) {
-            if (PF != 1) issue_a(kb0 + s, s);
-            if (PF != 2) issue_b(kb0 + s, s);
+            if (PF == 0) slot_free(s);
+            if (PF != 1) issue_a(kb0 + s, slot_of(s));
+            if (PF != 2) issue_b(kb0 + s, slot_of(s));
         }
         cp_async_commit();
     }
-    if (tl) tl_t[tl_i++] = gtime();  // 4: prologue issued
+    if (tl) tl_t[tl_i++] = gtime();  // 3: prologue issued
     for (int i = 0; i < nk; ++i) {
-        const int s = i % STAGES;
+        const int s = slot_of(i);
         cp_async_wait<PRE - 1>();
         post(kb0 + i, s);
         fence_proxy_async_smem();
         __syncthreads();
         if (tid == 0) {
             tc_fence_after();
-            const uint32_t a_addr = smem_s + s * Cfg::STAGE;
+            const uint32_t a_addr = smem_s + s * SLOT;
             const uint32_t b_addr = a_addr + GEMM_A_BYTES;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -723,28 +786,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 uint64_t bd = BMN ? desc_sw128(b_addr + j * 2048, 8192) : desc_sw128(b_addr + j * 32, 0);
                 umma_bf16(tmem, ad, bd, IDESC, (i > 0 || j > 0) ? 1u : 0u);
             }
-            umma_commit(&bars[s]);
-            if (tl && (i == 0 || i == nk - 1)) tl_t[tl_i++] = gtime();  // 5, 6: first / last MMA issued
+            umma_commit(&R.bars[s]);
+            if (tl && (i == 0 || i == nk - 1)) tl_t[tl_i++] = gtime();  // 4, 5: first / last MMA issued
         }
         const int jn = i + PRE;
         if (jn < nk) {
-            const int sl = jn % STAGES;
-            if (jn >= STAGES) mbar_wait(&bars[sl], ((jn / STAGES) - 1) & 1);
+            const int sl = slot_of(jn);
+            slot_free(jn);
             issue_a(kb0 + jn, sl);
             issue_b(kb0 + jn, sl);
         }
         cp_async_commit();
     }
     if (nk > 0) {
-        const int last = nk - 1;
-        mbar_wait(&bars[last % STAGES], (last / STAGES) & 1);
+        const uint32_t q = seq0 + (uint32_t)(nk - 1);
+        mbar_wait(&R.bars[q % STAGES], (q / STAGES) & 1);
     }
+    R.seq = seq0 + (uint32_t)nk;
     tc_fence_after();
-    if (tl) tl_t[tl_i++] = gtime();  // 7: accumulator ready
+    if (tl) tl_t[tl_i++] = gtime();  // 6: accumulator ready
 
     // epilogue: warp w reads TMEM lanes 32*(w%4).. (tile rows); the two warpgroups
     // split the columns
-    const EP &ep = g.e[grp];
     const int wq = warp & 3, half = warp >> 2;
     const int row = m0 + wq * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
@@ -752,7 +815,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if constexpr (is_staged<EP>::value) {
         // park the accumulator tile in the (now idle) operand ring, then let the
         // epilogue walk it row-wise; row stride BN+1 keeps both passes conflict-free
-        static_assert(128 * (BN + 1) * 4 <= Cfg::STAGES * Cfg::STAGE, "staging tile");
+        static_assert(128 * (BN + 1) * 4 <= STAGES * SLOT, "staging tile");
         float *tile = reinterpret_cast<float *>(smem);
         if (BN >= 64 || half == 0) {
             const int cbeg = BN >= 64 ? half * CW : 0;
@@ -787,17 +850,52 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             ep.apply(row, n0 + c0, v, BN < 32 ? BN : 32, split);
         }
     }
+    // TMEM reads and ring reads are complete before anyone starts the next tile
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc<TMEM_COLS>(tmem);
     if (tl) {
-        tl_t[tl_i++] = gtime();  // 8: epilogue done
+        tl_t[tl_i++] = gtime();  // 7: epilogue done
         const int slot = atomicAdd(&g_tl.n, 1);
         if (slot < 256) {
             for (int k = 0; k < 12; ++k) g_tl.t[slot][k] = k < tl_i ? tl_t[k] : 0ull;
             g_tl.tag[slot] = (char)('a' + (BN >> 4) % 26);
         }
     }
+}
+
+struct GridDepHook {
+    PQ_DEV void operator()() const {
+        griddep_wait();
+        griddep_launch();
+    }
+};
+
+// One-shot kernel: one tile per CTA (grid x = M tiles, y = N tiles, z = group x split).
+template <int BN, bool AMN, bool BMN, int ST, int PF, class LA, class LB, class EP>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    k_gemm(const __grid_constant__ GemmArgs<LA, LB, EP> g) {
+    using Cfg = GemmCfg<BN, LA::U8, ST>;
+    constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t bars[Cfg::STAGES];
+    __shared__ uint32_t tmem_base_s;
+    __shared__ int32_t table[LA::TABLE ? TABLE_SAMPLES * 4 : 1];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int grp = blockIdx.z / g.splits, split = blockIdx.z - grp * g.splits;
+    const int nk_total = (g.K + 63) >> 6;
+    const int kb0 = split * g.kc_per_split;
+    const int kb1 = min(nk_total, kb0 + g.kc_per_split);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < Cfg::STAGES; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    if ((threadIdx.x >> 5) == 0) tmem_alloc<TMEM_COLS>(&tmem_base_s);
+    TileRing R{smem, smem_u32(smem), bars, 0u, &tmem_base_s, table};
+    gemm_tile<BN, AMN, BMN, Cfg::STAGES, Cfg::STAGE, PF>(g.a[grp], g.b[grp], g.e[grp], kb0, kb1,
+                                                        blockIdx.x * 128, blockIdx.y * BN, split,
+                                                        g.ones_at, g.ones_extent, R, GridDepHook{});
+    if ((threadIdx.x >> 5) == 0) tmem_dealloc<TMEM_COLS>(tmem_base_s);
 }
 
 template <int BN, bool AMN, bool BMN, int ST = 0, int PF = 0, class LA, class LB, class EP>

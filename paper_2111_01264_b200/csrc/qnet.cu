@@ -14,6 +14,7 @@
 
 #include "../../include/paraq_b200.h"
 #include "gemm.cuh"
+#include "learn_parts.cuh"
 #include "qnet.cuh"
 
 namespace pq {
@@ -99,50 +100,8 @@ struct FwdInput {  // frame-stack addressing of one group
 };
 
 
-// loader / epilogue constructors (host side precomputes the multiply-shift divisors)
-static LoadIm2col im2col(const bf16 *x, int n, int H, int W, int C, int KS, int S, int OH, int OW) {
-    LoadIm2col l{x, n, H, W, C, KS, S, OH, OW};
-    l.f_npix = FastDiv(OH * OW), l.f_ow = FastDiv(OW), l.f_kc = FastDiv(KS * C), l.f_c = FastDiv(C);
-    return l;
-}
-static LoadTConv tconv(const bf16 *dy, int n, int H, int W, int OH, int OW, int O, int KS) {
-    LoadTConv l{dy, n, H, W, OH, OW, O, KS};
-    l.f_npix = FastDiv(H * W), l.f_w = FastDiv(W), l.f_ko = FastDiv(KS * O), l.f_o = FastDiv(O);
-    return l;
-}
-static LoadWeightT weight_t(const bf16 *w, int O, int KS, int C) {
-    LoadWeightT l{w, O, KS, C};
-    l.f_ko = FastDiv(KS * O), l.f_o = FastDiv(O);
-    return l;
-}
-static LoadTConvP tconv_p(const bf16 *dy, int n, int H2, int W2, int OH, int OW, int O, int tpc) {
-    LoadTConvP l{dy, n, H2, W2, OH, OW, O, tpc};
-    l.f_per = FastDiv(tpc * 128), l.f_npix = FastDiv(H2 * W2), l.f_w2 = FastDiv(W2), l.f_o = FastDiv(O);
-    return l;
-}
-static LoadWeightTP weight_tp(const bf16 *w, int O, int KS, int C, int tpc) {
-    LoadWeightTP l{w, O, KS, C, tpc};
-    l.f_o = FastDiv(O);
-    return l;
-}
-static EpiMaskP epi_mask_p(bf16 *out, const bf16 *mask, int n, int H2, int W2, int C, int tpc) {
-    EpiMaskP e{out, mask, n, H2, W2, C, tpc};
-    e.f_per = FastDiv(tpc * 128), e.f_npix = FastDiv(H2 * W2), e.f_w2 = FastDiv(W2);
-    return e;
-}
-
 static LoadFrames frames_loader(const FwdInput &in, int n) {
-    LoadFrames l;
-    l.ring = in.ring;
-    l.refs = in.refs;
-    l.map = in.map;
-    l.counter = in.counter;
-    l.map_stride = in.map_stride;
-    l.n = n;
-    l.ref_stride = in.ref_stride;
-    l.ref_off = in.ref_off;
-    l.f400 = FastDiv(400), l.f20 = FastDiv(20);
-    return l;
+    return frames(in.ring, in.refs, in.map, in.counter, in.map_stride, n, in.ref_stride, in.ref_off);
 }
 
 static int choose_bn(int n) {
@@ -209,148 +168,11 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
 }
 
 // ------------------------------------------------------------------ head kernel
-struct HeadArgs {
-    const float *part[2];
-    const float *master[2];
-    int groups, n, A, n8;
-    const int32_t *records;
-    const int64_t *idx;       // sampled slots, or
-    const int64_t *idx_base;  // epoch table sliced by *counter
-    const int32_t *counter;
-    const float *ext_targets;
-    const int32_t *ext_actions;
-    float gamma;
-    int learner;
-    float *q_out;  // [groups][n][A]
-    float *h1, *dh1, *td;
-    bf16 *dh1_bf, *dh1T;
-    int32_t *act_out;
-    float *q_copy;  // optional extra copy [groups][n][A]
-    float *td_copy; // optional [n][3]
-};
-
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// fc1 split-K reduction + bias + ReLU into shared memory, fc2 with one warp per action,
-// and (learner) the TD target / error (agent.py:69-81, output_delta) and the fc2
-// back-prop through the fc1 ReLU mask (hidden_delta).  One 256-thread CTA per sample;
-// every global load of a phase is independent so they are all in flight together.
-constexpr int HEAD_THREADS = 256;
+// one 256-thread CTA per sample (learn_parts.cuh: head_sample)
 __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
-    const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     griddep_wait();
     griddep_launch();
-    __shared__ float hs[2][512];
-    __shared__ float qs[2][MAX_ACTIONS];
-    __shared__ float s_delta;
-    __shared__ int s_act;
-    // the sampled record (action, reward, terminal) is fetched early by thread 0
-    int4 rec_hi = make_int4(0, 0, 0, 0);
-    if (a.learner && tid == 0 && !a.ext_targets) {
-        int64_t slot = a.idx        ? a.idx[b]
-                       : a.idx_base ? a.idx_base[(int64_t)(*a.counter) * a.n + b]
-                                    : (int64_t)b;
-        rec_hi = *reinterpret_cast<const int4 *>(a.records + slot * REC_INTS + 4);
-    }
-    {
-        float v[2][2][FC1_SPLITS + 1];
-#pragma unroll
-        for (int g = 0; g < 2; ++g)
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const int j = tid + HEAD_THREADS * i;
-                const int gg = g < a.groups ? g : 0;
-                const float *P = a.part[gg] + (size_t)b * 512 + j;
-#pragma unroll
-                for (int sp = 0; sp < FC1_SPLITS; ++sp) v[g][i][sp] = P[(size_t)sp * a.n * 512];
-                v[g][i][FC1_SPLITS] = a.master[gg][P_B4 + j];
-            }
-#pragma unroll
-        for (int g = 0; g < 2; ++g)
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                float s = 0.f;
-#pragma unroll
-                for (int sp = 0; sp < FC1_SPLITS; ++sp) s += v[g][i][sp];
-                s += v[g][i][FC1_SPLITS];
-                hs[g][tid + HEAD_THREADS * i] = s > 0.f ? s : 0.f;
-            }
-    }
-    __syncthreads();
-    for (int g = 0; g < a.groups; ++g) {
-        const float *w5 = a.master[g] + P_W5;
-        float wv[4][16];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int aa = min(warp + 8 * u, a.A - 1);
-#pragma unroll
-            for (int t = 0; t < 16; ++t) wv[u][t] = w5[aa * 512 + lane + 32 * t];
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int aa = warp + 8 * u;
-            float acc = 0.f;
-#pragma unroll
-            for (int t = 0; t < 16; ++t) acc += wv[u][t] * hs[g][lane + 32 * t];
-            acc = warp_sum(acc);
-            if (lane == 0 && aa < a.A) {
-                float q = acc + a.master[g][p_b5(a.A) + aa];
-                qs[g][aa] = q;
-                a.q_out[((size_t)g * a.n + b) * a.A + aa] = q;
-                if (a.q_copy) a.q_copy[((size_t)g * a.n + b) * a.A + aa] = q;
-            }
-        }
-    }
-    if (!a.learner) return;
-    __syncthreads();
-    if (tid == 0) {
-        int act;
-        float target;
-        if (a.ext_targets) {
-            act = a.ext_actions[b];
-            target = a.ext_targets[b];
-        } else {
-            act = rec_hi.y;
-            const float r = __int_as_float(rec_hi.z);
-            if (rec_hi.w) {
-                target = r;
-            } else {
-                float mx = qs[1][0];
-                for (int aa = 1; aa < a.A; ++aa) mx = fmaxf(mx, qs[1][aa]);
-                target = r + a.gamma * mx;
-            }
-        }
-        float d = qs[0][act] - target;  // = n * output_delta (agent.py:103-104 summed gradient)
-        s_delta = d;
-        s_act = act;
-        a.act_out[b] = act;
-        a.td[b * 3 + 0] = target;
-        a.td[b * 3 + 1] = d;
-        a.td[b * 3 + 2] = 0.5f * d * d;
-        if (a.td_copy) {
-            a.td_copy[b * 3 + 0] = target;
-            a.td_copy[b * 3 + 1] = d;
-            a.td_copy[b * 3 + 2] = 0.5f * d * d;
-        }
-    }
-    __syncthreads();
-    const float d = s_delta;
-    const float *w5 = a.master[0] + P_W5 + (size_t)s_act * 512;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const int j = tid + HEAD_THREADS * i;
-        const float hv = hs[0][j];
-        const float g = hv > 0.f ? d * w5[j] : 0.f;  // hidden_delta with the fc1 ReLU mask
-        a.h1[(size_t)b * 512 + j] = hv;
-        a.dh1[(size_t)b * 512 + j] = g;
-        const bf16 gb = __float2bfloat16_rn(g);
-        a.dh1_bf[(size_t)b * 512 + j] = gb;
-        a.dh1T[(size_t)j * a.n8 + b] = gb;
-    }
+    head_sample<FC1_SPLITS>(a, blockIdx.x);
 }
 
 static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int learner,
@@ -374,36 +196,6 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
 }
 
 // ------------------------------------------------------------------ optimizer
-struct OptArgs {
-    const float *p, *m, *v;
-    float *p2, *m2, *v2;
-    bf16 *shadow;
-    const float *part1, *part2, *part3, *grad4;
-    int s1, s2, s3;
-    const float *dh1, *h1, *td;
-    const int32_t *act;
-    int n, A;
-    float lr, rho, kappa;
-    int32_t *flag;
-    int32_t *counter;  // update id source; incremented once per step by the last CTA
-    uint32_t *done;    // CTA completion counter for that increment
-    float *grad_out;
-    int64_t total;
-};
-
-__device__ __forceinline__ float sum_part(const float *part, int splits, size_t stride, size_t off) {
-    // up to 32 independent loads in flight per round; fixed (split-ascending) add order
-    float s = 0.f;
-    for (int q = 0; q < splits; q += 32) {
-        float v[32];
-#pragma unroll
-        for (int u = 0; u < 32; ++u) v[u] = q + u < splits ? part[(q + u) * stride + off] : 0.f;
-#pragma unroll
-        for (int u = 0; u < 32; ++u) s += v[u];
-    }
-    return s;
-}
-
 // last CTA of a grid bumps a device step counter (replaces a separate launch)
 __device__ __forceinline__ void last_block_bump(int32_t *counter, uint32_t *done) {
     __shared__ bool s_last;
@@ -420,89 +212,14 @@ __device__ __forceinline__ void last_block_bump(int32_t *counter, uint32_t *done
     }
 }
 
-// sum over the batch of f(b) with 8 samples' loads in flight (fixed add order)
-template <class F>
-__device__ __forceinline__ float batch_sum(int n, F f) {
-    float s = 0.f;
-    for (int b0 = 0; b0 < n; b0 += 16) {
-        float v[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) v[u] = b0 + u < n ? f(b0 + u) : 0.f;
-#pragma unroll
-        for (int u = 0; u < 16; ++u) s += v[u];
-    }
-    return s;
-}
-
-__device__ __forceinline__ float grad_of(const OptArgs &a, int64_t i, int64_t &sh) {
-    sh = -1;
-    if (i < P_B1) {
-        int o = (int)(i >> 8), k = (int)(i & 255);
-        sh = S_W1 + i;
-        return sum_part(a.part1, a.s1, 32 * 257, (size_t)o * 257 + k) * (1.0f / 255.0f);
-    }
-    if (i < P_W2) return sum_part(a.part1, a.s1, 32 * 257, (size_t)(i - P_B1) * 257 + 256);
-    if (i < P_B2) {
-        int64_t r = i - P_W2;
-        sh = S_W2 + r;
-        return sum_part(a.part2, a.s2, 64 * 513, (size_t)(r >> 9) * 513 + (r & 511));
-    }
-    if (i < P_W3) return sum_part(a.part2, a.s2, 64 * 513, (size_t)(i - P_B2) * 513 + 512);
-    if (i < P_B3) {
-        int64_t r = i - P_W3;
-        sh = S_W3 + r;
-        return sum_part(a.part3, a.s3, 64 * 577, (size_t)(r / 576) * 577 + (r % 576));
-    }
-    if (i < P_W4) return sum_part(a.part3, a.s3, 64 * 577, (size_t)(i - P_B3) * 577 + 576);
-    if (i < P_B4) {
-        sh = S_W4 + (i - P_W4);
-        return a.grad4[i - P_W4];
-    }
-    if (i < P_W5) {
-        const int j = (int)(i - P_B4);
-        return batch_sum(a.n, [&](int b) { return a.dh1[(size_t)b * 512 + j]; });
-    }
-    if (i < p_b5(a.A)) {
-        const int64_t r = i - P_W5;
-        const int aa = (int)(r >> 9), j = (int)(r & 511);
-        return batch_sum(a.n, [&](int b) {
-            const float x = a.td[b * 3 + 1] * a.h1[(size_t)b * 512 + j];
-            return a.act[b] == aa ? x : 0.f;
-        });
-    }
-    const int aa = (int)(i - p_b5(a.A));
-    return batch_sum(a.n, [&](int b) { return a.act[b] == aa ? a.td[b * 3 + 1] : 0.f; });
-}
-
-// centered RMSProp, kappa inside the square root (_kernels_numba.py:98-111)
-__device__ __forceinline__ void rms(const OptArgs &a, float g, float m, float v, float p,
-                                    float &m2, float &v2, float &p2) {
-    m2 = a.rho * m + (1.0f - a.rho) * g;
-    v2 = a.rho * v + (1.0f - a.rho) * g * g;
-    p2 = p - a.lr * g * rsqrtf(v2 - m2 * m2 + a.kappa);
-}
-
 // every parameter except fc1's weight (updated in the fc1 wgrad epilogue unless
-// a.grad4 is given), one parameter per thread
+// a.grad4 is given), one parameter per thread (learn_parts.cuh: opt_param)
 __global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
     griddep_wait();
     griddep_launch();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t i = a.grad4 ? t : (t < P_W4 ? t : P_B4 + (t - P_W4));
-    if (i < a.total) {
-        const int upd = a.counter ? *a.counter : 0;
-        const float m = a.m[i], v = a.v[i], p = a.p[i];
-        int64_t sh;
-        const float g = grad_of(a, i, sh);
-        float m2, v2, p2;
-        rms(a, g, m, v, p, m2, v2, p2);
-        a.m2[i] = m2;
-        a.v2[i] = v2;
-        a.p2[i] = p2;
-        if (sh >= 0) a.shadow[sh] = __float2bfloat16_rn(p2);
-        if (a.grad_out) a.grad_out[i] = g;
-        if (!isfinite(g)) atomicMin(a.flag, upd);
-    }
+    if (i < a.total) opt_param(a, i, a.counter ? *a.counter : 0);
     if (a.counter) last_block_bump(a.counter, a.done);
 }
 

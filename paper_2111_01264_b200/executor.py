@@ -157,13 +157,15 @@ class DeviceRun:
     """Shared state and epoch driver of one device run (executor.py:341-594)."""
 
     def __init__(self, hp: HyperParams, sink=None, use_graphs: bool = True, graph_chunk: int = 25,
-                 hash_epochs: bool = True, sequential: bool = False):
+                 hash_epochs: bool = True, sequential: bool = False, persistent: bool = True):
         hp.validate()
         if not hp.concurrent:
             raise NotImplementedError("the device executor implements the concurrent modes "
                                       "('both', 'concurrent')")
         torch = N.require_cuda()
         self.sequential = sequential
+        # persistent learner: the epoch's C/F learner steps in one launch (pq_learn_run)
+        self.persistent = persistent
         self.torch = torch
         self.hp = hp
         self.sink = sink
@@ -201,6 +203,9 @@ class DeviceRun:
         self.nonfinite = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
         self.act_ws, self.act_cap = self._own_ws(W)
         self.learn_ws, self.learn_cap = self._own_ws(B)
+        if persistent:
+            nbytes = N.load().pq_plearn_workspace_bytes(self.learn_cap, hp.actions)
+            self.plearn_ws = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
         self.act_stream = torch.cuda.Stream()
         self.learn_stream = torch.cuda.Stream()
         self.epoch_start = 0
@@ -247,6 +252,20 @@ class DeviceRun:
     def learn_step(self, stream=None):
         a = self._learn_args()
         N.check(N.load().pq_learn_step(N.C.byref(a), N.stream_ptr(stream)), "learn_step")
+
+    def learn_run(self, n_updates: int, stream=None):
+        """n_updates learner steps in one persistent launch (same counters and tables)."""
+        a = self._learn_args()
+        a.ws = self.plearn_ws.data_ptr()
+        N.check(N.load().pq_learn_run(N.C.byref(a), n_updates, N.stream_ptr(stream)), "learn_run")
+
+    def learn_epoch(self):
+        """All C/F learner steps of the epoch on the current stream."""
+        if self.persistent:
+            self.learn_run(self.updates)
+        else:
+            for _ in range(self.updates):
+                self.learn_step()
 
     def act_step(self, stream=None):
         a = self._act_args()
@@ -346,17 +365,15 @@ class DeviceRun:
             # sampler blocks, then the epoch's minibatches, on one stream
             for _ in range(self.steps):
                 self.act_step()
-            for _ in range(self.updates):
-                self.learn_step()
+            self.learn_epoch()
         elif self.use_graphs:
             self._replay_epoch()
         else:
+            with torch.cuda.stream(self.learn_stream):
+                self.learn_epoch()
             with torch.cuda.stream(self.act_stream):
                 for _ in range(self.steps):
                     self.act_step()
-            with torch.cuda.stream(self.learn_stream):
-                for _ in range(self.updates):
-                    self.learn_step()
         cur.wait_stream(self.act_stream)
         cur.wait_stream(self.learn_stream)
         self.staged = True
@@ -374,6 +391,13 @@ class DeviceRun:
         # t labels come from the run-global device block counter, so the same
         # captured graph serves every epoch
         ra, rl = self.steps // na, self.updates // nl
+        if self.persistent:
+            with torch.cuda.stream(self.learn_stream):
+                self.learn_run(self.updates)
+            with torch.cuda.stream(self.act_stream):
+                for _ in range(ra):
+                    ga.replay()
+            return
         ia = il = 0
         while ia < ra or il < rl:
             if ia < ra:
@@ -551,7 +575,10 @@ class HostEnvRun(DeviceRun):
         self.act_stream.wait_stream(cur)
         self.learn_stream.wait_stream(cur)
         # the learner's whole epoch is enqueued first
-        if self.use_graphs:
+        if self.persistent:
+            with torch.cuda.stream(self.learn_stream):
+                self.learn_run(self.updates)
+        elif self.use_graphs:
             gl, nl = self._graphs["learn"]
             with torch.cuda.stream(self.learn_stream):
                 for _ in range(self.updates // nl):
