@@ -159,8 +159,9 @@ size_t pq_plearn_workspace_bytes(int max_batch, int actions);
 int pq_learn_run(const pq_learn_args *args, int n_updates, void *stream);
 /* CTAs of the persistent learner (0 = SM count minus 20 kept for acting). */
 int pq_plearn_set_ctas(int ctas);
-/* Latency probe: device buffer u64 [phases][ctas][2] receiving, per phase and CTA, the
- * %globaltimer when its jobs finished and when the grid barrier released (NULL = off). */
+/* Latency probe: device buffer u64 [phases][ctas][4] receiving, per phase and CTA, the
+ * %globaltimer when its jobs finished, when the grid barrier released, the type of its
+ * last job and that job's duration in ns (NULL = off). */
 int pq_plearn_trace(unsigned long long *device_buf);
 /* GEMM-tile phase probes of the persistent learner's CTA 0 (layout of pq_timeline). */
 int pq_plearn_timeline(int on, unsigned long long *out, int *count);

@@ -320,6 +320,17 @@ PQ_DEV void tma_load_4d(uint32_t dst, const void *map, uint64_t *bar, int c0, in
         : "memory");
 }
 
+// 4 rows (row0..row3, any order, negative / past-the-end = zero-filled) x one box width of
+// a 2D tensor map whose box is {width, 1}: Blackwell tile::gather4.  The rows land at
+// consecutive box-row positions of dst (swizzled like a 4-row tile box).
+PQ_DEV void tma_gather4(uint32_t dst, const void *map, uint64_t *bar, int col, int r0, int r1, int r2, int r3) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+        "l"(map), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+        : "memory");
+}
+
 // ---------------------------------------------------------------- programmatic dependent launch
 // wait: block until the predecessor grid in the stream has completed (no-op when the
 // kernel was launched without the PDL attribute); launch: let the dependent grid start

@@ -501,32 +501,32 @@ struct EpiRms {
     int upd;  // update id reported on a non-finite gradient when counter is NULL
     PQ_DEV void apply(int, int, const float *, int, int) const {}
     // tile: [128][ld] fp32, rows m0.., cols n0.. (width BN); 256 threads.  Rows are
-    // walked by warps, lanes cover consecutive parameters (coalesced); 4 rows per
-    // round keep 3 x 4 x BN/32 loads in flight per thread.
+    // walked by warps, lanes cover consecutive parameters (coalesced); 4 rows per round
+    // keep 3 x 4 x BN/32 loads in flight per thread.
     template <int BN>
     PQ_DEV void apply_tile(const float *tile, int ld, int m0, int n0) const {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        constexpr int U = BN / 32;
+        constexpr int U = BN / 32, RR = 4;
         const float one_m_rho = 1.0f - rho;
         bool bad = false;
-        for (int r0 = warp; r0 < 128; r0 += 32) {
-            float mm[4][U], vv[4][U], pp[4][U];
-            int off[4][U];
+        for (int r0 = warp; r0 < 128; r0 += 8 * RR) {
+            float mm[RR][U], vv[RR][U], pp[RR][U];
+            int off[RR][U];
 #pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
+            for (int rr = 0; rr < RR; ++rr) {
                 const int r = r0 + rr * 8;
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int col = lane + 32 * u;
                     const bool ok = m0 + r < M && n0 + col < N;
                     off[rr][u] = ok ? (m0 + r) * N + n0 + col : -1;  // < 2^31 for fc1
-                    mm[rr][u] = ok ? m[pbase + off[rr][u]] : 0.f;
-                    vv[rr][u] = ok ? v[pbase + off[rr][u]] : 0.f;
-                    pp[rr][u] = ok ? p[pbase + off[rr][u]] : 0.f;
+                    mm[rr][u] = ok ? __ldcg(m + pbase + off[rr][u]) : 0.f;
+                    vv[rr][u] = ok ? __ldcg(v + pbase + off[rr][u]) : 0.f;
+                    pp[rr][u] = ok ? __ldcg(p + pbase + off[rr][u]) : 0.f;
                 }
             }
 #pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
+            for (int rr = 0; rr < RR; ++rr) {
                 const int r = r0 + rr * 8;
 #pragma unroll
                 for (int u = 0; u < U; ++u) {

@@ -157,14 +157,15 @@ class DeviceRun:
     """Shared state and epoch driver of one device run (executor.py:341-594)."""
 
     def __init__(self, hp: HyperParams, sink=None, use_graphs: bool = True, graph_chunk: int = 25,
-                 hash_epochs: bool = True, sequential: bool = False, persistent: bool = True):
+                 hash_epochs: bool = True, sequential: bool = False, persistent: bool = False):
         hp.validate()
         if not hp.concurrent:
             raise NotImplementedError("the device executor implements the concurrent modes "
                                       "('both', 'concurrent')")
         torch = N.require_cuda()
         self.sequential = sequential
-        # persistent learner: the epoch's C/F learner steps in one launch (pq_learn_run)
+        # persistent learner (experimental): the epoch's C/F learner steps in one launch
+        # (pq_learn_run); the default is the CUDA-graph path of one-shot kernels
         self.persistent = persistent
         self.torch = torch
         self.hp = hp

@@ -74,39 +74,31 @@ for _ in range(3):
 # per-phase trace of a few steps: max over CTAs of (jobs done - previous barrier release)
 G = int(sys.argv[3]) if len(sys.argv) > 3 else torch.cuda.get_device_properties(0).multi_processor_count - 20
 steps = 6
-nph = 4 + 10 * steps
-buf = torch.zeros(nph * G * 2, dtype=torch.int64, device="cuda")
+nph = 5 + 10 * steps
+buf = torch.zeros(nph * G * 4, dtype=torch.int64, device="cuda")
 N.load().pq_plearn_trace(buf.data_ptr())
 restore()
 r.learn_run(steps)
 torch.cuda.synchronize()
 N.load().pq_plearn_trace(None)
-t = buf.view(nph, G, 2).cpu().numpy().astype(np.int64)
+t = buf.view(nph, G, 4).cpu().numpy().astype(np.int64)
 rel = t[:, :, 1].min(axis=1)  # first barrier release per phase
 spread = t[:, :, 1].max(axis=1) - rel
 prev = np.concatenate([[t[0, :, 0].min()], rel[:-1]])
 work = t[:, :, 0].max(axis=1) - prev
 work_med = np.median(t[:, :, 0] - prev[:, None], axis=1)
 bar = rel - t[:, :, 0].max(axis=1)
-print("phase: work(max CTA) / work(median CTA) / last-arrival->release / release spread  [us]")
+JOBS = ["F1", "F2", "F3", "F4", "HEAD", "B4D", "OPT_FC2", "B3D", "B3W", "B4W", "B2D", "B2W", "OPT_C3",
+        "B1W", "OPT_C2", "OPT_C1", "G1"]
+print("phase: work(max CTA) / work(median CTA) / last-arrival->release / release spread [us] | slowest job types")
 for k in range(nph):
-    lab = f"pro{k}" if k < 4 else f"u{(k - 4) // 10}.P{(k - 4) % 10}"
-    print(f"{lab:>8}: {work[k] / 1e3:7.2f} {work_med[k] / 1e3:7.2f} {bar[k] / 1e3:6.2f} {spread[k] / 1e3:6.2f}")
+    lab = f"pro{k}" if k < 5 else f"u{(k - 5) // 10}.P{(k - 5) % 10}"
+    typ = t[k, :, 2]
+    dur = t[k, :, 3]
+    per = {}
+    for ty, d in zip(typ, dur):
+        if d > 0:
+            per.setdefault(JOBS[ty], []).append(d / 1e3)
+    desc = " ".join(f"{nm}:{np.median(v):.1f}/{max(v):.1f}" for nm, v in sorted(per.items(), key=lambda kv: -max(kv[1])))
+    print(f"{lab:>8}: {work[k] / 1e3:7.2f} {work_med[k] / 1e3:7.2f} {bar[k] / 1e3:6.2f} {spread[k] / 1e3:6.2f} | {desc}")
 
-# per-tile probes of CTA 0 (gemm_tile timeline): start, hook, ctx, prologue issued,
-# first MMA, last MMA, accumulator ready, epilogue done
-import ctypes
-lib = N.load()
-out = (ctypes.c_ulonglong * (256 * 12))()
-cnt = ctypes.c_int(0)
-restore()
-lib.pq_plearn_timeline(1, None, None)
-r.learn_run(3)
-torch.cuda.synchronize()
-lib.pq_plearn_timeline(0, ctypes.addressof(out), ctypes.addressof(cnt))
-tt = np.array(out).reshape(256, 12)[: cnt.value].astype(np.int64)
-print(f"{cnt.value} CTA-0 tiles; deltas in us: hook ctx prol mma0 mmaN acc epi | total")
-for row in tt:
-    n_ok = int((row > 0).sum())
-    d = np.diff(row[:n_ok]) / 1e3
-    print(" ".join(f"{x:6.2f}" for x in d), f"| {(row[n_ok - 1] - row[0]) / 1e3:6.2f}")
