@@ -285,6 +285,14 @@ struct TmaOp {
     }
 };
 
+// latency probe of CTA 0's tiles (pq_plearn_timeline): thread-0 timestamps in shared
+// memory, copied out at the end of the tile
+__shared__ unsigned long long s_tl[8];
+#define PL_PROBE(i)                                                 \
+    do {                                                            \
+        if (g_tl.on && blockIdx.x == 0 && threadIdx.x == 0) s_tl[i] = gtime(); \
+    } while (0)
+
 struct Pipe {
     uint8_t *smem;
     uint32_t smem_s;
@@ -304,6 +312,8 @@ PQ_DEV void tma_tile(const TmaOp &A, const TmaOp &B, const EP &ep, int kb0, int 
     const int nk = kb1 > kb0 ? kb1 - kb0 : 0;
     const uint32_t seq0 = P.seq;
     const uint32_t tmem = *P.tmem_s;
+    PL_PROBE(0);
+    if (g_tl.on && blockIdx.x == 0 && tid == 0) s_tl[2] = s_tl[3] = 0;
     if (warp == 0) {  // producer warp: lane 0 arms the slot, every lane may gather
         const uint32_t bytes = (uint32_t)(A.boxes + B.boxes) * PL_BOX;
         const bool any_gather = A.gather() || B.gather();
@@ -335,6 +345,7 @@ PQ_DEV void tma_tile(const TmaOp &A, const TmaOp &B, const EP &ep, int kb0, int 
         umma_commit(P.acc);
     }
     mbar_wait(P.acc, P.tiles & 1);
+    PL_PROBE(1);
     __syncwarp();
     tc_fence_after();
     P.seq = seq0 + nk;
@@ -366,6 +377,7 @@ PQ_DEV void tma_tile(const TmaOp &A, const TmaOp &B, const EP &ep, int kb0, int 
                 for (int q = 0; q < 4; ++q) d[q] = o[q];
             }
         }
+        PL_PROBE(2);
         // destination offsets of every (row, segment) once, then whole-chunk copies
         int32_t *dtab = reinterpret_cast<int32_t *>(P.smem + 128 * TS * 2);
         if (tid < 128) {
@@ -376,6 +388,7 @@ PQ_DEV void tma_tile(const TmaOp &A, const TmaOp &B, const EP &ep, int kb0, int 
             }
         }
         __syncthreads();
+        PL_PROBE(3);
         constexpr int CH = EP::ROW_CHUNKS;
         bf16 *base = ep.wsb;
 #pragma unroll 1
@@ -419,8 +432,18 @@ PQ_DEV void tma_tile(const TmaOp &A, const TmaOp &B, const EP &ep, int kb0, int 
             ep.apply(row, n0 + c0, v, 32, split);
         }
     }
+    PL_PROBE(4);
     tc_fence_before();
     __syncthreads();
+    if (g_tl.on && blockIdx.x == 0 && threadIdx.x == 0) {
+        s_tl[5] = gtime();
+        const int slot = atomicAdd(&g_tl.n, 1);
+        if (slot < 256) {
+            for (int k = 0; k < 6; ++k) g_tl.t[slot][k] = s_tl[k];
+            g_tl.t[slot][6] = (unsigned long long)nk;
+            g_tl.t[slot][7] = (unsigned long long)BN;
+        }
+    }
 }
 
 // ------------------------------------------------------------------ scatter epilogues

@@ -204,9 +204,7 @@ class DeviceRun:
         self.nonfinite = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
         self.act_ws, self.act_cap = self._own_ws(W)
         self.learn_ws, self.learn_cap = self._own_ws(B)
-        if persistent:
-            nbytes = N.load().pq_plearn_workspace_bytes(self.learn_cap, hp.actions)
-            self.plearn_ws = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+        self.plearn_ws = None  # persistent-learner workspace, allocated on first use
         self.act_stream = torch.cuda.Stream()
         self.learn_stream = torch.cuda.Stream()
         self.epoch_start = 0
@@ -256,6 +254,9 @@ class DeviceRun:
 
     def learn_run(self, n_updates: int, stream=None):
         """n_updates learner steps in one persistent launch (same counters and tables)."""
+        if self.plearn_ws is None:
+            nbytes = N.load().pq_plearn_workspace_bytes(self.learn_cap, self.hp.actions)
+            self.plearn_ws = self.torch.zeros(nbytes, dtype=self.torch.uint8, device="cuda")
         a = self._learn_args()
         a.ws = self.plearn_ws.data_ptr()
         N.check(N.load().pq_learn_run(N.C.byref(a), n_updates, N.stream_ptr(stream)), "learn_run")

@@ -102,3 +102,27 @@ for k in range(nph):
     desc = " ".join(f"{nm}:{np.median(v):.1f}/{max(v):.1f}" for nm, v in sorted(per.items(), key=lambda kv: -max(kv[1])))
     print(f"{lab:>8}: {work[k] / 1e3:7.2f} {work_med[k] / 1e3:7.2f} {bar[k] / 1e3:6.2f} {spread[k] / 1e3:6.2f} | {desc}")
 
+
+# per-tile probes of CTA 0: start, accumulator ready, staged, tables, copies done, synced
+import ctypes
+lib = N.load()
+out = (ctypes.c_ulonglong * (256 * 12))()
+cnt = ctypes.c_int(0)
+restore()
+lib.pq_plearn_timeline(1, None, None)
+r.learn_run(3)
+torch.cuda.synchronize()
+lib.pq_plearn_timeline(0, ctypes.addressof(out), ctypes.addressof(cnt))
+tt = np.array(out).reshape(256, 12)[: cnt.value].astype(np.int64)
+print(f"{cnt.value} CTA-0 tiles; us: mainloop(->acc) ->staged ->tables ->copies ->sync | nk BN")
+for row in tt:
+    ts = row[:6].astype(np.float64)
+    seg = []
+    prev = ts[0]
+    for k in range(1, 6):
+        if ts[k] > 0:
+            seg.append(f"{(ts[k] - prev) / 1e3:6.2f}")
+            prev = ts[k]
+        else:
+            seg.append("     -")
+    print(" ".join(seg), f"| {row[6]} {row[7]}")
