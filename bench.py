@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-sweeps", action="store_true",
+                    help="skip the learner-batch / acting-W sweeps and the DP learner line items")
+    ap.add_argument("--dp-batch", type=int, default=1024,
+                    help="global batch of the data-parallel learner measurement (configs[4])")
     return ap.parse_args()
 
 
@@ -259,6 +263,133 @@ def time_gather(runner, transitions: int = 80_000, reps: int = 10):
     return ms
 
 
+def learner_sweep(memory, actions: int, batches=(32, 64, 128, 256, 512, 1024), steps: int = 40):
+    """configs[4] sizes on one GPU: learner updates/s of the one-shot tcgen05 learner step
+    (eager launches, theta / opt updated in place) at each batch, and the achieved
+    tensor-core rate over the step (68.26 MFLOP per sample)."""
+    import ctypes
+
+    import torch
+    from paper_2111_01264_b200 import _native as N
+    from paper_2111_01264_b200 import nn as dnn
+
+    lib = N.load()
+    out = []
+    for B in batches:
+        theta = dnn.init_network(1, actions)
+        target = dnn.init_network(2, actions)
+        opt = dnn.OptState.zeros(theta)
+        ws, cap = dnn.workspace(B, actions)
+        flag = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
+        idx = torch.as_tensor(memory.sample_indices(B * (steps + 5), np.random.default_rng(B)), device="cuda")
+        a = N.PqLearnArgs(theta=theta.struct(), opt=opt.struct(), theta_out=theta.struct(), opt_out=opt.struct(),
+                          target=target.struct(), ring=memory.ring.data_ptr(), records=memory.records.data_ptr(),
+                          idx=None, idx_base=None, update_counter=None, ext_targets=None, ext_actions=None,
+                          n=B, actions=actions, gamma=0.99, lr=2.5e-4, rho=0.95, kappa=0.01,
+                          nonfinite=flag.data_ptr(), grad_out=None, q_out=None, td_out=None,
+                          ws=ws.data_ptr(), max_batch=cap)
+        st = N.stream_ptr()
+
+        def go(k):
+            a.idx = idx[k * B:(k + 1) * B].data_ptr()
+            N.check(lib.pq_learn_step(ctypes.byref(a), st), "learn_step")
+
+        for k in range(5):
+            go(steps + k)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for k in range(steps):
+            go(k)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        out.append({"batch": B, "updates_per_s": 1e3 / ms, "us_per_update": ms * 1e3,
+                    "tflops": FLOP_PER_SAMPLE_LEARN * B / (ms * 1e-3) / 1e12})
+    return out
+
+
+def act_sweep(actions: int, widths=(8, 32, 128, 512), reps: int = 50):
+    """configs[2]: batched Q inference over W synchronized env states (nn.forward on
+    theta-minus, tcgen05 conv/fc GEMMs + head): states/s and tensor-core rate
+    (18.70 MFLOP per state).  The env step / epsilon-greedy kernel is measured inside
+    the epoch bench (k_act_env)."""
+    import torch
+    from paper_2111_01264_b200 import _native as N
+    from paper_2111_01264_b200 import nn as dnn
+
+    lib = N.load()
+    net = dnn.init_network(3, actions)
+    out = []
+    for W in widths:
+        ring = torch.randint(0, 256, (4 * W, 84 * 84), dtype=torch.uint8, device="cuda")
+        refs = torch.arange(4 * W, dtype=torch.int32, device="cuda").view(W, 4)
+        q = torch.empty((W, actions), dtype=torch.float32, device="cuda")
+        ws, cap = dnn.workspace(W, actions)
+
+        def go():
+            N.check(lib.pq_forward(net.struct(), ring.data_ptr(), refs.data_ptr(), None, 4, 0, W, actions,
+                                   q.data_ptr(), ws.data_ptr(), cap, N.stream_ptr()), "forward")
+
+        for _ in range(5):
+            go()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            go()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        out.append({"W": W, "us_per_block": ms * 1e3, "states_per_s": W / (ms * 1e-3),
+                    "tflops": FLOP_PER_STATE_ACT * W / (ms * 1e-3) / 1e12})
+    return out
+
+
+def dp_learner(args, rank: int, world: int, dist, steps: int = 30):
+    """configs[4] across ranks: global batch args.dp_batch split over the ranks, shard
+    gradients sum-all-reduced over NCCL, identical RMSProp everywhere (dist.py).  All
+    ranks hold the same 100k-transition replay memory (same prepopulation seed) and
+    draw the same indices.  Returns updates/s of the whole job (max-over-ranks time)."""
+    import torch
+    from paper_2111_01264_b200 import nn as dnn
+    from paper_2111_01264_b200.dist import DataParallelLearner
+    from paper_2111_01264_b200.envs import FrameEnvSpec
+    from paper_2111_01264_b200.replay import ReplayMemory, device_pcg, sample_indices_device
+
+    B = args.dp_batch
+    mem = ReplayMemory(100_000)
+    mem.prepopulate(FrameEnvSpec(key=77), 100_000, np.random.default_rng(4))
+    theta = dnn.init_network(5)
+    target = dnn.init_network(6)
+    opt = dnn.OptState.zeros(theta)
+    lr = DataParallelLearner(theta, opt, target, mem, B, rank=rank, world_size=world)
+    pcg = device_pcg(np.random.default_rng(8))
+    idx = sample_indices_device(pcg, len(mem), B * (steps + 3))
+    for k in range(3):
+        lr.step(idx[(steps + k) * B:(steps + k + 1) * B])
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(steps):
+        lr.step(idx[k * B:(k + 1) * B])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    lr.check_finite()
+    ups = steps / (ms / 1e3)
+    return {"global_batch": B, "ranks": world, "per_rank_batch": lr.n, "updates_per_s": ups,
+            "samples_per_s": ups * B, "tflops": FLOP_PER_SAMPLE_LEARN * B * ups / 1e12,
+            "collective": "NCCL all-reduce (sum) of the 6.77 MB fp32 gradient per update"
+            if world > 1 else "none (1 rank)"}
+
+
 def run_b200(args, rank: int, world: int, local_rank: int):
     import torch
 
@@ -318,7 +449,14 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     # kernel-level measurements (outside the timed region; same inputs)
     learn_ms = time_kernel_isolated(runner)
     gather_ms = time_gather(runner)
+    sweeps = {}
+    if not args.no_sweeps and world == 1:
+        sweeps["learner_batch_sweep"] = learner_sweep(runner.D, hp.actions)
+        sweeps["acting_width_sweep"] = act_sweep(hp.actions)
     del runner
+    torch.cuda.empty_cache()
+    if not args.no_sweeps:
+        sweeps["dp_learner"] = dp_learner(args, rank, world, dist)
     torch.cuda.empty_cache()
     # end to end through the public API with host envs: H2D frames + D2H Q-rows per
     # lockstep block, theta hash D2H per epoch (the paper's CPU-env / GPU setting)
@@ -402,6 +540,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             "ms": gather_ms,
         },
         "gpu_launches": per_epoch_launches * args.steps,
+        **sweeps,
         "clocks": clk,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -148,6 +148,17 @@ typedef struct pq_learn_args {
  * TD error, backward, centered RMSProp on the summed gradient. */
 int pq_learn_step(const pq_learn_args *args, void *stream);
 
+/* Data-parallel learner (configs[4]): the summed gradient of this
+ * rank's shard of the batch (same forward / TD / backward as pq_learn_step, no update)
+ * into grad f32 [pq_num_params]; the ranks sum-all-reduce it (NCCL) and every rank
+ * applies the identical centered RMSProp with pq_rmsprop_apply (theta / opt in place,
+ * bf16 shadow refreshed, *nonfinite = min(update_id) on a non-finite gradient).
+ * agent.py:103-104 feeds the optimizer the summed gradient, so a sum of shard sums is
+ * the reference semantics (fp32 summation order aside). */
+int pq_learn_grad(const pq_learn_args *args, float *grad, void *stream);
+int pq_rmsprop_apply(pq_net theta, pq_opt opt, const float *grad, int actions, float lr, float rho,
+                     float kappa, int32_t *nonfinite, int update_id, void *stream);
+
 /* Persistent learner: n_updates consecutive learner steps of an epoch in ONE launch
  * (one CTA per SM minus an acting reserve, grid barriers between the step's phases).
  * Same arithmetic as n_updates pq_learn_step calls over idx_base sliced by

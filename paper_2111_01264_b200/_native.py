@@ -82,6 +82,9 @@ EXPORTS = {
                    C.c_int),
     "pq_learn_step": ([C.POINTER(PqLearnArgs), vp], C.c_int),
     "pq_act_step": ([C.POINTER(PqActArgs), vp], C.c_int),
+    "pq_learn_grad": ([C.POINTER(PqLearnArgs), vp, vp], C.c_int),
+    "pq_rmsprop_apply": ([PqNet, PqOpt, vp, C.c_int, C.c_float, C.c_float, C.c_float, vp, C.c_int, vp],
+                         C.c_int),
     "pq_plearn_workspace_bytes": ([C.c_int, C.c_int], C.c_size_t),
     "pq_learn_run": ([C.POINTER(PqLearnArgs), C.c_int, vp], C.c_int),
     "pq_plearn_set_ctas": ([C.c_int], C.c_int),

@@ -223,6 +223,41 @@ __global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
     if (a.counter) last_block_bump(a.counter, a.done);
 }
 
+// summed gradient of every parameter except fc1's weight (written by the fc1 wgrad GEMM)
+__global__ void __launch_bounds__(256) k_grad_only(const OptArgs a) {
+    griddep_wait();
+    griddep_launch();
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = t < P_W4 ? t : P_B4 + (t - P_W4);
+    if (i < a.total) {
+        int64_t sh;
+        a.grad_out[i] = grad_of(a, i, sh);
+    }
+}
+
+// centered RMSProp of every parameter from a gradient vector, bf16 shadow refresh,
+// non-finite flag (rmsprop_step, nn.py:173-203; _kernels_numba.py:98-111)
+__global__ void __launch_bounds__(256) k_rmsprop_apply(float *p, float *m, float *v, bf16 *shadow,
+                                                       const float *g, int64_t total, float lr, float rho,
+                                                       float kappa, int32_t *flag, int upd) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const float gi = g[i];
+    const float mi = rho * m[i] + (1.0f - rho) * gi;
+    const float vi = rho * v[i] + (1.0f - rho) * gi * gi;
+    const float pi = p[i] - lr * gi * rsqrtf(vi - mi * mi + kappa);
+    m[i] = mi;
+    v[i] = vi;
+    p[i] = pi;
+    int64_t sh = -1;
+    if (i < P_B1) sh = S_W1 + i;
+    else if (i >= P_W2 && i < P_B2) sh = S_W2 + (i - P_W2);
+    else if (i >= P_W3 && i < P_B3) sh = S_W3 + (i - P_W3);
+    else if (i >= P_W4 && i < P_B4) sh = S_W4 + (i - P_W4);
+    if (sh >= 0) shadow[sh] = __float2bfloat16_rn(pi);
+    if (!isfinite(gi) && flag) atomicMin(flag, upd);
+}
+
 static int choose_kc(int nchunks, int mtiles, int *splits, int kc_max = 1 << 30) {
     int kc = (nchunks * mtiles + 147) / 148;
     if (kc < 2) kc = 2;
@@ -254,7 +289,10 @@ static int get_fork(Fork **out) {
     return 0;
 }
 
-static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cudaStream_t st) {
+// grad_only != NULL: write the summed gradient of every parameter there instead of
+// updating theta / opt (the data-parallel learner all-reduces it, then pq_rmsprop_apply)
+static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cudaStream_t st,
+                               float *grad_only = nullptr) {
     const pq_net &th = la->theta;
     const bf16 *sh = (const bf16 *)th.shadow;
     int s1 = 1, s2 = 1, s3 = 1;
@@ -275,7 +313,14 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     PQ_CHECK(cudaEventRecord(fk->ev[1], st), "fork1");
     PQ_CHECK(cudaStreamWaitEvent(side, fk->ev[1], 0), "fork1 wait");
     PQ_CHECK(cudaStreamWaitEvent(side2, fk->ev[1], 0), "fork1 wait 2");
-    {  // B4w + RMSProp: dW4[j][k] = sum_b dh1[b][j] x3[b][k] (contraction over the batch),
+    if (grad_only) {  // B4w: dW4[j][k] = sum_b dh1[b][j] x3[b][k] -> grad (row-major = param order)
+        GemmArgs<LoadDense, LoadDense, EpiF32> g{};
+        g.a[0] = LoadDense{w.dh1T, 512, n, w.n8};
+        g.b[0] = LoadDense{w.act3[0], n, 3136, 3136};
+        g.e[0] = EpiF32{grad_only + P_W4, 512, 3136, 3136, 0};
+        g.M = 512, g.N = 3136, g.K = n, g.kc_per_split = (n + 63) / 64, g.splits = 1, g.ones_at = -1;
+        PQ_CHECK((launch_gemm<64, false, true, 4>(g, 1, side)), "fc1 wgrad");
+    } else {  // B4w + RMSProp: dW4[j][k] = sum_b dh1[b][j] x3[b][k] (contraction over the batch),
        // centered RMSProp applied in the epilogue (no fp32 gradient round trip)
         GemmArgs<LoadDense, LoadDense, EpiRms> g{};
         g.a[0] = LoadDense{w.dh1T, 512, n, w.n8};
@@ -348,6 +393,18 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     PQ_CHECK(cudaEventRecord(fk->ev[4], side2), "join 2");
     PQ_CHECK(cudaStreamWaitEvent(st, fk->ev[3], 0), "join wait");
     PQ_CHECK(cudaStreamWaitEvent(st, fk->ev[4], 0), "join wait 2");
+    if (grad_only) {
+        OptArgs o{};
+        o.part1 = w.part1, o.part2 = w.part2, o.part3 = w.part3;
+        o.s1 = s1, o.s2 = s2, o.s3 = s3;
+        o.dh1 = w.dh1, o.h1 = w.h1, o.td = w.td, o.act = w.act;
+        o.n = n, o.A = la->actions;
+        o.grad_out = grad_only;
+        o.total = n_params(la->actions);
+        const int64_t cnt = P_W4 + (o.total - P_B4);
+        PQ_CHECK(launch_k(k_grad_only, dim3((unsigned)((cnt + 255) / 256)), dim3(256), 0, st, o), "gradient");
+        return 0;
+    }
     {
         OptArgs o{};
         o.p = th.master, o.m = la->opt.m, o.v = la->opt.v;
@@ -494,6 +551,35 @@ int pq_learn_step(const pq_learn_args *la, void *stream) {
     rc = head(nets, groups, n, la->actions, w, 1, la, st);
     if (rc) return rc;
     return backward_and_update(la, n, w, st);
+}
+
+int pq_learn_grad(const pq_learn_args *la, float *grad, void *stream) {
+    const int n = la->n;
+    if (n < 1 || n > la->max_batch) return set_err("batch size out of range for the workspace");
+    if (la->actions < 1 || la->actions > MAX_ACTIONS) return set_err("actions must be in [1, 32]");
+    if (!grad) return set_err("gradient buffer required");
+    cudaStream_t st = (cudaStream_t)stream;
+    WS w = carve(la->ws, la->max_batch, la->actions);
+    const int64_t *map = la->idx ? la->idx : la->idx_base;
+    const int32_t *counter = la->idx ? nullptr : la->update_counter;
+    pq_net nets[2] = {la->theta, la->target};
+    FwdInput ins[2] = {{la->ring, la->records, map, counter, n, REC_INTS, 0},
+                       {la->ring, la->records, map, counter, n, REC_INTS, 1}};
+    const int groups = la->ext_targets ? 1 : 2;
+    int rc = forward_gemms(nets, ins, groups, n, w, st);
+    if (rc) return rc;
+    rc = head(nets, groups, n, la->actions, w, 1, la, st);
+    if (rc) return rc;
+    return backward_and_update(la, n, w, st, grad);
+}
+
+int pq_rmsprop_apply(pq_net theta, pq_opt opt, const float *grad, int actions, float lr, float rho,
+                     float kappa, int32_t *nonfinite, int update_id, void *stream) {
+    if (actions < 1 || actions > MAX_ACTIONS) return set_err("actions must be in [1, 32]");
+    const int64_t total = n_params(actions);
+    k_rmsprop_apply<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        theta.master, opt.m, opt.v, (bf16 *)theta.shadow, grad, total, lr, rho, kappa, nonfinite, update_id);
+    return cuda_err(cudaGetLastError(), "rmsprop_apply");
 }
 
 int pq_rmsprop_f32(const float *p, const float *g, const float *m, const float *v, int64_t n,

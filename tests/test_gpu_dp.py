@@ -1,0 +1,108 @@
+"""Data-parallel learner (configs[4]) and persistent learner on one GPU.
+
+The DP step's semantics are checked without a second GPU: the summed gradients of the
+shards of a batch ("virtual ranks" rank r of G, all on cuda:0) must add up to the
+summed gradient of the whole batch, and one DP update (shard gradients summed as the
+NCCL all-reduce would, then pq_rmsprop_apply) must equal the single-device learner
+step (agent.train_minibatch) up to fp32 summation order.  The per-sample forward rows
+are bit-identical whatever the batch composition (row independence, test_nn.py:117-124),
+so only the batch reductions of the weight gradients can differ: tolerance 1e-5
+relative.  The persistent learner (pq_learn_run) must reproduce the CUDA-graph learner
+step the same way."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2111_01264_b200 import nn as dnn  # noqa: E402
+from paper_2111_01264_b200.agent import EpsilonSchedule, HyperParams  # noqa: E402
+from paper_2111_01264_b200.dist import DataParallelLearner  # noqa: E402
+from paper_2111_01264_b200.envs import FrameEnvSpec  # noqa: E402
+from paper_2111_01264_b200.executor import DeviceRun  # noqa: E402
+from paper_2111_01264_b200.replay import ReplayMemory  # noqa: E402
+
+A = 18
+
+
+def rel(a, b):
+    a, b = a.double(), b.double()
+    return float((a - b).norm() / max(b.norm(), 1e-30))
+
+
+@pytest.fixture(scope="module")
+def memory():
+    mem = ReplayMemory(4096)
+    mem.prepopulate(FrameEnvSpec(key=11, terminal_p=1 / 64), 3000, np.random.default_rng(5))
+    return mem
+
+
+def fresh(seed=2):
+    theta = dnn.init_network(seed, A)
+    target = dnn.init_network(seed + 1, A)
+    return theta, dnn.OptState.zeros(theta), target
+
+
+@pytest.mark.parametrize("B,G", [(64, 2), (256, 4), (1024, 8), (33, 3)])
+def test_shard_gradients_sum_to_batch_gradient(memory, B, G):
+    idx = torch.as_tensor(memory.sample_indices(B, np.random.default_rng(B)), device="cuda")
+    theta, opt, target = fresh()
+    full = DataParallelLearner(theta, opt, target, memory, B).shard_gradient(idx).clone()
+    total = torch.zeros_like(full)
+    for r in range(G):
+        total += DataParallelLearner(theta, opt, target, memory, B, rank=r,
+                                     world_size=G).shard_gradient(idx)
+    assert torch.isfinite(full).all()
+    assert rel(total, full) < 1e-5
+
+
+@pytest.mark.parametrize("B", [64, 512])
+def test_dp_update_equals_single_device_step(memory, B):
+    idx = torch.as_tensor(memory.sample_indices(B, np.random.default_rng(7)), device="cuda")
+    theta, opt, target = fresh()
+    ref_theta, ref_opt, _, _, _ = dnn._learn(theta, opt, target, memory.ring, memory.records, idx, B)
+    G = 4
+    learners = [DataParallelLearner(theta.copy(), dnn.OptState(opt.m.clone(), opt.v.clone()), target,
+                                     memory, B, rank=r, world_size=G) for r in range(G)]
+    grad = sum(lr.shard_gradient(idx).clone() for lr in learners)   # the NCCL sum all-reduce
+    for lr in learners:
+        lr.apply(grad)
+        lr.check_finite()
+    torch.cuda.synchronize()
+    for lr in learners[1:]:   # every rank holds the identical update
+        assert torch.equal(lr.theta.master, learners[0].theta.master)
+    d_ref = ref_theta.master - theta.master
+    assert rel(learners[0].theta.master - theta.master, d_ref) < 1e-4
+    assert rel(learners[0].opt.v, ref_opt.v) < 1e-4
+    # the bf16 GEMM shadow follows the master
+    assert torch.equal(learners[0].theta.shadow[:8192],
+                       learners[0].theta.master[:8192].bfloat16().view(torch.int16))
+
+
+def test_persistent_learner_matches_graph_learner():
+    hp = HyperParams(C=1600, F=4, N=8000, W=8, batch_size=32, total_steps=1600, capacity=20000,
+                     seed=3, schedule=EpsilonSchedule(0.1, 0.1, 1))
+    r = DeviceRun(hp, use_graphs=False)
+    r.begin_epoch(0)
+    keep = [r.theta.master, r.theta.shadow, r.opt.m, r.opt.v, r.update_counter]
+    saved = [t.clone() for t in keep]
+    for steps in (1, 3):
+        for t, v in zip(keep, saved):
+            t.copy_(v)
+        for _ in range(steps):
+            r.learn_step()
+        one_shot = [t.clone() for t in keep]
+        for t, v in zip(keep, saved):
+            t.copy_(v)
+        r.learn_run(steps)
+        torch.cuda.synchronize()
+        assert int(r.update_counter.item()) == steps == int(one_shot[4].item())
+        d = one_shot[0] - saved[0]
+        # one step: fp32 split-K order only; three steps: plus rare bf16 ReLU-mask flips
+        assert rel(r.theta.master - saved[0], d) < (1e-5 if steps == 1 else 5e-2)
+        assert rel(r.opt.v, one_shot[3]) < (1e-5 if steps == 1 else 5e-2)
+    assert int(r.nonfinite.item()) == 2**31 - 1
