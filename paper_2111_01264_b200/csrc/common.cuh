@@ -320,6 +320,18 @@ PQ_DEV void tma_load_4d(uint32_t dst, const void *map, uint64_t *bar, int c0, in
         : "memory");
 }
 
+// im2col load of an NHWC tensor map (cuTensorMapEncodeIm2col): pixelsPerColumn pixels
+// from base pixel (n, h, w) walked W -> H -> N through the map's bounding box, each
+// contributing channelsPerPixel channels from c, at filter-tap offset (ow, oh).
+PQ_DEV void tma_im2col_4d(uint32_t dst, const void *map, uint64_t *bar, int c, int w, int h, int n, uint16_t ow,
+                          uint16_t oh) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+        "l"(map), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+        : "memory");
+}
+
 // 4 rows (row0..row3, any order, negative / past-the-end = zero-filled) x one box width of
 // a 2D tensor map whose box is {width, 1}: Blackwell tile::gather4.  The rows land at
 // consecutive box-row positions of dst (swizzled like a 4-row tile box).

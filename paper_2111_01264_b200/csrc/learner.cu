@@ -32,11 +32,11 @@
 //   P2 F3 online conv3            | F2 target (u+1) | fc1 wgrad+RMS (u-1)
 //   P3 F4 online fc1 (split-K)    | F3 target (u+1)
 //   P4 head (fc2, TD target, delta, fc2 back-prop) | F4 target (u+1)
-//   P5 fc1 dgrad                  | fc2 / fc1-bias RMSProp | frame gather online (u+1)
+//   P5 fc1 dgrad                  | fc2 / fc1-bias RMSProp | frame gather target (u+2)
 //   P6 conv3 dgrad, conv3 wgrad   | fc1 wgrad+RMS
 //   P7 conv2 dgrad, conv2 wgrad   | fc1 wgrad+RMS
 //   P8 conv1 wgrad                | fc1 wgrad+RMS
-//   P9 conv1/2/3 RMSProp          | frame gather target (u+2) | fc1 wgrad+RMS
+//   P9 conv1/2/3 RMSProp          | frame gather online (u+1) | fc1 wgrad+RMS
 // The arithmetic of each stage is the one-shot path's (same K order, epilogues, head and
 // optimizer functions); the two agree to fp32 split-K summation order.
 #include <cuda.h>
@@ -79,8 +79,9 @@ enum Map {
     M_W1 = 0, M_W2 = 2, M_W3 = 4, M_W4 = 6,  // [g]
     M_ACT3 = 8,                              // [g][par]
     M_P1 = 12,                               // [g][par]
-    M_P2 = 16, M_ACT2G = 18,                 // [g]  (ACT2G: row-gather map, box 64 x 1)
-    M_DY3G = 20, M_DY2G, M_DH1, M_DH1T, M_DY3, M_DY2, M_DY1, M_W3V, M_W2V, M_COUNT
+    M_P2 = 16, M_ACT2I = 18,                 // [g]  ACT2I: im2col map of act2, 128 pixels
+    M_ACT2W = 20,                            // im2col map of act2 (online), 64 pixels (wgrad)
+    M_DY3I, M_DY2I, M_ONES, M_DH1, M_DH1T, M_DY3, M_DY2, M_DY1, M_W3V, M_W2V, M_COUNT
 };
 
 struct Seg {
@@ -116,7 +117,8 @@ struct PLearnArgs {
     float *grad_out, *q_out, *td_out;  // optional (values of the last step)
     // workspace
     bf16 *wsb;  // base of the workspace (lowest buffer)
-    bf16 *act1, *act2[2], *act3[2][2];  // act2: n*81 rows + the constant ones row
+    bf16 *act1, *act2[2], *act3[2][2];
+    bf16 *ones;  // [64][64], column 0 = 1: the bias-gradient atom of the conv3 wgrad
     bf16 *P1[2][2], *P2[2];
     float *fc1part[2][2];
     float *q, *h1, *dh1, *td;
@@ -199,97 +201,80 @@ struct is_scatter<EP, decltype((void)EP::NDEST)> {
 };
 
 // ------------------------------------------------------------------ TMA GEMM tile
-// One operand of a K-chunk: `boxes` 64x64 boxes of a tensor map, or 128 rows gathered
-// from an NHWC activation / gradient by tile::gather4 (4 rows per lane of the producer
-// warp; rows outside the tensor or the tap's window are zero-filled):
+// One operand of a K-chunk: `boxes` 64x64 boxes of a tiled tensor map, or an im2col
+// load of an NHWC activation / gradient (hardware patch gather, zero padding):
 //   K2:  K-major rows r0 + 64b, columns 64 kb          (row-major [MN][K] matrix)
 //   M2:  MN-major columns r0 + 64b, rows 64 kb         (row-major [K][MN] matrix)
 //   W3V: conv3 weight as [c][(kh,kw)][o]: tap kb      (MN-major B of the conv3 dgrad)
 //   W2V: conv2 weight as [c][kw][kh][o]: tap of the parity class (conv2 dgrad)
-//   GF3: conv3 im2col of act2 (9x9x64 -> 7x7, tap kb = (kh, kw)), K-major rows m
-//   GT3: conv3 transposed-conv window of dY3 (7x7x64 -> 9x9), K-major rows m
-//   GT2: conv2 parity-class transposed-conv window of dY2 (9x9x64 -> 10x10 per class)
-//   GW3: conv3 im2col of act2 as the MN-major A of the conv3 weight gradient: K-chunk =
-//        64 output pixels, MN atoms = taps 2 mt, 2 mt + 1 (tap 9 = the ones row)
-enum { OP_K2, OP_M2, OP_W3V, OP_W2V, OP_GF3, OP_GT3, OP_GT2, OP_GW3 };
+//   IF3: conv3 forward patches of act2 (9x9x64 -> 7x7), 128 output pixels from r0, tap kb
+//   IT3: conv3 transposed-conv window of dY3 (7x7x64 -> 9x9, padding 2), tap kb
+//   IT2: conv2 parity-class transposed-conv window of dY2 (9x9x64 -> 10x10, padding 1)
+//   IW3: conv3 patches of act2 as the MN-major A of the conv3 weight gradient: K-chunk =
+//        64 output pixels from 64 kb, MN atoms = taps 2 mt, 2 mt + 1; tap 9 = the ones
+//        tile (bias gradient: column 0 = 1)
+enum { OP_K2, OP_M2, OP_W3V, OP_W2V, OP_IF3, OP_IT3, OP_IT2, OP_IW3 };
 struct TmaOp {
     const CUtensorMap *map;
     int kind, boxes, r0, cls, n;
-    PQ_DEV bool gather() const { return kind >= OP_GF3; }
-    // lane of the producer warp; box kinds issue from lane 0 only
+    const CUtensorMap *aux;  // IW3: the ones tile
     PQ_DEV void issue(uint32_t dst, uint64_t *bar, int kb, int lane) const {
-        if (!gather()) {
-            if (lane != 0) return;
-            if (kind == OP_K2) {
+        if (lane != 0) return;
+        switch (kind) {
+            case OP_K2:
                 for (int b = 0; b < boxes; ++b) tma_load_2d(dst + b * PL_BOX, map, bar, kb * 64, r0 + 64 * b);
-            } else if (kind == OP_M2) {
+                break;
+            case OP_M2:
                 for (int b = 0; b < boxes; ++b) tma_load_2d(dst + b * PL_BOX, map, bar, r0 + 64 * b, kb * 64);
-            } else if (kind == OP_W3V) {
+                break;
+            case OP_W3V:
                 tma_load_3d(dst, map, bar, 0, kb, 0);
-            } else {
+                break;
+            case OP_W2V: {
                 const int kh = (cls >> 1) + 2 * (kb >> 1), kw = (cls & 1) + 2 * (kb & 1);
                 tma_load_4d(dst, map, bar, 0, kw, kh, 0);
+                break;
             }
-            return;
-        }
-        int row[4];
-        uint32_t d;
-        if (kind == OP_GW3) {
-            const int atom = lane >> 4, t = 2 * (r0 >> 7) + atom;
-            const int kh = t / 3, kw = t - kh * 3;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int pix = kb * 64 + 4 * (lane & 15) + i;
-                int r = -1;
-                if (pix < n * 49) {
+            case OP_IF3: {  // output pixel r0 = (b, oy, ox) of 7x7; input base (ox, oy), tap offset
+                const int b = r0 / 49, q = r0 - b * 49, oy = q / 7, ox = q - oy * 7;
+                const int kh = kb / 3, kw = kb - kh * 3;
+                tma_im2col_4d(dst, map, bar, 0, ox, oy, b, (uint16_t)kw, (uint16_t)kh);
+                break;
+            }
+            case OP_IT3: {  // input pixel r0 = (b, iy, ix) of 9x9 reads dY3[iy - kh][ix - kw]
+                const int b = r0 / 81, q = r0 - b * 81, iy = q / 9, ix = q - iy * 9;
+                const int kh = kb / 3, kw = kb - kh * 3;
+                tma_im2col_4d(dst, map, bar, 0, ix - 2, iy - 2, b, (uint16_t)(2 - kw), (uint16_t)(2 - kh));
+                break;
+            }
+            case OP_IT2: {  // class-local row r0 = (b, iy', ix') of 10x10 reads dY2[iy' - ty][ix' - tx]
+                const int b = r0 / 100, q = r0 - b * 100, iy = q / 10, ix = q - iy * 10;
+                const int ty = kb >> 1, tx = kb & 1;
+                tma_im2col_4d(dst, map, bar, 0, ix - 1, iy - 1, b, (uint16_t)(1 - tx), (uint16_t)(1 - ty));
+                break;
+            }
+            default: {  // OP_IW3
+                const int p0 = kb * 64, b = p0 / 49, q = p0 - b * 49, oy = q / 7, ox = q - oy * 7;
+                for (int atom = 0; atom < 2; ++atom) {
+                    const int t = 2 * (r0 >> 7) + atom;
                     if (t < 9) {
-                        const int b = pix / 49, q = pix - b * 49, oy = q / 7, ox = q - oy * 7;
-                        r = b * 81 + (oy + kh) * 9 + ox + kw;
-                    } else if (t == 9) {
-                        r = n * 81;  // the constant ones row (bias gradient)
+                        const int kh = t / 3, kw = t - kh * 3;
+                        tma_im2col_4d(dst + atom * PL_BOX, map, bar, 0, ox, oy, b, (uint16_t)kw, (uint16_t)kh);
+                    } else {
+                        tma_load_2d(dst + atom * PL_BOX, aux, bar, 0, 0);
                     }
                 }
-                row[i] = r;
+                break;
             }
-            d = dst + atom * PL_BOX + (4 * (lane & 15)) * 128;
-        } else {
-            const int kh = kind == OP_GT2 ? (kb >> 1) : kb / 3;
-            const int kw = kind == OP_GT2 ? (kb & 1) : kb - (kb / 3) * 3;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int m = r0 + 4 * lane + i;
-                int r = -1;
-                if (kind == OP_GF3) {
-                    if (m < n * 49) {
-                        const int b = m / 49, q = m - b * 49, oy = q / 7, ox = q - oy * 7;
-                        r = b * 81 + (oy + kh) * 9 + ox + kw;
-                    }
-                } else if (kind == OP_GT3) {
-                    if (m < n * 81) {
-                        const int b = m / 81, q = m - b * 81, iy = q / 9, ix = q - iy * 9;
-                        const int oy = iy - kh, ox = ix - kw;
-                        if (oy >= 0 && oy < 7 && ox >= 0 && ox < 7) r = b * 49 + oy * 7 + ox;
-                    }
-                } else {  // OP_GT2: m is the row within the parity class
-                    if (m < n * 100) {
-                        const int b = m / 100, q = m - b * 100, iy = q / 10, ix = q - iy * 10;
-                        const int y = iy - kh, x = ix - kw;
-                        if (y >= 0 && y < 9 && x >= 0 && x < 9) r = b * 81 + y * 9 + x;
-                    }
-                }
-                row[i] = r;
-            }
-            d = dst + (4 * lane) * 128;
         }
-        tma_gather4(d, map, bar, 0, row[0], row[1], row[2], row[3]);
     }
 };
 
 // latency probe of CTA 0's tiles (pq_plearn_timeline): thread-0 timestamps in shared
 // memory, copied out at the end of the tile
 __shared__ unsigned long long s_tl[8];
-#define PL_PROBE(i)                                                 \
-    do {                                                            \
+#define PL_PROBE(i)                                                                \
+    do {                                                                           \
         if (g_tl.on && blockIdx.x == 0 && threadIdx.x == 0) s_tl[i] = gtime(); \
     } while (0)
 
@@ -316,14 +301,12 @@ PQ_DEV void tma_tile(const TmaOp &A, const TmaOp &B, const EP &ep, int kb0, int 
     if (g_tl.on && blockIdx.x == 0 && tid == 0) s_tl[2] = s_tl[3] = 0;
     if (warp == 0) {  // producer warp: lane 0 arms the slot, every lane may gather
         const uint32_t bytes = (uint32_t)(A.boxes + B.boxes) * PL_BOX;
-        const bool any_gather = A.gather() || B.gather();
         for (int i = 0; i < nk; ++i) {
             const uint32_t q = seq0 + i, s = q % PL_STAGES;
             if (lane == 0) {
                 if (q >= PL_STAGES) mbar_wait(&P.empty[s], ((q / PL_STAGES) - 1) & 1);
                 mbar_expect_tx(&P.full[s], bytes);
             }
-            if (any_gather) __syncwarp();
             const uint32_t dst = P.smem_s + s * PL_SLOT;
             A.issue(dst, &P.full[s], kb0 + i, lane);
             B.issue(dst + PL_B_OFF, &P.full[s], kb0 + i, lane);
@@ -622,7 +605,7 @@ struct Ctx {
 };
 
 PQ_DEV TmaOp op(const PLearnArgs &a, int map, int kind, int boxes, int r0, int cls = 0) {
-    return TmaOp{&a.maps[map], kind, boxes, r0, cls, a.n};
+    return TmaOp{&a.maps[map], kind, boxes, r0, cls, a.n, &a.maps[M_ONES]};
 }
 
 // conv1 patch rows of sample b (g = 0: state frames f0..f3, 1: next state f1..f4):
@@ -683,7 +666,7 @@ PQ_DEV void run_job(const Ctx &c, int type, int g, int uj, int j) {
                                        0, P);
             break;
         case J_F3:
-            tma_tile<64, false, false>(op(a, M_ACT2G + g, OP_GF3, 2, j * 128), op(a, M_W3 + g, OP_K2, 1, 0),
+            tma_tile<64, false, false>(op(a, M_ACT2I + g, OP_IF3, 2, j * 128), op(a, M_W3 + g, OP_K2, 1, 0),
                                        EpiConv3{a.wsb, a.act3[g][par], net.master + P_B3, n}, 0, 9,
                                        j * 128, 0, 0, P);
             break;
@@ -717,13 +700,13 @@ PQ_DEV void run_job(const Ctx &c, int type, int g, int uj, int j) {
             break;
         }
         case J_B3D:  // dY2 = relu'(x2) * transposed conv3(dY3): TP3 x W3 taps
-            tma_tile<64, false, true>(op(a, M_DY3G, OP_GT3, 2, j * 128), op(a, M_W3V, OP_W3V, 1, 0),
+            tma_tile<64, false, true>(op(a, M_DY3I, OP_IT3, 2, j * 128), op(a, M_W3V, OP_W3V, 1, 0),
                                       EpiB3D{a.wsb, a.dY2, a.act2[0], n}, 0, 9, j * 128, 0, 0, P);
             break;
         case J_B3W: {  // dW3^T[k][o] = sum_m P3[m][k] dY3[m][o]; column 576 = ones -> bias
             const int mt = j % 5, sp = j / 5;
             const int nch = (n * 49 + 63) / 64, kb0 = sp * a.kc3, kb1 = min(nch, kb0 + a.kc3);
-            tma_tile<64, true, true>(op(a, M_ACT2G, OP_GW3, 2, mt * 128), op(a, M_DY3, OP_M2, 1, 0),
+            tma_tile<64, true, true>(op(a, M_ACT2W, OP_IW3, 2, mt * 128), op(a, M_DY3, OP_M2, 1, 0),
                                      EpiF32T{a.part3, 577, 64, 577, (size_t)64 * 577}, kb0, kb1, mt * 128, 0, sp, P);
             break;
         }
@@ -742,7 +725,7 @@ PQ_DEV void run_job(const Ctx &c, int type, int g, int uj, int j) {
         }
         case J_B2D: {  // dY1 = relu'(x1) * transposed conv2(dY2), 4 input-parity classes
             const int tpc = counts_of(n).tpc, cls = j / tpc, loc = j - cls * tpc;
-            tma_tile<64, false, true>(op(a, M_DY2G, OP_GT2, 2, loc * 128), op(a, M_W2V, OP_W2V, 1, 0, cls),
+            tma_tile<64, false, true>(op(a, M_DY2I, OP_IT2, 2, loc * 128), op(a, M_W2V, OP_W2V, 1, 0, cls),
                                       EpiB2D{a.wsb, a.dY1, a.act1, n, tpc}, 0, 4, j * 128, 0, 0, P);
             break;
         }
@@ -869,16 +852,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_learn_persistent(const __gr
     if ((threadIdx.x >> 5) == 0) tmem_dealloc<64>(tmem_base_s);
 }
 
-// constant ones column / row of the online operands of the weight-gradient GEMMs
-// (bias gradients): P1 column 256, P2 column 512, act2 row n*81 = [1, 0, .., 0];
-// everything else never written stays zero from the allocation
-__global__ void k_plearn_ones(bf16 *P1a, bf16 *P1b, bf16 *P2, bf16 *act2, int n) {
+// constant ones of the online operands of the weight-gradient GEMMs (bias gradients):
+// P1 column 256, P2 column 512 and column 0 of the [64][64] ones tile; everything else
+// never written stays zero from the allocation
+__global__ void k_plearn_ones(bf16 *P1a, bf16 *P1b, bf16 *P2, bf16 *ones, int n) {
     const bf16 one = __float2bfloat16_rn(1.0f);
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n * 400; r += gridDim.x * blockDim.x) {
         P1a[(size_t)r * P1_LD + 256] = one;
         P1b[(size_t)r * P1_LD + 256] = one;
         if (r < n * 81) P2[(size_t)r * P2_LD + 512] = one;
-        if (r == 0) act2[(size_t)n * 81 * 64] = one;
+        if (r < 64) ones[r * 64] = one;
     }
 }
 
@@ -886,7 +869,8 @@ __global__ void k_plearn_ones(bf16 *P1a, bf16 *P1b, bf16 *P2, bf16 *act2, int n)
 static size_t al(size_t x) { return (x + 1023) & ~size_t(1023); }
 
 struct PWS {
-    bf16 *act1, *act2[2], *act3[2][2];  // act2: n*81 rows + the constant ones row
+    bf16 *act1, *act2[2], *act3[2][2];
+    bf16 *ones;  // [64][64], column 0 = 1: the bias-gradient atom of the conv3 wgrad
     bf16 *P1[2][2], *P2[2];
     float *fc1part[2][2];
     float *q, *h1, *dh1, *td;
@@ -910,7 +894,7 @@ static PWS carve_p(void *base, int N, int A) {
     const int n8 = (N + 7) & ~7;
     w.act1 = (bf16 *)take((size_t)N * 400 * 32 * 2);
     for (int g = 0; g < 2; ++g) {
-        w.act2[g] = (bf16 *)take(((size_t)N * 81 + 1) * 64 * 2);
+        w.act2[g] = (bf16 *)take((size_t)N * 81 * 64 * 2);
         for (int p = 0; p < 2; ++p) {
             w.act3[g][p] = (bf16 *)take((size_t)N * 3136 * 2);
             w.P1[g][p] = (bf16 *)take((size_t)N * 400 * P1_LD * 2);
@@ -928,6 +912,7 @@ static PWS carve_p(void *base, int N, int A) {
     w.dY3 = (bf16 *)take((size_t)N * 3136 * 2);
     w.dY2 = (bf16 *)take((size_t)N * 81 * 64 * 2);
     w.dY1 = (bf16 *)take((size_t)N * 400 * 32 * 2);
+    w.ones = (bf16 *)take(64 * 64 * 2);
     w.part1 = (float *)take((size_t)MAX_SPLITS * 32 * 257 * 4);
     w.part2 = (float *)take((size_t)MAX_SPLITS * 64 * 513 * 4);
     w.part3 = (float *)take((size_t)MAX_SPLITS * 64 * 577 * 4);
@@ -977,10 +962,36 @@ static int map2(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols, 
     const uint64_t dims[2] = {cols, rows}, st[1] = {ld};
     return make_map(m, base, 2, dims, st, what);
 }
-// [rows][64] bf16 matrix read one row per gather4 index
-static int map_rows(CUtensorMap *m, const void *base, uint64_t rows, const char *what) {
-    const uint64_t dims[2] = {64, rows}, st[1] = {64};
-    return make_map(m, base, 2, dims, st, what, 1);
+static PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col() {
+    static void *fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+    }
+    return reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(fn);
+}
+
+// im2col map of an NHWC bf16 tensor [n][H][W][64]: `pixels` pixels x 64 channels per
+// load; base pixels range over [lo, W-1+hi] x [lo, H-1+hi] (corners in W, H order)
+static int map_im2col(CUtensorMap *m, const void *base, int n, int H, int W, int lo, int hi, int pixels,
+                      const char *what) {
+    auto enc = encode_im2col();
+    if (!enc) return set_err("cuTensorMapEncodeIm2col unavailable (driver entry point)");
+    const cuuint64_t gd[4] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n};
+    const cuuint64_t gs[3] = {64 * 2, (cuuint64_t)W * 64 * 2, (cuuint64_t)H * W * 64 * 2};
+    const int lower[2] = {lo, lo}, upper[2] = {hi, hi};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), gd, gs, lower, upper, 64,
+                     (cuuint32_t)pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        char msg[160];
+        snprintf(msg, sizeof(msg), "im2col tensor map %s: CUresult %d", what, (int)r);
+        return set_err(msg);
+    }
+    return 0;
 }
 
 static int build_maps(PLearnArgs &a) {
@@ -996,10 +1007,12 @@ static int build_maps(PLearnArgs &a) {
             if (int rc = map2(&a.maps[M_P1 + 2 * g + p], a.P1[g][p], (uint64_t)n * 400, 257, P1_LD, "P1")) return rc;
         }
         if (int rc = map2(&a.maps[M_P2 + g], a.P2[g], (uint64_t)n * 81, 513, P2_LD, "P2")) return rc;
-        if (int rc = map_rows(&a.maps[M_ACT2G + g], a.act2[g], (uint64_t)n * 81 + 1, "act2 rows")) return rc;
+        if (int rc = map_im2col(&a.maps[M_ACT2I + g], a.act2[g], n, 9, 9, 0, -2, 128, "act2")) return rc;
     }
-    if (int rc = map_rows(&a.maps[M_DY3G], a.dY3, (uint64_t)n * 49, "dY3 rows")) return rc;
-    if (int rc = map_rows(&a.maps[M_DY2G], a.dY2, (uint64_t)n * 81, "dY2 rows")) return rc;
+    if (int rc = map_im2col(&a.maps[M_ACT2W], a.act2[0], n, 9, 9, 0, -2, 64, "act2 wgrad")) return rc;
+    if (int rc = map_im2col(&a.maps[M_DY3I], a.dY3, n, 7, 7, -2, 0, 128, "dY3")) return rc;
+    if (int rc = map_im2col(&a.maps[M_DY2I], a.dY2, n, 9, 9, -1, 0, 128, "dY2")) return rc;
+    if (int rc = map2(&a.maps[M_ONES], a.ones, 64, 64, 64, "ones")) return rc;
     if (int rc = map2(&a.maps[M_DH1], a.dh1_bf, n, 512, 512, "dh1")) return rc;
     if (int rc = map2(&a.maps[M_DH1T], a.dh1T, 512, n, a.n8, "dh1T")) return rc;
     if (int rc = map2(&a.maps[M_DY3], a.dY3, (uint64_t)n * 49, 64, 64, "dY3")) return rc;
@@ -1195,6 +1208,7 @@ int pq_learn_run(const pq_learn_args *la, int n_updates, void *stream) {
         }
         a.P2[g] = w.P2[g], a.act2[g] = w.act2[g];
     }
+    a.ones = w.ones;
     a.q = w.q, a.h1 = w.h1, a.dh1 = w.dh1, a.td = w.td, a.dh1_bf = w.dh1_bf, a.dh1T = w.dh1T, a.act = w.act;
     a.dY3 = w.dY3, a.dY2 = w.dY2, a.dY1 = w.dY1;
     a.part1 = w.part1, a.part2 = w.part2, a.part3 = w.part3;
@@ -1203,7 +1217,7 @@ int pq_learn_run(const pq_learn_args *la, int n_updates, void *stream) {
     if (int rc = build_maps(a)) return rc;
     build_plans(a, G);
     PQ_CUDA_TRY(cudaMemsetAsync(w.bar, 0, sizeof(unsigned), st));
-    k_plearn_ones<<<64, 256, 0, st>>>(w.P1[0][0], w.P1[0][1], w.P2[0], w.act2[0], n);
+    k_plearn_ones<<<64, 256, 0, st>>>(w.P1[0][0], w.P1[0][1], w.P2[0], w.ones, n);
     PQ_CUDA_TRY(cudaGetLastError());
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(G);
