@@ -72,6 +72,15 @@ PQ_DEV void mbar_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 
+PQ_DEV void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// barrier among `count` threads (multiple of 32) on hardware barrier `id` (1..15)
+PQ_DEV void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // generic-proxy smem writes -> visible to the async proxy (UMMA operand reads)
 PQ_DEV void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

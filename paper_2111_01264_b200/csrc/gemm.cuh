@@ -500,21 +500,26 @@ struct EpiRms {
     int64_t pbase, sbase;
     int upd;  // update id reported on a non-finite gradient when counter is NULL
     PQ_DEV void apply(int, int, const float *, int, int) const {}
-    // tile: [128][ld] fp32, rows m0.., cols n0.. (width BN); 256 threads.  Rows are
-    // walked by warps, lanes cover consecutive parameters (coalesced); 4 rows per round
-    // keep 3 x 4 x BN/32 loads in flight per thread.
+    // tile: [128][ld] fp32, rows m0.., cols n0.. (width BN).  Rows are walked by warps,
+    // lanes cover consecutive parameters (coalesced); 32 / NW rows per round keep
+    // 3 x (32 / NW) x BN/32 loads in flight per thread.
     template <int BN>
     PQ_DEV void apply_tile(const float *tile, int ld, int m0, int n0) const {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        constexpr int U = BN / 32, RR = 4;
+        apply_tile_w<BN, 8>(tile, ld, m0, n0, threadIdx.x >> 5);
+    }
+    // the same walk by NW warps (warp = 0..NW-1 of the participating warps)
+    template <int BN, int NW>
+    PQ_DEV void apply_tile_w(const float *tile, int ld, int m0, int n0, int warp) const {
+        const int lane = threadIdx.x & 31;
+        constexpr int U = BN / 32, RR = 32 / NW;
         const float one_m_rho = 1.0f - rho;
         bool bad = false;
-        for (int r0 = warp; r0 < 128; r0 += 8 * RR) {
+        for (int r0 = warp; r0 < 128; r0 += NW * RR) {
             float mm[RR][U], vv[RR][U], pp[RR][U];
             int off[RR][U];
 #pragma unroll
             for (int rr = 0; rr < RR; ++rr) {
-                const int r = r0 + rr * 8;
+                const int r = r0 + rr * NW;
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int col = lane + 32 * u;
@@ -527,7 +532,7 @@ struct EpiRms {
             }
 #pragma unroll
             for (int rr = 0; rr < RR; ++rr) {
-                const int r = r0 + rr * 8;
+                const int r = r0 + rr * NW;
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int o = off[rr][u];

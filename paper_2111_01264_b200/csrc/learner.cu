@@ -1134,6 +1134,326 @@ static void build_plans(PLearnArgs &a, int G) {
     if (next < total) ls.add(9, J_B4W, 0, 0, 1, next, total);
 }
 
+// ================================================================== one-shot TMA GEMMs
+// The learner-step GEMMs of the CUDA-graph path (qnet.cu) on the TMA engine: one CTA per
+// SM loops over the output tiles of ONE GEMM (up to 2 parameter groups), keeping its
+// TMEM, ring and barriers across tiles; operands as TmaOp (tiled boxes / im2col).
+template <class EP>
+struct TmaGemm {
+    CUtensorMap a[2], b[2], aux;
+    EP ep[2];
+    int kindA, kindB, boxesA, boxesB;
+    int n, tpc;
+    int mtiles, ntiles, splits, groups;
+    int kc, nk;       // K-chunks per split, total K-chunks
+    int b_is_weight;  // B never comes from the preceding kernel: prefetched before the PDL wait
+};
+
+// Warp-specialised persistent tile loop (one CTA per SM):
+//   warp 0      producer: streams every tile's operand boxes into the 6-slot ring,
+//               running ahead across tile boundaries (slot reuse gated by `empty`);
+//   warp 1      MMA issuer: alternates two 64-column TMEM accumulators; tile i waits
+//               until the epilogue released the buffer of tile i-2 (`acce`), commits
+//               each slot back to the producer and the finished accumulator (`accf`);
+//   warps 4-7   epilogue: TMEM lane quadrant w-4 = tile rows 32(w-4).., read the
+//               accumulator into registers, release it, then apply the fused epilogue
+//               (staged epilogues use a dedicated 33 KB shared tile, not the ring),
+// so tile t's epilogue overlaps tile t+1's loads and MMAs.
+constexpr int TG_STAGES = 6;
+constexpr int TG_STAGE_TILE = 128 * 65 * 4;  // fp32 staging tile of EpiRms (BN = 64)
+constexpr int TG_SMEM = TG_STAGES * PL_SLOT + TG_STAGE_TILE + 1024;
+
+template <class EP>
+PQ_DEV void tg_decode(const TmaGemm<EP> &g, int t, int BN, TmaOp &A, TmaOp &B, int &kb0, int &kb1, int &m0,
+                      int &n0, int &sp, int &grp) {
+    const int per_grp = g.mtiles * g.ntiles * g.splits;
+    grp = t / per_grp;
+    const int r = t - grp * per_grp;
+    const int mt = r % g.mtiles, r2 = r / g.mtiles, nt = r2 % g.ntiles;
+    sp = r2 / g.ntiles;
+    int r0 = mt * 128, cls = 0;
+    if (g.kindA == OP_IT2) {  // class-major tiles: tpc tiles per input-parity class
+        cls = mt / g.tpc;
+        r0 = (mt - cls * g.tpc) * 128;
+    }
+    A = TmaOp{&g.a[grp], g.kindA, g.boxesA, r0, cls, g.n, &g.aux};
+    B = TmaOp{&g.b[grp], g.kindB, g.boxesB, nt * BN, cls, g.n, &g.aux};
+    kb0 = sp * g.kc;
+    kb1 = min(g.nk, kb0 + g.kc);
+    m0 = mt * 128;
+    n0 = nt * BN;
+}
+
+template <int BN, bool AMN, bool BMN, class EP>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_tma_gemm(const __grid_constant__ TmaGemm<EP> g) {
+    static_assert(BN == 64, "the one-shot TMA GEMMs use 64-column accumulators");
+    constexpr uint32_t IDESC = idesc_bf16(BN, AMN, BMN);
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t full[TG_STAGES], empty[TG_STAGES], accf[2], acce[2];
+    __shared__ uint32_t tmem_base_s;
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t smem_s = smem_u32(smem);
+    float *stage_tile = reinterpret_cast<float *>(smem + TG_STAGES * PL_SLOT);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < TG_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&accf[b], 1);
+            mbar_init(&acce[b], 4);  // one arrival per epilogue warp
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<128>(&tmem_base_s);
+    if (tid < 2 * g.groups) {
+        const CUtensorMap *m = (tid & 1) ? &g.b[tid >> 1] : &g.a[tid >> 1];
+        asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const int total = g.mtiles * g.ntiles * g.splits * g.groups;
+    // weights (never written by the preceding kernel) of the first tile's first chunks
+    // are requested before the dependency wait, so they land while the predecessor drains
+    int pre = 0;
+    if (tid == 0 && g.b_is_weight && (int)blockIdx.x < total) {
+        TmaOp A, B;
+        int kb0, kb1, m0, n0, sp, grp;
+        tg_decode(g, blockIdx.x, BN, A, B, kb0, kb1, m0, n0, sp, grp);
+        const uint32_t bytes = (uint32_t)(A.boxes + B.boxes) * PL_BOX;
+        for (int kb = kb0; kb < kb1 && pre < TG_STAGES; ++kb, ++pre) {
+            mbar_expect_tx(&full[pre], bytes);
+            B.issue(smem_s + pre * PL_SLOT + PL_B_OFF, &full[pre], kb, 0);
+        }
+    }
+    griddep_wait();
+    griddep_launch();
+    if (warp == 0) {
+        if (lane == 0) {  // producer
+            uint32_t q = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                TmaOp A, B;
+                int kb0, kb1, m0, n0, sp, grp;
+                tg_decode(g, t, BN, A, B, kb0, kb1, m0, n0, sp, grp);
+                const uint32_t bytes = (uint32_t)(A.boxes + B.boxes) * PL_BOX;
+                for (int kb = kb0; kb < kb1; ++kb, ++q) {
+                    const uint32_t s = q % TG_STAGES;
+                    const uint32_t dst = smem_s + s * PL_SLOT;
+                    if ((int)q < pre) {  // B already requested (and the slot armed) before the wait
+                        A.issue(dst, &full[s], kb, 0);
+                        continue;
+                    }
+                    if (q >= TG_STAGES) mbar_wait(&empty[s], ((q / TG_STAGES) - 1) & 1);
+                    mbar_expect_tx(&full[s], bytes);
+                    A.issue(dst, &full[s], kb, 0);
+                    B.issue(dst + PL_B_OFF, &full[s], kb, 0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            uint32_t q = 0, it = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+                TmaOp A, B;
+                int kb0, kb1, m0, n0, sp, grp;
+                tg_decode(g, t, BN, A, B, kb0, kb1, m0, n0, sp, grp);
+                const uint32_t buf = it & 1;
+                if (it >= 2) mbar_wait(&acce[buf], ((it >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t acc = tmem + buf * BN;
+                for (int kb = kb0; kb < kb1; ++kb, ++q) {
+                    const uint32_t s = q % TG_STAGES;
+                    mbar_wait(&full[s], (q / TG_STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_s + s * PL_SLOT, b_addr = a_addr + PL_B_OFF;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint64_t ad =
+                            AMN ? desc_sw128(a_addr + j * 2048, 8192) : desc_sw128(a_addr + j * 32, 0);
+                        const uint64_t bd =
+                            BMN ? desc_sw128(b_addr + j * 2048, 8192) : desc_sw128(b_addr + j * 32, 0);
+                        umma_bf16(acc, ad, bd, IDESC, (kb > kb0 || j > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&accf[buf]);
+            }
+        }
+    } else if (warp >= 4) {  // epilogue
+        const int wq = warp - 4;
+        uint32_t it = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+            TmaOp A, B;
+            int kb0, kb1, m0, n0, sp, grp;
+            tg_decode(g, t, BN, A, B, kb0, kb1, m0, n0, sp, grp);
+            const uint32_t buf = it & 1;
+            mbar_wait(&accf[buf], (it >> 1) & 1);
+            __syncwarp();
+            tc_fence_after();
+            float v[2][32];
+            const uint32_t trow = tmem + buf * BN + ((uint32_t)(wq * 32) << 16);
+            if (kb1 > kb0) {
+                tmem_ld32(trow, v[0]);
+                tmem_ld32(trow + 32, v[1]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) v[0][e] = v[1][e] = 0.f;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acce[buf]);
+            const EP &ep = g.ep[grp];
+            const int row = m0 + wq * 32 + lane;
+            if constexpr (is_staged<EP>::value) {
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) stage_tile[(wq * 32 + lane) * (BN + 1) + c * 32 + e] = v[c][e];
+                named_bar_sync(1, 128);
+                ep.template apply_tile_w<BN, 4>(stage_tile, BN + 1, m0, n0, wq);
+                named_bar_sync(1, 128);
+            } else {
+                ep.apply(row, n0, v[0], 32, sp);
+                ep.apply(row, n0 + 32, v[1], 32, sp);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<128>(tmem);
+}
+
+static int g_sms = 0;
+template <int BN, bool AMN, bool BMN, class EP>
+static int launch_tma(const TmaGemm<EP> &g, cudaStream_t st, const char *what) {
+    auto kern = k_tma_gemm<BN, AMN, BMN, EP>;
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        PQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TG_SMEM));
+        configured = true;
+    }
+    if (!g_sms) {
+        int dev = 0;
+        PQ_CUDA_TRY(cudaGetDevice(&dev));
+        PQ_CUDA_TRY(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int total = g.mtiles * g.ntiles * g.splits * g.groups;
+    return cuda_err(launch_k(kern, dim3(std::min(total, g_sms)), dim3(GEMM_THREADS), TG_SMEM, st, g), what);
+}
+
+// the [64][64] ones tile (column 0 = 1): bias-gradient atom of the conv3 wgrad
+__global__ void k_ones_tile(bf16 *t) {
+    for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) t[i] = __float2bfloat16_rn((i & 63) == 0 ? 1.f : 0.f);
+}
+static bf16 *ones_tile(cudaStream_t st) {
+    static bf16 *t = nullptr;
+    if (!t) {
+        if (cudaMalloc(&t, 64 * 64 * 2) != cudaSuccess) return nullptr;
+        k_ones_tile<<<1, 256, 0, st>>>(t);
+    }
+    return t;
+}
+
+// conv3 forward, groups online / target: act3[g] = relu(im2col(act2[g]) W3[g]^T + b3[g])
+int tma_conv3_fwd(const pq_net *nets, bf16 *const *act2, bf16 *const *act3, int groups, int n, cudaStream_t st) {
+    static TmaGemm<EpiBiasRelu> g;
+    memset(&g, 0, sizeof(g));
+    for (int q = 0; q < groups; ++q) {
+        if (int rc = map_im2col(&g.a[q], act2[q], n, 9, 9, 0, -2, 128, "act2")) return rc;
+        if (int rc = map2(&g.b[q], (const bf16 *)nets[q].shadow + S_W3, 64, 576, 576, "W3")) return rc;
+        g.ep[q] = EpiBiasRelu{act3[q], nets[q].master + P_B3, n * 49, 64, 64, 1.0f};
+    }
+    g.kindA = OP_IF3, g.kindB = OP_K2, g.boxesA = 2, g.boxesB = 1, g.n = n, g.b_is_weight = 1;
+    g.mtiles = (n * 49 + 127) / 128, g.ntiles = 1, g.splits = 1, g.groups = groups, g.kc = 9, g.nk = 9;
+    return launch_tma<64, false, false>(g, st, "conv3 forward (TMA)");
+}
+
+// fc1 forward, swapped: part[g][s][b][j] = sum over split s of W4[g][j] . act3[g][b]
+int tma_fc1_fwd(const pq_net *nets, bf16 *const *act3, float *const *part, int splits, int groups, int n,
+                cudaStream_t st) {
+    static TmaGemm<EpiF32T> g;
+    memset(&g, 0, sizeof(g));
+    for (int q = 0; q < groups; ++q) {
+        if (int rc = map2(&g.a[q], (const bf16 *)nets[q].shadow + S_W4, 512, 3136, 3136, "W4")) return rc;
+        if (int rc = map2(&g.b[q], act3[q], n, 3136, 3136, "act3")) return rc;
+        g.ep[q] = EpiF32T{part[q], 512, n, 512, (size_t)n * 512};
+    }
+    g.kindA = OP_K2, g.kindB = OP_K2, g.boxesA = 2, g.boxesB = 1, g.n = n;
+    g.mtiles = 4, g.ntiles = (n + 63) / 64, g.splits = splits, g.groups = groups;
+    g.nk = 49, g.kc = (49 + splits - 1) / splits;
+    return launch_tma<64, false, false>(g, st, "fc1 forward (TMA)");
+}
+
+// fc1 data gradient: dY3[b][k] = relu'(act3) * sum_j dh1[b][j] W4[j][k] (W4 as MN-major B)
+int tma_fc1_dgrad(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *dY3, int n, cudaStream_t st) {
+    static TmaGemm<EpiMask> g;
+    memset(&g, 0, sizeof(g));
+    if (int rc = map2(&g.a[0], dh1_bf, n, 512, 512, "dh1")) return rc;
+    if (int rc = map2(&g.b[0], (const bf16 *)th.shadow + S_W4, 512, 3136, 3136, "W4")) return rc;
+    g.ep[0] = EpiMask{dY3, act3, n, 3136, 3136};
+    g.kindA = OP_K2, g.kindB = OP_M2, g.boxesA = 2, g.boxesB = 1, g.n = n;
+    g.mtiles = (n + 127) / 128, g.ntiles = 49, g.splits = 1, g.groups = 1, g.kc = 8, g.nk = 8;
+    return launch_tma<64, false, true>(g, st, "fc1 dgrad (TMA)");
+}
+
+// fc1 weight gradient with the centered RMSProp update fused in the epilogue
+int tma_fc1_wgrad_rms(const EpiRms &e, const bf16 *dh1T, int n8, const bf16 *act3, int n, cudaStream_t st) {
+    static TmaGemm<EpiRms> g;
+    memset(&g, 0, sizeof(g));
+    if (int rc = map2(&g.a[0], dh1T, 512, n, n8, "dh1T")) return rc;
+    if (int rc = map2(&g.b[0], act3, n, 3136, 3136, "act3")) return rc;
+    g.ep[0] = e;
+    g.kindA = OP_K2, g.kindB = OP_M2, g.boxesA = 2, g.boxesB = 1, g.n = n;
+    g.mtiles = 4, g.ntiles = 49, g.splits = 1, g.groups = 1, g.nk = (n + 63) / 64, g.kc = g.nk;
+    return launch_tma<64, false, true>(g, st, "fc1 wgrad+rmsprop (TMA)");
+}
+
+// conv3 data gradient: dY2 = relu'(act2) * transposed conv3(dY3) (im2col window, pad 2)
+int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st) {
+    static TmaGemm<EpiMask> g;
+    memset(&g, 0, sizeof(g));
+    if (int rc = map_im2col(&g.a[0], dY3, n, 7, 7, -2, 0, 128, "dY3")) return rc;
+    const uint64_t dims[3] = {64, 9, 64}, strd[2] = {64, 576};
+    if (int rc = make_map(&g.b[0], (const bf16 *)th.shadow + S_W3, 3, dims, strd, "W3 view")) return rc;
+    g.ep[0] = EpiMask{dY2, act2, n * 81, 64, 64};
+    g.kindA = OP_IT3, g.kindB = OP_W3V, g.boxesA = 2, g.boxesB = 1, g.n = n, g.b_is_weight = 1;
+    g.mtiles = (n * 81 + 127) / 128, g.ntiles = 1, g.splits = 1, g.groups = 1, g.kc = 9, g.nk = 9;
+    return launch_tma<64, false, true>(g, st, "conv3 dgrad (TMA)");
+}
+
+// conv3 weight gradient: part3[s][o][k] = sum over split s of im2col(act2)[m][k] dY3[m][o];
+// k = 576 is the bias row (ones tile)
+int tma_conv3_wgrad(const bf16 *act2, const bf16 *dY3, float *part3, int kc, int splits, int n, cudaStream_t st) {
+    static TmaGemm<EpiF32T> g;
+    memset(&g, 0, sizeof(g));
+    bf16 *ones = ones_tile(st);
+    if (!ones) return set_err("ones tile allocation failed");
+    if (int rc = map_im2col(&g.a[0], act2, n, 9, 9, 0, -2, 64, "act2 wgrad")) return rc;
+    if (int rc = map2(&g.b[0], dY3, (uint64_t)n * 49, 64, 64, "dY3")) return rc;
+    if (int rc = map2(&g.aux, ones, 64, 64, 64, "ones")) return rc;
+    g.ep[0] = EpiF32T{part3, 577, 64, 577, (size_t)64 * 577};
+    g.kindA = OP_IW3, g.kindB = OP_M2, g.boxesA = 2, g.boxesB = 1, g.n = n;
+    g.mtiles = 5, g.ntiles = 1, g.splits = splits, g.groups = 1, g.kc = kc, g.nk = (n * 49 + 63) / 64;
+    return launch_tma<64, true, true>(g, st, "conv3 wgrad (TMA)");
+}
+
+// conv2 data gradient per input-parity class: dY1 = relu'(act1) * transposed conv2(dY2)
+int tma_conv2_dgrad(const pq_net &th, const bf16 *dY2, const bf16 *act1, bf16 *dY1, int n, cudaStream_t st) {
+    static TmaGemm<EpiMaskP> g;
+    memset(&g, 0, sizeof(g));
+    const int tpc = (n * 100 + 127) / 128;
+    if (int rc = map_im2col(&g.a[0], dY2, n, 9, 9, -1, 0, 128, "dY2")) return rc;
+    const uint64_t dims[4] = {32, 4, 4, 64}, strd[3] = {32, 128, 512};
+    if (int rc = make_map(&g.b[0], (const bf16 *)th.shadow + S_W2, 4, dims, strd, "W2 view")) return rc;
+    g.ep[0] = epi_mask_p(dY1, act1, n, 10, 10, 32, tpc);
+    g.kindA = OP_IT2, g.kindB = OP_W2V, g.boxesA = 2, g.boxesB = 1, g.n = n, g.tpc = tpc, g.b_is_weight = 1;
+    g.mtiles = 4 * tpc, g.ntiles = 1, g.splits = 1, g.groups = 1, g.kc = 4, g.nk = 4;
+    return launch_tma<64, false, true>(g, st, "conv2 dgrad (TMA)");
+}
+
 static int g_learn_ctas = 0;  // 0 = all SMs minus the acting reserve
 static unsigned long long *g_trace = nullptr;
 

@@ -37,6 +37,27 @@ int cuda_err(cudaError_t e, const char *where) {
         if (_rc) return _rc;                           \
     } while (0)
 
+// TMA-engine GEMMs (learner.cu); PQ_TMA=0 selects the cp.async engine for every GEMM
+int tma_conv3_fwd(const pq_net *nets, bf16 *const *act2, bf16 *const *act3, int groups, int n, cudaStream_t st);
+int tma_fc1_fwd(const pq_net *nets, bf16 *const *act3, float *const *part, int splits, int groups, int n,
+                cudaStream_t st);
+int tma_fc1_dgrad(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *dY3, int n, cudaStream_t st);
+int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st);
+int tma_conv3_wgrad(const bf16 *act2, const bf16 *dY3, float *part3, int kc, int splits, int n, cudaStream_t st);
+int tma_conv2_dgrad(const pq_net &th, const bf16 *dY2, const bf16 *act1, bf16 *dY1, int n, cudaStream_t st);
+// Engine per GEMM (measured, profiles/r1_engine_compare.md): below batch 128 every CTA
+// owns ~one tile and the cp.async engine's shorter first-load latency wins inside the
+// CUDA graph; from 128 up the warp-specialised TMA engine overlaps tiles and wins.
+// PQ_TMA=0 / 1 forces one engine.
+static bool use_tma(int n) {
+    static int mode = -2;
+    if (mode == -2) {
+        const char *e = getenv("PQ_TMA");
+        mode = e ? (e[0] == '0' ? 0 : 1) : -1;
+    }
+    return mode >= 0 ? mode == 1 : n >= 128;
+}
+
 // ------------------------------------------------------------------ workspace
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -142,7 +163,13 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
         g.M = n * 81, g.N = 64, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
         PQ_CHECK((launch_gemm<64, false, false, 0, 2>(g, groups, st)), "conv2 forward");
     }
-    {  // F3: conv3 3x3/1 over 9x9x64 (K = 576)
+    bf16 *a2[2] = {w.act2[0], w.act2[1]}, *a3[2] = {w.act3[0], w.act3[1]};
+    float *pt[2] = {w.fc1part[0], w.fc1part[1]};
+    // engine per GEMM (measured, profiles/r1_engine_compare.md): the TMA im2col conv3
+    // forward wins once a CTA has several tiles; at small batch the cp.async one does
+    if (use_tma(n)) {
+        if (int rc = tma_conv3_fwd(nets, a2, a3, groups, n, st)) return rc;
+    } else {  // F3: conv3 3x3/1 over 9x9x64 (K = 576)
         GemmArgs<LoadIm2col, LoadDense, EpiBiasRelu> g{};
         for (int q = 0; q < groups; ++q) {
             g.a[q] = im2col(w.act2[q], n, 9, 9, 64, 3, 1, 7, 7);
@@ -152,6 +179,7 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
         g.M = n * 49, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
         PQ_CHECK((launch_gemm<64, false, false, 0, 2>(g, groups, st)), "conv3 forward");
     }
+    if (use_tma(n)) return tma_fc1_fwd(nets, a3, pt, FC1_SPLITS, groups, n, st);
     {  // F4: fc1, swapped (D[j][b] = W4[j] . x[b]) with split-K partials [s][b][j]
         GemmArgs<LoadDense, LoadDense, EpiF32T> g{};
         for (int q = 0; q < groups; ++q) {
@@ -299,7 +327,9 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     Fork *fk = nullptr;
     if (int rc = get_fork(&fk)) return rc;
     cudaStream_t side = fk->side, side2 = fk->side2;
-    {  // B4d: dY3[b][k] = relu'(x3) * sum_j W4[j][k] dh1[b][j]   (D[k][b], MN-major W4)
+    if (use_tma(n)) {  // B4d unswapped on the TMA engine: D[b][k], W4 as MN-major B
+        if (int rc = tma_fc1_dgrad(th, w.dh1_bf, w.act3[0], w.dY3, n, st)) return rc;
+    } else {  // B4d: dY3[b][k] = relu'(x3) * sum_j W4[j][k] dh1[b][j]   (D[k][b], MN-major W4)
         GemmArgs<LoadDense, LoadDense, EpiMaskT> g{};
         g.a[0] = LoadDense{sh + S_W4, 512, 3136, 3136};
         g.b[0] = LoadDense{w.dh1_bf, n, 512, 512};
@@ -332,6 +362,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         e.grad_out = la->grad_out, e.flag = la->nonfinite, e.counter = la->update_counter;
         e.lr = la->lr, e.rho = la->rho, e.kappa = la->kappa;
         e.M = 512, e.N = 3136, e.pbase = P_W4, e.sbase = S_W4;
+        // (the cp.async engine: its staged RMSProp epilogue walks the tile with all 8 warps)
         g.e[0] = e;
         g.M = 512, g.N = 3136, g.K = n, g.kc_per_split = (n + 63) / 64, g.splits = 1, g.ones_at = -1;
         PQ_CHECK((launch_gemm<64, false, true, 4>(g, 1, side)), "fc1 wgrad+rmsprop");
@@ -344,7 +375,11 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         int nch = (n * 49 + 63) / 64;
         g.kc_per_split = choose_kc(nch, 5, &s3);
         g.M = 577, g.N = 64, g.K = n * 49, g.splits = s3, g.ones_at = 576, g.ones_extent = n * 49;
-        PQ_CHECK((launch_gemm<64, true, true>(g, 1, side2)), "conv3 wgrad");
+        if (use_tma(n)) {
+            if (int rc = tma_conv3_wgrad(w.act2[0], w.dY3, w.part3, g.kc_per_split, s3, n, side2)) return rc;
+        } else {
+            PQ_CHECK((launch_gemm<64, true, true>(g, 1, side2)), "conv3 wgrad");
+        }
     }
     {  // B3d: dY2 = relu'(x2) * transposed conv3(dY3)
         GemmArgs<LoadTConv, LoadWeightT, EpiMask> g{};
@@ -352,7 +387,11 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         g.b[0] = weight_t(sh + S_W3, 64, 3, 64);
         g.e[0] = EpiMask{w.dY2, w.act2[0], n * 81, 64, 64};
         g.M = n * 81, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<64, false, true, 0, 2>(g, 1, st)), "conv3 dgrad");
+        if (use_tma(n)) {
+            if (int rc = tma_conv3_dgrad(th, w.dY3, w.act2[0], w.dY2, n, st)) return rc;
+        } else {
+            PQ_CHECK((launch_gemm<64, false, true, 0, 2>(g, 1, st)), "conv3 dgrad");
+        }
     }
     PQ_CHECK(cudaEventRecord(fk->ev[2], st), "fork2");
     PQ_CHECK(cudaStreamWaitEvent(side2, fk->ev[2], 0), "fork2 wait");
@@ -374,7 +413,11 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         g.b[0] = weight_tp(sh + S_W2, 64, 4, 32, tpc);
         g.e[0] = epi_mask_p(w.dY1, w.act1[0], n, 10, 10, 32, tpc);
         g.M = 4 * tpc * 128, g.N = 32, g.K = 256, g.kc_per_split = 4, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<64, false, true, 0, 2>(g, 1, st)), "conv2 dgrad");
+        if (use_tma(n)) {
+            if (int rc = tma_conv2_dgrad(th, w.dY2, w.act1[0], w.dY1, n, st)) return rc;
+        } else {
+            PQ_CHECK((launch_gemm<64, false, true, 0, 2>(g, 1, st)), "conv2 dgrad");
+        }
     }
     {  // B1w: dW1^T[k][o] = sum_m P1[m][k] dY1[m][o] over uint8 frames; row 256 = ones
         GemmArgs<LoadFrames, LoadDense, EpiF32T> g{};
