@@ -38,6 +38,8 @@ struct HeadArgs {
     int32_t *act_out;
     float *q_copy;   // optional extra copy [groups][n][A]
     float *td_copy;  // optional [n][3]
+    int64_t *idx_cur;  // optional: the step's sampled slots [n] (read later without the counter)
+    int32_t *upd_cur;  // optional: the step's update id (*counter before the bump)
 };
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -59,11 +61,13 @@ PQ_DEV void head_sample(const HeadArgs &a, int b) {
     __shared__ int s_act;
     // the sampled record (action, reward, terminal) is fetched early by thread 0
     int4 rec_hi = make_int4(0, 0, 0, 0);
-    if (a.learner && tid == 0 && !a.ext_targets) {
+    if (a.learner && tid == 0) {
         int64_t slot = a.idx        ? a.idx[b]
                        : a.idx_base ? a.idx_base[(int64_t)(*a.counter) * a.n + b]
                                     : (int64_t)b;
-        rec_hi = *reinterpret_cast<const int4 *>(a.records + slot * REC_INTS + 4);
+        if (!a.ext_targets) rec_hi = *reinterpret_cast<const int4 *>(a.records + slot * REC_INTS + 4);
+        if (a.idx_cur) a.idx_cur[b] = slot;
+        if (a.upd_cur && b == 0) *a.upd_cur = a.counter ? *a.counter : 0;
     }
     {
         float v[2][2][S + 1];
@@ -174,10 +178,11 @@ struct OptArgs {
     int n, A;
     float lr, rho, kappa;
     int32_t *flag;
-    int32_t *counter;  // update id source; incremented once per step by the last CTA
-    uint32_t *done;    // CTA completion counter for that increment
+    int32_t *counter;  // update id source (read only)
+    uint32_t *done;
     float *grad_out;
     int64_t total;
+    int64_t lo1, hi1, lo2, hi2;  // k_optimizer: the parameter ranges it updates
 };
 
 __device__ __forceinline__ float sum_part(const float *part, int splits, size_t stride, size_t off) {

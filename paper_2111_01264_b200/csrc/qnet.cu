@@ -69,7 +69,9 @@ struct WS {
     int32_t *act;
     bf16 *dY3, *dY2, *dY1;
     float *part1, *part2, *part3, *grad4;
-    uint32_t *done;  // [2] CTA completion counters (optimizer, acting)
+    uint32_t *done;  // [3] CTA completion counters (unused, acting, head)
+    int64_t *idx_cur;  // the step's sampled slots (stashed by the head)
+    int32_t *upd_cur;  // the step's update id (stashed by the head)
     int n8;
     size_t bytes;
 };
@@ -105,7 +107,9 @@ static WS carve(void *base, int N, int A) {
     w.part2 = (float *)take((size_t)MAX_SPLITS * 64 * 513 * 4);
     w.part3 = (float *)take((size_t)MAX_SPLITS * 64 * 577 * 4);
     w.grad4 = (float *)take((size_t)512 * 3136 * 4);
-    w.done = (uint32_t *)take(2 * sizeof(uint32_t));
+    w.done = (uint32_t *)take(3 * sizeof(uint32_t));
+    w.idx_cur = (int64_t *)take((size_t)N * 8);
+    w.upd_cur = (int32_t *)take(sizeof(int32_t));
     w.bytes = off;
     return w;
 }
@@ -197,10 +201,30 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
 
 // ------------------------------------------------------------------ head kernel
 // one 256-thread CTA per sample (learn_parts.cuh: head_sample)
-__global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
+// last CTA of a grid bumps a device step counter (replaces a separate launch)
+__device__ __forceinline__ void last_block_bump(int32_t *counter, uint32_t *done) {
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(done, 1u) == gridDim.x * gridDim.y * gridDim.z - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        *counter += 1;
+        *done = 0;
+        __threadfence();
+    }
+}
+
+// The learner's head also stashes the step's sampled slots and update id, then advances
+// the step counter (last CTA): later kernels of the step read the stash, so the
+// optimizer can be split across streams without racing on the counter.
+__global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a, int32_t *bump, uint32_t *done) {
     griddep_wait();
     griddep_launch();
     head_sample<FC1_SPLITS>(a, blockIdx.x);
+    if (bump) last_block_bump(bump, done);
 }
 
 static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int learner,
@@ -219,36 +243,22 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
         h.counter = la->update_counter, h.ext_targets = la->ext_targets;
         h.ext_actions = la->ext_actions, h.gamma = la->gamma;
         h.q_copy = la->q_out, h.td_copy = la->td_out;
+        h.idx_cur = w.idx_cur, h.upd_cur = w.upd_cur;
     }
-    return cuda_err(launch_k(k_head, dim3(n), dim3(HEAD_THREADS), 0, st, h), "head");
+    int32_t *bump = (la && learner && !la->idx && la->update_counter) ? la->update_counter : nullptr;
+    return cuda_err(launch_k(k_head, dim3(n), dim3(HEAD_THREADS), 0, st, h, bump, w.done + 2), "head");
 }
 
 // ------------------------------------------------------------------ optimizer
-// last CTA of a grid bumps a device step counter (replaces a separate launch)
-__device__ __forceinline__ void last_block_bump(int32_t *counter, uint32_t *done) {
-    __shared__ bool s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(done, 1u) == gridDim.x * gridDim.y * gridDim.z - 1;
-    }
-    __syncthreads();
-    if (s_last && threadIdx.x == 0) {
-        *counter += 1;
-        *done = 0;
-        __threadfence();
-    }
-}
 
-// every parameter except fc1's weight (updated in the fc1 wgrad epilogue unless
-// a.grad4 is given), one parameter per thread (learn_parts.cuh: opt_param)
+// the parameters in [lo1, hi1) and [lo2, hi2), one per thread (learn_parts.cuh: opt_param)
 __global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
     griddep_wait();
     griddep_launch();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t i = a.grad4 ? t : (t < P_W4 ? t : P_B4 + (t - P_W4));
-    if (i < a.total) opt_param(a, i, a.counter ? *a.counter : 0);
-    if (a.counter) last_block_bump(a.counter, a.done);
+    const int64_t n1 = a.hi1 - a.lo1;
+    const int64_t i = t < n1 ? a.lo1 + t : a.lo2 + (t - n1);
+    if (t < n1 || i < a.hi2) opt_param(a, i, a.counter ? *a.counter : 0);
 }
 
 // summed gradient of every parameter except fc1's weight (written by the fc1 wgrad GEMM)
@@ -359,7 +369,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         e.p = th.master, e.m = la->opt.m, e.v = la->opt.v;
         e.p2 = la->theta_out.master, e.m2 = la->opt_out.m, e.v2 = la->opt_out.v;
         e.shadow = (bf16 *)la->theta_out.shadow;
-        e.grad_out = la->grad_out, e.flag = la->nonfinite, e.counter = la->update_counter;
+        e.grad_out = la->grad_out, e.flag = la->nonfinite, e.counter = w.upd_cur;
         e.lr = la->lr, e.rho = la->rho, e.kappa = la->kappa;
         e.M = 512, e.N = 3136, e.pbase = P_W4, e.sbase = S_W4;
         // (the cp.async engine: its staged RMSProp epilogue walks the tile with all 8 warps)
@@ -419,10 +429,42 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
             PQ_CHECK((launch_gemm<64, false, true, 0, 2>(g, 1, st)), "conv2 dgrad");
         }
     }
+    OptArgs o{};
+    o.p = th.master, o.m = la->opt.m, o.v = la->opt.v;
+    o.p2 = la->theta_out.master, o.m2 = la->opt_out.m, o.v2 = la->opt_out.v;
+    o.shadow = (bf16 *)la->theta_out.shadow;
+    o.part1 = w.part1, o.part2 = w.part2, o.part3 = w.part3, o.grad4 = nullptr;
+    o.dh1 = w.dh1, o.h1 = w.h1, o.td = w.td, o.act = w.act;
+    o.n = n, o.A = la->actions;
+    o.lr = la->lr, o.rho = la->rho, o.kappa = la->kappa;
+    o.flag = la->nonfinite, o.counter = w.upd_cur;
+    o.grad_out = la->grad_out;
+    o.total = n_params(la->actions);
+    // PQ_SPLIT_OPT=1: update conv2 / conv3 / fc on the weight-gradient branch and only
+    // conv1 on the critical path.  Measured slower at batch 32 (93.6 vs 92.1 us per step:
+    // its CTAs crowd out the conv1 weight gradient), so the default is one optimizer
+    // launch after the join.
+    static int split_opt = -1;
+    if (split_opt < 0) {
+        const char *e = getenv("PQ_SPLIT_OPT");
+        split_opt = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (!grad_only && split_opt) {
+        // the conv2 / conv3 / fc1-bias / fc2 update runs on the weight-gradient branch as
+        // soon as conv2's data gradient (the last reader of W2 / W3) is done; only conv1's
+        // update stays behind the conv1 weight gradient on the critical path
+        PQ_CHECK(cudaEventRecord(fk->ev[5], st), "fork3");
+        PQ_CHECK(cudaStreamWaitEvent(side2, fk->ev[5], 0), "fork3 wait");
+        OptArgs os = o;
+        os.s1 = s1, os.s2 = s2, os.s3 = s3;
+        os.lo1 = P_W2, os.hi1 = P_W4, os.lo2 = P_B4, os.hi2 = os.total;
+        const int64_t cnt = (P_W4 - P_W2) + (os.total - P_B4);
+        PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((cnt + 255) / 256)), dim3(256), 0, side2, os),
+                 "optimizer (conv2, conv3, fc)");
+    }
     {  // B1w: dW1^T[k][o] = sum_m P1[m][k] dY1[m][o] over uint8 frames; row 256 = ones
         GemmArgs<LoadFrames, LoadDense, EpiF32T> g{};
-        FwdInput in{la->ring, la->records, la->idx ? la->idx : la->idx_base,
-                    la->idx ? nullptr : la->update_counter, n, REC_INTS, 0};
+        FwdInput in{la->ring, la->records, la->idx ? la->idx : w.idx_cur, nullptr, n, REC_INTS, 0};
         g.a[0] = frames_loader(in, n);
         g.b[0] = LoadDense{w.dY1, n * 400, 32, 32};
         g.e[0] = EpiF32T{w.part1, 257, 32, 257, (size_t)32 * 257};
@@ -431,39 +473,28 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         g.M = 257, g.N = 32, g.K = n * 400, g.splits = s1, g.ones_at = 256, g.ones_extent = n * 400;
         PQ_CHECK((launch_gemm<64, true, true>(g, 1, st)), "conv1 wgrad");
     }
+    if (!grad_only && split_opt) {  // conv1's update (main stream)
+        o.s1 = s1, o.s2 = s2, o.s3 = s3;
+        o.lo1 = P_W1, o.hi1 = P_W2, o.lo2 = P_W2, o.hi2 = P_W2;
+        PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((P_W2 - P_W1 + 255) / 256)), dim3(256), 0, st, o),
+                 "optimizer (conv1)");
+    }
     // join the weight-gradient branch
     PQ_CHECK(cudaEventRecord(fk->ev[3], side), "join");
     PQ_CHECK(cudaEventRecord(fk->ev[4], side2), "join 2");
     PQ_CHECK(cudaStreamWaitEvent(st, fk->ev[3], 0), "join wait");
     PQ_CHECK(cudaStreamWaitEvent(st, fk->ev[4], 0), "join wait 2");
-    if (grad_only) {
-        OptArgs o{};
-        o.part1 = w.part1, o.part2 = w.part2, o.part3 = w.part3;
+    if (!grad_only && !split_opt) {  // every parameter but fc1's weight, after the join
         o.s1 = s1, o.s2 = s2, o.s3 = s3;
-        o.dh1 = w.dh1, o.h1 = w.h1, o.td = w.td, o.act = w.act;
-        o.n = n, o.A = la->actions;
+        o.lo1 = P_W1, o.hi1 = P_W4, o.lo2 = P_B4, o.hi2 = o.total;
+        const int64_t cnt = P_W4 + (o.total - P_B4);
+        PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((cnt + 255) / 256)), dim3(256), 0, st, o), "optimizer");
+    }
+    if (grad_only) {
+        o.s1 = s1, o.s2 = s2, o.s3 = s3;
         o.grad_out = grad_only;
-        o.total = n_params(la->actions);
         const int64_t cnt = P_W4 + (o.total - P_B4);
         PQ_CHECK(launch_k(k_grad_only, dim3((unsigned)((cnt + 255) / 256)), dim3(256), 0, st, o), "gradient");
-        return 0;
-    }
-    {
-        OptArgs o{};
-        o.p = th.master, o.m = la->opt.m, o.v = la->opt.v;
-        o.p2 = la->theta_out.master, o.m2 = la->opt_out.m, o.v2 = la->opt_out.v;
-        o.shadow = (bf16 *)la->theta_out.shadow;
-        o.part1 = w.part1, o.part2 = w.part2, o.part3 = w.part3, o.grad4 = nullptr;
-        o.s1 = s1, o.s2 = s2, o.s3 = s3;
-        o.dh1 = w.dh1, o.h1 = w.h1, o.td = w.td, o.act = w.act;
-        o.n = n, o.A = la->actions;
-        o.lr = la->lr, o.rho = la->rho, o.kappa = la->kappa;
-        o.flag = la->nonfinite, o.counter = la->update_counter, o.done = w.done;
-        o.grad_out = la->grad_out;
-        o.total = n_params(la->actions);
-        const int64_t cnt = P_W4 + (o.total - P_B4);
-        PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((cnt + 255) / 256)), dim3(256), 0, st, o),
-                 "optimizer");
     }
     return 0;
 }
