@@ -355,7 +355,7 @@ struct EpiBiasRelu {
     PQ_DEV void apply(int m, int n0, const float *v, int cnt, int) const {
         float bv[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) bv[e] = (e < cnt && n0 + e < N) ? __ldcg(bias + n0 + e) : 0.f;
+        for (int e = 0; e < 32; ++e) bv[e] = (e < cnt && n0 + e < N) ? __ldg(bias + n0 + e) : 0.f;
         if (m >= M) return;
         bf16 *dst = out + (size_t)m * ld;
 #pragma unroll
@@ -413,7 +413,7 @@ PQ_DEV void store_masked32(bf16 *dst, const bf16 *mask, const float *v, int nval
     uint4 mk[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-        mk[c] = c * 8 < nvalid ? __ldcg(reinterpret_cast<const uint4 *>(mask + c * 8)) : make_uint4(0, 0, 0, 0);
+        mk[c] = c * 8 < nvalid ? __ldg(reinterpret_cast<const uint4 *>(mask + c * 8)) : make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         if (c * 8 >= nvalid) break;

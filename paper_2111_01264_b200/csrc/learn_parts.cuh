@@ -183,6 +183,8 @@ struct OptArgs {
     float *grad_out;
     int64_t total;
     int64_t lo1, hi1, lo2, hi2;  // k_optimizer: the parameter ranges it updates
+    int32_t *bump;               // optional: step counter the last CTA advances
+    uint32_t *bump_done;         // CTA completion counter for that increment
 };
 
 __device__ __forceinline__ float sum_part(const float *part, int splits, size_t stride, size_t off) {

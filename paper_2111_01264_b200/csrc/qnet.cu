@@ -199,6 +199,19 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
     return 0;
 }
 
+// PQ_SPLIT_OPT=1: update conv2 / conv3 / fc on the weight-gradient branch and only conv1
+// on the critical path.  Measured slower at batch 32 (93.6 vs 92.1 us per step: its CTAs
+// crowd out the conv1 weight gradient), so the default is one optimizer launch after
+// the join, which also advances the step counter.
+static bool split_optimizer() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("PQ_SPLIT_OPT");
+        on = (e && e[0] == '1') ? 1 : 0;
+    }
+    return on == 1;
+}
+
 // ------------------------------------------------------------------ head kernel
 // one 256-thread CTA per sample (learn_parts.cuh: head_sample)
 // last CTA of a grid bumps a device step counter (replaces a separate launch)
@@ -245,7 +258,10 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
         h.q_copy = la->q_out, h.td_copy = la->td_out;
         h.idx_cur = w.idx_cur, h.upd_cur = w.upd_cur;
     }
-    int32_t *bump = (la && learner && !la->idx && la->update_counter) ? la->update_counter : nullptr;
+    // the step counter advances in the head only when the optimizer is split over two
+    // streams (split_optimizer()); otherwise at the tail of the one optimizer launch
+    int32_t *bump = (la && learner && !la->idx && la->update_counter && split_optimizer()) ? la->update_counter
+                                                                                            : nullptr;
     return cuda_err(launch_k(k_head, dim3(n), dim3(HEAD_THREADS), 0, st, h, bump, w.done + 2), "head");
 }
 
@@ -259,6 +275,7 @@ __global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
     const int64_t n1 = a.hi1 - a.lo1;
     const int64_t i = t < n1 ? a.lo1 + t : a.lo2 + (t - n1);
     if (t < n1 || i < a.hi2) opt_param(a, i, a.counter ? *a.counter : 0);
+    if (a.bump) last_block_bump(a.bump, a.bump_done);
 }
 
 // summed gradient of every parameter except fc1's weight (written by the fc1 wgrad GEMM)
@@ -440,15 +457,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     o.flag = la->nonfinite, o.counter = w.upd_cur;
     o.grad_out = la->grad_out;
     o.total = n_params(la->actions);
-    // PQ_SPLIT_OPT=1: update conv2 / conv3 / fc on the weight-gradient branch and only
-    // conv1 on the critical path.  Measured slower at batch 32 (93.6 vs 92.1 us per step:
-    // its CTAs crowd out the conv1 weight gradient), so the default is one optimizer
-    // launch after the join.
-    static int split_opt = -1;
-    if (split_opt < 0) {
-        const char *e = getenv("PQ_SPLIT_OPT");
-        split_opt = (e && e[0] == '1') ? 1 : 0;
-    }
+    const bool split_opt = split_optimizer();
     if (!grad_only && split_opt) {
         // the conv2 / conv3 / fc1-bias / fc2 update runs on the weight-gradient branch as
         // soon as conv2's data gradient (the last reader of W2 / W3) is done; only conv1's
@@ -487,6 +496,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     if (!grad_only && !split_opt) {  // every parameter but fc1's weight, after the join
         o.s1 = s1, o.s2 = s2, o.s3 = s3;
         o.lo1 = P_W1, o.hi1 = P_W4, o.lo2 = P_B4, o.hi2 = o.total;
+        if (!la->idx && la->update_counter) o.bump = la->update_counter, o.bump_done = w.done;
         const int64_t cnt = P_W4 + (o.total - P_B4);
         PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((cnt + 255) / 256)), dim3(256), 0, st, o), "optimizer");
     }
