@@ -501,6 +501,11 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     if rank != 0:
         return
     hbm, bf16_burst, bf16_sus, peak_src = measured_peaks()
+    traffic = None  # DRAM bytes of one learner step from the committed ncu --set full capture
+    tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("learner_step_dram_bytes")
     learn_flop = FLOP_PER_SAMPLE_LEARN * hp.batch_size
     achieved_tf = learn_flop / (learn_ms * 1e-3) / 1e12
     gather_gbs = 80_000 * GATHER_BYTES_PER_TRANSITION / (gather_ms * 1e-3) / 1e9
@@ -530,7 +535,9 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         "roofline": {
             "kernel": "learner step (15 tcgen05 GEMM/head/optimizer launches, batch 32)",
             "bound": "tensor", "achieved": achieved_tf, "peak": bf16_burst, "unit": "TFLOP/s",
-            "frac": achieved_tf / bf16_burst, "traffic": None,
+            "frac": achieved_tf / bf16_burst, "traffic": traffic,
+            "traffic_source": "profiles/r1_traffic.json (ncu --set full, dram__bytes_read+write of one "
+                              "step's 14 launches; algorithmic ~47 MB: fc1 RMSProp 28 B/param)",
             "per_launch": f"{learn_flop / 1e9:.3f} GFLOP (68.26 MFLOP/sample x {hp.batch_size}) "
                           f"in {learn_ms * 1e3:.1f} us", "peak_source": peak_src,
         },
