@@ -185,6 +185,8 @@ struct OptArgs {
     int64_t lo1, hi1, lo2, hi2;  // k_optimizer: the parameter ranges it updates
     int32_t *bump;               // optional: step counter the last CTA advances
     uint32_t *bump_done;         // CTA completion counter for that increment
+    const float *fcpart;         // optional: per-64-sample-chunk partials [chunks][A+2][512] of
+    int fcchunks;                //   the fc2 / fc1-bias batch sums (k_fc2_partials)
 };
 
 __device__ __forceinline__ float sum_part(const float *part, int splits, size_t stride, size_t off) {
@@ -239,21 +241,27 @@ __device__ __forceinline__ float grad_of(const OptArgs &a, int64_t i, int64_t &s
         sh = S_W4 + (i - P_W4);
         return __ldcg(a.grad4 + (i - P_W4));
     }
+    const size_t fstride = (size_t)(a.A + 2) * 512;
     if (i < P_W5) {
         const int j = (int)(i - P_B4);
+        if (a.fcpart) return sum_part(a.fcpart, a.fcchunks, fstride, (size_t)a.A * 512 + j);
         return batch_sum(a.n, [&](int b) { return __ldcg(a.dh1 + (size_t)b * 512 + j); });
     }
     if (i < p_b5(a.A)) {
         const int64_t r = i - P_W5;
         const int aa = (int)(r >> 9), j = (int)(r & 511);
+        if (a.fcpart) return sum_part(a.fcpart, a.fcchunks, fstride, (size_t)aa * 512 + j);
         return batch_sum(a.n, [&](int b) {
             const float x = __ldcg(a.td + b * 3 + 1) * __ldcg(a.h1 + (size_t)b * 512 + j);
             return __ldcg(a.act + b) == aa ? x : 0.f;
         });
     }
     const int aa = (int)(i - p_b5(a.A));
+    if (a.fcpart) return sum_part(a.fcpart, a.fcchunks, fstride, (size_t)(a.A + 1) * 512 + aa);
     return batch_sum(a.n, [&](int b) { return __ldcg(a.act + b) == aa ? __ldcg(a.td + b * 3 + 1) : 0.f; });
 }
+
+constexpr int FC_CHUNK = 64;  // samples per fc2 / fc1-bias gradient partial (qnet.cu)
 
 // centered RMSProp, kappa inside the square root (_kernels_numba.py:98-111)
 __device__ __forceinline__ void rms(const OptArgs &a, float g, float m, float v, float p,

@@ -72,6 +72,7 @@ struct WS {
     uint32_t *done;  // [3] CTA completion counters (unused, acting, head)
     int64_t *idx_cur;  // the step's sampled slots (stashed by the head)
     int32_t *upd_cur;  // the step's update id (stashed by the head)
+    float *fcpart;     // fc2 / fc1-bias gradient partials per 64-sample chunk (large batches)
     int n8;
     size_t bytes;
 };
@@ -110,6 +111,7 @@ static WS carve(void *base, int N, int A) {
     w.done = (uint32_t *)take(3 * sizeof(uint32_t));
     w.idx_cur = (int64_t *)take((size_t)N * 8);
     w.upd_cur = (int32_t *)take(sizeof(int32_t));
+    w.fcpart = (float *)take((size_t)((N + FC_CHUNK - 1) / FC_CHUNK) * (A + 2) * 512 * 4);
     w.bytes = off;
     return w;
 }
@@ -265,6 +267,41 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
     return cuda_err(launch_k(k_head, dim3(n), dim3(HEAD_THREADS), 0, st, h, bump, w.done + 2), "head");
 }
 
+// fc2 / fc1-bias gradient partials of one 64-sample chunk (blockIdx.x), 512 threads =
+// hidden units j: rows 0..A-1 = sum_b [a_b = a] delta_b h1[b][j] (fc2 weights), row A =
+// sum_b dh1[b][j] (fc1 bias), row A+1 = sum_b [a_b = a] delta_b (fc2 bias, columns a < A).
+// Fixed order within and across chunks (deterministic); large batches only.
+__global__ void __launch_bounds__(512) k_fc2_partials(const float *h1, const float *dh1, const float *td,
+                                                      const int32_t *act, int n, int A, float *part) {
+    griddep_wait();
+    griddep_launch();
+    __shared__ float s_d[FC_CHUNK];
+    __shared__ int s_a[FC_CHUNK];
+    const int b0 = blockIdx.x * FC_CHUNK, nb = min(FC_CHUNK, n - b0), j = threadIdx.x;
+    if (j < nb) {
+        s_d[j] = td[(b0 + j) * 3 + 1];
+        s_a[j] = act[b0 + j];
+    }
+    __syncthreads();
+    float acc[MAX_ACTIONS], ab = 0.f, bb = 0.f;
+#pragma unroll
+    for (int aa = 0; aa < MAX_ACTIONS; ++aa) acc[aa] = 0.f;
+    for (int b = 0; b < nb; ++b) {
+        const float x = s_d[b] * h1[(size_t)(b0 + b) * 512 + j];
+        const int ab_ = s_a[b];
+#pragma unroll
+        for (int aa = 0; aa < MAX_ACTIONS; ++aa) acc[aa] += (ab_ == aa) ? x : 0.f;
+        ab += dh1[(size_t)(b0 + b) * 512 + j];
+        if (j < A && ab_ == j) bb += s_d[b];
+    }
+    float *out = part + (size_t)blockIdx.x * (A + 2) * 512;
+#pragma unroll
+    for (int aa = 0; aa < MAX_ACTIONS; ++aa)
+        if (aa < A) out[aa * 512 + j] = acc[aa];
+    out[A * 512 + j] = ab;
+    if (j < A) out[(A + 1) * 512 + j] = bb;
+}
+
 // ------------------------------------------------------------------ optimizer
 
 // the parameters in [lo1, hi1) and [lo2, hi2), one per thread (learn_parts.cuh: opt_param)
@@ -370,6 +407,14 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     PQ_CHECK(cudaEventRecord(fk->ev[1], st), "fork1");
     PQ_CHECK(cudaStreamWaitEvent(side, fk->ev[1], 0), "fork1 wait");
     PQ_CHECK(cudaStreamWaitEvent(side2, fk->ev[1], 0), "fork1 wait 2");
+    // large batches: the fc2 / fc1-bias batch sums as chunk partials on the wgrad branch
+    // (the optimizer then reduces n/64 partials per parameter instead of n samples)
+    const int fc_chunks = n > 2 * FC_CHUNK ? (n + FC_CHUNK - 1) / FC_CHUNK : 0;
+    if (fc_chunks)
+        PQ_CHECK(launch_k(k_fc2_partials, dim3(fc_chunks), dim3(512), 0, side2, (const float *)w.h1,
+                          (const float *)w.dh1, (const float *)w.td, (const int32_t *)w.act, n, la->actions,
+                          w.fcpart),
+                 "fc2 partials");
     if (grad_only) {  // B4w: dW4[j][k] = sum_b dh1[b][j] x3[b][k] -> grad (row-major = param order)
         GemmArgs<LoadDense, LoadDense, EpiF32> g{};
         g.a[0] = LoadDense{w.dh1T, 512, n, w.n8};
@@ -457,6 +502,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     o.flag = la->nonfinite, o.counter = w.upd_cur;
     o.grad_out = la->grad_out;
     o.total = n_params(la->actions);
+    if (fc_chunks) o.fcpart = w.fcpart, o.fcchunks = fc_chunks;
     const bool split_opt = split_optimizer();
     if (!grad_only && split_opt) {
         // the conv2 / conv3 / fc1-bias / fc2 update runs on the weight-gradient branch as
