@@ -615,7 +615,7 @@ struct NoHook {
 // kernel's griddepcontrol.wait -- so it lands while the predecessor drains
 // (0 = none, 1 = A, 2 = B).  All 256 threads enter; returns with TMEM and the ring free.
 template <int BN, bool AMN, bool BMN, int STAGES, int SLOT, int PF, class LA, class LB, class EP,
-          class Hook>
+          class Hook, bool FRESH = false>
 PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, int kb1, int m0, int n0,
                       int split, int ones_at, int ones_extent, TileRing &R, const Hook &hook) {
     static_assert(BN == 16 || BN == 32 || BN == 64 || BN == 128 || BN == 256, "BN");
@@ -640,7 +640,7 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
     lb.at_tile(m0);
     uint8_t *smem = R.smem;
     const uint32_t smem_s = R.smem_s;
-    const uint32_t seq0 = R.seq;
+    const uint32_t seq0 = FRESH ? 0u : R.seq;  // FRESH: a one-shot kernel's first tile
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool tl = g_tl.on && tl_cta0() && tid == 0;
     int tl_i = 0;
@@ -897,9 +897,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     if ((threadIdx.x >> 5) == 0) tmem_alloc<TMEM_COLS>(&tmem_base_s);
     TileRing R{smem, smem_u32(smem), bars, 0u, &tmem_base_s, table};
-    gemm_tile<BN, AMN, BMN, Cfg::STAGES, Cfg::STAGE, PF>(g.a[grp], g.b[grp], g.e[grp], kb0, kb1,
-                                                        blockIdx.x * 128, blockIdx.y * BN, split,
-                                                        g.ones_at, g.ones_extent, R, GridDepHook{});
+    gemm_tile<BN, AMN, BMN, Cfg::STAGES, Cfg::STAGE, PF, LA, LB, EP, GridDepHook, true>(
+        g.a[grp], g.b[grp], g.e[grp], kb0, kb1, blockIdx.x * 128, blockIdx.y * BN, split, g.ones_at,
+        g.ones_extent, R, GridDepHook{});
     if ((threadIdx.x >> 5) == 0) tmem_dealloc<TMEM_COLS>(tmem_base_s);
 }
 

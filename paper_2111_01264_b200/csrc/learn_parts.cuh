@@ -11,8 +11,9 @@
 //                   split-K weight-gradient partials in a fixed order; refreshes the bf16
 //                   GEMM shadow and raises the non-finite flag (nn.py:181-183).
 //
-// Data written inside a persistent launch is read with ld.global.cg (L2), never through
-// the non-coherent path.
+// Loads are plain ld.global: data written earlier in a persistent launch is visible
+// because the grid barrier's gpu-scope fences invalidate the SM's L1 (CCTL.IVALL);
+// never the non-coherent path.
 #pragma once
 
 #include "gemm.cuh"
@@ -79,8 +80,8 @@ PQ_DEV void head_sample(const HeadArgs &a, int b) {
                 const int gg = g < a.groups ? g : 0;
                 const float *P = a.part[gg] + (size_t)b * 512 + j;
 #pragma unroll
-                for (int sp = 0; sp < S; ++sp) v[g][i][sp] = __ldcg(P + (size_t)sp * a.n * 512);
-                v[g][i][S] = __ldcg(a.master[gg] + P_B4 + j);
+                for (int sp = 0; sp < S; ++sp) v[g][i][sp] = (*(P + (size_t)sp * a.n * 512));
+                v[g][i][S] = (*(a.master[gg] + P_B4 + j));
             }
 #pragma unroll
         for (int g = 0; g < 2; ++g)
@@ -101,7 +102,7 @@ PQ_DEV void head_sample(const HeadArgs &a, int b) {
         for (int u = 0; u < 4; ++u) {
             const int aa = min(warp + 8 * u, a.A - 1);
 #pragma unroll
-            for (int t = 0; t < 16; ++t) wv[u][t] = __ldcg(w5 + aa * 512 + lane + 32 * t);
+            for (int t = 0; t < 16; ++t) wv[u][t] = (*(w5 + aa * 512 + lane + 32 * t));
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -111,7 +112,7 @@ PQ_DEV void head_sample(const HeadArgs &a, int b) {
             for (int t = 0; t < 16; ++t) acc += wv[u][t] * hs[g][lane + 32 * t];
             acc = warp_sum(acc);
             if (lane == 0 && aa < a.A) {
-                float q = acc + __ldcg(a.master[g] + p_b5(a.A) + aa);
+                float q = acc + (*(a.master[g] + p_b5(a.A) + aa));
                 qs[g][aa] = q;
                 a.q_out[((size_t)g * a.n + b) * a.A + aa] = q;
                 if (a.q_copy) a.q_copy[((size_t)g * a.n + b) * a.A + aa] = q;
@@ -157,7 +158,7 @@ PQ_DEV void head_sample(const HeadArgs &a, int b) {
     for (int i = 0; i < 2; ++i) {
         const int j = tid + HEAD_THREADS * i;
         const float hv = hs[0][j];
-        const float g = hv > 0.f ? d * __ldcg(w5 + j) : 0.f;  // hidden_delta with the fc1 ReLU mask
+        const float g = hv > 0.f ? d * (*(w5 + j)) : 0.f;  // hidden_delta with the fc1 ReLU mask
         a.h1[(size_t)b * 512 + j] = hv;
         a.dh1[(size_t)b * 512 + j] = g;
         const bf16 gb = __float2bfloat16_rn(g);
@@ -195,7 +196,7 @@ __device__ __forceinline__ float sum_part(const float *part, int splits, size_t 
     for (int q = 0; q < splits; q += 32) {
         float v[32];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) v[u] = q + u < splits ? __ldcg(part + (q + u) * stride + off) : 0.f;
+        for (int u = 0; u < 32; ++u) v[u] = q + u < splits ? (*(part + (q + u) * stride + off)) : 0.f;
 #pragma unroll
         for (int u = 0; u < 32; ++u) s += v[u];
     }
@@ -239,26 +240,26 @@ __device__ __forceinline__ float grad_of(const OptArgs &a, int64_t i, int64_t &s
     if (i < P_W4) return sum_part(a.part3, a.s3, 64 * 577, (size_t)(i - P_B3) * 577 + 576);
     if (i < P_B4) {
         sh = S_W4 + (i - P_W4);
-        return __ldcg(a.grad4 + (i - P_W4));
+        return (*(a.grad4 + (i - P_W4)));
     }
     const size_t fstride = (size_t)(a.A + 2) * 512;
     if (i < P_W5) {
         const int j = (int)(i - P_B4);
         if (a.fcpart) return sum_part(a.fcpart, a.fcchunks, fstride, (size_t)a.A * 512 + j);
-        return batch_sum(a.n, [&](int b) { return __ldcg(a.dh1 + (size_t)b * 512 + j); });
+        return batch_sum(a.n, [&](int b) { return (*(a.dh1 + (size_t)b * 512 + j)); });
     }
     if (i < p_b5(a.A)) {
         const int64_t r = i - P_W5;
         const int aa = (int)(r >> 9), j = (int)(r & 511);
         if (a.fcpart) return sum_part(a.fcpart, a.fcchunks, fstride, (size_t)aa * 512 + j);
         return batch_sum(a.n, [&](int b) {
-            const float x = __ldcg(a.td + b * 3 + 1) * __ldcg(a.h1 + (size_t)b * 512 + j);
-            return __ldcg(a.act + b) == aa ? x : 0.f;
+            const float x = (*(a.td + b * 3 + 1)) * (*(a.h1 + (size_t)b * 512 + j));
+            return (*(a.act + b)) == aa ? x : 0.f;
         });
     }
     const int aa = (int)(i - p_b5(a.A));
     if (a.fcpart) return sum_part(a.fcpart, a.fcchunks, fstride, (size_t)(a.A + 1) * 512 + aa);
-    return batch_sum(a.n, [&](int b) { return __ldcg(a.act + b) == aa ? __ldcg(a.td + b * 3 + 1) : 0.f; });
+    return batch_sum(a.n, [&](int b) { return (*(a.act + b)) == aa ? (*(a.td + b * 3 + 1)) : 0.f; });
 }
 
 constexpr int FC_CHUNK = 64;  // samples per fc2 / fc1-bias gradient partial (qnet.cu)
@@ -273,7 +274,7 @@ __device__ __forceinline__ void rms(const OptArgs &a, float g, float m, float v,
 
 // one parameter's update; upd = the update id reported on a non-finite gradient
 __device__ __forceinline__ void opt_param(const OptArgs &a, int64_t i, int upd) {
-    const float m = __ldcg(a.m + i), v = __ldcg(a.v + i), p = __ldcg(a.p + i);
+    const float m = (*(a.m + i)), v = (*(a.v + i)), p = (*(a.p + i));
     int64_t sh;
     const float g = grad_of(a, i, sh);
     float m2, v2, p2;
@@ -324,7 +325,7 @@ PQ_DEV void opt_conv_slice(const OptArgs &a, int64_t lo, int64_t hi, int upd) {
             } else {  // bias o: the ones row
                 off[q] = (size_t)(i - b0) * rows + K;
             }
-            p[q] = __ldcg(a.p + i), m[q] = __ldcg(a.m + i), v[q] = __ldcg(a.v + i);
+            p[q] = (*(a.p + i)), m[q] = (*(a.m + i)), v[q] = (*(a.v + i));
         }
         g[q] = 0.f;
     }
@@ -332,7 +333,7 @@ PQ_DEV void opt_conv_slice(const OptArgs &a, int64_t lo, int64_t hi, int upd) {
     for (int sp = 0; sp < splits; ++sp) {
 #pragma unroll
         for (int q = 0; q < PPT; ++q)
-            if (idx[q] >= 0) g[q] += __ldcg(part + sp * stride + off[q]);
+            if (idx[q] >= 0) g[q] += (*(part + sp * stride + off[q]));
     }
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
