@@ -343,6 +343,56 @@ PQ_HD LoadFrames frames(const uint8_t *ring, const int32_t *refs, const int64_t 
     return l;
 }
 
+// Patch gather from an activation tile held in SHARED memory (one sample, NHWC
+// [H][W][C] bf16, C = 32 or 64): row m = output pixel (oy, ox) of an OH x OW grid,
+// col k = (tap t = (kh, kw), channel c); the input pixel is (oy*S + kh*D - pad,
+// ox*S + kw*D - pad) (D = +1 convolution, D = -1 transposed-convolution window);
+// out-of-range pixels and rows >= rows read zero.  gemm_tile copies such operands
+// with plain 16-byte shared loads / stores instead of cp.async.
+struct LoadSmemConv {
+    static constexpr bool U8 = false, TABLE = false, SMEM = true;
+    const bf16 *src;  // generic pointer into shared memory
+    int H, W, C, KW, S, D, pad, OW, rows;
+    int ty0, tx0;  // tap origin (parity classes: the class's first tap)
+    PQ_DEV void at_tile(int) {}
+    struct Row {
+        int oy, ox;
+        bool ok;
+    };
+    struct Col {
+        int kh, kw, c;
+    };
+    PQ_DEV Row row(int m) const {
+        if (m >= rows) return {0, 0, false};
+        const int oy = m / OW;
+        return {oy, m - oy * OW, true};
+    }
+    PQ_DEV Col col(int k) const {
+        const int t = k / C, c = k - t * C, kh = t / KW;
+        return {kh, t - kh * KW, c};
+    }
+    PQ_DEV const bf16 *at(const Row &R, const Col &c) const {
+        if (!R.ok) return nullptr;
+        const int iy = R.oy * S + (ty0 + c.kh) * D - pad, ix = R.ox * S + (tx0 + c.kw) * D - pad;
+        if (iy < 0 || iy >= H || ix < 0 || ix >= W) return nullptr;
+        return src + (iy * W + ix) * C + c.c;
+    }
+    // unused by the shared-memory path; present for the generic loader interface
+    PQ_DEV const void *addr(const Row &, const Col &, int &bytes, const LoadCtx &) const {
+        bytes = 0;
+        return src;
+    }
+};
+
+template <class L, class = void>
+struct is_smem_src {
+    static constexpr bool value = false;
+};
+template <class L>
+struct is_smem_src<L, decltype((void)L::SMEM)> {
+    static constexpr bool value = L::SMEM;
+};
+
 // ------------------------------------------------------------------------ epilogues
 // apply(m, n0, v, cnt, split): tile row m (global), columns n0 .. n0+cnt-1
 
@@ -554,6 +604,28 @@ struct EpiRms {
     }
 };
 
+// Split-K with an in-kernel fixup: every split CTA of an output tile parks its fp32
+// partial tile in a workspace, the last CTA to arrive (device counter per tile) sums
+// the partials in split order (deterministic) and runs the real epilogue, then resets
+// the counter.  Shortens the serial K-chunk chain of small-batch GEMMs.
+template <class EP>
+struct EpiSplitK {
+    static constexpr bool SPLITK = true;
+    EP inner;
+    float *part;      // [tiles][splits][128][64] fp32 (tile = blockIdx.x + blockIdx.y * gridDim.x)
+    uint32_t *count;  // [tiles], zero between launches
+    int splits;
+    PQ_DEV void apply(int, int, const float *, int, int) const {}
+};
+template <class EP, class = void>
+struct is_splitk {
+    static constexpr bool value = false;
+};
+template <class EP>
+struct is_splitk<EP, decltype((void)EP::SPLITK)> {
+    static constexpr bool value = EP::SPLITK;
+};
+
 template <class EP, class = void>
 struct is_staged {
     static constexpr bool value = false;
@@ -691,6 +763,15 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
             const int r = a_r0 + i * a_rs;  // outer row within the tile
             const int q = AMN ? (r * 16 + a_c8) : (r * 8 + a_c8);
             typename LA::Row rr = AMN ? la.row(k0 + r) : ra[i];
+            if constexpr (is_smem_src<LA>::value) {  // synchronous 16-byte shared copy
+                const bf16 *p = la.at(rr, cak);
+                const uint4 v = p ? *reinterpret_cast<const uint4 *>(p) : make_uint4(0, 0, 0, 0);
+                const uint32_t off = AMN ? mnmaj_off(r, a_c8) : kmaj_off(r, a_c8);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a_s + off), "r"(v.x), "r"(v.y),
+                             "r"(v.z), "r"(v.w)
+                             : "memory");
+                continue;
+            }
             int bytes;
             const void *src = la.addr(rr, cak, bytes, cx);
             if (LA::U8) {
@@ -817,7 +898,56 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
     const int row = m0 + wq * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
     constexpr int CW = BN >= 64 ? BN / 2 : BN;  // columns per warpgroup
-    if constexpr (is_staged<EP>::value) {
+    if constexpr (is_splitk<EP>::value) {
+        static_assert(BN <= 64, "split-K fixup tiles are at most 64 columns");
+        __shared__ int s_last;
+        const int tile = blockIdx.x + blockIdx.y * gridDim.x;
+        const int r = wq * 32 + lane;
+        float *base = ep.part + (size_t)tile * ep.splits * 128 * 64;
+        const int cbeg = BN >= 64 ? half * CW : 0;
+        const bool active = BN >= 64 || half == 0;
+        if (active) {
+            for (int c0 = cbeg; c0 < cbeg + CW; c0 += 32) {
+                float v[32];
+                if (nk > 0) {
+                    if (BN >= 32)
+                        tmem_ld32(trow + c0, v);
+                    else
+                        tmem_ld16(trow + c0, v);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
+                }
+                float4 *d = reinterpret_cast<float4 *>(base + ((size_t)split * 128 + r) * 64 + c0);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = atomicAdd(&ep.count[tile], 1u) == (unsigned)(ep.splits - 1);
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            if (active) {
+                for (int c0 = cbeg; c0 < cbeg + CW; c0 += 32) {
+                    float acc[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+                    for (int sp = 0; sp < ep.splits; ++sp) {
+                        const float4 *q4 = reinterpret_cast<const float4 *>(base + ((size_t)sp * 128 + r) * 64 + c0);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 t = __ldcg(q4 + q);
+                            acc[4 * q] += t.x, acc[4 * q + 1] += t.y, acc[4 * q + 2] += t.z, acc[4 * q + 3] += t.w;
+                        }
+                    }
+                    ep.inner.apply(row, n0 + c0, acc, BN < 32 ? BN : 32, 0);
+                }
+            }
+            if (tid == 0) ep.count[tile] = 0;
+        }
+    } else if constexpr (is_staged<EP>::value) {
         // park the accumulator tile in the (now idle) operand ring, then let the
         // epilogue walk it row-wise; row stride BN+1 keeps both passes conflict-free
         static_assert(128 * (BN + 1) * 4 <= STAGES * SLOT, "staging tile");

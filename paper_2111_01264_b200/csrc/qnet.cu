@@ -73,6 +73,9 @@ struct WS {
     int64_t *idx_cur;  // the step's sampled slots (stashed by the head)
     int32_t *upd_cur;  // the step's update id (stashed by the head)
     float *fcpart;     // fc2 / fc1-bias gradient partials per 64-sample chunk (large batches)
+    float *skpart;     // split-K fixup partial tiles [2 groups][SK per group] (small batches)
+    uint32_t *skcount; // [2][256] tile arrival counters
+    size_t sk_group;   // floats per group
     int n8;
     size_t bytes;
 };
@@ -112,6 +115,20 @@ static WS carve(void *base, int N, int A) {
     w.idx_cur = (int64_t *)take((size_t)N * 8);
     w.upd_cur = (int32_t *)take(sizeof(int32_t));
     w.fcpart = (float *)take((size_t)((N + FC_CHUNK - 1) / FC_CHUNK) * (A + 2) * 512 * 4);
+    // split-K fixup workspace: up to 4 splits of ceil(N*81/128) tiles per group; only for
+    // workspaces of small batches (the learner's batch-32 critical path)
+    // PQ_SPLITK=1 enables split-K with the in-kernel fixup for conv2 / conv3 forward,
+    // fc1 dgrad and conv3 dgrad at small batch.  Measured slower inside the CUDA graph
+    // (101 vs 81-84 us per step: the fence + counter + partial re-read outweigh the
+    // shorter K chain), so it is off by default.
+    static int sk_env = -1;
+    if (sk_env < 0) {
+        const char *e = getenv("PQ_SPLITK");
+        sk_env = (e && e[0] == '1') ? 1 : 0;
+    }
+    w.sk_group = (N < 128 && sk_env) ? (size_t)((N * 81 + 127) / 128) * 4 * 128 * 64 : 0;
+    w.skpart = w.sk_group ? (float *)take(2 * w.sk_group * 4) : nullptr;
+    w.skcount = (uint32_t *)take(2 * 256 * sizeof(uint32_t));
     w.bytes = off;
     return w;
 }
@@ -146,6 +163,122 @@ static cudaError_t launch_bn(int bn, const GemmArgs<LA, LB, EP> &g, int groups, 
     }
 }
 
+// ------------------------------------------------------------------ fused conv2 -> conv3
+// One sample per CTA (grid n x groups): the sample's conv1 output (20x20x32) is staged in
+// shared memory, conv2 (9x9 outputs, K = 512) gathers its patches from there, its
+// bias + ReLU output stays in shared memory (and goes out for the conv3 dgrad mask / wgrad
+// operand), conv3 (7x7 outputs, K = 576) gathers from that.  One launch and no act2
+// round trip instead of two dependent GEMM kernels.
+struct F23Args {
+    const bf16 *act1[2];
+    bf16 *act2[2], *act3[2];
+    const bf16 *w2[2], *w3[2];
+    const float *b2[2], *b3[2];
+};
+constexpr int F23_STAGES = 6;
+constexpr int F23_SLOT = GEMM_A_BYTES + 64 * 128;
+constexpr int F23_ACT1 = 400 * 32 * 2, F23_ACT2 = 81 * 64 * 2;
+constexpr int F23_SMEM = F23_STAGES * F23_SLOT + F23_ACT1 + F23_ACT2 + 1024;
+
+// conv2 epilogue: bias + ReLU of the 81 output pixels to global act2 and the smem tile
+struct EpiAct2 {
+    bf16 *out, *tile;
+    const float *bias;
+    PQ_DEV void apply(int m, int n0, const float *v, int, int) const {
+        float bv[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) bv[e] = __ldg(bias + n0 + e);
+        if (m >= 81) return;
+        uint4 o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float y[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const float t = v[8 * q + e] + bv[8 * q + e];
+                y[e] = t > 0.f ? t : 0.f;
+            }
+            o[q] = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]),
+                              pack_bf16(y[6], y[7]));
+        }
+        uint4 *g = reinterpret_cast<uint4 *>(out + (size_t)m * 64 + n0);
+        uint4 *t = reinterpret_cast<uint4 *>(tile + m * 64 + n0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) g[q] = o[q], t[q] = o[q];
+    }
+};
+
+struct F23Hook {  // after the weight prefetch: wait for conv1, stage the sample's act1
+    const bf16 *src;
+    bf16 *dst;
+    PQ_DEV void operator()() const {
+        griddep_wait();
+        griddep_launch();
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+        for (int i = threadIdx.x; i < F23_ACT1 / 16; i += blockDim.x) d4[i] = s4[i];
+        __syncthreads();
+    }
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv23(const __grid_constant__ F23Args a) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t bars[F23_STAGES];
+    __shared__ uint32_t tmem_base_s;
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    bf16 *act1_t = reinterpret_cast<bf16 *>(smem + F23_STAGES * F23_SLOT);
+    bf16 *act2_t = reinterpret_cast<bf16 *>(smem + F23_STAGES * F23_SLOT + F23_ACT1);
+    const int b = blockIdx.x, g = blockIdx.y;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < F23_STAGES; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    if ((threadIdx.x >> 5) == 0) tmem_alloc<64>(&tmem_base_s);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    TileRing R{smem, smem_u32(smem), bars, 0u, &tmem_base_s, nullptr};
+    const LoadSmemConv c2{act1_t, 20, 20, 32, 4, 2, 1, 0, 9, 81, 0, 0};
+    gemm_tile<64, false, false, F23_STAGES, F23_SLOT, 2>(
+        c2, LoadDense{a.w2[g], 64, 512, 512}, EpiAct2{a.act2[g] + (size_t)b * 81 * 64, act2_t, a.b2[g]}, 0, 8, 0,
+        0, 0, -1, 0, R, F23Hook{a.act1[g] + (size_t)b * 400 * 32, act1_t});
+    const LoadSmemConv c3{act2_t, 9, 9, 64, 3, 1, 1, 0, 7, 49, 0, 0};
+    gemm_tile<64, false, false, F23_STAGES, F23_SLOT, 0>(
+        c3, LoadDense{a.w3[g], 64, 576, 576}, EpiBiasRelu{a.act3[g] + (size_t)b * 3136, a.b3[g], 49, 64, 64, 1.0f},
+        0, 9, 0, 0, 0, -1, 0, R, NoHook{});
+    tc_fence_before();
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0) tmem_dealloc<64>(tmem_base_s);
+}
+
+// PQ_CONV23=1 selects the fused kernel.  Measured no faster inside the CUDA graph at
+// batch 32 (84.7 vs 84.5 us per step: PDL already hides the kernel boundary and the 17
+// serial K-chunks remain) and slower at 1024 (200 vs ~103 us), so it is off by default.
+static bool use_conv23() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("PQ_CONV23");
+        on = (e && e[0] == '1') ? 1 : 0;
+    }
+    return on == 1;
+}
+
+static int conv23(const pq_net *nets, int groups, int n, const WS &w, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        PQ_CHECK(cudaFuncSetAttribute(k_conv23, cudaFuncAttributeMaxDynamicSharedMemorySize, F23_SMEM),
+                 "conv23 smem");
+        configured = true;
+    }
+    F23Args a{};
+    for (int q = 0; q < groups; ++q) {
+        a.act1[q] = w.act1[q], a.act2[q] = w.act2[q], a.act3[q] = w.act3[q];
+        a.w2[q] = (const bf16 *)nets[q].shadow + S_W2, a.w3[q] = (const bf16 *)nets[q].shadow + S_W3;
+        a.b2[q] = nets[q].master + P_B2, a.b3[q] = nets[q].master + P_B3;
+    }
+    return cuda_err(launch_k(k_conv23, dim3(n, groups), dim3(GEMM_THREADS), F23_SMEM, st, a), "conv2+conv3 forward");
+}
+
 // F1..F4 for `groups` parameter sets (group 0 / 1 = online / target in the learner)
 static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, int n, const WS &w,
                          cudaStream_t st) {
@@ -159,7 +292,22 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
         g.M = n * 400, g.N = 32, g.K = 256, g.kc_per_split = 4, g.splits = 1, g.ones_at = -1;
         PQ_CHECK((launch_gemm<32, false, false, 3>(g, groups, st)), "conv1 forward");
     }
-    {  // F2: conv2 4x4/2 over 20x20x32 (K = 512)
+    bf16 *a2[2] = {w.act2[0], w.act2[1]}, *a3[2] = {w.act3[0], w.act3[1]};
+    float *pt[2] = {w.fc1part[0], w.fc1part[1]};
+    const bool fused = use_conv23();
+    if (fused) {
+        if (int rc = conv23(nets, groups, n, w, st)) return rc;
+    } else if (w.skpart) {  // F2 with split-K 4 (2 K-chunks per CTA) and in-kernel fixup
+        GemmArgs<LoadIm2col, LoadDense, EpiSplitK<EpiBiasRelu>> g{};
+        for (int q = 0; q < groups; ++q) {
+            g.a[q] = im2col(w.act1[q], n, 20, 20, 32, 4, 2, 9, 9);
+            g.b[q] = LoadDense{(const bf16 *)nets[q].shadow + S_W2, 64, 512, 512};
+            g.e[q] = EpiSplitK<EpiBiasRelu>{EpiBiasRelu{w.act2[q], nets[q].master + P_B2, n * 81, 64, 64, 1.0f},
+                                            w.skpart + q * w.sk_group, w.skcount + q * 256, 4};
+        }
+        g.M = n * 81, g.N = 64, g.K = 512, g.kc_per_split = 2, g.splits = 4, g.ones_at = -1;
+        PQ_CHECK((launch_gemm<64, false, false, 0, 2>(g, groups, st)), "conv2 forward (split-K)");
+    } else {  // F2: conv2 4x4/2 over 20x20x32 (K = 512)
         GemmArgs<LoadIm2col, LoadDense, EpiBiasRelu> g{};
         for (int q = 0; q < groups; ++q) {
             g.a[q] = im2col(w.act1[q], n, 20, 20, 32, 4, 2, 9, 9);
@@ -169,12 +317,21 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
         g.M = n * 81, g.N = 64, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
         PQ_CHECK((launch_gemm<64, false, false, 0, 2>(g, groups, st)), "conv2 forward");
     }
-    bf16 *a2[2] = {w.act2[0], w.act2[1]}, *a3[2] = {w.act3[0], w.act3[1]};
-    float *pt[2] = {w.fc1part[0], w.fc1part[1]};
     // engine per GEMM (measured, profiles/r1_engine_compare.md): the TMA im2col conv3
     // forward wins once a CTA has several tiles; at small batch the cp.async one does
-    if (use_tma(n)) {
+    if (fused) {
+    } else if (use_tma(n)) {
         if (int rc = tma_conv3_fwd(nets, a2, a3, groups, n, st)) return rc;
+    } else if (w.skpart) {  // F3 with split-K 3 (3 K-chunks per CTA) and in-kernel fixup
+        GemmArgs<LoadIm2col, LoadDense, EpiSplitK<EpiBiasRelu>> g{};
+        for (int q = 0; q < groups; ++q) {
+            g.a[q] = im2col(w.act2[q], n, 9, 9, 64, 3, 1, 7, 7);
+            g.b[q] = LoadDense{(const bf16 *)nets[q].shadow + S_W3, 64, 576, 576};
+            g.e[q] = EpiSplitK<EpiBiasRelu>{EpiBiasRelu{w.act3[q], nets[q].master + P_B3, n * 49, 64, 64, 1.0f},
+                                            w.skpart + q * w.sk_group, w.skcount + q * 256, 3};
+        }
+        g.M = n * 49, g.N = 64, g.K = 576, g.kc_per_split = 3, g.splits = 3, g.ones_at = -1;
+        PQ_CHECK((launch_gemm<64, false, false, 0, 2>(g, groups, st)), "conv3 forward (split-K)");
     } else {  // F3: conv3 3x3/1 over 9x9x64 (K = 576)
         GemmArgs<LoadIm2col, LoadDense, EpiBiasRelu> g{};
         for (int q = 0; q < groups; ++q) {
@@ -393,6 +550,17 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     cudaStream_t side = fk->side, side2 = fk->side2;
     if (use_tma(n)) {  // B4d unswapped on the TMA engine: D[b][k], W4 as MN-major B
         if (int rc = tma_fc1_dgrad(th, w.dh1_bf, w.act3[0], w.dY3, n, st)) return rc;
+    } else if (w.skpart && n <= 64) {  // B4d with split-K 4 and in-kernel fixup
+        GemmArgs<LoadDense, LoadDense, EpiSplitK<EpiMaskT>> g{};
+        g.a[0] = LoadDense{sh + S_W4, 512, 3136, 3136};
+        g.b[0] = LoadDense{w.dh1_bf, n, 512, 512};
+        g.e[0] = EpiSplitK<EpiMaskT>{EpiMaskT{w.dY3, w.act3[0], 3136, n, 3136}, w.skpart, w.skcount, 4};
+        g.M = 3136, g.N = n, g.K = 512, g.kc_per_split = 2, g.splits = 4, g.ones_at = -1;
+        const int bn = choose_bn(n);
+        cudaError_t e = bn == 16   ? launch_gemm<16, true, false, 0, 1>(g, 1, st)
+                        : bn == 32 ? launch_gemm<32, true, false, 0, 1>(g, 1, st)
+                                   : launch_gemm<64, true, false, 0, 1>(g, 1, st);
+        PQ_CHECK(e, "fc1 dgrad (split-K)");
     } else {  // B4d: dY3[b][k] = relu'(x3) * sum_j W4[j][k] dh1[b][j]   (D[k][b], MN-major W4)
         GemmArgs<LoadDense, LoadDense, EpiMaskT> g{};
         g.a[0] = LoadDense{sh + S_W4, 512, 3136, 3136};
@@ -461,6 +629,12 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         g.M = n * 81, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
         if (use_tma(n)) {
             if (int rc = tma_conv3_dgrad(th, w.dY3, w.act2[0], w.dY2, n, st)) return rc;
+        } else if (w.skpart) {  // split-K 3 with in-kernel fixup
+            GemmArgs<LoadTConv, LoadWeightT, EpiSplitK<EpiMask>> gs{};
+            gs.a[0] = g.a[0], gs.b[0] = g.b[0];
+            gs.e[0] = EpiSplitK<EpiMask>{g.e[0], w.skpart, w.skcount, 3};
+            gs.M = g.M, gs.N = 64, gs.K = 576, gs.kc_per_split = 3, gs.splits = 3, gs.ones_at = -1;
+            PQ_CHECK((launch_gemm<64, false, true, 0, 2>(gs, 1, st)), "conv3 dgrad (split-K)");
         } else {
             PQ_CHECK((launch_gemm<64, false, true, 0, 2>(g, 1, st)), "conv3 dgrad");
         }
