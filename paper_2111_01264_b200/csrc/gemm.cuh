@@ -604,28 +604,6 @@ struct EpiRms {
     }
 };
 
-// Split-K with an in-kernel fixup: every split CTA of an output tile parks its fp32
-// partial tile in a workspace, the last CTA to arrive (device counter per tile) sums
-// the partials in split order (deterministic) and runs the real epilogue, then resets
-// the counter.  Shortens the serial K-chunk chain of small-batch GEMMs.
-template <class EP>
-struct EpiSplitK {
-    static constexpr bool SPLITK = true;
-    EP inner;
-    float *part;      // [tiles][splits][128][64] fp32 (tile = blockIdx.x + blockIdx.y * gridDim.x)
-    uint32_t *count;  // [tiles], zero between launches
-    int splits;
-    PQ_DEV void apply(int, int, const float *, int, int) const {}
-};
-template <class EP, class = void>
-struct is_splitk {
-    static constexpr bool value = false;
-};
-template <class EP>
-struct is_splitk<EP, decltype((void)EP::SPLITK)> {
-    static constexpr bool value = EP::SPLITK;
-};
-
 template <class EP, class = void>
 struct is_staged {
     static constexpr bool value = false;
@@ -898,56 +876,7 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
     const int row = m0 + wq * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
     constexpr int CW = BN >= 64 ? BN / 2 : BN;  // columns per warpgroup
-    if constexpr (is_splitk<EP>::value) {
-        static_assert(BN <= 64, "split-K fixup tiles are at most 64 columns");
-        __shared__ int s_last;
-        const int tile = blockIdx.x + blockIdx.y * gridDim.x;
-        const int r = wq * 32 + lane;
-        float *base = ep.part + (size_t)tile * ep.splits * 128 * 64;
-        const int cbeg = BN >= 64 ? half * CW : 0;
-        const bool active = BN >= 64 || half == 0;
-        if (active) {
-            for (int c0 = cbeg; c0 < cbeg + CW; c0 += 32) {
-                float v[32];
-                if (nk > 0) {
-                    if (BN >= 32)
-                        tmem_ld32(trow + c0, v);
-                    else
-                        tmem_ld16(trow + c0, v);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
-                }
-                float4 *d = reinterpret_cast<float4 *>(base + ((size_t)split * 128 + r) * 64 + c0);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            }
-        }
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) s_last = atomicAdd(&ep.count[tile], 1u) == (unsigned)(ep.splits - 1);
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            if (active) {
-                for (int c0 = cbeg; c0 < cbeg + CW; c0 += 32) {
-                    float acc[32];
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) acc[e] = 0.f;
-                    for (int sp = 0; sp < ep.splits; ++sp) {
-                        const float4 *q4 = reinterpret_cast<const float4 *>(base + ((size_t)sp * 128 + r) * 64 + c0);
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const float4 t = __ldcg(q4 + q);
-                            acc[4 * q] += t.x, acc[4 * q + 1] += t.y, acc[4 * q + 2] += t.z, acc[4 * q + 3] += t.w;
-                        }
-                    }
-                    ep.inner.apply(row, n0 + c0, acc, BN < 32 ? BN : 32, 0);
-                }
-            }
-            if (tid == 0) ep.count[tile] = 0;
-        }
-    } else if constexpr (is_staged<EP>::value) {
+    if constexpr (is_staged<EP>::value) {
         // park the accumulator tile in the (now idle) operand ring, then let the
         // epilogue walk it row-wise; row stride BN+1 keeps both passes conflict-free
         static_assert(128 * (BN + 1) * 4 <= STAGES * SLOT, "staging tile");

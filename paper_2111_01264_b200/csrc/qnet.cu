@@ -73,9 +73,6 @@ struct WS {
     int64_t *idx_cur;  // the step's sampled slots (stashed by the head)
     int32_t *upd_cur;  // the step's update id (stashed by the head)
     float *fcpart;     // fc2 / fc1-bias gradient partials per 64-sample chunk (large batches)
-    float *skpart;     // split-K fixup partial tiles [2 groups][SK per group] (small batches)
-    uint32_t *skcount; // [2][256] tile arrival counters
-    size_t sk_group;   // floats per group
     int n8;
     size_t bytes;
 };
@@ -115,20 +112,6 @@ static WS carve(void *base, int N, int A) {
     w.idx_cur = (int64_t *)take((size_t)N * 8);
     w.upd_cur = (int32_t *)take(sizeof(int32_t));
     w.fcpart = (float *)take((size_t)((N + FC_CHUNK - 1) / FC_CHUNK) * (A + 2) * 512 * 4);
-    // split-K fixup workspace: up to 4 splits of ceil(N*81/128) tiles per group; only for
-    // workspaces of small batches (the learner's batch-32 critical path)
-    // PQ_SPLITK=1 enables split-K with the in-kernel fixup for conv2 / conv3 forward,
-    // fc1 dgrad and conv3 dgrad at small batch.  Measured slower inside the CUDA graph
-    // (101 vs 81-84 us per step: the fence + counter + partial re-read outweigh the
-    // shorter K chain), so it is off by default.
-    static int sk_env = -1;
-    if (sk_env < 0) {
-        const char *e = getenv("PQ_SPLITK");
-        sk_env = (e && e[0] == '1') ? 1 : 0;
-    }
-    w.sk_group = (N < 128 && sk_env) ? (size_t)((N * 81 + 127) / 128) * 4 * 128 * 64 : 0;
-    w.skpart = w.sk_group ? (float *)take(2 * w.sk_group * 4) : nullptr;
-    w.skcount = (uint32_t *)take(2 * 256 * sizeof(uint32_t));
     w.bytes = off;
     return w;
 }
@@ -297,16 +280,6 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
     const bool fused = use_conv23();
     if (fused) {
         if (int rc = conv23(nets, groups, n, w, st)) return rc;
-    } else if (w.skpart) {  // F2 with split-K 4 (2 K-chunks per CTA) and in-kernel fixup
-        GemmArgs<LoadIm2col, LoadDense, EpiSplitK<EpiBiasRelu>> g{};
-        for (int q = 0; q < groups; ++q) {
-            g.a[q] = im2col(w.act1[q], n, 20, 20, 32, 4, 2, 9, 9);
-            g.b[q] = LoadDense{(const bf16 *)nets[q].shadow + S_W2, 64, 512, 512};
-            g.e[q] = EpiSplitK<EpiBiasRelu>{EpiBiasRelu{w.act2[q], nets[q].master + P_B2, n * 81, 64, 64, 1.0f},
-                                            w.skpart + q * w.sk_group, w.skcount + q * 256, 4};
-        }
-        g.M = n * 81, g.N = 64, g.K = 512, g.kc_per_split = 2, g.splits = 4, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<64, false, false, 0, 2>(g, groups, st)), "conv2 forward (split-K)");
     } else {  // F2: conv2 4x4/2 over 20x20x32 (K = 512)
         GemmArgs<LoadIm2col, LoadDense, EpiBiasRelu> g{};
         for (int q = 0; q < groups; ++q) {
@@ -322,16 +295,6 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
     if (fused) {
     } else if (use_tma(n)) {
         if (int rc = tma_conv3_fwd(nets, a2, a3, groups, n, st)) return rc;
-    } else if (w.skpart) {  // F3 with split-K 3 (3 K-chunks per CTA) and in-kernel fixup
-        GemmArgs<LoadIm2col, LoadDense, EpiSplitK<EpiBiasRelu>> g{};
-        for (int q = 0; q < groups; ++q) {
-            g.a[q] = im2col(w.act2[q], n, 9, 9, 64, 3, 1, 7, 7);
-            g.b[q] = LoadDense{(const bf16 *)nets[q].shadow + S_W3, 64, 576, 576};
-            g.e[q] = EpiSplitK<EpiBiasRelu>{EpiBiasRelu{w.act3[q], nets[q].master + P_B3, n * 49, 64, 64, 1.0f},
-                                            w.skpart + q * w.sk_group, w.skcount + q * 256, 3};
-        }
-        g.M = n * 49, g.N = 64, g.K = 576, g.kc_per_split = 3, g.splits = 3, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<64, false, false, 0, 2>(g, groups, st)), "conv3 forward (split-K)");
     } else {  // F3: conv3 3x3/1 over 9x9x64 (K = 576)
         GemmArgs<LoadIm2col, LoadDense, EpiBiasRelu> g{};
         for (int q = 0; q < groups; ++q) {
@@ -550,17 +513,6 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     cudaStream_t side = fk->side, side2 = fk->side2;
     if (use_tma(n)) {  // B4d unswapped on the TMA engine: D[b][k], W4 as MN-major B
         if (int rc = tma_fc1_dgrad(th, w.dh1_bf, w.act3[0], w.dY3, n, st)) return rc;
-    } else if (w.skpart && n <= 64) {  // B4d with split-K 4 and in-kernel fixup
-        GemmArgs<LoadDense, LoadDense, EpiSplitK<EpiMaskT>> g{};
-        g.a[0] = LoadDense{sh + S_W4, 512, 3136, 3136};
-        g.b[0] = LoadDense{w.dh1_bf, n, 512, 512};
-        g.e[0] = EpiSplitK<EpiMaskT>{EpiMaskT{w.dY3, w.act3[0], 3136, n, 3136}, w.skpart, w.skcount, 4};
-        g.M = 3136, g.N = n, g.K = 512, g.kc_per_split = 2, g.splits = 4, g.ones_at = -1;
-        const int bn = choose_bn(n);
-        cudaError_t e = bn == 16   ? launch_gemm<16, true, false, 0, 1>(g, 1, st)
-                        : bn == 32 ? launch_gemm<32, true, false, 0, 1>(g, 1, st)
-                                   : launch_gemm<64, true, false, 0, 1>(g, 1, st);
-        PQ_CHECK(e, "fc1 dgrad (split-K)");
     } else {  // B4d: dY3[b][k] = relu'(x3) * sum_j W4[j][k] dh1[b][j]   (D[k][b], MN-major W4)
         GemmArgs<LoadDense, LoadDense, EpiMaskT> g{};
         g.a[0] = LoadDense{sh + S_W4, 512, 3136, 3136};
@@ -629,12 +581,6 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         g.M = n * 81, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
         if (use_tma(n)) {
             if (int rc = tma_conv3_dgrad(th, w.dY3, w.act2[0], w.dY2, n, st)) return rc;
-        } else if (w.skpart) {  // split-K 3 with in-kernel fixup
-            GemmArgs<LoadTConv, LoadWeightT, EpiSplitK<EpiMask>> gs{};
-            gs.a[0] = g.a[0], gs.b[0] = g.b[0];
-            gs.e[0] = EpiSplitK<EpiMask>{g.e[0], w.skpart, w.skcount, 3};
-            gs.M = g.M, gs.N = 64, gs.K = 576, gs.kc_per_split = 3, gs.splits = 3, gs.ones_at = -1;
-            PQ_CHECK((launch_gemm<64, false, true, 0, 2>(gs, 1, st)), "conv3 dgrad (split-K)");
         } else {
             PQ_CHECK((launch_gemm<64, false, true, 0, 2>(g, 1, st)), "conv3 dgrad");
         }
