@@ -121,13 +121,16 @@ struct LoadIm2col {
 
 // im2col over uint8 frame stacks addressed through a frame table:
 // sample b, channel c -> frame slot refs[map(b) * ref_stride + ref_off + c] (-1 = zero
-// frame) inside the frame ring; row m = (b, oy, ox) of the 20x20 conv1 output, col
-// k = (c, kh, kw) with kw = 0..7 being one 8-byte run (4-byte aligned).  Values are the
-// raw bytes 0..255 (exact in bf16); the 1/255 input scale is applied in the epilogue.
+// frame) inside the frame ring; row m = (b, oy, ox) of the 20x20 conv1 output, col k in
+// the space-to-depth order k = ((ty, tx), c, dy, dx), kh = 4 ty + dy, kw = 4 tx + dx
+// (qnet.cuh w1_perm), the order the TMA engine's space-to-depth conv1 uses, so both
+// engines accumulate identically; an 8-element chunk is two 4-byte runs (rows dy, dy+1).
+// Values are the raw bytes 0..255 (exact in bf16); the 1/255 scale is in the epilogue.
 // The CTA first stages the slots of its sample window in shared memory (fill()); an
 // optional device counter slices the map (graph replay of the epoch index table).
 struct LoadFrames {
     static constexpr bool U8 = true, TABLE = true;
+    static constexpr int HALF2 = 84;  // second 4-byte run of a chunk: the next frame row
     PQ_DEV void at_tile(int) {}
     const uint8_t *ring;
     const int32_t *refs;
@@ -141,7 +144,7 @@ struct LoadFrames {
         bool ok;
     };
     struct Col {
-        int c, kh;
+        int c, off;
         bool ok;
     };
     PQ_DEV Row row(int m) const {
@@ -150,14 +153,17 @@ struct LoadFrames {
         int oy = f20.div(rem), ox = rem - oy * 20;
         return {oy * 336 + ox * 4, b, true};
     }
-    PQ_DEV Col col(int k) const { return {k >> 6, (k >> 3) & 7, k < 256}; }
+    PQ_DEV Col col(int k) const {  // k % 8 == 0: tap (ty, tx), frame c, rows dy, dy + 1
+        const int tap = k >> 6, dy = (k >> 2) & 3;
+        return {(k >> 4) & 3, (4 * (tap >> 1) + dy) * 84 + 4 * (tap & 1), k < 256};
+    }
     PQ_DEV const void *addr(const Row &R, const Col &Cc, int &bytes, const LoadCtx &cx) const {
         bytes = 0;
         if (!R.ok || !Cc.ok) return ring;
         int slot = cx.table[(R.b - cx.tb) * 4 + Cc.c];
         if (slot < 0) return ring;
         bytes = 8;
-        return ring + (size_t)slot * 7056 + R.pix + Cc.kh * 84;
+        return ring + (size_t)slot * 7056 + R.pix + Cc.off;
     }
     // stage frame slots of samples [b_lo, b_hi] (all threads of the CTA)
     PQ_DEV void fill(int b_lo, int b_hi, int32_t *table) const {
@@ -752,10 +758,10 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
             }
             int bytes;
             const void *src = la.addr(rr, cak, bytes, cx);
-            if (LA::U8) {
+            if constexpr (LA::U8) {
                 const uint8_t *p = static_cast<const uint8_t *>(src);
                 cp_async4(u_s + q * 8, p, bytes > 0 ? 4 : 0);
-                cp_async4(u_s + q * 8 + 4, bytes > 0 ? p + 4 : p, bytes > 0 ? 4 : 0);
+                cp_async4(u_s + q * 8 + 4, bytes > 0 ? p + LA::HALF2 : p, bytes > 0 ? 4 : 0);
             } else {
                 const uint32_t off = AMN ? mnmaj_off(r, a_c8) : kmaj_off(r, a_c8);
                 cp_async16(a_s + off, src, bytes);

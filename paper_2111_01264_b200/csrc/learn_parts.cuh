@@ -188,6 +188,7 @@ struct OptArgs {
     uint32_t *bump_done;         // CTA completion counter for that increment
     const float *fcpart;         // optional: per-64-sample-chunk partials [chunks][A+2][512] of
     int fcchunks;                //   the fc2 / fc1-bias batch sums (k_fc2_partials)
+    int w1_perm;                 // part1 rows in the permuted conv1 K order (TMA conv1 wgrad)
 };
 
 __device__ __forceinline__ float sum_part(const float *part, int splits, size_t stride, size_t off) {
@@ -223,7 +224,8 @@ __device__ __forceinline__ float grad_of(const OptArgs &a, int64_t i, int64_t &s
     if (i < P_B1) {
         int o = (int)(i >> 8), k = (int)(i & 255);
         sh = S_W1 + i;
-        return sum_part(a.part1, a.s1, 32 * 257, (size_t)o * 257 + k) * (1.0f / 255.0f);
+        const int row = a.w1_perm ? w1_perm(k) : k;  // TMA conv1 wgrad rows are permuted
+        return sum_part(a.part1, a.s1, 32 * 257, (size_t)o * 257 + row) * (1.0f / 255.0f);
     }
     if (i < P_W2) return sum_part(a.part1, a.s1, 32 * 257, (size_t)(i - P_B1) * 257 + 256);
     if (i < P_B2) {
@@ -283,72 +285,9 @@ __device__ __forceinline__ void opt_param(const OptArgs &a, int64_t i, int upd) 
     a.v2[i] = v2;
     a.p2[i] = p2;
     if (sh >= 0) a.shadow[sh] = __float2bfloat16_rn(p2);
+    if (i < P_B1) a.shadow[S_W1P + (i >> 8) * 256 + w1_perm((int)(i & 255))] = __float2bfloat16_rn(p2);
     if (a.grad_out) a.grad_out[i] = g;
     if (!isfinite(g)) atomicMin(a.flag, upd);
-}
-
-// RMSProp of the parameters [lo, hi) of ONE conv layer (weights then bias), PPT per
-// thread with every load of the slice in flight together: p / m / v, then the split-K
-// partials of all PPT parameters split by split (fixed split-ascending add order, the
-// same sums as grad_of).
-template <int PPT>
-PQ_DEV void opt_conv_slice(const OptArgs &a, int64_t lo, int64_t hi, int upd) {
-    int layer;
-    int64_t w0, b0;
-    const float *part;
-    int splits, rows;
-    if (lo < P_W2) {
-        layer = 1, w0 = P_W1, b0 = P_B1, part = a.part1, splits = a.s1, rows = 257;
-    } else if (lo < P_W3) {
-        layer = 2, w0 = P_W2, b0 = P_B2, part = a.part2, splits = a.s2, rows = 513;
-    } else {
-        layer = 3, w0 = P_W3, b0 = P_B3, part = a.part3, splits = a.s3, rows = 577;
-    }
-    const int K = rows - 1;  // fan-in of one output channel
-    const int nout = layer == 1 ? 32 : 64;
-    const size_t stride = (size_t)nout * rows;
-    int64_t idx[PPT], sh[PPT];
-    size_t off[PPT];
-    float p[PPT], m[PPT], v[PPT], g[PPT];
-#pragma unroll
-    for (int q = 0; q < PPT; ++q) {
-        const int64_t i = lo + threadIdx.x + (int64_t)q * blockDim.x;
-        idx[q] = i < hi ? i : -1;
-        sh[q] = -1;
-        off[q] = 0;
-        if (i < hi) {
-            if (i < b0) {  // weight (o, k): partial row k, column o
-                const int64_t r = i - w0;
-                const int o = (int)(r / K), k = (int)(r - (int64_t)o * K);
-                off[q] = (size_t)o * rows + k;
-                sh[q] = (layer == 1 ? S_W1 : layer == 2 ? S_W2 : S_W3) + r;
-            } else {  // bias o: the ones row
-                off[q] = (size_t)(i - b0) * rows + K;
-            }
-            p[q] = (*(a.p + i)), m[q] = (*(a.m + i)), v[q] = (*(a.v + i));
-        }
-        g[q] = 0.f;
-    }
-#pragma unroll 4
-    for (int sp = 0; sp < splits; ++sp) {
-#pragma unroll
-        for (int q = 0; q < PPT; ++q)
-            if (idx[q] >= 0) g[q] += (*(part + sp * stride + off[q]));
-    }
-#pragma unroll
-    for (int q = 0; q < PPT; ++q) {
-        if (idx[q] < 0) continue;
-        const int64_t i = idx[q];
-        const float gq = (layer == 1 && sh[q] >= 0) ? g[q] * (1.0f / 255.0f) : g[q];
-        float m2, v2, p2;
-        rms(a, gq, m[q], v[q], p[q], m2, v2, p2);
-        a.m2[i] = m2;
-        a.v2[i] = v2;
-        a.p2[i] = p2;
-        if (sh[q] >= 0) a.shadow[sh[q]] = __float2bfloat16_rn(p2);
-        if (a.grad_out) a.grad_out[i] = gq;
-        if (!isfinite(gq)) atomicMin(a.flag, upd);
-    }
 }
 
 }  // namespace pq

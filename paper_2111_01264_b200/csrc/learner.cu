@@ -213,7 +213,11 @@ struct is_scatter<EP, decltype((void)EP::NDEST)> {
 //   IW3: conv3 patches of act2 as the MN-major A of the conv3 weight gradient: K-chunk =
 //        64 output pixels from 64 kb, MN atoms = taps 2 mt, 2 mt + 1; tap 9 = the ones
 //        tile (bias gradient: column 0 = 1)
-enum { OP_K2, OP_M2, OP_W3V, OP_W2V, OP_IF3, OP_IT3, OP_IT2, OP_IW3 };
+//   IF1: conv1 forward over the space-to-depth frame stacks (21x21 pixels x 16 sub-pixels
+//        per frame): 2x2 taps, 128 output pixels from r0, channels from cls (16 g)
+//   IW1: the same patches as the MN-major A of the conv1 weight gradient (64 pixels per
+//        K-chunk, taps 2 mt, 2 mt + 1; tap 4 = the ones tile, tap 5 = zeros)
+enum { OP_K2, OP_M2, OP_W3V, OP_W2V, OP_IF3, OP_IT3, OP_IT2, OP_IW3, OP_IF1, OP_IW1 };
 struct TmaOp {
     const CUtensorMap *map;
     int kind, boxes, r0, cls, n;
@@ -251,6 +255,22 @@ struct TmaOp {
                 const int b = r0 / 100, q = r0 - b * 100, iy = q / 10, ix = q - iy * 10;
                 const int ty = kb >> 1, tx = kb & 1;
                 tma_im2col_4d(dst, map, bar, 0, ix - 1, iy - 1, b, (uint16_t)(1 - tx), (uint16_t)(1 - ty));
+                break;
+            }
+            case OP_IF1: {
+                const int b = r0 / 400, q = r0 - b * 400, oy = q / 20, ox = q - oy * 20;
+                tma_im2col_4d(dst, map, bar, cls, ox, oy, b, (uint16_t)(kb & 1), (uint16_t)(kb >> 1));
+                break;
+            }
+            case OP_IW1: {
+                const int p0 = kb * 64, b = p0 / 400, q = p0 - b * 400, oy = q / 20, ox = q - oy * 20;
+                for (int atom = 0; atom < 2; ++atom) {
+                    const int t = 2 * (r0 >> 7) + atom;
+                    if (t < 4)
+                        tma_im2col_4d(dst + atom * PL_BOX, map, bar, 0, ox, oy, b, (uint16_t)(t & 1), (uint16_t)(t >> 1));
+                    else  // ones tile (bias row), then a fully out-of-bounds box = zeros
+                        tma_load_2d(dst + atom * PL_BOX, aux, bar, t == 4 ? 0 : 64, 0);
+                }
                 break;
             }
             default: {  // OP_IW3
@@ -609,7 +629,7 @@ PQ_DEV TmaOp op(const PLearnArgs &a, int map, int kind, int boxes, int r0, int c
 }
 
 // conv1 patch rows of sample b (g = 0: state frames f0..f3, 1: next state f1..f4):
-// P1[(b, oy, ox)][(c, kh, kw)] = frame_c[4 oy + kh][4 ox + kw] (0..255, exact in bf16;
+// P1[(b, oy, ox)][k'(c, kh, kw)] = frame_c[4 oy + kh][4 ox + kw] (permuted K; 0..255 in bf16;
 // the 1/255 input scale is applied in the conv1 epilogue); slot -1 = masked zero frame.
 // The 4 frames are staged in the (idle) operand ring with coalesced 16-byte loads, all
 // in flight together; the patch rows leave as consecutive 16-byte chunks.
@@ -636,10 +656,13 @@ PQ_DEV void gather_patches(const PLearnArgs &a, int g, const int64_t *map, int b
     __syncthreads();
     bf16 *dst = P1 + (size_t)b * 400 * P1_LD;
     for (int e = quarter * 100 * 32 + threadIdx.x; e < (quarter + 1) * 100 * 32; e += GEMM_THREADS) {
-        const int row = e >> 5, c = (e >> 3) & 3, kh = e & 7;
+        // 8-column chunk j of patch row `row` in the permuted K order (qnet.cuh w1_perm):
+        // tap (ty, tx) = j >> 3, frame c = (j >> 1) & 3, rows dy0 = 2 (j & 1), dy0 + 1
+        const int row = e >> 5, j = e & 31, tap = j >> 3, c = (j >> 1) & 3, dy0 = (j & 1) * 2;
         const int oy = row / 20, ox = row - oy * 20;
-        const uint32_t *src = reinterpret_cast<const uint32_t *>(stage + c * FRAME_BYTES + (4 * oy + kh) * 84 + 4 * ox);
-        *reinterpret_cast<uint4 *>(dst + (size_t)row * P1_LD + c * 64 + kh * 8) = u8x8_to_bf16(src[0], src[1]);
+        const uint8_t *src = stage + c * FRAME_BYTES + (4 * oy + 4 * (tap >> 1) + dy0) * 84 + 4 * ox + 4 * (tap & 1);
+        *reinterpret_cast<uint4 *>(dst + (size_t)row * P1_LD + j * 8) =
+            u8x8_to_bf16(*reinterpret_cast<const uint32_t *>(src), *reinterpret_cast<const uint32_t *>(src + 84));
     }
     __syncthreads();
 }
@@ -755,6 +778,7 @@ PQ_DEV void run_job(const Ctx &c, int type, int g, int uj, int j) {
             o.lr = a.lr, o.rho = a.rho, o.kappa = a.kappa;
             o.flag = a.nonfinite, o.grad_out = a.grad_out;
             o.total = n_params(a.A);
+            o.w1_perm = 1;  // conv1 weight-gradient rows in the permuted K order
             const int64_t lo = opt_lo(type) + (int64_t)j * PL_OPT_PER_JOB;
             const int64_t hi = min(opt_hi(type, a.A), lo + PL_OPT_PER_JOB);
             for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) opt_param(o, i, upd);
@@ -976,11 +1000,11 @@ static PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col() {
 // im2col map of an NHWC bf16 tensor [n][H][W][64]: `pixels` pixels x 64 channels per
 // load; base pixels range over [lo, W-1+hi] x [lo, H-1+hi] (corners in W, H order)
 static int map_im2col(CUtensorMap *m, const void *base, int n, int H, int W, int lo, int hi, int pixels,
-                      const char *what) {
+                      const char *what, int C = 64) {
     auto enc = encode_im2col();
     if (!enc) return set_err("cuTensorMapEncodeIm2col unavailable (driver entry point)");
-    const cuuint64_t gd[4] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n};
-    const cuuint64_t gs[3] = {64 * 2, (cuuint64_t)W * 64 * 2, (cuuint64_t)H * W * 64 * 2};
+    const cuuint64_t gd[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n};
+    const cuuint64_t gs[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
     const int lower[2] = {lo, lo}, upper[2] = {hi, hi};
     const cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), gd, gs, lower, upper, 64,
@@ -998,7 +1022,7 @@ static int build_maps(PLearnArgs &a) {
     const int n = a.n;
     for (int g = 0; g < 2; ++g) {
         const bf16 *sh = (const bf16 *)(g ? a.target.shadow : a.theta.shadow);
-        if (int rc = map2(&a.maps[M_W1 + g], sh + S_W1, 32, 256, 256, "W1")) return rc;
+        if (int rc = map2(&a.maps[M_W1 + g], sh + S_W1P, 32, 256, 256, "W1 permuted")) return rc;
         if (int rc = map2(&a.maps[M_W2 + g], sh + S_W2, 64, 512, 512, "W2")) return rc;
         if (int rc = map2(&a.maps[M_W3 + g], sh + S_W3, 64, 576, 576, "W3")) return rc;
         if (int rc = map2(&a.maps[M_W4 + g], sh + S_W4, 512, 3136, 3136, "W4")) return rc;
@@ -1147,6 +1171,7 @@ struct TmaGemm {
     int mtiles, ntiles, splits, groups;
     int kc, nk;       // K-chunks per split, total K-chunks
     int b_is_weight;  // B never comes from the preceding kernel: prefetched before the PDL wait
+    int cls0[2];      // IF1: channel start of each group (16 g: frames g..g+3)
 };
 
 // Warp-specialised persistent tile loop (one CTA per SM):
@@ -1176,7 +1201,7 @@ PQ_DEV void tg_decode(const TmaGemm<EP> &g, int t, int BN, TmaOp &A, TmaOp &B, i
         cls = mt / g.tpc;
         r0 = (mt - cls * g.tpc) * 128;
     }
-    A = TmaOp{&g.a[grp], g.kindA, g.boxesA, r0, cls, g.n, &g.aux};
+    A = TmaOp{&g.a[grp], g.kindA, g.boxesA, r0, g.kindA == OP_IF1 ? g.cls0[grp] : cls, g.n, &g.aux};
     B = TmaOp{&g.b[grp], g.kindB, g.boxesB, nt * BN, cls, g.n, &g.aux};
     kb0 = sp * g.kc;
     kb1 = min(g.nk, kb0 + g.kc);
@@ -1452,6 +1477,81 @@ int tma_conv2_dgrad(const pq_net &th, const bf16 *dY2, const bf16 *act1, bf16 *d
     g.kindA = OP_IT2, g.kindB = OP_W2V, g.boxesA = 2, g.boxesB = 1, g.n = n, g.tpc = tpc, g.b_is_weight = 1;
     g.mtiles = 4 * tpc, g.ntiles = 1, g.splits = 1, g.groups = 1, g.kc = 4, g.nk = 4;
     return launch_tma<64, false, true>(g, st, "conv2 dgrad (TMA)");
+}
+
+// Space-to-depth gather of the frame stacks: out[b][by][bx][f*16 + dy*4 + dx] =
+// frame_f[4 by + dy][4 bx + dx] (0..255 exact in bf16; slot -1 = the masked zero frame),
+// f < nframes; sample b's frame slots are refs[map(b) * ref_stride + ref_off + f].  conv1
+// (8x8 stride 4 over 84x84) becomes a 2x2 stride-1 conv over 21x21 pixels of 16*nframes
+// channels, which TMA im2col feeds (64 channels = 4 frames from channel 16 g).
+__global__ void __launch_bounds__(256) k_frames_s2d(const uint8_t *ring, const int32_t *refs, const int64_t *map,
+                                                    const int32_t *counter, int map_stride, int ref_stride,
+                                                    int ref_off, int nframes, bf16 *out) {
+    const int b = blockIdx.x;
+    __shared__ int32_t slot[8];
+    griddep_wait();
+    griddep_launch();
+    if ((int)threadIdx.x < nframes) {
+        const int64_t base = (map && counter) ? (int64_t)(*counter) * map_stride : 0;
+        const int64_t rec = map ? map[base + b] : (int64_t)b;
+        slot[threadIdx.x] = refs[rec * ref_stride + ref_off + threadIdx.x];
+    }
+    __syncthreads();
+    bf16 *o = out + (size_t)b * 441 * nframes * 16;
+    for (int e = threadIdx.x; e < 441 * nframes; e += blockDim.x) {
+        const int pix = e / nframes, f = e - pix * nframes, by = pix / 21, bx = pix - by * 21;
+        const int sl = slot[f];
+        uint32_t w[4] = {0, 0, 0, 0};
+        if (sl >= 0) {
+            const uint8_t *src = ring + (size_t)sl * FRAME_BYTES + (4 * by) * 84 + 4 * bx;
+#pragma unroll
+            for (int dy = 0; dy < 4; ++dy) w[dy] = __ldg(reinterpret_cast<const uint32_t *>(src + dy * 84));
+        }
+        uint4 *d = reinterpret_cast<uint4 *>(o + (size_t)(pix * nframes + f) * 16);
+        d[0] = u8x8_to_bf16(w[0], w[1]);
+        d[1] = u8x8_to_bf16(w[2], w[3]);
+    }
+}
+
+int tma_frames_s2d(const uint8_t *ring, const int32_t *refs, const int64_t *map, const int32_t *counter,
+                   int map_stride, int ref_stride, int ref_off, int nframes, int n, bf16 *out, cudaStream_t st) {
+    return cuda_err(launch_k(k_frames_s2d, dim3(n), dim3(256), 0, st, ring, refs, map, counter, map_stride, ref_stride,
+                             ref_off, nframes, out),
+                    "frames space-to-depth");
+}
+
+// conv1 forward on the TMA engine: act1[g] = relu(im2col(s2d, channels 16 c0g..) W1p[g]^T / 255 + b1)
+int tma_conv1_fwd(const pq_net *nets, const bf16 *s2d, int nframes, const int *c0, bf16 *const *act1, int groups,
+                  int n, cudaStream_t st) {
+    static TmaGemm<EpiBiasRelu> g;
+    memset(&g, 0, sizeof(g));
+    for (int q = 0; q < groups; ++q) {
+        if (int rc = map_im2col(&g.a[q], s2d, n, 21, 21, 0, -1, 128, "frames s2d", nframes * 16)) return rc;
+        if (int rc = map2(&g.b[q], (const bf16 *)nets[q].shadow + S_W1P, 32, 256, 256, "W1 permuted")) return rc;
+        g.ep[q] = EpiBiasRelu{act1[q], nets[q].master + P_B1, n * 400, 32, 32, 1.0f / 255.0f};
+    }
+    g.kindA = OP_IF1, g.kindB = OP_K2, g.boxesA = 2, g.boxesB = 1, g.n = n, g.b_is_weight = 1;
+    g.tpc = 0;
+    g.mtiles = (n * 400 + 127) / 128, g.ntiles = 1, g.splits = 1, g.groups = groups, g.kc = 4, g.nk = 4;
+    g.cls0[0] = c0[0], g.cls0[1] = groups > 1 ? c0[1] : 0;
+    return launch_tma<64, false, false>(g, st, "conv1 forward (TMA)");
+}
+
+// conv1 weight gradient on the TMA engine: part1[s][o][k'] over the permuted K order
+// (k' = 256: bias row from the ones tile)
+int tma_conv1_wgrad(const bf16 *s2d, int nframes, const bf16 *dY1, float *part1, int kc, int splits, int n,
+                    cudaStream_t st) {
+    static TmaGemm<EpiF32T> g;
+    memset(&g, 0, sizeof(g));
+    bf16 *ones = ones_tile(st);
+    if (!ones) return set_err("ones tile allocation failed");
+    if (int rc = map_im2col(&g.a[0], s2d, n, 21, 21, 0, -1, 64, "frames s2d wgrad", nframes * 16)) return rc;
+    if (int rc = map2(&g.b[0], dY1, (uint64_t)n * 400, 32, 32, "dY1")) return rc;
+    if (int rc = map2(&g.aux, ones, 64, 64, 64, "ones")) return rc;
+    g.ep[0] = EpiF32T{part1, 257, 32, 257, (size_t)32 * 257};
+    g.kindA = OP_IW1, g.kindB = OP_M2, g.boxesA = 2, g.boxesB = 1, g.n = n;
+    g.mtiles = 3, g.ntiles = 1, g.splits = splits, g.groups = 1, g.kc = kc, g.nk = (n * 400 + 63) / 64;
+    return launch_tma<64, true, true>(g, st, "conv1 wgrad (TMA)");
 }
 
 static int g_learn_ctas = 0;  // 0 = all SMs minus the acting reserve

@@ -45,6 +45,12 @@ int tma_fc1_dgrad(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *
 int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st);
 int tma_conv3_wgrad(const bf16 *act2, const bf16 *dY3, float *part3, int kc, int splits, int n, cudaStream_t st);
 int tma_conv2_dgrad(const pq_net &th, const bf16 *dY2, const bf16 *act1, bf16 *dY1, int n, cudaStream_t st);
+int tma_frames_s2d(const uint8_t *ring, const int32_t *refs, const int64_t *map, const int32_t *counter,
+                   int map_stride, int ref_stride, int ref_off, int nframes, int n, bf16 *out, cudaStream_t st);
+int tma_conv1_fwd(const pq_net *nets, const bf16 *s2d, int nframes, const int *c0, bf16 *const *act1, int groups,
+                  int n, cudaStream_t st);
+int tma_conv1_wgrad(const bf16 *s2d, int nframes, const bf16 *dY1, float *part1, int kc, int splits, int n,
+                    cudaStream_t st);
 // Engine per GEMM (measured, profiles/r1_engine_compare.md): below batch 128 every CTA
 // owns ~one tile and the cp.async engine's shorter first-load latency wins inside the
 // CUDA graph; from 128 up the warp-specialised TMA engine overlaps tiles and wins.
@@ -73,6 +79,7 @@ struct WS {
     int64_t *idx_cur;  // the step's sampled slots (stashed by the head)
     int32_t *upd_cur;  // the step's update id (stashed by the head)
     float *fcpart;     // fc2 / fc1-bias gradient partials per 64-sample chunk (large batches)
+    bf16 *s2d;         // space-to-depth frame stacks [n][21][21][80] (TMA conv1, large batches)
     int n8;
     size_t bytes;
 };
@@ -112,6 +119,7 @@ static WS carve(void *base, int N, int A) {
     w.idx_cur = (int64_t *)take((size_t)N * 8);
     w.upd_cur = (int32_t *)take(sizeof(int32_t));
     w.fcpart = (float *)take((size_t)((N + FC_CHUNK - 1) / FC_CHUNK) * (A + 2) * 512 * 4);
+    w.s2d = N >= 128 ? (bf16 *)take((size_t)N * 441 * 80 * 2) : nullptr;
     w.bytes = off;
     return w;
 }
@@ -265,11 +273,20 @@ static int conv23(const pq_net *nets, int groups, int n, const WS &w, cudaStream
 // F1..F4 for `groups` parameter sets (group 0 / 1 = online / target in the learner)
 static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, int n, const WS &w,
                          cudaStream_t st) {
-    {  // F1: conv1 8x8/4 over uint8 frames (K = 256), bias + ReLU, x 1/255
+    if (use_tma(n) && w.s2d) {  // F1 on the TMA engine over the space-to-depth stacks
+        // learner: frames f0..f4 once, online = channels 0..63, target = 16..79
+        const int nframes = groups == 2 ? 5 : 4;
+        const int c0[2] = {0, 16};
+        bf16 *a1[2] = {w.act1[0], w.act1[1]};
+        if (int rc = tma_frames_s2d(ins[0].ring, ins[0].refs, ins[0].map, ins[0].counter, ins[0].map_stride,
+                                    ins[0].ref_stride, ins[0].ref_off, nframes, n, w.s2d, st))
+            return rc;
+        if (int rc = tma_conv1_fwd(nets, w.s2d, nframes, c0, a1, groups, n, st)) return rc;
+    } else {  // F1: conv1 8x8/4 over uint8 frames (K = 256), bias + ReLU, x 1/255
         GemmArgs<LoadFrames, LoadDense, EpiBiasRelu> g{};
         for (int q = 0; q < groups; ++q) {
             g.a[q] = frames_loader(ins[q], n);
-            g.b[q] = LoadDense{(const bf16 *)nets[q].shadow + S_W1, 32, 256, 256};
+            g.b[q] = LoadDense{(const bf16 *)nets[q].shadow + S_W1P, 32, 256, 256};  // permuted K
             g.e[q] = EpiBiasRelu{w.act1[q], nets[q].master + P_B1, n * 400, 32, 32, 1.0f / 255.0f};
         }
         g.M = n * 400, g.N = 32, g.K = 256, g.kc_per_split = 4, g.splits = 1, g.ones_at = -1;
@@ -467,6 +484,7 @@ __global__ void __launch_bounds__(256) k_rmsprop_apply(float *p, float *m, float
     else if (i >= P_W3 && i < P_B3) sh = S_W3 + (i - P_W3);
     else if (i >= P_W4 && i < P_B4) sh = S_W4 + (i - P_W4);
     if (sh >= 0) shadow[sh] = __float2bfloat16_rn(pi);
+    if (i < P_B1) shadow[S_W1P + (i >> 8) * 256 + w1_perm((int)(i & 255))] = __float2bfloat16_rn(pi);
     if (!isfinite(gi) && flag) atomicMin(flag, upd);
 }
 
@@ -646,7 +664,13 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         int nch = (n * 400 + 63) / 64;
         g.kc_per_split = choose_kc(nch, 3, &s1, (TABLE_SAMPLES - 2) * 400 / 64);
         g.M = 257, g.N = 32, g.K = n * 400, g.splits = s1, g.ones_at = 256, g.ones_extent = n * 400;
-        PQ_CHECK((launch_gemm<64, true, true>(g, 1, st)), "conv1 wgrad");
+        if (use_tma(n) && w.s2d) {  // TMA im2col of the space-to-depth stacks
+            const int nframes = la->ext_targets ? 4 : 5;
+            if (int rc = tma_conv1_wgrad(w.s2d, nframes, w.dY1, w.part1, g.kc_per_split, s1, n, st)) return rc;
+        } else {
+            PQ_CHECK((launch_gemm<64, true, true>(g, 1, st)), "conv1 wgrad");
+        }
+        o.w1_perm = 1;  // both engines produce the rows in the permuted K order
     }
     if (!grad_only && split_opt) {  // conv1's update (main stream)
         o.s1 = s1, o.s2 = s2, o.s3 = s3;
@@ -679,6 +703,10 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
 __global__ void k_f32_to_bf16(const float *src, bf16 *dst, int64_t n) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) dst[i] = __float2bfloat16_rn(src[i]);
+}
+__global__ void k_w1_perm(const float *w1, bf16 *dst) {  // dst[o][w1_perm(k)] = w1[o][k]
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < 8192) dst[(i >> 8) * 256 + w1_perm(i & 255)] = __float2bfloat16_rn(w1[i]);
 }
 
 __global__ void k_rmsprop(const float *p, const float *g, const float *m, const float *v,
@@ -754,6 +782,7 @@ int pq_net_sync_shadow(pq_net net, void *stream) {
         k_f32_to_bf16<<<(unsigned)((cnt[l] + 255) / 256), 256, 0, st>>>(
             net.master + src_off[l], (bf16 *)net.shadow + dst_off[l], cnt[l]);
     }
+    k_w1_perm<<<32, 256, 0, st>>>(net.master + P_W1, (bf16 *)net.shadow + S_W1P);
     return cuda_err(cudaGetLastError(), "sync_shadow");
 }
 

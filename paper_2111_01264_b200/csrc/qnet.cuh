@@ -19,7 +19,14 @@ constexpr int64_t P_W1 = 0, P_B1 = 8192, P_W2 = 8224, P_B2 = 40992, P_W3 = 41056
 __host__ __device__ constexpr int64_t p_b5(int A) { return P_W5 + (int64_t)A * 512; }
 __host__ __device__ constexpr int64_t n_params(int A) { return p_b5(A) + A; }
 // bf16 shadow (GEMM operand) copies of the conv1..fc1 weights
-constexpr int64_t S_W1 = 0, S_W2 = 8192, S_W3 = 40960, S_W4 = 77824, S_TOTAL = 1683456;
+constexpr int64_t S_W1 = 0, S_W2 = 8192, S_W3 = 40960, S_W4 = 77824;
+// W1 again with its K index permuted for the space-to-depth conv1 (TMA engine):
+// k = (c, kh, kw) -> k' = ((ty, tx), c, dy, dx) with kh = 4 ty + dy, kw = 4 tx + dx
+constexpr int64_t S_W1P = 1683456, S_TOTAL = 1683456 + 8192;
+__host__ __device__ inline int w1_perm(int k) {
+    const int c = k >> 6, kh = (k >> 3) & 7, kw = k & 7;
+    return (((kh >> 2) * 2 + (kw >> 2)) * 4 + c) * 16 + (kh & 3) * 4 + (kw & 3);
+}
 constexpr int MAX_ACTIONS = 32;
 constexpr int MAX_SPLITS = 64;
 constexpr int FC1_SPLITS = 7;  // 49 K-chunks of fc1 -> 7 x 7
