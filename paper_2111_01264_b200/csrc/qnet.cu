@@ -510,9 +510,13 @@ static int get_fork(Fork **out) {
     int dev = 0;
     PQ_CHECK(cudaGetDevice(&dev), "get device");
     Fork &f = g_fork[dev & 15];
-    if (!f.side) {
-        PQ_CHECK(cudaStreamCreateWithFlags(&f.side, cudaStreamNonBlocking), "side stream");
-        PQ_CHECK(cudaStreamCreateWithFlags(&f.side2, cudaStreamNonBlocking), "side stream 2");
+    if (!f.side) {  // the weight-gradient branch (PQ_PRIO=1: highest stream priority)
+        int lo = 0, hi = 0;
+        PQ_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+        const char *e = getenv("PQ_PRIO");
+        const int prio = (e && e[0] == '1') ? hi : lo;
+        PQ_CHECK(cudaStreamCreateWithPriority(&f.side, cudaStreamNonBlocking, prio), "side stream");
+        PQ_CHECK(cudaStreamCreateWithPriority(&f.side2, cudaStreamNonBlocking, prio), "side stream 2");
         for (auto &e : f.ev) PQ_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     }
     *out = &f;
