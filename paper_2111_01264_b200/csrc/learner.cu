@@ -1424,18 +1424,6 @@ int tma_fc1_dgrad(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *
     return launch_tma<64, false, true>(g, st, "fc1 dgrad (TMA)");
 }
 
-// fc1 weight gradient with the centered RMSProp update fused in the epilogue
-int tma_fc1_wgrad_rms(const EpiRms &e, const bf16 *dh1T, int n8, const bf16 *act3, int n, cudaStream_t st) {
-    static TmaGemm<EpiRms> g;
-    memset(&g, 0, sizeof(g));
-    if (int rc = map2(&g.a[0], dh1T, 512, n, n8, "dh1T")) return rc;
-    if (int rc = map2(&g.b[0], act3, n, 3136, 3136, "act3")) return rc;
-    g.ep[0] = e;
-    g.kindA = OP_K2, g.kindB = OP_M2, g.boxesA = 2, g.boxesB = 1, g.n = n;
-    g.mtiles = 4, g.ntiles = 49, g.splits = 1, g.groups = 1, g.nk = (n + 63) / 64, g.kc = g.nk;
-    return launch_tma<64, false, true>(g, st, "fc1 wgrad+rmsprop (TMA)");
-}
-
 // conv3 data gradient: dY2 = relu'(act2) * transposed conv3(dY3) (im2col window, pad 2)
 int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st) {
     static TmaGemm<EpiMask> g;

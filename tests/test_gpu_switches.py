@@ -1,0 +1,60 @@
+"""The switch-selected GPU paths stay correct (each runs in a subprocess because the
+switches are read once per process):
+
+* PQ_CONV23=1 — fused conv2 -> conv3 forward with the shared-memory patch loader: the
+  same K order and MMA sequence as the separate GEMMs, so Q-values are bit-identical;
+* PQ_TMA=1 — the warp-specialised TMA engine forced at batch 32 (default: from 128):
+  Q-values bit-identical, one learner step within fp32 summation order (1e-5) of the
+  cp.async engine."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+PROBE = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import torch
+from paper_2111_01264_b200 import nn as dnn
+from paper_2111_01264_b200.envs import FrameEnvSpec
+from paper_2111_01264_b200.replay import ReplayMemory
+net = dnn.init_network(5)
+x = np.random.default_rng(1).integers(0, 256, size=(24, 4, 84, 84), dtype=np.uint8)
+q = dnn.forward(net, x)
+mem = ReplayMemory(4096)
+mem.prepopulate(FrameEnvSpec(key=3), 2000, np.random.default_rng(2))
+theta, target = dnn.init_network(6), dnn.init_network(7)
+idx = mem.sample_indices(32, np.random.default_rng(4))
+th2, _, _, _, _ = dnn._learn(theta, dnn.OptState.zeros(theta), target, mem.ring, mem.records, idx, 32)
+np.savez(sys.argv[2], q=q, theta=th2.master.cpu().numpy(), theta0=theta.master.cpu().numpy())
+"""
+
+
+def run_probe(tmp_path, name, env):
+    out = tmp_path / f"{name}.npz"
+    e = dict(os.environ)
+    e.update(env)
+    subprocess.run([sys.executable, "-c", PROBE, ROOT, str(out)], check=True, env=e, timeout=600)
+    return np.load(out)
+
+
+def test_fused_conv23_and_forced_tma_match_default(tmp_path):
+    base = run_probe(tmp_path, "base", {"PQ_CONV23": "0", "PQ_TMA": "0"})
+    fused = run_probe(tmp_path, "fused", {"PQ_CONV23": "1", "PQ_TMA": "0"})
+    tma = run_probe(tmp_path, "tma", {"PQ_CONV23": "0", "PQ_TMA": "1"})
+    assert np.array_equal(fused["q"], base["q"])
+    assert np.array_equal(tma["q"], base["q"])
+    d = base["theta"] - base["theta0"]
+    for other in (fused, tma):
+        assert np.linalg.norm(other["theta"] - base["theta"]) <= 1e-5 * np.linalg.norm(d)
