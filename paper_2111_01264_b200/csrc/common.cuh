@@ -377,6 +377,30 @@ PQ_DEV unsigned long long gtime() {
     return t;
 }
 PQ_DEV bool tl_cta0() { return blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0; }
+// slots 8..11 of a record: grid dims and a kernel tag (identify the launch)
+PQ_DEV void tl_ident(int slot, char tag) {
+    g_tl.t[slot][8] = gridDim.x, g_tl.t[slot][9] = gridDim.y, g_tl.t[slot][10] = gridDim.z;
+    g_tl.t[slot][11] = (unsigned long long)tag;
+    g_tl.tag[slot] = tag;
+}
+// start / predecessor-done / end stamps of CTA 0 of a non-GEMM kernel (same slot layout)
+struct TlProbe {
+    bool on;
+    unsigned long long t0, t1;
+    PQ_DEV TlProbe() : on(g_tl.on && tl_cta0() && threadIdx.x == 0), t0(on ? gtime() : 0ull), t1(0ull) {}
+    PQ_DEV void waited() {
+        if (on) t1 = gtime();
+    }
+    PQ_DEV void done(char tag) {
+        if (!on) return;
+        const unsigned long long t2 = gtime();
+        const int slot = atomicAdd(&g_tl.n, 1);
+        if (slot < 256) {
+            for (int k = 0; k < 8; ++k) g_tl.t[slot][k] = k == 0 ? t0 : k == 1 ? t1 : k == 2 ? t2 : 0ull;
+            tl_ident(slot, tag);
+        }
+    }
+};
 
 // ---------------------------------------------------------------- misc
 PQ_DEV uint64_t splitmix64(uint64_t z) {

@@ -566,6 +566,10 @@ struct EpiRms {
     // the same walk by NW warps (warp = 0..NW-1 of the participating warps)
     template <int BN, int NW>
     PQ_DEV void apply_tile_w(const float *tile, int ld, int m0, int n0, int warp) const {
+        if (BN >= 16 && ((N | pbase | sbase) & 3) == 0) {
+            apply_tile_v<BN, NW>(tile, ld, m0, n0, warp);
+            return;
+        }
         const int lane = threadIdx.x & 31;
         constexpr int U = BN / 32, RR = 32 / NW;
         const float one_m_rho = 1.0f - rho;
@@ -604,6 +608,61 @@ struct EpiRms {
                     shadow[sbase + o] = __float2bfloat16_rn(pi);
                     if (grad_out) grad_out[pbase + o] = g;
                 }
+            }
+        }
+        if (bad) atomicMin(flag, counter ? *counter : upd);
+    }
+    // float4 walk (N, pbase, sbase multiples of 4): a lane owns 4 consecutive parameters,
+    // BN/4 lanes span a tile row, and every thread keeps Q rows x 3 float4 loads in flight
+    // (4x the bytes in flight of the scalar walk: the epilogue is L2/HBM-latency bound)
+    template <int BN, int NW>
+    PQ_DEV void apply_tile_v(const float *tile, int ld, int m0, int n0, int warp) const {
+        constexpr int LPR = BN / 4, RPW = 32 / LPR, Q = 8;
+        const int lane = threadIdx.x & 31;
+        const int c = (lane % LPR) * 4, rsub = lane / LPR;
+        const float one_m_rho = 1.0f - rho;
+        bool bad = false;
+        for (int r0 = warp * RPW + rsub; r0 < 128; r0 += NW * RPW * Q) {
+            float4 mm[Q], vv[Q], pp[Q];
+            int off[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const int r = r0 + q * NW * RPW;
+                const bool ok = r < 128 && m0 + r < M && n0 + c < N;
+                off[q] = ok ? (m0 + r) * N + n0 + c : -1;
+                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                mm[q] = ok ? __ldcg(reinterpret_cast<const float4 *>(m + pbase + off[q])) : z;
+                vv[q] = ok ? __ldcg(reinterpret_cast<const float4 *>(v + pbase + off[q])) : z;
+                pp[q] = ok ? __ldcg(reinterpret_cast<const float4 *>(p + pbase + off[q])) : z;
+            }
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const int o = off[q];
+                if (o < 0) continue;
+                const float *t = tile + (r0 + q * NW * RPW) * ld + c;
+                const float g[4] = {t[0], t[1], t[2], t[3]};
+                const float ma[4] = {mm[q].x, mm[q].y, mm[q].z, mm[q].w};
+                const float va[4] = {vv[q].x, vv[q].y, vv[q].z, vv[q].w};
+                const float pa[4] = {pp[q].x, pp[q].y, pp[q].z, pp[q].w};
+                float mi[4], vi[4], pi[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    bad |= !isfinite(g[e]);
+                    mi[e] = rho * ma[e] + one_m_rho * g[e];
+                    vi[e] = rho * va[e] + one_m_rho * g[e] * g[e];
+                    pi[e] = pa[e] - lr * g[e] * rsqrtf(vi[e] - mi[e] * mi[e] + kappa);
+                }
+                *reinterpret_cast<float4 *>(m2 + pbase + o) = make_float4(mi[0], mi[1], mi[2], mi[3]);
+                *reinterpret_cast<float4 *>(v2 + pbase + o) = make_float4(vi[0], vi[1], vi[2], vi[3]);
+                *reinterpret_cast<float4 *>(p2 + pbase + o) = make_float4(pi[0], pi[1], pi[2], pi[3]);
+                __nv_bfloat162 s01 = __floats2bfloat162_rn(pi[0], pi[1]);
+                __nv_bfloat162 s23 = __floats2bfloat162_rn(pi[2], pi[3]);
+                uint2 sv;
+                sv.x = *reinterpret_cast<uint32_t *>(&s01);
+                sv.y = *reinterpret_cast<uint32_t *>(&s23);
+                *reinterpret_cast<uint2 *>(shadow + sbase + o) = sv;
+                if (grad_out)
+                    *reinterpret_cast<float4 *>(grad_out + pbase + o) = make_float4(g[0], g[1], g[2], g[3]);
             }
         }
         if (bad) atomicMin(flag, counter ? *counter : upd);
@@ -927,8 +986,8 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
         tl_t[tl_i++] = gtime();  // 7: epilogue done
         const int slot = atomicAdd(&g_tl.n, 1);
         if (slot < 256) {
-            for (int k = 0; k < 12; ++k) g_tl.t[slot][k] = k < tl_i ? tl_t[k] : 0ull;
-            g_tl.tag[slot] = (char)('a' + (BN >> 4) % 26);
+            for (int k = 0; k < 8; ++k) g_tl.t[slot][k] = k < tl_i ? tl_t[k] : 0ull;
+            tl_ident(slot, 'G');
         }
     }
 }

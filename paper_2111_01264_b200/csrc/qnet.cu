@@ -373,10 +373,13 @@ __device__ __forceinline__ void last_block_bump(int32_t *counter, uint32_t *done
 // the step counter (last CTA): later kernels of the step read the stash, so the
 // optimizer can be split across streams without racing on the counter.
 __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a, int32_t *bump, uint32_t *done) {
+    TlProbe tp;
     griddep_wait();
     griddep_launch();
+    tp.waited();
     head_sample<FC1_SPLITS>(a, blockIdx.x);
     if (bump) last_block_bump(bump, done);
+    tp.done('H');
 }
 
 static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int learner,
@@ -443,13 +446,16 @@ __global__ void __launch_bounds__(512) k_fc2_partials(const float *h1, const flo
 
 // the parameters in [lo1, hi1) and [lo2, hi2), one per thread (learn_parts.cuh: opt_param)
 __global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
+    TlProbe tp;
     griddep_wait();
     griddep_launch();
+    tp.waited();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t n1 = a.hi1 - a.lo1;
     const int64_t i = t < n1 ? a.lo1 + t : a.lo2 + (t - n1);
     if (t < n1 || i < a.hi2) opt_param(a, i, a.counter ? *a.counter : 0);
     if (a.bump) last_block_bump(a.bump, a.bump_done);
+    tp.done('O');
 }
 
 // summed gradient of every parameter except fc1's weight (written by the fc1 wgrad GEMM)
