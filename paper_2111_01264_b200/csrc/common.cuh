@@ -368,6 +368,7 @@ struct Timeline {
     int n;
     unsigned long long t[256][12];
     char tag[256];
+    unsigned int ctas[64];  // finished CTAs per (tag, grid) key of the running launches
 };
 static __device__ Timeline g_tl;  // one copy per translation unit (GEMMs live in qnet.cu)
 
@@ -383,6 +384,23 @@ PQ_DEV void tl_ident(int slot, char tag) {
     g_tl.t[slot][11] = (unsigned long long)tag;
     g_tl.tag[slot] = tag;
 }
+// every CTA's thread 0 at its very end: the last CTA of a launch appends an 'E' record
+// (end time, grid dims, tag in slot 7) -- matched to the launch by grid and order
+PQ_DEV void tl_cta_end(char tag) {
+    if (!g_tl.on || threadIdx.x != 0) return;
+    const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned key = (gridDim.x * 131u + gridDim.y * 7u + gridDim.z * 3u + (unsigned)tag) & 63u;
+    __threadfence();
+    if (atomicAdd(&g_tl.ctas[key], 1u) + 1 == total) {
+        const unsigned long long t = gtime();
+        g_tl.ctas[key] = 0;
+        const int slot = atomicAdd(&g_tl.n, 1);
+        if (slot < 256) {
+            for (int k = 0; k < 8; ++k) g_tl.t[slot][k] = k == 0 ? t : k == 7 ? (unsigned long long)tag : 0ull;
+            tl_ident(slot, 'E');
+        }
+    }
+}
 // start / predecessor-done / end stamps of CTA 0 of a non-GEMM kernel (same slot layout)
 struct TlProbe {
     bool on;
@@ -392,6 +410,7 @@ struct TlProbe {
         if (on) t1 = gtime();
     }
     PQ_DEV void done(char tag) {
+        tl_cta_end(tag);
         if (!on) return;
         const unsigned long long t2 = gtime();
         const int slot = atomicAdd(&g_tl.n, 1);

@@ -564,10 +564,10 @@ struct EpiRms {
         apply_tile_w<BN, 8>(tile, ld, m0, n0, threadIdx.x >> 5);
     }
     // the same walk by NW warps (warp = 0..NW-1 of the participating warps)
-    template <int BN, int NW>
+    template <int BN, int NW, int Q = 8>
     PQ_DEV void apply_tile_w(const float *tile, int ld, int m0, int n0, int warp) const {
         if (BN >= 16 && ((N | pbase | sbase) & 3) == 0) {
-            apply_tile_v<BN, NW>(tile, ld, m0, n0, warp);
+            apply_tile_v<BN, NW, Q>(tile, ld, m0, n0, warp);
             return;
         }
         const int lane = threadIdx.x & 31;
@@ -615,9 +615,9 @@ struct EpiRms {
     // float4 walk (N, pbase, sbase multiples of 4): a lane owns 4 consecutive parameters,
     // BN/4 lanes span a tile row, and every thread keeps Q rows x 3 float4 loads in flight
     // (4x the bytes in flight of the scalar walk: the epilogue is L2/HBM-latency bound)
-    template <int BN, int NW>
+    template <int BN, int NW, int Q>
     PQ_DEV void apply_tile_v(const float *tile, int ld, int m0, int n0, int warp) const {
-        constexpr int LPR = BN / 4, RPW = 32 / LPR, Q = 8;
+        constexpr int LPR = BN / 4, RPW = 32 / LPR;
         const int lane = threadIdx.x & 31;
         const int c = (lane % LPR) * 4, rsub = lane / LPR;
         const float one_m_rho = 1.0f - rho;
@@ -669,6 +669,15 @@ struct EpiRms {
     }
 };
 
+// EpiRms with 4 rows of loads in flight per thread (fits the 128-register budget of a
+// two-CTAs-per-SM fused launch)
+struct EpiRms4 : EpiRms {
+    template <int BN>
+    PQ_DEV void apply_tile(const float *tile, int ld, int m0, int n0) const {
+        apply_tile_w<BN, 8, 4>(tile, ld, m0, n0, threadIdx.x >> 5);
+    }
+};
+
 template <class EP, class = void>
 struct is_staged {
     static constexpr bool value = false;
@@ -700,7 +709,10 @@ struct GemmCfg {
     static constexpr int B_BYTES = BN * 128;
     static constexpr int U8_BYTES = U8A ? 128 * 64 : 0;  // raw uint8 staging of the A tile
     static constexpr int STAGE = GEMM_A_BYTES + B_BYTES + U8_BYTES;
-    static constexpr int AUTO = (200 * 1024 / STAGE) < 6 ? (200 * 1024 / STAGE) : 6;
+#ifndef PQ_MAX_STAGES
+#define PQ_MAX_STAGES 4
+#endif
+    static constexpr int AUTO = (200 * 1024 / STAGE) < PQ_MAX_STAGES ? (200 * 1024 / STAGE) : PQ_MAX_STAGES;
     static constexpr int STAGES = ST > 0 ? ST : AUTO;
     static constexpr int SMEM = STAGES * STAGE + 1024;
 };
@@ -1025,6 +1037,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         g.a[grp], g.b[grp], g.e[grp], kb0, kb1, blockIdx.x * 128, blockIdx.y * BN, split, g.ones_at,
         g.ones_extent, R, GridDepHook{});
     if ((threadIdx.x >> 5) == 0) tmem_dealloc<TMEM_COLS>(tmem_base_s);
+    tl_cta_end('G');
 }
 
 template <int BN, bool AMN, bool BMN, int ST = 0, int PF = 0, class LA, class LB, class EP>
@@ -1039,6 +1052,99 @@ cudaError_t launch_gemm(const GemmArgs<LA, LB, EP> &g, int groups, cudaStream_t 
     }
     dim3 grid(grid_x ? grid_x : (g.M + 127) / 128, (g.N + BN - 1) / BN, groups * g.splits);
     return launch_k(kern, grid, dim3(GEMM_THREADS), smem, st, g);
+}
+
+// ------------------------------------------------------------ fused heterogeneous launches
+// Independent GEMMs (and other 256-thread work) of one learner stage share ONE grid:
+// CTAs [0, n0) run part 0, [n0, n0 + n1) part 1, ...  On one stream every launch then
+// chains to the next by programmatic dependent launch, with no cross-stream joins (a
+// joined graph node only starts once all its predecessors have completed), and the
+// side work fills SMs next to the critical-path tiles (two CTAs per SM).
+template <int BN_, bool AMN_, bool BMN_, int ST_, int PF_, class LA_, class LB_, class EP_>
+struct GemmOp {
+    using Args = GemmArgs<LA_, LB_, EP_>;
+    using Cfg = GemmCfg<BN_, LA_::U8, ST_>;
+    static constexpr bool GEMM = true, TABLE = LA_::TABLE;
+    static constexpr int SMEM = Cfg::SMEM, STAGES = Cfg::STAGES;
+    static constexpr uint32_t TMEM_COLS = BN_ < 32 ? 32 : BN_;
+    struct Launch {
+        Args g;
+        int gx, gy;
+    };
+    static Launch make(const Args &g) { return Launch{g, (g.M + 127) / 128, (g.N + BN_ - 1) / BN_}; }
+    static int ctas(const Launch &l, int groups) { return l.gx * l.gy * groups * l.g.splits; }
+    PQ_DEV static void run(const Launch &l, int lin, TileRing &R) {
+        const Args &g = l.g;
+        const int x = lin % l.gx, y = (lin / l.gx) % l.gy, z = lin / (l.gx * l.gy);
+        const int grp = z / g.splits, split = z - grp * g.splits;
+        const int nk_total = (g.K + 63) >> 6;
+        const int kb0 = split * g.kc_per_split, kb1 = min(nk_total, kb0 + g.kc_per_split);
+        gemm_tile<BN_, AMN_, BMN_, STAGES, Cfg::STAGE, PF_, LA_, LB_, EP_, GridDepHook, true>(
+            g.a[grp], g.b[grp], g.e[grp], kb0, kb1, x * 128, y * BN_, split, g.ones_at, g.ones_extent, R,
+            GridDepHook{});
+    }
+};
+struct NoOp {
+    static constexpr bool GEMM = false, TABLE = false;
+    static constexpr int SMEM = 0, STAGES = 1;
+    static constexpr uint32_t TMEM_COLS = 32;
+    struct Launch {};
+    PQ_DEV static void run(const Launch &, int, TileRing &) {}
+};
+
+template <class P0, class P1, class P2>
+struct FusedArgs {
+    typename P0::Launch p0;
+    typename P1::Launch p1;
+    typename P2::Launch p2;
+    int n0, n1;  // CTAs of parts 0 and 1
+};
+
+PQ_HD constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
+template <class P0, class P1, class P2>
+__global__ void __launch_bounds__(GEMM_THREADS, 2) k_fused(const __grid_constant__ FusedArgs<P0, P1, P2> f) {
+    constexpr int STAGES = cmax(P0::STAGES, cmax(P1::STAGES, P2::STAGES));
+    constexpr uint32_t COLS = (uint32_t)cmax(P0::TMEM_COLS, cmax(P1::TMEM_COLS, P2::TMEM_COLS));
+    constexpr bool TABLE = P0::TABLE || P1::TABLE || P2::TABLE;
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t bars[STAGES];
+    __shared__ uint32_t tmem_base_s;
+    __shared__ int32_t table[TABLE ? TABLE_SAMPLES * 4 : 1];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int lin = blockIdx.x;
+    const int part = lin < f.n0 ? 0 : lin < f.n0 + f.n1 ? 1 : 2;
+    const bool gemm = part == 0 ? P0::GEMM : part == 1 ? P1::GEMM : P2::GEMM;
+    if (gemm) {
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+            fence_mbar_init();
+        }
+        if ((threadIdx.x >> 5) == 0) tmem_alloc<COLS>(&tmem_base_s);
+    }
+    TileRing R{smem, smem_u32(smem), bars, 0u, &tmem_base_s, table};
+    if (part == 0)
+        P0::run(f.p0, lin, R);
+    else if (part == 1)
+        P1::run(f.p1, lin - f.n0, R);
+    else
+        P2::run(f.p2, lin - f.n0 - f.n1, R);
+    if (gemm && (threadIdx.x >> 5) == 0) tmem_dealloc<COLS>(tmem_base_s);
+    tl_cta_end('F');
+}
+
+template <class P0, class P1, class P2>
+cudaError_t launch_fused(const FusedArgs<P0, P1, P2> &f, int n2, cudaStream_t st) {
+    auto kern = k_fused<P0, P1, P2>;
+    constexpr int smem = cmax(P0::SMEM, cmax(P1::SMEM, P2::SMEM));
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    return launch_k(kern, dim3(f.n0 + f.n1 + n2), dim3(GEMM_THREADS), smem, st, f);
 }
 
 }  // namespace pq

@@ -382,8 +382,12 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a, int32_t
     tp.done('H');
 }
 
+static bool fused_backward(int n, const pq_learn_args *la, float *grad_only);
+
+// bump_here: the step counter advances in the head (split or fused optimizer schedules);
+// otherwise at the tail of the one optimizer launch
 static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int learner,
-                const pq_learn_args *la, cudaStream_t st) {
+                const pq_learn_args *la, cudaStream_t st, bool bump_here = false) {
     HeadArgs h{};
     for (int g = 0; g < groups; ++g) {
         h.part[g] = w.fc1part[g];
@@ -400,10 +404,7 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
         h.q_copy = la->q_out, h.td_copy = la->td_out;
         h.idx_cur = w.idx_cur, h.upd_cur = w.upd_cur;
     }
-    // the step counter advances in the head only when the optimizer is split over two
-    // streams (split_optimizer()); otherwise at the tail of the one optimizer launch
-    int32_t *bump = (la && learner && !la->idx && la->update_counter && split_optimizer()) ? la->update_counter
-                                                                                            : nullptr;
+    int32_t *bump = (la && learner && !la->idx && la->update_counter && bump_here) ? la->update_counter : nullptr;
     return cuda_err(launch_k(k_head, dim3(n), dim3(HEAD_THREADS), 0, st, h, bump, w.done + 2), "head");
 }
 
@@ -531,25 +532,199 @@ static int get_fork(Fork **out) {
 
 // grad_only != NULL: write the summed gradient of every parameter there instead of
 // updating theta / opt (the data-parallel learner all-reduces it, then pq_rmsprop_apply)
+// ---- the backward GEMMs of the cp.async engine (also the fused single-stream schedule)
+using B3wOp = GemmOp<64, true, true, 0, 0, LoadIm2col, LoadDense, EpiF32T>;
+using B3dOp = GemmOp<64, false, true, 0, 2, LoadTConv, LoadWeightT, EpiMask>;
+using B4wOp = GemmOp<64, false, true, 4, 0, LoadDense, LoadDense, EpiRms4>;
+using B2wOp = GemmOp<64, true, true, 0, 0, LoadIm2col, LoadDense, EpiF32T>;
+using B2dOp = GemmOp<64, false, true, 0, 2, LoadTConvP, LoadWeightTP, EpiMaskP>;
+using B1wOp = GemmOp<64, true, true, 3, 0, LoadFrames, LoadDense, EpiF32T>;
+
+// B4w + RMSProp: dW4[j][k] = sum_b dh1[b][j] x3[b][k] (contraction over the batch),
+// centered RMSProp applied in the epilogue (no fp32 gradient round trip)
+template <class EP>
+static GemmArgs<LoadDense, LoadDense, EP> args_b4w_rms(const pq_learn_args *la, int n, const WS &w) {
+    const pq_net &th = la->theta;
+    GemmArgs<LoadDense, LoadDense, EP> g{};
+    g.a[0] = LoadDense{w.dh1T, 512, n, w.n8};
+    g.b[0] = LoadDense{w.act3[0], n, 3136, 3136};
+    EP e{};
+    e.p = th.master, e.m = la->opt.m, e.v = la->opt.v;
+    e.p2 = la->theta_out.master, e.m2 = la->opt_out.m, e.v2 = la->opt_out.v;
+    e.shadow = (bf16 *)la->theta_out.shadow;
+    e.grad_out = la->grad_out, e.flag = la->nonfinite, e.counter = w.upd_cur;
+    e.lr = la->lr, e.rho = la->rho, e.kappa = la->kappa;
+    e.M = 512, e.N = 3136, e.pbase = P_W4, e.sbase = S_W4;
+    g.e[0] = e;
+    g.M = 512, g.N = 3136, g.K = n, g.kc_per_split = (n + 63) / 64, g.splits = 1, g.ones_at = -1;
+    return g;
+}
+// B3w: dW3^T[k][o] = sum_m P3[m][k] dY3[m][o]; row 576 = ones -> bias grad
+static B3wOp::Args args_b3w(const WS &w, int n, int *s3) {
+    B3wOp::Args g{};
+    g.a[0] = im2col(w.act2[0], n, 9, 9, 64, 3, 1, 7, 7);
+    g.b[0] = LoadDense{w.dY3, n * 49, 64, 64};
+    g.e[0] = EpiF32T{w.part3, 577, 64, 577, (size_t)64 * 577};
+    const int nch = (n * 49 + 63) / 64;
+    g.kc_per_split = choose_kc(nch, 5, s3);
+    g.M = 577, g.N = 64, g.K = n * 49, g.splits = *s3, g.ones_at = 576, g.ones_extent = n * 49;
+    return g;
+}
+// B3d: dY2 = relu'(x2) * transposed conv3(dY3)
+static B3dOp::Args args_b3d(const bf16 *sh, const WS &w, int n) {
+    B3dOp::Args g{};
+    g.a[0] = tconv(w.dY3, n, 9, 9, 7, 7, 64, 3);
+    g.b[0] = weight_t(sh + S_W3, 64, 3, 64);
+    g.e[0] = EpiMask{w.dY2, w.act2[0], n * 81, 64, 64};
+    g.M = n * 81, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
+    return g;
+}
+// B2w: dW2^T[k][o] = sum_m P2[m][k] dY2[m][o]; row 512 = ones -> bias grad
+static B2wOp::Args args_b2w(const WS &w, int n, int *s2) {
+    B2wOp::Args g{};
+    g.a[0] = im2col(w.act1[0], n, 20, 20, 32, 4, 2, 9, 9);
+    g.b[0] = LoadDense{w.dY2, n * 81, 64, 64};
+    g.e[0] = EpiF32T{w.part2, 513, 64, 513, (size_t)64 * 513};
+    const int nch = (n * 81 + 63) / 64;
+    g.kc_per_split = choose_kc(nch, 5, s2);
+    g.M = 513, g.N = 64, g.K = n * 81, g.splits = *s2, g.ones_at = 512, g.ones_extent = n * 81;
+    return g;
+}
+// B2d: dY1 = relu'(x1) * transposed conv2(dY2), stride 2 split into the 4 input parity
+// classes -> K = 4 taps x 64 per class instead of 16 x 64
+static B2dOp::Args args_b2d(const bf16 *sh, const WS &w, int n) {
+    const int tpc = (n * 100 + 127) / 128;
+    B2dOp::Args g{};
+    g.a[0] = tconv_p(w.dY2, n, 10, 10, 9, 9, 64, tpc);
+    g.b[0] = weight_tp(sh + S_W2, 64, 4, 32, tpc);
+    g.e[0] = epi_mask_p(w.dY1, w.act1[0], n, 10, 10, 32, tpc);
+    g.M = 4 * tpc * 128, g.N = 32, g.K = 256, g.kc_per_split = 4, g.splits = 1, g.ones_at = -1;
+    return g;
+}
+// B1w: dW1^T[k][o] = sum_m P1[m][k] dY1[m][o] over uint8 frames; row 256 = ones
+static B1wOp::Args args_b1w(const pq_learn_args *la, const WS &w, int n, int *s1) {
+    B1wOp::Args g{};
+    FwdInput in{la->ring, la->records, la->idx ? la->idx : w.idx_cur, nullptr, n, REC_INTS, 0};
+    g.a[0] = frames_loader(in, n);
+    g.b[0] = LoadDense{w.dY1, n * 400, 32, 32};
+    g.e[0] = EpiF32T{w.part1, 257, 32, 257, (size_t)32 * 257};
+    const int nch = (n * 400 + 63) / 64;
+    g.kc_per_split = choose_kc(nch, 3, s1, (TABLE_SAMPLES - 2) * 400 / 64);
+    g.M = 257, g.N = 32, g.K = n * 400, g.splits = *s1, g.ones_at = 256, g.ones_extent = n * 400;
+    return g;
+}
+// B4d: dY3[b][k] = relu'(x3) * sum_j W4[j][k] dh1[b][j]   (D[k][b], MN-major W4)
+static int launch_b4d(const pq_net &th, int n, const WS &w, cudaStream_t st) {
+    if (use_tma(n))  // unswapped on the TMA engine: D[b][k], W4 as MN-major B
+        return tma_fc1_dgrad(th, w.dh1_bf, w.act3[0], w.dY3, n, st);
+    GemmArgs<LoadDense, LoadDense, EpiMaskT> g{};
+    g.a[0] = LoadDense{(const bf16 *)th.shadow + S_W4, 512, 3136, 3136};
+    g.b[0] = LoadDense{w.dh1_bf, n, 512, 512};
+    g.e[0] = EpiMaskT{w.dY3, w.act3[0], 3136, n, 3136};
+    g.M = 3136, g.N = n, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
+    PQ_CHECK((launch_bn<LoadDense, LoadDense, EpiMaskT, true, false, 1>(choose_bn(n), g, 1, st)), "fc1 dgrad");
+    return 0;
+}
+static OptArgs opt_args(const pq_learn_args *la, int n, const WS &w) {
+    const pq_net &th = la->theta;
+    OptArgs o{};
+    o.p = th.master, o.m = la->opt.m, o.v = la->opt.v;
+    o.p2 = la->theta_out.master, o.m2 = la->opt_out.m, o.v2 = la->opt_out.v;
+    o.shadow = (bf16 *)la->theta_out.shadow;
+    o.part1 = w.part1, o.part2 = w.part2, o.part3 = w.part3, o.grad4 = nullptr;
+    o.dh1 = w.dh1, o.h1 = w.h1, o.td = w.td, o.act = w.act;
+    o.n = n, o.A = la->actions;
+    o.lr = la->lr, o.rho = la->rho, o.kappa = la->kappa;
+    o.flag = la->nonfinite, o.counter = w.upd_cur;
+    o.grad_out = la->grad_out;
+    o.total = n_params(la->actions);
+    o.w1_perm = 1;  // both engines produce conv1's weight-gradient rows in the permuted K order
+    return o;
+}
+
+// the optimizer over [lo1, hi1) u [lo2, hi2) as one part of a fused launch
+struct OptOp {
+    static constexpr bool GEMM = false, TABLE = false;
+    static constexpr int SMEM = 0, STAGES = 1;
+    static constexpr uint32_t TMEM_COLS = 32;
+    using Launch = OptArgs;
+    static int ctas(const OptArgs &a) { return (int)(((a.hi1 - a.lo1) + (a.hi2 - a.lo2) + 255) / 256); }
+    PQ_DEV static void run(const OptArgs &a, int lin, TileRing &) {
+        griddep_wait();
+        griddep_launch();
+        const int64_t t = (int64_t)lin * 256 + threadIdx.x;
+        const int64_t n1 = a.hi1 - a.lo1;
+        const int64_t i = t < n1 ? a.lo1 + t : a.lo2 + (t - n1);
+        if (t < n1 || i < a.hi2) opt_param(a, i, a.counter ? *a.counter : 0);
+    }
+};
+
+// Single-stream learner backward (cp.async engine, PQ_FUSED, default on below batch
+// 128): every launch chains to the next by PDL; the weight-gradient branch rides in
+// the critical-path launches as extra CTAs:
+//   B4d | {B3d, B3w, B4w+RMSProp} | {B2d, B2w} | {B1w, update of conv2/conv3/fc} | update of conv1
+// Each part reads only what the launch before it (or older ones) wrote: B4w rewrites
+// the W4 shadow after B4d read it; the conv2/conv3 update follows B3d / B2d, the last
+// readers of W3 / W2; conv1's update follows B1w.  The step counter advances in the head.
+static bool fused_backward(int n, const pq_learn_args *la, float *grad_only) {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("PQ_FUSED");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1 && !use_tma(n) && !grad_only && n <= 2 * FC_CHUNK;
+}
+
+static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStream_t st) {
+    const pq_net &th = la->theta;
+    const bf16 *sh = (const bf16 *)th.shadow;
+    int s1 = 1, s2 = 1, s3 = 1;
+    if (int rc = launch_b4d(th, n, w, st)) return rc;
+    {
+        FusedArgs<B3dOp, B3wOp, B4wOp> f{};
+        f.p0 = B3dOp::make(args_b3d(sh, w, n));
+        f.p1 = B3wOp::make(args_b3w(w, n, &s3));
+        f.p2 = B4wOp::make(args_b4w_rms<EpiRms4>(la, n, w));
+        f.n0 = B3dOp::ctas(f.p0, 1), f.n1 = B3wOp::ctas(f.p1, 1);
+        PQ_CHECK(launch_fused(f, B4wOp::ctas(f.p2, 1), st), "conv3 dgrad | conv3 wgrad | fc1 wgrad+rmsprop");
+    }
+    {
+        FusedArgs<B2dOp, B2wOp, NoOp> f{};
+        f.p0 = B2dOp::make(args_b2d(sh, w, n));
+        f.p1 = B2wOp::make(args_b2w(w, n, &s2));
+        f.n0 = B2dOp::ctas(f.p0, 1), f.n1 = B2wOp::ctas(f.p1, 1);
+        PQ_CHECK(launch_fused(f, 0, st), "conv2 dgrad | conv2 wgrad");
+    }
+    OptArgs o = opt_args(la, n, w);
+    o.s1 = s1, o.s2 = s2, o.s3 = s3;
+    {
+        FusedArgs<B1wOp, OptOp, NoOp> f{};
+        f.p0 = B1wOp::make(args_b1w(la, w, n, &s1));
+        o.s1 = s1;
+        OptArgs os = o;
+        os.lo1 = P_W2, os.hi1 = P_W4, os.lo2 = P_B4, os.hi2 = os.total;
+        f.p1 = os;
+        f.n0 = B1wOp::ctas(f.p0, 1), f.n1 = OptOp::ctas(os);
+        PQ_CHECK(launch_fused(f, 0, st), "conv1 wgrad | update conv2, conv3, fc");
+    }
+    o.lo1 = P_W1, o.hi1 = P_W2, o.lo2 = P_W2, o.hi2 = P_W2;
+    PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((P_W2 - P_W1 + 255) / 256)), dim3(256), 0, st, o),
+             "optimizer (conv1)");
+    return 0;
+}
+
+// grad_only != NULL: write the summed gradient of every parameter there instead of
+// updating theta / opt (the data-parallel learner all-reduces it, then pq_rmsprop_apply)
 static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cudaStream_t st,
                                float *grad_only = nullptr) {
+    if (fused_backward(n, la, grad_only)) return backward_fused(la, n, w, st);
     const pq_net &th = la->theta;
     const bf16 *sh = (const bf16 *)th.shadow;
     int s1 = 1, s2 = 1, s3 = 1;
     Fork *fk = nullptr;
     if (int rc = get_fork(&fk)) return rc;
     cudaStream_t side = fk->side, side2 = fk->side2;
-    if (use_tma(n)) {  // B4d unswapped on the TMA engine: D[b][k], W4 as MN-major B
-        if (int rc = tma_fc1_dgrad(th, w.dh1_bf, w.act3[0], w.dY3, n, st)) return rc;
-    } else {  // B4d: dY3[b][k] = relu'(x3) * sum_j W4[j][k] dh1[b][j]   (D[k][b], MN-major W4)
-        GemmArgs<LoadDense, LoadDense, EpiMaskT> g{};
-        g.a[0] = LoadDense{sh + S_W4, 512, 3136, 3136};
-        g.b[0] = LoadDense{w.dh1_bf, n, 512, 512};
-        g.e[0] = EpiMaskT{w.dY3, w.act3[0], 3136, n, 3136};
-        g.M = 3136, g.N = n, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_bn<LoadDense, LoadDense, EpiMaskT, true, false, 1>(choose_bn(n), g, 1, st)),
-                 "fc1 dgrad");
-    }
+    if (int rc = launch_b4d(th, n, w, st)) return rc;
     // fork after the fc1 data gradient: the fused fc1 update below rewrites the W4
     // shadow that B4d reads, so it must not start earlier
     PQ_CHECK(cudaEventRecord(fk->ev[1], st), "fork1");
@@ -570,86 +745,31 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         g.e[0] = EpiF32{grad_only + P_W4, 512, 3136, 3136, 0};
         g.M = 512, g.N = 3136, g.K = n, g.kc_per_split = (n + 63) / 64, g.splits = 1, g.ones_at = -1;
         PQ_CHECK((launch_gemm<64, false, true, 4>(g, 1, side)), "fc1 wgrad");
-    } else {  // B4w + RMSProp: dW4[j][k] = sum_b dh1[b][j] x3[b][k] (contraction over the batch),
-       // centered RMSProp applied in the epilogue (no fp32 gradient round trip)
-        GemmArgs<LoadDense, LoadDense, EpiRms> g{};
-        g.a[0] = LoadDense{w.dh1T, 512, n, w.n8};
-        g.b[0] = LoadDense{w.act3[0], n, 3136, 3136};
-        EpiRms e{};
-        e.p = th.master, e.m = la->opt.m, e.v = la->opt.v;
-        e.p2 = la->theta_out.master, e.m2 = la->opt_out.m, e.v2 = la->opt_out.v;
-        e.shadow = (bf16 *)la->theta_out.shadow;
-        e.grad_out = la->grad_out, e.flag = la->nonfinite, e.counter = w.upd_cur;
-        e.lr = la->lr, e.rho = la->rho, e.kappa = la->kappa;
-        e.M = 512, e.N = 3136, e.pbase = P_W4, e.sbase = S_W4;
-        // (the cp.async engine: its staged RMSProp epilogue walks the tile with all 8 warps)
-        g.e[0] = e;
-        g.M = 512, g.N = 3136, g.K = n, g.kc_per_split = (n + 63) / 64, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<64, false, true, 4>(g, 1, side)), "fc1 wgrad+rmsprop");
+    } else {  // (the cp.async engine: its staged RMSProp epilogue walks the tile with all 8 warps)
+        PQ_CHECK((launch_gemm<64, false, true, 4>(args_b4w_rms<EpiRms>(la, n, w), 1, side)), "fc1 wgrad+rmsprop");
     }
-    {  // B3w: dW3^T[k][o] = sum_m P3[m][k] dY3[m][o]; row 576 = ones -> bias grad
-        GemmArgs<LoadIm2col, LoadDense, EpiF32T> g{};
-        g.a[0] = im2col(w.act2[0], n, 9, 9, 64, 3, 1, 7, 7);
-        g.b[0] = LoadDense{w.dY3, n * 49, 64, 64};
-        g.e[0] = EpiF32T{w.part3, 577, 64, 577, (size_t)64 * 577};
-        int nch = (n * 49 + 63) / 64;
-        g.kc_per_split = choose_kc(nch, 5, &s3);
-        g.M = 577, g.N = 64, g.K = n * 49, g.splits = s3, g.ones_at = 576, g.ones_extent = n * 49;
+    {
+        B3wOp::Args g = args_b3w(w, n, &s3);
         if (use_tma(n)) {
             if (int rc = tma_conv3_wgrad(w.act2[0], w.dY3, w.part3, g.kc_per_split, s3, n, side2)) return rc;
         } else {
             PQ_CHECK((launch_gemm<64, true, true>(g, 1, side2)), "conv3 wgrad");
         }
     }
-    {  // B3d: dY2 = relu'(x2) * transposed conv3(dY3)
-        GemmArgs<LoadTConv, LoadWeightT, EpiMask> g{};
-        g.a[0] = tconv(w.dY3, n, 9, 9, 7, 7, 64, 3);
-        g.b[0] = weight_t(sh + S_W3, 64, 3, 64);
-        g.e[0] = EpiMask{w.dY2, w.act2[0], n * 81, 64, 64};
-        g.M = n * 81, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
-        if (use_tma(n)) {
-            if (int rc = tma_conv3_dgrad(th, w.dY3, w.act2[0], w.dY2, n, st)) return rc;
-        } else {
-            PQ_CHECK((launch_gemm<64, false, true, 0, 2>(g, 1, st)), "conv3 dgrad");
-        }
+    if (use_tma(n)) {
+        if (int rc = tma_conv3_dgrad(th, w.dY3, w.act2[0], w.dY2, n, st)) return rc;
+    } else {
+        PQ_CHECK((launch_gemm<64, false, true, 0, 2>(args_b3d(sh, w, n), 1, st)), "conv3 dgrad");
     }
     PQ_CHECK(cudaEventRecord(fk->ev[2], st), "fork2");
     PQ_CHECK(cudaStreamWaitEvent(side2, fk->ev[2], 0), "fork2 wait");
-    {  // B2w
-        GemmArgs<LoadIm2col, LoadDense, EpiF32T> g{};
-        g.a[0] = im2col(w.act1[0], n, 20, 20, 32, 4, 2, 9, 9);
-        g.b[0] = LoadDense{w.dY2, n * 81, 64, 64};
-        g.e[0] = EpiF32T{w.part2, 513, 64, 513, (size_t)64 * 513};
-        int nch = (n * 81 + 63) / 64;
-        g.kc_per_split = choose_kc(nch, 5, &s2);
-        g.M = 513, g.N = 64, g.K = n * 81, g.splits = s2, g.ones_at = 512, g.ones_extent = n * 81;
-        PQ_CHECK((launch_gemm<64, true, true>(g, 1, side2)), "conv2 wgrad");
+    PQ_CHECK((launch_gemm<64, true, true>(args_b2w(w, n, &s2), 1, side2)), "conv2 wgrad");
+    if (use_tma(n)) {
+        if (int rc = tma_conv2_dgrad(th, w.dY2, w.act1[0], w.dY1, n, st)) return rc;
+    } else {
+        PQ_CHECK((launch_gemm<64, false, true, 0, 2>(args_b2d(sh, w, n), 1, st)), "conv2 dgrad");
     }
-    {  // B2d: dY1 = relu'(x1) * transposed conv2(dY2), stride 2 split into the 4 input
-       // parity classes -> K = 4 taps x 64 per class instead of 16 x 64
-        const int tpc = (n * 100 + 127) / 128;
-        GemmArgs<LoadTConvP, LoadWeightTP, EpiMaskP> g{};
-        g.a[0] = tconv_p(w.dY2, n, 10, 10, 9, 9, 64, tpc);
-        g.b[0] = weight_tp(sh + S_W2, 64, 4, 32, tpc);
-        g.e[0] = epi_mask_p(w.dY1, w.act1[0], n, 10, 10, 32, tpc);
-        g.M = 4 * tpc * 128, g.N = 32, g.K = 256, g.kc_per_split = 4, g.splits = 1, g.ones_at = -1;
-        if (use_tma(n)) {
-            if (int rc = tma_conv2_dgrad(th, w.dY2, w.act1[0], w.dY1, n, st)) return rc;
-        } else {
-            PQ_CHECK((launch_gemm<64, false, true, 0, 2>(g, 1, st)), "conv2 dgrad");
-        }
-    }
-    OptArgs o{};
-    o.p = th.master, o.m = la->opt.m, o.v = la->opt.v;
-    o.p2 = la->theta_out.master, o.m2 = la->opt_out.m, o.v2 = la->opt_out.v;
-    o.shadow = (bf16 *)la->theta_out.shadow;
-    o.part1 = w.part1, o.part2 = w.part2, o.part3 = w.part3, o.grad4 = nullptr;
-    o.dh1 = w.dh1, o.h1 = w.h1, o.td = w.td, o.act = w.act;
-    o.n = n, o.A = la->actions;
-    o.lr = la->lr, o.rho = la->rho, o.kappa = la->kappa;
-    o.flag = la->nonfinite, o.counter = w.upd_cur;
-    o.grad_out = la->grad_out;
-    o.total = n_params(la->actions);
+    OptArgs o = opt_args(la, n, w);
     if (fc_chunks) o.fcpart = w.fcpart, o.fcchunks = fc_chunks;
     const bool split_opt = split_optimizer();
     if (!grad_only && split_opt) {
@@ -665,22 +785,14 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((cnt + 255) / 256)), dim3(256), 0, side2, os),
                  "optimizer (conv2, conv3, fc)");
     }
-    {  // B1w: dW1^T[k][o] = sum_m P1[m][k] dY1[m][o] over uint8 frames; row 256 = ones
-        GemmArgs<LoadFrames, LoadDense, EpiF32T> g{};
-        FwdInput in{la->ring, la->records, la->idx ? la->idx : w.idx_cur, nullptr, n, REC_INTS, 0};
-        g.a[0] = frames_loader(in, n);
-        g.b[0] = LoadDense{w.dY1, n * 400, 32, 32};
-        g.e[0] = EpiF32T{w.part1, 257, 32, 257, (size_t)32 * 257};
-        int nch = (n * 400 + 63) / 64;
-        g.kc_per_split = choose_kc(nch, 3, &s1, (TABLE_SAMPLES - 2) * 400 / 64);
-        g.M = 257, g.N = 32, g.K = n * 400, g.splits = s1, g.ones_at = 256, g.ones_extent = n * 400;
+    {
+        B1wOp::Args g = args_b1w(la, w, n, &s1);
         if (use_tma(n) && w.s2d) {  // TMA im2col of the space-to-depth stacks
             const int nframes = la->ext_targets ? 4 : 5;
             if (int rc = tma_conv1_wgrad(w.s2d, nframes, w.dY1, w.part1, g.kc_per_split, s1, n, st)) return rc;
         } else {
             PQ_CHECK((launch_gemm<64, true, true>(g, 1, st)), "conv1 wgrad");
         }
-        o.w1_perm = 1;  // both engines produce the rows in the permuted K order
     }
     if (!grad_only && split_opt) {  // conv1's update (main stream)
         o.s1 = s1, o.s2 = s2, o.s3 = s3;
@@ -760,9 +872,10 @@ int pq_timeline(int on, unsigned long long *out, int *count) {
         *count = h.n < 256 ? h.n : 256;
         memcpy(out, h.t, sizeof(h.t));
     }
-    Timeline z{};
+    static Timeline z;
+    memset(&z, 0, sizeof(z));
     z.on = on;
-    PQ_CHECK(cudaMemcpyToSymbol(g_tl, &z, sizeof(int) * 2), "timeline reset");
+    PQ_CHECK(cudaMemcpyToSymbol(g_tl, &z, sizeof(Timeline)), "timeline reset");
     return 0;
 }
 const char *pq_last_error(void) { return g_err; }
@@ -837,7 +950,7 @@ int pq_learn_step(const pq_learn_args *la, void *stream) {
     const int groups = la->ext_targets ? 1 : 2;
     int rc = forward_gemms(nets, ins, groups, n, w, st);
     if (rc) return rc;
-    rc = head(nets, groups, n, la->actions, w, 1, la, st);
+    rc = head(nets, groups, n, la->actions, w, 1, la, st, split_optimizer() || fused_backward(n, la, nullptr));
     if (rc) return rc;
     return backward_and_update(la, n, w, st);
 }
@@ -857,7 +970,7 @@ int pq_learn_grad(const pq_learn_args *la, float *grad, void *stream) {
     const int groups = la->ext_targets ? 1 : 2;
     int rc = forward_gemms(nets, ins, groups, n, w, st);
     if (rc) return rc;
-    rc = head(nets, groups, n, la->actions, w, 1, la, st);
+    rc = head(nets, groups, n, la->actions, w, 1, la, st, split_optimizer());
     if (rc) return rc;
     return backward_and_update(la, n, w, st, grad);
 }

@@ -42,13 +42,21 @@ torch.cuda.synchronize()
 lib.pq_timeline(0, ctypes.addressof(out), ctypes.addressof(cnt))
 t = np.array(out).reshape(256, 12)[: cnt.value].astype(np.int64)
 t0 = t[:, 0].min()
-print(f"batch {B}: {cnt.value} probed launches in one replay of {nl} steps, "
+ends = {}  # (grid, tag) -> end times of the last CTA, in order
+for rr in sorted(t, key=lambda x: x[0]):
+    if chr(int(rr[11])) == "E":
+        ends.setdefault((tuple(rr[8:11]), int(rr[7])), []).append(rr[0])
+print(f"batch {B}: {cnt.value} probe records in one replay of {nl} steps, "
       f"{e0.elapsed_time(e1) * 1e3 / nl:.1f} us/step (CUDA events)")
-print("tag grid            start -> stamps (us from the first start) | durations")
+print("tag grid       last-CTA-end | start -> CTA-0 stamps (us from the first start) | durations")
 for rr in sorted(t, key=lambda x: x[0]):
     tag = chr(int(rr[11])) if rr[11] else "?"
+    if tag == "E":
+        continue
+    q = ends.get((tuple(rr[8:11]), ord(tag)), [])
+    end = f"{(q.pop(0) - t0) / 1000:7.1f}" if q else "      ?"
     v = [x for x in rr[:8] if x > 0]
     rel = [(x - t0) / 1000 for x in v]
     d = np.diff(v) / 1000
     grid = f"{rr[8]}x{rr[9]}x{rr[10]}"
-    print(f"{tag} {grid:>12}  " + " ".join(f"{x:6.1f}" for x in rel), "|", " ".join(f"{x:4.1f}" for x in d))
+    print(f"{tag} {grid:>10} {end} | " + " ".join(f"{x:6.1f}" for x in rel), "|", " ".join(f"{x:4.1f}" for x in d))
