@@ -875,6 +875,25 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
         }
     };
 
+    // frame-table operands: the sample window of the rows this CTA reads -- MN rows
+    // (K-major) or the split's contraction range (MN-major)
+    auto fill_table = [&] {
+        if constexpr (LA::TABLE) {
+            const int lo = AMN ? kb0 * 64 : m0;
+            const int hi = AMN ? max(lo, kb1 * 64 - 1) : m0 + 127;
+            cx.tb = lo / 400;
+            int last = min(hi / 400, cx.tb + TABLE_SAMPLES - 1);
+            la.fill(cx.tb, last, R.table);
+        }
+    };
+    // PF == 1 with a frame table (the learner's conv1 forward): the replay frames and
+    // records are not written by the predecessor either, so the table is built and the
+    // first A chunks requested before the dependency wait
+    constexpr bool EARLY_TABLE = LA::TABLE && PF == 1;
+    if constexpr (EARLY_TABLE) {
+        fill_table();
+        __syncthreads();
+    }
     // weights (never written by the previous producer) go out before the dependency wait
 #pragma unroll
     for (int s = 0; s < PRE; ++s) {
@@ -886,15 +905,7 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
     }
     hook();
     if (tl) tl_t[tl_i++] = gtime();  // 1: predecessor done
-    if constexpr (LA::TABLE) {
-        // sample window of the rows this CTA reads: MN rows (K-major) or the split's
-        // contraction range (MN-major)
-        const int lo = AMN ? kb0 * 64 : m0;
-        const int hi = AMN ? max(lo, kb1 * 64 - 1) : m0 + 127;
-        cx.tb = lo / 400;
-        int last = min(hi / 400, cx.tb + TABLE_SAMPLES - 1);
-        la.fill(cx.tb, last, R.table);
-    }
+    if constexpr (LA::TABLE && !EARLY_TABLE) fill_table();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();

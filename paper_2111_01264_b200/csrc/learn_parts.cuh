@@ -52,9 +52,12 @@ __device__ __forceinline__ float warp_sum(float v) {
 constexpr int HEAD_THREADS = 256;
 
 // One sample b (one 256-thread CTA).  S = fc1 split count; every global load of a
-// phase is independent so they are all in flight together.
-template <int S>
-PQ_DEV void head_sample(const HeadArgs &a, int b) {
+// phase is independent so they are all in flight together.  Everything that does not
+// depend on the fc1 forward -- the sampled record, the fc1 / fc2 biases, the fc2
+// weights (prefetched into L1) -- is requested before `wait()` (the kernel's
+// griddepcontrol.wait): they were written four or more launches back.
+template <int S, class Wait = NoHook>
+PQ_DEV void head_sample(const HeadArgs &a, int b, Wait wait = Wait{}) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     __shared__ float hs[2][512];
     __shared__ float qs[2][MAX_ACTIONS];
@@ -70,6 +73,19 @@ PQ_DEV void head_sample(const HeadArgs &a, int b) {
         if (a.idx_cur) a.idx_cur[b] = slot;
         if (a.upd_cur && b == 0) *a.upd_cur = a.counter ? *a.counter : 0;
     }
+    float b4[2][2], b5[2][4];
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        const int gg = g < a.groups ? g : 0;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) b4[g][i] = (*(a.master[gg] + P_B4 + tid + HEAD_THREADS * i));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) b5[g][u] = (*(a.master[gg] + p_b5(a.A) + min(warp + 8 * u, a.A - 1)));
+        // fc2 weights: A x 512 floats = A x 16 lines of 128 B per network
+        for (int l = tid; l < a.A * 16; l += HEAD_THREADS)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.master[gg] + P_W5 + l * 32));
+    }
+    wait();
     {
         float v[2][2][S + 1];
 #pragma unroll
@@ -81,7 +97,7 @@ PQ_DEV void head_sample(const HeadArgs &a, int b) {
                 const float *P = a.part[gg] + (size_t)b * 512 + j;
 #pragma unroll
                 for (int sp = 0; sp < S; ++sp) v[g][i][sp] = (*(P + (size_t)sp * a.n * 512));
-                v[g][i][S] = (*(a.master[gg] + P_B4 + j));
+                v[g][i][S] = b4[g][i];
             }
 #pragma unroll
         for (int g = 0; g < 2; ++g)
@@ -95,7 +111,9 @@ PQ_DEV void head_sample(const HeadArgs &a, int b) {
             }
     }
     __syncthreads();
-    for (int g = 0; g < a.groups; ++g) {
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        if (g >= a.groups) break;
         const float *w5 = a.master[g] + P_W5;
         float wv[4][16];
 #pragma unroll
@@ -112,7 +130,7 @@ PQ_DEV void head_sample(const HeadArgs &a, int b) {
             for (int t = 0; t < 16; ++t) acc += wv[u][t] * hs[g][lane + 32 * t];
             acc = warp_sum(acc);
             if (lane == 0 && aa < a.A) {
-                float q = acc + (*(a.master[g] + p_b5(a.A) + aa));
+                float q = acc + b5[g][u];
                 qs[g][aa] = q;
                 a.q_out[((size_t)g * a.n + b) * a.A + aa] = q;
                 if (a.q_copy) a.q_copy[((size_t)g * a.n + b) * a.A + aa] = q;

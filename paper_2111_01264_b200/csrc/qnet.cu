@@ -271,8 +271,11 @@ static int conv23(const pq_net *nets, int groups, int n, const WS &w, cudaStream
 }
 
 // F1..F4 for `groups` parameter sets (group 0 / 1 = online / target in the learner)
+// early_frames: the learner -- its frames / records are never written by the kernel
+// before it (only the acting kernel writes frames, and it triggers its dependents
+// early), so conv1 builds its frame table and requests frames before the wait
 static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, int n, const WS &w,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool early_frames = false) {
     if (use_tma(n) && w.s2d) {  // F1 on the TMA engine over the space-to-depth stacks
         // learner: frames f0..f4 once, online = channels 0..63, target = 16..79
         const int nframes = groups == 2 ? 5 : 4;
@@ -290,7 +293,10 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
             g.e[q] = EpiBiasRelu{w.act1[q], nets[q].master + P_B1, n * 400, 32, 32, 1.0f / 255.0f};
         }
         g.M = n * 400, g.N = 32, g.K = 256, g.kc_per_split = 4, g.splits = 1, g.ones_at = -1;
-        PQ_CHECK((launch_gemm<32, false, false, 3>(g, groups, st)), "conv1 forward");
+        if (early_frames)
+            PQ_CHECK((launch_gemm<32, false, false, 3, 1>(g, groups, st)), "conv1 forward");
+        else
+            PQ_CHECK((launch_gemm<32, false, false, 3>(g, groups, st)), "conv1 forward");
     }
     bf16 *a2[2] = {w.act2[0], w.act2[1]}, *a3[2] = {w.act3[0], w.act3[1]};
     float *pt[2] = {w.fc1part[0], w.fc1part[1]};
@@ -374,10 +380,11 @@ __device__ __forceinline__ void last_block_bump(int32_t *counter, uint32_t *done
 // optimizer can be split across streams without racing on the counter.
 __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a, int32_t *bump, uint32_t *done) {
     TlProbe tp;
-    griddep_wait();
-    griddep_launch();
-    tp.waited();
-    head_sample<FC1_SPLITS>(a, blockIdx.x);
+    head_sample<FC1_SPLITS>(a, blockIdx.x, [&] {
+        griddep_wait();
+        griddep_launch();
+        tp.waited();
+    });
     if (bump) last_block_bump(bump, done);
     tp.done('H');
 }
@@ -538,7 +545,7 @@ using B3dOp = GemmOp<64, false, true, 0, 2, LoadTConv, LoadWeightT, EpiMask>;
 using B4wOp = GemmOp<64, false, true, 4, 0, LoadDense, LoadDense, EpiRms4>;
 using B2wOp = GemmOp<64, true, true, 0, 0, LoadIm2col, LoadDense, EpiF32T>;
 using B2dOp = GemmOp<64, false, true, 0, 2, LoadTConvP, LoadWeightTP, EpiMaskP>;
-using B1wOp = GemmOp<64, true, true, 3, 0, LoadFrames, LoadDense, EpiF32T>;
+using B1wOp = GemmOp<64, true, true, 3, 1, LoadFrames, LoadDense, EpiF32T>;  // frames before the wait
 
 // B4w + RMSProp: dW4[j][k] = sum_b dh1[b][j] x3[b][k] (contraction over the batch),
 // centered RMSProp applied in the epilogue (no fp32 gradient round trip)
@@ -948,7 +955,7 @@ int pq_learn_step(const pq_learn_args *la, void *stream) {
     FwdInput ins[2] = {{la->ring, la->records, map, counter, n, REC_INTS, 0},
                        {la->ring, la->records, map, counter, n, REC_INTS, 1}};
     const int groups = la->ext_targets ? 1 : 2;
-    int rc = forward_gemms(nets, ins, groups, n, w, st);
+    int rc = forward_gemms(nets, ins, groups, n, w, st, true);
     if (rc) return rc;
     rc = head(nets, groups, n, la->actions, w, 1, la, st, split_optimizer() || fused_backward(n, la, nullptr));
     if (rc) return rc;
@@ -968,7 +975,7 @@ int pq_learn_grad(const pq_learn_args *la, float *grad, void *stream) {
     FwdInput ins[2] = {{la->ring, la->records, map, counter, n, REC_INTS, 0},
                        {la->ring, la->records, map, counter, n, REC_INTS, 1}};
     const int groups = la->ext_targets ? 1 : 2;
-    int rc = forward_gemms(nets, ins, groups, n, w, st);
+    int rc = forward_gemms(nets, ins, groups, n, w, st, true);
     if (rc) return rc;
     rc = head(nets, groups, n, la->actions, w, 1, la, st, split_optimizer());
     if (rc) return rc;
