@@ -293,8 +293,16 @@ __device__ __forceinline__ void rms(const OptArgs &a, float g, float m, float v,
 }
 
 // one parameter's update; upd = the update id reported on a non-finite gradient
-__device__ __forceinline__ void opt_param(const OptArgs &a, int64_t i, int upd) {
-    const float m = (*(a.m + i)), v = (*(a.v + i)), p = (*(a.p + i));
+// a parameter's optimizer state, loaded ahead of the gradient (the one-shot optimizer
+// kernels issue these loads before their dependency wait: the previous update wrote them)
+struct OptPre {
+    float m, v, p;
+};
+__device__ __forceinline__ OptPre opt_load(const OptArgs &a, int64_t i) {
+    return OptPre{(*(a.m + i)), (*(a.v + i)), (*(a.p + i))};
+}
+__device__ __forceinline__ void opt_param(const OptArgs &a, int64_t i, int upd, const OptPre &pre) {
+    const float m = pre.m, v = pre.v, p = pre.p;
     int64_t sh;
     const float g = grad_of(a, i, sh);
     float m2, v2, p2;
@@ -306,6 +314,9 @@ __device__ __forceinline__ void opt_param(const OptArgs &a, int64_t i, int upd) 
     if (i < P_B1) a.shadow[S_W1P + (i >> 8) * 256 + w1_perm((int)(i & 255))] = __float2bfloat16_rn(p2);
     if (a.grad_out) a.grad_out[i] = g;
     if (!isfinite(g)) atomicMin(a.flag, upd);
+}
+__device__ __forceinline__ void opt_param(const OptArgs &a, int64_t i, int upd) {
+    opt_param(a, i, upd, opt_load(a, i));
 }
 
 }  // namespace pq

@@ -455,13 +455,17 @@ __global__ void __launch_bounds__(512) k_fc2_partials(const float *h1, const flo
 // the parameters in [lo1, hi1) and [lo2, hi2), one per thread (learn_parts.cuh: opt_param)
 __global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
     TlProbe tp;
-    griddep_wait();
-    griddep_launch();
-    tp.waited();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t n1 = a.hi1 - a.lo1;
     const int64_t i = t < n1 ? a.lo1 + t : a.lo2 + (t - n1);
-    if (t < n1 || i < a.hi2) opt_param(a, i, a.counter ? *a.counter : 0);
+    const bool live = t < n1 || i < a.hi2;
+    // optimizer state and update id before the wait (written two or more launches back)
+    const OptPre pre = live ? opt_load(a, i) : OptPre{};
+    const int upd = a.counter ? *a.counter : 0;
+    griddep_wait();
+    griddep_launch();
+    tp.waited();
+    if (live) opt_param(a, i, upd, pre);
     if (a.bump) last_block_bump(a.bump, a.bump_done);
     tp.done('O');
 }
@@ -657,12 +661,15 @@ struct OptOp {
     using Launch = OptArgs;
     static int ctas(const OptArgs &a) { return (int)(((a.hi1 - a.lo1) + (a.hi2 - a.lo2) + 255) / 256); }
     PQ_DEV static void run(const OptArgs &a, int lin, TileRing &) {
-        griddep_wait();
-        griddep_launch();
         const int64_t t = (int64_t)lin * 256 + threadIdx.x;
         const int64_t n1 = a.hi1 - a.lo1;
         const int64_t i = t < n1 ? a.lo1 + t : a.lo2 + (t - n1);
-        if (t < n1 || i < a.hi2) opt_param(a, i, a.counter ? *a.counter : 0);
+        const bool live = t < n1 || i < a.hi2;
+        const OptPre pre = live ? opt_load(a, i) : OptPre{};
+        const int upd = a.counter ? *a.counter : 0;
+        griddep_wait();
+        griddep_launch();
+        if (live) opt_param(a, i, upd, pre);
     }
 };
 
