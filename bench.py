@@ -509,7 +509,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     learn_flop = FLOP_PER_SAMPLE_LEARN * hp.batch_size
     achieved_tf = learn_flop / (learn_ms * 1e-3) / 1e12
     gather_gbs = 80_000 * GATHER_BYTES_PER_TRANSITION / (gather_ms * 1e-3) / 1e9
-    per_epoch_launches = (hp.C // hp.W) * 6 + (hp.C // hp.F) * 14 + 2
+    per_epoch_launches = (hp.C // hp.W) * 5 + (hp.C // hp.F) * 10 + 2
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         threads = len(os.sched_getaffinity(0))
@@ -533,11 +533,11 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             "setup_s": round(setup_s, 2),
         },
         "roofline": {
-            "kernel": "learner step (15 tcgen05 GEMM/head/optimizer launches, batch 32)",
+            "kernel": "learner step (10 launches: 4 forward GEMMs, head, fc1 dgrad, 3 fused dgrad/wgrad/update grids, conv1 update; batch 32)",
             "bound": "tensor", "achieved": achieved_tf, "peak": bf16_burst, "unit": "TFLOP/s",
             "frac": achieved_tf / bf16_burst, "traffic": traffic,
             "traffic_source": "profiles/r1_traffic.json (ncu --set full, dram__bytes_read+write of one "
-                              "step's 14 launches; algorithmic ~47 MB: fc1 RMSProp 28 B/param)",
+                              "step's 10 launches; algorithmic ~47 MB: fc1 RMSProp 28 B/param)",
             "per_launch": f"{learn_flop / 1e9:.3f} GFLOP (68.26 MFLOP/sample x {hp.batch_size}) "
                           f"in {learn_ms * 1e3:.1f} us", "peak_source": peak_src,
         },

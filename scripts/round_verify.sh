@@ -11,8 +11,8 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 3000 -c 400 --csv \
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 1 --warmup 0 --prefill 50000 \
   --capacity 100000 --no-cpu-baseline --no-sweeps > gpurun_out/ncu_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gemm|k_tma_gemm|k_optimizer|k_head" \
-  -s 60 -c 14 -o gpurun_out/full_$TAG python profiles/one_step.py > gpurun_out/ncufull_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gemm|k_fused|k_tma_gemm|k_optimizer|k_head" \
+  -s 30 -c 10 -o gpurun_out/full_$TAG python profiles/one_step.py > gpurun_out/ncufull_$TAG.log 2>&1
 tail -1 gpurun_out/ncufull_$TAG.log
 python - <<PY
 import json
