@@ -348,8 +348,9 @@ def parameter_bytes(params) -> bytes:
 
 def theta_hash(params) -> str:
     """64-bit FNV-1a over parameter_bytes as 16 hex digits (nn.py:223-229), in C."""
-    flat = np.ascontiguousarray(params.flat() if hasattr(params, "flat") else params,
-                                dtype="<f8")
+    if not isinstance(params, np.ndarray):
+        params = params.flat() if hasattr(params, "flat") else params
+    flat = np.ascontiguousarray(params, dtype="<f8")
     h = N.load().pq_theta_hash_f64(flat.ctypes.data, flat.size)
     return f"{h:016x}"
 
