@@ -203,29 +203,29 @@ def run_reference(args, rank: int):
 
 
 # ----------------------------------------------------------------------------- B200 arm
-def time_kernel_isolated(runner, reps: int = 200):
-    """Average device time of one learner step and of its dominant GEMM, eager
-    launches bracketed by CUDA events on the launching stream."""
+def time_learner_graph(runner, epoch: int):
+    """Average device time of one learner step as the bench runs it: one epoch's worth
+    of replays of the captured learner graph (the PDL-chained launches) on the learner
+    stream, CUDA events on that stream; learner state restored afterwards."""
     import torch
 
-    s = torch.cuda.current_stream()
-    saved = [t.clone() for t in (runner.theta.master, runner.theta.shadow, runner.opt.m,
-                                 runner.opt.v, runner.update_counter)]
-    runner.update_counter.zero_()
-    for _ in range(10):
-        runner.learn_step()
-        runner.update_counter.zero_()
+    gl, nl = runner._graphs["learn"]
+    keep = (runner.theta.master, runner.theta.shadow, runner.opt.m, runner.opt.v, runner.update_counter)
+    saved = [t.clone() for t in keep]
+    runner.begin_epoch(epoch)
+    ls = runner.learn_stream
+    ls.wait_stream(torch.cuda.current_stream())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s)
-    for _ in range(reps):
-        runner.learn_step()
-        runner.update_counter.zero_()
-    e1.record(s)
+    with torch.cuda.stream(ls):
+        e0.record(ls)
+        for _ in range(runner.updates // nl):
+            gl.replay()
+        e1.record(ls)
     torch.cuda.synchronize()
-    learn_ms = e0.elapsed_time(e1) / reps
-    for t, v in zip((runner.theta.master, runner.theta.shadow, runner.opt.m, runner.opt.v,
-                     runner.update_counter), saved):
+    learn_ms = e0.elapsed_time(e1) / (runner.updates // nl * nl)
+    for t, v in zip(keep, saved):
         t.copy_(v)
+    torch.cuda.synchronize()
     return learn_ms
 
 
@@ -447,7 +447,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     value = frames / secs
     updates_s = world * args.steps * (hp.C // hp.F) / secs
     # kernel-level measurements (outside the timed region; same inputs)
-    learn_ms = time_kernel_isolated(runner)
+    learn_ms = time_learner_graph(runner, total_epochs)
     gather_ms = time_gather(runner)
     sweeps = {}
     if not args.no_sweeps and world == 1:

@@ -1525,6 +1525,174 @@ int tma_conv1_fwd(const pq_net *nets, const bf16 *s2d, int nframes, const int *c
     return launch_tma<64, false, false>(g, st, "conv1 forward (TMA)");
 }
 
+// ---- conv1 forward as four row-shifted GEMMs over the space-to-depth stacks
+// On the 21 x 21 grid of s2d pixels conv1 (8x8 / 4 over 84 x 84) is a 2 x 2 stride-1
+// conv.  Computed for all 21 x 21 base pixels of a sample (outputs with y or x = 20 are
+// discarded), tap (ty, tx) of GEMM row r reads s2d row r + 21 ty + tx of the same
+// sample, so one TMA box of 152 rows x 64 channels feeds all four taps through UMMA
+// descriptors starting 0, 1, 21 and 22 rows into it -- the SW128 swizzle is a function
+// of the shared-memory address, so any 128-byte row is a valid operand start
+// (scripts/desc_probe.cu) -- instead of four im2col loads (4x less L2 -> SM traffic).
+// The online (channels 0..63) and target (16..79) networks share the box; the target's
+// last K step (channels 64..79) comes from a second box at channel 64.  Same MMA order
+// (tap, 16-channel step) as the im2col kernels, so the outputs are bit-identical.
+constexpr int C1_ROWS = 152, C1_BOX = C1_ROWS * 128, C1_STAGES = 4, C1_W = 32 * 128;
+constexpr int C1_SMEM = 1024 + 2 * 4 * C1_W + C1_STAGES * 2 * C1_BOX;
+struct C1Args {
+    CUtensorMap a, w[2];
+    EpiBiasRelu ep[2];
+    int n, groups, coff[2];  // channel offset of group g in the s2d pixel row
+    int a_early, w_early;    // operands not written by the preceding launch: load before the wait
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_constant__ C1Args g) {
+    constexpr uint32_t IDESC = idesc_bf16(32, false, false);
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t full[C1_STAGES], empty[C1_STAGES], accf[2], acce[2], wbar;
+    __shared__ uint32_t tmem_base_s;
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t w_s = smem_u32(smem), ring_s = w_s + 2 * 4 * C1_W;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < C1_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&accf[b], 1);
+            mbar_init(&acce[b], 4);  // one arrival per epilogue warp
+        }
+        mbar_init(&wbar, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<128>(&tmem_base_s);
+    if (tid == 32) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&g.a) : "memory");
+        for (int q = 0; q < g.groups; ++q) asm volatile("prefetch.tensormap [%0];" ::"l"(&g.w[q]) : "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const int total = (g.n * 441 + 127) / 128;
+    const int nbox = g.coff[g.groups - 1] > 0 ? 2 : 1;
+    auto load_w = [&] {
+        mbar_expect_tx(&wbar, (uint32_t)(g.groups * 4 * C1_W));
+        for (int q = 0; q < g.groups; ++q)
+            for (int t = 0; t < 4; ++t) tma_load_2d(w_s + (q * 4 + t) * C1_W, &g.w[q], &wbar, t * 64, 0);
+    };
+    auto load_a = [&](uint32_t q, int t) {
+        const uint32_t s = q % C1_STAGES, dst = ring_s + s * 2 * C1_BOX;
+        mbar_expect_tx(&full[s], (uint32_t)(nbox * C1_BOX));
+        tma_load_2d(dst, &g.a, &full[s], 0, t * 128);
+        if (nbox > 1) tma_load_2d(dst + C1_BOX, &g.a, &full[s], 64, t * 128);
+    };
+    int pre = 0;
+    if (tid == 0) {
+        if (g.w_early) load_w();
+        if (g.a_early)
+            for (int t = blockIdx.x; t < total && pre < C1_STAGES; t += gridDim.x, ++pre) load_a(pre, t);
+    }
+    griddep_wait();
+    griddep_launch();
+    if (warp == 0) {
+        if (lane == 0) {  // producer
+            if (!g.w_early) load_w();
+            uint32_t q = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
+                if ((int)q < pre) continue;
+                if (q >= C1_STAGES) mbar_wait(&empty[q % C1_STAGES], ((q / C1_STAGES) - 1) & 1);
+                load_a(q, t);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            mbar_wait(&wbar, 0);
+            uint32_t q = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
+                const uint32_t buf = q & 1, s = q % C1_STAGES;
+                if (q >= 2) mbar_wait(&acce[buf], ((q >> 1) - 1) & 1);
+                mbar_wait(&full[s], (q / C1_STAGES) & 1);
+                tc_fence_after();
+                const uint32_t a0 = ring_s + s * 2 * C1_BOX;
+                for (int gg = 0; gg < g.groups; ++gg) {
+                    const uint32_t acc = tmem + buf * 64 + gg * 32;
+#pragma unroll
+                    for (int tap = 0; tap < 4; ++tap) {
+                        const uint32_t shift = (uint32_t)((tap >> 1) * 21 + (tap & 1)) * 128;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int ch = g.coff[gg] + 16 * j;
+                            const uint64_t ad = desc_sw128(a0 + (ch >> 6) * C1_BOX + shift + (ch & 63) * 2, 0);
+                            const uint64_t bd = desc_sw128(w_s + (gg * 4 + tap) * C1_W + j * 32, 0);
+                            umma_bf16(acc, ad, bd, IDESC, (tap > 0 || j > 0) ? 1u : 0u);
+                        }
+                    }
+                }
+                umma_commit(&empty[s]);
+                umma_commit(&accf[buf]);
+            }
+        }
+    } else if (warp >= 4) {  // epilogue: TMEM lane quadrant = warp % 4
+        const int wq = warp - 4;
+        uint32_t q = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
+            const uint32_t buf = q & 1;
+            mbar_wait(&accf[buf], (q >> 1) & 1);
+            __syncwarp();
+            tc_fence_after();
+            float v[2][32];
+            const uint32_t trow = tmem + buf * 64 + ((uint32_t)(wq * 32) << 16);
+            tmem_ld32(trow, v[0]);
+            if (g.groups > 1) tmem_ld32(trow + 32, v[1]);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acce[buf]);
+            const int r = t * 128 + wq * 32 + lane, smp = r / 441, p = r - smp * 441, y = p / 21, x = p - y * 21;
+            if (smp < g.n && y < 20 && x < 20) {
+                const int m = smp * 400 + y * 20 + x;
+                g.ep[0].apply(m, 0, v[0], 32, 0);
+                if (g.groups > 1) g.ep[1].apply(m, 0, v[1], 32, 0);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<128>(tmem);
+}
+
+// conv1 forward by row-shifted descriptors (k_conv1_shift): groups online / target over
+// channel offsets c0[g] of the s2d stacks (16 * nframes channels per pixel)
+int tma_conv1_shift(const pq_net *nets, const bf16 *s2d, int nframes, const int *c0, bf16 *const *act1,
+                    int groups, int n, int a_early, int w_early, cudaStream_t st) {
+    static C1Args g;
+    memset(&g, 0, sizeof(g));
+    const uint64_t ad[2] = {(uint64_t)nframes * 16, (uint64_t)n * 441}, as[1] = {(uint64_t)nframes * 16};
+    if (int rc = make_map(&g.a, s2d, 2, ad, as, "s2d pixel rows", C1_ROWS)) return rc;
+    for (int q = 0; q < groups; ++q) {
+        const uint64_t wd[2] = {256, 32}, ws[1] = {256};
+        if (int rc = make_map(&g.w[q], (const bf16 *)nets[q].shadow + S_W1P, 2, wd, ws, "W1 permuted", 32))
+            return rc;
+        g.ep[q] = EpiBiasRelu{act1[q], nets[q].master + P_B1, n * 400, 32, 32, 1.0f / 255.0f};
+        g.coff[q] = c0[q];
+    }
+    if (groups > 1 && (c0[1] + 64 > nframes * 16 || c0[0] != 0)) return set_err("conv1 shift: channel window");
+    g.n = n, g.groups = groups, g.a_early = a_early, g.w_early = w_early;
+    static bool configured = false;
+    if (!configured) {
+        PQ_CUDA_TRY(cudaFuncSetAttribute(k_conv1_shift, cudaFuncAttributeMaxDynamicSharedMemorySize, C1_SMEM));
+        configured = true;
+    }
+    if (!g_sms) {
+        int dev = 0;
+        PQ_CUDA_TRY(cudaGetDevice(&dev));
+        PQ_CUDA_TRY(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int total = (n * 441 + 127) / 128;
+    return cuda_err(launch_k(k_conv1_shift, dim3(std::min(total, g_sms)), dim3(GEMM_THREADS), C1_SMEM, st, g),
+                    "conv1 forward (shifted descriptors)");
+}
+
 // conv1 weight gradient on the TMA engine: part1[s][o][k'] over the permuted K order
 // (k' = 256: bias row from the ones tile)
 int tma_conv1_wgrad(const bf16 *s2d, int nframes, const bf16 *dY1, float *part1, int kc, int splits, int n,

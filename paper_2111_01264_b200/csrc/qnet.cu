@@ -49,8 +49,20 @@ int tma_frames_s2d(const uint8_t *ring, const int32_t *refs, const int64_t *map,
                    int map_stride, int ref_stride, int ref_off, int nframes, int n, bf16 *out, cudaStream_t st);
 int tma_conv1_fwd(const pq_net *nets, const bf16 *s2d, int nframes, const int *c0, bf16 *const *act1, int groups,
                   int n, cudaStream_t st);
+int tma_conv1_shift(const pq_net *nets, const bf16 *s2d, int nframes, const int *c0, bf16 *const *act1,
+                    int groups, int n, int a_early, int w_early, cudaStream_t st);
 int tma_conv1_wgrad(const bf16 *s2d, int nframes, const bf16 *dY1, float *part1, int kc, int splits, int n,
                     cudaStream_t st);
+// conv1 forward by row-shifted UMMA descriptors over the s2d stacks (PQ_C1SHIFT=0: the
+// im2col TMA kernel)
+static bool conv1_shift() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("PQ_C1SHIFT");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
 // Engine per GEMM (measured, profiles/r1_engine_compare.md): below batch 128 every CTA
 // owns ~one tile and the cp.async engine's shorter first-load latency wins inside the
 // CUDA graph; from 128 up the warp-specialised TMA engine overlaps tiles and wins.
@@ -284,7 +296,11 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
         if (int rc = tma_frames_s2d(ins[0].ring, ins[0].refs, ins[0].map, ins[0].counter, ins[0].map_stride,
                                     ins[0].ref_stride, ins[0].ref_off, nframes, n, w.s2d, st))
             return rc;
-        if (int rc = tma_conv1_fwd(nets, w.s2d, nframes, c0, a1, groups, n, st)) return rc;
+        if (conv1_shift()) {  // the s2d kernel just wrote the frames; weights are two launches back
+            if (int rc = tma_conv1_shift(nets, w.s2d, nframes, c0, a1, groups, n, 0, 1, st)) return rc;
+        } else if (int rc = tma_conv1_fwd(nets, w.s2d, nframes, c0, a1, groups, n, st)) {
+            return rc;
+        }
     } else {  // F1: conv1 8x8/4 over uint8 frames (K = 256), bias + ReLU, x 1/255
         GemmArgs<LoadFrames, LoadDense, EpiBiasRelu> g{};
         for (int q = 0; q < groups; ++q) {
@@ -434,13 +450,28 @@ __global__ void __launch_bounds__(512) k_fc2_partials(const float *h1, const flo
     float acc[MAX_ACTIONS], ab = 0.f, bb = 0.f;
 #pragma unroll
     for (int aa = 0; aa < MAX_ACTIONS; ++aa) acc[aa] = 0.f;
-    for (int b = 0; b < nb; ++b) {
-        const float x = s_d[b] * h1[(size_t)(b0 + b) * 512 + j];
-        const int ab_ = s_a[b];
+    // 16 samples' loads in flight per round (a one-sample loop is load-latency bound);
+    // the adds stay in sample order
+    constexpr int U = 16;
+    for (int q = 0; q < nb; q += U) {
+        float hv[U], dv[U];
 #pragma unroll
-        for (int aa = 0; aa < MAX_ACTIONS; ++aa) acc[aa] += (ab_ == aa) ? x : 0.f;
-        ab += dh1[(size_t)(b0 + b) * 512 + j];
-        if (j < A && ab_ == j) bb += s_d[b];
+        for (int u = 0; u < U; ++u) {
+            const bool ok = q + u < nb;
+            hv[u] = ok ? h1[(size_t)(b0 + q + u) * 512 + j] : 0.f;
+            dv[u] = ok ? dh1[(size_t)(b0 + q + u) * 512 + j] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (q + u >= nb) break;
+            const int b = q + u;
+            const float x = s_d[b] * hv[u];
+            const int ab_ = s_a[b];
+#pragma unroll
+            for (int aa = 0; aa < MAX_ACTIONS; ++aa) acc[aa] += (ab_ == aa) ? x : 0.f;
+            ab += dv[u];
+            if (j < A && ab_ == j) bb += s_d[b];
+        }
     }
     float *out = part + (size_t)blockIdx.x * (A + 2) * 512;
 #pragma unroll

@@ -5,7 +5,11 @@ switches are read once per process):
   same K order and MMA sequence as the separate GEMMs, so Q-values are bit-identical;
 * PQ_TMA=1 — the warp-specialised TMA engine forced at batch 32 (default: from 128):
   Q-values bit-identical, one learner step within fp32 summation order (1e-5) of the
-  cp.async engine."""
+  cp.async engine;
+* PQ_C1SHIFT=0 — conv1 forward by TMA im2col instead of row-shifted descriptors (batch
+  >= 128): the same MMA sequence, so Q-values and the learner update are bit-identical;
+* PQ_FUSED=0 — the multi-stream learner backward instead of the single-stream fused
+  launches (batch < 128): the same GEMMs and reductions, bit-identical update."""
 
 import os
 import subprocess
@@ -29,23 +33,24 @@ import torch
 from paper_2111_01264_b200 import nn as dnn
 from paper_2111_01264_b200.envs import FrameEnvSpec
 from paper_2111_01264_b200.replay import ReplayMemory
+W, B = int(sys.argv[3]), int(sys.argv[4])
 net = dnn.init_network(5)
-x = np.random.default_rng(1).integers(0, 256, size=(24, 4, 84, 84), dtype=np.uint8)
+x = np.random.default_rng(1).integers(0, 256, size=(W, 4, 84, 84), dtype=np.uint8)
 q = dnn.forward(net, x)
 mem = ReplayMemory(4096)
 mem.prepopulate(FrameEnvSpec(key=3), 2000, np.random.default_rng(2))
 theta, target = dnn.init_network(6), dnn.init_network(7)
-idx = mem.sample_indices(32, np.random.default_rng(4))
-th2, _, _, _, _ = dnn._learn(theta, dnn.OptState.zeros(theta), target, mem.ring, mem.records, idx, 32)
+idx = mem.sample_indices(B, np.random.default_rng(4))
+th2, _, _, _, _ = dnn._learn(theta, dnn.OptState.zeros(theta), target, mem.ring, mem.records, idx, B)
 np.savez(sys.argv[2], q=q, theta=th2.master.cpu().numpy(), theta0=theta.master.cpu().numpy())
 """
 
 
-def run_probe(tmp_path, name, env):
+def run_probe(tmp_path, name, env, W=24, B=32):
     out = tmp_path / f"{name}.npz"
     e = dict(os.environ)
     e.update(env)
-    subprocess.run([sys.executable, "-c", PROBE, ROOT, str(out)], check=True, env=e, timeout=600)
+    subprocess.run([sys.executable, "-c", PROBE, ROOT, str(out), str(W), str(B)], check=True, env=e, timeout=600)
     return np.load(out)
 
 
@@ -58,3 +63,17 @@ def test_fused_conv23_and_forced_tma_match_default(tmp_path):
     d = base["theta"] - base["theta0"]
     for other in (fused, tma):
         assert np.linalg.norm(other["theta"] - base["theta"]) <= 1e-5 * np.linalg.norm(d)
+
+
+def test_conv1_shift_matches_im2col(tmp_path):
+    shift = run_probe(tmp_path, "shift", {"PQ_C1SHIFT": "1"}, W=200, B=256)
+    im2col = run_probe(tmp_path, "im2col", {"PQ_C1SHIFT": "0"}, W=200, B=256)
+    assert np.array_equal(shift["q"], im2col["q"])
+    assert np.array_equal(shift["theta"], im2col["theta"])
+
+
+def test_fused_backward_matches_multistream(tmp_path):
+    fused = run_probe(tmp_path, "fused_bw", {"PQ_FUSED": "1"})
+    multi = run_probe(tmp_path, "multi_bw", {"PQ_FUSED": "0"})
+    assert np.array_equal(fused["q"], multi["q"])
+    assert np.array_equal(fused["theta"], multi["theta"])
