@@ -503,6 +503,7 @@ struct EpiMaskP {
     const bf16 *mask;
     int n, H2, W2, C, tpc;
     FastDiv f_per, f_npix, f_w2;
+    int pad;  // out on the (2 H2 + 1) x (2 W2 + 1) grid of the space-to-depth conv1 (k_conv1_wgrad_shift)
     PQ_DEV void apply(int m, int n0, const float *v, int cnt, int) const {
         int cls = f_per.div(m), loc = m - cls * tpc * 128;
         int npix = H2 * W2;
@@ -511,12 +512,14 @@ struct EpiMaskP {
         int ry = f_w2.div(rem);
         int iy = 2 * ry + (cls >> 1), ix = 2 * (rem - ry * W2) + (cls & 1);
         size_t o = ((size_t)(b * 2 * H2 + iy) * (2 * W2) + ix) * C + n0;
-        store_masked32(out + o, mask + o, v, min(cnt, C - n0));
+        size_t oo = pad ? ((size_t)(b * (2 * H2 + 1) + iy) * (2 * W2 + 1) + ix) * C + n0 : o;
+        store_masked32(out + oo, mask + o, v, min(cnt, C - n0));
     }
 };
-PQ_HD EpiMaskP epi_mask_p(bf16 *out, const bf16 *mask, int n, int H2, int W2, int C, int tpc) {
+PQ_HD EpiMaskP epi_mask_p(bf16 *out, const bf16 *mask, int n, int H2, int W2, int C, int tpc, int pad = 0) {
     EpiMaskP e{out, mask, n, H2, W2, C, tpc};
     e.f_per = FastDiv(tpc * 128), e.f_npix = FastDiv(H2 * W2), e.f_w2 = FastDiv(W2);
+    e.pad = pad;
     return e;
 }
 

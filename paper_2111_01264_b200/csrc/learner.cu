@@ -1454,14 +1454,15 @@ int tma_conv3_wgrad(const bf16 *act2, const bf16 *dY3, float *part3, int kc, int
 }
 
 // conv2 data gradient per input-parity class: dY1 = relu'(act1) * transposed conv2(dY2)
-int tma_conv2_dgrad(const pq_net &th, const bf16 *dY2, const bf16 *act1, bf16 *dY1, int n, cudaStream_t st) {
+int tma_conv2_dgrad(const pq_net &th, const bf16 *dY2, const bf16 *act1, bf16 *dY1, int n, cudaStream_t st,
+                    int pad21) {
     static TmaGemm<EpiMaskP> g;
     memset(&g, 0, sizeof(g));
     const int tpc = (n * 100 + 127) / 128;
     if (int rc = map_im2col(&g.a[0], dY2, n, 9, 9, -1, 0, 128, "dY2")) return rc;
     const uint64_t dims[4] = {32, 4, 4, 64}, strd[3] = {32, 128, 512};
     if (int rc = make_map(&g.b[0], (const bf16 *)th.shadow + S_W2, 4, dims, strd, "W2 view")) return rc;
-    g.ep[0] = epi_mask_p(dY1, act1, n, 10, 10, 32, tpc);
+    g.ep[0] = epi_mask_p(dY1, act1, n, 10, 10, 32, tpc, pad21);
     g.kindA = OP_IT2, g.kindB = OP_W2V, g.boxesA = 2, g.boxesB = 1, g.n = n, g.tpc = tpc, g.b_is_weight = 1;
     g.mtiles = 4 * tpc, g.ntiles = 1, g.splits = 1, g.groups = 1, g.kc = 4, g.nk = 4;
     return launch_tma<64, false, true>(g, st, "conv2 dgrad (TMA)");
@@ -1691,6 +1692,144 @@ int tma_conv1_shift(const pq_net *nets, const bf16 *s2d, int nframes, const int 
     const int total = (n * 441 + 127) / 128;
     return cuda_err(launch_k(k_conv1_shift, dim3(std::min(total, g_sms)), dim3(GEMM_THREADS), C1_SMEM, st, g),
                     "conv1 forward (shifted descriptors)");
+}
+
+// ---- conv1 weight gradient by row-shifted descriptors (the transpose of k_conv1_shift)
+// part1[split][k'][o] = sum over the split's rows r of the padded 21 x 21 grid of
+// s2d[r + 21 ty + tx][c] dY1p[r][o] (k' = tap * 64 + c, tap = (ty, tx)), row 256 = the
+// bias gradient sum_r dY1p[r][o].  dY1p holds conv2's data gradient on the same padded
+// grid (zero rows at y or x = 20, written by tma_conv2_dgrad(pad21)), so one TMA box of
+// 88 s2d rows per 64-row K chunk feeds all four taps as MN-major operands: M tile 0 =
+// taps (0,0), (0,1) (rows +0 / +1: start +0, LBO 128 B), M tile 1 = taps (1,0), (1,1)
+// (start +21 rows, LBO 128 B), M tile 2 = a ones column (bias row).  One CTA per split
+// runs all three M tiles from the same operands.
+constexpr int W1S_ROWS = 88, W1S_ABOX = W1S_ROWS * 128, W1S_BBOX = 64 * 128, W1S_STAGES = 6;
+constexpr int W1S_SLOT = ((W1S_ABOX + W1S_BBOX + 1023) / 1024) * 1024;
+constexpr int W1S_SMEM = 1024 + 2 * 8192 + W1S_STAGES * W1S_SLOT;
+struct W1SArgs {
+    CUtensorMap a, b;  // s2d pixel rows [n*441][16*nframes]; dY1p [n*441][32]
+    EpiF32T ep;        // part1[split][257][32]
+    int nk, kc;        // 64-row K chunks in all, per split
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __grid_constant__ W1SArgs g) {
+    constexpr uint32_t IDESC = idesc_bf16(64, true, true);
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t full[W1S_STAGES], empty[W1S_STAGES], accf;
+    __shared__ uint32_t tmem_base_s;
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t ones_s = smem_u32(smem), ring_s = ones_s + 2 * 8192;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // ones operand (MN-major, 64 K rows x 128 B per M atom, two atoms): M index 0 = 1
+    for (int i = tid; i < 2 * 8192 / 16; i += blockDim.x) {
+        const int atom = i >> 9, k = (i >> 3) & 63, c8 = i & 7;
+        uint4 val = make_uint4(0, 0, 0, 0);
+        if (atom == 0 && c8 == 0) val.x = 0x3F80u;  // bf16 1.0 at M index 0 of every K row
+        *reinterpret_cast<uint4 *>(smem + atom * 8192 + mnmaj_off(k, c8) % 8192) = val;
+    }
+    if (tid == 0) {
+        for (int s = 0; s < W1S_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&accf, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<256>(&tmem_base_s);
+    if (tid == 32) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&g.a) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&g.b) : "memory");
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const int split = blockIdx.x, kb0 = split * g.kc, kb1 = min(g.nk, kb0 + g.kc);
+    // the frames (written two launches back) go out before the dependency wait
+    int pre = 0;
+    if (tid == 0)
+        for (int kb = kb0; kb < kb1 && pre < W1S_STAGES; ++kb, ++pre) {
+            mbar_expect_tx(&full[pre], (uint32_t)(W1S_ABOX + W1S_BBOX));
+            tma_load_2d(ring_s + pre * W1S_SLOT, &g.a, &full[pre], 0, kb * 64);
+        }
+    griddep_wait();
+    griddep_launch();
+    if (warp == 0) {
+        if (lane == 0) {  // producer
+            uint32_t q = 0;
+            for (int kb = kb0; kb < kb1; ++kb, ++q) {
+                const uint32_t s = q % W1S_STAGES, dst = ring_s + s * W1S_SLOT;
+                if ((int)q >= pre) {
+                    if (q >= W1S_STAGES) mbar_wait(&empty[s], ((q / W1S_STAGES) - 1) & 1);
+                    mbar_expect_tx(&full[s], (uint32_t)(W1S_ABOX + W1S_BBOX));
+                    tma_load_2d(dst, &g.a, &full[s], 0, kb * 64);
+                }
+                tma_load_2d(dst + W1S_ABOX, &g.b, &full[s], 0, kb * 64);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer: three 128 x 64 accumulators
+            uint32_t q = 0;
+            for (int kb = kb0; kb < kb1; ++kb, ++q) {
+                const uint32_t s = q % W1S_STAGES;
+                mbar_wait(&full[s], (q / W1S_STAGES) & 1);
+                tc_fence_after();
+                const uint32_t a0 = ring_s + s * W1S_SLOT, b0 = a0 + W1S_ABOX;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {  // K steps of 16 rows (2048 B)
+                    const uint32_t acc_on = (kb > kb0 || j > 0) ? 1u : 0u;
+                    const uint64_t bd = desc_sw128(b0 + j * 2048, 8192);
+                    umma_bf16(tmem, desc_sw128(a0 + j * 2048, 128), bd, IDESC, acc_on);
+                    umma_bf16(tmem + 64, desc_sw128(a0 + 21 * 128 + j * 2048, 128), bd, IDESC, acc_on);
+                    umma_bf16(tmem + 128, desc_sw128(ones_s + j * 2048, 8192), bd, IDESC, acc_on);
+                }
+                umma_commit(&empty[s]);
+            }
+            umma_commit(&accf);
+        }
+    } else if (warp >= 4) {  // epilogue
+        const int wq = warp - 4;
+        mbar_wait(&accf, 0);
+        __syncwarp();
+        tc_fence_after();
+#pragma unroll 1
+        for (int mt = 0; mt < 3; ++mt) {
+            float v[32];
+            const int row = mt * 128 + wq * 32 + lane;
+            if (kb1 > kb0) {
+                tmem_ld32(tmem + mt * 64 + ((uint32_t)(wq * 32) << 16), v);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) v[e] = 0.f;
+            }
+            if (mt < 2 || row == 256) g.ep.apply(row, 0, v, 32, split);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<256>(tmem);
+}
+
+int tma_conv1_wgrad_shift(const bf16 *s2d, int nframes, const bf16 *dY1p, float *part1, int kc, int splits,
+                          int n, cudaStream_t st) {
+    static W1SArgs g;
+    memset(&g, 0, sizeof(g));
+    const uint64_t ad[2] = {(uint64_t)nframes * 16, (uint64_t)n * 441}, as[1] = {(uint64_t)nframes * 16};
+    if (int rc = make_map(&g.a, s2d, 2, ad, as, "s2d pixel rows (wgrad)", W1S_ROWS)) return rc;
+    if (int rc = map2(&g.b, dY1p, (uint64_t)n * 441, 32, 32, "dY1 padded")) return rc;
+    g.ep = EpiF32T{part1, 257, 32, 257, (size_t)32 * 257};
+    g.nk = (n * 441 + 63) / 64;
+    g.kc = kc;
+    const int grid = (g.nk + kc - 1) / kc;
+    if (grid != splits) return set_err("conv1 wgrad shift: split count mismatch");
+    static bool configured = false;
+    if (!configured) {
+        PQ_CUDA_TRY(cudaFuncSetAttribute(k_conv1_wgrad_shift, cudaFuncAttributeMaxDynamicSharedMemorySize, W1S_SMEM));
+        configured = true;
+    }
+    return cuda_err(launch_k(k_conv1_wgrad_shift, dim3(grid), dim3(GEMM_THREADS), W1S_SMEM, st, g),
+                    "conv1 wgrad (shifted descriptors)");
 }
 
 // conv1 weight gradient on the TMA engine: part1[s][o][k'] over the permuted K order

@@ -6,8 +6,10 @@ switches are read once per process):
 * PQ_TMA=1 — the warp-specialised TMA engine forced at batch 32 (default: from 128):
   Q-values bit-identical, one learner step within fp32 summation order (1e-5) of the
   cp.async engine;
-* PQ_C1SHIFT=0 — conv1 forward by TMA im2col instead of row-shifted descriptors (batch
-  >= 128): the same MMA sequence, so Q-values and the learner update are bit-identical;
+* PQ_C1SHIFT=0 — conv1 forward / weight gradient by TMA im2col instead of row-shifted
+  descriptors (batch >= 128): the forward runs the same MMA sequence, so Q-values are
+  bit-identical; the weight gradient sums the padded 21 x 21 grid in other K chunks and
+  splits, so the learner update agrees to fp32 summation order (1e-5);
 * PQ_FUSED=0 — the multi-stream learner backward instead of the single-stream fused
   launches (batch < 128): the same GEMMs and reductions, bit-identical update."""
 
@@ -69,7 +71,8 @@ def test_conv1_shift_matches_im2col(tmp_path):
     shift = run_probe(tmp_path, "shift", {"PQ_C1SHIFT": "1"}, W=200, B=256)
     im2col = run_probe(tmp_path, "im2col", {"PQ_C1SHIFT": "0"}, W=200, B=256)
     assert np.array_equal(shift["q"], im2col["q"])
-    assert np.array_equal(shift["theta"], im2col["theta"])
+    d = im2col["theta"] - im2col["theta0"]
+    assert np.linalg.norm(shift["theta"] - im2col["theta"]) <= 1e-5 * np.linalg.norm(d)
 
 
 def test_fused_backward_matches_multistream(tmp_path):
