@@ -282,7 +282,8 @@ __device__ __forceinline__ float grad_of(const OptArgs &a, int64_t i, int64_t &s
     return batch_sum(a.n, [&](int b) { return (*(a.act + b)) == aa ? (*(a.td + b * 3 + 1)) : 0.f; });
 }
 
-constexpr int FC_CHUNK = 64;  // samples per fc2 / fc1-bias gradient partial (qnet.cu)
+constexpr int FC_CHUNK = 16;            // samples per fc2 / fc1-bias gradient partial (qnet.cu)
+constexpr int FC_PART_MIN_BATCH = 129;  // batches from which the fc2 / fc1-bias sums use partials
 
 // centered RMSProp, kappa inside the square root (_kernels_numba.py:98-111)
 __device__ __forceinline__ void rms(const OptArgs &a, float g, float m, float v, float p,

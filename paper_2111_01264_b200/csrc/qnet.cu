@@ -127,7 +127,7 @@ static WS carve(void *base, int N, int A) {
     w.dY3 = (bf16 *)take((size_t)N * 3136 * 2);
     w.dY2 = (bf16 *)take((size_t)N * 81 * 64 * 2);
     w.dY1 = (bf16 *)take((size_t)N * 400 * 32 * 2);
-    w.part1 = (float *)take((size_t)MAX_SPLITS * 32 * 257 * 4);
+    w.part1 = (float *)take((size_t)P1_MAX_SPLITS * 32 * 257 * 4);
     w.part2 = (float *)take((size_t)MAX_SPLITS * 64 * 513 * 4);
     w.part3 = (float *)take((size_t)MAX_SPLITS * 64 * 577 * 4);
     w.grad4 = (float *)take((size_t)512 * 3136 * 4);
@@ -722,7 +722,7 @@ static bool fused_backward(int n, const pq_learn_args *la, float *grad_only) {
         const char *e = getenv("PQ_FUSED");
         on = (e && e[0] == '0') ? 0 : 1;
     }
-    return on == 1 && !use_tma(n) && !grad_only && n <= 2 * FC_CHUNK;
+    return on == 1 && !use_tma(n) && !grad_only && n < FC_PART_MIN_BATCH;
 }
 
 static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStream_t st) {
@@ -782,7 +782,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     PQ_CHECK(cudaStreamWaitEvent(side2, fk->ev[1], 0), "fork1 wait 2");
     // large batches: the fc2 / fc1-bias batch sums as chunk partials on the wgrad branch
     // (the optimizer then reduces n/64 partials per parameter instead of n samples)
-    const int fc_chunks = n > 2 * FC_CHUNK ? (n + FC_CHUNK - 1) / FC_CHUNK : 0;
+    const int fc_chunks = n >= FC_PART_MIN_BATCH ? (n + FC_CHUNK - 1) / FC_CHUNK : 0;
     if (fc_chunks)
         PQ_CHECK(launch_k(k_fc2_partials, dim3(fc_chunks), dim3(512), 0, side2, (const float *)w.h1,
                           (const float *)w.dh1, (const float *)w.td, (const int32_t *)w.act, n, la->actions,
@@ -841,7 +841,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         if (use_tma(n) && w.s2d) {  // over the space-to-depth stacks
             const int nframes = la->ext_targets ? 4 : 5;
             if (conv1_shift() && w.dY1p) {
-                const int nk = (n * 441 + 63) / 64, kc = (nk + MAX_SPLITS - 1) / MAX_SPLITS;
+                const int nk = (n * 441 + 63) / 64, kc = (nk + P1_MAX_SPLITS - 1) / P1_MAX_SPLITS;
                 s1 = (nk + kc - 1) / kc;  // one CTA per split, all three M tiles
                 if (int rc = tma_conv1_wgrad_shift(w.s2d, nframes, w.dY1p, w.part1, kc, s1, n, st)) return rc;
             } else if (int rc = tma_conv1_wgrad(w.s2d, nframes, w.dY1, w.part1, g.kc_per_split, s1, n, st)) {

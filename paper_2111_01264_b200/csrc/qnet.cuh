@@ -29,6 +29,7 @@ __host__ __device__ inline int w1_perm(int k) {
 }
 constexpr int MAX_ACTIONS = 32;
 constexpr int MAX_SPLITS = 64;
+constexpr int P1_MAX_SPLITS = 148;  // part1 rows: the shifted conv1 weight gradient runs one CTA per SM
 constexpr int FC1_SPLITS = 7;  // 49 K-chunks of fc1 -> 7 x 7
 
 }  // namespace pq
