@@ -1476,10 +1476,13 @@ int tma_conv2_dgrad(const pq_net &th, const bf16 *dY2, const bf16 *act1, bf16 *d
 __global__ void __launch_bounds__(256) k_frames_s2d(const uint8_t *ring, const int32_t *refs, const int64_t *map,
                                                     const int32_t *counter, int map_stride, int ref_stride,
                                                     int ref_off, int nframes, bf16 *out) {
+    // Inputs (replay ring, records, the epoch's index table and the step counter) are not
+    // written by the preceding launch, and `out` was last read two launches back, so the
+    // gather runs before the dependency wait (overlapping the previous step's optimizer);
+    // the wait precedes the trigger so the next launch's early prologue still finds
+    // everything two launches back complete.
     const int b = blockIdx.x;
     __shared__ int32_t slot[8];
-    griddep_wait();
-    griddep_launch();
     if ((int)threadIdx.x < nframes) {
         const int64_t base = (map && counter) ? (int64_t)(*counter) * map_stride : 0;
         const int64_t rec = map ? map[base + b] : (int64_t)b;
@@ -1500,6 +1503,8 @@ __global__ void __launch_bounds__(256) k_frames_s2d(const uint8_t *ring, const i
         d[0] = u8x8_to_bf16(w[0], w[1]);
         d[1] = u8x8_to_bf16(w[2], w[3]);
     }
+    griddep_wait();
+    griddep_launch();
 }
 
 int tma_frames_s2d(const uint8_t *ring, const int32_t *refs, const int64_t *map, const int32_t *counter,
