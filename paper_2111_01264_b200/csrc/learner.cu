@@ -1425,7 +1425,19 @@ int tma_fc1_dgrad(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *
 }
 
 // conv3 data gradient: dY2 = relu'(act2) * transposed conv3(dY3) (im2col window, pad 2)
-int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st) {
+int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st,
+                    bf16 *dY2p) {
+    if (dY2p) {  // also onto the padded 11 x 11 grid of the shifted conv2 data gradient
+        static TmaGemm<EpiMaskPad> g;
+        memset(&g, 0, sizeof(g));
+        if (int rc = map_im2col(&g.a[0], dY3, n, 7, 7, -2, 0, 128, "dY3")) return rc;
+        const uint64_t dims[3] = {64, 9, 64}, strd[2] = {64, 576};
+        if (int rc = make_map(&g.b[0], (const bf16 *)th.shadow + S_W3, 3, dims, strd, "W3 view")) return rc;
+        g.ep[0] = EpiMaskPad{EpiMask{dY2, act2, n * 81, 64, 64}, dY2p, FastDiv(81), FastDiv(9)};
+        g.kindA = OP_IT3, g.kindB = OP_W3V, g.boxesA = 2, g.boxesB = 1, g.n = n, g.b_is_weight = 1;
+        g.mtiles = (n * 81 + 127) / 128, g.ntiles = 1, g.splits = 1, g.groups = 1, g.kc = 9, g.nk = 9;
+        return launch_tma<64, false, true>(g, st, "conv3 dgrad (TMA, padded copy)");
+    }
     static TmaGemm<EpiMask> g;
     memset(&g, 0, sizeof(g));
     if (int rc = map_im2col(&g.a[0], dY3, n, 7, 7, -2, 0, 128, "dY3")) return rc;
@@ -1466,6 +1478,157 @@ int tma_conv2_dgrad(const pq_net &th, const bf16 *dY2, const bf16 *act1, bf16 *d
     g.kindA = OP_IT2, g.kindB = OP_W2V, g.boxesA = 2, g.boxesB = 1, g.n = n, g.tpc = tpc, g.b_is_weight = 1;
     g.mtiles = 4 * tpc, g.ntiles = 1, g.splits = 1, g.groups = 1, g.kc = 4, g.nk = 4;
     return launch_tma<64, false, true>(g, st, "conv2 dgrad (TMA)");
+}
+
+// ---- conv2 data gradient by row-shifted descriptors
+// The stride-2 transposed conv splits into the 4 parity classes (py, px) of the 20 x 20
+// input: dY1(2y+py, 2x+px) = relu'(act1) * sum_{ty,tx} dY2(y-ty, x-tx) W2[py+2ty][px+2tx].
+// On the zero-padded 11 x 11 grid dY2p (dY2 at (y+1, x+1), written by conv3's data
+// gradient) GEMM row r = (s, y, x) of an 11 x 11 grid (y, x = 10 discarded) reads row
+// r + 11 (1 - ty) + (1 - tx) for every class, so one TMA box of 144 rows feeds all 4 taps
+// x 4 classes (16 resident MN-major W2 tiles); four 64-column accumulators per tile,
+// double-buffered (all 512 TMEM columns).  Same MMA order per class as the im2col
+// kernel, so dY1 is bit-identical.
+constexpr int C2D_ROWS = 144, C2D_BOX = C2D_ROWS * 128, C2D_STAGES = 4, C2D_W = 64 * 128;
+constexpr int C2D_SMEM = 1024 + 16 * C2D_W + C2D_STAGES * C2D_BOX;
+struct C2DArgs {
+    CUtensorMap a, w;  // dY2p pixel rows [n*121][64]; W2 view {c1, kw, kh, c2}
+    bf16 *out;         // dY1 (dense 20 x 20, or the padded 21 x 21 grid when pad21)
+    const bf16 *mask;  // act1 (dense)
+    int n, pad21;
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_dgrad_shift(const __grid_constant__ C2DArgs g) {
+    constexpr uint32_t IDESC = idesc_bf16(64, false, true);
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t full[C2D_STAGES], empty[C2D_STAGES], accf[2], acce[2], wbar;
+    __shared__ uint32_t tmem_base_s;
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t w_s = smem_u32(smem), ring_s = w_s + 16 * C2D_W;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < C2D_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&accf[b], 1);
+            mbar_init(&acce[b], 4);
+        }
+        mbar_init(&wbar, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<512>(&tmem_base_s);
+    if (tid == 32) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&g.a) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&g.w) : "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const int total = (g.n * 121 + 127) / 128;
+    if (tid == 0) {  // W2 (two launches back) before the dependency wait: tile (class, tap)
+        mbar_expect_tx(&wbar, 16u * C2D_W);
+        for (int cls = 0; cls < 4; ++cls)
+            for (int tap = 0; tap < 4; ++tap) {
+                const int kh = (cls >> 1) + 2 * (tap >> 1), kw = (cls & 1) + 2 * (tap & 1);
+                tma_load_4d(w_s + (cls * 4 + tap) * C2D_W, &g.w, &wbar, 0, kw, kh, 0);
+            }
+    }
+    griddep_wait();
+    griddep_launch();
+    if (warp == 0) {
+        if (lane == 0) {  // producer
+            uint32_t q = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
+                const uint32_t s = q % C2D_STAGES;
+                if (q >= C2D_STAGES) mbar_wait(&empty[s], ((q / C2D_STAGES) - 1) & 1);
+                mbar_expect_tx(&full[s], (uint32_t)C2D_BOX);
+                tma_load_2d(ring_s + s * C2D_BOX, &g.a, &full[s], 0, t * 128);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            mbar_wait(&wbar, 0);
+            uint32_t q = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
+                const uint32_t buf = q & 1, s = q % C2D_STAGES;
+                if (q >= 2) mbar_wait(&acce[buf], ((q >> 1) - 1) & 1);
+                mbar_wait(&full[s], (q / C2D_STAGES) & 1);
+                tc_fence_after();
+                const uint32_t a0 = ring_s + s * C2D_BOX;
+#pragma unroll 1
+                for (int cls = 0; cls < 4; ++cls) {
+                    const uint32_t acc = tmem + buf * 256 + cls * 64;
+#pragma unroll
+                    for (int tap = 0; tap < 4; ++tap) {
+                        const uint32_t shift = (uint32_t)((1 - (tap >> 1)) * 11 + (1 - (tap & 1))) * 128;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint64_t ad = desc_sw128(a0 + shift + j * 32, 0);
+                            const uint64_t bd = desc_sw128(w_s + (cls * 4 + tap) * C2D_W + j * 2048, 8192);
+                            umma_bf16(acc, ad, bd, IDESC, (tap > 0 || j > 0) ? 1u : 0u);
+                        }
+                    }
+                }
+                umma_commit(&empty[s]);
+                umma_commit(&accf[buf]);
+            }
+        }
+    } else if (warp >= 4) {  // epilogue
+        const int wq = warp - 4;
+        uint32_t q = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
+            const uint32_t buf = q & 1;
+            mbar_wait(&accf[buf], (q >> 1) & 1);
+            __syncwarp();
+            tc_fence_after();
+            const int r = t * 128 + wq * 32 + lane, smp = r / 121, p = r - smp * 121, y = p / 11, x = p - y * 11;
+            const bool ok = smp < g.n && y < 10 && x < 10;
+#pragma unroll 1
+            for (int cls = 0; cls < 4; ++cls) {
+                float v[32];
+                tmem_ld32(tmem + buf * 256 + cls * 64 + ((uint32_t)(wq * 32) << 16), v);
+                if (ok) {
+                    const int iy = 2 * y + (cls >> 1), ix = 2 * x + (cls & 1);
+                    const size_t o = ((size_t)(smp * 20 + iy) * 20 + ix) * 32;
+                    const size_t oo = g.pad21 ? ((size_t)(smp * 21 + iy) * 21 + ix) * 32 : o;
+                    store_masked32(g.out + oo, g.mask + o, v, 32);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acce[buf]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+int tma_conv2_dgrad_shift(const pq_net &th, const bf16 *dY2p, const bf16 *act1, bf16 *dY1, int n, int pad21,
+                          cudaStream_t st) {
+    static C2DArgs g;
+    memset(&g, 0, sizeof(g));
+    const uint64_t ad[2] = {64, (uint64_t)n * 121}, as[1] = {64};
+    if (int rc = make_map(&g.a, dY2p, 2, ad, as, "dY2 padded rows", C2D_ROWS)) return rc;
+    const uint64_t dims[4] = {32, 4, 4, 64}, strd[3] = {32, 128, 512};
+    if (int rc = make_map(&g.w, (const bf16 *)th.shadow + S_W2, 4, dims, strd, "W2 view")) return rc;
+    g.out = dY1, g.mask = act1, g.n = n, g.pad21 = pad21;
+    static bool configured = false;
+    if (!configured) {
+        PQ_CUDA_TRY(cudaFuncSetAttribute(k_conv2_dgrad_shift, cudaFuncAttributeMaxDynamicSharedMemorySize, C2D_SMEM));
+        configured = true;
+    }
+    if (!g_sms) {
+        int dev = 0;
+        PQ_CUDA_TRY(cudaGetDevice(&dev));
+        PQ_CUDA_TRY(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int total = (n * 121 + 127) / 128;
+    return cuda_err(launch_k(k_conv2_dgrad_shift, dim3(std::min(total, g_sms)), dim3(GEMM_THREADS), C2D_SMEM, st, g),
+                    "conv2 dgrad (shifted descriptors)");
 }
 
 // Space-to-depth gather of the frame stacks: out[b][by][bx][f*16 + dy*4 + dx] =

@@ -42,7 +42,10 @@ int tma_conv3_fwd(const pq_net *nets, bf16 *const *act2, bf16 *const *act3, int 
 int tma_fc1_fwd(const pq_net *nets, bf16 *const *act3, float *const *part, int splits, int groups, int n,
                 cudaStream_t st);
 int tma_fc1_dgrad(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *dY3, int n, cudaStream_t st);
-int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st);
+int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st,
+                    bf16 *dY2p);
+int tma_conv2_dgrad_shift(const pq_net &th, const bf16 *dY2p, const bf16 *act1, bf16 *dY1, int n, int pad21,
+                          cudaStream_t st);
 int tma_conv3_wgrad(const bf16 *act2, const bf16 *dY3, float *part3, int kc, int splits, int n, cudaStream_t st);
 int tma_conv2_dgrad(const pq_net &th, const bf16 *dY2, const bf16 *act1, bf16 *dY1, int n, cudaStream_t st,
                     int pad21);
@@ -90,6 +93,7 @@ struct WS {
     int32_t *act;
     bf16 *dY3, *dY2, *dY1;
     bf16 *dY1p;  // conv2's data gradient on the padded 21 x 21 grid (TMA engine; pad rows stay 0)
+    bf16 *dY2p;  // conv3's data gradient on the padded 11 x 11 grid (TMA engine; pad rows stay 0)
     float *part1, *part2, *part3, *grad4;
     uint32_t *done;  // [3] CTA completion counters (unused, acting, head)
     int64_t *idx_cur;  // the step's sampled slots (stashed by the head)
@@ -137,6 +141,7 @@ static WS carve(void *base, int N, int A) {
     w.fcpart = (float *)take((size_t)((N + FC_CHUNK - 1) / FC_CHUNK) * (A + 2) * 512 * 4);
     w.s2d = N >= 128 ? (bf16 *)take((size_t)N * 441 * 80 * 2) : nullptr;
     w.dY1p = N >= 128 ? (bf16 *)take((size_t)N * 441 * 32 * 2) : nullptr;  // zeroed with the workspace
+    w.dY2p = N >= 128 ? (bf16 *)take((size_t)N * 121 * 64 * 2) : nullptr;
     w.bytes = off;
     return w;
 }
@@ -806,8 +811,9 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
             PQ_CHECK((launch_gemm<64, true, true>(g, 1, side2)), "conv3 wgrad");
         }
     }
+    const bool shift = conv1_shift() && w.dY1p && w.dY2p;  // shifted-descriptor conv kernels (TMA engine)
     if (use_tma(n)) {
-        if (int rc = tma_conv3_dgrad(th, w.dY3, w.act2[0], w.dY2, n, st)) return rc;
+        if (int rc = tma_conv3_dgrad(th, w.dY3, w.act2[0], w.dY2, n, st, shift ? w.dY2p : nullptr)) return rc;
     } else {
         PQ_CHECK((launch_gemm<64, false, true, 0, 2>(args_b3d(sh, w, n), 1, st)), "conv3 dgrad");
     }
@@ -815,8 +821,11 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     PQ_CHECK(cudaStreamWaitEvent(side2, fk->ev[2], 0), "fork2 wait");
     PQ_CHECK((launch_gemm<64, true, true>(args_b2w(w, n, &s2), 1, side2)), "conv2 wgrad");
     if (use_tma(n)) {
-        const int pad = conv1_shift() && w.dY1p ? 1 : 0;  // for the shifted conv1 weight gradient
-        if (int rc = tma_conv2_dgrad(th, w.dY2, w.act1[0], pad ? w.dY1p : w.dY1, n, st, pad)) return rc;
+        if (shift) {  // dY1 onto the padded grid of the shifted conv1 weight gradient
+            if (int rc = tma_conv2_dgrad_shift(th, w.dY2p, w.act1[0], w.dY1p, n, 1, st)) return rc;
+        } else if (int rc = tma_conv2_dgrad(th, w.dY2, w.act1[0], w.dY1, n, st, 0)) {
+            return rc;
+        }
     } else {
         PQ_CHECK((launch_gemm<64, false, true, 0, 2>(args_b2d(sh, w, n), 1, st)), "conv2 dgrad");
     }
@@ -840,7 +849,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         B1wOp::Args g = args_b1w(la, w, n, &s1);
         if (use_tma(n) && w.s2d) {  // over the space-to-depth stacks
             const int nframes = la->ext_targets ? 4 : 5;
-            if (conv1_shift() && w.dY1p) {
+            if (shift) {
                 const int nk = (n * 441 + 63) / 64, kc = (nk + P1_MAX_SPLITS - 1) / P1_MAX_SPLITS;
                 s1 = (nk + kc - 1) / kc;  // one CTA per split, all three M tiles
                 if (int rc = tma_conv1_wgrad_shift(w.s2d, nframes, w.dY1p, w.part1, kc, s1, n, st)) return rc;
@@ -948,8 +957,8 @@ int pq_workspace_layout(int max_batch, int actions, int64_t *offsets) {
     WS w = carve(base, max_batch, actions);
     const void *ptrs[] = {w.act1[0], w.act2[0], w.act3[0], w.fc1part[0], w.act1[1], w.act2[1],
                           w.act3[1], w.fc1part[1], w.q, w.h1, w.dh1, w.td, w.dh1_bf, w.dh1T,
-                          w.act, w.dY3, w.dY2, w.dY1, w.part1, w.part2, w.part3, w.grad4, w.dY1p};
-    for (int i = 0; i < 23; ++i) offsets[i] = ptrs[i] ? (const char *)ptrs[i] - base : -1;
+                          w.act, w.dY3, w.dY2, w.dY1, w.part1, w.part2, w.part3, w.grad4, w.dY1p, w.dY2p};
+    for (int i = 0; i < 24; ++i) offsets[i] = ptrs[i] ? (const char *)ptrs[i] - base : -1;
     return 0;
 }
 

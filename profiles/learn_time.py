@@ -28,12 +28,17 @@ for B in [int(x) for x in sys.argv[1:]] or [256, 1024]:
                       actions=18, gamma=0.99, lr=2.5e-4, rho=0.95, kappa=0.01, nonfinite=flag.data_ptr(),
                       grad_out=None, q_out=None, td_out=None, ws=ws.data_ptr(), max_batch=cap)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    import time
     for k in range(steps):
         if k == 3:
+            torch.cuda.synchronize()
+            h0 = time.perf_counter()
             e0.record()
         a.idx = idx[k * B:(k + 1) * B].data_ptr()
         N.check(N.load().pq_learn_step(ctypes.byref(a), N.stream_ptr()), "learn_step")
     e1.record()
+    host_us = (time.perf_counter() - h0) * 1e6 / (steps - 3)
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / (steps - 3)
-    print(f"B={B}: {us:.1f} us/step, {68.26e6 * B / (us * 1e-6) / 1e12:.1f} TFLOP/s, flag {int(flag.item())}")
+    print(f"B={B}: {us:.1f} us/step, {68.26e6 * B / (us * 1e-6) / 1e12:.1f} TFLOP/s, host issue {host_us:.1f} us/step, "
+          f"flag {int(flag.item())}")

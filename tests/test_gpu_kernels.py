@@ -154,6 +154,11 @@ def test_learner_step_stagewise(B):
     ref = torch.nn.grad.conv2d_input((B, 64, 9, 9), S["W3"].view(64, 3, 3, 64).permute(0, 3, 1, 2),
                                      dy3, stride=1).permute(0, 2, 3, 1) * (act2 > 0)
     assert rel(dY2, ref) < 2e-3, "conv3 dgrad"
+    if B >= 128:   # TMA engine: the same rows on the zero-padded 11 x 11 grid (shifted conv2 dgrad)
+        dY2p = view(ws, L["dY2p"], (B, 11, 11, 64), torch.bfloat16).float()
+        assert torch.equal(dY2p[:, 1:10, 1:10], dY2)
+        assert not dY2p[:, 0].any() and not dY2p[:, 10].any()
+        assert not dY2p[:, :, 0].any() and not dY2p[:, :, 10].any()
     # conv2
     x1 = act1.permute(0, 3, 1, 2)
     dy2 = dY2.permute(0, 3, 1, 2)
