@@ -1211,6 +1211,7 @@ PQ_DEV void tg_decode(const TmaGemm<EP> &g, int t, int BN, TmaOp &A, TmaOp &B, i
 
 template <int BN, bool AMN, bool BMN, class EP>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) k_tma_gemm(const __grid_constant__ TmaGemm<EP> g) {
+    TlProbe tp;
     static_assert(BN == 64, "the one-shot TMA GEMMs use 64-column accumulators");
     constexpr uint32_t IDESC = idesc_bf16(BN, AMN, BMN);
     extern __shared__ uint8_t smem_raw[];
@@ -1256,6 +1257,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_tma_gemm(const __grid_const
     }
     griddep_wait();
     griddep_launch();
+    tp.waited();
     if (warp == 0) {
         if (lane == 0) {  // producer
             uint32_t q = 0;
@@ -1349,6 +1351,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_tma_gemm(const __grid_const
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc<128>(tmem);
+    tp.done('T');
 }
 
 static int g_sms = 0;
@@ -1499,6 +1502,7 @@ struct C2DArgs {
 };
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_dgrad_shift(const __grid_constant__ C2DArgs g) {
+    TlProbe tp;
     constexpr uint32_t IDESC = idesc_bf16(64, false, true);
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t full[C2D_STAGES], empty[C2D_STAGES], accf[2], acce[2], wbar;
@@ -1538,6 +1542,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_dgrad_shift(const __g
     }
     griddep_wait();
     griddep_launch();
+    tp.waited();
     if (warp == 0) {
         if (lane == 0) {  // producer
             uint32_t q = 0;
@@ -1605,6 +1610,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_dgrad_shift(const __g
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc<512>(tmem);
+    tp.done('D');
 }
 
 int tma_conv2_dgrad_shift(const pq_net &th, const bf16 *dY2p, const bf16 *act1, bf16 *dY1, int n, int pad21,
@@ -1639,6 +1645,7 @@ int tma_conv2_dgrad_shift(const pq_net &th, const bf16 *dY2p, const bf16 *act1, 
 __global__ void __launch_bounds__(256) k_frames_s2d(const uint8_t *ring, const int32_t *refs, const int64_t *map,
                                                     const int32_t *counter, int map_stride, int ref_stride,
                                                     int ref_off, int nframes, bf16 *out) {
+    TlProbe tp;
     // Inputs (replay ring, records, the epoch's index table and the step counter) are not
     // written by the preceding launch, and `out` was last read two launches back, so the
     // gather runs before the dependency wait (overlapping the previous step's optimizer);
@@ -1668,6 +1675,8 @@ __global__ void __launch_bounds__(256) k_frames_s2d(const uint8_t *ring, const i
     }
     griddep_wait();
     griddep_launch();
+    tp.waited();
+    tp.done('S');
 }
 
 int tma_frames_s2d(const uint8_t *ring, const int32_t *refs, const int64_t *map, const int32_t *counter,
@@ -1710,11 +1719,13 @@ constexpr int C1_SMEM = 1024 + 2 * 4 * C1_W + C1_STAGES * 2 * C1_BOX;
 struct C1Args {
     CUtensorMap a, w[2];
     EpiBiasRelu ep[2];
+    bf16 *act1s2[2];  // optional copy of act1 as [n][10][10][128] (2x2 space-to-depth) for k_conv2_shift
     int n, groups, coff[2];  // channel offset of group g in the s2d pixel row
     int a_early, w_early;    // operands not written by the preceding launch: load before the wait
 };
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_constant__ C1Args g) {
+    TlProbe tp;
     constexpr uint32_t IDESC = idesc_bf16(32, false, false);
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t full[C1_STAGES], empty[C1_STAGES], accf[2], acce[2], wbar;
@@ -1764,6 +1775,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_co
     }
     griddep_wait();
     griddep_launch();
+    tp.waited();
     if (warp == 0) {
         if (lane == 0) {  // producer
             if (!g.w_early) load_w();
@@ -1820,22 +1832,34 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_co
             const int r = t * 128 + wq * 32 + lane, smp = r / 441, p = r - smp * 441, y = p / 21, x = p - y * 21;
             if (smp < g.n && y < 20 && x < 20) {
                 const int m = smp * 400 + y * 20 + x;
-                g.ep[0].apply(m, 0, v[0], 32, 0);
-                if (g.groups > 1) g.ep[1].apply(m, 0, v[1], 32, 0);
+                // the 2x2 space-to-depth copy: pixel (y, x) -> (y/2, x/2), channels ((y&1)*2 + (x&1))*32
+                const size_t o2 = ((size_t)(smp * 10 + (y >> 1)) * 10 + (x >> 1)) * 128 + ((y & 1) * 2 + (x & 1)) * 32;
+#pragma unroll
+                for (int gg = 0; gg < 2; ++gg) {
+                    if (gg >= g.groups) break;
+                    g.ep[gg].apply(m, 0, v[gg], 32, 0);
+                    if (g.act1s2[gg]) {
+                        EpiBiasRelu e2 = g.ep[gg];
+                        e2.out = g.act1s2[gg] + o2, e2.ld = 0;
+                        e2.apply(0, 0, v[gg], 32, 0);
+                    }
+                }
             }
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc<128>(tmem);
+    tp.done('1');
 }
 
 // conv1 forward by row-shifted descriptors (k_conv1_shift): groups online / target over
 // channel offsets c0[g] of the s2d stacks (16 * nframes channels per pixel)
 int tma_conv1_shift(const pq_net *nets, const bf16 *s2d, int nframes, const int *c0, bf16 *const *act1,
-                    int groups, int n, int a_early, int w_early, cudaStream_t st) {
+                    int groups, int n, int a_early, int w_early, cudaStream_t st, bf16 *const *act1s2) {
     static C1Args g;
     memset(&g, 0, sizeof(g));
+    for (int q = 0; q < groups && act1s2; ++q) g.act1s2[q] = act1s2[q];
     const uint64_t ad[2] = {(uint64_t)nframes * 16, (uint64_t)n * 441}, as[1] = {(uint64_t)nframes * 16};
     if (int rc = make_map(&g.a, s2d, 2, ad, as, "s2d pixel rows", C1_ROWS)) return rc;
     for (int q = 0; q < groups; ++q) {
@@ -1862,6 +1886,154 @@ int tma_conv1_shift(const pq_net *nets, const bf16 *s2d, int nframes, const int 
                     "conv1 forward (shifted descriptors)");
 }
 
+// ---- conv2 forward by row-shifted descriptors over the 2x2 space-to-depth of act1
+// act1s2[s][Y][X][(dy*2 + dx)*32 + c] = act1[s][2Y+dy][2X+dx][c] (written by k_conv1_shift)
+// turns conv2 (4x4 / 2 over 20 x 20 x 32) into a 2 x 2 stride-1 conv over 10 x 10 x 128:
+// GEMM row r = (s, Y, X) of the 10 x 10 grid (Y, X = 9 discarded), tap (ty, tx) reads row
+// r + 10 ty + tx.  One TMA box of 144 rows per 64-channel half (dy = 0 / 1) feeds all
+// taps.  The MMAs run in the K order of the im2col kernel (ky = 2 ty + dy, kx pair tx, c:
+// K chunk q of W2 is its plain column block), so act2 is bit-identical.
+constexpr int C2F_ROWS = 144, C2F_BOX = C2F_ROWS * 128, C2F_STAGES = 2, C2F_W = 64 * 128;
+constexpr int C2F_SMEM = 1024 + 2 * 8 * C2F_W + C2F_STAGES * 2 * C2F_BOX;
+struct C2FArgs {
+    CUtensorMap a[2], w[2];  // act1s2 pixel rows [n*100][128]; W2 [64][512]
+    EpiBiasRelu ep[2];       // act2 [n*81][64]
+    int n, groups;
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_shift(const __grid_constant__ C2FArgs g) {
+    TlProbe tp;
+    constexpr uint32_t IDESC = idesc_bf16(64, false, false);
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t full[C2F_STAGES], empty[C2F_STAGES], accf[2], acce[2], wbar;
+    __shared__ uint32_t tmem_base_s;
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t w_s = smem_u32(smem), ring_s = w_s + 2 * 8 * C2F_W;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < C2F_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&accf[b], 1);
+            mbar_init(&acce[b], 4);
+        }
+        mbar_init(&wbar, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<128>(&tmem_base_s);
+    if (tid == 32)
+        for (int q = 0; q < g.groups; ++q) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&g.a[q]) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&g.w[q]) : "memory");
+        }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const int mt = (g.n * 100 + 127) / 128, total = mt * g.groups;
+    if (tid == 0) {  // W2 (updated two or more launches back) before the dependency wait
+        mbar_expect_tx(&wbar, (uint32_t)(g.groups * 8 * C2F_W));
+        for (int q = 0; q < g.groups; ++q)
+            for (int c = 0; c < 8; ++c) tma_load_2d(w_s + (q * 8 + c) * C2F_W, &g.w[q], &wbar, c * 64, 0);
+    }
+    griddep_wait();
+    griddep_launch();
+    tp.waited();
+    if (warp == 0) {
+        if (lane == 0) {  // producer: tile t = (m-tile t / groups, group t % groups)
+            uint32_t q = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
+                const uint32_t s = q % C2F_STAGES, dst = ring_s + s * 2 * C2F_BOX;
+                const int grp = t % g.groups, m = t / g.groups;
+                if (q >= C2F_STAGES) mbar_wait(&empty[s], ((q / C2F_STAGES) - 1) & 1);
+                mbar_expect_tx(&full[s], (uint32_t)(2 * C2F_BOX));
+                tma_load_2d(dst, &g.a[grp], &full[s], 0, m * 128);
+                tma_load_2d(dst + C2F_BOX, &g.a[grp], &full[s], 64, m * 128);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            mbar_wait(&wbar, 0);
+            uint32_t q = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
+                const uint32_t buf = q & 1, s = q % C2F_STAGES;
+                const int grp = t % g.groups;
+                if (q >= 2) mbar_wait(&acce[buf], ((q >> 1) - 1) & 1);
+                mbar_wait(&full[s], (q / C2F_STAGES) & 1);
+                tc_fence_after();
+                const uint32_t a0 = ring_s + s * 2 * C2F_BOX, acc = tmem + buf * 64;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {  // K chunk c of the im2col order: ky = c >> 1, kx pair c & 1
+                    const int ky = c >> 1, ty = ky >> 1, dy = ky & 1, tx = c & 1;
+                    const uint32_t abase = a0 + dy * C2F_BOX + (uint32_t)(ty * 10 + tx) * 128;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint64_t ad = desc_sw128(abase + j * 32, 0);
+                        const uint64_t bd = desc_sw128(w_s + (grp * 8 + c) * C2F_W + j * 32, 0);
+                        umma_bf16(acc, ad, bd, IDESC, (c > 0 || j > 0) ? 1u : 0u);
+                    }
+                }
+                umma_commit(&empty[s]);
+                umma_commit(&accf[buf]);
+            }
+        }
+    } else if (warp >= 4) {  // epilogue
+        const int wq = warp - 4;
+        uint32_t q = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
+            const uint32_t buf = q & 1;
+            const int grp = t % g.groups, m = t / g.groups;
+            mbar_wait(&accf[buf], (q >> 1) & 1);
+            __syncwarp();
+            tc_fence_after();
+            float v[2][32];
+            const uint32_t trow = tmem + buf * 64 + ((uint32_t)(wq * 32) << 16);
+            tmem_ld32(trow, v[0]);
+            tmem_ld32(trow + 32, v[1]);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acce[buf]);
+            const int r = m * 128 + wq * 32 + lane, smp = r / 100, p = r - smp * 100, y = p / 10, x = p - y * 10;
+            if (smp < g.n && y < 9 && x < 9) {
+                const int o = smp * 81 + y * 9 + x;
+                g.ep[grp].apply(o, 0, v[0], 32, 0);
+                g.ep[grp].apply(o, 32, v[1], 32, 0);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<128>(tmem);
+    tp.done('2');
+}
+
+int tma_conv2_shift(const pq_net *nets, bf16 *const *act1s2, bf16 *const *act2, int groups, int n, cudaStream_t st) {
+    static C2FArgs g;
+    memset(&g, 0, sizeof(g));
+    for (int q = 0; q < groups; ++q) {
+        const uint64_t ad[2] = {128, (uint64_t)n * 100}, as[1] = {128};
+        if (int rc = make_map(&g.a[q], act1s2[q], 2, ad, as, "act1 s2d rows", C2F_ROWS)) return rc;
+        if (int rc = map2(&g.w[q], (const bf16 *)nets[q].shadow + S_W2, 64, 512, 512, "W2")) return rc;
+        g.ep[q] = EpiBiasRelu{act2[q], nets[q].master + P_B2, n * 81, 64, 64, 1.0f};
+    }
+    g.n = n, g.groups = groups;
+    static bool configured = false;
+    if (!configured) {
+        PQ_CUDA_TRY(cudaFuncSetAttribute(k_conv2_shift, cudaFuncAttributeMaxDynamicSharedMemorySize, C2F_SMEM));
+        configured = true;
+    }
+    if (!g_sms) {
+        int dev = 0;
+        PQ_CUDA_TRY(cudaGetDevice(&dev));
+        PQ_CUDA_TRY(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int total = ((n * 100 + 127) / 128) * groups;
+    return cuda_err(launch_k(k_conv2_shift, dim3(std::min(total, g_sms)), dim3(GEMM_THREADS), C2F_SMEM, st, g),
+                    "conv2 forward (shifted descriptors)");
+}
+
 // ---- conv1 weight gradient by row-shifted descriptors (the transpose of k_conv1_shift)
 // part1[split][k'][o] = sum over the split's rows r of the padded 21 x 21 grid of
 // s2d[r + 21 ty + tx][c] dY1p[r][o] (k' = tap * 64 + c, tap = (ty, tx)), row 256 = the
@@ -1881,6 +2053,7 @@ struct W1SArgs {
 };
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __grid_constant__ W1SArgs g) {
+    TlProbe tp;
     constexpr uint32_t IDESC = idesc_bf16(64, true, true);
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t full[W1S_STAGES], empty[W1S_STAGES], accf;
@@ -1923,6 +2096,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __g
         }
     griddep_wait();
     griddep_launch();
+    tp.waited();
     if (warp == 0) {
         if (lane == 0) {  // producer
             uint32_t q = 0;
@@ -1977,6 +2151,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __g
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc<256>(tmem);
+    tp.done('W');
 }
 
 int tma_conv1_wgrad_shift(const bf16 *s2d, int nframes, const bf16 *dY1p, float *part1, int kc, int splits,
@@ -2043,9 +2218,10 @@ int pq_plearn_timeline(int on, unsigned long long *out, int *count) {
         *count = h.n < 256 ? h.n : 256;
         memcpy(out, h.t, sizeof(h.t));
     }
-    Timeline z{};
+    static Timeline z;
+    memset(&z, 0, sizeof(z));
     z.on = on;
-    PQ_CUDA_TRY(cudaMemcpyToSymbol(g_tl, &z, sizeof(int) * 2));
+    PQ_CUDA_TRY(cudaMemcpyToSymbol(g_tl, &z, sizeof(Timeline)));
     return 0;
 }
 

@@ -54,7 +54,8 @@ int tma_frames_s2d(const uint8_t *ring, const int32_t *refs, const int64_t *map,
 int tma_conv1_fwd(const pq_net *nets, const bf16 *s2d, int nframes, const int *c0, bf16 *const *act1, int groups,
                   int n, cudaStream_t st);
 int tma_conv1_shift(const pq_net *nets, const bf16 *s2d, int nframes, const int *c0, bf16 *const *act1,
-                    int groups, int n, int a_early, int w_early, cudaStream_t st);
+                    int groups, int n, int a_early, int w_early, cudaStream_t st, bf16 *const *act1s2);
+int tma_conv2_shift(const pq_net *nets, bf16 *const *act1s2, bf16 *const *act2, int groups, int n, cudaStream_t st);
 int tma_conv1_wgrad(const bf16 *s2d, int nframes, const bf16 *dY1, float *part1, int kc, int splits, int n,
                     cudaStream_t st);
 int tma_conv1_wgrad_shift(const bf16 *s2d, int nframes, const bf16 *dY1p, float *part1, int kc, int splits,
@@ -94,6 +95,7 @@ struct WS {
     bf16 *dY3, *dY2, *dY1;
     bf16 *dY1p;  // conv2's data gradient on the padded 21 x 21 grid (TMA engine; pad rows stay 0)
     bf16 *dY2p;  // conv3's data gradient on the padded 11 x 11 grid (TMA engine; pad rows stay 0)
+    bf16 *act1s2[2];  // act1 as 2x2 space-to-depth [n][10][10][128] (TMA engine, shifted conv2)
     float *part1, *part2, *part3, *grad4;
     uint32_t *done;  // [3] CTA completion counters (unused, acting, head)
     int64_t *idx_cur;  // the step's sampled slots (stashed by the head)
@@ -142,6 +144,7 @@ static WS carve(void *base, int N, int A) {
     w.s2d = N >= 128 ? (bf16 *)take((size_t)N * 441 * 80 * 2) : nullptr;
     w.dY1p = N >= 128 ? (bf16 *)take((size_t)N * 441 * 32 * 2) : nullptr;  // zeroed with the workspace
     w.dY2p = N >= 128 ? (bf16 *)take((size_t)N * 121 * 64 * 2) : nullptr;
+    for (int g = 0; g < 2; ++g) w.act1s2[g] = N >= 128 ? (bf16 *)take((size_t)N * 100 * 128 * 2) : nullptr;
     w.bytes = off;
     return w;
 }
@@ -307,7 +310,7 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
                                     ins[0].ref_stride, ins[0].ref_off, nframes, n, w.s2d, st))
             return rc;
         if (conv1_shift()) {  // the s2d kernel just wrote the frames; weights are two launches back
-            if (int rc = tma_conv1_shift(nets, w.s2d, nframes, c0, a1, groups, n, 0, 1, st)) return rc;
+            if (int rc = tma_conv1_shift(nets, w.s2d, nframes, c0, a1, groups, n, 0, 1, st, w.act1s2)) return rc;
         } else if (int rc = tma_conv1_fwd(nets, w.s2d, nframes, c0, a1, groups, n, st)) {
             return rc;
         }
@@ -329,6 +332,9 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
     const bool fused = use_conv23();
     if (fused) {
         if (int rc = conv23(nets, groups, n, w, st)) return rc;
+    } else if (use_tma(n) && w.s2d && conv1_shift() && w.act1s2[0]) {  // F2 over act1's 2x2 space-to-depth
+        bf16 *s2[2] = {w.act1s2[0], w.act1s2[1]};
+        if (int rc = tma_conv2_shift(nets, s2, a2, groups, n, st)) return rc;
     } else {  // F2: conv2 4x4/2 over 20x20x32 (K = 512)
         GemmArgs<LoadIm2col, LoadDense, EpiBiasRelu> g{};
         for (int q = 0; q < groups; ++q) {
@@ -447,8 +453,10 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
 // Fixed order within and across chunks (deterministic); large batches only.
 __global__ void __launch_bounds__(512) k_fc2_partials(const float *h1, const float *dh1, const float *td,
                                                       const int32_t *act, int n, int A, float *part) {
+    TlProbe tp;
     griddep_wait();
     griddep_launch();
+    tp.waited();
     __shared__ float s_d[FC_CHUNK];
     __shared__ int s_a[FC_CHUNK];
     const int b0 = blockIdx.x * FC_CHUNK, nb = min(FC_CHUNK, n - b0), j = threadIdx.x;
@@ -489,6 +497,7 @@ __global__ void __launch_bounds__(512) k_fc2_partials(const float *h1, const flo
         if (aa < A) out[aa * 512 + j] = acc[aa];
     out[A * 512 + j] = ab;
     if (j < A) out[(A + 1) * 512 + j] = bb;
+    tp.done('P');
 }
 
 // ------------------------------------------------------------------ optimizer
@@ -569,11 +578,13 @@ static int get_fork(Fork **out) {
     int dev = 0;
     PQ_CHECK(cudaGetDevice(&dev), "get device");
     Fork &f = g_fork[dev & 15];
-    if (!f.side) {  // the weight-gradient branch (PQ_PRIO=1: highest stream priority)
+    if (!f.side) {  // the weight-gradient branch at the highest stream priority (PQ_SIDE_PRIO=0:
+        // default priority): its kernels otherwise wait for SMs behind the main stream's
+        // persistent grids and end up on the critical path (batch 1024: 427 -> 405 us/step)
         int lo = 0, hi = 0;
         PQ_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
-        const char *e = getenv("PQ_PRIO");
-        const int prio = (e && e[0] == '1') ? hi : lo;
+        const char *e = getenv("PQ_SIDE_PRIO");
+        const int prio = (e && e[0] == '0') ? lo : hi;
         PQ_CHECK(cudaStreamCreateWithPriority(&f.side, cudaStreamNonBlocking, prio), "side stream");
         PQ_CHECK(cudaStreamCreateWithPriority(&f.side2, cudaStreamNonBlocking, prio), "side stream 2");
         for (auto &e : f.ev) PQ_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
