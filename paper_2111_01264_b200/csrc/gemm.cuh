@@ -408,6 +408,23 @@ struct EpiBiasRelu {
     const float *bias;
     int M, N, ld;
     float scale;
+    // all 32 columns of row m (n0 = 0, N >= 32) to out[m] and to dst2 as well
+    PQ_DEV void apply_dual(int m, const float *v, bf16 *dst2) const {
+        bf16 *dst = out + (size_t)m * ld;
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+            float y[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const float t = v[j + e] * scale + __ldg(bias + j + e);
+                y[e] = t > 0.f ? t : 0.f;
+            }
+            const uint4 pk = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]),
+                                        pack_bf16(y[6], y[7]));
+            *reinterpret_cast<uint4 *>(dst + j) = pk;
+            *reinterpret_cast<uint4 *>(dst2 + j) = pk;
+        }
+    }
     PQ_DEV void apply(int m, int n0, const float *v, int cnt, int) const {
         float bv[32];
 #pragma unroll

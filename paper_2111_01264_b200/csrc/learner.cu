@@ -1837,12 +1837,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_co
 #pragma unroll
                 for (int gg = 0; gg < 2; ++gg) {
                     if (gg >= g.groups) break;
-                    g.ep[gg].apply(m, 0, v[gg], 32, 0);
-                    if (g.act1s2[gg]) {
-                        EpiBiasRelu e2 = g.ep[gg];
-                        e2.out = g.act1s2[gg] + o2, e2.ld = 0;
-                        e2.apply(0, 0, v[gg], 32, 0);
-                    }
+                    if (g.act1s2[gg])
+                        g.ep[gg].apply_dual(m, v[gg], g.act1s2[gg] + o2);
+                    else
+                        g.ep[gg].apply(m, 0, v[gg], 32, 0);
                 }
             }
         }
