@@ -516,16 +516,21 @@ struct EpiMask {
 
 // EpiMask that also writes the masked rows of a 9 x 9 map onto a zero-padded 11 x 11
 // grid at (y + 1, x + 1) (conv3's data gradient for k_conv2_dgrad_shift)
+// (and, if out10 is set, onto a 10 x 10 grid at (y, x): k_conv2_wgrad_shift's operand)
 struct EpiMaskPad {
     EpiMask e;
     bf16 *out_pad;
     FastDiv f81, f9;
+    bf16 *out10;
     PQ_DEV void apply(int m, int n0, const float *v, int cnt, int sp) const {
         e.apply(m, n0, v, cnt, sp);
         if (m >= e.M || n0 >= e.N) return;
         const int s = f81.div(m), q = m - s * 81, y = f9.div(q), x = q - y * 9;
         const size_t oo = ((size_t)(s * 11 + y + 1) * 11 + x + 1) * e.ld + n0;
         store_masked32(out_pad + oo, e.mask + (size_t)m * e.ld + n0, v, min(cnt, e.N - n0));
+        if (out10)
+            store_masked32(out10 + ((size_t)(s * 10 + y) * 10 + x) * e.ld + n0, e.mask + (size_t)m * e.ld + n0, v,
+                           min(cnt, e.N - n0));
     }
 };
 

@@ -1429,14 +1429,14 @@ int tma_fc1_dgrad(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *
 
 // conv3 data gradient: dY2 = relu'(act2) * transposed conv3(dY3) (im2col window, pad 2)
 int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st,
-                    bf16 *dY2p) {
+                    bf16 *dY2p, bf16 *dY2q) {
     if (dY2p) {  // also onto the padded 11 x 11 grid of the shifted conv2 data gradient
         static TmaGemm<EpiMaskPad> g;
         memset(&g, 0, sizeof(g));
         if (int rc = map_im2col(&g.a[0], dY3, n, 7, 7, -2, 0, 128, "dY3")) return rc;
         const uint64_t dims[3] = {64, 9, 64}, strd[2] = {64, 576};
         if (int rc = make_map(&g.b[0], (const bf16 *)th.shadow + S_W3, 3, dims, strd, "W3 view")) return rc;
-        g.ep[0] = EpiMaskPad{EpiMask{dY2, act2, n * 81, 64, 64}, dY2p, FastDiv(81), FastDiv(9)};
+        g.ep[0] = EpiMaskPad{EpiMask{dY2, act2, n * 81, 64, 64}, dY2p, FastDiv(81), FastDiv(9), dY2q};
         g.kindA = OP_IT3, g.kindB = OP_W3V, g.boxesA = 2, g.boxesB = 1, g.n = n, g.b_is_weight = 1;
         g.mtiles = (n * 81 + 127) / 128, g.ntiles = 1, g.splits = 1, g.groups = 1, g.kc = 9, g.nk = 9;
         return launch_tma<64, false, true>(g, st, "conv3 dgrad (TMA, padded copy)");
@@ -2030,6 +2030,150 @@ int tma_conv2_shift(const pq_net *nets, bf16 *const *act1s2, bf16 *const *act2, 
     const int total = ((n * 100 + 127) / 128) * groups;
     return cuda_err(launch_k(k_conv2_shift, dim3(std::min(total, g_sms)), dim3(GEMM_THREADS), C2F_SMEM, st, g),
                     "conv2 forward (shifted descriptors)");
+}
+
+// ---- conv2 weight gradient by row-shifted descriptors (the transpose of k_conv2_shift)
+// part2[split][c2][k] (k = (ky*4 + kx)*32 + c, the im2col order; k = 512 the bias row) =
+// sum over the split's rows r of the 10 x 10 grid of act1s2[r + 10 ty + tx][ch] dY2q[r][c2]
+// with dY2q = conv3's data gradient on that grid (zero rows at y or x = 9).  For tap
+// (ty, tx) the 128 channels of a space-to-depth pixel are the two contiguous 64-wide K
+// blocks ky = 2 ty + dy, kx = 2 tx .. 2 tx + 1: M tile = one tap, its two MN-major atoms
+// are the two 64-channel boxes at the same row shift (LBO = box distance); M tile 4 = a
+// ones column (bias row).  One CTA per split runs all five M tiles (320 TMEM columns).
+constexpr int W2S_ROWS = 80, W2S_ABOX = W2S_ROWS * 128, W2S_BBOX = 64 * 128, W2S_STAGES = 5;
+constexpr int W2S_SLOT = 2 * W2S_ABOX + W2S_BBOX;  // 28 KB, 1024-aligned
+constexpr int W2S_SMEM = 1024 + 2 * 8192 + W2S_STAGES * W2S_SLOT;
+struct W2SArgs {
+    CUtensorMap a, b;  // act1s2 pixel rows [n*100][128]; dY2q [n*100][64]
+    EpiF32T ep;        // part2[split][64][513]
+    int nk, kc;
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_wgrad_shift(const __grid_constant__ W2SArgs g) {
+    constexpr uint32_t IDESC = idesc_bf16(64, true, true);
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t full[W2S_STAGES], empty[W2S_STAGES], accf;
+    __shared__ uint32_t tmem_base_s;
+    TlProbe tp;
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t ones_s = smem_u32(smem), ring_s = ones_s + 2 * 8192;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int i = tid; i < 2 * 8192 / 16; i += blockDim.x) {  // ones operand: M index 0 = 1
+        const int atom = i >> 9, k = (i >> 3) & 63, c8 = i & 7;
+        uint4 val = make_uint4(0, 0, 0, 0);
+        if (atom == 0 && c8 == 0) val.x = 0x3F80u;
+        *reinterpret_cast<uint4 *>(smem + atom * 8192 + mnmaj_off(k, c8) % 8192) = val;
+    }
+    if (tid == 0) {
+        for (int s = 0; s < W2S_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&accf, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<512>(&tmem_base_s);
+    if (tid == 32) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&g.a) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&g.b) : "memory");
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const int split = blockIdx.x, kb0 = split * g.kc, kb1 = min(g.nk, kb0 + g.kc);
+    griddep_wait();
+    griddep_launch();
+    tp.waited();
+    if (warp == 0) {
+        if (lane == 0) {  // producer
+            uint32_t q = 0;
+            for (int kb = kb0; kb < kb1; ++kb, ++q) {
+                const uint32_t s = q % W2S_STAGES, dst = ring_s + s * W2S_SLOT;
+                if (q >= W2S_STAGES) mbar_wait(&empty[s], ((q / W2S_STAGES) - 1) & 1);
+                mbar_expect_tx(&full[s], (uint32_t)W2S_SLOT);
+                tma_load_2d(dst, &g.a, &full[s], 0, kb * 64);
+                tma_load_2d(dst + W2S_ABOX, &g.a, &full[s], 64, kb * 64);
+                tma_load_2d(dst + 2 * W2S_ABOX, &g.b, &full[s], 0, kb * 64);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer: five 128 x 64 accumulators
+            uint32_t q = 0;
+            for (int kb = kb0; kb < kb1; ++kb, ++q) {
+                const uint32_t s = q % W2S_STAGES;
+                mbar_wait(&full[s], (q / W2S_STAGES) & 1);
+                tc_fence_after();
+                const uint32_t a0 = ring_s + s * W2S_SLOT, b0 = a0 + 2 * W2S_ABOX;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {  // K steps of 16 rows (2048 B)
+                    const uint32_t acc_on = (kb > kb0 || j > 0) ? 1u : 0u;
+                    const uint64_t bd = desc_sw128(b0 + j * 2048, 8192);
+#pragma unroll
+                    for (int tap = 0; tap < 4; ++tap) {
+                        const uint32_t shift = (uint32_t)((tap >> 1) * 10 + (tap & 1)) * 128;
+                        umma_bf16(tmem + tap * 64, desc_sw128(a0 + shift + j * 2048, W2S_ABOX), bd, IDESC, acc_on);
+                    }
+                    umma_bf16(tmem + 256, desc_sw128(ones_s + j * 2048, 8192), bd, IDESC, acc_on);
+                }
+                umma_commit(&empty[s]);
+            }
+            umma_commit(&accf);
+        }
+    } else if (warp >= 4) {  // epilogue: M row i of tap tile -> k
+        const int wq = warp - 4;
+        mbar_wait(&accf, 0);
+        __syncwarp();
+        tc_fence_after();
+#pragma unroll 1
+        for (int mt = 0; mt < 5; ++mt) {
+            const int i = wq * 32 + lane;
+            int k;
+            if (mt < 4) {
+                const int ty = mt >> 1, tx = mt & 1, dy = i >> 6;
+                k = ((2 * ty + dy) * 4 + 2 * tx) * 32 + (i & 63);
+            } else {
+                k = i == 0 ? 512 : -1;
+            }
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                float v[32];
+                if (kb1 > kb0) {
+                    tmem_ld32(tmem + mt * 64 + h * 32 + ((uint32_t)(wq * 32) << 16), v);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
+                }
+                if (k >= 0) g.ep.apply(k, h * 32, v, 32, split);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem);
+    tp.done('V');
+}
+
+int tma_conv2_wgrad_shift(const bf16 *act1s2, const bf16 *dY2q, float *part2, int kc, int splits, int n,
+                          cudaStream_t st) {
+    static W2SArgs g;
+    memset(&g, 0, sizeof(g));
+    const uint64_t ad[2] = {128, (uint64_t)n * 100}, as[1] = {128};
+    if (int rc = make_map(&g.a, act1s2, 2, ad, as, "act1 s2d rows (wgrad)", W2S_ROWS)) return rc;
+    if (int rc = map2(&g.b, dY2q, (uint64_t)n * 100, 64, 64, "dY2 10x10")) return rc;
+    g.ep = EpiF32T{part2, 513, 64, 513, (size_t)64 * 513};
+    g.nk = (n * 100 + 63) / 64;
+    g.kc = kc;
+    const int grid = (g.nk + kc - 1) / kc;
+    if (grid != splits) return set_err("conv2 wgrad shift: split count mismatch");
+    static bool configured = false;
+    if (!configured) {
+        PQ_CUDA_TRY(cudaFuncSetAttribute(k_conv2_wgrad_shift, cudaFuncAttributeMaxDynamicSharedMemorySize, W2S_SMEM));
+        configured = true;
+    }
+    return cuda_err(launch_k(k_conv2_wgrad_shift, dim3(grid), dim3(GEMM_THREADS), W2S_SMEM, st, g),
+                    "conv2 wgrad (shifted descriptors)");
 }
 
 // ---- conv1 weight gradient by row-shifted descriptors (the transpose of k_conv1_shift)

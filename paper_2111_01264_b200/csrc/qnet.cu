@@ -43,7 +43,9 @@ int tma_fc1_fwd(const pq_net *nets, bf16 *const *act3, float *const *part, int s
                 cudaStream_t st);
 int tma_fc1_dgrad(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *dY3, int n, cudaStream_t st);
 int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st,
-                    bf16 *dY2p);
+                    bf16 *dY2p, bf16 *dY2q);
+int tma_conv2_wgrad_shift(const bf16 *act1s2, const bf16 *dY2q, float *part2, int kc, int splits, int n,
+                          cudaStream_t st);
 int tma_conv2_dgrad_shift(const pq_net &th, const bf16 *dY2p, const bf16 *act1, bf16 *dY1, int n, int pad21,
                           cudaStream_t st);
 int tma_conv3_wgrad(const bf16 *act2, const bf16 *dY3, float *part3, int kc, int splits, int n, cudaStream_t st);
@@ -96,6 +98,7 @@ struct WS {
     bf16 *dY1p;  // conv2's data gradient on the padded 21 x 21 grid (TMA engine; pad rows stay 0)
     bf16 *dY2p;  // conv3's data gradient on the padded 11 x 11 grid (TMA engine; pad rows stay 0)
     bf16 *act1s2[2];  // act1 as 2x2 space-to-depth [n][10][10][128] (TMA engine, shifted conv2)
+    bf16 *dY2q;       // conv3's data gradient on the 10 x 10 grid (zero rows at 9; shifted conv2 wgrad)
     float *part1, *part2, *part3, *grad4;
     uint32_t *done;  // [3] CTA completion counters (unused, acting, head)
     int64_t *idx_cur;  // the step's sampled slots (stashed by the head)
@@ -145,6 +148,7 @@ static WS carve(void *base, int N, int A) {
     w.dY1p = N >= 128 ? (bf16 *)take((size_t)N * 441 * 32 * 2) : nullptr;  // zeroed with the workspace
     w.dY2p = N >= 128 ? (bf16 *)take((size_t)N * 121 * 64 * 2) : nullptr;
     for (int g = 0; g < 2; ++g) w.act1s2[g] = N >= 128 ? (bf16 *)take((size_t)N * 100 * 128 * 2) : nullptr;
+    w.dY2q = N >= 128 ? (bf16 *)take((size_t)N * 100 * 64 * 2) : nullptr;
     w.bytes = off;
     return w;
 }
@@ -824,13 +828,21 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     }
     const bool shift = conv1_shift() && w.dY1p && w.dY2p;  // shifted-descriptor conv kernels (TMA engine)
     if (use_tma(n)) {
-        if (int rc = tma_conv3_dgrad(th, w.dY3, w.act2[0], w.dY2, n, st, shift ? w.dY2p : nullptr)) return rc;
+        if (int rc = tma_conv3_dgrad(th, w.dY3, w.act2[0], w.dY2, n, st, shift ? w.dY2p : nullptr,
+                                     shift ? w.dY2q : nullptr))
+            return rc;
     } else {
         PQ_CHECK((launch_gemm<64, false, true, 0, 2>(args_b3d(sh, w, n), 1, st)), "conv3 dgrad");
     }
     PQ_CHECK(cudaEventRecord(fk->ev[2], st), "fork2");
     PQ_CHECK(cudaStreamWaitEvent(side2, fk->ev[2], 0), "fork2 wait");
-    PQ_CHECK((launch_gemm<64, true, true>(args_b2w(w, n, &s2), 1, side2)), "conv2 wgrad");
+    if (shift) {  // over act1's space-to-depth copy and dY2 on the 10 x 10 grid
+        const int nk = (n * 100 + 63) / 64, kc = (nk + MAX_SPLITS - 1) / MAX_SPLITS;
+        s2 = (nk + kc - 1) / kc;
+        if (int rc = tma_conv2_wgrad_shift(w.act1s2[0], w.dY2q, w.part2, kc, s2, n, side2)) return rc;
+    } else {
+        PQ_CHECK((launch_gemm<64, true, true>(args_b2w(w, n, &s2), 1, side2)), "conv2 wgrad");
+    }
     if (use_tma(n)) {
         if (shift) {  // dY1 onto the padded grid of the shifted conv1 weight gradient
             if (int rc = tma_conv2_dgrad_shift(th, w.dY2p, w.act1[0], w.dY1p, n, 1, st)) return rc;
