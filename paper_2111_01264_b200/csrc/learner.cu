@@ -1884,32 +1884,47 @@ int tma_conv1_shift(const pq_net *nets, const bf16 *s2d, int nframes, const int 
                     "conv1 forward (shifted descriptors)");
 }
 
-// ---- conv2 forward by row-shifted descriptors over the 2x2 space-to-depth of act1
-// act1s2[s][Y][X][(dy*2 + dx)*32 + c] = act1[s][2Y+dy][2X+dx][c] (written by k_conv1_shift)
-// turns conv2 (4x4 / 2 over 20 x 20 x 32) into a 2 x 2 stride-1 conv over 10 x 10 x 128:
-// GEMM row r = (s, Y, X) of the 10 x 10 grid (Y, X = 9 discarded), tap (ty, tx) reads row
-// r + 10 ty + tx.  One TMA box of 144 rows per 64-channel half (dy = 0 / 1) feeds all
-// taps.  The MMAs run in the K order of the im2col kernel (ky = 2 ty + dy, kx pair tx, c:
-// K chunk q of W2 is its plain column block), so act2 is bit-identical.
-constexpr int C2F_ROWS = 144, C2F_BOX = C2F_ROWS * 128, C2F_STAGES = 2, C2F_W = 64 * 128;
-constexpr int C2F_SMEM = 1024 + 2 * 8 * C2F_W + C2F_STAGES * 2 * C2F_BOX;
-struct C2FArgs {
-    CUtensorMap a[2], w[2];  // act1s2 pixel rows [n*100][128]; W2 [64][512]
-    EpiBiasRelu ep[2];       // act2 [n*81][64]
+// ---- conv2 / conv3 forward by row-shifted descriptors
+// conv2: act1s2[s][Y][X][(dy*2 + dx)*32 + c] = act1[s][2Y+dy][2X+dx][c] (written by
+// k_conv1_shift) turns conv2 (4x4 / 2 over 20 x 20 x 32) into a 2 x 2 stride-1 conv over
+// 10 x 10 x 128: GEMM row r = (s, Y, X) of the 10 x 10 grid (Y, X = 9 discarded), tap
+// (ty, tx) reads row r + 10 ty + tx; one TMA box of 144 rows per 64-channel half
+// (dy = 0 / 1).  conv3 (3x3 / 1 over 9 x 9 x 64): the 7 x 7 outputs on the 9 x 9 grid of
+// act2 itself, tap (ky, kx) reads row r + 9 ky + kx; one box of 148 rows.  The MMAs run in
+// the K order of the im2col kernels (K chunk c of W is its plain 64-column block: conv2
+// ky = c >> 1, kx pair c & 1; conv3 tap c), so the activations are bit-identical.
+template <int CV>
+struct ConvShift {
+    static constexpr int GW = CV == 2 ? 10 : 9;    // grid width (rows per grid row)
+    static constexpr int RPS = GW * GW;            // grid rows per sample
+    static constexpr int OW = CV == 2 ? 9 : 7;     // valid output width
+    static constexpr int NCH = CV == 2 ? 8 : 9;    // 64-wide K chunks
+    static constexpr int NBOX = CV == 2 ? 2 : 1;   // 64-channel boxes per pixel row
+    static constexpr int ROWS = CV == 2 ? 144 : 152;
+    static constexpr int BOX = ROWS * 128, W = 64 * 128, STAGES = 2;
+    static constexpr int SMEM = 1024 + 2 * NCH * W + STAGES * NBOX * BOX;
+    PQ_HD static int box_of(int c) { return CV == 2 ? ((c >> 1) & 1) : 0; }
+    PQ_HD static int shift_of(int c) { return CV == 2 ? ((c >> 2) * 10 + (c & 1)) : ((c / 3) * 9 + c % 3); }
+};
+struct CSArgs {
+    CUtensorMap a[2], w[2];  // input pixel rows [n*RPS][64*NBOX]; W [64][64*NCH]
+    EpiBiasRelu ep[2];       // output [n*OW*OW][64]
     int n, groups;
 };
 
-__global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_shift(const __grid_constant__ C2FArgs g) {
-    TlProbe tp;
+template <int CV>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv_shift(const __grid_constant__ CSArgs g) {
+    using C = ConvShift<CV>;
     constexpr uint32_t IDESC = idesc_bf16(64, false, false);
     extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t full[C2F_STAGES], empty[C2F_STAGES], accf[2], acce[2], wbar;
+    __shared__ uint64_t full[C::STAGES], empty[C::STAGES], accf[2], acce[2], wbar;
     __shared__ uint32_t tmem_base_s;
+    TlProbe tp;
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t w_s = smem_u32(smem), ring_s = w_s + 2 * 8 * C2F_W;
+    const uint32_t w_s = smem_u32(smem), ring_s = w_s + 2 * C::NCH * C::W;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int s = 0; s < C2F_STAGES; ++s) {
+        for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -1930,11 +1945,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_shift(const __grid_co
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
-    const int mt = (g.n * 100 + 127) / 128, total = mt * g.groups;
-    if (tid == 0) {  // W2 (updated two or more launches back) before the dependency wait
-        mbar_expect_tx(&wbar, (uint32_t)(g.groups * 8 * C2F_W));
+    const int mt = (g.n * C::RPS + 127) / 128, total = mt * g.groups;
+    if (tid == 0) {  // weights (updated two or more launches back) before the dependency wait
+        mbar_expect_tx(&wbar, (uint32_t)(g.groups * C::NCH * C::W));
         for (int q = 0; q < g.groups; ++q)
-            for (int c = 0; c < 8; ++c) tma_load_2d(w_s + (q * 8 + c) * C2F_W, &g.w[q], &wbar, c * 64, 0);
+            for (int c = 0; c < C::NCH; ++c) tma_load_2d(w_s + (q * C::NCH + c) * C::W, &g.w[q], &wbar, c * 64, 0);
     }
     griddep_wait();
     griddep_launch();
@@ -1943,12 +1958,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_shift(const __grid_co
         if (lane == 0) {  // producer: tile t = (m-tile t / groups, group t % groups)
             uint32_t q = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
-                const uint32_t s = q % C2F_STAGES, dst = ring_s + s * 2 * C2F_BOX;
+                const uint32_t s = q % C::STAGES, dst = ring_s + s * C::NBOX * C::BOX;
                 const int grp = t % g.groups, m = t / g.groups;
-                if (q >= C2F_STAGES) mbar_wait(&empty[s], ((q / C2F_STAGES) - 1) & 1);
-                mbar_expect_tx(&full[s], (uint32_t)(2 * C2F_BOX));
-                tma_load_2d(dst, &g.a[grp], &full[s], 0, m * 128);
-                tma_load_2d(dst + C2F_BOX, &g.a[grp], &full[s], 64, m * 128);
+                if (q >= C::STAGES) mbar_wait(&empty[s], ((q / C::STAGES) - 1) & 1);
+                mbar_expect_tx(&full[s], (uint32_t)(C::NBOX * C::BOX));
+                for (int b = 0; b < C::NBOX; ++b) tma_load_2d(dst + b * C::BOX, &g.a[grp], &full[s], b * 64, m * 128);
             }
         }
     } else if (warp == 1) {
@@ -1956,20 +1970,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_shift(const __grid_co
             mbar_wait(&wbar, 0);
             uint32_t q = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
-                const uint32_t buf = q & 1, s = q % C2F_STAGES;
+                const uint32_t buf = q & 1, s = q % C::STAGES;
                 const int grp = t % g.groups;
                 if (q >= 2) mbar_wait(&acce[buf], ((q >> 1) - 1) & 1);
-                mbar_wait(&full[s], (q / C2F_STAGES) & 1);
+                mbar_wait(&full[s], (q / C::STAGES) & 1);
                 tc_fence_after();
-                const uint32_t a0 = ring_s + s * 2 * C2F_BOX, acc = tmem + buf * 64;
+                const uint32_t a0 = ring_s + s * C::NBOX * C::BOX, acc = tmem + buf * 64;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {  // K chunk c of the im2col order: ky = c >> 1, kx pair c & 1
-                    const int ky = c >> 1, ty = ky >> 1, dy = ky & 1, tx = c & 1;
-                    const uint32_t abase = a0 + dy * C2F_BOX + (uint32_t)(ty * 10 + tx) * 128;
+                for (int c = 0; c < C::NCH; ++c) {
+                    const uint32_t abase = a0 + C::box_of(c) * C::BOX + (uint32_t)C::shift_of(c) * 128;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         const uint64_t ad = desc_sw128(abase + j * 32, 0);
-                        const uint64_t bd = desc_sw128(w_s + (grp * 8 + c) * C2F_W + j * 32, 0);
+                        const uint64_t bd = desc_sw128(w_s + (grp * C::NCH + c) * C::W + j * 32, 0);
                         umma_bf16(acc, ad, bd, IDESC, (c > 0 || j > 0) ? 1u : 0u);
                     }
                 }
@@ -1993,9 +2006,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_shift(const __grid_co
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acce[buf]);
-            const int r = m * 128 + wq * 32 + lane, smp = r / 100, p = r - smp * 100, y = p / 10, x = p - y * 10;
-            if (smp < g.n && y < 9 && x < 9) {
-                const int o = smp * 81 + y * 9 + x;
+            const int r = m * 128 + wq * 32 + lane, smp = r / C::RPS, p = r - smp * C::RPS, y = p / C::GW,
+                      x = p - y * C::GW;
+            if (smp < g.n && y < C::OW && x < C::OW) {
+                const int o = (smp * C::OW + y) * C::OW + x;
                 g.ep[grp].apply(o, 0, v[0], 32, 0);
                 g.ep[grp].apply(o, 32, v[1], 32, 0);
             }
@@ -2004,22 +2018,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_shift(const __grid_co
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc<128>(tmem);
-    tp.done('2');
+    tp.done(CV == 2 ? '2' : '3');
 }
 
-int tma_conv2_shift(const pq_net *nets, bf16 *const *act1s2, bf16 *const *act2, int groups, int n, cudaStream_t st) {
-    static C2FArgs g;
+template <int CV>
+static int launch_conv_shift(const pq_net *nets, bf16 *const *in, bf16 *const *out, int groups, int n, cudaStream_t st) {
+    using C = ConvShift<CV>;
+    static CSArgs g;
     memset(&g, 0, sizeof(g));
+    const int64_t wofs = CV == 2 ? S_W2 : S_W3, bofs = CV == 2 ? P_B2 : P_B3;
     for (int q = 0; q < groups; ++q) {
-        const uint64_t ad[2] = {128, (uint64_t)n * 100}, as[1] = {128};
-        if (int rc = make_map(&g.a[q], act1s2[q], 2, ad, as, "act1 s2d rows", C2F_ROWS)) return rc;
-        if (int rc = map2(&g.w[q], (const bf16 *)nets[q].shadow + S_W2, 64, 512, 512, "W2")) return rc;
-        g.ep[q] = EpiBiasRelu{act2[q], nets[q].master + P_B2, n * 81, 64, 64, 1.0f};
+        const uint64_t ad[2] = {(uint64_t)64 * C::NBOX, (uint64_t)n * C::RPS}, as[1] = {(uint64_t)64 * C::NBOX};
+        if (int rc = make_map(&g.a[q], in[q], 2, ad, as, "conv input pixel rows", C::ROWS)) return rc;
+        if (int rc = map2(&g.w[q], (const bf16 *)nets[q].shadow + wofs, 64, 64 * C::NCH, 64 * C::NCH, "conv W"))
+            return rc;
+        g.ep[q] = EpiBiasRelu{out[q], nets[q].master + bofs, n * C::OW * C::OW, 64, 64, 1.0f};
     }
     g.n = n, g.groups = groups;
     static bool configured = false;
     if (!configured) {
-        PQ_CUDA_TRY(cudaFuncSetAttribute(k_conv2_shift, cudaFuncAttributeMaxDynamicSharedMemorySize, C2F_SMEM));
+        PQ_CUDA_TRY(cudaFuncSetAttribute(k_conv_shift<CV>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         configured = true;
     }
     if (!g_sms) {
@@ -2027,9 +2045,15 @@ int tma_conv2_shift(const pq_net *nets, bf16 *const *act1s2, bf16 *const *act2, 
         PQ_CUDA_TRY(cudaGetDevice(&dev));
         PQ_CUDA_TRY(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    const int total = ((n * 100 + 127) / 128) * groups;
-    return cuda_err(launch_k(k_conv2_shift, dim3(std::min(total, g_sms)), dim3(GEMM_THREADS), C2F_SMEM, st, g),
-                    "conv2 forward (shifted descriptors)");
+    const int total = ((n * C::RPS + 127) / 128) * groups;
+    return cuda_err(launch_k(k_conv_shift<CV>, dim3(std::min(total, g_sms)), dim3(GEMM_THREADS), C::SMEM, st, g),
+                    CV == 2 ? "conv2 forward (shifted descriptors)" : "conv3 forward (shifted descriptors)");
+}
+int tma_conv2_shift(const pq_net *nets, bf16 *const *act1s2, bf16 *const *act2, int groups, int n, cudaStream_t st) {
+    return launch_conv_shift<2>(nets, act1s2, act2, groups, n, st);
+}
+int tma_conv3_shift(const pq_net *nets, bf16 *const *act2, bf16 *const *act3, int groups, int n, cudaStream_t st) {
+    return launch_conv_shift<3>(nets, act2, act3, groups, n, st);
 }
 
 // ---- conv2 weight gradient by row-shifted descriptors (the transpose of k_conv2_shift)

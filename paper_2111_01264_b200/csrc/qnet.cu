@@ -58,6 +58,7 @@ int tma_conv1_fwd(const pq_net *nets, const bf16 *s2d, int nframes, const int *c
 int tma_conv1_shift(const pq_net *nets, const bf16 *s2d, int nframes, const int *c0, bf16 *const *act1,
                     int groups, int n, int a_early, int w_early, cudaStream_t st, bf16 *const *act1s2);
 int tma_conv2_shift(const pq_net *nets, bf16 *const *act1s2, bf16 *const *act2, int groups, int n, cudaStream_t st);
+int tma_conv3_shift(const pq_net *nets, bf16 *const *act2, bf16 *const *act3, int groups, int n, cudaStream_t st);
 int tma_conv1_wgrad(const bf16 *s2d, int nframes, const bf16 *dY1, float *part1, int kc, int splits, int n,
                     cudaStream_t st);
 int tma_conv1_wgrad_shift(const bf16 *s2d, int nframes, const bf16 *dY1p, float *part1, int kc, int splits,
@@ -352,6 +353,8 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
     // engine per GEMM (measured, profiles/r1_engine_compare.md): the TMA im2col conv3
     // forward wins once a CTA has several tiles; at small batch the cp.async one does
     if (fused) {
+    } else if (use_tma(n) && conv1_shift()) {  // the 7 x 7 outputs on act2's own 9 x 9 grid
+        if (int rc = tma_conv3_shift(nets, a2, a3, groups, n, st)) return rc;
     } else if (use_tma(n)) {
         if (int rc = tma_conv3_fwd(nets, a2, a3, groups, n, st)) return rc;
     } else {  // F3: conv3 3x3/1 over 9x9x64 (K = 576)

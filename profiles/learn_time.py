@@ -4,7 +4,7 @@ import ctypes
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.getcwd())  # the tree under test (scripts/ab_learn_time.sh runs it from each tree)
 import numpy as np
 import torch
 

@@ -6,11 +6,11 @@ switches are read once per process):
 * PQ_TMA=1 — the warp-specialised TMA engine forced at batch 32 (default: from 128):
   Q-values bit-identical, one learner step within fp32 summation order (1e-5) of the
   cp.async engine;
-* PQ_C1SHIFT=0 — conv1 forward / weight gradient and conv2 data gradient by TMA im2col
-  instead of row-shifted descriptors (batch >= 128): the forward and the data gradient
-  run the same MMA sequences, so Q-values are bit-identical; the conv1 weight gradient
-  sums the padded 21 x 21 grid in other K chunks and splits, so the learner update agrees
-  to fp32 summation order (1e-5);
+* PQ_C1SHIFT=0 — the conv layers by TMA im2col / cp.async gathers instead of row-shifted
+  descriptors (batch >= 128): the conv1/2/3 forward and the conv2 data gradient run the
+  same MMA sequences, so Q-values are bit-identical; the conv1/conv2 weight gradients sum
+  the padded grids in other K chunks and splits, so the learner update agrees to fp32
+  summation order (1e-5);
 * PQ_FUSED=0 — the multi-stream learner backward instead of the single-stream fused
   launches (batch < 128): the same GEMMs and reductions, bit-identical update."""
 
