@@ -114,8 +114,9 @@ size_t pq_workspace_bytes(int max_batch, int actions);
 /* Byte offsets of the workspace buffers (stage-wise kernel tests), in order:
  * act1, act2, act3, fc1part (online), act1, act2, act3, fc1part (target), q, h1, dh1,
  * td, dh1_bf16, dh1T_bf16, actions, dY3, dY2, dY1, part1, part2, part3, grad4, then dY1
- * on the padded 21 x 21 grid and dY2 on the padded 11 x 11 grid (-1 below batch 128; the
- * TMA engine's shifted-descriptor conv1 weight gradient / conv2 data gradient). */
+ * on the padded 21 x 21 grid, dY2 on the padded 11 x 11 grid, act1 (online, target) as
+ * 2x2 space-to-depth [n][10][10][128] (-1 below batch 128; the TMA engine's
+ * shifted-descriptor conv kernels, which then leave the dense act1 unwritten). */
 int pq_workspace_layout(int max_batch, int actions, int64_t *offsets);
 
 /* Q-values for n states (nn.forward): q_out f32 [n][actions]. */

@@ -156,7 +156,7 @@ def stream_ptr(stream=None) -> int:
 
 WS_BUFFERS = ("act1", "act2", "act3", "fc1part", "act1_t", "act2_t", "act3_t", "fc1part_t", "q",
               "h1", "dh1", "td", "dh1_bf", "dh1T", "act", "dY3", "dY2", "dY1", "part1", "part2",
-              "part3", "grad4", "dY1p", "dY2p")
+              "part3", "grad4", "dY1p", "dY2p", "act1s2", "act1s2_t")
 
 
 def workspace_layout(max_batch: int, actions: int) -> dict:

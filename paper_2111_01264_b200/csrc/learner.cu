@@ -1497,8 +1497,8 @@ constexpr int C2D_SMEM = 1024 + 16 * C2D_W + C2D_STAGES * C2D_BOX;
 struct C2DArgs {
     CUtensorMap a, w;  // dY2p pixel rows [n*121][64]; W2 view {c1, kw, kh, c2}
     bf16 *out;         // dY1 (dense 20 x 20, or the padded 21 x 21 grid when pad21)
-    const bf16 *mask;  // act1 (dense)
-    int n, pad21;
+    const bf16 *mask;  // act1 (dense), or its 2x2 space-to-depth copy when mask_s2
+    int n, pad21, mask_s2;
 };
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_dgrad_shift(const __grid_constant__ C2DArgs g) {
@@ -1599,7 +1599,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_dgrad_shift(const __g
                     const int iy = 2 * y + (cls >> 1), ix = 2 * x + (cls & 1);
                     const size_t o = ((size_t)(smp * 20 + iy) * 20 + ix) * 32;
                     const size_t oo = g.pad21 ? ((size_t)(smp * 21 + iy) * 21 + ix) * 32 : o;
-                    store_masked32(g.out + oo, g.mask + o, v, 32);
+                    // act1 pixel (iy, ix) = s2d pixel (y, x), channels (py * 2 + px) * 32
+                    const size_t om = g.mask_s2 ? ((size_t)(smp * 10 + y) * 10 + x) * 128 + cls * 32 : o;
+                    store_masked32(g.out + oo, g.mask + om, v, 32);
                 }
             }
             tc_fence_before();
@@ -1614,14 +1616,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_dgrad_shift(const __g
 }
 
 int tma_conv2_dgrad_shift(const pq_net &th, const bf16 *dY2p, const bf16 *act1, bf16 *dY1, int n, int pad21,
-                          cudaStream_t st) {
+                          cudaStream_t st, int mask_s2) {
     static C2DArgs g;
     memset(&g, 0, sizeof(g));
     const uint64_t ad[2] = {64, (uint64_t)n * 121}, as[1] = {64};
     if (int rc = make_map(&g.a, dY2p, 2, ad, as, "dY2 padded rows", C2D_ROWS)) return rc;
     const uint64_t dims[4] = {32, 4, 4, 64}, strd[3] = {32, 128, 512};
     if (int rc = make_map(&g.w, (const bf16 *)th.shadow + S_W2, 4, dims, strd, "W2 view")) return rc;
-    g.out = dY1, g.mask = act1, g.n = n, g.pad21 = pad21;
+    g.out = dY1, g.mask = act1, g.n = n, g.pad21 = pad21, g.mask_s2 = mask_s2;
     static bool configured = false;
     if (!configured) {
         PQ_CUDA_TRY(cudaFuncSetAttribute(k_conv2_dgrad_shift, cudaFuncAttributeMaxDynamicSharedMemorySize, C2D_SMEM));
@@ -1837,10 +1839,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_co
 #pragma unroll
                 for (int gg = 0; gg < 2; ++gg) {
                     if (gg >= g.groups) break;
-                    if (g.act1s2[gg])
-                        g.ep[gg].apply_dual(m, v[gg], g.act1s2[gg] + o2);
-                    else
+                    if (!g.act1s2[gg]) {
                         g.ep[gg].apply(m, 0, v[gg], 32, 0);
+                    } else if (g.ep[gg].out) {  // both layouts
+                        g.ep[gg].apply_dual(m, v[gg], g.act1s2[gg] + o2);
+                    } else {  // only the space-to-depth copy
+                        EpiBiasRelu e = g.ep[gg];
+                        e.out = g.act1s2[gg] + o2, e.ld = 0;
+                        e.apply(0, 0, v[gg], 32, 0);
+                    }
                 }
             }
         }
@@ -1864,7 +1871,9 @@ int tma_conv1_shift(const pq_net *nets, const bf16 *s2d, int nframes, const int 
         const uint64_t wd[2] = {256, 32}, ws[1] = {256};
         if (int rc = make_map(&g.w[q], (const bf16 *)nets[q].shadow + S_W1P, 2, wd, ws, "W1 permuted", 32))
             return rc;
-        g.ep[q] = EpiBiasRelu{act1[q], nets[q].master + P_B1, n * 400, 32, 32, 1.0f / 255.0f};
+        // with the space-to-depth copy the dense act1 has no reader (conv2 forward / weight
+        // gradient read the copy, conv2's data gradient takes its ReLU mask from it)
+        g.ep[q] = EpiBiasRelu{act1s2 ? nullptr : act1[q], nets[q].master + P_B1, n * 400, 32, 32, 1.0f / 255.0f};
         g.coff[q] = c0[q];
     }
     if (groups > 1 && (c0[1] + 64 > nframes * 16 || c0[0] != 0)) return set_err("conv1 shift: channel window");

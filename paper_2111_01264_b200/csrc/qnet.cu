@@ -47,7 +47,7 @@ int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *d
 int tma_conv2_wgrad_shift(const bf16 *act1s2, const bf16 *dY2q, float *part2, int kc, int splits, int n,
                           cudaStream_t st);
 int tma_conv2_dgrad_shift(const pq_net &th, const bf16 *dY2p, const bf16 *act1, bf16 *dY1, int n, int pad21,
-                          cudaStream_t st);
+                          cudaStream_t st, int mask_s2);
 int tma_conv3_wgrad(const bf16 *act2, const bf16 *dY3, float *part3, int kc, int splits, int n, cudaStream_t st);
 int tma_conv2_dgrad(const pq_net &th, const bf16 *dY2, const bf16 *act1, bf16 *dY1, int n, cudaStream_t st,
                     int pad21);
@@ -848,7 +848,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     }
     if (use_tma(n)) {
         if (shift) {  // dY1 onto the padded grid of the shifted conv1 weight gradient
-            if (int rc = tma_conv2_dgrad_shift(th, w.dY2p, w.act1[0], w.dY1p, n, 1, st)) return rc;
+            if (int rc = tma_conv2_dgrad_shift(th, w.dY2p, w.act1s2[0], w.dY1p, n, 1, st, 1)) return rc;
         } else if (int rc = tma_conv2_dgrad(th, w.dY2, w.act1[0], w.dY1, n, st, 0)) {
             return rc;
         }
@@ -983,8 +983,9 @@ int pq_workspace_layout(int max_batch, int actions, int64_t *offsets) {
     WS w = carve(base, max_batch, actions);
     const void *ptrs[] = {w.act1[0], w.act2[0], w.act3[0], w.fc1part[0], w.act1[1], w.act2[1],
                           w.act3[1], w.fc1part[1], w.q, w.h1, w.dh1, w.td, w.dh1_bf, w.dh1T,
-                          w.act, w.dY3, w.dY2, w.dY1, w.part1, w.part2, w.part3, w.grad4, w.dY1p, w.dY2p};
-    for (int i = 0; i < 24; ++i) offsets[i] = ptrs[i] ? (const char *)ptrs[i] - base : -1;
+                          w.act, w.dY3, w.dY2, w.dY1, w.part1, w.part2, w.part3, w.grad4, w.dY1p, w.dY2p,
+                          w.act1s2[0], w.act1s2[1]};
+    for (int i = 0; i < 26; ++i) offsets[i] = ptrs[i] ? (const char *)ptrs[i] - base : -1;
     return 0;
 }
 

@@ -36,7 +36,8 @@ def test_abi_constants():
     assert lib.pq_num_params(18) == 1_693_362
     assert lib.pq_workspace_bytes(32, 18) > 0
     lay = N.workspace_layout(64, 18)
-    assert lay.pop("dY1p") == -1 and lay.pop("dY2p") == -1   # padded grids exist from batch 128
+    for k in ("dY1p", "dY2p", "act1s2", "act1s2_t"):   # the shifted-conv buffers exist from batch 128
+        assert lay.pop(k) == -1
     offs = list(lay.values())
     assert offs == sorted(offs) and offs[0] == 0
     big = N.workspace_layout(256, 18)

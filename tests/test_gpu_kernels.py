@@ -104,8 +104,14 @@ def test_learner_step_stagewise(B):
     PT, ST = unpack(target)
     s, a, r, s2, term = mem.gather(batch.idx)
 
+    def act1_of(suffix):
+        if B >= 128:   # TMA engine: conv1 writes only act1's 2x2 space-to-depth copy
+            a = view(ws, L["act1s2" + suffix], (B, 10, 10, 2, 2, 32), torch.bfloat16).float()
+            return a.permute(0, 1, 3, 2, 4, 5).reshape(B, 20, 20, 32)
+        return view(ws, L["act1" + suffix], (B, 20, 20, 32), torch.bfloat16).float()
+
     def fwd_stage(x_u8, Pp, Sp, suffix):
-        act1 = view(ws, L["act1" + suffix], (B, 20, 20, 32), torch.bfloat16).float()
+        act1 = act1_of(suffix)
         x = x_u8.float()
         ref1 = F.relu(F.conv2d(x, Sp["W1"].view(32, 4, 8, 8), stride=4) / 255.0 +
                       Pp["b1"].view(1, -1, 1, 1)).permute(0, 2, 3, 1)
