@@ -83,7 +83,7 @@ def unpack(net):
     return P, S
 
 
-@pytest.mark.parametrize("B", [32, 8, 40, 256, 1024])
+@pytest.mark.parametrize("B", [32, 8, 40, 256, 333, 1024])
 def test_learner_step_stagewise(B):
     rng = np.random.default_rng(B)
     mem = make_memory(rng)
