@@ -393,6 +393,12 @@ def dp_learner(args, rank: int, world: int, dist, steps: int = 30):
 def run_b200(args, rank: int, world: int, local_rank: int):
     import torch
 
+    # PQ_BENCH_SHARE_GPU=1 (multi-rank smoke test on a one-GPU box only): ranks share the
+    # visible devices and the collectives go over gloo; the driver's runs use one GPU per
+    # rank and NCCL
+    share = os.environ.get("PQ_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     from paper_2111_01264_b200.agent import EpsilonSchedule, HyperParams
     from paper_2111_01264_b200.executor import ROLE_BENCH, DeviceRun, derived_seed
@@ -402,7 +408,10 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     seed = derived_seed(args.seed, ROLE_BENCH, rank) % (2**31)
     total_epochs = args.warmup + args.steps
     hp = HyperParams(C=args.C, F=args.F, N=args.prefill, W=args.W, batch_size=args.B,
