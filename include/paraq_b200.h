@@ -150,6 +150,15 @@ typedef struct pq_learn_args {
 /* One learner step (agent.train_minibatch): target forward + max, online forward,
  * TD error, backward, centered RMSProp on the summed gradient. */
 int pq_learn_step(const pq_learn_args *args, void *stream);
+/* The same step with the target network's forward pipelined: step k's backward launches
+ * also run the target conv1..conv3 of the minibatch at *update_counter + 1 and the next
+ * step's conv1 launch its fc1 (theta-minus is fixed within an epoch).  Requires the
+ * epoch-table mode (idx_base + update_counter, one spare table row), no external targets
+ * and the small-batch fused schedule; otherwise identical to pq_learn_step.  Results are
+ * bit-identical to pq_learn_step.  pq_learn_target_prologue computes the target
+ * conv1..conv3 of the step at *update_counter (call it at the start of every epoch). */
+int pq_learn_step_pipelined(const pq_learn_args *args, void *stream);
+int pq_learn_target_prologue(const pq_learn_args *args, void *stream);
 
 /* Data-parallel learner (configs[4]): the summed gradient of this
  * rank's shard of the batch (same forward / TD / backward as pq_learn_step, no update)

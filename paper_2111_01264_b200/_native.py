@@ -81,6 +81,8 @@ EXPORTS = {
     "pq_forward": ([PqNet, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, vp],
                    C.c_int),
     "pq_learn_step": ([C.POINTER(PqLearnArgs), vp], C.c_int),
+    "pq_learn_step_pipelined": ([C.POINTER(PqLearnArgs), vp], C.c_int),
+    "pq_learn_target_prologue": ([C.POINTER(PqLearnArgs), vp], C.c_int),
     "pq_act_step": ([C.POINTER(PqActArgs), vp], C.c_int),
     "pq_learn_grad": ([C.POINTER(PqLearnArgs), vp, vp], C.c_int),
     "pq_rmsprop_apply": ([PqNet, PqOpt, vp, C.c_int, C.c_float, C.c_float, C.c_float, vp, C.c_int, vp],

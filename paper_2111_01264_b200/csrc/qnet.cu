@@ -748,7 +748,58 @@ static bool fused_backward(int n, const pq_learn_args *la, float *grad_only) {
     return on == 1 && !use_tma(n) && !grad_only && n < FC_PART_MIN_BATCH;
 }
 
-static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStream_t st) {
+// ---- the target network's forward of the NEXT step, pipelined into this step's launches
+// (executor epochs, batch 32-class: pq_learn_step_pipelined).  theta-minus is fixed within
+// an epoch and the head has already advanced the step counter to the next minibatch, so
+// conv1 / conv2 / conv3 of the target network for step k+1 ride as extra CTAs in step k's
+// {conv2 dgrad | conv2 wgrad}, {conv1 wgrad | update} and conv1-update launches, and its
+// fc1 in step k+1's conv1 launch.  Each stage reads what the launch before it wrote; the
+// same GEMM configurations as the one-shot forward, so the results are bit-identical.
+// pq_learn_target_prologue primes conv1..conv3 for the first step of an epoch.
+using F1Op = GemmOp<32, false, false, 3, 1, LoadFrames, LoadDense, EpiBiasRelu>;
+using F23Op = GemmOp<64, false, false, 0, 2, LoadIm2col, LoadDense, EpiBiasRelu>;
+using F4Op = GemmOp<32, false, false, 0, 1, LoadDense, LoadDense, EpiF32T>;
+static F1Op::Args args_f1(const pq_net &net, const FwdInput &in, int n, bf16 *act1) {
+    F1Op::Args g{};
+    g.a[0] = frames_loader(in, n);
+    g.b[0] = LoadDense{(const bf16 *)net.shadow + S_W1P, 32, 256, 256};  // permuted K
+    g.e[0] = EpiBiasRelu{act1, net.master + P_B1, n * 400, 32, 32, 1.0f / 255.0f};
+    g.M = n * 400, g.N = 32, g.K = 256, g.kc_per_split = 4, g.splits = 1, g.ones_at = -1;
+    return g;
+}
+static F23Op::Args args_f2(const pq_net &net, const bf16 *act1, int n, bf16 *act2) {
+    F23Op::Args g{};
+    g.a[0] = im2col(act1, n, 20, 20, 32, 4, 2, 9, 9);
+    g.b[0] = LoadDense{(const bf16 *)net.shadow + S_W2, 64, 512, 512};
+    g.e[0] = EpiBiasRelu{act2, net.master + P_B2, n * 81, 64, 64, 1.0f};
+    g.M = n * 81, g.N = 64, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
+    return g;
+}
+static F23Op::Args args_f3(const pq_net &net, const bf16 *act2, int n, bf16 *act3) {
+    F23Op::Args g{};
+    g.a[0] = im2col(act2, n, 9, 9, 64, 3, 1, 7, 7);
+    g.b[0] = LoadDense{(const bf16 *)net.shadow + S_W3, 64, 576, 576};
+    g.e[0] = EpiBiasRelu{act3, net.master + P_B3, n * 49, 64, 64, 1.0f};
+    g.M = n * 49, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
+    return g;
+}
+static F4Op::Args args_f4(const pq_net &net, const bf16 *act3, int n, float *part) {
+    F4Op::Args g{};
+    g.a[0] = LoadDense{(const bf16 *)net.shadow + S_W4, 512, 3136, 3136};
+    g.b[0] = LoadDense{act3, n, 3136, 3136};
+    g.e[0] = EpiF32T{part, 512, n, 512, (size_t)n * 512};
+    g.M = 512, g.N = n, g.K = 3136, g.kc_per_split = 49 / FC1_SPLITS, g.splits = FC1_SPLITS, g.ones_at = -1;
+    return g;
+}
+static FwdInput target_input(const pq_learn_args *la) {  // next-state frames f1..f4 at *counter
+    return FwdInput{la->ring, la->records, la->idx_base, la->update_counter, la->n, REC_INTS, 1};
+}
+static bool pipeline_ok(const pq_learn_args *la) {
+    return !la->idx && la->idx_base && la->update_counter && !la->ext_targets && choose_bn(la->n) == 32 &&
+           fused_backward(la->n, la, nullptr);
+}
+
+static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStream_t st, bool pipe = false) {
     const pq_net &th = la->theta;
     const bf16 *sh = (const bf16 *)th.shadow;
     int s1 = 1, s2 = 1, s3 = 1;
@@ -761,7 +812,15 @@ static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStrea
         f.n0 = B3dOp::ctas(f.p0, 1), f.n1 = B3wOp::ctas(f.p1, 1);
         PQ_CHECK(launch_fused(f, B4wOp::ctas(f.p2, 1), st), "conv3 dgrad | conv3 wgrad | fc1 wgrad+rmsprop");
     }
-    {
+    const pq_net &tg = la->target;
+    if (pipe) {  // + the target conv1 of the next step
+        FusedArgs<B2dOp, B2wOp, F1Op> f{};
+        f.p0 = B2dOp::make(args_b2d(sh, w, n));
+        f.p1 = B2wOp::make(args_b2w(w, n, &s2));
+        f.p2 = F1Op::make(args_f1(tg, target_input(la), n, w.act1[1]));
+        f.n0 = B2dOp::ctas(f.p0, 1), f.n1 = B2wOp::ctas(f.p1, 1);
+        PQ_CHECK(launch_fused(f, F1Op::ctas(f.p2, 1), st), "conv2 dgrad | conv2 wgrad | target conv1");
+    } else {
         FusedArgs<B2dOp, B2wOp, NoOp> f{};
         f.p0 = B2dOp::make(args_b2d(sh, w, n));
         f.p1 = B2wOp::make(args_b2w(w, n, &s2));
@@ -771,18 +830,32 @@ static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStrea
     OptArgs o = opt_args(la, n, w);
     o.s1 = s1, o.s2 = s2, o.s3 = s3;
     {
-        FusedArgs<B1wOp, OptOp, NoOp> f{};
-        f.p0 = B1wOp::make(args_b1w(la, w, n, &s1));
+        B1wOp::Launch b1 = B1wOp::make(args_b1w(la, w, n, &s1));
         o.s1 = s1;
         OptArgs os = o;
         os.lo1 = P_W2, os.hi1 = P_W4, os.lo2 = P_B4, os.hi2 = os.total;
-        f.p1 = os;
-        f.n0 = B1wOp::ctas(f.p0, 1), f.n1 = OptOp::ctas(os);
-        PQ_CHECK(launch_fused(f, 0, st), "conv1 wgrad | update conv2, conv3, fc");
+        if (pipe) {  // + the target conv2 of the next step
+            FusedArgs<B1wOp, OptOp, F23Op> f{};
+            f.p0 = b1, f.p1 = os, f.p2 = F23Op::make(args_f2(tg, w.act1[1], n, w.act2[1]));
+            f.n0 = B1wOp::ctas(f.p0, 1), f.n1 = OptOp::ctas(os);
+            PQ_CHECK(launch_fused(f, F23Op::ctas(f.p2, 1), st), "conv1 wgrad | update | target conv2");
+        } else {
+            FusedArgs<B1wOp, OptOp, NoOp> f{};
+            f.p0 = b1, f.p1 = os;
+            f.n0 = B1wOp::ctas(f.p0, 1), f.n1 = OptOp::ctas(os);
+            PQ_CHECK(launch_fused(f, 0, st), "conv1 wgrad | update conv2, conv3, fc");
+        }
     }
     o.lo1 = P_W1, o.hi1 = P_W2, o.lo2 = P_W2, o.hi2 = P_W2;
-    PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((P_W2 - P_W1 + 255) / 256)), dim3(256), 0, st, o),
-             "optimizer (conv1)");
+    if (pipe) {  // conv1's update + the target conv3 of the next step
+        FusedArgs<OptOp, F23Op, NoOp> f{};
+        f.p0 = o, f.p1 = F23Op::make(args_f3(tg, w.act2[1], n, w.act3[1]));
+        f.n0 = OptOp::ctas(o), f.n1 = F23Op::ctas(f.p1, 1);
+        PQ_CHECK(launch_fused(f, 0, st), "update conv1 | target conv3");
+    } else {
+        PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((P_W2 - P_W1 + 255) / 256)), dim3(256), 0, st, o),
+                 "optimizer (conv1)");
+    }
     return 0;
 }
 
@@ -1046,6 +1119,52 @@ int pq_learn_step(const pq_learn_args *la, void *stream) {
     rc = head(nets, groups, n, la->actions, w, 1, la, st, split_optimizer() || fused_backward(n, la, nullptr));
     if (rc) return rc;
     return backward_and_update(la, n, w, st);
+}
+
+// One learner step with the target forward pipelined (see backward_fused): the online
+// conv1 launch also runs the target fc1 of this step (its conv3 output came from the
+// previous step or the prologue); then online conv2..fc1, the head, the backward.
+int pq_learn_step_pipelined(const pq_learn_args *la, void *stream) {
+    const int n = la->n;
+    if (n < 1 || n > la->max_batch) return set_err("batch size out of range for the workspace");
+    if (la->actions < 1 || la->actions > MAX_ACTIONS) return set_err("actions must be in [1, 32]");
+    if (!pipeline_ok(la)) return pq_learn_step(la, stream);
+    cudaStream_t st = (cudaStream_t)stream;
+    WS w = carve(la->ws, la->max_batch, la->actions);
+    const pq_net nets[2] = {la->theta, la->target};
+    const FwdInput in{la->ring, la->records, la->idx_base, la->update_counter, n, REC_INTS, 0};
+    {
+        FusedArgs<F1Op, F4Op, NoOp> f{};
+        f.p0 = F1Op::make(args_f1(la->theta, in, n, w.act1[0]));
+        f.p1 = F4Op::make(args_f4(la->target, w.act3[1], n, w.fc1part[1]));
+        f.n0 = F1Op::ctas(f.p0, 1), f.n1 = F4Op::ctas(f.p1, 1);
+        PQ_CHECK(launch_fused(f, 0, st), "conv1 | target fc1");
+    }
+    PQ_CHECK((launch_gemm<64, false, false, 0, 2>(args_f2(la->theta, w.act1[0], n, w.act2[0]), 1, st)),
+             "conv2 forward");
+    PQ_CHECK((launch_gemm<64, false, false, 0, 2>(args_f3(la->theta, w.act2[0], n, w.act3[0]), 1, st)),
+             "conv3 forward");
+    PQ_CHECK((launch_gemm<32, false, false, 0, 1>(args_f4(la->theta, w.act3[0], n, w.fc1part[0]), 1, st)),
+             "fc1 forward");
+    if (int rc = head(nets, 2, n, la->actions, w, 1, la, st, true)) return rc;
+    return backward_fused(la, n, w, st, true);
+}
+
+// Target conv1..conv3 of the minibatch at *update_counter (the first step of an epoch,
+// after theta-minus and the index table changed): primes pq_learn_step_pipelined.
+int pq_learn_target_prologue(const pq_learn_args *la, void *stream) {
+    if (!pipeline_ok(la)) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int n = la->n;
+    WS w = carve(la->ws, la->max_batch, la->actions);
+    const pq_net &tg = la->target;
+    PQ_CHECK((launch_gemm<32, false, false, 3, 1>(args_f1(tg, target_input(la), n, w.act1[1]), 1, st)),
+             "target conv1 (prologue)");
+    PQ_CHECK((launch_gemm<64, false, false, 0, 2>(args_f2(tg, w.act1[1], n, w.act2[1]), 1, st)),
+             "target conv2 (prologue)");
+    PQ_CHECK((launch_gemm<64, false, false, 0, 2>(args_f3(tg, w.act2[1], n, w.act3[1]), 1, st)),
+             "target conv3 (prologue)");
+    return 0;
 }
 
 int pq_learn_grad(const pq_learn_args *la, float *grad, void *stream) {

@@ -201,7 +201,12 @@ class DeviceRun:
         self.trainer_pcg = device_pcg(rng_stream(hp.seed, ROLE_TRAINER))
         self.staging = torch.full((W, self.steps, REC_INTS), -1, dtype=torch.int32, device="cuda")
         self.staged = False
-        self.idx_table = torch.empty(self.updates * B, dtype=torch.int64, device="cuda")
+        # one spare row: the pipelined target forward of the epoch's last step reads the
+        # (unused) minibatch after it
+        self.idx_table = torch.zeros((self.updates + 1) * B, dtype=torch.int64, device="cuda")
+        # PQ_PIPE_TARGET=1: pipelined target forward (bit-identical; measured slower at
+        # batch 32, 80 vs 71 us/update: see DESIGN.md section 4)
+        self.pipelined = os.environ.get("PQ_PIPE_TARGET", "0") == "1" and not persistent
         self.update_counter = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.step_counter = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.nonfinite = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
@@ -256,7 +261,14 @@ class DeviceRun:
 
     def learn_step(self, stream=None):
         a = self._learn_args()
-        N.check(N.load().pq_learn_step(N.C.byref(a), N.stream_ptr(stream)), "learn_step")
+        fn = N.load().pq_learn_step_pipelined if self.pipelined else N.load().pq_learn_step
+        N.check(fn(N.C.byref(a), N.stream_ptr(stream)), "learn_step")
+
+    def target_prologue(self, stream=None):
+        """Target conv1..conv3 of the minibatch at the step counter (pipelined learner)."""
+        if self.pipelined:
+            a = self._learn_args()
+            N.check(N.load().pq_learn_target_prologue(N.C.byref(a), N.stream_ptr(stream)), "target prologue")
 
     def learn_run(self, n_updates: int, stream=None):
         """n_updates learner steps in one persistent launch (same counters and tables)."""
@@ -314,6 +326,7 @@ class DeviceRun:
         torch.cuda.synchronize()
         for t, v in zip(keep, saved):
             t.copy_(v)
+        self.target_prologue()  # the warm-up step advanced the target pipeline
         return graphs
 
     # -- epoch pieces -------------------------------------------------------------------
@@ -352,12 +365,13 @@ class DeviceRun:
         torch = self.torch
         self.epoch_start = epoch * hp.C
         sample_indices_device(self.trainer_pcg, len(self.D), self.updates * hp.batch_size,
-                              out=self.idx_table)
+                              out=self.idx_table[: self.updates * hp.batch_size])
         base = self.D._reserve_frames(2 * hp.C)
         self.epoch_bases.append(base)
         per = 2 * self.steps
         self.envs.slot_next.copy_(torch.arange(hp.W, device="cuda", dtype=torch.int64) * per + base)
         self.update_counter.zero_()
+        self.target_prologue()  # theta-minus and the index table are this epoch's
 
     def run_epoch(self, epoch: int):
         hp = self.hp

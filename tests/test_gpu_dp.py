@@ -111,6 +111,7 @@ def test_persistent_learner_matches_graph_learner():
     for steps in (1, 3):
         for t, v in zip(keep, saved):
             t.copy_(v)
+        r.target_prologue()   # the step counter was reset: re-prime the pipelined target forward
         for _ in range(steps):
             r.learn_step()
         one_shot = [t.clone() for t in keep]

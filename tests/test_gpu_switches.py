@@ -81,3 +81,21 @@ def test_fused_backward_matches_multistream(tmp_path):
     multi = run_probe(tmp_path, "multi_bw", {"PQ_FUSED": "0"})
     assert np.array_equal(fused["q"], multi["q"])
     assert np.array_equal(fused["theta"], multi["theta"])
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_pipelined_target_forward_is_bit_identical(graphs, monkeypatch):
+    """PQ_PIPE_TARGET=1 (executor switch): the target network's forward of step k+1 runs
+    inside step k's backward launches; epoch after epoch the parameters must match the
+    unpipelined learner bit for bit (theta hash per epoch and at the end)."""
+    from paper_2111_01264_b200.agent import EpsilonSchedule, HyperParams
+    from paper_2111_01264_b200.executor import run
+
+    hp = HyperParams(C=400, F=4, N=2000, W=8, batch_size=32, total_steps=1200, capacity=5000, seed=3,
+                     schedule=EpsilonSchedule(1.0, 0.1, 600))
+    recs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PQ_PIPE_TARGET", flag)
+        recs.append(run(hp, use_graphs=graphs, graph_chunk=25))
+    assert recs[0].epoch_hashes == recs[1].epoch_hashes
+    assert recs[0].final_hash == recs[1].final_hash
