@@ -1387,7 +1387,7 @@ static bf16 *ones_tile(cudaStream_t st) {
 
 // conv3 forward, groups online / target: act3[g] = relu(im2col(act2[g]) W3[g]^T + b3[g])
 int tma_conv3_fwd(const pq_net *nets, bf16 *const *act2, bf16 *const *act3, int groups, int n, cudaStream_t st) {
-    static TmaGemm<EpiBiasRelu> g;
+    static thread_local TmaGemm<EpiBiasRelu> g;  // per host thread (launch arguments are copied at launch)
     memset(&g, 0, sizeof(g));
     for (int q = 0; q < groups; ++q) {
         if (int rc = map_im2col(&g.a[q], act2[q], n, 9, 9, 0, -2, 128, "act2")) return rc;
@@ -1402,7 +1402,7 @@ int tma_conv3_fwd(const pq_net *nets, bf16 *const *act2, bf16 *const *act3, int 
 // fc1 forward, swapped: part[g][s][b][j] = sum over split s of W4[g][j] . act3[g][b]
 int tma_fc1_fwd(const pq_net *nets, bf16 *const *act3, float *const *part, int splits, int groups, int n,
                 cudaStream_t st) {
-    static TmaGemm<EpiF32T> g;
+    static thread_local TmaGemm<EpiF32T> g;
     memset(&g, 0, sizeof(g));
     for (int q = 0; q < groups; ++q) {
         if (int rc = map2(&g.a[q], (const bf16 *)nets[q].shadow + S_W4, 512, 3136, 3136, "W4")) return rc;
@@ -1417,7 +1417,7 @@ int tma_fc1_fwd(const pq_net *nets, bf16 *const *act3, float *const *part, int s
 
 // fc1 data gradient: dY3[b][k] = relu'(act3) * sum_j dh1[b][j] W4[j][k] (W4 as MN-major B)
 int tma_fc1_dgrad(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *dY3, int n, cudaStream_t st) {
-    static TmaGemm<EpiMask> g;
+    static thread_local TmaGemm<EpiMask> g;
     memset(&g, 0, sizeof(g));
     if (int rc = map2(&g.a[0], dh1_bf, n, 512, 512, "dh1")) return rc;
     if (int rc = map2(&g.b[0], (const bf16 *)th.shadow + S_W4, 512, 3136, 3136, "W4")) return rc;
@@ -1431,7 +1431,7 @@ int tma_fc1_dgrad(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *
 int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st,
                     bf16 *dY2p, bf16 *dY2q) {
     if (dY2p) {  // also onto the padded 11 x 11 grid of the shifted conv2 data gradient
-        static TmaGemm<EpiMaskPad> g;
+        static thread_local TmaGemm<EpiMaskPad> g;
         memset(&g, 0, sizeof(g));
         if (int rc = map_im2col(&g.a[0], dY3, n, 7, 7, -2, 0, 128, "dY3")) return rc;
         const uint64_t dims[3] = {64, 9, 64}, strd[2] = {64, 576};
@@ -1441,7 +1441,7 @@ int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *d
         g.mtiles = (n * 81 + 127) / 128, g.ntiles = 1, g.splits = 1, g.groups = 1, g.kc = 9, g.nk = 9;
         return launch_tma<64, false, true>(g, st, "conv3 dgrad (TMA, padded copy)");
     }
-    static TmaGemm<EpiMask> g;
+    static thread_local TmaGemm<EpiMask> g;
     memset(&g, 0, sizeof(g));
     if (int rc = map_im2col(&g.a[0], dY3, n, 7, 7, -2, 0, 128, "dY3")) return rc;
     const uint64_t dims[3] = {64, 9, 64}, strd[2] = {64, 576};
@@ -1455,7 +1455,7 @@ int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *d
 // conv3 weight gradient: part3[s][o][k] = sum over split s of im2col(act2)[m][k] dY3[m][o];
 // k = 576 is the bias row (ones tile)
 int tma_conv3_wgrad(const bf16 *act2, const bf16 *dY3, float *part3, int kc, int splits, int n, cudaStream_t st) {
-    static TmaGemm<EpiF32T> g;
+    static thread_local TmaGemm<EpiF32T> g;
     memset(&g, 0, sizeof(g));
     bf16 *ones = ones_tile(st);
     if (!ones) return set_err("ones tile allocation failed");
@@ -1471,7 +1471,7 @@ int tma_conv3_wgrad(const bf16 *act2, const bf16 *dY3, float *part3, int kc, int
 // conv2 data gradient per input-parity class: dY1 = relu'(act1) * transposed conv2(dY2)
 int tma_conv2_dgrad(const pq_net &th, const bf16 *dY2, const bf16 *act1, bf16 *dY1, int n, cudaStream_t st,
                     int pad21) {
-    static TmaGemm<EpiMaskP> g;
+    static thread_local TmaGemm<EpiMaskP> g;
     memset(&g, 0, sizeof(g));
     const int tpc = (n * 100 + 127) / 128;
     if (int rc = map_im2col(&g.a[0], dY2, n, 9, 9, -1, 0, 128, "dY2")) return rc;
@@ -1617,7 +1617,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_dgrad_shift(const __g
 
 int tma_conv2_dgrad_shift(const pq_net &th, const bf16 *dY2p, const bf16 *act1, bf16 *dY1, int n, int pad21,
                           cudaStream_t st, int mask_s2) {
-    static C2DArgs g;
+    static thread_local C2DArgs g;
     memset(&g, 0, sizeof(g));
     const uint64_t ad[2] = {64, (uint64_t)n * 121}, as[1] = {64};
     if (int rc = make_map(&g.a, dY2p, 2, ad, as, "dY2 padded rows", C2D_ROWS)) return rc;
@@ -1691,7 +1691,7 @@ int tma_frames_s2d(const uint8_t *ring, const int32_t *refs, const int64_t *map,
 // conv1 forward on the TMA engine: act1[g] = relu(im2col(s2d, channels 16 c0g..) W1p[g]^T / 255 + b1)
 int tma_conv1_fwd(const pq_net *nets, const bf16 *s2d, int nframes, const int *c0, bf16 *const *act1, int groups,
                   int n, cudaStream_t st) {
-    static TmaGemm<EpiBiasRelu> g;
+    static thread_local TmaGemm<EpiBiasRelu> g;
     memset(&g, 0, sizeof(g));
     for (int q = 0; q < groups; ++q) {
         if (int rc = map_im2col(&g.a[q], s2d, n, 21, 21, 0, -1, 128, "frames s2d", nframes * 16)) return rc;
@@ -1862,7 +1862,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_co
 // channel offsets c0[g] of the s2d stacks (16 * nframes channels per pixel)
 int tma_conv1_shift(const pq_net *nets, const bf16 *s2d, int nframes, const int *c0, bf16 *const *act1,
                     int groups, int n, int a_early, int w_early, cudaStream_t st, bf16 *const *act1s2) {
-    static C1Args g;
+    static thread_local C1Args g;
     memset(&g, 0, sizeof(g));
     for (int q = 0; q < groups && act1s2; ++q) g.act1s2[q] = act1s2[q];
     const uint64_t ad[2] = {(uint64_t)nframes * 16, (uint64_t)n * 441}, as[1] = {(uint64_t)nframes * 16};
@@ -2033,7 +2033,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv_shift(const __grid_con
 template <int CV>
 static int launch_conv_shift(const pq_net *nets, bf16 *const *in, bf16 *const *out, int groups, int n, cudaStream_t st) {
     using C = ConvShift<CV>;
-    static CSArgs g;
+    static thread_local CSArgs g;
     memset(&g, 0, sizeof(g));
     const int64_t wofs = CV == 2 ? S_W2 : S_W3, bofs = CV == 2 ? P_B2 : P_B3;
     for (int q = 0; q < groups; ++q) {
@@ -2190,7 +2190,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_wgrad_shift(const __g
 
 int tma_conv2_wgrad_shift(const bf16 *act1s2, const bf16 *dY2q, float *part2, int kc, int splits, int n,
                           cudaStream_t st) {
-    static W2SArgs g;
+    static thread_local W2SArgs g;
     memset(&g, 0, sizeof(g));
     const uint64_t ad[2] = {128, (uint64_t)n * 100}, as[1] = {128};
     if (int rc = make_map(&g.a, act1s2, 2, ad, as, "act1 s2d rows (wgrad)", W2S_ROWS)) return rc;
@@ -2331,7 +2331,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __g
 
 int tma_conv1_wgrad_shift(const bf16 *s2d, int nframes, const bf16 *dY1p, float *part1, int kc, int splits,
                           int n, cudaStream_t st) {
-    static W1SArgs g;
+    static thread_local W1SArgs g;
     memset(&g, 0, sizeof(g));
     const uint64_t ad[2] = {(uint64_t)nframes * 16, (uint64_t)n * 441}, as[1] = {(uint64_t)nframes * 16};
     if (int rc = make_map(&g.a, s2d, 2, ad, as, "s2d pixel rows (wgrad)", W1S_ROWS)) return rc;
@@ -2354,7 +2354,7 @@ int tma_conv1_wgrad_shift(const bf16 *s2d, int nframes, const bf16 *dY1p, float 
 // (k' = 256: bias row from the ones tile)
 int tma_conv1_wgrad(const bf16 *s2d, int nframes, const bf16 *dY1, float *part1, int kc, int splits, int n,
                     cudaStream_t st) {
-    static TmaGemm<EpiF32T> g;
+    static thread_local TmaGemm<EpiF32T> g;
     memset(&g, 0, sizeof(g));
     bf16 *ones = ones_tile(st);
     if (!ones) return set_err("ones tile allocation failed");
