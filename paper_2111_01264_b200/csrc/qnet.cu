@@ -41,6 +41,8 @@ int cuda_err(cudaError_t e, const char *where) {
 int tma_conv3_fwd(const pq_net *nets, bf16 *const *act2, bf16 *const *act3, int groups, int n, cudaStream_t st);
 int tma_fc1_fwd(const pq_net *nets, bf16 *const *act3, float *const *part, int splits, int groups, int n,
                 cudaStream_t st);
+int tma_fc1_fwd_resident(const pq_net *nets, bf16 *const *act3, float *const *part, int splits, int groups, int n,
+                         cudaStream_t st);
 int tma_fc1_dgrad(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *dY3, int n, cudaStream_t st);
 int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st,
                     bf16 *dY2p, bf16 *dY2q);
@@ -367,6 +369,8 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
         g.M = n * 49, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
         PQ_CHECK((launch_gemm<64, false, false, 0, 2>(g, groups, st)), "conv3 forward");
     }
+    if (use_tma(n) && conv1_shift())  // W4 chunks resident per CTA
+        return tma_fc1_fwd_resident(nets, a3, pt, FC1_SPLITS, groups, n, st);
     if (use_tma(n)) return tma_fc1_fwd(nets, a3, pt, FC1_SPLITS, groups, n, st);
     {  // F4: fc1, swapped (D[j][b] = W4[j] . x[b]) with split-K partials [s][b][j]
         GemmArgs<LoadDense, LoadDense, EpiF32T> g{};
