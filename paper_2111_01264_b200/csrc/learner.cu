@@ -1415,41 +1415,45 @@ int tma_fc1_fwd(const pq_net *nets, bf16 *const *act3, float *const *part, int s
     return launch_tma<64, false, false>(g, st, "fc1 forward (TMA)");
 }
 
-// ---- fc1 forward with the weight operand resident (large batches)
-// part[g][s][b][j] = sum over split s of W4[g][j] . act3[g][b], as tma_fc1_fwd, but one CTA
-// per (group, 128-row hidden tile, K split, batch range) keeps its 7 W4 chunks (112 KB) in
-// shared memory and streams only the activation tiles of its batch range: W4 is read once
-// per CTA instead of once per 64-sample tile (5x less L2 -> SM traffic at batch 1024).  Per
-// output tile the same K chunks in the same order as tma_fc1_fwd: bit-identical partials.
-constexpr int F4R_KC = 7, F4R_STAGES = 4;
-constexpr int F4R_SMEM = 1024 + F4R_KC * 2 * PL_BOX + F4R_STAGES * PL_BOX;
-struct F4RArgs {
-    CUtensorMap a[2], b[2];  // W4 [512][3136]; act3 [n][3136]
-    EpiF32T ep[2];
-    int n, groups, splits, nparts;
+// ---- fc1 GEMMs with the A operand resident (large batches)
+// One CTA per (group, 128-row M tile, K split, N range) keeps all its A chunks in shared
+// memory and streams only the B tiles of its N range, so A is read once per CTA instead of
+// once per 64-wide N tile.  Per output tile the same K chunks in the same order as the
+// k_tma_gemm version, so results are bit-identical.
+//  * fc1 forward (swapped): A = W4 [512][3136] (7 chunks per split, 112 KB, requested
+//    before the dependency wait), B = act3 (K-major), EpiF32T split partials;
+//  * fc1 data gradient: A = dh1 [n][512] (8 chunks, 128 KB; written by the head, so after
+//    the wait), B = W4 as MN-major [512][3136], EpiMask (relu' of act3).
+constexpr int RA_MAXKC = 8, RA_STAGES = 4;
+constexpr int RA_SMEM = 1024 + RA_MAXKC * 2 * PL_BOX + RA_STAGES * PL_BOX;
+template <class EP>
+struct RAArgs {
+    CUtensorMap a[2], b[2];
+    EP ep[2];
+    int groups, mtiles, ntiles, splits, nparts, nk, kc, a_early;
 };
 
-__global__ void __launch_bounds__(GEMM_THREADS, 1) k_fc1_fwd_resident(const __grid_constant__ F4RArgs g) {
-    constexpr uint32_t IDESC = idesc_bf16(64, false, false);
+template <class EP, bool BMN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_resident_a(const __grid_constant__ RAArgs<EP> g) {
+    constexpr uint32_t IDESC = idesc_bf16(64, false, BMN);
     extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t full[F4R_STAGES], empty[F4R_STAGES], accf[2], acce[2], abar;
+    __shared__ uint64_t full[RA_STAGES], empty[RA_STAGES], accf[2], acce[2], abar;
     __shared__ uint32_t tmem_base_s;
     TlProbe tp;
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t a_s = smem_u32(smem), ring_s = a_s + F4R_KC * 2 * PL_BOX;
+    const uint32_t a_s = smem_u32(smem), ring_s = a_s + RA_MAXKC * 2 * PL_BOX;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // CTA -> (group, hidden tile, split, batch range)
-    int t = blockIdx.x;
+    int t = blockIdx.x;  // -> (group, M tile, split, N range)
     const int part = t % g.nparts;
     t /= g.nparts;
     const int split = t % g.splits;
     t /= g.splits;
-    const int mt = t % 4, grp = t / 4;
-    const int ntiles = (g.n + 63) / 64, per = (ntiles + g.nparts - 1) / g.nparts;
-    const int nt0 = part * per, nt1 = min(ntiles, nt0 + per);
-    const int kb0 = split * F4R_KC, kb1 = min(49, kb0 + F4R_KC), nk = kb1 - kb0;
+    const int mt = t % g.mtiles, grp = t / g.mtiles;
+    const int per = (g.ntiles + g.nparts - 1) / g.nparts;
+    const int nt0 = part * per, nt1 = min(g.ntiles, nt0 + per);
+    const int kb0 = split * g.kc, kb1 = min(g.nk, kb0 + g.kc), nk = kb1 - kb0;
     if (tid == 0) {
-        for (int s = 0; s < F4R_STAGES; ++s) {
+        for (int s = 0; s < RA_STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -1469,24 +1473,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_fc1_fwd_resident(const __gr
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
-    if (tid == 0 && nk > 0) {  // W4 (updated two or more launches back) before the dependency wait
+    auto load_a = [&] {
         mbar_expect_tx(&abar, (uint32_t)(nk * 2 * PL_BOX));
         for (int c = 0; c < nk; ++c)
             for (int h = 0; h < 2; ++h)
                 tma_load_2d(a_s + (c * 2 + h) * PL_BOX, &g.a[grp], &abar, (kb0 + c) * 64, mt * 128 + h * 64);
-    }
+    };
+    if (tid == 0 && nk > 0 && g.a_early) load_a();
     griddep_wait();
     griddep_launch();
     tp.waited();
     if (warp == 0) {
-        if (lane == 0) {  // producer: activation tile (n-tile, chunk) per ring slot
+        if (lane == 0 && nk > 0) {  // producer: A once (unless early), then B tile (n-tile, chunk) per slot
+            if (!g.a_early) load_a();
             uint32_t q = 0;
             for (int nt = nt0; nt < nt1; ++nt)
                 for (int c = 0; c < nk; ++c, ++q) {
-                    const uint32_t s = q % F4R_STAGES;
-                    if (q >= F4R_STAGES) mbar_wait(&empty[s], ((q / F4R_STAGES) - 1) & 1);
+                    const uint32_t s = q % RA_STAGES;
+                    if (q >= RA_STAGES) mbar_wait(&empty[s], ((q / RA_STAGES) - 1) & 1);
                     mbar_expect_tx(&full[s], (uint32_t)PL_BOX);
-                    tma_load_2d(ring_s + s * PL_BOX, &g.b[grp], &full[s], (kb0 + c) * 64, nt * 64);
+                    if (BMN)
+                        tma_load_2d(ring_s + s * PL_BOX, &g.b[grp], &full[s], nt * 64, (kb0 + c) * 64);
+                    else
+                        tma_load_2d(ring_s + s * PL_BOX, &g.b[grp], &full[s], (kb0 + c) * 64, nt * 64);
                 }
         }
     } else if (warp == 1) {
@@ -1498,14 +1507,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_fc1_fwd_resident(const __gr
                 if (it >= 2) mbar_wait(&acce[buf], ((it >> 1) - 1) & 1);
                 tc_fence_after();
                 for (int c = 0; c < nk; ++c, ++q) {
-                    const uint32_t s = q % F4R_STAGES;
-                    mbar_wait(&full[s], (q / F4R_STAGES) & 1);
+                    const uint32_t s = q % RA_STAGES;
+                    mbar_wait(&full[s], (q / RA_STAGES) & 1);
                     tc_fence_after();
                     const uint32_t a_addr = a_s + c * 2 * PL_BOX, b_addr = ring_s + s * PL_BOX;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        umma_bf16(acc, desc_sw128(a_addr + j * 32, 0), desc_sw128(b_addr + j * 32, 0), IDESC,
-                                  (c > 0 || j > 0) ? 1u : 0u);
+                    for (int j = 0; j < 4; ++j) {
+                        const uint64_t bd = BMN ? desc_sw128(b_addr + j * 2048, 8192) : desc_sw128(b_addr + j * 32, 0);
+                        umma_bf16(acc, desc_sw128(a_addr + j * 32, 0), bd, IDESC, (c > 0 || j > 0) ? 1u : 0u);
+                    }
                     umma_commit(&empty[s]);
                 }
                 umma_commit(&accf[buf]);
@@ -1537,31 +1547,48 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_fc1_fwd_resident(const __gr
     tp.done('4');
 }
 
-int tma_fc1_fwd_resident(const pq_net *nets, bf16 *const *act3, float *const *part, int splits, int groups, int n,
-                         cudaStream_t st) {
-    static thread_local F4RArgs g;
-    memset(&g, 0, sizeof(g));
-    if ((49 + splits - 1) / splits != F4R_KC) return set_err("fc1 resident: 7 K chunks per split");
-    for (int q = 0; q < groups; ++q) {
-        if (int rc = map2(&g.a[q], (const bf16 *)nets[q].shadow + S_W4, 512, 3136, 3136, "W4")) return rc;
-        if (int rc = map2(&g.b[q], act3[q], n, 3136, 3136, "act3")) return rc;
-        g.ep[q] = EpiF32T{part[q], 512, n, 512, (size_t)n * 512};
+template <class EP, bool BMN>
+static int launch_resident_a(RAArgs<EP> &g, cudaStream_t st, const char *what) {
+    auto kern = k_resident_a<EP, BMN>;
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        PQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, RA_SMEM));
+        configured = true;
     }
     if (!g_sms) {
         int dev = 0;
         PQ_CUDA_TRY(cudaGetDevice(&dev));
         PQ_CUDA_TRY(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    const int base = groups * 4 * splits, ntiles = (n + 63) / 64;
-    g.n = n, g.groups = groups, g.splits = splits;
-    g.nparts = std::max(1, std::min(ntiles, g_sms / base));  // one wave of CTAs
-    static bool configured = false;
-    if (!configured) {
-        PQ_CUDA_TRY(cudaFuncSetAttribute(k_fc1_fwd_resident, cudaFuncAttributeMaxDynamicSharedMemorySize, F4R_SMEM));
-        configured = true;
+    if (g.kc > RA_MAXKC) return set_err("resident-A GEMM: too many K chunks per split");
+    const int base = g.groups * g.mtiles * g.splits;
+    g.nparts = std::max(1, std::min(g.ntiles, g_sms / base));  // one wave of CTAs
+    return cuda_err(launch_k(kern, dim3(base * g.nparts), dim3(GEMM_THREADS), RA_SMEM, st, g), what);
+}
+
+int tma_fc1_fwd_resident(const pq_net *nets, bf16 *const *act3, float *const *part, int splits, int groups, int n,
+                         cudaStream_t st) {
+    static thread_local RAArgs<EpiF32T> g;
+    memset(&g, 0, sizeof(g));
+    for (int q = 0; q < groups; ++q) {
+        if (int rc = map2(&g.a[q], (const bf16 *)nets[q].shadow + S_W4, 512, 3136, 3136, "W4")) return rc;
+        if (int rc = map2(&g.b[q], act3[q], n, 3136, 3136, "act3")) return rc;
+        g.ep[q] = EpiF32T{part[q], 512, n, 512, (size_t)n * 512};
     }
-    return cuda_err(launch_k(k_fc1_fwd_resident, dim3(base * g.nparts), dim3(GEMM_THREADS), F4R_SMEM, st, g),
-                    "fc1 forward (resident W4)");
+    g.groups = groups, g.mtiles = 4, g.ntiles = (n + 63) / 64, g.splits = splits, g.nk = 49;
+    g.kc = (49 + splits - 1) / splits, g.a_early = 1;  // W4: updated two or more launches back
+    return launch_resident_a<EpiF32T, false>(g, st, "fc1 forward (resident W4)");
+}
+
+int tma_fc1_dgrad_resident(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *dY3, int n,
+                           cudaStream_t st) {
+    static thread_local RAArgs<EpiMask> g;
+    memset(&g, 0, sizeof(g));
+    if (int rc = map2(&g.a[0], dh1_bf, n, 512, 512, "dh1")) return rc;
+    if (int rc = map2(&g.b[0], (const bf16 *)th.shadow + S_W4, 512, 3136, 3136, "W4")) return rc;
+    g.ep[0] = EpiMask{dY3, act3, n, 3136, 3136};
+    g.groups = 1, g.mtiles = (n + 127) / 128, g.ntiles = 49, g.splits = 1, g.nk = 8, g.kc = 8, g.a_early = 0;
+    return launch_resident_a<EpiMask, true>(g, st, "fc1 dgrad (resident dh1)");
 }
 
 // fc1 data gradient: dY3[b][k] = relu'(act3) * sum_j dh1[b][j] W4[j][k] (W4 as MN-major B)

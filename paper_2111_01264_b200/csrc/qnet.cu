@@ -43,6 +43,8 @@ int tma_fc1_fwd(const pq_net *nets, bf16 *const *act3, float *const *part, int s
                 cudaStream_t st);
 int tma_fc1_fwd_resident(const pq_net *nets, bf16 *const *act3, float *const *part, int splits, int groups, int n,
                          cudaStream_t st);
+int tma_fc1_dgrad_resident(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *dY3, int n,
+                           cudaStream_t st);
 int tma_fc1_dgrad(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *dY3, int n, cudaStream_t st);
 int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st,
                     bf16 *dY2p, bf16 *dY2q);
@@ -689,6 +691,8 @@ static B1wOp::Args args_b1w(const pq_learn_args *la, const WS &w, int n, int *s1
 }
 // B4d: dY3[b][k] = relu'(x3) * sum_j W4[j][k] dh1[b][j]   (D[k][b], MN-major W4)
 static int launch_b4d(const pq_net &th, int n, const WS &w, cudaStream_t st) {
+    if (use_tma(n) && conv1_shift())  // unswapped, the 128-sample dh1 tile resident per CTA
+        return tma_fc1_dgrad_resident(th, w.dh1_bf, w.act3[0], w.dY3, n, st);
     if (use_tma(n))  // unswapped on the TMA engine: D[b][k], W4 as MN-major B
         return tma_fc1_dgrad(th, w.dh1_bf, w.act3[0], w.dY3, n, st);
     GemmArgs<LoadDense, LoadDense, EpiMaskT> g{};
