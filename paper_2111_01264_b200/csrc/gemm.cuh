@@ -516,6 +516,20 @@ struct EpiMask {
 
 // EpiMask that also writes the masked rows of a 9 x 9 map onto a zero-padded 11 x 11
 // grid at (y + 1, x + 1) (conv3's data gradient for k_conv2_dgrad_shift)
+// fc1's data gradient [b][(y*7 + x)*64 + c] also onto a zero-padded 11 x 11 grid at
+// (y + 2, x + 2) (k_conv3_dgrad_shift's operand); rows = samples, columns = (pixel, channel)
+struct EpiMaskPad7 {
+    EpiMask e;
+    bf16 *out_pad;
+    PQ_DEV void apply(int m, int n0, const float *v, int cnt, int sp) const {
+        e.apply(m, n0, v, cnt, sp);
+        if (m >= e.M || n0 >= e.N) return;
+        const int p = n0 >> 6, y = p / 7, x = p - y * 7;
+        const size_t oo = ((size_t)(m * 11 + y + 2) * 11 + x + 2) * 64 + (n0 & 63);
+        store_masked32(out_pad + oo, e.mask + (size_t)m * e.ld + n0, v, min(cnt, e.N - n0));
+    }
+};
+
 // (and, if out10 is set, onto a 10 x 10 grid at (y, x): k_conv2_wgrad_shift's operand)
 struct EpiMaskPad {
     EpiMask e;

@@ -1581,14 +1581,164 @@ int tma_fc1_fwd_resident(const pq_net *nets, bf16 *const *act3, float *const *pa
 }
 
 int tma_fc1_dgrad_resident(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *dY3, int n,
-                           cudaStream_t st) {
+                           cudaStream_t st, bf16 *dY3p) {
+    auto setup = [&](auto &g) -> int {
+        memset(&g, 0, sizeof(g));
+        if (int rc = map2(&g.a[0], dh1_bf, n, 512, 512, "dh1")) return rc;
+        if (int rc = map2(&g.b[0], (const bf16 *)th.shadow + S_W4, 512, 3136, 3136, "W4")) return rc;
+        g.groups = 1, g.mtiles = (n + 127) / 128, g.ntiles = 49, g.splits = 1, g.nk = 8, g.kc = 8, g.a_early = 0;
+        return 0;
+    };
+    if (dY3p) {  // also onto the padded 11 x 11 grid of the shifted conv3 data gradient
+        static thread_local RAArgs<EpiMaskPad7> g;
+        if (int rc = setup(g)) return rc;
+        g.ep[0] = EpiMaskPad7{EpiMask{dY3, act3, n, 3136, 3136}, dY3p};
+        return launch_resident_a<EpiMaskPad7, true>(g, st, "fc1 dgrad (resident dh1, padded copy)");
+    }
     static thread_local RAArgs<EpiMask> g;
-    memset(&g, 0, sizeof(g));
-    if (int rc = map2(&g.a[0], dh1_bf, n, 512, 512, "dh1")) return rc;
-    if (int rc = map2(&g.b[0], (const bf16 *)th.shadow + S_W4, 512, 3136, 3136, "W4")) return rc;
+    if (int rc = setup(g)) return rc;
     g.ep[0] = EpiMask{dY3, act3, n, 3136, 3136};
-    g.groups = 1, g.mtiles = (n + 127) / 128, g.ntiles = 49, g.splits = 1, g.nk = 8, g.kc = 8, g.a_early = 0;
     return launch_resident_a<EpiMask, true>(g, st, "fc1 dgrad (resident dh1)");
+}
+
+// ---- conv3 data gradient by row-shifted descriptors
+// dY2 = relu'(act2) * transposed conv3(dY3): on the zero-padded 11 x 11 grid dY3p (dY3 at
+// (y + 2, x + 2), written by fc1's data gradient) GEMM row r = (s, y, x) (y, x = 9, 10
+// discarded) reads row r + 11 (2 - kh) + (2 - kw) for tap (kh, kw); one TMA box of 152 rows
+// feeds the 9 taps against 9 resident MN-major W3 tiles, in the tap order of the im2col
+// kernel, so dY2 (and its padded copies) are bit-identical.
+constexpr int C3D_ROWS = 152, C3D_BOX = C3D_ROWS * 128, C3D_STAGES = 3, C3D_W = 64 * 128;
+constexpr int C3D_SMEM = 1024 + 9 * C3D_W + C3D_STAGES * C3D_BOX;
+struct C3DArgs {
+    CUtensorMap a, w;  // dY3p pixel rows [n*121][64]; W3 view {c, tap, o}
+    EpiMaskPad ep;     // dY2 [n*81][64] + padded copies
+    int n;
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv3_dgrad_shift(const __grid_constant__ C3DArgs g) {
+    constexpr uint32_t IDESC = idesc_bf16(64, false, true);
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t full[C3D_STAGES], empty[C3D_STAGES], accf[2], acce[2], wbar;
+    __shared__ uint32_t tmem_base_s;
+    TlProbe tp;
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t w_s = smem_u32(smem), ring_s = w_s + 9 * C3D_W;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < C3D_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&accf[b], 1);
+            mbar_init(&acce[b], 4);
+        }
+        mbar_init(&wbar, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<128>(&tmem_base_s);
+    if (tid == 32) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&g.a) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&g.w) : "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const int total = (g.n * 121 + 127) / 128;
+    if (tid == 0) {  // W3 (updated two or more launches back) before the dependency wait
+        mbar_expect_tx(&wbar, 9u * C3D_W);
+        for (int tap = 0; tap < 9; ++tap) tma_load_3d(w_s + tap * C3D_W, &g.w, &wbar, 0, tap, 0);
+    }
+    griddep_wait();
+    griddep_launch();
+    tp.waited();
+    if (warp == 0) {
+        if (lane == 0) {  // producer
+            uint32_t q = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
+                const uint32_t s = q % C3D_STAGES;
+                if (q >= C3D_STAGES) mbar_wait(&empty[s], ((q / C3D_STAGES) - 1) & 1);
+                mbar_expect_tx(&full[s], (uint32_t)C3D_BOX);
+                tma_load_2d(ring_s + s * C3D_BOX, &g.a, &full[s], 0, t * 128);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            mbar_wait(&wbar, 0);
+            uint32_t q = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
+                const uint32_t buf = q & 1, s = q % C3D_STAGES;
+                if (q >= 2) mbar_wait(&acce[buf], ((q >> 1) - 1) & 1);
+                mbar_wait(&full[s], (q / C3D_STAGES) & 1);
+                tc_fence_after();
+                const uint32_t a0 = ring_s + s * C3D_BOX, acc = tmem + buf * 64;
+#pragma unroll
+                for (int tap = 0; tap < 9; ++tap) {
+                    const uint32_t shift = (uint32_t)((2 - tap / 3) * 11 + (2 - tap % 3)) * 128;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint64_t ad = desc_sw128(a0 + shift + j * 32, 0);
+                        const uint64_t bd = desc_sw128(w_s + tap * C3D_W + j * 2048, 8192);
+                        umma_bf16(acc, ad, bd, IDESC, (tap > 0 || j > 0) ? 1u : 0u);
+                    }
+                }
+                umma_commit(&empty[s]);
+                umma_commit(&accf[buf]);
+            }
+        }
+    } else if (warp >= 4) {  // epilogue
+        const int wq = warp - 4;
+        uint32_t q = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
+            const uint32_t buf = q & 1;
+            mbar_wait(&accf[buf], (q >> 1) & 1);
+            __syncwarp();
+            tc_fence_after();
+            float v[2][32];
+            const uint32_t trow = tmem + buf * 64 + ((uint32_t)(wq * 32) << 16);
+            tmem_ld32(trow, v[0]);
+            tmem_ld32(trow + 32, v[1]);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acce[buf]);
+            const int r = t * 128 + wq * 32 + lane, smp = r / 121, p = r - smp * 121, y = p / 11, x = p - y * 11;
+            if (smp < g.n && y < 9 && x < 9) {
+                const int m = smp * 81 + y * 9 + x;
+                g.ep.apply(m, 0, v[0], 32, 0);
+                g.ep.apply(m, 32, v[1], 32, 0);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<128>(tmem);
+    tp.done('C');
+}
+
+int tma_conv3_dgrad_shift(const pq_net &th, const bf16 *dY3p, const bf16 *act2, bf16 *dY2, bf16 *dY2p, bf16 *dY2q,
+                          int n, cudaStream_t st) {
+    static thread_local C3DArgs g;
+    memset(&g, 0, sizeof(g));
+    const uint64_t ad[2] = {64, (uint64_t)n * 121}, as[1] = {64};
+    if (int rc = make_map(&g.a, dY3p, 2, ad, as, "dY3 padded rows", C3D_ROWS)) return rc;
+    const uint64_t dims[3] = {64, 9, 64}, strd[2] = {64, 576};
+    if (int rc = make_map(&g.w, (const bf16 *)th.shadow + S_W3, 3, dims, strd, "W3 view")) return rc;
+    g.ep = EpiMaskPad{EpiMask{dY2, act2, n * 81, 64, 64}, dY2p, FastDiv(81), FastDiv(9), dY2q};
+    g.n = n;
+    static bool configured = false;
+    if (!configured) {
+        PQ_CUDA_TRY(cudaFuncSetAttribute(k_conv3_dgrad_shift, cudaFuncAttributeMaxDynamicSharedMemorySize, C3D_SMEM));
+        configured = true;
+    }
+    if (!g_sms) {
+        int dev = 0;
+        PQ_CUDA_TRY(cudaGetDevice(&dev));
+        PQ_CUDA_TRY(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int total = (n * 121 + 127) / 128;
+    return cuda_err(launch_k(k_conv3_dgrad_shift, dim3(std::min(total, g_sms)), dim3(GEMM_THREADS), C3D_SMEM, st, g),
+                    "conv3 dgrad (shifted descriptors)");
 }
 
 // fc1 data gradient: dY3[b][k] = relu'(act3) * sum_j dh1[b][j] W4[j][k] (W4 as MN-major B)

@@ -44,7 +44,9 @@ int tma_fc1_fwd(const pq_net *nets, bf16 *const *act3, float *const *part, int s
 int tma_fc1_fwd_resident(const pq_net *nets, bf16 *const *act3, float *const *part, int splits, int groups, int n,
                          cudaStream_t st);
 int tma_fc1_dgrad_resident(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *dY3, int n,
-                           cudaStream_t st);
+                           cudaStream_t st, bf16 *dY3p);
+int tma_conv3_dgrad_shift(const pq_net &th, const bf16 *dY3p, const bf16 *act2, bf16 *dY2, bf16 *dY2p, bf16 *dY2q,
+                          int n, cudaStream_t st);
 int tma_fc1_dgrad(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *dY3, int n, cudaStream_t st);
 int tma_conv3_dgrad(const pq_net &th, const bf16 *dY3, const bf16 *act2, bf16 *dY2, int n, cudaStream_t st,
                     bf16 *dY2p, bf16 *dY2q);
@@ -104,6 +106,7 @@ struct WS {
     bf16 *dY2p;  // conv3's data gradient on the padded 11 x 11 grid (TMA engine; pad rows stay 0)
     bf16 *act1s2[2];  // act1 as 2x2 space-to-depth [n][10][10][128] (TMA engine, shifted conv2)
     bf16 *dY2q;       // conv3's data gradient on the 10 x 10 grid (zero rows at 9; shifted conv2 wgrad)
+    bf16 *dY3p;       // fc1's data gradient on the zero-padded 11 x 11 grid (shifted conv3 dgrad)
     float *part1, *part2, *part3, *grad4;
     uint32_t *done;  // [3] CTA completion counters (unused, acting, head)
     int64_t *idx_cur;  // the step's sampled slots (stashed by the head)
@@ -154,6 +157,7 @@ static WS carve(void *base, int N, int A) {
     w.dY2p = N >= 128 ? (bf16 *)take((size_t)N * 121 * 64 * 2) : nullptr;
     for (int g = 0; g < 2; ++g) w.act1s2[g] = N >= 128 ? (bf16 *)take((size_t)N * 100 * 128 * 2) : nullptr;
     w.dY2q = N >= 128 ? (bf16 *)take((size_t)N * 100 * 64 * 2) : nullptr;
+    w.dY3p = N >= 128 ? (bf16 *)take((size_t)N * 121 * 64 * 2) : nullptr;
     w.bytes = off;
     return w;
 }
@@ -691,8 +695,8 @@ static B1wOp::Args args_b1w(const pq_learn_args *la, const WS &w, int n, int *s1
 }
 // B4d: dY3[b][k] = relu'(x3) * sum_j W4[j][k] dh1[b][j]   (D[k][b], MN-major W4)
 static int launch_b4d(const pq_net &th, int n, const WS &w, cudaStream_t st) {
-    if (use_tma(n) && conv1_shift())  // unswapped, the 128-sample dh1 tile resident per CTA
-        return tma_fc1_dgrad_resident(th, w.dh1_bf, w.act3[0], w.dY3, n, st);
+    if (use_tma(n) && conv1_shift() && w.dY3p)  // unswapped, the 128-sample dh1 tile resident per CTA
+        return tma_fc1_dgrad_resident(th, w.dh1_bf, w.act3[0], w.dY3, n, st, w.dY3p);
     if (use_tma(n))  // unswapped on the TMA engine: D[b][k], W4 as MN-major B
         return tma_fc1_dgrad(th, w.dh1_bf, w.act3[0], w.dY3, n, st);
     GemmArgs<LoadDense, LoadDense, EpiMaskT> g{};
@@ -911,7 +915,9 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         }
     }
     const bool shift = conv1_shift() && w.dY1p && w.dY2p;  // shifted-descriptor conv kernels (TMA engine)
-    if (use_tma(n)) {
+    if (use_tma(n) && shift && w.dY3p) {  // over fc1's data gradient on the padded 11 x 11 grid
+        if (int rc = tma_conv3_dgrad_shift(th, w.dY3p, w.act2[0], w.dY2, w.dY2p, w.dY2q, n, st)) return rc;
+    } else if (use_tma(n)) {
         if (int rc = tma_conv3_dgrad(th, w.dY3, w.act2[0], w.dY2, n, st, shift ? w.dY2p : nullptr,
                                      shift ? w.dY2q : nullptr))
             return rc;

@@ -19,7 +19,7 @@ from paper_2111_01264_b200.replay import ReplayMemory
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 NAMES = {"G": "k_gemm", "F": "k_fused", "H": "k_head", "O": "k_optimizer", "P": "k_fc2_partials",
          "T": "k_tma_gemm", "D": "k_conv2_dgrad_shift", "S": "k_frames_s2d", "1": "k_conv1_shift",
-         "2": "k_conv2_shift", "W": "k_conv1_wgrad_shift", "V": "k_conv2_wgrad_shift", "3": "k_conv3_shift", "4": "k_resident_a"}
+         "2": "k_conv2_shift", "W": "k_conv1_wgrad_shift", "V": "k_conv2_wgrad_shift", "3": "k_conv3_shift", "4": "k_resident_a", "C": "k_conv3_dgrad_shift"}
 mem = ReplayMemory(40000)
 mem.prepopulate(FrameEnvSpec(key=5), 40000, np.random.default_rng(1))
 theta, target = dnn.init_network(1), dnn.init_network(2)
