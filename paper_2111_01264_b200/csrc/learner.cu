@@ -2031,6 +2031,24 @@ int tma_conv1_fwd(const pq_net *nets, const bf16 *s2d, int nframes, const int *c
     return launch_tma<64, false, false>(g, st, "conv1 forward (TMA)");
 }
 
+// bias + ReLU of 32 accumulator columns (scale folded in) -> 32 bf16 at dst (and dst2):
+// EpiBiasRelu's arithmetic with the biases from shared memory
+PQ_DEV void bias_relu_store32(const float *v, const float *bias, float scale, bf16 *dst, bf16 *dst2) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+        float y[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const float t = v[j + e] * scale + bias[j + e];
+            y[e] = t > 0.f ? t : 0.f;
+        }
+        const uint4 pk = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]),
+                                    pack_bf16(y[6], y[7]));
+        *reinterpret_cast<uint4 *>(dst + j) = pk;
+        if (dst2) *reinterpret_cast<uint4 *>(dst2 + j) = pk;
+    }
+}
+
 // ---- conv1 forward as four row-shifted GEMMs over the space-to-depth stacks
 // On the 21 x 21 grid of s2d pixels conv1 (8x8 / 4 over 84 x 84) is a 2 x 2 stride-1
 // conv.  Computed for all 21 x 21 base pixels of a sample (outputs with y or x = 20 are
@@ -2144,6 +2162,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_co
         }
     } else if (warp >= 4) {  // epilogue: TMEM lane quadrant = warp % 4
         const int wq = warp - 4;
+        __shared__ float s_bias[2][32];  // conv1 biases (after the wait: the update is upstream)
+        if (wq == 0)
+            for (int gg = 0; gg < g.groups; ++gg) s_bias[gg][lane] = g.ep[gg].bias[lane];
+        named_bar_sync(1, 128);
         uint32_t q = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
             const uint32_t buf = q & 1;
@@ -2165,15 +2187,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_co
 #pragma unroll
                 for (int gg = 0; gg < 2; ++gg) {
                     if (gg >= g.groups) break;
-                    if (!g.act1s2[gg]) {
-                        g.ep[gg].apply(m, 0, v[gg], 32, 0);
-                    } else if (g.ep[gg].out) {  // both layouts
-                        g.ep[gg].apply_dual(m, v[gg], g.act1s2[gg] + o2);
-                    } else {  // only the space-to-depth copy
-                        EpiBiasRelu e = g.ep[gg];
-                        e.out = g.act1s2[gg] + o2, e.ld = 0;
-                        e.apply(0, 0, v[gg], 32, 0);
-                    }
+                    const EpiBiasRelu &e = g.ep[gg];
+                    bf16 *d1 = e.out ? e.out + (size_t)m * e.ld : nullptr;  // dense act1 (absent with the copy)
+                    bf16 *d2 = g.act1s2[gg] ? g.act1s2[gg] + o2 : nullptr;   // 2x2 space-to-depth copy
+                    bias_relu_store32(v[gg], s_bias[gg], e.scale, d1 ? d1 : d2, d1 ? d2 : nullptr);
                 }
             }
         }
@@ -2327,6 +2344,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv_shift(const __grid_con
         }
     } else if (warp >= 4) {  // epilogue
         const int wq = warp - 4;
+        __shared__ float s_bias[2][64];
+        if (wq < g.groups)
+            for (int c = lane; c < 64; c += 32) s_bias[wq][c] = g.ep[wq].bias[c];
+        named_bar_sync(1, 128);
         uint32_t q = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
             const uint32_t buf = q & 1;
@@ -2345,8 +2366,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv_shift(const __grid_con
                       x = p - y * C::GW;
             if (smp < g.n && y < C::OW && x < C::OW) {
                 const int o = (smp * C::OW + y) * C::OW + x;
-                g.ep[grp].apply(o, 0, v[0], 32, 0);
-                g.ep[grp].apply(o, 32, v[1], 32, 0);
+                bf16 *dst = g.ep[grp].out + (size_t)o * 64;
+                bias_relu_store32(v[0], s_bias[grp], 1.0f, dst, nullptr);
+                bias_relu_store32(v[1], s_bias[grp] + 32, 1.0f, dst + 32, nullptr);
             }
         }
     }
