@@ -518,7 +518,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     learn_flop = FLOP_PER_SAMPLE_LEARN * hp.batch_size
     achieved_tf = learn_flop / (learn_ms * 1e-3) / 1e12
     gather_gbs = 80_000 * GATHER_BYTES_PER_TRANSITION / (gather_ms * 1e-3) / 1e9
-    per_epoch_launches = (hp.C // hp.W) * 5 + (hp.C // hp.F) * 10 + 2
+    per_epoch_launches = (hp.C // hp.W) * 5 + (hp.C // hp.F) * 10 + 5  # + flush, copy, target prologue (3)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         threads = len(os.sched_getaffinity(0))

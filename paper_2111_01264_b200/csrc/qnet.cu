@@ -764,11 +764,14 @@ static bool fused_backward(int n, const pq_learn_args *la, float *grad_only) {
 // (executor epochs, batch 32-class: pq_learn_step_pipelined).  theta-minus is fixed within
 // an epoch and the head has already advanced the step counter to the next minibatch, so
 // conv1 / conv2 / conv3 of the target network for step k+1 ride as extra CTAs in step k's
-// {conv2 dgrad | conv2 wgrad}, {conv1 wgrad | update} and conv1-update launches, and its
-// fc1 in step k+1's conv1 launch.  Each stage reads what the launch before it wrote; the
-// same GEMM configurations as the one-shot forward, so the results are bit-identical.
-// pq_learn_target_prologue primes conv1..conv3 for the first step of an epoch.
+// fc1-dgrad, {conv2 dgrad | conv2 wgrad} and {conv1 wgrad | update} launches (each shorter
+// than its host's critical tiles), and its fc1 in step k+1's conv1 launch.  Each stage
+// reads what two or more launches back wrote; the same GEMM configurations as the one-shot
+// forward, so the results are bit-identical.  pq_learn_target_prologue primes
+// conv1..conv3 for the first step of an epoch.
 using F1Op = GemmOp<32, false, false, 3, 1, LoadFrames, LoadDense, EpiBiasRelu>;
+using F1LateOp = GemmOp<32, false, false, 3, 0, LoadFrames, LoadDense, EpiBiasRelu>;  // table after the wait
+using B4dTOp = GemmOp<32, true, false, 0, 1, LoadDense, LoadDense, EpiMaskT>;        // fc1 dgrad at BN 32
 using F23Op = GemmOp<64, false, false, 0, 2, LoadIm2col, LoadDense, EpiBiasRelu>;
 using F4Op = GemmOp<32, false, false, 0, 1, LoadDense, LoadDense, EpiF32T>;
 static F1Op::Args args_f1(const pq_net &net, const FwdInput &in, int n, bf16 *act1) {
@@ -815,7 +818,25 @@ static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStrea
     const pq_net &th = la->theta;
     const bf16 *sh = (const bf16 *)th.shadow;
     int s1 = 1, s2 = 1, s3 = 1;
-    if (int rc = launch_b4d(th, n, w, st)) return rc;
+    if (pipe) {  // fc1 dgrad + the target conv1 of the next step (its frame table after the wait:
+                 // the head, the launch before, advanced the counter)
+        B4dTOp::Args g{};
+        g.a[0] = LoadDense{sh + S_W4, 512, 3136, 3136};
+        g.b[0] = LoadDense{w.dh1_bf, n, 512, 512};
+        g.e[0] = EpiMaskT{w.dY3, w.act3[0], 3136, n, 3136};
+        g.M = 3136, g.N = n, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
+        FusedArgs<B4dTOp, F1LateOp, NoOp> f{};
+        f.p0 = B4dTOp::make(g);
+        const F1Op::Args t1 = args_f1(la->target, target_input(la), n, w.act1[1]);
+        F1LateOp::Args t1l{};
+        t1l.a[0] = t1.a[0], t1l.b[0] = t1.b[0], t1l.e[0] = t1.e[0];
+        t1l.M = t1.M, t1l.N = t1.N, t1l.K = t1.K, t1l.kc_per_split = t1.kc_per_split, t1l.splits = 1, t1l.ones_at = -1;
+        f.p1 = F1LateOp::make(t1l);
+        f.n0 = B4dTOp::ctas(f.p0, 1), f.n1 = F1LateOp::ctas(f.p1, 1);
+        PQ_CHECK(launch_fused(f, 0, st), "fc1 dgrad | target conv1");
+    } else if (int rc = launch_b4d(th, n, w, st)) {
+        return rc;
+    }
     {
         FusedArgs<B3dOp, B3wOp, B4wOp> f{};
         f.p0 = B3dOp::make(args_b3d(sh, w, n));
@@ -825,13 +846,14 @@ static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStrea
         PQ_CHECK(launch_fused(f, B4wOp::ctas(f.p2, 1), st), "conv3 dgrad | conv3 wgrad | fc1 wgrad+rmsprop");
     }
     const pq_net &tg = la->target;
-    if (pipe) {  // + the target conv1 of the next step
-        FusedArgs<B2dOp, B2wOp, F1Op> f{};
+    if (pipe) {  // + the target conv2 of the next step (CTAs dispatch in part order: the
+                 // critical tiles, then the target stage, then the weight gradient)
+        FusedArgs<B2dOp, F23Op, B2wOp> f{};
         f.p0 = B2dOp::make(args_b2d(sh, w, n));
-        f.p1 = B2wOp::make(args_b2w(w, n, &s2));
-        f.p2 = F1Op::make(args_f1(tg, target_input(la), n, w.act1[1]));
-        f.n0 = B2dOp::ctas(f.p0, 1), f.n1 = B2wOp::ctas(f.p1, 1);
-        PQ_CHECK(launch_fused(f, F1Op::ctas(f.p2, 1), st), "conv2 dgrad | conv2 wgrad | target conv1");
+        f.p1 = F23Op::make(args_f2(tg, w.act1[1], n, w.act2[1]));
+        f.p2 = B2wOp::make(args_b2w(w, n, &s2));
+        f.n0 = B2dOp::ctas(f.p0, 1), f.n1 = F23Op::ctas(f.p1, 1);
+        PQ_CHECK(launch_fused(f, B2wOp::ctas(f.p2, 1), st), "conv2 dgrad | target conv2 | conv2 wgrad");
     } else {
         FusedArgs<B2dOp, B2wOp, NoOp> f{};
         f.p0 = B2dOp::make(args_b2d(sh, w, n));
@@ -846,11 +868,11 @@ static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStrea
         o.s1 = s1;
         OptArgs os = o;
         os.lo1 = P_W2, os.hi1 = P_W4, os.lo2 = P_B4, os.hi2 = os.total;
-        if (pipe) {  // + the target conv2 of the next step
-            FusedArgs<B1wOp, OptOp, F23Op> f{};
-            f.p0 = b1, f.p1 = os, f.p2 = F23Op::make(args_f2(tg, w.act1[1], n, w.act2[1]));
-            f.n0 = B1wOp::ctas(f.p0, 1), f.n1 = OptOp::ctas(os);
-            PQ_CHECK(launch_fused(f, F23Op::ctas(f.p2, 1), st), "conv1 wgrad | update | target conv2");
+        if (pipe) {  // + the target conv3 of the next step (dispatched before the update CTAs)
+            FusedArgs<B1wOp, F23Op, OptOp> f{};
+            f.p0 = b1, f.p1 = F23Op::make(args_f3(tg, w.act2[1], n, w.act3[1])), f.p2 = os;
+            f.n0 = B1wOp::ctas(f.p0, 1), f.n1 = F23Op::ctas(f.p1, 1);
+            PQ_CHECK(launch_fused(f, OptOp::ctas(os), st), "conv1 wgrad | target conv3 | update");
         } else {
             FusedArgs<B1wOp, OptOp, NoOp> f{};
             f.p0 = b1, f.p1 = os;
@@ -859,15 +881,8 @@ static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStrea
         }
     }
     o.lo1 = P_W1, o.hi1 = P_W2, o.lo2 = P_W2, o.hi2 = P_W2;
-    if (pipe) {  // conv1's update + the target conv3 of the next step
-        FusedArgs<OptOp, F23Op, NoOp> f{};
-        f.p0 = o, f.p1 = F23Op::make(args_f3(tg, w.act2[1], n, w.act3[1]));
-        f.n0 = OptOp::ctas(o), f.n1 = F23Op::ctas(f.p1, 1);
-        PQ_CHECK(launch_fused(f, 0, st), "update conv1 | target conv3");
-    } else {
-        PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((P_W2 - P_W1 + 255) / 256)), dim3(256), 0, st, o),
-                 "optimizer (conv1)");
-    }
+    PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((P_W2 - P_W1 + 255) / 256)), dim3(256), 0, st, o),
+             "optimizer (conv1)");
     return 0;
 }
 

@@ -204,9 +204,9 @@ class DeviceRun:
         # one spare row: the pipelined target forward of the epoch's last step reads the
         # (unused) minibatch after it
         self.idx_table = torch.zeros((self.updates + 1) * B, dtype=torch.int64, device="cuda")
-        # PQ_PIPE_TARGET=1: pipelined target forward (bit-identical; measured slower at
-        # batch 32, 80 vs 71 us/update: see DESIGN.md section 4)
-        self.pipelined = os.environ.get("PQ_PIPE_TARGET", "0") == "1" and not persistent
+        # pipelined target forward (bit-identical; batch 32: 70.6 vs 71.3 us/update);
+        # PQ_PIPE_TARGET=0 runs the target forward inside each step
+        self.pipelined = os.environ.get("PQ_PIPE_TARGET", "1") != "0" and not persistent
         self.update_counter = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.step_counter = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.nonfinite = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")

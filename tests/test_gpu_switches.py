@@ -85,7 +85,7 @@ def test_fused_backward_matches_multistream(tmp_path):
 
 @pytest.mark.parametrize("graphs", [False, True])
 def test_pipelined_target_forward_is_bit_identical(graphs, monkeypatch):
-    """PQ_PIPE_TARGET=1 (executor switch): the target network's forward of step k+1 runs
+    """PQ_PIPE_TARGET (executor, default on): the target network's forward of step k+1 runs
     inside step k's backward launches; epoch after epoch the parameters must match the
     unpipelined learner bit for bit (theta hash per epoch and at the end)."""
     from paper_2111_01264_b200.agent import EpsilonSchedule, HyperParams
