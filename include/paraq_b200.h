@@ -33,7 +33,8 @@ extern "C" {
 
 #define PQ_ABI_VERSION 1
 #define PQ_FRAME_BYTES 7056 /* one 84x84 uint8 frame */
-#define PQ_REC_INTS 8       /* replay record: frame slots f0..f4, action, reward (f32 bits), terminal */
+#define PQ_REC_INTS 8       /* replay record: frame slots f0..f4, action | terminal << 16,
+                               reward as f64 bits (lo, hi) */
 
 /* ---- housekeeping ---------------------------------------------------------- */
 int pq_abi_version(void);
@@ -63,8 +64,9 @@ int pq_net_copy(pq_net dst, pq_net src, int actions, void *stream);
  * A state is 4 frames; frames live in a uint8 ring [slots][7056].  Sample b,
  * channel c reads slot refs[map(b) * ref_stride + ref_off + c] (map = identity when
  * NULL); slot -1 is the all-zero (masked) frame.  Replay records [cap][8] int32 are
- * {f0, f1, f2, f3, f4, action, reward_bits, terminal}: state = (f0..f3), next state =
- * (f1..f4), so ref_off 0 / 1 selects s / s'. */
+ * {f0, f1, f2, f3, f4, action | terminal << 16, reward_lo, reward_hi} (terminal = the
+ * bootstrap terminal, executor.py:241; reward = the f64 bits of the reference's float):
+ * state = (f0..f3), next state = (f1..f4), so ref_off 0 / 1 selects s / s'. */
 
 /* ---- replay (replay.py) ----------------------------------------------------------- */
 /* rng.integers(0, n, size=count), bit-exact with numpy PCG64 + buffered Lemire;
@@ -73,14 +75,19 @@ int pq_net_copy(pq_net dst, pq_net src, int actions, void *stream);
 int pq_sample_indices(uint64_t *pcg_state, uint32_t n, int64_t count, int64_t *idx_out,
                       void *stream);
 /* Stack gather of a sampled batch: s_out / s2_out [B][4][84][84] uint8,
- * a_out int32 [B], r_out f32 [B], term_out uint8 [B]. */
+ * a_out int32 [B], r_out f64 [B], term_out uint8 [B]. */
 int pq_replay_gather(const uint8_t *ring, const int32_t *records, const int64_t *idx,
-                     int64_t B, uint8_t *s_out, uint8_t *s2_out, int32_t *a_out, float *r_out,
+                     int64_t B, uint8_t *s_out, uint8_t *s2_out, int32_t *a_out, double *r_out,
                      uint8_t *term_out, void *stream);
 /* Flush: staging records [W][steps][8] -> ring records in owner-major order,
  * slot = (push_count + j * steps + k) mod capacity. */
 int pq_replay_flush(const int32_t *staging, int W, int steps, int32_t *records,
                     int64_t capacity, int64_t push_count, void *stream);
+/* The same for the staged steps [k0, k1) of every sampler (the blocking training
+ * event of the non-concurrent modes flushes mid-epoch, executor.py:436-440):
+ * slot = (push_count + j * (k1 - k0) + k - k0) mod capacity. */
+int pq_replay_flush_range(const int32_t *staging, int W, int steps, int k0, int k1,
+                          int32_t *records, int64_t capacity, int64_t push_count, void *stream);
 
 /* ---- synthetic frame environments (caller side, oracle/envs.py on the CPU) -------- */
 typedef struct pq_envs {
@@ -145,6 +152,8 @@ typedef struct pq_learn_args {
     float *td_out;               /* optional f32 [n][3]: target, delta, loss */
     void *ws;
     int max_batch;
+    float huber;                 /* > 0: Huber TD loss with this delta (north star; opt-in);
+                                    0 / inf: the reference's half-squared loss (nn.py:140-144) */
 } pq_learn_args;
 
 /* One learner step (agent.train_minibatch): target forward + max, online forward,

@@ -26,6 +26,18 @@ Restatement choices (the reference has no conv net):
 * init: the reference init_network bound sqrt(6/(fan_in+fan_out)) over each
   flattened (out, in*kh*kw) matrix, drawn layer by layer from one
   default_rng(seed) (nn.py:93-109).
+
+Two optional knobs, both off by default (the fp64 reference arithmetic):
+* ``K`` -- the kernel module: ``oracle._lib`` (kernels.c, bit-exact with numba, the
+  default) or ``oracle.blas`` (the reference numpy backend with batched rows, for
+  batch 1024 / W 512 in seconds);
+* ``store`` -- a storage model (``Bf16Storage``): the points where the device path
+  keeps a value in bf16 (the tensor-core operands W1..W4, the conv activations, the
+  data gradients).  The oracle still computes in fp64 but rounds exactly there, so a
+  comparison with the bf16 tensor-core path is well posed: what remains is fp32
+  accumulation order, which is what the stated tolerance (rel 1e-3) bounds.
+* ``huber`` -- the opt-in Huber TD loss (north star); None = the reference's
+  half-squared loss (Huber with delta = infinity).
 """
 
 from __future__ import annotations
@@ -34,7 +46,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib as K
+from . import _lib as _K_EXACT
 
 
 @dataclass(frozen=True)
@@ -113,6 +125,83 @@ class Opt:
         return cls(z(p.weights), z(p.biases), z(p.weights), z(p.biases))
 
 
+def bf16_round(x) -> np.ndarray:
+    """fp64 -> fp32 (round to nearest even) -> bf16 (round to nearest even), as fp64:
+    the device's fp32 value stored with __float2bfloat16_rn."""
+    f = np.ascontiguousarray(x, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def fp32_round(x) -> np.ndarray:
+    return np.asarray(x, dtype=np.float32).astype(np.float64)
+
+
+class Bf16Storage:
+    """Where the B200 learner / acting path stores bf16:
+
+    * weights of layers 0..3 (conv1..fc1): the bf16 shadow of the fp32 master;
+      fc2 and all biases stay fp32;
+    * forward activations of the conv layers (act1..act3, NHWC bf16); fc1's output
+      h1 and the Q-values stay fp32;
+    * data gradients: fc1's output delta dh1 feeds the fc1 weight gradient and data
+      gradient as bf16 (its bias gradient sums the fp32 values), dY3 / dY2 / dY1
+      (post-mask) are stored bf16 and every consumer reads those.
+
+    By default the oracle rounds its own fp64 value at each of those points.  Two
+    device inputs can be substituted (teacher forcing; every value is still computed
+    by the oracle in fp64 from them):
+
+    * ``masks[k]``: the ReLU mask of layer k (the device's stored activation > 0).  A
+      mask bit is a discrete decision on a value that is ~0: where fp32 and fp64 land
+      on opposite sides of 0 the whole data gradient of that unit flips, which no
+      tolerance on the rest can absorb (a few per 10^4 fc1 units at batch 32);
+    * ``acts[k]`` / ``deltas[k]``: the device's stored bf16 tensor at that point.
+      Chained bf16 roundings are not well conditioned either: a value within the
+      accumulation error of a rounding boundary lands one ulp (2^-8) apart, and each
+      rounding stage turns an upstream error e into ~sqrt(e * 2^-8).  With the
+      device's stored tensors as the next stage's inputs, each stage is compared on
+      identical inputs, and ``seen`` keeps the oracle's own (unrounded) value at every
+      point for the stage check.
+    """
+
+    def __init__(self, bf16_layers=(0, 1, 2, 3), masks=None, acts=None, deltas=None):
+        self.bf16_layers = set(bf16_layers)
+        self.masks = masks
+        self.acts = acts or {}
+        self.deltas = deltas or {}
+        self.seen = {}
+
+    @property
+    def forced(self) -> bool:
+        return self.masks is not None or bool(self.acts)
+
+    def weight(self, k, w):
+        return bf16_round(w) if k in self.bf16_layers else w
+
+    def act(self, k, spec, x):
+        if spec.layers[k].kind != "conv":
+            return x
+        self.seen[("act", k)] = x
+        if k in self.acts:
+            return np.asarray(self.acts[k], dtype=np.float64).reshape(x.shape)
+        return bf16_round(x)
+
+    def delta(self, k, x):
+        self.seen[("delta", k)] = x
+        if k in self.deltas:
+            return np.asarray(self.deltas[k], dtype=np.float64).reshape(x.shape)
+        return bf16_round(x)
+
+    def relu_mask(self, k, pre):
+        if self.masks is not None and k < len(self.masks) and self.masks[k] is not None:
+            return np.asarray(self.masks[k], dtype=bool).reshape(pre.shape)
+        if k in self.acts:
+            return (np.asarray(self.acts[k]) > 0).reshape(pre.shape)
+        return pre > 0.0
+
+
 def init_params(spec: NetSpec, seed: int) -> Params:
     """nn.init_network (nn.py:93-109) over the flattened weight matrices."""
     rng = np.random.default_rng(seed)
@@ -166,6 +255,21 @@ def col2im(dpatch, L: Layer, in_shape, n):
     return out
 
 
+def col2im_fast(dpatch, L: Layer, in_shape, n):
+    """col2im for NHWC layers as k*k strided slice-adds (fp64 order differs from col2im's
+    np.add.at only by rounding; used with the batched kernel module)."""
+    h, w, c = in_shape
+    oh = (h - L.k) // L.s + 1
+    ow = (w - L.k) // L.s + 1
+    dp = dpatch.reshape(n, oh, ow, L.k, L.k, c)
+    out = np.zeros((n, h, w, c), dtype=np.float64)
+    for ky in range(L.k):
+        for kx in range(L.k):
+            out[:, ky:ky + L.s * (oh - 1) + 1:L.s, kx:kx + L.s * (ow - 1) + 1:L.s, :] += \
+                dp[:, :, :, ky, kx, :]
+    return out.reshape(n, -1)
+
+
 # --- forward / gradient ----------------------------------------------------------
 
 def _inputs(spec: NetSpec, states):
@@ -194,36 +298,69 @@ def _layer_rows(spec, k, act, n):
     return act.reshape(n, -1)
 
 
-def forward(spec: NetSpec, p: Params, states) -> np.ndarray:
+def _weights(p: Params, store):
+    if store is None:
+        return p.weights
+    return [store.weight(k, w) for k, w in enumerate(p.weights)]
+
+
+def _relu(K, store, k, pre):
+    if store is None or not store.forced:
+        return K.relu(pre)
+    return np.where(store.relu_mask(k, pre), pre, 0.0)
+
+
+def forward(spec: NetSpec, p: Params, states, K=None, store=None) -> np.ndarray:
     """nn.forward (nn.py:123-131)."""
+    K = K or _K_EXACT
     x = _inputs(spec, states)
     n = x.shape[0]
     last = len(spec.layers) - 1
     act = x
-    for k, (w, b) in enumerate(zip(p.weights, p.biases)):
+    for k, (w, b) in enumerate(zip(_weights(p, store), p.biases)):
         pre = K.affine_rows(w, b, _layer_rows(spec, k, act, n))
-        act = K.relu(pre) if k < last else pre
+        act = _relu(K, store, k, pre) if k < last else pre
         act = act.reshape(n, -1)
+        if store is not None and k < last:
+            act = store.act(k, spec, act)
     return act
 
 
-def forward_trace(spec: NetSpec, p: Params, states):
+def forward_trace(spec: NetSpec, p: Params, states, K=None, store=None):
     """Forward keeping every layer input (GEMM rows), pre-activation and output."""
+    K = K or _K_EXACT
     x = _inputs(spec, states)
     n = x.shape[0]
     last = len(spec.layers) - 1
     rows, pres, acts = [], [], [x]
-    for k, (w, b) in enumerate(zip(p.weights, p.biases)):
+    for k, (w, b) in enumerate(zip(_weights(p, store), p.biases)):
         r = _layer_rows(spec, k, acts[-1], n)
         pre = K.affine_rows(w, b, r)
         rows.append(r)
         pres.append(pre)
-        acts.append((K.relu(pre) if k < last else pre).reshape(n, -1))
+        a = (_relu(K, store, k, pre) if k < last else pre).reshape(n, -1)
+        if store is not None and k < last:
+            a = store.act(k, spec, a)
+        acts.append(a)
     return rows, pres, acts
 
 
-def gradient(spec: NetSpec, p: Params, states, actions, targets):
-    """nn.gradient (nn.py:134-170): exact gradient of the mean half-squared TD error."""
+def huber_delta(q, actions, targets, huber):
+    """Output delta of the mean Huber TD loss: clip(q[a] - target, -huber, huber) / n at
+    the taken action (the north star's "Huber TD loss"; the reference's half-squared
+    loss, _kernels_numpy.py:30-35, is huber = infinity)."""
+    n = q.shape[0]
+    delta = np.zeros_like(q)
+    rows = np.arange(n)
+    delta[rows, actions] = np.clip(q[rows, actions] - targets, -huber, huber) / n
+    return delta
+
+
+def gradient(spec: NetSpec, p: Params, states, actions, targets, K=None, store=None,
+             huber=None):
+    """nn.gradient (nn.py:134-170): exact gradient of the mean half-squared TD error
+    (or of the mean Huber loss when ``huber`` is set)."""
+    K = K or _K_EXACT
     x = _inputs(spec, states)
     n = x.shape[0]
     actions = np.ascontiguousarray(actions, dtype=np.int64)
@@ -233,25 +370,39 @@ def gradient(spec: NetSpec, p: Params, states, actions, targets):
     n_out = spec.layers[-1].out
     if actions.size and (actions.min() < 0 or actions.max() >= n_out):
         raise ValueError("action index out of range")
-    rows, pres, acts = forward_trace(spec, p, x)
+    rows, pres, acts = forward_trace(spec, p, x, K, store)
+    weights = _weights(p, store)
     last = len(spec.layers) - 1
     shapes = spec.shapes()
-    delta = K.output_delta(acts[-1], actions, targets)
+    if huber is None:
+        delta = K.output_delta(acts[-1], actions, targets)
+    else:
+        delta = huber_delta(acts[-1], actions, targets, huber)
     gw = [None] * len(spec.layers)
     gb = [None] * len(spec.layers)
     for k in range(last, -1, -1):
+        gb_src = delta
+        if store is not None and k < last:
+            # the stored (bf16) data gradient feeds this layer's weight gradient and the
+            # next data gradient; fc1's bias gradient sums the fp32 values
+            delta = store.delta(k, delta)
+            if k < last - 1:
+                gb_src = delta
         gw[k] = K.weight_grad(delta, rows[k])
-        gb[k] = K.bias_grad(delta)
+        gb[k] = K.bias_grad(gb_src)
         if k == 0:
             break
         L = spec.layers[k]
         in_shape = shapes[k][0]
         prev_pre = pres[k - 1].reshape(n, -1)
+        if store is not None:
+            prev_pre = store.relu_mask(k - 1, pres[k - 1]).reshape(n, -1).astype(np.float64)
         if L.kind == "fc":
-            delta = K.hidden_delta(delta, p.weights[k], prev_pre)
+            delta = K.hidden_delta(delta, weights[k], prev_pre)
         else:
-            dpatch = K.hidden_delta(delta, p.weights[k], np.ones_like(rows[k]))
-            dx = col2im(dpatch, L, in_shape, n)
+            dpatch = K.hidden_delta(delta, weights[k], np.ones_like(rows[k]))
+            dx = (col2im_fast if K is not _K_EXACT and not L.planar else col2im)(
+                dpatch, L, in_shape, n)
             dx = dx * (prev_pre > 0.0)
             delta = dx
         # delta rows for layer k-1: pixels x channels for a conv, samples x units for fc
@@ -260,8 +411,9 @@ def gradient(spec: NetSpec, p: Params, states, actions, targets):
     return Params(gw, gb)
 
 
-def rmsprop_step(opt: Opt, p: Params, g: Params, lr=2.5e-4, rho=0.95, kappa=0.01):
+def rmsprop_step(opt: Opt, p: Params, g: Params, lr=2.5e-4, rho=0.95, kappa=0.01, K=None):
     """nn.rmsprop_step (nn.py:173-203)."""
+    K = K or _K_EXACT
     for a in g.weights + g.biases:
         if not np.all(np.isfinite(a)):
             raise ValueError("gradient contains non-finite entries")
@@ -281,9 +433,10 @@ def rmsprop_step(opt: Opt, p: Params, g: Params, lr=2.5e-4, rho=0.95, kappa=0.01
     return Params(nw, nb), Opt(nmw, nmb, nvw, nvb, opt.step + 1)
 
 
-def td_targets(spec, target: Params, rewards, next_states, terminals, gamma):
+def td_targets(spec, target: Params, rewards, next_states, terminals, gamma, K=None,
+               store=None):
     """agent.td_targets (agent.py:69-81)."""
-    q_next = forward(spec, target, next_states)
+    q_next = forward(spec, target, next_states, K, store)
     out = np.empty(len(rewards), dtype=np.float64)
     for i in range(len(rewards)):
         r = float(rewards[i])
@@ -292,22 +445,24 @@ def td_targets(spec, target: Params, rewards, next_states, terminals, gamma):
 
 
 def train_minibatch(spec, theta: Params, opt: Opt, batch, target: Params, gamma,
-                    lr=2.5e-4, rho=0.95, kappa=0.01, *, return_grad=False):
+                    lr=2.5e-4, rho=0.95, kappa=0.01, *, return_grad=False, K=None, store=None,
+                    huber=None, target_store=None):
     """agent.train_minibatch (agent.py:84-105).  batch = (states, actions, rewards,
     next_states, terminals) as arrays."""
     states, actions, rewards, next_states, terminals = batch
-    targets = td_targets(spec, target, rewards, next_states, terminals, gamma)
-    g = gradient(spec, theta, states, actions, targets)
+    targets = td_targets(spec, target, rewards, next_states, terminals, gamma, K,
+                         target_store if target_store is not None else store)
+    g = gradient(spec, theta, states, actions, targets, K, store, huber)
     n = float(len(actions))
     summed = Params([w * n for w in g.weights], [b * n for b in g.biases])
-    p2, o2 = rmsprop_step(opt, theta, summed, lr, rho, kappa)
+    p2, o2 = rmsprop_step(opt, theta, summed, lr, rho, kappa, K)
     if return_grad:
         return p2, o2, summed, targets
     return p2, o2
 
 
-def loss_value(spec, p, states, actions, targets):
-    q = forward(spec, p, states)
+def loss_value(spec, p, states, actions, targets, K=None):
+    q = forward(spec, p, states, K)
     err = targets - q[np.arange(len(actions)), actions]
     return float(np.mean(0.5 * err ** 2))
 

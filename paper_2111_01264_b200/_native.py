@@ -46,7 +46,7 @@ class PqLearnArgs(C.Structure):
         ("n", C.c_int), ("actions", C.c_int),
         ("gamma", C.c_float), ("lr", C.c_float), ("rho", C.c_float), ("kappa", C.c_float),
         ("nonfinite", vp), ("grad_out", vp), ("q_out", vp), ("td_out", vp),
-        ("ws", vp), ("max_batch", C.c_int),
+        ("ws", vp), ("max_batch", C.c_int), ("huber", C.c_float),
     ]
 
 
@@ -72,6 +72,8 @@ EXPORTS = {
     "pq_sample_indices": ([vp, C.c_uint32, C.c_int64, vp, vp], C.c_int),
     "pq_replay_gather": ([vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp], C.c_int),
     "pq_replay_flush": ([vp, C.c_int, C.c_int, vp, C.c_int64, C.c_int64, vp], C.c_int),
+    "pq_replay_flush_range": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int64, C.c_int64,
+                               vp], C.c_int),
     "pq_env_reset": ([PqEnvs, C.c_int, vp, vp, vp], C.c_int),
     "pq_prepopulate": ([vp, C.c_uint64, C.c_int, C.c_int, C.c_double, C.c_int64, vp, C.c_int64,
                         C.c_int64, vp, vp, vp, vp], C.c_int),

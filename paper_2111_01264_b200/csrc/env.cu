@@ -155,7 +155,9 @@ __global__ void __launch_bounds__(256) k_act_env(const ActArgs a) {
         const bool trunc = !term && t >= a.L;
         int4 *rec = reinterpret_cast<int4 *>(a.staging + ((int64_t)j * a.steps + b) * REC_INTS);
         rec[0] = make_int4(st4[0], st4[1], st4[2], st4[3]);
-        rec[1] = make_int4(fs, act, __float_as_int((float)reward), term ? 1 : 0);
+        int32_t hi[3];
+        rec_pack(hi, act, term, reward);
+        rec[1] = make_int4(fs, hi[0], hi[1], hi[2]);
         double ret = ret0 + reward;
         s_slot[1] = -1;
         int4 nst;

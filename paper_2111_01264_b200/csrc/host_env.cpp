@@ -126,11 +126,11 @@ int pq_henv_step(pq_henv *e, int W, const float *q, int A, int episode_length, d
         const bool trunc = !term && t >= episode_length;
         int32_t *rec = records + (size_t)j * PQ_REC_INTS;
         int32_t *st = stacks + j * 4;
-        float rf = (float)reward;
-        int32_t rbits;
-        memcpy(&rbits, &rf, 4);
+        uint64_t rbits;
+        memcpy(&rbits, &reward, 8);
         rec[0] = st[0], rec[1] = st[1], rec[2] = st[2], rec[3] = st[3], rec[4] = fs;
-        rec[5] = act, rec[6] = rbits, rec[7] = term ? 1 : 0;
+        rec[5] = act | (term ? 1 << 16 : 0);  // action | bootstrap terminal << 16
+        rec[6] = (int32_t)(uint32_t)rbits, rec[7] = (int32_t)(uint32_t)(rbits >> 32);  // f64 reward
         e[j].ep_return += reward;
         if (term || trunc) {
             ep_labels[*n_eps] = t_label;

@@ -32,6 +32,7 @@ struct HeadArgs {
     const float *ext_targets;
     const int32_t *ext_actions;
     float gamma;
+    float huber;  // > 0: Huber TD loss with this delta (dL/dq clipped to [-huber, huber])
     int learner;
     float *q_out;  // [groups][n][A]
     float *h1, *dh1, *td;
@@ -146,27 +147,35 @@ PQ_DEV void head_sample(const HeadArgs &a, int b, Wait wait = Wait{}) {
             act = a.ext_actions[b];
             target = a.ext_targets[b];
         } else {
-            act = rec_hi.y;
-            const float r = __int_as_float(rec_hi.z);
-            if (rec_hi.w) {
-                target = r;
+            act = rec_action(rec_hi.y);
+            // td_targets (agent.py:69-81) in f64 on the f64 reward, rounded once
+            const double r = rec_reward(rec_hi.z, rec_hi.w);
+            if (rec_terminal(rec_hi.y)) {
+                target = (float)r;
             } else {
                 float mx = qs[1][0];
                 for (int aa = 1; aa < a.A; ++aa) mx = fmaxf(mx, qs[1][aa]);
-                target = r + a.gamma * mx;
+                target = (float)(r + (double)a.gamma * (double)mx);
             }
         }
-        float d = qs[0][act] - target;  // = n * output_delta (agent.py:103-104 summed gradient)
+        const float e = qs[0][act] - target;
+        // d = n * output_delta (agent.py:103-104 summed gradient); the opt-in Huber loss
+        // clips it (huber <= 0 or inf: the reference's half-squared loss)
+        float d = e, loss = 0.5f * e * e;
+        if (a.huber > 0.f && fabsf(e) > a.huber) {
+            d = copysignf(a.huber, e);
+            loss = a.huber * (fabsf(e) - 0.5f * a.huber);
+        }
         s_delta = d;
         s_act = act;
         a.act_out[b] = act;
         a.td[b * 3 + 0] = target;
         a.td[b * 3 + 1] = d;
-        a.td[b * 3 + 2] = 0.5f * d * d;
+        a.td[b * 3 + 2] = loss;
         if (a.td_copy) {
             a.td_copy[b * 3 + 0] = target;
             a.td_copy[b * 3 + 1] = d;
-            a.td_copy[b * 3 + 2] = 0.5f * d * d;
+            a.td_copy[b * 3 + 2] = loss;
         }
     }
     __syncthreads();

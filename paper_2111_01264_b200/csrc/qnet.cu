@@ -456,7 +456,7 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
     if (la) {
         h.records = la->records, h.idx = la->idx, h.idx_base = la->idx_base;
         h.counter = la->update_counter, h.ext_targets = la->ext_targets;
-        h.ext_actions = la->ext_actions, h.gamma = la->gamma;
+        h.ext_actions = la->ext_actions, h.gamma = la->gamma, h.huber = la->huber;
         h.q_copy = la->q_out, h.td_copy = la->td_out;
         h.idx_cur = w.idx_cur, h.upd_cur = w.upd_cur;
     }

@@ -12,7 +12,36 @@
 namespace pq {
 
 constexpr int FRAME_BYTES = 84 * 84;  // 7056 = 441 x 16 B
-constexpr int REC_INTS = 8;           // replay record: f0..f4, action, reward bits, terminal
+constexpr int REC_INTS = 8;  // replay record: f0..f4, action | terminal << 16, f64 reward (lo, hi)
+
+// Record fields 5..7: the action (< 32) with the bootstrap terminal in bit 16, then the
+// reward as the two 32-bit halves of its IEEE f64 bits (the reference keeps a Python
+// float, replay.py:19-27).
+__host__ __device__ inline int rec_action(int32_t f5) { return f5 & 0xFFFF; }
+__host__ __device__ inline bool rec_terminal(int32_t f5) { return (f5 >> 16) & 1; }
+#ifdef __CUDACC__
+__host__ __device__ inline double rec_reward(int32_t lo, int32_t hi) {
+#ifdef __CUDA_ARCH__
+    return __hiloint2double(hi, lo);
+#else
+    uint64_t u = ((uint64_t)(uint32_t)hi << 32) | (uint32_t)lo;
+    double d;
+    __builtin_memcpy(&d, &u, 8);
+    return d;
+#endif
+}
+__host__ __device__ inline void rec_pack(int32_t *f5, int action, bool terminal, double reward) {
+#ifdef __CUDA_ARCH__
+    const long long u = __double_as_longlong(reward);
+#else
+    long long u;
+    __builtin_memcpy(&u, &reward, 8);
+#endif
+    f5[0] = action | (terminal ? 1 << 16 : 0);
+    f5[1] = (int32_t)(uint32_t)(unsigned long long)u;
+    f5[2] = (int32_t)(uint32_t)((unsigned long long)u >> 32);
+}
+#endif
 
 constexpr int64_t P_W1 = 0, P_B1 = 8192, P_W2 = 8224, P_B2 = 40992, P_W3 = 41056, P_B3 = 77920,
                   P_W4 = 77984, P_B4 = 1683616, P_W5 = 1684128;

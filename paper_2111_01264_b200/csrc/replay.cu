@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) k_sample_indices(uint64_t *st,
 // loads), write the two 4-frame stacks (masked slots -> zeros)
 __global__ void __launch_bounds__(256) k_gather(const uint8_t *ring, const int32_t *records,
                                                 const int64_t *idx, uint8_t *s_out,
-                                                uint8_t *s2_out, int32_t *a_out, float *r_out,
+                                                uint8_t *s2_out, int32_t *a_out, double *r_out,
                                                 uint8_t *term_out) {
     const int b = blockIdx.x;
     const int32_t *rec = records + idx[b] * REC_INTS;
@@ -144,9 +144,9 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t *ring, const int32
     if (threadIdx.x < REC_INTS) f[threadIdx.x] = rec[threadIdx.x];
     __syncthreads();
     if (threadIdx.x == 0) {
-        a_out[b] = f[5];
-        r_out[b] = __int_as_float(f[6]);
-        term_out[b] = (uint8_t)f[7];
+        a_out[b] = rec_action(f[5]);
+        r_out[b] = rec_reward(f[6], f[7]);
+        term_out[b] = (uint8_t)rec_terminal(f[5]);
     }
     constexpr int V = FRAME_BYTES / 16;  // 441
     uint4 *s4 = reinterpret_cast<uint4 *>(s_out + (size_t)b * 4 * FRAME_BYTES);
@@ -162,12 +162,16 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t *ring, const int32
 }
 
 // ------------------------------------------------------------------ flush
-__global__ void k_flush(const int32_t *staging, int W, int steps, int32_t *records,
+// sampler j's staged steps [k0, k1) -> slots push_count + j * (k1 - k0) + (k - k0)
+// (ReplayMemory.flush, replay.py:82-93: ascending owner id, each chronological)
+__global__ void k_flush(const int32_t *staging, int W, int steps, int k0, int k1, int32_t *records,
                         int64_t capacity, int64_t push_count) {
+    const int len = k1 - k0;
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // owner-major index
-    if (i >= (int64_t)W * steps) return;
+    if (i >= (int64_t)W * len) return;
+    const int64_t j = i / len, k = k0 + (i - j * len);
     int64_t slot = (push_count + i) % capacity;
-    const uint4 *src = reinterpret_cast<const uint4 *>(staging + i * REC_INTS);
+    const uint4 *src = reinterpret_cast<const uint4 *>(staging + (j * steps + k) * REC_INTS);
     uint4 *dst = reinterpret_cast<uint4 *>(records + slot * REC_INTS);
     dst[0] = src[0];
     dst[1] = src[1];
@@ -218,9 +222,8 @@ __global__ void k_prepop_scalar(uint64_t *pcg, int L, int A, double term_p, int6
         bool trunc = !term && t >= L;
         int32_t *r = rec + i * REC_INTS;
         r[0] = stack[0], r[1] = stack[1], r[2] = stack[2], r[3] = stack[3], r[4] = fs;
-        r[5] = a;
-        r[6] = __float_as_int((float)reward);
-        r[7] = term ? 1 : 0;  // bootstrap terminal = terminal and not truncated
+        // action | bootstrap terminal (= terminal and not truncated) << 16, f64 reward
+        rec_pack(r + 5, a, term, reward);
         if (term || trunc) {
             if (i + 1 < n) {
                 episode += 1;
@@ -261,7 +264,7 @@ int pq_sample_indices(uint64_t *pcg_state, uint32_t n, int64_t count, int64_t *i
 }
 
 int pq_replay_gather(const uint8_t *ring, const int32_t *records, const int64_t *idx, int64_t B,
-                     uint8_t *s_out, uint8_t *s2_out, int32_t *a_out, float *r_out,
+                     uint8_t *s_out, uint8_t *s2_out, int32_t *a_out, double *r_out,
                      uint8_t *term_out, void *stream) {
     if (B <= 0) return 0;
     k_gather<<<(unsigned)B, 256, 0, (cudaStream_t)stream>>>(ring, records, idx, s_out, s2_out,
@@ -269,13 +272,19 @@ int pq_replay_gather(const uint8_t *ring, const int32_t *records, const int64_t 
     return cuda_err(cudaGetLastError(), "gather");
 }
 
-int pq_replay_flush(const int32_t *staging, int W, int steps, int32_t *records, int64_t capacity,
-                    int64_t push_count, void *stream) {
-    int64_t total = (int64_t)W * steps;
+int pq_replay_flush_range(const int32_t *staging, int W, int steps, int k0, int k1, int32_t *records,
+                          int64_t capacity, int64_t push_count, void *stream) {
+    if (k0 < 0 || k1 > steps || k0 > k1) return set_err("flush range outside the staged steps");
+    int64_t total = (int64_t)W * (k1 - k0);
     if (total <= 0) return 0;
     k_flush<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        staging, W, steps, records, capacity, push_count);
+        staging, W, steps, k0, k1, records, capacity, push_count);
     return cuda_err(cudaGetLastError(), "flush");
+}
+
+int pq_replay_flush(const int32_t *staging, int W, int steps, int32_t *records, int64_t capacity,
+                    int64_t push_count, void *stream) {
+    return pq_replay_flush_range(staging, W, steps, 0, steps, records, capacity, push_count, stream);
 }
 
 size_t pq_prepopulate_scratch_bytes(int64_t n) { return (size_t)(2 * n + 2) * sizeof(FrameDesc); }

@@ -246,10 +246,19 @@ def forward(params: QNet, states):
     return q
 
 
+def huber_arg(huber) -> float:
+    """The C ABI's Huber knob: 0 = the reference's half-squared TD loss."""
+    if huber is None or huber == float("inf"):
+        return 0.0
+    if not huber > 0:
+        raise ValueError("huber delta must be positive (or None for the squared loss)")
+    return float(huber)
+
+
 def _learn(theta: QNet, opt: OptState, target: QNet | None, ring, records, idx, n,
            gamma=0.99, cfg: OptConfig | None = None, ext_targets=None, ext_actions=None,
            theta_out=None, opt_out=None, want_grad=False, want_q=False, flag=None,
-           update_counter=None, idx_base=None, stream=None):
+           update_counter=None, idx_base=None, stream=None, huber=None):
     torch = _torch()
     cfg = cfg or OptConfig()
     A = theta.actions
@@ -272,7 +281,7 @@ def _learn(theta: QNet, opt: OptState, target: QNet | None, ring, records, idx, 
         ext_targets=N.ptr(ext_targets), ext_actions=N.ptr(ext_actions), n=n, actions=A,
         gamma=gamma, lr=cfg.learning_rate, rho=cfg.rho, kappa=cfg.kappa,
         nonfinite=flag.data_ptr(), grad_out=N.ptr(grad), q_out=N.ptr(qout), td_out=N.ptr(td),
-        ws=ws.data_ptr(), max_batch=cap)
+        ws=ws.data_ptr(), max_batch=cap, huber=huber_arg(huber))
     N.check(N.load().pq_learn_step(ctypes.byref(a), N.stream_ptr(stream)), "learn_step")
     if own_flag and int(flag.item()) != 2**31 - 1:
         raise ValueError("gradient contains non-finite entries")

@@ -3,9 +3,10 @@
 Layout in HBM:
 
 * ``ring``    uint8 [frame_capacity, 7056]: every 84x84 frame stored once;
-* ``records`` int32 [capacity, 8]: per transition {f0, f1, f2, f3, f4, action,
-  reward (f32 bits), bootstrap terminal}; the state is frames f0..f3 and the next
-  state f1..f4 (slot -1 = masked all-zero frame before an episode start).
+* ``records`` int32 [capacity, 8]: per transition {f0, f1, f2, f3, f4,
+  action | bootstrap terminal << 16, reward (f64 bits: lo, hi)}; the state is frames
+  f0..f3 and the next state f1..f4 (slot -1 = masked all-zero frame before an episode
+  start).
 
 Semantics kept from the reference: physical slot of the k-th push is k mod capacity
 (append then overwrite, replay.py:53-59), ``version`` counts every push, ``sample``
@@ -177,8 +178,9 @@ class ReplayMemory:
             self.ring.index_copy_(0, idx, torch.from_numpy(host).cuda())
         if not s2[STACK - 1].any():
             refs[4] = -1
-        rec = np.array(refs + [int(t.action), int(np.float32(t.reward).view(np.int32)),
-                               1 if t.terminal else 0], dtype=np.int32)
+        rec = np.array(refs + [int(t.action) | (1 << 16 if t.terminal else 0), 0, 0],
+                       dtype=np.int32)
+        rec[6:8] = np.array([float(t.reward)], dtype="<f8").view(np.int32)
         valid = [q for q in seqs if q >= 0]
         slot = int(self._advance(1, min(valid) if valid else -1)[0])
         self.records[slot] = torch.from_numpy(rec).cuda()
@@ -216,7 +218,7 @@ class ReplayMemory:
         s = torch.empty((B, STACK, FRAME, FRAME), dtype=torch.uint8, device="cuda")
         s2 = torch.empty_like(s)
         a = torch.empty(B, dtype=torch.int32, device="cuda")
-        r = torch.empty(B, dtype=torch.float32, device="cuda")
+        r = torch.empty(B, dtype=torch.float64, device="cuda")
         term = torch.empty(B, dtype=torch.uint8, device="cuda")
         N.check(N.load().pq_replay_gather(self.ring.data_ptr(), self.records.data_ptr(),
                                           idx.data_ptr(), B, s.data_ptr(), s2.data_ptr(),

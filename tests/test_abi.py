@@ -122,10 +122,10 @@ def test_host_samplers_bit_exact_vs_oracle_env_and_select_action():
             st = OK.pcg_state_from_generator(rngs[j])
             a = OK.select_action(st, q[j].astype(np.float64), epsilon_at(b * W + j + 1, sched))
             OK.pcg_state_to_generator(st, rngs[j])
-            assert a == recs[j, 5]
+            assert a == recs[j, 5] & 0xFFFF
             nxt, rew, done = oenv[j].step(a, rngs[j])
-            assert np.float32(rew).view(np.int32) == recs[j, 6]
-            assert bool(recs[j, 7]) == (done and not oenv[j].truncated)
+            assert np.float64(rew).view(np.int64) == recs[j, 6:8].copy().view(np.int64)[0]
+            assert bool(recs[j, 5] >> 16) == (done and not oenv[j].truncated)
             assert ring[int(recs[j, 4])].tobytes() == nxt[3].tobytes()
             if done:
                 nxt = oenv[j].reset(rngs[j])

@@ -2,12 +2,11 @@
 seeded inputs, through the C ABI.
 
 Bit-exact: replay index sampling (incl. the reference's golden vectors), the
-frame-stack gather, prepopulation, epsilon-greedy draws and the env step.
-Tolerance (bf16 tensor-core arithmetic vs the fp64 oracle, relative Frobenius):
-Q-values <= 1e-2, TD targets <= 1e-2, fc2 gradient <= 2e-2, lower-layer gradients
-<= 0.2 -- bf16 weight rounding flips ~0.1% of the ReLU masks and, at batch 32, that
-moves the conv/fc1 gradients by ~7% exactly as 0.2% fp64 weight noise does
-(tests/test_oracle.py::test_gradient_conditioning_under_weight_noise documents it).
+frame-stack gather (f64 rewards), prepopulation, epsilon-greedy draws and the env step.
+Tolerance (bf16 tensor-core arithmetic vs the fp64 oracle with the device's storage
+model, relative Frobenius): Q-values and TD targets <= 1e-3; stage outputs <= 1e-3;
+every layer's gradient, the post-RMSProp update and the moments <= 1e-5 on identical
+stage inputs (see the section comment below).
 """
 
 import os
@@ -30,7 +29,8 @@ from paper_2111_01264_b200.replay import ReplayMemory, Transition, device_pcg, \
     sample_indices_device  # noqa: E402
 
 from oracle import _lib as OK  # noqa: E402
-from oracle import natcnn, replay as oreplay  # noqa: E402
+from oracle import blas, natcnn, replay as oreplay  # noqa: E402
+import devtap  # noqa: E402
 from oracle.envs import SyntheticFrameEnv  # noqa: E402
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -102,7 +102,7 @@ def test_gather_bit_exact_vs_oracle_host_push():
     ref = oreplay.gather(ora.sample(64, r2))
     assert np.array_equal(s.cpu().numpy(), ref[0])
     assert np.array_equal(a.cpu().numpy(), ref[1])
-    assert np.array_equal(r.cpu().numpy(), ref[2].astype(np.float32))
+    assert np.array_equal(r.cpu().numpy(), ref[2])
     assert np.array_equal(s2.cpu().numpy(), ref[3])
     assert np.array_equal(term.cpu().numpy().astype(bool), ref[4])
 
@@ -145,58 +145,163 @@ def test_device_prepopulate_bit_exact_vs_oracle():
     assert np.array_equal(s.cpu().numpy(), ref[0])
     assert np.array_equal(s2.cpu().numpy(), ref[3])
     assert np.array_equal(a.cpu().numpy(), ref[1])
-    assert np.array_equal(r.cpu().numpy(), ref[2].astype(np.float32))
+    assert np.array_equal(r.cpu().numpy(), ref[2])
     assert np.array_equal(term.cpu().numpy().astype(bool), ref[4])
 
 
 # --- Q network vs the fp64 oracle ----------------------------------------------------------
+#
+# Tolerances (north star: "rel 1e-3 for bf16"), relative Frobenius, on identical weights
+# and minibatches.  The oracle (oracle/natcnn.py, the reference arithmetic in fp64) runs
+# with the device's storage model (natcnn.Bf16Storage: bf16 W1..W4, bf16 conv
+# activations and data gradients) so the comparison is well posed:
+#   * chained (the oracle rounds its own values): Q-values of both networks and the TD
+#     targets <= 1e-3 (measured ~2e-4);
+#   * per stage, teacher-forced (each oracle stage reads the device's stored bf16 input
+#     of that stage and its ReLU masks): every stored tensor equals the oracle's value
+#     rounded to bf16 within 1e-3 (measured <= 6e-5), and every layer's weight and bias
+#     gradient, the post-RMSProp parameter update and the moments within 1e-5, the
+#     north star's fp32 bar (measured 2e-8 .. 2e-6 at batch 32 / 256 / 1024).  Chained gradients are not a well-posed comparison: a bf16
+#     value within the accumulation error of a rounding boundary lands one ulp (2^-8)
+#     away, and a ReLU pre-activation within it flips a whole unit's gradient
+#     (natcnn.Bf16Storage docstring).
 
-def _nets(seed):
+RTOL_BF16 = 1e-3   # north star: bf16 arithmetic
+RTOL_STAGE = 1e-5  # teacher-forced gradients / update (fp32 accumulation on equal inputs)
+
+
+def _nets(seed, bias_scale=0.0):
     spec = natcnn.nature_cnn(A)
     p = natcnn.init_params(spec, seed)
+    if bias_scale:
+        brng = np.random.default_rng(seed + 100)
+        for b in p.biases:
+            b[:] = brng.normal(scale=bias_scale, size=b.shape)
     flat = np.concatenate([np.r_[w.ravel(), b] for w, b in zip(p.weights, p.biases)])
-    return spec, p, dnn.QNet.from_flat(flat, A)
+    net = dnn.QNet.from_flat(flat, A)
+    # the oracle runs on the device's fp32 master values
+    dp = dnn.Parameters.from_flat(net.flat(), A)
+    return spec, natcnn.Params(dp.weights, dp.biases), net
 
 
-def test_forward_vs_oracle():
-    spec, p, net = _nets(11)
-    x = np.random.default_rng(0).integers(0, 256, size=(32, 4, 84, 84), dtype=np.uint8)
+def _flat(p):
+    return np.concatenate([np.r_[w.ravel(), b] for w, b in zip(p.weights, p.biases)])
+
+
+@pytest.mark.parametrize("W", [8, 128, 512])
+def test_forward_vs_oracle_bf16_faithful(W):
+    """Batched acting inference (configs[2] widths) vs the oracle forward."""
+    spec, p, net = _nets(11, bias_scale=0.05)
+    x = np.random.default_rng(W).integers(0, 256, size=(W, 4, 84, 84), dtype=np.uint8)
     q = dnn.forward(net, x)
-    assert rel(q, natcnn.forward(spec, p, x)) < 1e-2
+    ref = natcnn.forward(spec, p, x, K=blas, store=natcnn.Bf16Storage())
+    e = rel(q, ref)
+    print(f"forward W={W}: rel {e:.2e}")
+    assert e < RTOL_BF16
 
 
-def test_train_minibatch_vs_oracle():
-    spec, p, theta = _nets(3)
-    _, pt, target = _nets(4)
-    env = SyntheticFrameEnv(21, episode_length=30, action_count=A)
-    mem, ora = ReplayMemory(200), oreplay.ReplayMemory(200)
-    mem.prepopulate(env, 150, np.random.default_rng(1))
-    ora.prepopulate(SyntheticFrameEnv(21, episode_length=30, action_count=A), 150,
+def _learner_case(B, seed=3, huber=None):
+    spec, p, theta = _nets(seed, bias_scale=0.05)
+    _, pt, target = _nets(seed + 1, bias_scale=0.05)
+    n = max(2 * B, 300)
+    env = FrameEnvSpec(key=21 + B, episode_length=30, action_count=A)
+    mem = ReplayMemory(n)
+    mem.prepopulate(env, n, np.random.default_rng(1))
+    ora = oreplay.ReplayMemory(n)
+    ora.prepopulate(SyntheticFrameEnv(21 + B, episode_length=30, action_count=A), n,
                     np.random.default_rng(1))
-    batch = mem.sample(32, np.random.default_rng(5))
-    obatch = oreplay.gather(ora.sample(32, np.random.default_rng(5)))
-    # oracle with the GPU's fp32-stored rewards
-    obatch = (obatch[0], obatch[1], obatch[2].astype(np.float32).astype(np.float64), obatch[3],
-              obatch[4])
-    op = natcnn.Opt.zeros(p)
-    p2, o2, g_ref, t_ref = natcnn.train_minibatch(spec, p, op, obatch, pt, 0.99, return_grad=True)
-    th2, op2, grad, qout, td = dnn._learn(theta, dnn.OptState.zeros(theta), target, mem.ring,
-                                          mem.records, batch.idx, 32, gamma=0.99,
-                                          want_grad=True, want_q=True)
-    qo = natcnn.forward(spec, p, obatch[0])
-    assert rel(qout[0].cpu().numpy(), qo) < 1e-2
-    assert rel(td[:, 0].cpu().numpy(), t_ref) < 1e-2
-    g = grad.cpu().numpy()
-    gref = np.concatenate([np.r_[w.ravel(), b] for w, b in zip(g_ref.weights, g_ref.biases)])
+    batch = mem.sample(B, np.random.default_rng(5))
+    obatch = oreplay.gather(ora.sample(B, np.random.default_rng(5)))
+    opt = dnn.OptState.zeros(theta)
+    g = torch.Generator(device="cuda").manual_seed(B)
+    opt.m.copy_(torch.randn(opt.m.shape, device="cuda", generator=g) * 1e-3)
+    opt.v.copy_(opt.m * opt.m + torch.rand(opt.v.shape, device="cuda", generator=g) * 1e-4)
+    m0 = dnn.Parameters.from_flat(opt.m.cpu().numpy().astype(np.float64), A)
+    v0 = dnn.Parameters.from_flat(opt.v.cpu().numpy().astype(np.float64), A)
+    oopt = natcnn.Opt(m0.weights, m0.biases, v0.weights, v0.biases)
+    th2, op2, grad, qout, td = dnn._learn(theta, opt, target, mem.ring, mem.records, batch.idx,
+                                          B, gamma=0.99, want_grad=True, want_q=True,
+                                          huber=huber)
+    taps = devtap.learner_taps(B, A)
+    return dict(spec=spec, p=p, pt=pt, theta=theta, obatch=obatch, oopt=oopt, th2=th2,
+                op2=op2, grad=grad.cpu().numpy().astype(np.float64),
+                qout=qout.cpu().numpy().astype(np.float64),
+                td=td.cpu().numpy().astype(np.float64), taps=taps)
+
+
+def _forced_stores(taps, B):
+    """Teacher-forced storage models from the device taps.  The device's data gradients
+    are those of the summed loss (agent.py:103-104 feeds the optimizer n x the mean
+    gradient, and the device never divides); the oracle's chain is nn.gradient's mean
+    loss, so they enter scaled by 1/n (exact: B is a power of two)."""
+    on = natcnn.Bf16Storage(masks=[None, None, None, taps["h1"] > 0, None], acts=taps["online"],
+                            deltas={k: v / B for k, v in taps["deltas"].items()})
+    return on, natcnn.Bf16Storage(acts=taps["target"])
+
+
+@pytest.mark.parametrize("B", [32, 256, 1024])
+def test_learner_step_vs_oracle_bf16_faithful(B):
+    """agent.train_minibatch (agent.py:84-105) on the GPU vs the fp64 oracle: batch 32
+    runs the cp.async / fused small-batch schedule, 256 and 1024 the TMA and
+    shifted-descriptor kernels."""
+    c = _learner_case(B)
+    spec, p, pt, obatch, taps = c["spec"], c["p"], c["pt"], c["obatch"], c["taps"]
+    s, a, r, s2, term = obatch
+    # -- chained: the oracle rounds its own values where the device stores bf16
+    q_on = natcnn.forward(spec, p, s, K=blas, store=natcnn.Bf16Storage())
+    q_tg = natcnn.forward(spec, pt, s2, K=blas, store=natcnn.Bf16Storage())
+    t_ref = natcnn.td_targets(spec, pt, r, s2, term, 0.99, K=blas, store=natcnn.Bf16Storage())
+    errs = {"Q": rel(c["qout"][0], q_on), "Q_target": rel(c["qout"][1], q_tg),
+            "td_target": rel(c["td"][:, 0], t_ref)}
+    # -- teacher-forced: every stage on the device's stored inputs and masks
+    st_on, st_tg = _forced_stores(taps, B)
+    p2, o2, g_ref, t_forced = natcnn.train_minibatch(spec, p, c["oopt"], obatch, pt, 0.99,
+                                                     return_grad=True, K=blas, store=st_on,
+                                                     target_store=st_tg)
+    errs["td_target_forced"] = rel(c["td"][:, 0], t_forced)
+    for key, val in sorted(st_on.seen.items()):
+        if key[0] == "act":
+            dev, mine = taps["online"][key[1]], val
+        else:  # the device's data gradients carry the summed-loss scale (x n)
+            dev, mine = taps["deltas"][key[1]], val * B
+        errs[f"stage_{key[0]}{key[1]}"] = rel(dev.reshape(-1), natcnn.bf16_round(mine).reshape(-1))
+    for key, val in sorted(st_tg.seen.items()):
+        errs[f"stage_target_{key[0]}{key[1]}"] = rel(taps["target"][key[1]].reshape(-1),
+                                                     natcnn.bf16_round(val).reshape(-1))
     offs = np.cumsum([0] + [o * i + o for o, i in dnn.layer_shapes(A)])
-    for k in range(5):
-        e = rel(g[offs[k]:offs[k + 1]], gref[offs[k]:offs[k + 1]])
-        assert e < (2e-2 if k == 4 else 0.2), (k, e)
-    new = th2.flat()
-    pref = np.concatenate([np.r_[w.ravel(), b] for w, b in zip(p2.weights, p2.biases)])
-    old = np.concatenate([np.r_[w.ravel(), b] for w, b in zip(p.weights, p.biases)])
-    assert rel(new - old, pref - old) < 0.2
-    assert np.abs(new - pref).max() < 1e-3
+    for k, (o, i) in enumerate(dnn.layer_shapes(A)):
+        gw = c["grad"][offs[k]:offs[k] + o * i]
+        gb = c["grad"][offs[k] + o * i:offs[k + 1]]
+        errs[f"grad_w{k + 1}"] = rel(gw, g_ref.weights[k].ravel())
+        errs[f"grad_b{k + 1}"] = rel(gb, g_ref.biases[k])
+    old = _flat(p)
+    errs["dtheta"] = rel(c["th2"].flat() - old, _flat(p2) - old)
+    errs["m"] = rel(c["op2"].m.cpu().numpy(), _flat(natcnn.Params(o2.m_weights, o2.m_biases)))
+    errs["v"] = rel(c["op2"].v.cpu().numpy(), _flat(natcnn.Params(o2.v_weights, o2.v_biases)))
+    print(f"learner B={B}: " + ", ".join(f"{k} {v:.1e}" for k, v in errs.items()))
+    for k, v in errs.items():
+        bound = RTOL_STAGE if k.startswith(("grad", "dtheta", "m", "v", "td_target_")) \
+            else RTOL_BF16
+        assert v < bound, (k, v, bound)
+
+
+@pytest.mark.parametrize("huber", [0.5, 2.0])
+def test_learner_step_huber_vs_oracle(huber):
+    """Opt-in Huber TD loss (north star): dL/dq clipped to [-delta, delta]; the default
+    (huber unset) is the reference's half-squared loss (nn.py:140-144)."""
+    B = 32
+    c = _learner_case(B, seed=5, huber=huber)
+    taps = c["taps"]
+    d_dev = c["td"][:, 1]
+    assert np.all(np.abs(d_dev) <= huber + 1e-7)
+    assert np.any(np.abs(d_dev) == np.float32(huber)), "no clipped sample: pick a smaller delta"
+    st_on, st_tg = _forced_stores(taps, B)
+    p2, _, g_ref, _ = natcnn.train_minibatch(c["spec"], c["p"], c["oopt"], c["obatch"], c["pt"],
+                                             0.99, return_grad=True, K=blas, store=st_on,
+                                             target_store=st_tg, huber=huber)
+    assert rel(c["grad"], _flat(g_ref)) < RTOL_STAGE
+    old = _flat(c["p"])
+    assert rel(c["th2"].flat() - old, _flat(p2) - old) < RTOL_STAGE
 
 
 def test_train_minibatch_leaves_target_untouched():

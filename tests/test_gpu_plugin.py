@@ -43,7 +43,7 @@ def test_reference_mlp_composition_on_b200_plugin_bit_exact(monkeypatch):
     mlp.npz) reproduced with the B200 kernel module swapped in for the kernels."""
     from oracle import natcnn as nc
 
-    monkeypatch.setattr(nc, "K", K)
+    monkeypatch.setattr(nc, "_K_EXACT", K)
     g = np.load(os.path.join(GOLD, "mlp.npz"))
     spec = nc.mlp([6, 9, 5, 4])
     theta = nc.Params([g[f"theta_w{k}"] for k in range(3)], [g[f"theta_b{k}"] for k in range(3)])
