@@ -180,24 +180,6 @@ int pq_learn_grad(const pq_learn_args *args, float *grad, void *stream);
 int pq_rmsprop_apply(pq_net theta, pq_opt opt, const float *grad, int actions, float lr, float rho,
                      float kappa, int32_t *nonfinite, int update_id, void *stream);
 
-/* Persistent learner: n_updates consecutive learner steps of an epoch in ONE launch
- * (one CTA per SM minus an acting reserve, grid barriers between the step's phases).
- * Same arithmetic as n_updates pq_learn_step calls over idx_base sliced by
- * *update_counter (fp32 split-K order aside); updates theta / opt in place
- * (theta_out == theta, opt_out == opt), needs idx_base + update_counter, no
- * ext_targets.  ws: pq_plearn_workspace_bytes(max_batch, actions) bytes.
- * Replaces the executor.py:421-447 trainer loop (train_one x C/F per epoch). */
-size_t pq_plearn_workspace_bytes(int max_batch, int actions);
-int pq_learn_run(const pq_learn_args *args, int n_updates, void *stream);
-/* CTAs of the persistent learner (0 = SM count minus 20 kept for acting). */
-int pq_plearn_set_ctas(int ctas);
-/* Latency probe: device buffer u64 [phases][ctas][4] receiving, per phase and CTA, the
- * %globaltimer when its jobs finished, when the grid barrier released, the type of its
- * last job and that job's duration in ns (NULL = off). */
-int pq_plearn_trace(unsigned long long *device_buf);
-/* GEMM-tile phase probes of the persistent learner's CTA 0 (layout of pq_timeline). */
-int pq_plearn_timeline(int on, unsigned long long *out, int *count);
-
 typedef struct pq_act_args {
     pq_net net;                 /* acting parameters (theta-minus when concurrent) */
     pq_envs envs;

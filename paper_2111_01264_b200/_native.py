@@ -89,11 +89,6 @@ EXPORTS = {
     "pq_learn_grad": ([C.POINTER(PqLearnArgs), vp, vp], C.c_int),
     "pq_rmsprop_apply": ([PqNet, PqOpt, vp, C.c_int, C.c_float, C.c_float, C.c_float, vp, C.c_int, vp],
                          C.c_int),
-    "pq_plearn_workspace_bytes": ([C.c_int, C.c_int], C.c_size_t),
-    "pq_learn_run": ([C.POINTER(PqLearnArgs), C.c_int, vp], C.c_int),
-    "pq_plearn_set_ctas": ([C.c_int], C.c_int),
-    "pq_plearn_trace": ([vp], C.c_int),
-    "pq_plearn_timeline": ([C.c_int, vp, vp], C.c_int),
     "pq_rmsprop_f32": ([vp, vp, vp, vp, C.c_int64, C.c_float, C.c_float, C.c_float, vp, vp, vp,
                         vp, vp], C.c_int),
     "pq_henv_reset": ([vp, C.c_int, vp, C.c_int64, vp, vp], C.c_int),

@@ -1,44 +1,17 @@
-// Persistent DQN learner: many learner steps (agent.train_minibatch, agent.py:84-105)
-// in ONE launch of one 256-thread CTA per SM, every GEMM operand moved by TMA.
+// TMA-engine learner GEMMs (agent.train_minibatch, agent.py:84-105; nn.gradient,
+// nn.py:134-170) for the CUDA-graph learner step of qnet.cu at batch >= 128:
 //
-// A batch-32 step is ~2 GFLOP spread over ten dependent GEMM-shaped stages.  As separate
-// launches with per-thread cp.async gathers it is a chain of launch / drain latencies and
-// of instruction-bound operand address generation (IPC ~1, ~235 SASS instructions per
-// warp per K-chunk; profiles/r1_v9_summary.md).  Here:
-//
-//  * every CTA keeps its TMEM accumulator, operand ring and mbarriers for the whole
-//    launch; the stages of a step are PHASES separated by a grid barrier; each phase is
-//    a list of jobs (GEMM tiles, head samples, optimizer slices, frame gathers) dealt
-//    round-robin to the CTAs;
-//  * every GEMM operand is a dense row-major matrix fetched by cp.async.bulk.tensor
-//    (128B-swizzled 64x64 boxes, one thread issues a K-chunk's 2-3 boxes): the im2col
-//    matrices of conv2 / conv3 and of the two transposed convolutions are SCATTERED by
-//    the epilogue that produces the activation / gradient (each element lands in the
-//    <= 9 patch rows it belongs to), and the conv1 patch matrix of the sampled uint8
-//    frame stacks is built by a gather job ahead of time (the epoch's indices are known);
-//    bias gradients ride on a constant ones column of those matrices;
-//  * the mainloop is warp-specialised: thread 0 produces (empty -> expect_tx -> TMA),
-//    thread 32 issues tcgen05.mma and commits to the slot's empty barrier and to the
-//    accumulator barrier, all 8 warps run the epilogue from TMEM;
-//  * work off the critical chain rides in the idle CTAs of other phases: the
-//    target-network forward of step u+1 (theta-minus and the indices are fixed for the
-//    launch), the frame gathers of steps u+1 / u+2, and the fc1 weight gradient + fused
-//    RMSProp (196 tiles, the HBM-heavy stage) spread over phases 6-9 of step u and 0-2
-//    of step u+1 (act3 double-buffered by step parity).
-//
-// Phase plan of step u (critical job first, fillers after):
-//   P0 F1 online conv1            | fc1 wgrad+RMS (u-1)
-//   P1 F2 online conv2            | F1 target (u+1) | fc1 wgrad+RMS (u-1)
-//   P2 F3 online conv3            | F2 target (u+1) | fc1 wgrad+RMS (u-1)
-//   P3 F4 online fc1 (split-K)    | F3 target (u+1)
-//   P4 head (fc2, TD target, delta, fc2 back-prop) | F4 target (u+1)
-//   P5 fc1 dgrad                  | fc2 / fc1-bias RMSProp | frame gather target (u+2)
-//   P6 conv3 dgrad, conv3 wgrad   | fc1 wgrad+RMS
-//   P7 conv2 dgrad, conv2 wgrad   | fc1 wgrad+RMS
-//   P8 conv1 wgrad                | fc1 wgrad+RMS
-//   P9 conv1/2/3 RMSProp          | frame gather online (u+1) | fc1 wgrad+RMS
-// The arithmetic of each stage is the one-shot path's (same K order, epilogues, head and
-// optimizer functions); the two agree to fp32 split-K summation order.
+//  * k_tma_gemm: warp-specialised persistent tile loop over ONE GEMM -- a producer warp
+//    streams cp.async.bulk.tensor boxes (tiled, or hardware im2col of NHWC activations /
+//    gradients / space-to-depth frame stacks) into a 6-slot mbarrier ring across tiles, one
+//    thread issues tcgen05.mma into two alternating TMEM accumulators, four epilogue warps
+//    drain tile t while tile t+1 computes;
+//  * k_resident_a: fc1 forward / data gradient with the A operand resident in shared memory;
+//  * k_conv1_shift, k_conv_shift<2/3>, k_conv{1,2}_wgrad_shift, k_conv{2,3}_dgrad_shift:
+//    every convolution as row-shifted UMMA descriptors over one TMA box of a
+//    space-to-depth / zero-padded pixel grid (no im2col), MMAs in the im2col K order so the
+//    results are bit-identical to the cp.async engine of gemm.cuh;
+//  * k_frames_s2d: the sampled uint8 frame stacks as a space-to-depth bf16 NHWC tensor.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -58,147 +31,9 @@ int cuda_err(cudaError_t e, const char *where);
         if (_rc) return _rc;               \
     } while (0)
 
-constexpr int PL_STAGES = 8;
 constexpr int PL_SLOT = 24 * 1024;  // A: two 8 KB boxes, B: one 8 KB box
 constexpr int PL_B_OFF = 16 * 1024;
-constexpr int PL_SMEM = PL_STAGES * PL_SLOT + 1024;
 constexpr int PL_BOX = 8192;        // one 64 x 64 bf16 box, 128B-swizzled
-constexpr int PL_FC1_KC = 3;        // fc1 forward: 49 K-chunks in 17 splits
-constexpr int PL_FC1_SPLITS = (49 + PL_FC1_KC - 1) / PL_FC1_KC;
-constexpr int PL_OPT_PER_JOB = 256;  // parameters per optimizer job (one per thread)
-// padded widths of the patch matrices (bf16 elements; 16-byte row strides)
-constexpr int P1_LD = 320, P2_LD = 576;
-
-enum Job : int16_t {
-    J_F1, J_F2, J_F3, J_F4, J_HEAD, J_B4D, J_OPT_FC2, J_B3D, J_B3W, J_B4W, J_B2D, J_B2W,
-    J_OPT_C3, J_B1W, J_OPT_C2, J_OPT_C1, J_G1, J_COUNT
-};
-
-// tensor maps
-enum Map {
-    M_W1 = 0, M_W2 = 2, M_W3 = 4, M_W4 = 6,  // [g]
-    M_ACT3 = 8,                              // [g][par]
-    M_P1 = 12,                               // [g][par]
-    M_P2 = 16, M_ACT2I = 18,                 // [g]  ACT2I: im2col map of act2, 128 pixels
-    M_ACT2W = 20,                            // im2col map of act2 (online), 64 pixels (wgrad)
-    M_DY3I, M_DY2I, M_ONES, M_DH1, M_DH1T, M_DY3, M_DY2, M_DY1, M_W3V, M_W2V, M_COUNT
-};
-
-struct Seg {
-    int16_t type;
-    int8_t grp;     // 0 online, 1 target (forward / gather jobs)
-    int8_t du;      // step offset of the job relative to the running step
-    int16_t filler; // off the step's critical chain: dealt to the CTAs without a critical job
-    int16_t pad;
-    int32_t begin, end;
-};
-constexpr int PL_MAX_PHASES = 12, PL_MAX_SEGS = 8;
-struct PhasePlan {
-    int nseg;
-    Seg seg[PL_MAX_SEGS];
-};
-struct Sched {
-    int nphases;
-    PhasePlan ph[PL_MAX_PHASES];
-};
-enum { SCHED_PROLOGUE = 0, SCHED_STEADY = 1, SCHED_LAST = 2 };
-
-struct PLearnArgs {
-    CUtensorMap maps[M_COUNT];
-    pq_net theta, target;
-    pq_opt opt;
-    const uint8_t *ring;
-    const int32_t *records;
-    const int64_t *idx_base;  // [updates][n] epoch index table
-    int32_t *update_counter;  // first step id of the launch; += n_updates at the end
-    int n, A, n8, n_updates;
-    float gamma, lr, rho, kappa;
-    int32_t *nonfinite;
-    float *grad_out, *q_out, *td_out;  // optional (values of the last step)
-    // workspace
-    bf16 *wsb;  // base of the workspace (lowest buffer)
-    bf16 *act1, *act2[2], *act3[2][2];
-    bf16 *ones;  // [64][64], column 0 = 1: the bias-gradient atom of the conv3 wgrad
-    bf16 *P1[2][2], *P2[2];
-    float *fc1part[2][2];
-    float *q, *h1, *dh1, *td;
-    bf16 *dh1_bf, *dh1T;
-    int32_t *act;
-    bf16 *dY3, *dY2, *dY1;
-    float *part1, *part2, *part3;
-    int s1, s2, s3, kc1, kc2, kc3;
-    unsigned *bar;
-    unsigned long long *trace;  // optional [phases run][gridDim][4]: jobs done, barrier passed, last job type, its ns
-    Sched sched[3];
-};
-
-// ------------------------------------------------------------------ job counts
-struct Counts {
-    int t1, t2, t3, nt64, mt128, tpc;
-};
-__host__ __device__ inline Counts counts_of(int n) {
-    Counts c;
-    c.t1 = (n * 400 + 127) / 128;
-    c.t2 = (n * 81 + 127) / 128;
-    c.t3 = (n * 49 + 127) / 128;
-    c.nt64 = (n + 63) / 64;
-    c.mt128 = (n + 127) / 128;
-    c.tpc = (n * 100 + 127) / 128;
-    return c;
-}
-__host__ __device__ inline int64_t opt_lo(int type) {
-    return type == J_OPT_C1 ? P_W1 : type == J_OPT_C2 ? P_W2 : type == J_OPT_C3 ? P_W3 : P_B4;
-}
-__host__ __device__ inline int64_t opt_hi(int type, int A) {
-    return type == J_OPT_C1 ? P_W2 : type == J_OPT_C2 ? P_W3 : type == J_OPT_C3 ? P_W4 : n_params(A);
-}
-__host__ __device__ inline int njobs(int type, int n, int A, int s1, int s2, int s3) {
-    const Counts c = counts_of(n);
-    switch (type) {
-        case J_F1: return c.t1;
-        case J_F2: return c.t2;
-        case J_F3: return c.t3;
-        case J_F4: return 4 * c.nt64 * PL_FC1_SPLITS;
-        case J_HEAD: return n;
-        case J_B4D: return c.mt128 * 49;
-        case J_B3D: return c.t2;
-        case J_B3W: return 5 * s3;
-        case J_B4W: return 4 * 49;
-        case J_B2D: return 4 * c.tpc;
-        case J_B2W: return 5 * s2;
-        case J_B1W: return 3 * s1;
-        case J_G1: return 4 * n;  // quarter samples (100 patch rows each)
-        default: return (int)((opt_hi(type, A) - opt_lo(type) + PL_OPT_PER_JOB - 1) / PL_OPT_PER_JOB);
-    }
-}
-
-// ------------------------------------------------------------------ grid barrier
-// Monotonic arrival counter (zeroed before the launch); the k-th barrier completes when
-// it reaches k * gridDim.x.  gpu-scope fences on both sides (they also invalidate the
-// SM's L1 so later plain loads see other CTAs' writes).
-PQ_DEV void grid_barrier(unsigned *bar, unsigned &target) {
-    target += gridDim.x;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(bar, 1u);
-        unsigned v;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-        } while (v < target);
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-template <class EP, class = void>
-struct is_scatter {
-    static constexpr bool value = false;
-};
-template <class EP>
-struct is_scatter<EP, decltype((void)EP::NDEST)> {
-    static constexpr bool value = true;
-};
 
 // ------------------------------------------------------------------ TMA GEMM tile
 // One operand of a K-chunk: `boxes` 64x64 boxes of a tiled tensor map, or an im2col
@@ -290,661 +125,6 @@ struct TmaOp {
     }
 };
 
-// latency probe of CTA 0's tiles (pq_plearn_timeline): thread-0 timestamps in shared
-// memory, copied out at the end of the tile
-__shared__ unsigned long long s_tl[8];
-#define PL_PROBE(i)                                                                \
-    do {                                                                           \
-        if (g_tl.on && blockIdx.x == 0 && threadIdx.x == 0) s_tl[i] = gtime(); \
-    } while (0)
-
-struct Pipe {
-    uint8_t *smem;
-    uint32_t smem_s;
-    uint64_t *full, *empty, *acc;
-    uint32_t seq, tiles;
-    const uint32_t *tmem_s;
-};
-
-// 128 x BN tile over K-chunks [kb0, kb1): thread 0 streams the operand boxes into the
-// ring (waiting on each slot's empty barrier), thread 32 issues 4 x tcgen05.mma per
-// chunk and commits the slot back, then the accumulator; all threads run the epilogue.
-template <int BN, bool AMN, bool BMN, class EP>
-PQ_DEV void tma_tile(const TmaOp &A, const TmaOp &B, const EP &ep, int kb0, int kb1, int m0, int n0,
-                     int split, Pipe &P) {
-    constexpr uint32_t IDESC = idesc_bf16(BN, AMN, BMN);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int nk = kb1 > kb0 ? kb1 - kb0 : 0;
-    const uint32_t seq0 = P.seq;
-    const uint32_t tmem = *P.tmem_s;
-    PL_PROBE(0);
-    if (g_tl.on && blockIdx.x == 0 && tid == 0) s_tl[2] = s_tl[3] = 0;
-    if (warp == 0) {  // producer warp: lane 0 arms the slot, every lane may gather
-        const uint32_t bytes = (uint32_t)(A.boxes + B.boxes) * PL_BOX;
-        for (int i = 0; i < nk; ++i) {
-            const uint32_t q = seq0 + i, s = q % PL_STAGES;
-            if (lane == 0) {
-                if (q >= PL_STAGES) mbar_wait(&P.empty[s], ((q / PL_STAGES) - 1) & 1);
-                mbar_expect_tx(&P.full[s], bytes);
-            }
-            const uint32_t dst = P.smem_s + s * PL_SLOT;
-            A.issue(dst, &P.full[s], kb0 + i, lane);
-            B.issue(dst + PL_B_OFF, &P.full[s], kb0 + i, lane);
-        }
-    } else if (tid == 32) {
-        for (int i = 0; i < nk; ++i) {
-            const uint32_t q = seq0 + i, s = q % PL_STAGES;
-            mbar_wait(&P.full[s], (q / PL_STAGES) & 1);
-            tc_fence_after();
-            const uint32_t a_addr = P.smem_s + s * PL_SLOT, b_addr = a_addr + PL_B_OFF;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint64_t ad = AMN ? desc_sw128(a_addr + j * 2048, 8192) : desc_sw128(a_addr + j * 32, 0);
-                const uint64_t bd = BMN ? desc_sw128(b_addr + j * 2048, 8192) : desc_sw128(b_addr + j * 32, 0);
-                umma_bf16(tmem, ad, bd, IDESC, (i > 0 || j > 0) ? 1u : 0u);
-            }
-            umma_commit(&P.empty[s]);
-        }
-        umma_commit(P.acc);
-    }
-    mbar_wait(P.acc, P.tiles & 1);
-    PL_PROBE(1);
-    __syncwarp();
-    tc_fence_after();
-    P.seq = seq0 + nk;
-    P.tiles += 1;
-
-    const int wq = warp & 3, half = warp >> 2;
-    const int row = m0 + wq * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
-    constexpr int CW = BN >= 64 ? BN / 2 : BN;
-    if constexpr (is_scatter<EP>::value) {
-        // bf16 results staged in the idle ring, then written as whole 16-byte chunks of
-        // each destination row segment (consecutive lanes -> consecutive chunks)
-        constexpr int TS = BN + 8;  // padded row stride (elements): conflict-free 16B stores
-        bf16 *tile = reinterpret_cast<bf16 *>(P.smem);
-        const int cbeg = BN >= 64 ? half * CW : 0;
-        if ((BN >= 64 || half == 0) && cbeg < EP::ROW_CHUNKS * 8) {
-            for (int c0 = cbeg; c0 < cbeg + CW && c0 < EP::ROW_CHUNKS * 8; c0 += 32) {
-                float v[32];
-                if (nk > 0) {
-                    tmem_ld32(trow + c0, v);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
-                }
-                uint4 o[4];
-                ep.compute(row, n0 + c0, v, o);
-                uint4 *d = reinterpret_cast<uint4 *>(tile + (wq * 32 + lane) * TS + c0);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) d[q] = o[q];
-            }
-        }
-        PL_PROBE(2);
-        // destination offsets of every (row, segment) once, then whole-chunk copies
-        int32_t *dtab = reinterpret_cast<int32_t *>(P.smem + 128 * TS * 2);
-        if (tid < 128) {
-#pragma unroll 1
-            for (int k = 0; k < EP::NDEST; ++k) {
-                const bf16 *d = ep.dest(m0 + tid, n0, k);
-                dtab[k * 128 + tid] = d ? (int32_t)(d - ep.wsb) : -1;
-            }
-        }
-        __syncthreads();
-        PL_PROBE(3);
-        constexpr int CH = EP::ROW_CHUNKS;
-        bf16 *base = ep.wsb;
-#pragma unroll 1
-        for (int e = tid; e < EP::NDEST * 128 * CH; e += GEMM_THREADS) {
-            const int ch = e % CH, rk = e / CH;  // rk = k * 128 + r
-            const int off = dtab[rk];
-            if (off >= 0)
-                *reinterpret_cast<uint4 *>(base + (size_t)(uint32_t)off + ch * 8) =
-                    *reinterpret_cast<const uint4 *>(tile + (rk & 127) * TS + ch * 8);
-        }
-    } else if constexpr (is_staged<EP>::value) {
-        static_assert(128 * (BN + 1) * 4 <= PL_STAGES * PL_SLOT, "staging tile");
-        float *tile = reinterpret_cast<float *>(P.smem);
-        if (BN >= 64 || half == 0) {
-            const int cbeg = BN >= 64 ? half * CW : 0;
-            for (int c0 = cbeg; c0 < cbeg + CW; c0 += 32) {
-                float v[32];
-                if (nk > 0) {
-                    tmem_ld32(trow + c0, v);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
-                }
-#pragma unroll
-                for (int e = 0; e < 32; ++e) tile[(wq * 32 + lane) * (BN + 1) + c0 + e] = v[e];
-            }
-        }
-        __syncthreads();
-        ep.template apply_tile<BN>(tile, BN + 1, m0, n0);
-    } else if (BN >= 64 || half == 0) {
-        const int cbeg = BN >= 64 ? half * CW : 0;
-#pragma unroll 1
-        for (int c0 = cbeg; c0 < cbeg + CW; c0 += 32) {
-            float v[32];
-            if (nk > 0) {
-                tmem_ld32(trow + c0, v);
-            } else {
-#pragma unroll
-                for (int e = 0; e < 32; ++e) v[e] = 0.f;
-            }
-            ep.apply(row, n0 + c0, v, 32, split);
-        }
-    }
-    PL_PROBE(4);
-    tc_fence_before();
-    __syncthreads();
-    if (g_tl.on && blockIdx.x == 0 && threadIdx.x == 0) {
-        s_tl[5] = gtime();
-        const int slot = atomicAdd(&g_tl.n, 1);
-        if (slot < 256) {
-            for (int k = 0; k < 6; ++k) g_tl.t[slot][k] = s_tl[k];
-            g_tl.t[slot][6] = (unsigned long long)nk;
-            g_tl.t[slot][7] = (unsigned long long)BN;
-        }
-    }
-}
-
-// ------------------------------------------------------------------ scatter epilogues
-PQ_DEV void relu_pack(const float *v, const float *bias, float scale, uint4 (&o)[4]) {
-    float y[32];
-#pragma unroll
-    for (int e = 0; e < 32; ++e) {
-        const float t = v[e] * scale + bias[e];
-        y[e] = t > 0.f ? t : 0.f;
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-        o[c] = make_uint4(pack_bf16(y[8 * c], y[8 * c + 1]), pack_bf16(y[8 * c + 2], y[8 * c + 3]),
-                          pack_bf16(y[8 * c + 4], y[8 * c + 5]), pack_bf16(y[8 * c + 6], y[8 * c + 7]));
-}
-PQ_DEV void store64(bf16 *dst, const uint4 (&o)[4]) {
-    uint4 *d = reinterpret_cast<uint4 *>(dst);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) d[c] = o[c];
-}
-// masked (relu') copy of 32 values: mask = forward activation at the same place
-PQ_DEV void mask_pack(const float *v, const bf16 *mask, uint4 (&o)[4]) {
-    uint4 mk[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) mk[c] = __ldcg(reinterpret_cast<const uint4 *>(mask) + c);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const uint32_t mw[4] = {mk[c].x, mk[c].y, mk[c].z, mk[c].w};
-        uint32_t r[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float a = bf16_lo(mw[e]) > 0.f ? v[8 * c + 2 * e] : 0.f;
-            const float b = bf16_hi(mw[e]) > 0.f ? v[8 * c + 2 * e + 1] : 0.f;
-            r[e] = pack_bf16(a, b);
-        }
-        o[c] = make_uint4(r[0], r[1], r[2], r[3]);
-    }
-}
-
-// Scatter epilogues: compute() turns 32 accumulator columns of a row into bf16
-// (bias + ReLU, or the relu' mask), dest(m, n0, k) names the k-th row segment that
-// receives the staged row (nullptr = none); ROW_CHUNKS 16-byte chunks per segment.
-
-// conv1: rows (b, oy, ox) of 20x20, 32 channels -> act1 (online, the relu' mask of the
-// conv2 dgrad) and the conv2 patch rows (b, oy2, ox2) col (kh, kw, c), oy = 2 oy2 + kh
-struct EpiConv1 {
-    static constexpr int NDEST = 5, ROW_CHUNKS = 4;
-    bf16 *wsb;  // workspace base: destinations are int32 element offsets from it
-    bf16 *act1, *P2;
-    const float *bias;
-    int n;
-    float scale;
-    PQ_DEV void compute(int, int n0, const float *v, uint4 (&o)[4]) const {
-        float bv[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) bv[e] = __ldcg(bias + n0 + e);
-        relu_pack(v, bv, scale, o);
-    }
-    PQ_DEV bf16 *dest(int m, int, int k) const {
-        if (m >= n * 400) return nullptr;
-        if (k == 0) return act1 ? act1 + (size_t)m * 32 : nullptr;
-        const int b = m / 400, p = m - b * 400, oy = p / 20, ox = p - oy * 20;
-        const int kh = (oy & 1) + 2 * ((k - 1) >> 1), kw = (ox & 1) + 2 * ((k - 1) & 1);
-        const int oy2 = (oy - kh) >> 1, ox2 = (ox - kw) >> 1;
-        if (oy2 < 0 || oy2 > 8 || ox2 < 0 || ox2 > 8) return nullptr;
-        return P2 + (size_t)(b * 81 + oy2 * 9 + ox2) * P2_LD + (kh * 4 + kw) * 32;
-    }
-};
-
-// conv2: rows (b, oy, ox) of 9x9, 64 channels -> act2 (gathered by conv3's TMA and
-// the relu' mask of the conv3 dgrad)
-struct EpiConv2 {
-    static constexpr int NDEST = 1, ROW_CHUNKS = 8;
-    bf16 *wsb;  // workspace base: destinations are int32 element offsets from it
-    bf16 *act2;
-    const float *bias;
-    int n;
-    PQ_DEV void compute(int, int n0, const float *v, uint4 (&o)[4]) const {
-        float bv[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) bv[e] = __ldcg(bias + n0 + e);
-        relu_pack(v, bv, 1.0f, o);
-    }
-    PQ_DEV bf16 *dest(int m, int, int) const { return m < n * 81 ? act2 + (size_t)m * 64 : nullptr; }
-};
-
-// conv3 forward: rows (b, p) -> act3 [b][p][64] (dense)
-struct EpiConv3 {
-    static constexpr int NDEST = 1, ROW_CHUNKS = 8;
-    bf16 *wsb;  // workspace base: destinations are int32 element offsets from it
-    bf16 *act3;
-    const float *bias;
-    int n;
-    PQ_DEV void compute(int, int n0, const float *v, uint4 (&o)[4]) const {
-        float bv[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) bv[e] = __ldcg(bias + n0 + e);
-        relu_pack(v, bv, 1.0f, o);
-    }
-    PQ_DEV bf16 *dest(int m, int, int) const { return m < n * 49 ? act3 + (size_t)m * 64 : nullptr; }
-};
-
-// fc1 data gradient (rows = samples, the 64 cols of a tile = the 64 channels of one
-// conv3 output pixel p): dY3 = acc * relu'(act3)
-struct EpiB4D {
-    static constexpr int NDEST = 1, ROW_CHUNKS = 8;
-    bf16 *wsb;  // workspace base: destinations are int32 element offsets from it
-    bf16 *dY3;
-    const bf16 *act3;
-    int n;
-    PQ_DEV void compute(int m, int n0, const float *v, uint4 (&o)[4]) const {
-        if (m < n) {
-            mask_pack(v, act3 + (size_t)m * 3136 + n0, o);
-        } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) o[q] = make_uint4(0, 0, 0, 0);
-        }
-    }
-    PQ_DEV bf16 *dest(int m, int n0, int) const { return m < n ? dY3 + (size_t)m * 3136 + n0 : nullptr; }
-};
-
-// conv3 data gradient (rows (b, iy, ix) of 9x9): dY2 = acc * relu'(act2)
-struct EpiB3D {
-    static constexpr int NDEST = 1, ROW_CHUNKS = 8;
-    bf16 *wsb;  // workspace base: destinations are int32 element offsets from it
-    bf16 *dY2;
-    const bf16 *act2;
-    int n;
-    PQ_DEV void compute(int m, int n0, const float *v, uint4 (&o)[4]) const {
-        if (m < n * 81) {
-            mask_pack(v, act2 + (size_t)m * 64 + n0, o);
-        } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) o[q] = make_uint4(0, 0, 0, 0);
-        }
-    }
-    PQ_DEV bf16 *dest(int m, int, int) const { return m < n * 81 ? dY2 + (size_t)m * 64 : nullptr; }
-};
-
-// conv2 data gradient per parity class (rows class-major, (b, iy', ix') of 10x10, 32
-// channels): dY1 = acc * relu'(act1) at NHWC position (2 iy' + py, 2 ix' + px)
-struct EpiB2D {
-    static constexpr int NDEST = 1, ROW_CHUNKS = 4;
-    bf16 *wsb;  // workspace base: destinations are int32 element offsets from it
-    bf16 *dY1;
-    const bf16 *act1;
-    int n, tpc;
-    PQ_DEV int64_t pos(int m) const {
-        const int cls = m / (tpc * 128), loc = m - cls * tpc * 128;
-        if (loc >= n * 100) return -1;
-        const int b = loc / 100, r = loc - b * 100, ry = r / 10, rx = r - ry * 10;
-        const int iy = 2 * ry + (cls >> 1), ix = 2 * rx + (cls & 1);
-        return ((int64_t)(b * 20 + iy) * 20 + ix) * 32;
-    }
-    PQ_DEV void compute(int m, int n0, const float *v, uint4 (&o)[4]) const {
-        const int64_t q = pos(m);
-        if (q >= 0) {
-            mask_pack(v, act1 + q + n0, o);
-        } else {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) o[c] = make_uint4(0, 0, 0, 0);
-        }
-    }
-    PQ_DEV bf16 *dest(int m, int, int) const {
-        const int64_t q = pos(m);
-        return q >= 0 ? dY1 + q : nullptr;
-    }
-};
-
-// ------------------------------------------------------------------ jobs
-struct Ctx {
-    const PLearnArgs *a;
-    Pipe *P;
-    int u_base;
-    int k;  // phases run (trace row)
-};
-
-PQ_DEV TmaOp op(const PLearnArgs &a, int map, int kind, int boxes, int r0, int cls = 0) {
-    return TmaOp{&a.maps[map], kind, boxes, r0, cls, a.n, &a.maps[M_ONES]};
-}
-
-// conv1 patch rows of sample b (g = 0: state frames f0..f3, 1: next state f1..f4):
-// P1[(b, oy, ox)][k'(c, kh, kw)] = frame_c[4 oy + kh][4 ox + kw] (permuted K; 0..255 in bf16;
-// the 1/255 input scale is applied in the conv1 epilogue); slot -1 = masked zero frame.
-// The 4 frames are staged in the (idle) operand ring with coalesced 16-byte loads, all
-// in flight together; the patch rows leave as consecutive 16-byte chunks.
-PQ_DEV void gather_patches(const PLearnArgs &a, int g, const int64_t *map, int b, int quarter, bf16 *P1,
-                           uint8_t *stage) {
-    __shared__ int32_t s_slot[4];
-    if (threadIdx.x < 4) s_slot[threadIdx.x] = a.records[map[b] * REC_INTS + g + threadIdx.x];
-    __syncthreads();
-    constexpr int F16 = FRAME_BYTES / 16;  // 441
-    constexpr int PER = (4 * F16 + GEMM_THREADS - 1) / GEMM_THREADS;
-    uint4 buf[PER];
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-        const int e = threadIdx.x + i * GEMM_THREADS, c = e / F16, o = e - c * F16;
-        buf[i] = make_uint4(0, 0, 0, 0);
-        if (e < 4 * F16 && s_slot[c] >= 0)
-            buf[i] = __ldg(reinterpret_cast<const uint4 *>(a.ring + (size_t)s_slot[c] * FRAME_BYTES) + o);
-    }
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-        const int e = threadIdx.x + i * GEMM_THREADS;
-        if (e < 4 * F16) reinterpret_cast<uint4 *>(stage)[e] = buf[i];
-    }
-    __syncthreads();
-    bf16 *dst = P1 + (size_t)b * 400 * P1_LD;
-    for (int e = quarter * 100 * 32 + threadIdx.x; e < (quarter + 1) * 100 * 32; e += GEMM_THREADS) {
-        // 8-column chunk j of patch row `row` in the permuted K order (qnet.cuh w1_perm):
-        // tap (ty, tx) = j >> 3, frame c = (j >> 1) & 3, rows dy0 = 2 (j & 1), dy0 + 1
-        const int row = e >> 5, j = e & 31, tap = j >> 3, c = (j >> 1) & 3, dy0 = (j & 1) * 2;
-        const int oy = row / 20, ox = row - oy * 20;
-        const uint8_t *src = stage + c * FRAME_BYTES + (4 * oy + 4 * (tap >> 1) + dy0) * 84 + 4 * ox + 4 * (tap & 1);
-        *reinterpret_cast<uint4 *>(dst + (size_t)row * P1_LD + j * 8) =
-            u8x8_to_bf16(*reinterpret_cast<const uint32_t *>(src), *reinterpret_cast<const uint32_t *>(src + 84));
-    }
-    __syncthreads();
-}
-
-PQ_DEV void run_job(const Ctx &c, int type, int g, int uj, int j) {
-    const PLearnArgs &a = *c.a;
-    Pipe &P = *c.P;
-    const int n = a.n, par = uj & 1;
-    const int upd = c.u_base + uj;
-    const int64_t *map = a.idx_base + (int64_t)upd * n;
-    const pq_net &net = g ? a.target : a.theta;
-    switch (type) {
-        case J_G1:
-            gather_patches(a, g, map, j >> 2, j & 3, a.P1[g][par], P.smem);
-            break;
-        case J_F1:  // conv1 8x8/4: P1 x W1^T, bias + ReLU with the 1/255 input scale
-            tma_tile<32, false, false>(op(a, M_P1 + 2 * g + par, OP_K2, 2, j * 128), op(a, M_W1 + g, OP_K2, 1, 0),
-                                       EpiConv1{a.wsb, g ? nullptr : a.act1, a.P2[g], net.master + P_B1, n, 1.0f / 255.0f},
-                                       0, 4, j * 128, 0, 0, P);
-            break;
-        case J_F2:
-            tma_tile<64, false, false>(op(a, M_P2 + g, OP_K2, 2, j * 128), op(a, M_W2 + g, OP_K2, 1, 0),
-                                       EpiConv2{a.wsb, a.act2[g], net.master + P_B2, n}, 0, 8, j * 128, 0,
-                                       0, P);
-            break;
-        case J_F3:
-            tma_tile<64, false, false>(op(a, M_ACT2I + g, OP_IF3, 2, j * 128), op(a, M_W3 + g, OP_K2, 1, 0),
-                                       EpiConv3{a.wsb, a.act3[g][par], net.master + P_B3, n}, 0, 9,
-                                       j * 128, 0, 0, P);
-            break;
-        case J_F4: {  // fc1 swapped: D[j][b] = W4[j] . x[b], split-K partials [s][b][j]
-            const Counts cn = counts_of(n);
-            const int mt = j & 3, r = j >> 2, nt = r % cn.nt64, sp = r / cn.nt64;
-            const int kb0 = sp * PL_FC1_KC, kb1 = min(49, kb0 + PL_FC1_KC);
-            tma_tile<64, false, false>(op(a, M_W4 + g, OP_K2, 2, mt * 128),
-                                       op(a, M_ACT3 + 2 * g + par, OP_K2, 1, nt * 64),
-                                       EpiF32T{a.fc1part[g][par], 512, n, 512, (size_t)n * 512}, kb0, kb1, mt * 128,
-                                       nt * 64, sp, P);
-            break;
-        }
-        case J_HEAD: {
-            HeadArgs h{};
-            h.part[0] = a.fc1part[0][par], h.part[1] = a.fc1part[1][par];
-            h.master[0] = a.theta.master, h.master[1] = a.target.master;
-            h.groups = 2, h.n = n, h.A = a.A, h.n8 = a.n8;
-            h.records = a.records, h.idx = map;
-            h.gamma = a.gamma, h.learner = 1;
-            h.q_out = a.q, h.h1 = a.h1, h.dh1 = a.dh1, h.td = a.td, h.dh1_bf = a.dh1_bf, h.dh1T = a.dh1T;
-            h.act_out = a.act, h.q_copy = a.q_out, h.td_copy = a.td_out;
-            head_sample<PL_FC1_SPLITS>(h, j);
-            __syncthreads();  // head shared memory is reused by the next job
-            break;
-        }
-        case J_B4D: {  // D[b][k] = sum_j dh1[b][j] W4[j][k] (W4 as MN-major B)
-            const int mt = j / 49, nt = j % 49;
-            tma_tile<64, false, true>(op(a, M_DH1, OP_K2, 2, mt * 128), op(a, M_W4, OP_M2, 1, nt * 64),
-                                      EpiB4D{a.wsb, a.dY3, a.act3[0][par], n}, 0, 8, mt * 128, nt * 64, 0, P);
-            break;
-        }
-        case J_B3D:  // dY2 = relu'(x2) * transposed conv3(dY3): TP3 x W3 taps
-            tma_tile<64, false, true>(op(a, M_DY3I, OP_IT3, 2, j * 128), op(a, M_W3V, OP_W3V, 1, 0),
-                                      EpiB3D{a.wsb, a.dY2, a.act2[0], n}, 0, 9, j * 128, 0, 0, P);
-            break;
-        case J_B3W: {  // dW3^T[k][o] = sum_m P3[m][k] dY3[m][o]; column 576 = ones -> bias
-            const int mt = j % 5, sp = j / 5;
-            const int nch = (n * 49 + 63) / 64, kb0 = sp * a.kc3, kb1 = min(nch, kb0 + a.kc3);
-            tma_tile<64, true, true>(op(a, M_ACT2W, OP_IW3, 2, mt * 128), op(a, M_DY3, OP_M2, 1, 0),
-                                     EpiF32T{a.part3, 577, 64, 577, (size_t)64 * 577}, kb0, kb1, mt * 128, 0, sp, P);
-            break;
-        }
-        case J_B4W: {  // dW4[j][k] = sum_b dh1[b][j] x3[b][k] with centered RMSProp in the epilogue
-            const int mt = j & 3, nt = j >> 2;
-            EpiRms e{};
-            e.p = a.theta.master, e.m = a.opt.m, e.v = a.opt.v;
-            e.p2 = a.theta.master, e.m2 = a.opt.m, e.v2 = a.opt.v;
-            e.shadow = (bf16 *)a.theta.shadow;
-            e.grad_out = a.grad_out, e.flag = a.nonfinite, e.counter = nullptr, e.upd = upd;
-            e.lr = a.lr, e.rho = a.rho, e.kappa = a.kappa;
-            e.M = 512, e.N = 3136, e.pbase = P_W4, e.sbase = S_W4;
-            tma_tile<64, false, true>(op(a, M_DH1T, OP_K2, 2, mt * 128), op(a, M_ACT3 + par, OP_M2, 1, nt * 64), e,
-                                      0, (n + 63) / 64, mt * 128, nt * 64, 0, P);
-            break;
-        }
-        case J_B2D: {  // dY1 = relu'(x1) * transposed conv2(dY2), 4 input-parity classes
-            const int tpc = counts_of(n).tpc, cls = j / tpc, loc = j - cls * tpc;
-            tma_tile<64, false, true>(op(a, M_DY2I, OP_IT2, 2, loc * 128), op(a, M_W2V, OP_W2V, 1, 0, cls),
-                                      EpiB2D{a.wsb, a.dY1, a.act1, n, tpc}, 0, 4, j * 128, 0, 0, P);
-            break;
-        }
-        case J_B2W: {
-            const int mt = j % 5, sp = j / 5;
-            const int nch = (n * 81 + 63) / 64, kb0 = sp * a.kc2, kb1 = min(nch, kb0 + a.kc2);
-            tma_tile<64, true, true>(op(a, M_P2, OP_M2, 2, mt * 128), op(a, M_DY2, OP_M2, 1, 0),
-                                     EpiF32T{a.part2, 513, 64, 513, (size_t)64 * 513}, kb0, kb1, mt * 128, 0, sp, P);
-            break;
-        }
-        case J_B1W: {  // dW1^T[k][o] = sum_m P1[m][k] dY1[m][o]; column 256 = ones
-            const int mt = j % 3, sp = j / 3;
-            const int nch = (n * 400 + 63) / 64, kb0 = sp * a.kc1, kb1 = min(nch, kb0 + a.kc1);
-            tma_tile<64, true, true>(op(a, M_P1 + par, OP_M2, 2, mt * 128), op(a, M_DY1, OP_M2, 1, 0),
-                                     EpiF32T{a.part1, 257, 32, 257, (size_t)32 * 257}, kb0, kb1, mt * 128, 0, sp, P);
-            break;
-        }
-        default: {  // RMSProp slices of the conv layers / fc1 bias / fc2
-            OptArgs o{};
-            o.p = a.theta.master, o.m = a.opt.m, o.v = a.opt.v;
-            o.p2 = a.theta.master, o.m2 = a.opt.m, o.v2 = a.opt.v;
-            o.shadow = (bf16 *)a.theta.shadow;
-            o.part1 = a.part1, o.part2 = a.part2, o.part3 = a.part3, o.grad4 = nullptr;
-            o.s1 = a.s1, o.s2 = a.s2, o.s3 = a.s3;
-            o.dh1 = a.dh1, o.h1 = a.h1, o.td = a.td, o.act = a.act;
-            o.n = n, o.A = a.A;
-            o.lr = a.lr, o.rho = a.rho, o.kappa = a.kappa;
-            o.flag = a.nonfinite, o.grad_out = a.grad_out;
-            o.total = n_params(a.A);
-            o.w1_perm = 1;  // conv1 weight-gradient rows in the permuted K order
-            const int64_t lo = opt_lo(type) + (int64_t)j * PL_OPT_PER_JOB;
-            const int64_t hi = min(opt_hi(type, a.A), lo + PL_OPT_PER_JOB);
-            for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) opt_param(o, i, upd);
-            break;
-        }
-    }
-}
-
-// the idx-th job of the critical (filler = 0) or filler (1) list of the phase
-PQ_DEV void run_listed(const Ctx &c, const PhasePlan &P, int u, int filler, int idx) {
-    const PLearnArgs &a = *c.a;
-    for (int s = 0; s < P.nseg; ++s) {
-        const Seg &g = P.seg[s];
-        if (g.filler != filler || u + g.du < 0 || u + g.du >= a.n_updates) continue;
-        const int cnt = g.end - g.begin;
-        if (idx < cnt) {
-            const unsigned long long t0 = a.trace ? gtime() : 0ull;
-            run_job(c, g.type, g.grp, u + g.du, g.begin + idx);
-            if (a.trace && threadIdx.x == 0) {  // last job of this CTA in the phase
-                unsigned long long *t = a.trace + ((size_t)c.k * gridDim.x + blockIdx.x) * 4;
-                t[2] = (unsigned long long)g.type;
-                t[3] = gtime() - t0;
-            }
-            return;
-        }
-        idx -= cnt;
-    }
-}
-
-// Critical jobs are dealt round-robin over all CTAs; fillers round-robin over the CTAs
-// left without a critical job (over all CTAs when there are none).
-PQ_DEV void run_phase(const Ctx &c, const PhasePlan &P, int u) {
-    const PLearnArgs &a = *c.a;
-    int ncrit = 0, nfill = 0;
-    for (int s = 0; s < P.nseg; ++s) {
-        const Seg &g = P.seg[s];
-        if (u + g.du < 0 || u + g.du >= a.n_updates) continue;
-        (g.filler ? nfill : ncrit) += g.end - g.begin;
-    }
-    const int G = gridDim.x, me = blockIdx.x;
-    for (int j = me; j < ncrit; j += G) run_listed(c, P, u, 0, j);
-    if (ncrit < G) {
-        if (me >= ncrit)
-            for (int f = me - ncrit; f < nfill; f += G - ncrit) run_listed(c, P, u, 1, f);
-    } else {
-        for (int f = ((me - ncrit) % G + G) % G; f < nfill; f += G) run_listed(c, P, u, 1, f);
-    }
-}
-
-// one phase, then the grid barrier (with the optional trace rows)
-PQ_DEV void run_phase_sync(Ctx &c, const PhasePlan &PP, int u, unsigned &target) {
-    const PLearnArgs &a = *c.a;
-    run_phase(c, PP, u);
-    if (a.trace && threadIdx.x == 0) a.trace[((size_t)c.k * gridDim.x + blockIdx.x) * 4] = gtime();
-    grid_barrier(a.bar, target);
-    if (a.trace && threadIdx.x == 0) a.trace[((size_t)c.k * gridDim.x + blockIdx.x) * 4 + 1] = gtime();
-    ++c.k;
-}
-
-__global__ void __launch_bounds__(GEMM_THREADS, 1) k_learn_persistent(const __grid_constant__ PLearnArgs a) {
-    extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t full[PL_STAGES], empty[PL_STAGES], accb;
-    __shared__ uint32_t tmem_base_s;
-    __shared__ int s_ubase;
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < PL_STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        mbar_init(&accb, 1);
-        fence_mbar_init();
-        s_ubase = *a.update_counter;
-    }
-    if ((threadIdx.x >> 5) == 0) tmem_alloc<64>(&tmem_base_s);
-    if (threadIdx.x < M_COUNT)
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&a.maps[threadIdx.x]) : "memory");
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    Pipe P{smem, smem_u32(smem), full, empty, &accb, 0u, 0u, &tmem_base_s};
-    Ctx c{&a, &P, s_ubase, 0};
-    unsigned target = 0;
-    {
-        const Sched &S = a.sched[SCHED_PROLOGUE];
-        for (int p = 0; p < S.nphases; ++p) run_phase_sync(c, S.ph[p], 0, target);
-    }
-    for (int u = 0; u < a.n_updates; ++u) {
-        const Sched &S = a.sched[u == a.n_updates - 1 ? SCHED_LAST : SCHED_STEADY];
-        for (int p = 0; p < S.nphases; ++p) run_phase_sync(c, S.ph[p], u, target);
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *a.update_counter = s_ubase + a.n_updates;
-    tc_fence_before();
-    __syncthreads();
-    if ((threadIdx.x >> 5) == 0) tmem_dealloc<64>(tmem_base_s);
-}
-
-// constant ones of the online operands of the weight-gradient GEMMs (bias gradients):
-// P1 column 256, P2 column 512 and column 0 of the [64][64] ones tile; everything else
-// never written stays zero from the allocation
-__global__ void k_plearn_ones(bf16 *P1a, bf16 *P1b, bf16 *P2, bf16 *ones, int n) {
-    const bf16 one = __float2bfloat16_rn(1.0f);
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n * 400; r += gridDim.x * blockDim.x) {
-        P1a[(size_t)r * P1_LD + 256] = one;
-        P1b[(size_t)r * P1_LD + 256] = one;
-        if (r < n * 81) P2[(size_t)r * P2_LD + 512] = one;
-        if (r < 64) ones[r * 64] = one;
-    }
-}
-
-// ------------------------------------------------------------------ host side
-static size_t al(size_t x) { return (x + 1023) & ~size_t(1023); }
-
-struct PWS {
-    bf16 *act1, *act2[2], *act3[2][2];
-    bf16 *ones;  // [64][64], column 0 = 1: the bias-gradient atom of the conv3 wgrad
-    bf16 *P1[2][2], *P2[2];
-    float *fc1part[2][2];
-    float *q, *h1, *dh1, *td;
-    bf16 *dh1_bf, *dh1T;
-    int32_t *act;
-    bf16 *dY3, *dY2, *dY1;
-    float *part1, *part2, *part3;
-    unsigned *bar;
-    size_t bytes;
-};
-
-static PWS carve_p(void *base, int N, int A) {
-    PWS w;
-    size_t off = 0;
-    char *b = static_cast<char *>(base);
-    auto take = [&](size_t bytes) -> void * {
-        void *p = b ? b + off : nullptr;
-        off += al(bytes);
-        return p;
-    };
-    const int n8 = (N + 7) & ~7;
-    w.act1 = (bf16 *)take((size_t)N * 400 * 32 * 2);
-    for (int g = 0; g < 2; ++g) {
-        w.act2[g] = (bf16 *)take((size_t)N * 81 * 64 * 2);
-        for (int p = 0; p < 2; ++p) {
-            w.act3[g][p] = (bf16 *)take((size_t)N * 3136 * 2);
-            w.P1[g][p] = (bf16 *)take((size_t)N * 400 * P1_LD * 2);
-            w.fc1part[g][p] = (float *)take((size_t)PL_FC1_SPLITS * N * 512 * 4);
-        }
-        w.P2[g] = (bf16 *)take((size_t)N * 81 * P2_LD * 2);
-    }
-    w.q = (float *)take((size_t)2 * N * A * 4);
-    w.h1 = (float *)take((size_t)N * 512 * 4);
-    w.dh1 = (float *)take((size_t)N * 512 * 4);
-    w.td = (float *)take((size_t)N * 3 * 4);
-    w.dh1_bf = (bf16 *)take((size_t)N * 512 * 2);
-    w.dh1T = (bf16 *)take((size_t)512 * n8 * 2);
-    w.act = (int32_t *)take((size_t)N * 4);
-    w.dY3 = (bf16 *)take((size_t)N * 3136 * 2);
-    w.dY2 = (bf16 *)take((size_t)N * 81 * 64 * 2);
-    w.dY1 = (bf16 *)take((size_t)N * 400 * 32 * 2);
-    w.ones = (bf16 *)take(64 * 64 * 2);
-    w.part1 = (float *)take((size_t)MAX_SPLITS * 32 * 257 * 4);
-    w.part2 = (float *)take((size_t)MAX_SPLITS * 64 * 513 * 4);
-    w.part3 = (float *)take((size_t)MAX_SPLITS * 64 * 577 * 4);
-    w.bar = (unsigned *)take(sizeof(unsigned));
-    w.bytes = off;
-    return w;
-}
-
 // ---- tensor maps (driver entry point; no -lcuda link)
 static PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
     static void *fn = nullptr;
@@ -1016,146 +196,6 @@ static int map_im2col(CUtensorMap *m, const void *base, int n, int H, int W, int
         return set_err(msg);
     }
     return 0;
-}
-
-static int build_maps(PLearnArgs &a) {
-    const int n = a.n;
-    for (int g = 0; g < 2; ++g) {
-        const bf16 *sh = (const bf16 *)(g ? a.target.shadow : a.theta.shadow);
-        if (int rc = map2(&a.maps[M_W1 + g], sh + S_W1P, 32, 256, 256, "W1 permuted")) return rc;
-        if (int rc = map2(&a.maps[M_W2 + g], sh + S_W2, 64, 512, 512, "W2")) return rc;
-        if (int rc = map2(&a.maps[M_W3 + g], sh + S_W3, 64, 576, 576, "W3")) return rc;
-        if (int rc = map2(&a.maps[M_W4 + g], sh + S_W4, 512, 3136, 3136, "W4")) return rc;
-        for (int p = 0; p < 2; ++p) {
-            if (int rc = map2(&a.maps[M_ACT3 + 2 * g + p], a.act3[g][p], n, 3136, 3136, "act3")) return rc;
-            if (int rc = map2(&a.maps[M_P1 + 2 * g + p], a.P1[g][p], (uint64_t)n * 400, 257, P1_LD, "P1")) return rc;
-        }
-        if (int rc = map2(&a.maps[M_P2 + g], a.P2[g], (uint64_t)n * 81, 513, P2_LD, "P2")) return rc;
-        if (int rc = map_im2col(&a.maps[M_ACT2I + g], a.act2[g], n, 9, 9, 0, -2, 128, "act2")) return rc;
-    }
-    if (int rc = map_im2col(&a.maps[M_ACT2W], a.act2[0], n, 9, 9, 0, -2, 64, "act2 wgrad")) return rc;
-    if (int rc = map_im2col(&a.maps[M_DY3I], a.dY3, n, 7, 7, -2, 0, 128, "dY3")) return rc;
-    if (int rc = map_im2col(&a.maps[M_DY2I], a.dY2, n, 9, 9, -1, 0, 128, "dY2")) return rc;
-    if (int rc = map2(&a.maps[M_ONES], a.ones, 64, 64, 64, "ones")) return rc;
-    if (int rc = map2(&a.maps[M_DH1], a.dh1_bf, n, 512, 512, "dh1")) return rc;
-    if (int rc = map2(&a.maps[M_DH1T], a.dh1T, 512, n, a.n8, "dh1T")) return rc;
-    if (int rc = map2(&a.maps[M_DY3], a.dY3, (uint64_t)n * 49, 64, 64, "dY3")) return rc;
-    if (int rc = map2(&a.maps[M_DY2], a.dY2, (uint64_t)n * 81, 64, 64, "dY2")) return rc;
-    if (int rc = map2(&a.maps[M_DY1], a.dY1, (uint64_t)n * 400, 32, 32, "dY1")) return rc;
-    const bf16 *sh = (const bf16 *)a.theta.shadow;
-    {  // conv3 weight [o][kh][kw][c] as (c, tap, o)
-        const uint64_t dims[3] = {64, 9, 64}, st[2] = {64, 576};
-        if (int rc = make_map(&a.maps[M_W3V], sh + S_W3, 3, dims, st, "W3 view")) return rc;
-    }
-    {  // conv2 weight [o][kh][kw][c] as (c, kw, kh, o)
-        const uint64_t dims[4] = {32, 4, 4, 64}, st[3] = {32, 128, 512};
-        if (int rc = make_map(&a.maps[M_W2V], sh + S_W2, 4, dims, st, "W2 view")) return rc;
-    }
-    return 0;
-}
-
-// split-K factor for `mtiles` M tiles of a contraction of `nch` 64-wide chunks given a
-// CTA budget: chunks per split >= 2, splits <= MAX_SPLITS
-static void choose_split(int nch, int mtiles, int budget, int *kc, int *splits) {
-    int s = std::max(1, budget / mtiles);
-    int k = std::max(2, (nch + s - 1) / s);
-    k = std::max(k, (nch + MAX_SPLITS - 1) / MAX_SPLITS);
-    *kc = k;
-    *splits = (nch + k - 1) / k;
-}
-
-struct PlanBuilder {
-    Sched &S;
-    int n, A, s1, s2, s3;
-    int count(int type) const { return njobs(type, n, A, s1, s2, s3); }
-    void add(int p, int type, int grp, int du, int filler, int begin = 0, int end = -1) {
-        if (end < 0) end = count(type);
-        if (end <= begin) return;
-        PhasePlan &P = S.ph[p];
-        P.seg[P.nseg++] = Seg{(int16_t)type, (int8_t)grp, (int8_t)du, (int16_t)filler, 0, begin, end};
-        S.nphases = std::max(S.nphases, p + 1);
-    }
-    int load(int p) const {
-        int t = 0;
-        for (int s = 0; s < S.ph[p].nseg; ++s) t += S.ph[p].seg[s].end - S.ph[p].seg[s].begin;
-        return t;
-    }
-};
-
-static void build_plans(PLearnArgs &a, int G) {
-    const int n = a.n, A = a.A;
-    const Counts cn = counts_of(n);
-    memset(a.sched, 0, sizeof(a.sched));
-    choose_split((n * 400 + 63) / 64, 3, G, &a.kc1, &a.s1);
-    choose_split((n * 81 + 63) / 64, 5, std::max(5, G - 4 * cn.tpc), &a.kc2, &a.s2);
-    choose_split((n * 49 + 63) / 64, 5, std::max(5, G - cn.t2), &a.kc3, &a.s3);
-    {  // prologue: frame gathers of steps 0 / 1 and the target forward of step 0
-        PlanBuilder b{a.sched[SCHED_PROLOGUE], n, A, a.s1, a.s2, a.s3};
-        b.add(0, J_G1, 1, 0, 0);
-        b.add(0, J_G1, 0, 0, 0);
-        b.add(0, J_G1, 1, +1, 0);
-        b.add(1, J_F1, 1, 0, 0);
-        b.add(2, J_F2, 1, 0, 0);
-        b.add(3, J_F3, 1, 0, 0);
-        b.add(4, J_F4, 1, 0, 0);
-    }
-    for (int last = 0; last < 2; ++last) {
-        PlanBuilder b{a.sched[last ? SCHED_LAST : SCHED_STEADY], n, A, a.s1, a.s2, a.s3};
-        // the critical chain of the step
-        b.add(0, J_F1, 0, 0, 0);
-        b.add(1, J_F2, 0, 0, 0);
-        b.add(2, J_F3, 0, 0, 0);
-        b.add(3, J_F4, 0, 0, 0);
-        b.add(4, J_HEAD, 0, 0, 0);
-        b.add(5, J_B4D, 0, 0, 0);
-        b.add(6, J_B3D, 0, 0, 0);
-        b.add(6, J_B3W, 0, 0, 0);
-        b.add(7, J_B2D, 0, 0, 0);
-        b.add(7, J_B2W, 0, 0, 0);
-        b.add(8, J_B1W, 0, 0, 0);
-        b.add(9, J_OPT_C1, 0, 0, 0);
-        b.add(9, J_OPT_C2, 0, 0, 0);
-        b.add(9, J_OPT_C3, 0, 0, 0);
-        // fillers: next steps' target forward and frame gathers (skipped past the
-        // launch's end), the fc2 / fc1-bias update
-        b.add(1, J_F1, 1, +1, 1);
-        b.add(2, J_F2, 1, +1, 1);
-        b.add(3, J_F3, 1, +1, 1);
-        b.add(4, J_F4, 1, +1, 1);
-        b.add(5, J_OPT_FC2, 0, 0, 1);
-        b.add(5, J_G1, 1, +2, 1);
-        b.add(9, J_G1, 0, +1, 1);
-    }
-    // fc1 weight gradient + RMSProp tiles into the spare CTAs of the phases where they
-    // may run: 6-9 of their own step, 0-2 of the next (du = -1 there).  The split is
-    // decided for a steady step; the last step of a launch runs the previous step's
-    // leftovers in 0-2 as usual and all of its own tiles in 6-9.
-    PlanBuilder st{a.sched[SCHED_STEADY], n, A, a.s1, a.s2, a.s3};
-    PlanBuilder ls{a.sched[SCHED_LAST], n, A, a.s1, a.s2, a.s3};
-    const int total = st.count(J_B4W);
-    const int own[3] = {6, 7, 8}, nxt[3] = {0, 1, 2};
-    int next = 0;
-    for (int p : own) {
-        const int take = std::min(total - next, std::max(0, G - st.load(p)));
-        if (take > 0) st.add(p, J_B4W, 0, 0, 1, next, next + take);
-        next += std::max(0, take);
-    }
-    for (int p : nxt) {
-        const int take = std::min(total - next, std::max(0, G - st.load(p)));
-        if (take > 0) {
-            st.add(p, J_B4W, 0, -1, 1, next, next + take);
-            ls.add(p, J_B4W, 0, -1, 1, next, next + take);
-        }
-        next += std::max(0, take);
-    }
-    if (next < total) st.add(9, J_B4W, 0, 0, 1, next, total);
-    next = 0;
-    for (int p : own) {
-        const int take = std::min(total - next, std::max(0, G - ls.load(p)));
-        if (take > 0) ls.add(p, J_B4W, 0, 0, 1, next, next + take);
-        next += std::max(0, take);
-    }
-    if (next < total) ls.add(9, J_B4W, 0, 0, 1, next, total);
 }
 
 // ================================================================== one-shot TMA GEMMs
@@ -2715,103 +1755,11 @@ int tma_conv1_wgrad(const bf16 *s2d, int nframes, const bf16 *dY1, float *part1,
     return launch_tma<64, true, true>(g, st, "conv1 wgrad (TMA)");
 }
 
-static int g_learn_ctas = 0;  // 0 = all SMs minus the acting reserve
-static unsigned long long *g_trace = nullptr;
 
 }  // namespace pq
 
 using namespace pq;
 
 extern "C" {
-
-size_t pq_plearn_workspace_bytes(int max_batch, int actions) {
-    return carve_p(nullptr, max_batch, actions).bytes;
-}
-
-int pq_plearn_set_ctas(int ctas) {
-    g_learn_ctas = ctas;
-    return 0;
-}
-
-// GEMM timeline probes of this translation unit (layout of pq_timeline)
-int pq_plearn_timeline(int on, unsigned long long *out, int *count) {
-    if (out) {
-        static Timeline h;
-        PQ_CUDA_TRY(cudaMemcpyFromSymbol(&h, g_tl, sizeof(Timeline)));
-        *count = h.n < 256 ? h.n : 256;
-        memcpy(out, h.t, sizeof(h.t));
-    }
-    static Timeline z;
-    memset(&z, 0, sizeof(z));
-    z.on = on;
-    PQ_CUDA_TRY(cudaMemcpyToSymbol(g_tl, &z, sizeof(Timeline)));
-    return 0;
-}
-
-int pq_plearn_trace(unsigned long long *device_buf) {
-    g_trace = device_buf;
-    return 0;
-}
-
-int pq_learn_run(const pq_learn_args *la, int n_updates, void *stream) {
-    const int n = la->n;
-    if (n < 1 || n > la->max_batch) return set_err("batch size out of range for the workspace");
-    if (la->actions < 1 || la->actions > MAX_ACTIONS) return set_err("actions must be in [1, 32]");
-    if (n_updates < 1) return set_err("n_updates must be >= 1");
-    if (la->ext_targets || la->idx || !la->idx_base || !la->update_counter)
-        return set_err("persistent learner: needs the epoch index table + update counter, no external targets");
-    if (la->theta_out.master != la->theta.master || la->opt_out.m != la->opt.m)
-        return set_err("persistent learner: updates theta / opt in place");
-    cudaStream_t st = (cudaStream_t)stream;
-    static int sms = 0;
-    static bool configured = false;
-    if (!configured) {
-        int dev = 0;
-        PQ_CUDA_TRY(cudaGetDevice(&dev));
-        PQ_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        PQ_CUDA_TRY(cudaFuncSetAttribute(k_learn_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, PL_SMEM));
-        configured = true;
-    }
-    const int G = g_learn_ctas > 0 ? std::min(g_learn_ctas, sms) : std::max(1, sms - 20);
-    PWS w = carve_p(la->ws, la->max_batch, la->actions);
-    static PLearnArgs a;  // large (tensor maps + schedules): not on the stack
-    memset(&a, 0, sizeof(a));
-    a.theta = la->theta, a.target = la->target, a.opt = la->opt;
-    a.ring = la->ring, a.records = la->records, a.idx_base = la->idx_base;
-    a.update_counter = la->update_counter;
-    a.n = n, a.A = la->actions, a.n8 = (n + 7) & ~7, a.n_updates = n_updates;
-    a.gamma = la->gamma, a.lr = la->lr, a.rho = la->rho, a.kappa = la->kappa;
-    a.nonfinite = la->nonfinite, a.grad_out = la->grad_out, a.q_out = la->q_out, a.td_out = la->td_out;
-    a.wsb = (bf16 *)la->ws;
-    a.act1 = w.act1;
-    for (int g = 0; g < 2; ++g) {
-        for (int p = 0; p < 2; ++p) {
-            a.act3[g][p] = w.act3[g][p], a.P1[g][p] = w.P1[g][p], a.fc1part[g][p] = w.fc1part[g][p];
-        }
-        a.P2[g] = w.P2[g], a.act2[g] = w.act2[g];
-    }
-    a.ones = w.ones;
-    a.q = w.q, a.h1 = w.h1, a.dh1 = w.dh1, a.td = w.td, a.dh1_bf = w.dh1_bf, a.dh1T = w.dh1T, a.act = w.act;
-    a.dY3 = w.dY3, a.dY2 = w.dY2, a.dY1 = w.dY1;
-    a.part1 = w.part1, a.part2 = w.part2, a.part3 = w.part3;
-    a.bar = w.bar;
-    a.trace = g_trace;
-    if (int rc = build_maps(a)) return rc;
-    build_plans(a, G);
-    PQ_CUDA_TRY(cudaMemsetAsync(w.bar, 0, sizeof(unsigned), st));
-    k_plearn_ones<<<64, 256, 0, st>>>(w.P1[0][0], w.P1[0][1], w.P2[0], w.ones, n);
-    PQ_CUDA_TRY(cudaGetLastError());
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(G);
-    cfg.blockDim = dim3(GEMM_THREADS);
-    cfg.dynamicSmemBytes = PL_SMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cuda_err(cudaLaunchKernelEx(&cfg, k_learn_persistent, a), "persistent learner");
-}
 
 }  // extern "C"

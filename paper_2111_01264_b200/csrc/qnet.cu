@@ -192,122 +192,6 @@ static cudaError_t launch_bn(int bn, const GemmArgs<LA, LB, EP> &g, int groups, 
     }
 }
 
-// ------------------------------------------------------------------ fused conv2 -> conv3
-// One sample per CTA (grid n x groups): the sample's conv1 output (20x20x32) is staged in
-// shared memory, conv2 (9x9 outputs, K = 512) gathers its patches from there, its
-// bias + ReLU output stays in shared memory (and goes out for the conv3 dgrad mask / wgrad
-// operand), conv3 (7x7 outputs, K = 576) gathers from that.  One launch and no act2
-// round trip instead of two dependent GEMM kernels.
-struct F23Args {
-    const bf16 *act1[2];
-    bf16 *act2[2], *act3[2];
-    const bf16 *w2[2], *w3[2];
-    const float *b2[2], *b3[2];
-};
-constexpr int F23_STAGES = 6;
-constexpr int F23_SLOT = GEMM_A_BYTES + 64 * 128;
-constexpr int F23_ACT1 = 400 * 32 * 2, F23_ACT2 = 81 * 64 * 2;
-constexpr int F23_SMEM = F23_STAGES * F23_SLOT + F23_ACT1 + F23_ACT2 + 1024;
-
-// conv2 epilogue: bias + ReLU of the 81 output pixels to global act2 and the smem tile
-struct EpiAct2 {
-    bf16 *out, *tile;
-    const float *bias;
-    PQ_DEV void apply(int m, int n0, const float *v, int, int) const {
-        float bv[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) bv[e] = __ldg(bias + n0 + e);
-        if (m >= 81) return;
-        uint4 o[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            float y[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const float t = v[8 * q + e] + bv[8 * q + e];
-                y[e] = t > 0.f ? t : 0.f;
-            }
-            o[q] = make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]),
-                              pack_bf16(y[6], y[7]));
-        }
-        uint4 *g = reinterpret_cast<uint4 *>(out + (size_t)m * 64 + n0);
-        uint4 *t = reinterpret_cast<uint4 *>(tile + m * 64 + n0);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) g[q] = o[q], t[q] = o[q];
-    }
-};
-
-struct F23Hook {  // after the weight prefetch: wait for conv1, stage the sample's act1
-    const bf16 *src;
-    bf16 *dst;
-    PQ_DEV void operator()() const {
-        griddep_wait();
-        griddep_launch();
-        const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
-        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-        for (int i = threadIdx.x; i < F23_ACT1 / 16; i += blockDim.x) d4[i] = s4[i];
-        __syncthreads();
-    }
-};
-
-__global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv23(const __grid_constant__ F23Args a) {
-    extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t bars[F23_STAGES];
-    __shared__ uint32_t tmem_base_s;
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    bf16 *act1_t = reinterpret_cast<bf16 *>(smem + F23_STAGES * F23_SLOT);
-    bf16 *act2_t = reinterpret_cast<bf16 *>(smem + F23_STAGES * F23_SLOT + F23_ACT1);
-    const int b = blockIdx.x, g = blockIdx.y;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < F23_STAGES; ++s) mbar_init(&bars[s], 1);
-        fence_mbar_init();
-    }
-    if ((threadIdx.x >> 5) == 0) tmem_alloc<64>(&tmem_base_s);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    TileRing R{smem, smem_u32(smem), bars, 0u, &tmem_base_s, nullptr};
-    const LoadSmemConv c2{act1_t, 20, 20, 32, 4, 2, 1, 0, 9, 81, 0, 0};
-    gemm_tile<64, false, false, F23_STAGES, F23_SLOT, 2>(
-        c2, LoadDense{a.w2[g], 64, 512, 512}, EpiAct2{a.act2[g] + (size_t)b * 81 * 64, act2_t, a.b2[g]}, 0, 8, 0,
-        0, 0, -1, 0, R, F23Hook{a.act1[g] + (size_t)b * 400 * 32, act1_t});
-    const LoadSmemConv c3{act2_t, 9, 9, 64, 3, 1, 1, 0, 7, 49, 0, 0};
-    gemm_tile<64, false, false, F23_STAGES, F23_SLOT, 0>(
-        c3, LoadDense{a.w3[g], 64, 576, 576}, EpiBiasRelu{a.act3[g] + (size_t)b * 3136, a.b3[g], 49, 64, 64, 1.0f},
-        0, 9, 0, 0, 0, -1, 0, R, NoHook{});
-    tc_fence_before();
-    __syncthreads();
-    if ((threadIdx.x >> 5) == 0) tmem_dealloc<64>(tmem_base_s);
-}
-
-// PQ_CONV23=1 selects the fused kernel.  Measured no faster inside the CUDA graph at
-// batch 32 (84.7 vs 84.5 us per step: PDL already hides the kernel boundary and the 17
-// serial K-chunks remain) and slower at 1024 (200 vs ~103 us), so it is off by default.
-static bool use_conv23() {
-    static int on = -1;
-    if (on < 0) {
-        const char *e = getenv("PQ_CONV23");
-        on = (e && e[0] == '1') ? 1 : 0;
-    }
-    return on == 1;
-}
-
-static int conv23(const pq_net *nets, int groups, int n, const WS &w, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        PQ_CHECK(cudaFuncSetAttribute(k_conv23, cudaFuncAttributeMaxDynamicSharedMemorySize, F23_SMEM),
-                 "conv23 smem");
-        configured = true;
-    }
-    F23Args a{};
-    for (int q = 0; q < groups; ++q) {
-        a.act1[q] = w.act1[q], a.act2[q] = w.act2[q], a.act3[q] = w.act3[q];
-        a.w2[q] = (const bf16 *)nets[q].shadow + S_W2, a.w3[q] = (const bf16 *)nets[q].shadow + S_W3;
-        a.b2[q] = nets[q].master + P_B2, a.b3[q] = nets[q].master + P_B3;
-    }
-    return cuda_err(launch_k(k_conv23, dim3(n, groups), dim3(GEMM_THREADS), F23_SMEM, st, a), "conv2+conv3 forward");
-}
-
 // F1..F4 for `groups` parameter sets (group 0 / 1 = online / target in the learner)
 // early_frames: the learner -- its frames / records are never written by the kernel
 // before it (only the acting kernel writes frames, and it triggers its dependents
@@ -342,10 +226,7 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
     }
     bf16 *a2[2] = {w.act2[0], w.act2[1]}, *a3[2] = {w.act3[0], w.act3[1]};
     float *pt[2] = {w.fc1part[0], w.fc1part[1]};
-    const bool fused = use_conv23();
-    if (fused) {
-        if (int rc = conv23(nets, groups, n, w, st)) return rc;
-    } else if (use_tma(n) && w.s2d && conv1_shift() && w.act1s2[0]) {  // F2 over act1's 2x2 space-to-depth
+    if (use_tma(n) && w.s2d && conv1_shift() && w.act1s2[0]) {  // F2 over act1's 2x2 space-to-depth
         bf16 *s2[2] = {w.act1s2[0], w.act1s2[1]};
         if (int rc = tma_conv2_shift(nets, s2, a2, groups, n, st)) return rc;
     } else {  // F2: conv2 4x4/2 over 20x20x32 (K = 512)
@@ -360,8 +241,7 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
     }
     // engine per GEMM (measured, profiles/r1_engine_compare.md): the TMA im2col conv3
     // forward wins once a CTA has several tiles; at small batch the cp.async one does
-    if (fused) {
-    } else if (use_tma(n) && conv1_shift()) {  // the 7 x 7 outputs on act2's own 9 x 9 grid
+    if (use_tma(n) && conv1_shift()) {  // the 7 x 7 outputs on act2's own 9 x 9 grid
         if (int rc = tma_conv3_shift(nets, a2, a3, groups, n, st)) return rc;
     } else if (use_tma(n)) {
         if (int rc = tma_conv3_fwd(nets, a2, a3, groups, n, st)) return rc;
@@ -391,19 +271,6 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
                  "fc1 forward");
     }
     return 0;
-}
-
-// PQ_SPLIT_OPT=1: update conv2 / conv3 / fc on the weight-gradient branch and only conv1
-// on the critical path.  Measured slower at batch 32 (93.6 vs 92.1 us per step: its CTAs
-// crowd out the conv1 weight gradient), so the default is one optimizer launch after
-// the join, which also advances the step counter.
-static bool split_optimizer() {
-    static int on = -1;
-    if (on < 0) {
-        const char *e = getenv("PQ_SPLIT_OPT");
-        on = (e && e[0] == '1') ? 1 : 0;
-    }
-    return on == 1;
 }
 
 // ------------------------------------------------------------------ head kernel
@@ -959,20 +826,6 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     }
     OptArgs o = opt_args(la, n, w);
     if (fc_chunks) o.fcpart = w.fcpart, o.fcchunks = fc_chunks;
-    const bool split_opt = split_optimizer();
-    if (!grad_only && split_opt) {
-        // the conv2 / conv3 / fc1-bias / fc2 update runs on the weight-gradient branch as
-        // soon as conv2's data gradient (the last reader of W2 / W3) is done; only conv1's
-        // update stays behind the conv1 weight gradient on the critical path
-        PQ_CHECK(cudaEventRecord(fk->ev[5], st), "fork3");
-        PQ_CHECK(cudaStreamWaitEvent(side2, fk->ev[5], 0), "fork3 wait");
-        OptArgs os = o;
-        os.s1 = s1, os.s2 = s2, os.s3 = s3;
-        os.lo1 = P_W2, os.hi1 = P_W4, os.lo2 = P_B4, os.hi2 = os.total;
-        const int64_t cnt = (P_W4 - P_W2) + (os.total - P_B4);
-        PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((cnt + 255) / 256)), dim3(256), 0, side2, os),
-                 "optimizer (conv2, conv3, fc)");
-    }
     {
         B1wOp::Args g = args_b1w(la, w, n, &s1);
         if (use_tma(n) && w.s2d) {  // over the space-to-depth stacks
@@ -988,18 +841,12 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
             PQ_CHECK((launch_gemm<64, true, true>(g, 1, st)), "conv1 wgrad");
         }
     }
-    if (!grad_only && split_opt) {  // conv1's update (main stream)
-        o.s1 = s1, o.s2 = s2, o.s3 = s3;
-        o.lo1 = P_W1, o.hi1 = P_W2, o.lo2 = P_W2, o.hi2 = P_W2;
-        PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((P_W2 - P_W1 + 255) / 256)), dim3(256), 0, st, o),
-                 "optimizer (conv1)");
-    }
     // join the weight-gradient branch
     PQ_CHECK(cudaEventRecord(fk->ev[3], side), "join");
     PQ_CHECK(cudaEventRecord(fk->ev[4], side2), "join 2");
     PQ_CHECK(cudaStreamWaitEvent(st, fk->ev[3], 0), "join wait");
     PQ_CHECK(cudaStreamWaitEvent(st, fk->ev[4], 0), "join wait 2");
-    if (!grad_only && !split_opt) {  // every parameter but fc1's weight, after the join
+    if (!grad_only) {  // every parameter but fc1's weight, after the join
         o.s1 = s1, o.s2 = s2, o.s3 = s3;
         o.lo1 = P_W1, o.hi1 = P_W4, o.lo2 = P_B4, o.hi2 = o.total;
         if (!la->idx && la->update_counter) o.bump = la->update_counter, o.bump_done = w.done;
@@ -1145,7 +992,7 @@ int pq_learn_step(const pq_learn_args *la, void *stream) {
     const int groups = la->ext_targets ? 1 : 2;
     int rc = forward_gemms(nets, ins, groups, n, w, st, true);
     if (rc) return rc;
-    rc = head(nets, groups, n, la->actions, w, 1, la, st, split_optimizer() || fused_backward(n, la, nullptr));
+    rc = head(nets, groups, n, la->actions, w, 1, la, st, fused_backward(n, la, nullptr));
     if (rc) return rc;
     return backward_and_update(la, n, w, st);
 }
@@ -1211,7 +1058,7 @@ int pq_learn_grad(const pq_learn_args *la, float *grad, void *stream) {
     const int groups = la->ext_targets ? 1 : 2;
     int rc = forward_gemms(nets, ins, groups, n, w, st, true);
     if (rc) return rc;
-    rc = head(nets, groups, n, la->actions, w, 1, la, st, split_optimizer());
+    rc = head(nets, groups, n, la->actions, w, 1, la, st, false);
     if (rc) return rc;
     return backward_and_update(la, n, w, st, grad);
 }

@@ -158,16 +158,13 @@ class DeviceRun:
     """Shared state and epoch driver of one device run (executor.py:341-594)."""
 
     def __init__(self, hp: HyperParams, sink=None, use_graphs: bool = True, graph_chunk: int = 25,
-                 hash_epochs: bool = True, sequential: bool = False, persistent: bool = False):
+                 hash_epochs: bool = True, sequential: bool = False):
         hp.validate()
         if not hp.concurrent:
             raise NotImplementedError("the device executor implements the concurrent modes "
                                       "('both', 'concurrent')")
         torch = N.require_cuda()
         self.sequential = sequential
-        # persistent learner (experimental): the epoch's C/F learner steps in one launch
-        # (pq_learn_run); the default is the CUDA-graph path of one-shot kernels
-        self.persistent = persistent
         self.torch = torch
         self.hp = hp
         self.sink = sink
@@ -206,13 +203,12 @@ class DeviceRun:
         self.idx_table = torch.zeros((self.updates + 1) * B, dtype=torch.int64, device="cuda")
         # pipelined target forward (bit-identical; batch 32: 70.6 vs 71.3 us/update);
         # PQ_PIPE_TARGET=0 runs the target forward inside each step
-        self.pipelined = os.environ.get("PQ_PIPE_TARGET", "1") != "0" and not persistent
+        self.pipelined = os.environ.get("PQ_PIPE_TARGET", "1") != "0"
         self.update_counter = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.step_counter = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.nonfinite = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
         self.act_ws, self.act_cap = self._own_ws(W)
         self.learn_ws, self.learn_cap = self._own_ws(B)
-        self.plearn_ws = None  # persistent-learner workspace, allocated on first use
         # PQ_PRIO=1 runs the learner's streams (and the library's wgrad branch) at the
         # highest priority; measured slower (86.7 vs 81.2 us per update), so off
         hi = -1 if os.environ.get("PQ_PRIO", "0") == "1" else 0
@@ -270,22 +266,10 @@ class DeviceRun:
             a = self._learn_args()
             N.check(N.load().pq_learn_target_prologue(N.C.byref(a), N.stream_ptr(stream)), "target prologue")
 
-    def learn_run(self, n_updates: int, stream=None):
-        """n_updates learner steps in one persistent launch (same counters and tables)."""
-        if self.plearn_ws is None:
-            nbytes = N.load().pq_plearn_workspace_bytes(self.learn_cap, self.hp.actions)
-            self.plearn_ws = self.torch.zeros(nbytes, dtype=self.torch.uint8, device="cuda")
-        a = self._learn_args()
-        a.ws = self.plearn_ws.data_ptr()
-        N.check(N.load().pq_learn_run(N.C.byref(a), n_updates, N.stream_ptr(stream)), "learn_run")
-
     def learn_epoch(self):
         """All C/F learner steps of the epoch on the current stream."""
-        if self.persistent:
-            self.learn_run(self.updates)
-        else:
-            for _ in range(self.updates):
-                self.learn_step()
+        for _ in range(self.updates):
+            self.learn_step()
 
     def act_step(self, stream=None):
         a = self._act_args()
@@ -413,13 +397,6 @@ class DeviceRun:
         # t labels come from the run-global device block counter, so the same
         # captured graph serves every epoch
         ra, rl = self.steps // na, self.updates // nl
-        if self.persistent:
-            with torch.cuda.stream(self.learn_stream):
-                self.learn_run(self.updates)
-            with torch.cuda.stream(self.act_stream):
-                for _ in range(ra):
-                    ga.replay()
-            return
         ia = il = 0
         while ia < ra or il < rl:
             if ia < ra:
@@ -630,10 +607,7 @@ class HostEnvRun(DeviceRun):
         self.act_stream.wait_stream(cur)
         self.learn_stream.wait_stream(cur)
         # the learner's whole epoch is enqueued first
-        if self.persistent:
-            with torch.cuda.stream(self.learn_stream):
-                self.learn_run(self.updates)
-        elif self.use_graphs:
+        if self.use_graphs:
             gl, nl = self._graphs["learn"]
             with torch.cuda.stream(self.learn_stream):
                 for _ in range(self.updates // nl):

@@ -31,11 +31,10 @@ for it in range(5):
     if it == 4:
         torch.cuda.synchronize()
         lib.pq_timeline(1, None, None)
-        lib.pq_plearn_timeline(1, None, None)
     theta, opt, _, _, _ = dnn._learn(theta, opt, target, mem.ring, mem.records, idx, B)
 torch.cuda.synchronize()
 recs = []
-for fn in (lib.pq_timeline, lib.pq_plearn_timeline):
+for fn in (lib.pq_timeline,):
     out = (ctypes.c_ulonglong * (256 * 12))()
     cnt = ctypes.c_int(0)
     fn(0, ctypes.addressof(out), ctypes.addressof(cnt))

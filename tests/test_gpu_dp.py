@@ -1,4 +1,4 @@
-"""Data-parallel learner (configs[4]) and persistent learner on one GPU.
+"""Data-parallel learner (configs[4]) on one GPU.
 
 The DP step's semantics are checked without a second GPU: the summed gradients of the
 shards of a batch ("virtual ranks" rank r of G, all on cuda:0) must add up to the
@@ -7,8 +7,7 @@ NCCL all-reduce would, then pq_rmsprop_apply) must equal the single-device learn
 step (agent.train_minibatch) up to fp32 summation order.  The per-sample forward rows
 are bit-identical whatever the batch composition (row independence, test_nn.py:117-124),
 so only the batch reductions of the weight gradients can differ: tolerance 1e-5
-relative.  The persistent learner (pq_learn_run) must reproduce the CUDA-graph learner
-step the same way."""
+relative."""
 
 import numpy as np
 import pytest
@@ -99,29 +98,3 @@ def test_dp_update_equals_single_device_step(memory, B):
     # the bf16 GEMM shadow follows the master
     assert torch.equal(learners[0].theta.shadow[:8192],
                        learners[0].theta.master[:8192].bfloat16().view(torch.int16))
-
-
-def test_persistent_learner_matches_graph_learner():
-    hp = HyperParams(C=1600, F=4, N=8000, W=8, batch_size=32, total_steps=1600, capacity=20000,
-                     seed=3, schedule=EpsilonSchedule(0.1, 0.1, 1))
-    r = DeviceRun(hp, use_graphs=False)
-    r.begin_epoch(0)
-    keep = [r.theta.master, r.theta.shadow, r.opt.m, r.opt.v, r.update_counter]
-    saved = [t.clone() for t in keep]
-    for steps in (1, 3):
-        for t, v in zip(keep, saved):
-            t.copy_(v)
-        r.target_prologue()   # the step counter was reset: re-prime the pipelined target forward
-        for _ in range(steps):
-            r.learn_step()
-        one_shot = [t.clone() for t in keep]
-        for t, v in zip(keep, saved):
-            t.copy_(v)
-        r.learn_run(steps)
-        torch.cuda.synchronize()
-        assert int(r.update_counter.item()) == steps == int(one_shot[4].item())
-        d = one_shot[0] - saved[0]
-        # one step: fp32 split-K order only; three steps: plus rare bf16 ReLU-mask flips
-        assert rel(r.theta.master - saved[0], d) < (1e-5 if steps == 1 else 5e-2)
-        assert rel(r.opt.v, one_shot[3]) < (1e-5 if steps == 1 else 5e-2)
-    assert int(r.nonfinite.item()) == 2**31 - 1

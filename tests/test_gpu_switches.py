@@ -1,8 +1,6 @@
 """The switch-selected GPU paths stay correct (each runs in a subprocess because the
 switches are read once per process):
 
-* PQ_CONV23=1 — fused conv2 -> conv3 forward with the shared-memory patch loader: the
-  same K order and MMA sequence as the separate GEMMs, so Q-values are bit-identical;
 * PQ_TMA=1 — the warp-specialised TMA engine forced at batch 32 (default: from 128):
   Q-values bit-identical, one learner step within fp32 summation order (1e-5) of the
   cp.async engine;
@@ -57,15 +55,12 @@ def run_probe(tmp_path, name, env, W=24, B=32):
     return np.load(out)
 
 
-def test_fused_conv23_and_forced_tma_match_default(tmp_path):
-    base = run_probe(tmp_path, "base", {"PQ_CONV23": "0", "PQ_TMA": "0"})
-    fused = run_probe(tmp_path, "fused", {"PQ_CONV23": "1", "PQ_TMA": "0"})
-    tma = run_probe(tmp_path, "tma", {"PQ_CONV23": "0", "PQ_TMA": "1"})
-    assert np.array_equal(fused["q"], base["q"])
+def test_forced_tma_matches_default(tmp_path):
+    base = run_probe(tmp_path, "base", {"PQ_TMA": "0"})
+    tma = run_probe(tmp_path, "tma", {"PQ_TMA": "1"})
     assert np.array_equal(tma["q"], base["q"])
     d = base["theta"] - base["theta0"]
-    for other in (fused, tma):
-        assert np.linalg.norm(other["theta"] - base["theta"]) <= 1e-5 * np.linalg.norm(d)
+    assert np.linalg.norm(tma["theta"] - base["theta"]) <= 1e-5 * np.linalg.norm(d)
 
 
 def test_conv1_shift_matches_im2col(tmp_path):
