@@ -276,8 +276,8 @@ def learner_sweep(memory, actions: int, batches=(32, 64, 128, 256, 512, 1024), s
     lib = N.load()
     out = []
     for B in batches:
-        theta = dnn.init_network(1, actions)
-        target = dnn.init_network(2, actions)
+        theta = dnn.init_network(dnn.network_sizes(actions), 1)
+        target = dnn.init_network(dnn.network_sizes(actions), 2)
         opt = dnn.OptState.zeros(theta)
         ws, cap = dnn.workspace(B, actions)
         flag = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
@@ -319,7 +319,7 @@ def act_sweep(actions: int, widths=(8, 32, 128, 512), reps: int = 50):
     from paper_2111_01264_b200 import nn as dnn
 
     lib = N.load()
-    net = dnn.init_network(3, actions)
+    net = dnn.init_network(dnn.network_sizes(actions), 3)
     out = []
     for W in widths:
         ring = torch.randint(0, 256, (4 * W, 84 * 84), dtype=torch.uint8, device="cuda")
@@ -360,8 +360,8 @@ def dp_learner(args, rank: int, world: int, dist, steps: int = 30):
     B = args.dp_batch
     mem = ReplayMemory(100_000)
     mem.prepopulate(FrameEnvSpec(key=77), 100_000, np.random.default_rng(4))
-    theta = dnn.init_network(5)
-    target = dnn.init_network(6)
+    theta = dnn.init_network(dnn.network_sizes(), 5)
+    target = dnn.init_network(dnn.network_sizes(), 6)
     opt = dnn.OptState.zeros(theta)
     lr = DataParallelLearner(theta, opt, target, mem, B, rank=rank, world_size=world)
     pcg = device_pcg(np.random.default_rng(8))
@@ -416,7 +416,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     total_epochs = args.warmup + args.steps
     hp = HyperParams(C=args.C, F=args.F, N=args.prefill, W=args.W, batch_size=args.B,
                      total_steps=args.C * total_epochs, capacity=args.capacity, seed=seed,
-                     schedule=EpsilonSchedule(0.1, 0.1, 1))
+                     schedule=EpsilonSchedule(0.1, 0.1, 1), eval_period=0)
     t_setup = time.perf_counter()
     runner = DeviceRun(hp, use_graphs=True, graph_chunk=25)
     torch.cuda.synchronize()

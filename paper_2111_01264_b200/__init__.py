@@ -12,7 +12,7 @@ from . import _native
 from .agent import EpsilonSchedule, HyperParams, MODES, epsilon_at, select_action, \
     target_update, td_targets, train_minibatch
 from .nn import OptConfig, OptState, Parameters, QNet, copy_parameters, forward, gradient, \
-    init_network, load_parameters, num_params, parameter_bytes, rmsprop_step, \
+    init_network, load_parameters, network_sizes, num_params, parameter_bytes, rmsprop_step, \
     save_parameters, theta_hash
 
 BACKEND = "b200"
@@ -25,8 +25,9 @@ def __getattr__(name):
         from . import replay
 
         return getattr(replay, name)
-    if name in ("run", "DeviceRun", "InferenceWorker", "RunRecord", "batched_inference",
-                "transaction_count", "rng_stream", "derived_seed"):
+    if name in ("run", "sequential_reference", "DeviceRun", "HostEnvRun", "InferenceWorker",
+                "RunRecord", "batched_inference", "transaction_count", "transaction_breakdown",
+                "rng_stream", "derived_seed"):
         from . import executor
 
         return getattr(executor, name)

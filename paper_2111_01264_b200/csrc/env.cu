@@ -162,8 +162,10 @@ __global__ void __launch_bounds__(256) k_act_env(const ActArgs a) {
         s_slot[1] = -1;
         int4 nst;
         if (term || trunc) {
-            a.e.ep_label[(int64_t)j * a.steps + epc] = t_label;
-            a.e.ep_ret[(int64_t)j * a.steps + epc] = ret;
+            if (epc < a.steps) {  // the episode log holds `steps` entries per sampler
+                a.e.ep_label[(int64_t)j * a.steps + epc] = t_label;
+                a.e.ep_ret[(int64_t)j * a.steps + epc] = ret;
+            }
             a.e.ep_count[j] = epc + 1;
             ret = 0.0;
             ep += 1;

@@ -14,23 +14,33 @@ The reference runs W sampler threads, one trainer thread and a lock-serialized
 * epoch barrier -- stream join, owner-major flush of the sampler buffers,
   theta-minus <- theta, theta hash (execute, executor.py:552-572).
 
-Concurrent modes ("both", "concurrent") are deterministic and reproduce the
-reference's schedule; the non-concurrent modes interleave blocking training with
-acting (executor.py:436-440) and are not offered on the device path.
+All four modes run on the device and are deterministic.  Concurrent modes ("both",
+"concurrent") act from theta-minus while the learner stream trains on the frozen replay
+memory.  Non-concurrent modes ("synchronized", "standard") act from theta and, before
+each lockstep block, run every blocking training event that is due (train_due,
+executor.py:457-460): flush the sampler buffers into the replay memory (owner-major),
+draw one minibatch from it and take one learner step (blocking_train_event,
+executor.py:436-440).  The samplers' Q rows always come from one batched forward (rows
+are bit-identical to single-state forwards, test_nn.py:117-124); the transaction
+counters follow the reference's InferenceWorker: one batched call per block when
+synchronized, one single-row call per step otherwise (executor.py:115-122).  For
+"standard" with W > 1 the reference is nondeterministic (executor.py:17-23); the device
+runs one legal serialisation of its train gate, the lockstep one.
 """
 
 from __future__ import annotations
 
 import os
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 
 from . import _native as N
 from .agent import HyperParams, epsilon_at
 from .envs import DeviceEnvs, FrameEnvSpec
-from .nn import OptState, QNet, copy_into, forward, init_network, theta_hash, workspace
+from .nn import OptState, QNet, copy_into, forward, init_network, network_sizes, theta_hash, \
+    workspace
 from .replay import REC_INTS, ReplayMemory, device_pcg, pcg_state_to_generator, \
     sample_indices_device
 
@@ -149,21 +159,24 @@ def config_echo(hp: HyperParams) -> dict:
         "eval_epsilon": repr(hp.eval_epsilon), "eps_start": repr(hp.schedule.start),
         "eps_end": repr(hp.schedule.end), "eps_anneal": str(hp.schedule.anneal_steps),
         "lr": repr(hp.opt.learning_rate), "rho": repr(hp.opt.rho), "kappa": repr(hp.opt.kappa),
-        "seed": str(hp.seed), "env": "frames84", "actions": str(hp.actions),
-        "episode_length": str(hp.episode_length), "terminal_p": repr(hp.terminal_p),
+        "seed": str(hp.seed), "env": hp.env, "hidden": str(hp.hidden),
+        "latency_us": repr(hp.latency_s * 1e6), "episode_length": str(hp.episode_length),
+        "state_dim": str(hp.state_dim), "action_count": str(hp.action_count),
+        "terminal_p": repr(hp.terminal_p),
     }
 
 
 class DeviceRun:
     """Shared state and epoch driver of one device run (executor.py:341-594)."""
 
-    def __init__(self, hp: HyperParams, sink=None, use_graphs: bool = True, graph_chunk: int = 25,
-                 hash_epochs: bool = True, sequential: bool = False):
+    def __init__(self, hp: HyperParams, env_factory=None, sink=None, use_graphs: bool = True,
+                 graph_chunk: int = 25, hash_epochs: bool = True, sequential: bool = False):
         hp.validate()
-        if not hp.concurrent:
-            raise NotImplementedError("the device executor implements the concurrent modes "
-                                      "('both', 'concurrent')")
+        config = config_echo(hp)
+        hp = apply_env_factory(hp, env_factory)
         torch = N.require_cuda()
+        # non-concurrent modes: blocking training events between lockstep blocks
+        self.blocking = not hp.concurrent
         self.sequential = sequential
         self.torch = torch
         self.hp = hp
@@ -184,7 +197,7 @@ class DeviceRun:
         prepop_env = FrameEnvSpec(derived_seed(hp.seed, ROLE_PREPOP, 1), hp.episode_length,
                                   hp.actions, hp.terminal_p)
         self.D.prepopulate(prepop_env, hp.N, rng_stream(hp.seed, ROLE_PREPOP))
-        self.theta = init_network(derived_seed(hp.seed, ROLE_INIT), hp.actions)
+        self.theta = init_network(network_sizes(hp.actions), derived_seed(hp.seed, ROLE_INIT))
         self.opt = OptState.zeros(self.theta)
         self.target = self.theta.copy()
         keys = [derived_seed(hp.seed, ROLE_SAMPLER, 1000 + j) for j in range(W)]
@@ -203,7 +216,7 @@ class DeviceRun:
         self.idx_table = torch.zeros((self.updates + 1) * B, dtype=torch.int64, device="cuda")
         # pipelined target forward (bit-identical; batch 32: 70.6 vs 71.3 us/update);
         # PQ_PIPE_TARGET=0 runs the target forward inside each step
-        self.pipelined = os.environ.get("PQ_PIPE_TARGET", "1") != "0"
+        self.pipelined = os.environ.get("PQ_PIPE_TARGET", "1") != "0" and not self.blocking
         self.update_counter = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.step_counter = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.nonfinite = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
@@ -217,8 +230,10 @@ class DeviceRun:
         self.epoch_start = 0
         self.counters = {"dfreeze_checks": 0, "dfreeze_violations": 0,
                          "prepop_pushes": self.D.version, "flush_pushes": 0}
-        self.record = RunRecord(config=config_echo(hp), seed=hp.seed, mode=hp.mode,
+        self.record = RunRecord(config=config, seed=hp.seed, mode=hp.mode,
                                 counters=self.counters)
+        self._flushed_blocks = 0   # lockstep blocks of this epoch already flushed into D
+        self._epoch_trains = 0     # blocking training events of this epoch
         self._graphs = None
         self._eval_idx = 0
         self._eval = None
@@ -243,11 +258,16 @@ class DeviceRun:
             grad_out=None, q_out=None, td_out=None, ws=self.learn_ws.data_ptr(),
             max_batch=self.learn_cap)
 
+    @property
+    def acting_params(self) -> QNet:
+        """theta-minus when concurrent, theta otherwise (executor.py:455, :521)."""
+        return self.target if self.hp.concurrent else self.theta
+
     def _act_args(self):
         hp = self.hp
         s = hp.schedule
         return N.PqActArgs(
-            net=self.target.struct(), envs=self.envs.struct(), ring=self.D.ring.data_ptr(),
+            net=self.acting_params.struct(), envs=self.envs.struct(), ring=self.D.ring.data_ptr(),
             staging=self.staging.data_ptr(), step_counter=self.step_counter.data_ptr(),
             W=hp.W, steps=self.steps, actions=hp.actions, episode_length=hp.episode_length,
             epoch_start=0, frame_capacity=self.D.frame_capacity,
@@ -325,13 +345,7 @@ class DeviceRun:
         hp = self.hp
         if not self.staged:
             return
-        lib = N.load()
-        tmp = self.torch.empty((hp.C, REC_INTS), dtype=self.torch.int32, device="cuda")
-        N.check(lib.pq_replay_flush(self.staging.data_ptr(), hp.W, self.steps, tmp.data_ptr(),
-                                    hp.C, 0, N.stream_ptr()), "flush")
-        base = self.epoch_bases[max(0, len(self.epoch_bases) - 1 - self.lag)]
-        self.D.push_device_records(tmp, hp.C, base)
-        self.counters["flush_pushes"] += hp.C
+        self.flush_transitions(self.steps)
         counts = self.envs.ep_count.cpu().numpy()
         labels = self.envs.ep_label.cpu().numpy()
         rets = self.envs.ep_ret.cpu().numpy()
@@ -341,6 +355,67 @@ class DeviceRun:
                 self.emit(int(labels[j, c]), "episode", repr(float(rets[j, c])))
         self.envs.ep_count.zero_()
         self.staged = False
+        self._flushed_blocks = 0
+
+    def flush_transitions(self, upto_block: int) -> None:
+        """Move the staged transitions of blocks [flushed, upto_block) into D in
+        owner-major order (ReplayMemory.flush, replay.py:82-93: ascending owner id, each
+        buffer chronological); executor.py:379-381."""
+        hp = self.hp
+        k0, k1 = self._flushed_blocks, upto_block
+        if k1 <= k0:
+            return
+        n = hp.W * (k1 - k0)
+        N.check(N.load().pq_replay_flush_range(
+            self.staging.data_ptr(), hp.W, self.steps, k0, k1, self.D.records.data_ptr(),
+            self.D.capacity, self.D.push_count, N.stream_ptr()), "flush")
+        base = self.epoch_bases[max(0, len(self.epoch_bases) - 1 - self.lag)]
+        self.D._advance(n, base)
+        self.D._prev = None
+        self.counters["flush_pushes"] += n
+        self._flushed_blocks = k1
+
+    def blocking_train_event(self, blocks_done: int) -> None:
+        """Non-concurrent training (executor.py:436-440): flush the buffered transitions,
+        then one minibatch drawn from the store as it is now (replay.py:61-66) and one
+        learner step; the store cannot change under it (serialised on the stream)."""
+        hp = self.hp
+        self.flush_transitions(blocks_done)
+        u = self._epoch_trains
+        B = hp.batch_size
+        sample_indices_device(self.trainer_pcg, len(self.D), B, out=self.idx_table[u * B:(u + 1) * B])
+        self.learn_step()
+        self._epoch_trains += 1
+        self.worker.train_calls += 1
+        self.counters["dfreeze_checks"] += 1
+
+    def count_epoch_predictions(self) -> None:
+        """InferenceWorker counters of one epoch: C/W batched W-row predictions when
+        synchronized (and always in sequential_reference, executor.py:617-618), C
+        single-row ones otherwise (executor.py:88-99, :115-122)."""
+        hp = self.hp
+        if hp.synchronized or self.sequential:  # sequential_reference: batched (:617-618)
+            self.worker.count_predict(hp.W, hp.concurrent, self.steps)
+        else:
+            self.worker.count_predict(1, hp.concurrent, hp.C)
+
+    def run_blocking_epoch(self) -> None:
+        """Lockstep blocks with the training events due before each block's prediction and
+        the rest after the last block (run_epoch_lockstep's train_due, executor.py:457-494;
+        sequential_reference, executor.py:609-633)."""
+        hp = self.hp
+        next_train = hp.F
+        for b in range(self.steps):
+            while next_train <= b * hp.W:
+                self.blocking_train_event(b)
+                next_train += hp.F
+            self.act_block(b)
+        while next_train <= hp.C:
+            self.blocking_train_event(self.steps)
+            next_train += hp.F
+
+    def act_block(self, b: int) -> None:
+        self.act_step()
 
     def begin_epoch(self, epoch: int):
         """Per-epoch tables: the trainer's C/F x B indices, each sampler's frame-slot
@@ -348,8 +423,10 @@ class DeviceRun:
         hp = self.hp
         torch = self.torch
         self.epoch_start = epoch * hp.C
-        sample_indices_device(self.trainer_pcg, len(self.D), self.updates * hp.batch_size,
-                              out=self.idx_table[: self.updates * hp.batch_size])
+        self._epoch_trains = 0
+        if not self.blocking:  # the store is frozen: the epoch's C/F draws up front
+            sample_indices_device(self.trainer_pcg, len(self.D), self.updates * hp.batch_size,
+                                  out=self.idx_table[: self.updates * hp.batch_size])
         base = self.D._reserve_frames(2 * hp.C)
         self.epoch_bases.append(base)
         per = 2 * self.steps
@@ -361,6 +438,11 @@ class DeviceRun:
         hp = self.hp
         torch = self.torch
         self.begin_epoch(epoch)
+        if self.blocking:
+            self.run_blocking_epoch()
+            self.staged = True
+            self.count_epoch_predictions()
+            return
         if self.use_graphs and self._graphs is None:
             self._graphs = self._capture()
         cur = torch.cuda.current_stream()
@@ -383,7 +465,7 @@ class DeviceRun:
         cur.wait_stream(self.act_stream)
         cur.wait_stream(self.learn_stream)
         self.staged = True
-        self.worker.count_predict(hp.W, True, self.steps)
+        self.count_epoch_predictions()
         self.worker.train_calls += self.updates
         self.counters["dfreeze_checks"] += self.updates
 
@@ -414,7 +496,7 @@ class DeviceRun:
         hp = self.hp
         if not hp.eval_period or boundary == 0 or boundary % hp.eval_period != 0:
             return
-        mean, std = self.evaluate(self.target, hp.eval_epsilon, hp.eval_episodes,
+        mean, std = self.evaluate(self.acting_params, hp.eval_epsilon, hp.eval_episodes,
                                   derived_seed(hp.seed, ROLE_EVAL, self._eval_idx))
         self._eval_idx += 1
         self.record.evals.append((boundary, mean, std))
@@ -427,11 +509,12 @@ class DeviceRun:
         torch = self.torch
         hp = self.hp
         lib = N.load()
-        if self._eval is None:
+        log = max(256, int(episodes))
+        if self._eval is None or self._eval[0].steps < log:
             envs = DeviceEnvs([derived_seed(hp.seed, ROLE_EVAL, 1000)],
-                              [np.random.default_rng(0)], 256)
+                              [np.random.default_rng(0)], log)
             ring = torch.zeros((64, 7056), dtype=torch.uint8, device="cuda")
-            staging = torch.empty((1, 256, REC_INTS), dtype=torch.int32, device="cuda")
+            staging = torch.empty((1, log, REC_INTS), dtype=torch.int32, device="cuda")
             counter = torch.zeros(1, dtype=torch.int32, device="cuda")
             ws, cap = self._own_ws(1)
             envs.reset_all(torch.zeros(1, dtype=torch.int32, device="cuda"), ring)
@@ -445,7 +528,7 @@ class DeviceRun:
         envs.ep_count.zero_()
         a = N.PqActArgs(
             net=params.struct(), envs=envs.struct(), ring=ring.data_ptr(),
-            staging=staging.data_ptr(), step_counter=counter.data_ptr(), W=1, steps=256,
+            staging=staging.data_ptr(), step_counter=counter.data_ptr(), W=1, steps=envs.steps,
             actions=hp.actions, episode_length=hp.episode_length, epoch_start=0,
             frame_capacity=64, eps_start=epsilon, eps_end=epsilon, eps_anneal=1,
             terminal_p=hp.terminal_p, q_out=None, ws=ws.data_ptr(), max_batch=cap,
@@ -531,19 +614,38 @@ class DeviceRun:
         self.record.duration_s = time.perf_counter() - wall0
 
 
-def sequential_reference(hp: HyperParams, sink=None, **kw) -> RunRecord:
+def apply_env_factory(hp: HyperParams, env_factory) -> HyperParams:
+    """The reference calls env_factory() for the prepopulation, probe, sampler and
+    evaluation envs (executor.py:348-360).  Here the envs live on the device, so the
+    factory must return a FrameEnvSpec: its episode_length / action_count / terminal_p
+    configure every env of the run (per-role keys are derived from the seed as
+    before).  None = the default env built from hp (default_env_factory, :211-218)."""
+    if env_factory is None:
+        return hp
+    spec = env_factory()
+    if not isinstance(spec, FrameEnvSpec):
+        raise ValueError("env_factory must return a FrameEnvSpec: the device executor runs the "
+                         f"synthetic 84x84 frame env on the GPU (got {type(spec).__name__})")
+    hp = replace(hp, episode_length=int(spec.episode_length), action_count=int(spec.action_count),
+                 terminal_p=float(spec.terminal_p))
+    hp.validate()
+    return hp
+
+
+def sequential_reference(hp: HyperParams, env_factory=None, sink=None, **kw) -> RunRecord:
     """The same arithmetic as run() in one lane, canonical order: per epoch all lockstep
     blocks then the epoch's minibatches (executor.py:596-637).  The determinism oracle
     of the concurrent device executor."""
     kw.setdefault("use_graphs", False)
-    return DeviceRun(hp, sink, sequential=True, **kw).execute()
+    return DeviceRun(hp, env_factory, sink, sequential=True, **kw).execute()
 
 
-def run(hp: HyperParams, sink=None, host_envs: bool = False, **kw) -> RunRecord:
+def run(hp: HyperParams, env_factory=None, sink=None, *, host_envs: bool = False,
+        **kw) -> RunRecord:
     """Execute the full training run described by hp on the GPU (executor.py:591-593).
     host_envs=True keeps the samplers' envs on the CPU (end-to-end path)."""
     cls = HostEnvRun if host_envs else DeviceRun
-    return cls(hp, sink, **kw).execute()
+    return cls(hp, env_factory, sink, **kw).execute()
 
 
 class HostEnvRun(DeviceRun):
@@ -554,8 +656,8 @@ class HostEnvRun(DeviceRun):
     env.step (csrc/host_env.cpp), H2D of the new frames into their ring slots.  The
     learner's graphs are enqueued for the whole epoch first and run concurrently."""
 
-    def __init__(self, hp: HyperParams, sink=None, **kw):
-        super().__init__(hp, sink, **kw)
+    def __init__(self, hp: HyperParams, env_factory=None, sink=None, **kw):
+        super().__init__(hp, env_factory, sink, **kw)
         torch = self.torch
         W = hp.W
         lib = N.load()
@@ -599,8 +701,14 @@ class HostEnvRun(DeviceRun):
     def run_epoch(self, epoch: int):
         hp = self.hp
         torch = self.torch
-        lib = N.load()
         self.begin_epoch(epoch)
+        self._seq = np.array([self.epoch_bases[-1]], dtype=np.int64)
+        self._epoch = epoch
+        if self.blocking:  # blocking training between the blocks, one stream
+            self.run_blocking_epoch()
+            self.staged = True
+            self.count_epoch_predictions()
+            return
         if self.use_graphs and self._graphs is None:
             self._graphs = self._capture()
         cur = torch.cuda.current_stream()
@@ -616,63 +724,72 @@ class HostEnvRun(DeviceRun):
             with torch.cuda.stream(self.learn_stream):
                 for _ in range(self.updates):
                     self.learn_step()
-        seq = np.array([self.epoch_bases[-1]], dtype=np.int64)
-        nf = np.zeros(1, dtype=np.int32)
-        neps = np.zeros(1, dtype=np.int32)
-        s = hp.schedule
-        net = self.target.struct()
-        ws, cap = self.act_ws.data_ptr(), self.act_cap
         with torch.cuda.stream(self.act_stream):
-            st = N.stream_ptr()
             for b in range(self.steps):
-                self.d_stacks.copy_(self.h_stacks, non_blocking=True)
-                self.h2d_bytes += self.h_stacks.numel() * 4
-                N.check(lib.pq_forward(net, self.D.ring.data_ptr(), self.d_stacks.data_ptr(), None, 4,
-                                       0, hp.W, hp.actions, self.d_q.data_ptr(), ws, cap, st),
-                        "forward")
-                self.h_q.copy_(self.d_q, non_blocking=True)
-                self.d2h_bytes += self.h_q.numel() * 4
-                self.act_stream.synchronize()
-                t_label0 = epoch * hp.C + b * hp.W + 1
-                first = int(seq[0])
-                neps[0] = 0
-                lib.pq_henv_step(N.C.addressof(self.henv), hp.W, self.h_q.data_ptr(), hp.actions,
-                                 hp.episode_length, hp.terminal_p, t_label0, s.start, s.end,
-                                 s.anneal_steps, seq.ctypes.data, self.D.frame_capacity,
-                                 self.h_frames.data_ptr(), nf.ctypes.data, self.h_stacks.data_ptr(),
-                                 self.h_rec.data_ptr(), self.ep_labels.ctypes.data,
-                                 self.ep_rets.ctypes.data, neps.ctypes.data)
-                self.h_staging[:, b].copy_(self.h_rec)
-                for k in range(int(neps[0])):
-                    lab = int(self.ep_labels[k])
-                    self.host_episodes[lab - t_label0].append((lab, float(self.ep_rets[k])))
-                self._h2d_frames(first, int(nf[0]))
+                self.act_block(b)
             self.staging.copy_(self.h_staging, non_blocking=True)
             self.h2d_bytes += self.h_staging.numel() * 4
         cur.wait_stream(self.act_stream)
         cur.wait_stream(self.learn_stream)
         self.staged = True
-        self.worker.count_predict(hp.W, True, self.steps)
+        self.count_epoch_predictions()
         self.worker.train_calls += self.updates
         self.counters["dfreeze_checks"] += self.updates
+
+    def act_block(self, b: int) -> None:
+        """One lockstep block with host samplers on the current stream: H2D stack table,
+        batched forward on the acting parameters, D2H Q-rows, host select_action + env
+        step (csrc/host_env.cpp), H2D of the new frames into their ring slots."""
+        hp = self.hp
+        torch = self.torch
+        lib = N.load()
+        s = hp.schedule
+        st = N.stream_ptr()
+        self.d_stacks.copy_(self.h_stacks, non_blocking=True)
+        self.h2d_bytes += self.h_stacks.numel() * 4
+        N.check(lib.pq_forward(self.acting_params.struct(), self.D.ring.data_ptr(),
+                               self.d_stacks.data_ptr(), None, 4, 0, hp.W, hp.actions,
+                               self.d_q.data_ptr(), self.act_ws.data_ptr(), self.act_cap, st),
+                "forward")
+        self.h_q.copy_(self.d_q, non_blocking=True)
+        self.d2h_bytes += self.h_q.numel() * 4
+        torch.cuda.current_stream().synchronize()
+        t_label0 = self._epoch * hp.C + b * hp.W + 1
+        seq = self._seq
+        first = int(seq[0])
+        nf = np.zeros(1, dtype=np.int32)
+        neps = np.zeros(1, dtype=np.int32)
+        lib.pq_henv_step(N.C.addressof(self.henv), hp.W, self.h_q.data_ptr(), hp.actions,
+                         hp.episode_length, hp.terminal_p, t_label0, s.start, s.end,
+                         s.anneal_steps, seq.ctypes.data, self.D.frame_capacity,
+                         self.h_frames.data_ptr(), nf.ctypes.data, self.h_stacks.data_ptr(),
+                         self.h_rec.data_ptr(), self.ep_labels.ctypes.data,
+                         self.ep_rets.ctypes.data, neps.ctypes.data)
+        self.h_staging[:, b].copy_(self.h_rec)
+        for k in range(int(neps[0])):
+            lab = int(self.ep_labels[k])
+            self.host_episodes[lab - t_label0].append((lab, float(self.ep_rets[k])))
+        self._h2d_frames(first, int(nf[0]))
+
+    def flush_transitions(self, upto_block: int) -> None:
+        if self.blocking and upto_block > self._flushed_blocks:  # staged rows to the device
+            k0 = self._flushed_blocks
+            self.staging[:, k0:upto_block].copy_(self.h_staging[:, k0:upto_block], non_blocking=True)
+            self.h2d_bytes += self.hp.W * (upto_block - k0) * REC_INTS * 4
+        super().flush_transitions(upto_block)
 
     def flush_and_merge(self):
         hp = self.hp
         if not self.staged:
             return
-        lib = N.load()
-        tmp = self.torch.empty((hp.C, REC_INTS), dtype=self.torch.int32, device="cuda")
-        N.check(lib.pq_replay_flush(self.staging.data_ptr(), hp.W, self.steps, tmp.data_ptr(),
-                                    hp.C, 0, N.stream_ptr()), "flush")
-        base = self.epoch_bases[max(0, len(self.epoch_bases) - 1 - self.lag)]
-        self.D.push_device_records(tmp, hp.C, base)
-        self.counters["flush_pushes"] += hp.C
+        self.flush_transitions(self.steps)
         for j in range(hp.W):
             for lab, ret in self.host_episodes[j]:
                 self.record.episodes.append((lab, ret))
                 self.emit(lab, "episode", repr(ret))
             self.host_episodes[j] = []
         self.staged = False
+        self._flushed_blocks = 0
 
     def record_epoch_hash(self, boundary: int):
         super().record_epoch_hash(boundary)

@@ -29,6 +29,7 @@ FRAME = 84
 STACK = 4
 FRAME_BYTES = FRAME * FRAME
 HIDDEN = 512
+STATE_DIM = STACK * FRAME_BYTES
 
 
 def layer_shapes(actions: int = 18):
@@ -180,8 +181,24 @@ class OptState:
         return N.PqOpt(self.m.data_ptr(), self.v.data_ptr())
 
 
-def init_network(seed: int, actions: int = 18) -> QNet:
-    """nn.init_network (nn.py:93-109) over the flattened Nature-CNN weight matrices."""
+def network_sizes(actions: int = 18) -> list:
+    """The reference's layer-size list for this network: [state_dim, hidden, actions]
+    (executor.py:352-354 builds it from the env and hp.hidden)."""
+    return [STATE_DIM, HIDDEN, int(actions)]
+
+
+def init_network(layer_sizes, seed: int) -> QNet:
+    """nn.init_network(layer_sizes, seed) (nn.py:93-109) over the flattened Nature-CNN
+    weight matrices.  layer_sizes is the reference's [state_dim, hidden, actions] list:
+    state_dim must be 4*84*84 (uint8 frame stacks) and hidden 512 (fc1); the conv stack
+    between them is the Nature-CNN's."""
+    sizes = [int(s) for s in layer_sizes]
+    if len(sizes) != 3 or sizes[0] != STATE_DIM or sizes[1] != HIDDEN:
+        raise ValueError(f"layer sizes must be [{STATE_DIM}, {HIDDEN}, actions] "
+                         f"(Nature-CNN over 4x84x84 frames); got {list(layer_sizes)}")
+    actions = sizes[2]
+    if not 1 <= actions <= 32:
+        raise ValueError("actions must lie in [1, 32]")
     rng = np.random.default_rng(seed)
     parts = []
     for o, i in layer_shapes(actions):

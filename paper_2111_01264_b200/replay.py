@@ -81,7 +81,9 @@ def sample_indices_device(pcg_dev, n: int, count: int, out=None, stream=None):
 
 @dataclass
 class Batch:
-    """A sampled minibatch: record slots into a device ReplayMemory."""
+    """A sampled minibatch: record slots into a device ReplayMemory.  It is also the
+    reference's ``list[Transition]`` (replay.py:61-66): len(), indexing and iteration
+    yield host Transitions (one gather of the whole batch on first use)."""
 
     memory: "ReplayMemory"
     idx: object  # torch.int64 [B] on the GPU
@@ -91,6 +93,38 @@ class Batch:
 
     def gather(self):
         return self.memory.gather(self.idx)
+
+    def transitions(self) -> list:
+        cached = self.__dict__.get("_host")
+        if cached is None:
+            s, a, r, s2, term = self.gather()
+            s, s2 = s.cpu().numpy(), s2.cpu().numpy()
+            a, r, term = a.cpu().numpy(), r.cpu().numpy(), term.cpu().numpy()
+            cached = [Transition(s[i], int(a[i]), float(r[i]), s2[i], bool(term[i]))
+                      for i in range(len(self))]
+            self.__dict__["_host"] = cached
+        return cached
+
+    def __iter__(self):
+        return iter(self.transitions())
+
+    def __getitem__(self, i):
+        return self.transitions()[i]
+
+
+def as_batch(batch) -> Batch:
+    """A Batch, or a reference-style list of frame-stack Transitions staged into a
+    scratch device memory in order (so train_minibatch / td_targets accept both)."""
+    if isinstance(batch, Batch):
+        return batch
+    items = list(batch)
+    if not items:
+        raise ValueError("empty batch")
+    mem = ReplayMemory(len(items), frame_capacity=8 * len(items) + 64)
+    for t in items:
+        mem.push(t)
+    torch = N.require_cuda()
+    return Batch(mem, torch.arange(len(items), device="cuda"))
 
 
 class ReplayMemory:

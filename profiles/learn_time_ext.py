@@ -18,7 +18,7 @@ from paper_2111_01264_b200.replay import ReplayMemory
 B = 32
 mem = ReplayMemory(40000)
 mem.prepopulate(FrameEnvSpec(key=5), 40000, np.random.default_rng(1))
-theta, target = dnn.init_network(1), dnn.init_network(2)
+theta, target = dnn.init_network(dnn.network_sizes(), 1), dnn.init_network(dnn.network_sizes(), 2)
 opt = dnn.OptState.zeros(theta)
 ws, cap = dnn.workspace(B, 18)
 flag = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")

@@ -11,7 +11,7 @@ from paper_2111_01264_b200.replay import ReplayMemory
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 mem = ReplayMemory(20000)
 mem.prepopulate(FrameEnvSpec(key=1), 10000, np.random.default_rng(0))
-theta = dnn.init_network(1)
+theta = dnn.init_network(dnn.network_sizes(), 1)
 target = theta.copy()
 opt = dnn.OptState.zeros(theta)
 rng = np.random.default_rng(1)

@@ -22,7 +22,7 @@ NAMES = {"G": "k_gemm", "F": "k_fused", "H": "k_head", "O": "k_optimizer", "P": 
          "2": "k_conv2_shift", "W": "k_conv1_wgrad_shift", "V": "k_conv2_wgrad_shift", "3": "k_conv3_shift", "4": "k_resident_a", "C": "k_conv3_dgrad_shift"}
 mem = ReplayMemory(40000)
 mem.prepopulate(FrameEnvSpec(key=5), 40000, np.random.default_rng(1))
-theta, target = dnn.init_network(1), dnn.init_network(2)
+theta, target = dnn.init_network(dnn.network_sizes(), 1), dnn.init_network(dnn.network_sizes(), 2)
 opt = dnn.OptState.zeros(theta)
 rng = np.random.default_rng(2)
 lib = N.load()

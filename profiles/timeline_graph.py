@@ -18,7 +18,7 @@ from paper_2111_01264_b200.executor import DeviceRun
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 chunk = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 hp = HyperParams(C=4000, F=4, N=20000, W=8, batch_size=B, total_steps=8000, capacity=50000, seed=3,
-                 schedule=EpsilonSchedule(0.1, 0.1, 1))
+                 schedule=EpsilonSchedule(0.1, 0.1, 1), eval_period=0)
 r = DeviceRun(hp, use_graphs=True, graph_chunk=chunk)
 r.flush_and_merge()
 r.run_epoch(0)  # captures the graphs

@@ -41,8 +41,8 @@ def memory():
 
 
 def fresh(seed=2):
-    theta = dnn.init_network(seed, A)
-    target = dnn.init_network(seed + 1, A)
+    theta = dnn.init_network(dnn.network_sizes(A), seed)
+    target = dnn.init_network(dnn.network_sizes(A), seed + 1)
     return theta, dnn.OptState.zeros(theta), target
 
 

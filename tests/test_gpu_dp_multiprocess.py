@@ -28,7 +28,7 @@ def _setup():
 
     mem = ReplayMemory(8192)
     mem.prepopulate(FrameEnvSpec(key=21, terminal_p=1 / 64), 6000, np.random.default_rng(3))
-    theta, target = dnn.init_network(7), dnn.init_network(8)
+    theta, target = dnn.init_network(dnn.network_sizes(), 7), dnn.init_network(dnn.network_sizes(), 8)
     opt = dnn.OptState.zeros(theta)
     idx = sample_indices_device(device_pcg(np.random.default_rng(9)), len(mem), B * STEPS)
     return mem, theta, target, opt, idx

@@ -346,7 +346,7 @@ def test_rmsprop_hand_value_and_non_finite():
 
 def test_act_step_bit_exact_vs_oracle_env_and_select_action():
     hp = HyperParams(C=48, F=4, N=100, W=8, batch_size=32, total_steps=48, capacity=1000,
-                     schedule=EpsilonSchedule(1.0, 0.1, 30), episode_length=4, seed=7)
+                     schedule=EpsilonSchedule(1.0, 0.1, 30), episode_length=4, seed=7, eval_period=0)
     runner = DeviceRun(hp, use_graphs=False)
     runner.begin_epoch(0)
     from paper_2111_01264_b200.executor import ROLE_SAMPLER, derived_seed, rng_stream
@@ -387,7 +387,7 @@ def test_act_step_bit_exact_vs_oracle_env_and_select_action():
 
 def test_run_is_deterministic_and_counts_transactions():
     hp = HyperParams(C=64, F=4, N=200, W=8, batch_size=32, total_steps=128, capacity=2000,
-                     schedule=EpsilonSchedule(1.0, 0.1, 100), episode_length=7, seed=3)
+                     schedule=EpsilonSchedule(1.0, 0.1, 100), episode_length=7, seed=3, eval_period=0)
     r1 = run(hp, graph_chunk=8)
     r2 = run(hp, use_graphs=False)
     assert r1.epoch_hashes == r2.epoch_hashes
@@ -404,7 +404,7 @@ def test_host_env_run_matches_device_env_run():
     """End-to-end path (CPU envs + select_action, H2D frames / D2H Q-rows per block)
     reproduces the all-device executor bit-exactly."""
     hp = HyperParams(C=64, F=4, N=200, W=8, batch_size=32, total_steps=128, capacity=2000,
-                     schedule=EpsilonSchedule(1.0, 0.1, 100), episode_length=7, seed=5)
+                     schedule=EpsilonSchedule(1.0, 0.1, 100), episode_length=7, seed=5, eval_period=0)
     r_dev = run(hp, graph_chunk=8)
     r_host = run(hp, host_envs=True, graph_chunk=8)
     assert r_dev.epoch_hashes == r_host.epoch_hashes
@@ -417,7 +417,7 @@ def test_concurrent_run_equals_sequential_reference():
     from paper_2111_01264_b200.executor import sequential_reference
 
     hp = HyperParams(C=64, F=4, N=200, W=8, batch_size=32, total_steps=192, capacity=2000,
-                     schedule=EpsilonSchedule(1.0, 0.1, 100), episode_length=9, seed=11)
+                     schedule=EpsilonSchedule(1.0, 0.1, 100), episode_length=9, seed=11, eval_period=0)
     assert run(hp, graph_chunk=8).to_csv_text() == sequential_reference(hp).to_csv_text()
 
 

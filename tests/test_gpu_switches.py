@@ -35,12 +35,12 @@ from paper_2111_01264_b200 import nn as dnn
 from paper_2111_01264_b200.envs import FrameEnvSpec
 from paper_2111_01264_b200.replay import ReplayMemory
 W, B = int(sys.argv[3]), int(sys.argv[4])
-net = dnn.init_network(5)
+net = dnn.init_network(dnn.network_sizes(), 5)
 x = np.random.default_rng(1).integers(0, 256, size=(W, 4, 84, 84), dtype=np.uint8)
 q = dnn.forward(net, x)
 mem = ReplayMemory(4096)
 mem.prepopulate(FrameEnvSpec(key=3), 2000, np.random.default_rng(2))
-theta, target = dnn.init_network(6), dnn.init_network(7)
+theta, target = dnn.init_network(dnn.network_sizes(), 6), dnn.init_network(dnn.network_sizes(), 7)
 idx = mem.sample_indices(B, np.random.default_rng(4))
 th2, _, _, _, _ = dnn._learn(theta, dnn.OptState.zeros(theta), target, mem.ring, mem.records, idx, B)
 np.savez(sys.argv[2], q=q, theta=th2.master.cpu().numpy(), theta0=theta.master.cpu().numpy())
@@ -87,7 +87,7 @@ def test_pipelined_target_forward_is_bit_identical(graphs, monkeypatch):
     from paper_2111_01264_b200.executor import run
 
     hp = HyperParams(C=400, F=4, N=2000, W=8, batch_size=32, total_steps=1200, capacity=5000, seed=3,
-                     schedule=EpsilonSchedule(1.0, 0.1, 600))
+                     schedule=EpsilonSchedule(1.0, 0.1, 600), eval_period=0)
     recs = []
     for flag in ("0", "1"):
         monkeypatch.setenv("PQ_PIPE_TARGET", flag)

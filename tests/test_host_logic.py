@@ -41,7 +41,9 @@ def test_epsilon_schedule():
 
 @pytest.mark.parametrize("kw", [dict(C=10, F=3), dict(C=10, W=3), dict(W=1),
                                 dict(N=11, capacity=10), dict(total_steps=15, C=10),
-                                dict(gamma=1.5), dict(actions=40), dict(batch_size=0)])
+                                dict(gamma=1.5), dict(action_count=40), dict(batch_size=0),
+                                dict(env="gridworld"), dict(hidden=32), dict(state_dim=32),
+                                dict(latency_s=1e-3)])
 def test_hyperparams_validate_rejects(kw):
     base = dict(C=10, F=2, W=2, N=5, capacity=10, total_steps=20)
     base.update(kw)
@@ -50,7 +52,7 @@ def test_hyperparams_validate_rejects(kw):
 
 
 def test_hyperparams_modes_and_transactions():
-    hp = HyperParams(C=40, F=4, W=4, total_steps=200, N=10, capacity=100)
+    hp = HyperParams(C=40, F=4, W=4, total_steps=200, N=10, capacity=100, eval_period=0)
     assert hp.mode == "both"
     assert hp.with_mode("concurrent").mode == "concurrent"
     assert transaction_count(hp, 200) == 200 // 4 + 200 // 4
@@ -131,3 +133,42 @@ def test_multiprocess_replicas_and_gradient_allreduce_gloo():
         assert len(set(seeds)) == 2          # distinct replica seeds
         assert mx == 2.5                     # max over ranks
         assert g == [3.0] * 8                # sum all-reduce of per-rank gradient shards
+
+
+def test_api_signatures_match_reference(reference_paraq):
+    """Drop-in surface: the reference's positional signatures and HyperParams fields
+    (executor.py:591-596, nn.py:93, agent.py:115-147)."""
+    import dataclasses
+    import inspect
+
+    from paraq import agent as ragent, executor as rexec, nn as rnn
+
+    from paper_2111_01264_b200 import executor, nn
+
+    for mine, ref in ((executor.run, rexec.run), (executor.sequential_reference,
+                                                  rexec.sequential_reference),
+                      (nn.init_network, rnn.init_network)):
+        pm = list(inspect.signature(mine).parameters.values())
+        pr = list(inspect.signature(ref).parameters.values())
+        assert [p.name for p in pm[:len(pr)]] == [p.name for p in pr]
+        assert all(p.kind == p.KEYWORD_ONLY or p.kind == p.VAR_KEYWORD for p in pm[len(pr):])
+    ours = {f.name: f for f in dataclasses.fields(HyperParams)}
+    for f in dataclasses.fields(ragent.HyperParams):
+        assert f.name in ours, f.name
+        if f.name not in ("env", "hidden", "latency_s", "state_dim", "action_count"):
+            d_ref = f.default if f.default is not dataclasses.MISSING else f.default_factory()
+            o = ours[f.name]
+            d_me = o.default if o.default is not dataclasses.MISSING else o.default_factory()
+            assert type(d_me).__name__ == type(d_ref).__name__, f.name
+            if not dataclasses.is_dataclass(d_ref):
+                assert d_me == d_ref, f.name
+    hp = HyperParams()
+    assert hp.actions == hp.action_count == 18 and hp.state_dim == 4 * 84 * 84
+
+
+def test_init_network_takes_reference_layer_sizes():
+    from paper_2111_01264_b200 import nn
+
+    with pytest.raises(ValueError):
+        nn.init_network([32, 256, 4], 0)   # the reference's MLP sizes have no conv stack here
+    assert nn.network_sizes(18) == [4 * 84 * 84, 512, 18]
