@@ -11,6 +11,20 @@ LIB = paper_2111_01264_b200/_lib/libparaq_b200.so
 
 all: $(LIB) oracle
 
+# profiling build with the timeline / per-CTA trace probes compiled in (PQ_LIB selects it)
+PLIB = paper_2111_01264_b200/_lib/probes/libparaq_b200.so
+POBJ = $(patsubst build/%.o,build/probes/%.o,$(OBJ))
+probes: $(PLIB)
+build/probes/%.o: paper_2111_01264_b200/csrc/%.cu $(HDR)
+	@mkdir -p build/probes
+	$(NVCC) $(NVFLAGS) -DPQ_PROBES=1 -c $< -o $@ 2> build/probes/$*.ptxas.log || (cat build/probes/$*.ptxas.log; exit 1)
+build/probes/%.host.o: paper_2111_01264_b200/csrc/%.cpp $(HDR)
+	@mkdir -p build/probes
+	g++ -O2 -std=c++17 -fPIC -ffp-contract=off -c $< -o $@
+$(PLIB): $(POBJ)
+	@mkdir -p paper_2111_01264_b200/_lib/probes
+	$(NVCC) $(ARCH) -shared -o $@ $(POBJ) -lcudart
+
 build/%.o: paper_2111_01264_b200/csrc/%.cu $(HDR)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
@@ -27,6 +41,6 @@ oracle:
 	$(MAKE) -s -C oracle
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(PLIB)
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean probes

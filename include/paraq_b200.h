@@ -43,6 +43,9 @@ int64_t pq_num_params(int actions);          /* 1,693,362 for 18 actions */
 int64_t pq_num_shadow(void);                 /* bf16 copies of the conv1..fc1 weights */
 /* Latency probes: enable/disable and read GEMM phase timestamps (out [256][12] ns). */
 int pq_timeline(int on, unsigned long long *out, int *count);
+/* Per-CTA trace of the learner kernels: out [8192][6] = start, dependency released,
+ * accumulator ready, end (ns), smid << 32 | linear CTA, tag << 48 | part << 40 | grid. */
+int pq_cta_trace(int on, unsigned long long *out, int *count);
 
 /* ---- one Q-network parameter set (theta or theta-minus), device memory ------------ */
 typedef struct pq_net {
@@ -59,6 +62,10 @@ typedef struct pq_opt {
 int pq_net_sync_shadow(pq_net net, void *stream);
 /* theta-minus <- theta (copy_parameters, nn.py:206-211; executor.py:559) */
 int pq_net_copy(pq_net dst, pq_net src, int actions, void *stream);
+/* L2 residency of the learner's working set: kernels launched into `stream` (and graph
+ * kernel nodes captured from it) keep [base, base + bytes) in the persisting L2 set-aside
+ * (hit_ratio of its lines, capped to the set-aside); bytes = 0 clears the window. */
+int pq_l2_persist(void *stream, const void *base, size_t bytes, float hit_ratio);
 
 /* ---- frame-stack addressing -------------------------------------------------------
  * A state is 4 frames; frames live in a uint8 ring [slots][7056].  Sample b,

@@ -67,8 +67,10 @@ EXPORTS = {
     "pq_num_params": ([C.c_int], C.c_int64),
     "pq_num_shadow": ([], C.c_int64),
     "pq_timeline": ([C.c_int, vp, vp], C.c_int),
+    "pq_cta_trace": ([C.c_int, vp, vp], C.c_int),
     "pq_net_sync_shadow": ([PqNet, vp], C.c_int),
     "pq_net_copy": ([PqNet, PqNet, C.c_int, vp], C.c_int),
+    "pq_l2_persist": ([vp, vp, C.c_size_t, C.c_float], C.c_int),
     "pq_sample_indices": ([vp, C.c_uint32, C.c_int64, vp, vp], C.c_int),
     "pq_replay_gather": ([vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp], C.c_int),
     "pq_replay_flush": ([vp, C.c_int, C.c_int, vp, C.c_int64, C.c_int64, vp], C.c_int),
@@ -111,10 +113,12 @@ class NativeError(RuntimeError):
     pass
 
 
-def load(path: str = LIB_PATH):
-    """Load and type the library (no GPU needed to load it)."""
+def load(path: str | None = None):
+    """Load and type the library (no GPU needed to load it).  PQ_LIB overrides the path
+    (profiling: the probe build from ``make probes``)."""
     global _lib
     if _lib is None:
+        path = path or os.environ.get("PQ_LIB") or LIB_PATH
         if not os.path.exists(path):
             raise NativeError(
                 f"{path} is missing: build the sm_100a library first (make, or "

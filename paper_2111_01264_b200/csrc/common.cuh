@@ -361,6 +361,12 @@ PQ_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); 
 PQ_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---------------------------------------------------------------- timeline probes
+// Compiled in only for profiling builds (make probes: -DPQ_PROBES=1 into _lib/probes/);
+// the shipped library carries none of their loads or branches.
+#ifndef PQ_PROBES
+#define PQ_PROBES 0
+#endif
+constexpr bool kProbes = PQ_PROBES != 0;
 // Runtime-gated phase timestamps (%globaltimer, ns) of CTA 0 of each launch plus the
 // last CTA's end, for latency analysis (pq_timeline_*).  Off by default.
 struct Timeline {
@@ -378,6 +384,41 @@ PQ_DEV unsigned long long gtime() {
     return t;
 }
 PQ_DEV bool tl_cta0() { return blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0; }
+
+// Per-CTA trace (pq_cta_trace): every CTA's thread 0 records its start, dependency
+// release, accumulator-ready and end times plus SM id, linear CTA index, kernel tag and
+// grid size.  Runtime-gated, off by default.
+struct CtaTrace {
+    int on;
+    unsigned n;
+    unsigned long long r[8192][6];
+};
+static __device__ CtaTrace g_ct;
+static __shared__ unsigned long long s_ct[3];
+static __shared__ int s_ct_on;  // thread 0's copy of g_ct.on (read once per CTA)
+PQ_DEV void ct_begin() {
+    if (!kProbes) return;
+    if (threadIdx.x == 0) {
+        s_ct_on = g_ct.on;
+        if (s_ct_on) s_ct[0] = gtime(), s_ct[1] = 0ull, s_ct[2] = 0ull;
+    }
+}
+PQ_DEV void ct_mark(int i) {
+    if (kProbes && threadIdx.x == 0 && s_ct_on) s_ct[i] = gtime();
+}
+PQ_DEV void ct_end(char tag, int part = 0) {
+    if (!kProbes || threadIdx.x != 0 || !s_ct_on) return;
+    const unsigned long long t = gtime();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const unsigned slot = atomicAdd(&g_ct.n, 1u);
+    if (slot >= 8192) return;
+    const unsigned lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+    g_ct.r[slot][0] = s_ct[0], g_ct.r[slot][1] = s_ct[1], g_ct.r[slot][2] = s_ct[2], g_ct.r[slot][3] = t;
+    g_ct.r[slot][4] = ((unsigned long long)smid << 32) | lin;
+    g_ct.r[slot][5] = ((unsigned long long)(unsigned char)tag << 48) | ((unsigned long long)part << 40) | total;
+}
 // slots 8..11 of a record: grid dims and a kernel tag (identify the launch)
 PQ_DEV void tl_ident(int slot, char tag) {
     g_tl.t[slot][8] = gridDim.x, g_tl.t[slot][9] = gridDim.y, g_tl.t[slot][10] = gridDim.z;
@@ -387,7 +428,7 @@ PQ_DEV void tl_ident(int slot, char tag) {
 // every CTA's thread 0 at its very end: the last CTA of a launch appends an 'E' record
 // (end time, grid dims, tag in slot 7) -- matched to the launch by grid and order
 PQ_DEV void tl_cta_end(char tag) {
-    if (!g_tl.on || threadIdx.x != 0) return;
+    if (!kProbes || !g_tl.on || threadIdx.x != 0) return;
     const unsigned total = gridDim.x * gridDim.y * gridDim.z;
     const unsigned key = (gridDim.x * 131u + gridDim.y * 7u + gridDim.z * 3u + (unsigned)tag) & 63u;
     __threadfence();
@@ -405,7 +446,7 @@ PQ_DEV void tl_cta_end(char tag) {
 struct TlProbe {
     bool on;
     unsigned long long t0, t1;
-    PQ_DEV TlProbe() : on(g_tl.on && tl_cta0() && threadIdx.x == 0), t0(on ? gtime() : 0ull), t1(0ull) {}
+    PQ_DEV TlProbe() : on(kProbes && g_tl.on && tl_cta0() && threadIdx.x == 0), t0(on ? gtime() : 0ull), t1(0ull) {}
     PQ_DEV void waited() {
         if (on) t1 = gtime();
     }

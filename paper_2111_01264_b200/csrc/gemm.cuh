@@ -806,8 +806,10 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
     static_assert(GEMM_A_BYTES + BN * 128 + (LA::U8 ? 128 * 64 : 0) <= SLOT, "slot size");
     constexpr int B_BYTES = BN * 128;
     // chunks in flight ahead of the MMA; refilling the slot of chunk i-2 (not i-1)
-    // gives each MMA a full iteration to retire before its slot is reused
-    constexpr int PRE = STAGES >= 4 ? STAGES - 2 : STAGES - 1;
+    // gives each MMA a full iteration to retire before its slot is reused.  Deep rings
+    // (>= 8 slots: the small-batch critical-path GEMMs, whose whole K range fits) put
+    // every chunk but at most one in flight before the first MMA.
+    constexpr int PRE = STAGES >= 8 ? STAGES - 1 : STAGES >= 4 ? STAGES - 2 : STAGES - 1;
     constexpr uint32_t IDESC = idesc_bf16(BN, AMN, BMN);
     constexpr int NA = 1024 / GEMM_THREADS;                   // A chunks per thread (4)
     constexpr int BCH = BN * 8;                               // B chunks per stage
@@ -823,7 +825,7 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
     const uint32_t smem_s = R.smem_s;
     const uint32_t seq0 = FRESH ? 0u : R.seq;  // FRESH: a one-shot kernel's first tile
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const bool tl = g_tl.on && tl_cta0() && tid == 0;
+    const bool tl = kProbes && g_tl.on && tl_cta0() && tid == 0;
     int tl_i = 0;
     unsigned long long tl_t[12];
     if (tl) tl_t[tl_i++] = gtime();
@@ -958,6 +960,7 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
         }
     }
     hook();
+    ct_mark(1);
     if (tl) tl_t[tl_i++] = gtime();  // 1: predecessor done
     if constexpr (LA::TABLE && !EARLY_TABLE) fill_table();
     tc_fence_before();
@@ -1010,6 +1013,7 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
     }
     R.seq = seq0 + (uint32_t)nk;
     tc_fence_after();
+    ct_mark(2);
     if (tl) tl_t[tl_i++] = gtime();  // 6: accumulator ready
 
     // epilogue: warp w reads TMEM lanes 32*(w%4).. (tile rows); the two warpgroups
@@ -1080,6 +1084,7 @@ struct GridDepHook {
 template <int BN, bool AMN, bool BMN, int ST, int PF, class LA, class LB, class EP>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm(const __grid_constant__ GemmArgs<LA, LB, EP> g) {
+    ct_begin();
     using Cfg = GemmCfg<BN, LA::U8, ST>;
     constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
     extern __shared__ uint8_t smem_raw[];
@@ -1103,6 +1108,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         g.ones_extent, R, GridDepHook{});
     if ((threadIdx.x >> 5) == 0) tmem_dealloc<TMEM_COLS>(tmem_base_s);
     tl_cta_end('G');
+    ct_end('G');
 }
 
 template <int BN, bool AMN, bool BMN, int ST = 0, int PF = 0, class LA, class LB, class EP>
@@ -1169,6 +1175,7 @@ PQ_HD constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
 template <class P0, class P1, class P2>
 __global__ void __launch_bounds__(GEMM_THREADS, 2) k_fused(const __grid_constant__ FusedArgs<P0, P1, P2> f) {
+    ct_begin();
     constexpr int STAGES = cmax(P0::STAGES, cmax(P1::STAGES, P2::STAGES));
     constexpr uint32_t COLS = (uint32_t)cmax(P0::TMEM_COLS, cmax(P1::TMEM_COLS, P2::TMEM_COLS));
     constexpr bool TABLE = P0::TABLE || P1::TABLE || P2::TABLE;
@@ -1197,6 +1204,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2) k_fused(const __grid_constant
         P2::run(f.p2, lin - f.n0 - f.n1, R);
     if (gemm && (threadIdx.x >> 5) == 0) tmem_dealloc<COLS>(tmem_base_s);
     tl_cta_end('F');
+    ct_end('F', part);
 }
 
 template <class P0, class P1, class P2>

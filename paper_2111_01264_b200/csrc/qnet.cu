@@ -296,13 +296,16 @@ __device__ __forceinline__ void last_block_bump(int32_t *counter, uint32_t *done
 // optimizer can be split across streams without racing on the counter.
 __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a, int32_t *bump, uint32_t *done) {
     TlProbe tp;
+    ct_begin();
     head_sample<FC1_SPLITS>(a, blockIdx.x, [&] {
         griddep_wait();
         griddep_launch();
         tp.waited();
+        ct_mark(1);
     });
     if (bump) last_block_bump(bump, done);
     tp.done('H');
+    ct_end('H');
 }
 
 static bool fused_backward(int n, const pq_learn_args *la, float *grad_only);
@@ -389,6 +392,7 @@ __global__ void __launch_bounds__(512) k_fc2_partials(const float *h1, const flo
 // the parameters in [lo1, hi1) and [lo2, hi2), one per thread (learn_parts.cuh: opt_param)
 __global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
     TlProbe tp;
+    ct_begin();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t n1 = a.hi1 - a.lo1;
     const int64_t i = t < n1 ? a.lo1 + t : a.lo2 + (t - n1);
@@ -399,9 +403,11 @@ __global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
     griddep_wait();
     griddep_launch();
     tp.waited();
+    ct_mark(1);
     if (live) opt_param(a, i, upd, pre);
     if (a.bump) last_block_bump(a.bump, a.bump_done);
     tp.done('O');
+    ct_end('O');
 }
 
 // summed gradient of every parameter except fc1's weight (written by the fc1 wgrad GEMM)
@@ -636,9 +642,27 @@ static bool fused_backward(int n, const pq_learn_args *la, float *grad_only) {
 // reads what two or more launches back wrote; the same GEMM configurations as the one-shot
 // forward, so the results are bit-identical.  pq_learn_target_prologue primes
 // conv1..conv3 for the first step of an epoch.
-using F1Op = GemmOp<32, false, false, 3, 1, LoadFrames, LoadDense, EpiBiasRelu>;
-using F1LateOp = GemmOp<32, false, false, 3, 0, LoadFrames, LoadDense, EpiBiasRelu>;  // table after the wait
-using B4dTOp = GemmOp<32, true, false, 0, 1, LoadDense, LoadDense, EpiMaskT>;        // fc1 dgrad at BN 32
+// Ring depths of the small-batch critical path: every K-chunk of a tile in flight before
+// its first MMA (the whole K range fits in shared memory: conv1 4 chunks of 28 KB, conv2 /
+// conv3 / fc1-dgrad 8-9 of 24 / 20 KB, fc1 7 of 20 KB); one CTA per SM (grids <= 148)
+// (PQ_DEEP=0: the 3-4 slot rings)
+constexpr int DEEP_U8 = 6, DEEP_BN64 = 9, DEEP_BN32 = 9;
+static bool deep_rings() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("PQ_DEEP");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+template <bool D>
+struct Ring {
+    using F1 = GemmOp<32, false, false, D ? DEEP_U8 : 3, 1, LoadFrames, LoadDense, EpiBiasRelu>;
+    using F1Late = GemmOp<32, false, false, D ? DEEP_U8 : 3, 0, LoadFrames, LoadDense, EpiBiasRelu>;  // table after the wait
+    using B4dT = GemmOp<32, true, false, D ? DEEP_BN32 : 0, 1, LoadDense, LoadDense, EpiMaskT>;     // fc1 dgrad at BN 32
+    static constexpr int BN64 = D ? DEEP_BN64 : 0, BN32 = D ? DEEP_BN32 : 0;
+};
+using F1Op = Ring<false>::F1;
 using F23Op = GemmOp<64, false, false, 0, 2, LoadIm2col, LoadDense, EpiBiasRelu>;
 using F4Op = GemmOp<32, false, false, 0, 1, LoadDense, LoadDense, EpiF32T>;
 static F1Op::Args args_f1(const pq_net &net, const FwdInput &in, int n, bf16 *act1) {
@@ -681,26 +705,37 @@ static bool pipeline_ok(const pq_learn_args *la) {
            fused_backward(la->n, la, nullptr);
 }
 
+template <bool D>
+static int launch_b4d_t1(const pq_learn_args *la, int n, const WS &w, cudaStream_t st) {
+    using B4dTOp = typename Ring<D>::B4dT;
+    using F1LateOp = typename Ring<D>::F1Late;
+    const bf16 *sh = (const bf16 *)la->theta.shadow;
+    typename B4dTOp::Args g{};
+    g.a[0] = LoadDense{sh + S_W4, 512, 3136, 3136};
+    g.b[0] = LoadDense{w.dh1_bf, n, 512, 512};
+    g.e[0] = EpiMaskT{w.dY3, w.act3[0], 3136, n, 3136};
+    g.M = 3136, g.N = n, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
+    FusedArgs<B4dTOp, F1LateOp, NoOp> f{};
+    f.p0 = B4dTOp::make(g);
+    const F1Op::Args t1 = args_f1(la->target, target_input(la), n, w.act1[1]);
+    typename F1LateOp::Args t1l{};
+    t1l.a[0] = t1.a[0], t1l.b[0] = t1.b[0], t1l.e[0] = t1.e[0];
+    t1l.M = t1.M, t1l.N = t1.N, t1l.K = t1.K, t1l.kc_per_split = t1.kc_per_split, t1l.splits = 1, t1l.ones_at = -1;
+    f.p1 = F1LateOp::make(t1l);
+    f.n0 = B4dTOp::ctas(f.p0, 1), f.n1 = F1LateOp::ctas(f.p1, 1);
+    PQ_CHECK(launch_fused(f, 0, st), "fc1 dgrad | target conv1");
+    return 0;
+}
+
+
 static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStream_t st, bool pipe = false) {
     const pq_net &th = la->theta;
     const bf16 *sh = (const bf16 *)th.shadow;
     int s1 = 1, s2 = 1, s3 = 1;
     if (pipe) {  // fc1 dgrad + the target conv1 of the next step (its frame table after the wait:
                  // the head, the launch before, advanced the counter)
-        B4dTOp::Args g{};
-        g.a[0] = LoadDense{sh + S_W4, 512, 3136, 3136};
-        g.b[0] = LoadDense{w.dh1_bf, n, 512, 512};
-        g.e[0] = EpiMaskT{w.dY3, w.act3[0], 3136, n, 3136};
-        g.M = 3136, g.N = n, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
-        FusedArgs<B4dTOp, F1LateOp, NoOp> f{};
-        f.p0 = B4dTOp::make(g);
-        const F1Op::Args t1 = args_f1(la->target, target_input(la), n, w.act1[1]);
-        F1LateOp::Args t1l{};
-        t1l.a[0] = t1.a[0], t1l.b[0] = t1.b[0], t1l.e[0] = t1.e[0];
-        t1l.M = t1.M, t1l.N = t1.N, t1l.K = t1.K, t1l.kc_per_split = t1.kc_per_split, t1l.splits = 1, t1l.ones_at = -1;
-        f.p1 = F1LateOp::make(t1l);
-        f.n0 = B4dTOp::ctas(f.p0, 1), f.n1 = F1LateOp::ctas(f.p1, 1);
-        PQ_CHECK(launch_fused(f, 0, st), "fc1 dgrad | target conv1");
+        if (int rc = deep_rings() ? launch_b4d_t1<true>(la, n, w, st) : launch_b4d_t1<false>(la, n, w, st))
+            return rc;
     } else if (int rc = launch_b4d(th, n, w, st)) {
         return rc;
     }
@@ -897,6 +932,26 @@ int act_forward(pq_net net, const uint8_t *ring, const int32_t *stack, int W, in
     return rc;
 }
 
+// online conv1 (+ the target fc1 of this step) .. fc1 of the pipelined step
+template <bool D>
+static int forward_pipelined(const pq_learn_args *la, const FwdInput &in, int n, const WS &w, cudaStream_t st) {
+    using F1T = typename Ring<D>::F1;
+    {
+        FusedArgs<F1T, F4Op, NoOp> f{};
+        f.p0 = F1T::make(args_f1(la->theta, in, n, w.act1[0]));
+        f.p1 = F4Op::make(args_f4(la->target, w.act3[1], n, w.fc1part[1]));
+        f.n0 = F1T::ctas(f.p0, 1), f.n1 = F4Op::ctas(f.p1, 1);
+        PQ_CHECK(launch_fused(f, 0, st), "conv1 | target fc1");
+    }
+    PQ_CHECK((launch_gemm<64, false, false, Ring<D>::BN64, 2>(args_f2(la->theta, w.act1[0], n, w.act2[0]), 1, st)),
+             "conv2 forward");
+    PQ_CHECK((launch_gemm<64, false, false, Ring<D>::BN64, 2>(args_f3(la->theta, w.act2[0], n, w.act3[0]), 1, st)),
+             "conv3 forward");
+    PQ_CHECK((launch_gemm<32, false, false, Ring<D>::BN32, 1>(args_f4(la->theta, w.act3[0], n, w.fc1part[0]), 1, st)),
+             "fc1 forward");
+    return 0;
+}
+
 }  // namespace pq
 
 using namespace pq;
@@ -905,6 +960,20 @@ using namespace pq;
 extern "C" {
 
 int pq_abi_version(void) { return PQ_ABI_VERSION; }
+
+int pq_cta_trace(int on, unsigned long long *out, int *count) {
+    if (out) {
+        static CtaTrace h;
+        PQ_CHECK(cudaMemcpyFromSymbol(&h, g_ct, sizeof(CtaTrace)), "cta trace read");
+        *count = h.n < 8192 ? (int)h.n : 8192;
+        memcpy(out, h.r, sizeof(h.r));
+    }
+    static CtaTrace z;
+    memset(&z, 0, sizeof(z));
+    z.on = on;
+    PQ_CHECK(cudaMemcpyToSymbol(g_ct, &z, sizeof(CtaTrace)), "cta trace reset");
+    return 0;
+}
 
 int pq_timeline(int on, unsigned long long *out, int *count) {
     if (out) {
@@ -935,6 +1004,31 @@ int pq_workspace_layout(int max_batch, int actions, int64_t *offsets) {
                           w.act, w.dY3, w.dY2, w.dY1, w.part1, w.part2, w.part3, w.grad4, w.dY1p, w.dY2p,
                           w.act1s2[0], w.act1s2[1]};
     for (int i = 0; i < 26; ++i) offsets[i] = ptrs[i] ? (const char *)ptrs[i] - base : -1;
+    return 0;
+}
+
+int pq_l2_persist(void *stream, const void *base, size_t bytes, float hit_ratio) {
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaStreamAttrValue v{};
+    if (bytes && base) {
+        int dev = 0, max_persist = 0, max_window = 0;
+        PQ_CHECK(cudaGetDevice(&dev), "device");
+        PQ_CHECK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev), "persisting L2 size");
+        PQ_CHECK(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev), "window size");
+        const size_t set_aside = bytes < (size_t)max_persist ? bytes : (size_t)max_persist;
+        PQ_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, set_aside), "persisting L2 limit");
+        const size_t win = bytes < (size_t)max_window ? bytes : (size_t)max_window;
+        v.accessPolicyWindow.base_ptr = const_cast<void *>(base);
+        v.accessPolicyWindow.num_bytes = win;
+        // hit ratio scaled so the persisting lines fit the set-aside
+        const float fit = (float)set_aside / (float)win;
+        v.accessPolicyWindow.hitRatio = hit_ratio < fit ? hit_ratio : fit;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    } else {
+        v.accessPolicyWindow.num_bytes = 0;
+    }
+    PQ_CHECK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v), "access policy window");
     return 0;
 }
 
@@ -1009,19 +1103,8 @@ int pq_learn_step_pipelined(const pq_learn_args *la, void *stream) {
     WS w = carve(la->ws, la->max_batch, la->actions);
     const pq_net nets[2] = {la->theta, la->target};
     const FwdInput in{la->ring, la->records, la->idx_base, la->update_counter, n, REC_INTS, 0};
-    {
-        FusedArgs<F1Op, F4Op, NoOp> f{};
-        f.p0 = F1Op::make(args_f1(la->theta, in, n, w.act1[0]));
-        f.p1 = F4Op::make(args_f4(la->target, w.act3[1], n, w.fc1part[1]));
-        f.n0 = F1Op::ctas(f.p0, 1), f.n1 = F4Op::ctas(f.p1, 1);
-        PQ_CHECK(launch_fused(f, 0, st), "conv1 | target fc1");
-    }
-    PQ_CHECK((launch_gemm<64, false, false, 0, 2>(args_f2(la->theta, w.act1[0], n, w.act2[0]), 1, st)),
-             "conv2 forward");
-    PQ_CHECK((launch_gemm<64, false, false, 0, 2>(args_f3(la->theta, w.act2[0], n, w.act3[0]), 1, st)),
-             "conv3 forward");
-    PQ_CHECK((launch_gemm<32, false, false, 0, 1>(args_f4(la->theta, w.act3[0], n, w.fc1part[0]), 1, st)),
-             "fc1 forward");
+    if (int rc = deep_rings() ? forward_pipelined<true>(la, in, n, w, st) : forward_pipelined<false>(la, in, n, w, st))
+        return rc;
     if (int rc = head(nets, 2, n, la->actions, w, 1, la, st, true)) return rc;
     return backward_fused(la, n, w, st, true);
 }

@@ -199,6 +199,8 @@ class DeviceRun:
         self.D.prepopulate(prepop_env, hp.N, rng_stream(hp.seed, ROLE_PREPOP))
         self.theta = init_network(network_sizes(hp.actions), derived_seed(hp.seed, ROLE_INIT))
         self.opt = OptState.zeros(self.theta)
+        self.l2_persist = os.environ.get("PQ_L2", "0") == "1"
+        self._arena = self._pack_learner_state() if self.l2_persist else None
         self.target = self.theta.copy()
         keys = [derived_seed(hp.seed, ROLE_SAMPLER, 1000 + j) for j in range(W)]
         rngs = [rng_stream(hp.seed, ROLE_SAMPLER, j) for j in range(W)]
@@ -227,6 +229,7 @@ class DeviceRun:
         hi = -1 if os.environ.get("PQ_PRIO", "0") == "1" else 0
         self.act_stream = torch.cuda.Stream()
         self.learn_stream = torch.cuda.Stream(priority=hi)
+        self._persist(self.learn_stream)
         self.epoch_start = 0
         self.counters = {"dfreeze_checks": 0, "dfreeze_violations": 0,
                          "prepop_pushes": self.D.version, "flush_pushes": 0}
@@ -238,11 +241,36 @@ class DeviceRun:
         self._eval_idx = 0
         self._eval = None
 
+    def _pack_learner_state(self):
+        """theta's fp32 master, its bf16 shadow and the RMSProp moments in ONE allocation,
+        so one L2 access-policy window can keep the learner's parameter / optimizer traffic
+        (28 B per parameter per update) in the persisting L2 set-aside (PQ_L2=1; measured no
+        faster at batch 32: off by default)."""
+        torch = self.torch
+        th, op = self.theta, self.opt
+        parts = [th.master, op.m, op.v, th.shadow]
+        sizes = [(t.numel() * t.element_size() + 255) // 256 * 256 for t in parts]
+        arena = torch.zeros(sum(sizes), dtype=torch.uint8, device="cuda")
+        views, off = [], 0
+        for t, s in zip(parts, sizes):
+            nb = t.numel() * t.element_size()
+            v = arena[off:off + nb].view(t.dtype)
+            v.copy_(t)
+            views.append(v)
+            off += s
+        th.master, op.m, op.v, th.shadow = views
+        return arena
+
     def _own_ws(self, n):
         torch = self.torch
         cap = max(64, 1 << (int(n) - 1).bit_length())
         nbytes = N.load().pq_workspace_bytes(cap, self.hp.actions)
         return torch.zeros(nbytes, dtype=torch.uint8, device="cuda"), cap
+
+    def _persist(self, stream):
+        if self.l2_persist:
+            N.check(N.load().pq_l2_persist(N.stream_ptr(stream), self._arena.data_ptr(),
+                                           self._arena.numel(), 1.0), "l2 persist")
 
     # -- raw step launchers (stream-ordered, graph-capturable) ----------------------------
     def _learn_args(self):
@@ -321,6 +349,8 @@ class DeviceRun:
                             ("learn", self.learn_step, min(k, self.updates))):
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream()
+            if name == "learn":
+                self._persist(s)
             s.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(s):
                 with torch.cuda.graph(g, stream=s):

@@ -5,6 +5,10 @@ import ctypes
 import os
 import sys
 
+# the probe build (make probes): the shipped library has no timeline / trace probes
+os.environ.setdefault("PQ_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                             "paper_2111_01264_b200", "_lib", "probes", "libparaq_b200.so"))
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
