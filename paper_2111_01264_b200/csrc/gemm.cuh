@@ -136,6 +136,7 @@ struct LoadFrames {
     const int32_t *refs;
     const int64_t *map;
     const int32_t *counter;
+    int counter_add;  // the map row is (*counter + counter_add)
     int map_stride;
     int n, ref_stride, ref_off;
     FastDiv f400, f20;
@@ -167,7 +168,7 @@ struct LoadFrames {
     }
     // stage frame slots of samples [b_lo, b_hi] (all threads of the CTA)
     PQ_DEV void fill(int b_lo, int b_hi, int32_t *table) const {
-        const int64_t base = (map && counter) ? (int64_t)(*counter) * map_stride : 0;
+        const int64_t base = (map && counter) ? (int64_t)(*counter + counter_add) * map_stride : 0;
         for (int e = threadIdx.x; e < (b_hi - b_lo + 1) * 4; e += blockDim.x) {
             int b = b_lo + (e >> 2), c = e & 3;
             int32_t v = -1;
@@ -343,7 +344,7 @@ PQ_HD LoadWeightTP weight_tp(const bf16 *w, int O, int KS, int C, int tpc) {
 PQ_HD LoadFrames frames(const uint8_t *ring, const int32_t *refs, const int64_t *map,
                         const int32_t *counter, int map_stride, int n, int ref_stride, int ref_off) {
     LoadFrames l;
-    l.ring = ring, l.refs = refs, l.map = map, l.counter = counter, l.map_stride = map_stride;
+    l.ring = ring, l.refs = refs, l.map = map, l.counter = counter, l.counter_add = 0, l.map_stride = map_stride;
     l.n = n, l.ref_stride = ref_stride, l.ref_off = ref_off;
     l.f400 = FastDiv(400), l.f20 = FastDiv(20);
     return l;
@@ -1169,6 +1170,10 @@ struct FusedArgs {
     typename P1::Launch p1;
     typename P2::Launch p2;
     int n0, n1;  // CTAs of parts 0 and 1
+    // optional: CTA 0 copies *stash_src to *stash_dst (a step's update id for launches
+    // that must not read the live counter before their dependency wait)
+    const int32_t *stash_src;
+    int32_t *stash_dst;
 };
 
 PQ_HD constexpr int cmax(int a, int b) { return a > b ? a : b; }
@@ -1187,6 +1192,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2) k_fused(const __grid_constant
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int lin = blockIdx.x;
     const int part = lin < f.n0 ? 0 : lin < f.n0 + f.n1 ? 1 : 2;
+    if (f.stash_dst && lin == 0 && threadIdx.x == 0) *f.stash_dst = *f.stash_src;
     const bool gemm = part == 0 ? P0::GEMM : part == 1 ? P1::GEMM : P2::GEMM;
     if (gemm) {
         if (threadIdx.x == 0) {

@@ -111,6 +111,8 @@ struct WS {
     uint32_t *done;  // [3] CTA completion counters (unused, acting, head)
     int64_t *idx_cur;  // the step's sampled slots (stashed by the head)
     int32_t *upd_cur;  // the step's update id (stashed by the head)
+    int32_t *step_stash;  // the step's update id, copied by the step's first launch (read
+                          // before the dependency wait by later launches of the step)
     float *fcpart;     // fc2 / fc1-bias gradient partials per 64-sample chunk (large batches)
     bf16 *s2d;         // space-to-depth frame stacks [n][21][21][80] (TMA conv1, large batches)
     int n8;
@@ -151,6 +153,7 @@ static WS carve(void *base, int N, int A) {
     w.done = (uint32_t *)take(3 * sizeof(uint32_t));
     w.idx_cur = (int64_t *)take((size_t)N * 8);
     w.upd_cur = (int32_t *)take(sizeof(int32_t));
+    w.step_stash = (int32_t *)take(sizeof(int32_t));
     w.fcpart = (float *)take((size_t)((N + FC_CHUNK - 1) / FC_CHUNK) * (A + 2) * 512 * 4);
     w.s2d = N >= 128 ? (bf16 *)take((size_t)N * 441 * 80 * 2) : nullptr;
     w.dY1p = N >= 128 ? (bf16 *)take((size_t)N * 441 * 32 * 2) : nullptr;  // zeroed with the workspace
@@ -390,6 +393,32 @@ __global__ void __launch_bounds__(512) k_fc2_partials(const float *h1, const flo
 // ------------------------------------------------------------------ optimizer
 
 // the parameters in [lo1, hi1) and [lo2, hi2), one per thread (learn_parts.cuh: opt_param)
+// The single-stream learner's update launch: blocks [0, nb1) update conv1 (one parameter
+// per thread) once the conv1 weight gradient -- the launch before -- is complete; the
+// other blocks update conv2 / conv3 / fc1-bias / fc2 (pt parameters per thread, strided)
+// without waiting: their gradients were complete two or more launches back and their last
+// readers (the conv2 / conv3 data gradients) likewise, so they finish while conv1's
+// weight gradient drains.  Few enough blocks to be resident next to it.
+__global__ void __launch_bounds__(256) k_opt_tail(const OptArgs a, int nb1, int pt) {
+    const int upd = a.counter ? *a.counter : 0;
+    if ((int)blockIdx.x < nb1) {
+        const int64_t i = P_W1 + (int64_t)blockIdx.x * 256 + threadIdx.x;
+        const bool live = i < P_W2;
+        const OptPre pre = live ? opt_load(a, i) : OptPre{};
+        griddep_wait();
+        griddep_launch();
+        if (live) opt_param(a, i, upd, pre);
+        return;
+    }
+    griddep_launch();
+    const int64_t n2a = P_W4 - P_W2, n2 = n2a + (a.total - P_B4);
+    const int64_t T = (int64_t)(gridDim.x - nb1) * 256, t = (int64_t)(blockIdx.x - nb1) * 256 + threadIdx.x;
+    for (int k = 0; k < pt; ++k) {
+        const int64_t r = t + k * T;
+        if (r < n2) opt_param(a, r < n2a ? P_W2 + r : P_B4 + (r - n2a), upd);
+    }
+}
+
 __global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
     TlProbe tp;
     ct_begin();
@@ -620,10 +649,10 @@ struct OptOp {
 // Single-stream learner backward (cp.async engine, PQ_FUSED, default on below batch
 // 128): every launch chains to the next by PDL; the weight-gradient branch rides in
 // the critical-path launches as extra CTAs:
-//   B4d | {B3d, B3w, B4w+RMSProp} | {B2d, B2w} | {B1w, update of conv2/conv3/fc} | update of conv1
+//   B4d | {B3d, B3w, B4w+RMSProp} | {B2d, B2w} | B1w | update of all but W4
 // Each part reads only what the launch before it (or older ones) wrote: B4w rewrites
-// the W4 shadow after B4d read it; the conv2/conv3 update follows B3d / B2d, the last
-// readers of W3 / W2; conv1's update follows B1w.  The step counter advances in the head.
+// the W4 shadow after B4d read it; the update follows B3d / B2d / B1w, the last readers
+// of W3 / W2 and the last producer.  The step counter advances in the head.
 static bool fused_backward(int n, const pq_learn_args *la, float *grad_only) {
     static int on = -1;
     if (on < 0) {
@@ -658,7 +687,7 @@ static bool deep_rings() {
 template <bool D>
 struct Ring {
     using F1 = GemmOp<32, false, false, D ? DEEP_U8 : 3, 1, LoadFrames, LoadDense, EpiBiasRelu>;
-    using F1Late = GemmOp<32, false, false, D ? DEEP_U8 : 3, 0, LoadFrames, LoadDense, EpiBiasRelu>;  // table after the wait
+    using F1Late = F1;  // the target conv1 of the next step: table from the step stash
     using B4dT = GemmOp<32, true, false, D ? DEEP_BN32 : 0, 1, LoadDense, LoadDense, EpiMaskT>;     // fc1 dgrad at BN 32
     static constexpr int BN64 = D ? DEEP_BN64 : 0, BN32 = D ? DEEP_BN32 : 0;
 };
@@ -717,16 +746,38 @@ static int launch_b4d_t1(const pq_learn_args *la, int n, const WS &w, cudaStream
     g.M = 3136, g.N = n, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
     FusedArgs<B4dTOp, F1LateOp, NoOp> f{};
     f.p0 = B4dTOp::make(g);
-    const F1Op::Args t1 = args_f1(la->target, target_input(la), n, w.act1[1]);
-    typename F1LateOp::Args t1l{};
-    t1l.a[0] = t1.a[0], t1l.b[0] = t1.b[0], t1l.e[0] = t1.e[0];
-    t1l.M = t1.M, t1l.N = t1.N, t1l.K = t1.K, t1l.kc_per_split = t1.kc_per_split, t1l.splits = 1, t1l.ones_at = -1;
-    f.p1 = F1LateOp::make(t1l);
+    // the next minibatch's frames: update id = the stash of this step's first launch + 1,
+    // so the frame table and the frames are requested before the wait (the head, the
+    // launch before, is what advances the live counter)
+    F1Op::Args t1 = args_f1(la->target, target_input(la), n, w.act1[1]);
+    t1.a[0].counter = w.step_stash;
+    t1.a[0].counter_add = 1;
+    f.p1 = F1LateOp::make(t1);
     f.n0 = B4dTOp::ctas(f.p0, 1), f.n1 = F1LateOp::ctas(f.p1, 1);
     PQ_CHECK(launch_fused(f, 0, st), "fc1 dgrad | target conv1");
     return 0;
 }
 
+
+// conv1 weight gradient (+ the pipelined target conv3 of the next step); the deep ring
+// (7 x 32 KB: all 5 K-chunks of a split in flight) needs the launch alone on its SMs
+template <bool D>
+static int launch_b1w(const pq_learn_args *la, int n, const WS &w, cudaStream_t st, bool pipe, int *s1) {
+    using B1 = GemmOp<64, true, true, D ? 7 : 3, 1, LoadFrames, LoadDense, EpiF32T>;  // frames before the wait
+    typename B1::Launch b1 = B1::make(args_b1w(la, w, n, s1));
+    if (pipe) {  // + the target conv3 of the next step
+        FusedArgs<B1, F23Op, NoOp> f{};
+        f.p0 = b1, f.p1 = F23Op::make(args_f3(la->target, w.act2[1], n, w.act3[1]));
+        f.n0 = B1::ctas(f.p0, 1), f.n1 = F23Op::ctas(f.p1, 1);
+        PQ_CHECK(launch_fused(f, 0, st), "conv1 wgrad | target conv3");
+    } else {
+        FusedArgs<B1, NoOp, NoOp> f{};
+        f.p0 = b1;
+        f.n0 = B1::ctas(f.p0, 1), f.n1 = 0;
+        PQ_CHECK(launch_fused(f, 0, st), "conv1 wgrad");
+    }
+    return 0;
+}
 
 static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStream_t st, bool pipe = false) {
     const pq_net &th = la->theta;
@@ -764,27 +815,15 @@ static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStrea
         PQ_CHECK(launch_fused(f, 0, st), "conv2 dgrad | conv2 wgrad");
     }
     OptArgs o = opt_args(la, n, w);
-    o.s1 = s1, o.s2 = s2, o.s3 = s3;
-    {
-        B1wOp::Launch b1 = B1wOp::make(args_b1w(la, w, n, &s1));
-        o.s1 = s1;
-        OptArgs os = o;
-        os.lo1 = P_W2, os.hi1 = P_W4, os.lo2 = P_B4, os.hi2 = os.total;
-        if (pipe) {  // + the target conv3 of the next step (dispatched before the update CTAs)
-            FusedArgs<B1wOp, F23Op, OptOp> f{};
-            f.p0 = b1, f.p1 = F23Op::make(args_f3(tg, w.act2[1], n, w.act3[1])), f.p2 = os;
-            f.n0 = B1wOp::ctas(f.p0, 1), f.n1 = F23Op::ctas(f.p1, 1);
-            PQ_CHECK(launch_fused(f, OptOp::ctas(os), st), "conv1 wgrad | target conv3 | update");
-        } else {
-            FusedArgs<B1wOp, OptOp, NoOp> f{};
-            f.p0 = b1, f.p1 = os;
-            f.n0 = B1wOp::ctas(f.p0, 1), f.n1 = OptOp::ctas(os);
-            PQ_CHECK(launch_fused(f, 0, st), "conv1 wgrad | update conv2, conv3, fc");
-        }
-    }
-    o.lo1 = P_W1, o.hi1 = P_W2, o.lo2 = P_W2, o.hi2 = P_W2;
-    PQ_CHECK(launch_k(k_optimizer, dim3((unsigned)((P_W2 - P_W1 + 255) / 256)), dim3(256), 0, st, o),
-             "optimizer (conv1)");
+    o.s2 = s2, o.s3 = s3;
+    if (int rc = deep_rings() ? launch_b1w<true>(la, n, w, st, pipe, &s1) : launch_b1w<false>(la, n, w, st, pipe, &s1))
+        return rc;
+    o.s1 = s1;
+    // one update launch after the conv1 weight gradient: every parameter but fc1's weight
+    // (updated inside its weight-gradient GEMM); only conv1's rows wait on the launch before
+    const int nb1 = (int)((P_W2 - P_W1 + 255) / 256), nb2 = 64;
+    const int pt = (int)((P_W4 - P_W2 + o.total - P_B4 + nb2 * 256 - 1) / (nb2 * 256));
+    PQ_CHECK(launch_k(k_opt_tail, dim3((unsigned)(nb1 + nb2)), dim3(256), 0, st, o, nb1, pt), "optimizer");
     return 0;
 }
 
@@ -941,6 +980,7 @@ static int forward_pipelined(const pq_learn_args *la, const FwdInput &in, int n,
         f.p0 = F1T::make(args_f1(la->theta, in, n, w.act1[0]));
         f.p1 = F4Op::make(args_f4(la->target, w.act3[1], n, w.fc1part[1]));
         f.n0 = F1T::ctas(f.p0, 1), f.n1 = F4Op::ctas(f.p1, 1);
+        f.stash_src = la->update_counter, f.stash_dst = w.step_stash;
         PQ_CHECK(launch_fused(f, 0, st), "conv1 | target fc1");
     }
     PQ_CHECK((launch_gemm<64, false, false, Ring<D>::BN64, 2>(args_f2(la->theta, w.act1[0], n, w.act2[0]), 1, st)),
