@@ -346,6 +346,60 @@ def act_sweep(actions: int, widths=(8, 32, 128, 512), reps: int = 50):
     return out
 
 
+def sharded_acting(args, rank: int, world: int, dist, per_rank: int = 512, blocks: int = 20, epochs: int = 2):
+    """configs[2] acting sharded over the ranks (dist.ShardedActing): each rank
+    hosts per_rank synchronized envs (W = per_rank x ranks, weak scaling) and runs the
+    epoch's lockstep blocks (batched Q inference + epsilon-greedy + env step); per epoch a
+    theta-minus broadcast from rank 0 and an all-gather of the epoch's frames and records,
+    which rank 0 appends to its replay memory.  Env steps/s over all ranks, timed on the
+    device, max over ranks, collectives and the ingest included."""
+    import torch
+    from paper_2111_01264_b200 import nn as dnn
+    from paper_2111_01264_b200.agent import EpsilonSchedule, HyperParams
+    from paper_2111_01264_b200.dist import ShardedActing
+    from paper_2111_01264_b200.replay import ReplayMemory
+
+    W = per_rank * world
+    C = W * blocks
+    hp = HyperParams(C=C, F=4, N=0, W=W, batch_size=32, total_steps=C, capacity=4 * C, seed=args.seed,
+                     eval_period=0, schedule=EpsilonSchedule(0.1, 0.1, 1))
+    act = ShardedActing(hp, rank, world)
+    theta = dnn.init_network(dnn.network_sizes(hp.actions), 11) if rank == 0 else None
+    mem = ReplayMemory(4 * C, frame_capacity=3 * world * (4 * per_rank + 2 * C // world) + 1024) if rank == 0 else None
+
+    def epoch(e):
+        act.sync_target(theta)
+        act.act_epoch(e)
+        fr, rec, eps = act.gather_epoch()
+        if rank == 0:
+            ShardedActing.ingest(mem, fr, rec)
+
+    epoch(0)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for e in range(1, 1 + epochs):
+        epoch(e)
+    e1.record()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    steps = epochs * C
+    return {"W_total": W, "per_rank_envs": per_rank, "ranks": world, "blocks_per_epoch": blocks,
+            "env_steps_per_s": steps / (ms * 1e-3), "us_per_block": ms * 1e3 / (epochs * blocks),
+            "q_inference_tflops": FLOP_PER_STATE_ACT * steps / (ms * 1e-3) / 1e12,
+            "scaling": "weak",
+            "collective": ("theta-minus broadcast + all-gather of the epoch's frames / records per epoch "
+                           f"({dist.get_backend()})") if dist else "none (1 rank)"}
+
+
 def dp_learner(args, rank: int, world: int, dist, steps: int = 30):
     """configs[4] across ranks: global batch args.dp_batch split over the ranks, shard
     gradients sum-all-reduced over NCCL, identical RMSProp everywhere (dist.py).  All
@@ -386,7 +440,7 @@ def dp_learner(args, rank: int, world: int, dist, steps: int = 30):
     ups = steps / (ms / 1e3)
     return {"global_batch": B, "ranks": world, "per_rank_batch": lr.n, "updates_per_s": ups,
             "samples_per_s": ups * B, "tflops": FLOP_PER_SAMPLE_LEARN * B * ups / 1e12,
-            "collective": "NCCL all-reduce (sum) of the 6.77 MB fp32 gradient per update"
+            "collective": f"all-reduce (sum) of the 6.77 MB fp32 gradient per update over {dist.get_backend()}"
             if world > 1 else "none (1 rank)"}
 
 
@@ -466,6 +520,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     torch.cuda.empty_cache()
     if not args.no_sweeps:
         sweeps["dp_learner"] = dp_learner(args, rank, world, dist)
+        torch.cuda.empty_cache()
+        sweeps["acting_sharded"] = sharded_acting(args, rank, world, dist)
     torch.cuda.empty_cache()
     # end to end through the public API with host envs: H2D frames + D2H Q-rows per
     # lockstep block, theta hash D2H per epoch (the paper's CPU-env / GPU setting)

@@ -205,6 +205,8 @@ typedef struct pq_act_args {
     int max_batch;
     int max_episodes;           /* > 0: a sampler stops after this many finished episodes
                                    (evaluate_policy's exact episode budget) */
+    int sampler0;               /* global index of this launch's first sampler (sharded acting) */
+    int W_total;                /* samplers of the whole run (t labels); 0 = W */
 } pq_act_args;
 
 /* One synchronized block (executor.py:451-510): batched Q inference for the W current

@@ -57,7 +57,7 @@ class PqActArgs(C.Structure):
         ("epoch_start", C.c_int64), ("frame_capacity", C.c_int64),
         ("eps_start", C.c_double), ("eps_end", C.c_double), ("eps_anneal", C.c_int64),
         ("terminal_p", C.c_double), ("q_out", vp), ("ws", vp), ("max_batch", C.c_int),
-        ("max_episodes", C.c_int),
+        ("max_episodes", C.c_int), ("sampler0", C.c_int), ("W_total", C.c_int),
     ]
 
 

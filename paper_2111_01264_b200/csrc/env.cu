@@ -43,6 +43,7 @@ struct ActArgs {
     int32_t *step_counter;
     uint32_t *done;
     int W, steps, A, L;
+    int sampler0, W_total;  // sharded acting: global index of sampler 0, samplers of the run
     int64_t epoch_start, frame_capacity;
     double eps_start, eps_end;
     int64_t eps_anneal;
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(256) k_act_env(const ActArgs a) {
         // step_counter counts lockstep blocks (run-global in the executor); the
         // staging row is the block index within the epoch
         const int b = (int)(bg % a.steps);
-        const int64_t t_label = a.epoch_start + bg * a.W + j + 1;
+        const int64_t t_label = a.epoch_start + bg * a.W_total + a.sampler0 + j + 1;
         const double eps = epsilon_at(t_label, a.eps_start, a.eps_end, a.eps_anneal);
         Pcg64 g;
         g.load(pcg);
@@ -258,6 +259,7 @@ int pq_act_step(const pq_act_args *x, void *stream) {
     a.step_counter = x->step_counter;
     a.done = done;
     a.W = x->W, a.steps = x->steps, a.A = x->actions, a.L = x->episode_length;
+    a.sampler0 = x->sampler0, a.W_total = x->W_total > 0 ? x->W_total : x->W;
     a.epoch_start = x->epoch_start;
     a.frame_capacity = x->frame_capacity;
     a.eps_start = x->eps_start, a.eps_end = x->eps_end, a.eps_anneal = x->eps_anneal;

@@ -130,3 +130,180 @@ class DataParallelLearner:
         v = int(self.flag.item())
         if v != 2**31 - 1:
             raise ValueError(f"gradient contains non-finite entries (update {v})")
+
+
+# ---------------------------------------------------------------- sharded acting
+def pack_epoch(ring, hist, epoch_slots, staging):
+    """One rank's epoch of acting as a self-contained block (pure torch; any device):
+    frames = [the stack history at the epoch start (4 per sampler, zeros where masked),
+    the epoch's reserved frame slots]; records = the staged [Wl, steps, 8] transitions
+    with their 5 frame slots renumbered into that block (-1 stays -1)."""
+    import torch
+
+    Wl = hist.shape[0]
+    fcap = ring.shape[0]
+    hflat = hist.reshape(-1).long()
+    nh = hflat.numel()
+    lut = torch.full((fcap,), -1, dtype=torch.int64, device=ring.device)
+    valid = hflat >= 0
+    lut[hflat[valid]] = torch.arange(nh, device=ring.device)[valid]
+    lut[epoch_slots.long()] = nh + torch.arange(epoch_slots.numel(), device=ring.device)
+    frames = torch.zeros((nh + epoch_slots.numel(), ring.shape[1]), dtype=ring.dtype, device=ring.device)
+    frames[:nh][valid] = ring[hflat[valid]]
+    frames[nh:] = ring[epoch_slots.long()]
+    rec = staging.clone()
+    s = rec[..., :5].long()
+    rec[..., :5] = torch.where(s >= 0, lut[s.clamp(min=0)], torch.full_like(s, -1)).to(rec.dtype)
+    assert Wl == staging.shape[0]
+    return frames, rec
+
+
+def remap_gathered(records, frames_per_rank: int, first_seq: int, frame_capacity: int):
+    """Gathered per-rank records [G, Wl, steps, 8] (slots local to each rank's block) ->
+    [G*Wl, steps, 8] in global sampler order with slots into a ring where rank g's block
+    starts at sequence number first_seq + g * frames_per_rank (pure torch)."""
+    import torch
+
+    G = records.shape[0]
+    rec = records.clone()
+    s = rec[..., :5].long()
+    off = (first_seq + torch.arange(G, device=rec.device) * frames_per_rank).view(G, 1, 1, 1)
+    rec[..., :5] = torch.where(s >= 0, (s + off) % frame_capacity, torch.full_like(s, -1)).to(rec.dtype)
+    return rec.reshape(G * records.shape[1], records.shape[2], records.shape[3])
+
+
+class ShardedActing:
+    """Synchronized acting split across ranks (SURVEY.md §8(e), configs[2] / [1]): rank r
+    hosts samplers shard(W, r, G) -- their device envs, PCG64 streams and frames -- and a
+    theta-minus replica broadcast from rank 0 once per epoch; every lockstep block runs the
+    batched Q inference + epsilon-greedy + env step of its samplers only (row
+    independence, test_nn.py:117-124: Q rows do not depend on the batch), with the
+    global t-labels of the unsharded schedule (executor.py:488).  At the epoch boundary
+    the ranks' transitions and frames are gathered to rank 0, which appends them to its
+    replay memory in ascending global owner order (replay.py:82-93) -- bit-identical to
+    one GPU acting for all W samplers.  No per-block collective."""
+
+    def __init__(self, hp, rank: int = 0, world_size: int = 1, process_group=None):
+        from . import _native as N
+        from .envs import DeviceEnvs
+        from .executor import ROLE_SAMPLER, rng_stream
+        from .nn import QNet
+        from .replay import REC_INTS
+
+        hp.validate()
+        if hp.W % world_size:
+            raise ValueError("W must be a multiple of the number of ranks")
+        self.N, self.torch = N, N.require_cuda()
+        torch = self.torch
+        self.hp, self.rank, self.world_size, self.group = hp, rank, world_size, process_group
+        self.lo, self.hi = shard(hp.W, rank, world_size)
+        self.Wl = Wl = self.hi - self.lo
+        self.steps = hp.C // hp.W
+        self.per = 2 * self.steps  # frame slots per sampler per epoch (next + reset frame)
+        lag = -(-3 // self.steps) + 1
+        self.fcap = Wl * (self.per * (lag + 1) + 8) + 64
+        self.ring = torch.zeros((self.fcap, 7056), dtype=torch.uint8, device="cuda")
+        keys = [derived_seed(hp.seed, ROLE_SAMPLER, 1000 + j) for j in range(self.lo, self.hi)]
+        rngs = [rng_stream(hp.seed, ROLE_SAMPLER, j) for j in range(self.lo, self.hi)]
+        self.envs = DeviceEnvs(keys, rngs, self.steps)
+        self.envs.reset_all(torch.arange(Wl, dtype=torch.int32, device="cuda"), self.ring)
+        self.seq = Wl
+        self.target = QNet.empty(hp.actions)
+        self.staging = torch.full((Wl, self.steps, REC_INTS), -1, dtype=torch.int32, device="cuda")
+        self.counter = torch.zeros(1, dtype=torch.int32, device="cuda")
+        cap = max(64, 1 << (Wl - 1).bit_length())
+        self.ws = torch.zeros(N.load().pq_workspace_bytes(cap, hp.actions), dtype=torch.uint8, device="cuda")
+        self.ws_cap = cap
+        self.q_last = torch.zeros((Wl, hp.actions), dtype=torch.float32, device="cuda")
+        self.epoch = 0
+
+    def _dist(self):
+        import torch.distributed as dist
+
+        return dist if (self.world_size > 1 and dist.is_available() and dist.is_initialized()) else None
+
+    def sync_target(self, theta_minus=None) -> None:
+        """theta-minus <- rank 0's parameters (ncclBroadcast of the fp32 master once per
+        epoch, executor.py:557-559), then the bf16 GEMM shadow."""
+        dist = self._dist()
+        if self.rank == 0:
+            self.target.master.copy_(theta_minus.master)
+        if dist:
+            if dist.get_backend(self.group) == "gloo":
+                buf = self.target.master.cpu()
+                dist.broadcast(buf, 0, group=self.group)
+                self.target.master.copy_(buf)
+            else:
+                dist.broadcast(self.target.master, 0, group=self.group)
+        self.target.sync_shadow()
+
+    def act_epoch(self, epoch: int) -> None:
+        """The epoch's C/W lockstep blocks for this rank's samplers."""
+        torch, N, hp = self.torch, self.N, self.hp
+        self.epoch = epoch
+        self.hist = self.envs.stack.clone()
+        self.base = self.seq
+        self.seq += self.Wl * self.per
+        self.envs.slot_next.copy_(torch.arange(self.Wl, device="cuda", dtype=torch.int64) * self.per + self.base)
+        self.envs.ep_count.zero_()
+        s = hp.schedule
+        a = N.PqActArgs(
+            net=self.target.struct(), envs=self.envs.struct(), ring=self.ring.data_ptr(),
+            staging=self.staging.data_ptr(), step_counter=self.counter.data_ptr(), W=self.Wl,
+            steps=self.steps, actions=hp.actions, episode_length=hp.episode_length, epoch_start=0,
+            frame_capacity=self.fcap, eps_start=s.start, eps_end=s.end, eps_anneal=s.anneal_steps,
+            terminal_p=hp.terminal_p, q_out=self.q_last.data_ptr(), ws=self.ws.data_ptr(),
+            max_batch=self.ws_cap, max_episodes=0, sampler0=self.lo, W_total=hp.W)
+        for _ in range(self.steps):
+            N.check(N.load().pq_act_step(N.C.byref(a), N.stream_ptr()), "act_step")
+
+    def gather_epoch(self):
+        """All ranks' epoch blocks at every rank (all_gather; rank 0 consumes them):
+        frames [G, 4Wl + 2C/G, 7056], records [G, Wl, steps, 8], episodes."""
+        torch = self.torch
+        slots = (self.base + torch.arange(self.Wl * self.per, device="cuda")) % self.fcap
+        frames, rec = pack_epoch(self.ring, self.hist, slots, self.staging)
+        eps = torch.stack([self.envs.ep_count.to(torch.float64).unsqueeze(1).expand(-1, self.steps),
+                           self.envs.ep_label.to(torch.float64), self.envs.ep_ret], dim=-1)
+        dist = self._dist()
+        if not dist:
+            return frames[None], rec[None], eps[None]
+        out = []
+        for x in (frames, rec, eps):
+            if dist.get_backend(self.group) == "gloo":
+                parts = [torch.empty_like(x.cpu()) for _ in range(self.world_size)]
+                dist.all_gather(parts, x.cpu(), group=self.group)
+                out.append(torch.stack(parts).to(x.device))
+            else:
+                y = torch.empty((self.world_size,) + tuple(x.shape), dtype=x.dtype, device=x.device)
+                dist.all_gather_into_tensor(y, x.contiguous(), group=self.group)
+                out.append(y)
+        return tuple(out)
+
+    @staticmethod
+    def ingest(memory, frames, records, episodes=None):
+        """Rank 0: append the gathered epoch to the replay memory -- frames into freshly
+        reserved ring slots, records renumbered and flushed owner-major (global sampler
+        order = rank-major order of the contiguous shards).  Returns the finished episodes
+        [(t_label, return)] in owner order (executor.py:385-394)."""
+        from . import _native as N
+
+        G, Fr = frames.shape[0], frames.shape[1]
+        total = G * Fr
+        first = memory._reserve_frames(total)
+        torch = N.require_cuda()
+        slots = (first + torch.arange(total, device="cuda")) % memory.frame_capacity
+        memory.ring.index_copy_(0, slots, frames.reshape(total, -1))
+        rec = remap_gathered(records, Fr, first, memory.frame_capacity).contiguous()
+        W, steps = rec.shape[0], rec.shape[1]
+        N.check(N.load().pq_replay_flush_range(rec.data_ptr(), W, steps, 0, steps, memory.records.data_ptr(),
+                                               memory.capacity, memory.push_count, N.stream_ptr()), "flush")
+        memory._advance(W * steps, first)
+        memory._prev = None
+        out = []
+        if episodes is not None:
+            e = episodes.reshape(W, steps, 3).cpu().numpy()
+            for j in range(W):
+                for c in range(int(e[j, 0, 0])):
+                    out.append((int(e[j, c, 1]), float(e[j, c, 2])))
+        return out

@@ -172,3 +172,73 @@ def test_init_network_takes_reference_layer_sizes():
     with pytest.raises(ValueError):
         nn.init_network([32, 256, 4], 0)   # the reference's MLP sizes have no conv stack here
     assert nn.network_sizes(18) == [4 * 84 * 84, 512, 18]
+
+
+def _acting_worker(rank, world, port, out):
+    """Sharded-acting plumbing on CPU tensors: pack each rank's epoch block, all-gather
+    over gloo, renumber into one ring; rank 0 checks every stack against the originals."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = torch.Generator().manual_seed(rank)
+    Wl, steps, fcap, F = 3, 4, 64, 16
+    ring = torch.randint(0, 256, (fcap, F), dtype=torch.uint8, generator=g)
+    hist = torch.tensor([[-1, -1, 5, 6], [-1, 7, 8, 9], [10, 11, 12, 13]], dtype=torch.int32)
+    base = 20
+    ep = (base + torch.arange(Wl * 2 * steps)) % fcap
+    staging = torch.full((Wl, steps, 8), -1, dtype=torch.int32)
+    for j in range(Wl):
+        cur = hist[j].tolist()
+        for b in range(steps):
+            nxt = int(ep[j * 2 * steps + b])
+            staging[j, b, :5] = torch.tensor(cur + [nxt])
+            staging[j, b, 5] = 100 * rank + 10 * j + b
+            cur = cur[1:] + [nxt]
+    frames, rec = pdist.pack_epoch(ring, hist, ep, staging)
+    fr = [torch.empty_like(frames) for _ in range(world)]
+    rr = [torch.empty_like(rec) for _ in range(world)]
+    dist.all_gather(fr, frames)
+    dist.all_gather(rr, rec)
+    st = [torch.empty_like(staging) for _ in range(world)]
+    rings = [torch.empty_like(ring) for _ in range(world)]
+    dist.all_gather(st, staging)
+    dist.all_gather(rings, ring)
+    ok = True
+    if rank == 0:
+        big_cap, first = 500, 470   # wraps around the big ring
+        G, Fr = world, fr[0].shape[0]
+        big = torch.zeros((big_cap, F), dtype=torch.uint8)
+        slots = (first + torch.arange(G * Fr)) % big_cap
+        big[slots] = torch.cat(fr)
+        flat = pdist.remap_gathered(torch.stack(rr), Fr, first, big_cap)
+        for r in range(G):
+            for j in range(Wl):
+                for b in range(steps):
+                    orig, new = st[r][j, b], flat[r * Wl + j, b]
+                    assert int(new[5]) == int(orig[5])
+                    for c in range(5):
+                        o, n = int(orig[c]), int(new[c])
+                        assert (o < 0) == (n < 0)
+                        if o >= 0:
+                            ok &= torch.equal(big[n], rings[r][o])
+    out.put((rank, ok))
+    dist.destroy_process_group()
+
+
+def test_sharded_acting_pack_gather_remap_gloo():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + (os.getpid() % 2000)
+    procs = [ctx.Process(target=_acting_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res)
