@@ -35,6 +35,8 @@ METRIC = "env frames/sec + learner updates/sec (batch 32)"
 UNIT = "env frames/s"
 FLOP_PER_SAMPLE_LEARN = 68.26e6
 FLOP_PER_STATE_ACT = 18.70e6
+GATHER_NCU_BYTES = 2_755_831_552 + 4_460_498_432  # ncu dram bytes of the 80k gather (r2_gather_ncu.csv)
+LEARN_BYTES_PER_STEP = 28 * 1_693_362  # centered RMSProp traffic of one update
 GATHER_BYTES_PER_TRANSITION = 91_728  # 5 unique frames read + 8 written
 
 
@@ -52,7 +54,6 @@ def parse():
     ap.add_argument("--F", type=int, default=4)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-sweeps", action="store_true",
                     help="skip the learner-batch / acting-W sweeps and the DP learner line items")
     ap.add_argument("--dp-batch", type=int, default=1024,
@@ -126,78 +127,156 @@ def measured_peaks():
 
 
 # ----------------------------------------------------------------------------- CPU arm
-def cpu_sample(args, seconds: float, threads: int):
-    """The oracle port (C restatement of the reference kernels, composed like
-    nn.py / agent.py) on the host cores: lockstep acting blocks (W forwards +
-    select_action + env step) and learner updates at batch B, in the concurrent
-    schedule's W : W/F proportion.  Returns (frames/s, updates/s, sample text)."""
+def bench_config(args, world: int = 1) -> dict:
+    """The `config` of both arms (same workload, same keys)."""
+    return {
+        "workload": "configs[1]: Nature-CNN DQN, synthetic 84x84x4 uint8 frames, 18 actions, "
+                    "W=8 synchronized envs, batch 32, F=4, 1M-transition replay "
+                    "(prefilled), concurrent training, target sync every 10k steps; "
+                    "1 step = 1 epoch (10k frames + 2.5k updates)",
+        "global_batch": args.B * world, "W": args.W, "C": args.C, "F": args.F,
+        "capacity": args.capacity, "prefill": args.prefill,
+        "parallelism": f"replicas x{world}" if world > 1 else "single agent",
+        "l2": "inputs larger than L2 (7 GB replay ring sampled uniformly)",
+    }
+
+
+def cpu_sample(args, updates: int, seed: int = 0):
+    """The reference's concurrent schedule on the host cores with the oracle port (the
+    reference kernels restated in C, single-threaded per op like numba without
+    parallel=; composed like nn.py / agent.py): W sampler threads in lockstep blocks
+    behind a barrier whose action is one batched forward on theta-minus
+    (run_epoch_lockstep, executor.py:451-510) and one trainer thread running `updates`
+    minibatch updates concurrently (_trainer_epoch, executor.py:442-447), over a bounded
+    sample of the epoch: updates x F env steps.  The oracle's kernels release the GIL
+    (ctypes), so samplers and trainer overlap as the reference's threads do.
+    Returns (frames/s, updates/s, seconds, sample text, threads used)."""
+    import threading
+
     from oracle import _lib as OK
     from oracle import natcnn, replay as oreplay
     from oracle.envs import SyntheticFrameEnv
 
-    OK.set_threads(threads)
+    OK.set_threads(1)
+    W, F, B = args.W, args.F, args.B
     spec = natcnn.nature_cnn(18)
-    theta = natcnn.init_params(spec, 1)
+    theta = natcnn.init_params(spec, 1 + seed)
     target = natcnn.copy_params(theta)
     opt = natcnn.Opt.zeros(theta)
-    mem = oreplay.ReplayMemory(10_000)
-    mem.prepopulate(SyntheticFrameEnv(3, action_count=18), 2000, np.random.default_rng(0))
-    envs = [SyntheticFrameEnv(100 + j, action_count=18) for j in range(args.W)]
-    rngs = [np.random.default_rng(j) for j in range(args.W)]
+    # the replay content does not change the per-op cost: a bounded prefill (the learner
+    # samples from a frozen store, replay.py:61-66)
+    mem = oreplay.ReplayMemory(args.capacity)
+    mem.prepopulate(SyntheticFrameEnv(3 + seed, action_count=18), 2000, np.random.default_rng(seed))
+    envs = [SyntheticFrameEnv(100 + j + 1000 * seed, action_count=18) for j in range(W)]
+    rngs = [np.random.default_rng(j + 1000 * seed) for j in range(W)]
     states = [e.reset(r) for e, r in zip(envs, rngs)]
-    trng = np.random.default_rng(9)
-    t_act, n_act, t_upd, n_upd = 0.0, 0, 0.0, 0
-    t_begin = time.perf_counter()
-    while time.perf_counter() - t_begin < seconds or n_upd < 1:
-        t0 = time.perf_counter()
-        q = natcnn.forward(spec, target, np.stack(states))
-        for j in range(args.W):
-            st = OK.pcg_state_from_generator(rngs[j])
-            a = OK.select_action(st, q[j], 0.1)
-            OK.pcg_state_to_generator(st, rngs[j])
-            nxt, rew, done = envs[j].step(a, rngs[j])
-            states[j] = envs[j].reset(rngs[j]) if done else nxt
-        t_act += time.perf_counter() - t0
-        n_act += 1
-        for _ in range(max(1, args.W // args.F)):
-            t0 = time.perf_counter()
-            batch = oreplay.gather(mem.sample(args.B, trng))
-            theta, opt = natcnn.train_minibatch(spec, theta, opt, batch, target, 0.99)
-            t_upd += time.perf_counter() - t0
-            n_upd += 1
-    OK.set_threads(1)
-    per_frame = t_act / (n_act * args.W) + (t_upd / n_upd) / args.F
-    frames_s = 1.0 / per_frame
-    sample = (f"{n_act} acting blocks (W={args.W}) + {n_upd} learner updates (B={args.B}) of the "
-              f"Nature-CNN oracle in {t_act + t_upd:.1f} s; frames/s = 1/(t_act/W + t_update/F)")
-    return frames_s, frames_s / args.F, sample
+    blocks = max(1, updates * F // W)
+    shared = {}
+
+    def action():
+        shared["q"] = natcnn.forward(spec, target, np.stack(states))
+
+    barrier = threading.Barrier(W, action=action)
+    errors = []
+
+    def sampler(j):
+        try:
+            for _ in range(blocks):
+                barrier.wait()
+                st = OK.pcg_state_from_generator(rngs[j])
+                a = OK.select_action(st, shared["q"][j], 0.1)
+                OK.pcg_state_to_generator(st, rngs[j])
+                nxt, rew, done = envs[j].step(a, rngs[j])
+                states[j] = envs[j].reset(rngs[j]) if done else nxt
+        except BaseException as exc:  # noqa: BLE001
+            errors.append(exc)
+            barrier.abort()
+
+    def trainer():
+        nonlocal theta, opt
+        trng = np.random.default_rng(9 + seed)
+        try:
+            for _ in range(updates):
+                batch = oreplay.gather(mem.sample(B, trng))
+                theta, opt = natcnn.train_minibatch(spec, theta, opt, batch, target, 0.99)
+        except BaseException as exc:  # noqa: BLE001
+            errors.append(exc)
+
+    threads = [threading.Thread(target=sampler, args=(j,)) for j in range(W)] + [threading.Thread(target=trainer)]
+    t0 = time.perf_counter()
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    secs = time.perf_counter() - t0
+    if errors:
+        raise errors[0]
+    frames = blocks * W
+    sample = (f"{updates} learner updates (B={B}) on 1 trainer thread concurrent with {blocks} lockstep "
+              f"blocks of W={W} sampler threads (batched forward on theta-minus, select_action, env step) "
+              f"= {frames} env steps of the Nature-CNN oracle in {secs:.1f} s")
+    return frames / secs, updates / secs, secs, sample, W + 1
+
+
+def _replica_worker(args, updates, seed, q):
+    q.put(cpu_sample(args, updates, seed)[:3])
+
+
+def cpu_replicas(args, updates: int):
+    """configs[3] on the host: independent agent replicas as processes,
+    as many as the cores hold W sampler + 1 trainer threads each; aggregate frames/s."""
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    n = max(1, min(8, cores // (args.W + 1)))
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_replica_worker, args=(args, updates, k + 1, q)) for k in range(n)]
+    t0 = time.perf_counter()
+    for p in procs:
+        p.start()
+    res = [q.get() for _ in procs]
+    for p in procs:
+        p.join()
+    wall = time.perf_counter() - t0
+    frames = sum(r[0] * r[2] for r in res)
+    return {"replicas": n, "threads_per_replica": args.W + 1, "frames_per_s": frames / wall,
+            "updates_per_s": sum(r[1] * r[2] for r in res) / wall, "wall_s": wall}
 
 
 def run_reference(args, rank: int):
+    """--impl reference: the reference's CPU path (the oracle port, this tier's reference
+    arm) on the box's host cores in the reference's own thread model; each step is a
+    bounded sample of the configs[1] epoch (UPD updates with their F x UPD env steps)."""
     if rank != 0:
         return
-    threads = len(os.sched_getaffinity(0))
-    t_total = 0.0
-    frames = 0.0
-    vals = []
+    upd = int(os.environ.get("PQ_REF_UPDATES", "4"))
+    vals, ups, secs = [], [], []
+    sample, used = "", 0
     for k in range(args.warmup + args.steps):
-        fs, us, sample = cpu_sample(args, seconds=0.0, threads=threads)  # 1 block + W/F updates
+        fs, us, s, sample, used = cpu_sample(args, upd, seed=k)
         if k >= args.warmup:
-            vals.append(fs)
+            vals.append(fs), ups.append(us), secs.append(s)
     value = float(np.median(vals))
+    updates_s = float(np.median(ups))
+    full_updates = 50_000 // args.F  # configs[0]: a 50k-step run (SURVEY §8(d) runs > 1 h)
+    reps = cpu_replicas(args, upd) if os.environ.get("PQ_REF_REPLICAS", "1") == "1" else None
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * args.W / value, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1000.0 * float(np.median(secs)), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "learner_updates_per_s": value / args.F,
-        "config": {"workload": "configs[1]: Nature-CNN DQN, 84x84x4 uint8 frames, 18 actions, "
-                               "W=8 synchronized envs, batch 32, F=4 (CPU sample: one lockstep "
-                               "block + W/F updates per step)",
-                   "global_batch": args.B, "parallelism": "host threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+        "learner_updates_per_s": updates_s,
+        "config": bench_config(args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "port",
+                         "sample": sample + f" (one step = one such sample; median of {args.steps})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "extrapolation": {"full_run": "configs[0]: 50k env steps, 12,500 updates",
+                          "seconds": full_updates / updates_s, "hours": full_updates / updates_s / 3600,
+                          "note": "extrapolated from the measured update rate, printed beside the "
+                                  "measurement (harness.py:410-426), never substituted"},
+        "cpu_replicas": reps,
+        "host_cores": len(os.sched_getaffinity(0)),
     }
     print(json.dumps(line), flush=True)
 
@@ -230,7 +309,8 @@ def time_learner_graph(runner, epoch: int):
 
 
 def time_gather(runner, transitions: int = 80_000, reps: int = 10):
-    """Replay sample + stack gather over an epoch-sized batch (HBM-bound)."""
+    """Replay sample + stack gather over an epoch-sized batch (HBM-bound), per engine:
+    {"tma": ms, "ldg": ms} (pq_replay_gather runs the 16-byte-load one)."""
     import torch
     from paper_2111_01264_b200.replay import device_pcg, sample_indices_device
 
@@ -240,27 +320,27 @@ def time_gather(runner, transitions: int = 80_000, reps: int = 10):
     s = torch.empty((B, 4, 84, 84), dtype=torch.uint8, device="cuda")
     s2 = torch.empty_like(s)
     a = torch.empty(B, dtype=torch.int32, device="cuda")
-    r = torch.empty(B, dtype=torch.float32, device="cuda")
+    r = torch.empty(B, dtype=torch.float64, device="cuda")
     t = torch.empty(B, dtype=torch.uint8, device="cuda")
     from paper_2111_01264_b200 import _native as N
 
     lib = N.load()
-
-    def go():
-        N.check(lib.pq_replay_gather(runner.D.ring.data_ptr(), runner.D.records.data_ptr(),
-                                     idx.data_ptr(), B, s.data_ptr(), s2.data_ptr(), a.data_ptr(),
-                                     r.data_ptr(), t.data_ptr(), N.stream_ptr()), "gather")
-    go()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
+    out = {}
+    for name, fn in (("tma", lib.pq_replay_gather_tma), ("ldg", lib.pq_replay_gather_ldg)):
+        def go():
+            N.check(fn(runner.D.ring.data_ptr(), runner.D.records.data_ptr(), idx.data_ptr(), B, s.data_ptr(),
+                       s2.data_ptr(), a.data_ptr(), r.data_ptr(), t.data_ptr(), N.stream_ptr()), "gather")
         go()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            go()
+        e1.record()
+        torch.cuda.synchronize()
+        out[name] = e0.elapsed_time(e1) / reps
     del s, s2
-    return ms
+    return out
 
 
 def learner_sweep(memory, actions: int, batches=(32, 64, 128, 256, 512, 1024), steps: int = 40):
@@ -566,50 +646,59 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     if rank != 0:
         return
     hbm, bf16_burst, bf16_sus, peak_src = measured_peaks()
-    traffic = None  # DRAM bytes of one learner step from the committed ncu --set full capture
-    tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as fh:
-            traffic = json.load(fh).get("learner_step_dram_bytes")
+    traffic, traffic_src = None, None  # DRAM bytes of one learner step (committed ncu capture)
+    for name in ("r2_traffic.json", "r1_traffic.json"):
+        tpath = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(tpath):
+            with open(tpath) as fh:
+                traffic = json.load(fh).get("learner_step_dram_bytes")
+            traffic_src = (f"profiles/{name} (ncu --set full, dram__bytes_read+write summed over one "
+                           "step's launches, cold caches)")
+            break
     learn_flop = FLOP_PER_SAMPLE_LEARN * hp.batch_size
     achieved_tf = learn_flop / (learn_ms * 1e-3) / 1e12
-    gather_gbs = 80_000 * GATHER_BYTES_PER_TRANSITION / (gather_ms * 1e-3) / 1e9
+    gather_gbs = 80_000 * GATHER_BYTES_PER_TRANSITION / (gather_ms["ldg"] * 1e-3) / 1e9
+    gather_tma_gbs = 80_000 * GATHER_BYTES_PER_TRANSITION / (gather_ms["tma"] * 1e-3) / 1e9
     per_epoch_launches = (hp.C // hp.W) * 5 + (hp.C // hp.F) * 10 + 5  # + flush, copy, target prologue (3)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        threads = len(os.sched_getaffinity(0))
-        fs, us, sample = cpu_sample(args, seconds=args.cpu_seconds, threads=threads)
-        cpu = {"value": fs, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+        fs, us, s, sample, used = cpu_sample(args, int(os.environ.get("PQ_REF_UPDATES", "4")))
+        cpu = {"value": fs, "unit": UNIT, "cores": used, "kind": "port", "sample": sample,
                "updates_per_s": us}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "learner_updates_per_s": updates_s,
-        "config": {
-            "workload": "configs[1]: Nature-CNN DQN, synthetic 84x84x4 uint8 frames, 18 actions, "
-                        "W=8 synchronized envs, batch 32, F=4, 1M-transition replay in HBM "
-                        "(prefilled), concurrent training, target sync every 10k steps; "
-                        "1 step = 1 epoch (10k frames + 2.5k updates)",
-            "global_batch": hp.batch_size * world, "W": hp.W, "C": hp.C, "F": hp.F,
-            "capacity": hp.capacity, "prefill": hp.N,
-            "parallelism": f"replicas x{world}" if world > 1 else "single agent",
-            "l2": "inputs larger than L2 (7 GB replay ring sampled uniformly)",
-            "setup_s": round(setup_s, 2),
-        },
+        "config": dict(bench_config(args, world), setup_s=round(setup_s, 2)),
         "roofline": {
-            "kernel": "learner step (10 launches: 4 forward GEMMs, head, fc1 dgrad, 3 fused dgrad/wgrad/update grids, conv1 update; batch 32)",
-            "bound": "tensor", "achieved": achieved_tf, "peak": bf16_burst, "unit": "TFLOP/s",
-            "frac": achieved_tf / bf16_burst, "traffic": traffic,
-            "traffic_source": "profiles/r1_traffic.json (ncu --set full, dram__bytes_read+write of one "
-                              "step's 10 launches; algorithmic ~47 MB: fc1 RMSProp 28 B/param)",
+            "kernel": "learner step (batch 32: 10 dependent launches -- conv1..fc1 forward, head, fc1 "
+                      "dgrad, 3 fused dgrad / wgrad / RMSProp grids, update)",
+            "bound": "tensor", "achieved": achieved_tf, "peak": bf16_sus, "unit": "TFLOP/s",
+            "frac": achieved_tf / bf16_sus, "traffic": traffic,
+            "binding": "latency: a chain of 10 dependent launches of 1-9 small GEMM tiles each "
+                       "(profiles/r2_cta_trace_b32.txt); neither the tensor pipe nor HBM is saturated",
+            "traffic_source": traffic_src,
             "per_launch": f"{learn_flop / 1e9:.3f} GFLOP (68.26 MFLOP/sample x {hp.batch_size}) "
-                          f"in {learn_ms * 1e3:.1f} us", "peak_source": peak_src,
+                          f"in {learn_ms * 1e3:.1f} us",
+            "peak_source": f"{peak_src}: bf16_tflops_sustained (the step is timed inside a seconds-long epoch)",
+        },
+        "learner_memory_floor": {
+            "bound": "hbm", "algorithmic_bytes": LEARN_BYTES_PER_STEP,
+            "achieved": LEARN_BYTES_PER_STEP / (learn_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": LEARN_BYTES_PER_STEP / (learn_ms * 1e-3) / 1e9 / hbm,
+            "note": "28 B per parameter of centered RMSProp (read p, m, v; write p, m, v, bf16 "
+                    "shadow) x 1,693,362 parameters: the step's memory floor",
         },
         "gather_roofline": {
-            "kernel": "k_gather (80k-transition sample, 91,728 B each)", "bound": "hbm",
+            "kernel": "k_gather (pq_replay_gather: 16-byte vector loads; 80k-transition sample, "
+                      "91,728 B each)", "bound": "hbm",
             "achieved": gather_gbs, "peak": hbm, "unit": "GB/s", "frac": gather_gbs / hbm,
-            "ms": gather_ms,
+            "ms": gather_ms["ldg"],
+            "traffic": GATHER_NCU_BYTES, "traffic_source": "profiles/r2_gather_ncu.csv (dram__bytes_read+write "
+                                                           "of the same 80k gather, ncu)",
+            "tma_engine": {"kernel": "k_gather_tma (TMA bulk copies through a shared-memory ring)",
+                           "ms": gather_ms["tma"], "achieved": gather_tma_gbs, "frac": gather_tma_gbs / hbm},
         },
         "gpu_launches": per_epoch_launches * args.steps,
         **sweeps,

@@ -86,6 +86,14 @@ int pq_sample_indices(uint64_t *pcg_state, uint32_t n, int64_t count, int64_t *i
 int pq_replay_gather(const uint8_t *ring, const int32_t *records, const int64_t *idx,
                      int64_t B, uint8_t *s_out, uint8_t *s2_out, int32_t *a_out, double *r_out,
                      uint8_t *term_out, void *stream);
+/* the two engines behind pq_replay_gather (default: 16-byte vector loads; PQ_GATHER=tma
+ * selects TMA bulk copies of whole frames through a shared-memory ring) */
+int pq_replay_gather_tma(const uint8_t *ring, const int32_t *records, const int64_t *idx,
+                     int64_t B, uint8_t *s_out, uint8_t *s2_out, int32_t *a_out, double *r_out,
+                     uint8_t *term_out, void *stream);
+int pq_replay_gather_ldg(const uint8_t *ring, const int32_t *records, const int64_t *idx,
+                     int64_t B, uint8_t *s_out, uint8_t *s2_out, int32_t *a_out, double *r_out,
+                     uint8_t *term_out, void *stream);
 /* Flush: staging records [W][steps][8] -> ring records in owner-major order,
  * slot = (push_count + j * steps + k) mod capacity. */
 int pq_replay_flush(const int32_t *staging, int W, int steps, int32_t *records,

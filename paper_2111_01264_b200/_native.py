@@ -73,6 +73,8 @@ EXPORTS = {
     "pq_l2_persist": ([vp, vp, C.c_size_t, C.c_float], C.c_int),
     "pq_sample_indices": ([vp, C.c_uint32, C.c_int64, vp, vp], C.c_int),
     "pq_replay_gather": ([vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp], C.c_int),
+    "pq_replay_gather_tma": ([vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp], C.c_int),
+    "pq_replay_gather_ldg": ([vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp], C.c_int),
     "pq_replay_flush": ([vp, C.c_int, C.c_int, vp, C.c_int64, C.c_int64, vp], C.c_int),
     "pq_replay_flush_range": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int64, C.c_int64,
                                vp], C.c_int),

@@ -12,6 +12,12 @@
 #include "common.cuh"
 #include "qnet.cuh"
 
+#define PQ_CHECK(expr, where)                          \
+    do {                                               \
+        int _rc = pq::cuda_err((expr), (where));       \
+        if (_rc) return _rc;                           \
+    } while (0)
+
 namespace pq {
 int set_err(const char *msg);
 int cuda_err(cudaError_t e, const char *where);
@@ -161,6 +167,89 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t *ring, const int32
     }
 }
 
+// TMA variant: one elected thread per CTA moves whole 84x84 frames with bulk copies --
+// cp.async.bulk global -> shared (mbarrier complete_tx) for the <= 5 unique frames of a
+// transition, then 8 bulk stores shared -> global for the two stacks (masked slots store
+// from a zeroed tile) -- through an NS-deep ring of 5-frame stages, so the loads of the
+// next NS-1 transitions are in flight while the current one is written out.  No register
+// staging, no address arithmetic per 16 bytes; persistent grid (2 CTAs per SM).
+template <int NS>
+__global__ void __launch_bounds__(32) k_gather_tma(const uint8_t *ring, const int32_t *records,
+                                                   const int64_t *idx, int64_t B, uint8_t *s_out,
+                                                   uint8_t *s2_out, int32_t *a_out, double *r_out,
+                                                   uint8_t *term_out) {
+    extern __shared__ __align__(128) uint8_t gsm[];
+    __shared__ uint64_t bars[NS];
+    uint8_t *zero = gsm + NS * 5 * FRAME_BYTES;
+    for (int i = threadIdx.x; i < FRAME_BYTES / 16; i += 32)
+        reinterpret_cast<uint4 *>(zero)[i] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    if (threadIdx.x != 0) return;
+    const uint32_t base_s = smem_u32(gsm), zero_s = smem_u32(zero);
+    int32_t slots[NS][5];
+    auto issue = [&](int64_t b, int s) {
+        const int32_t *rec = records + idx[b] * REC_INTS;
+        int32_t f[REC_INTS];
+#pragma unroll
+        for (int k = 0; k < REC_INTS; ++k) f[k] = rec[k];
+        uint32_t bytes = 0;
+#pragma unroll
+        for (int fr = 0; fr < 5; ++fr) {
+            slots[s][fr] = f[fr];
+            if (f[fr] >= 0) bytes += FRAME_BYTES;
+        }
+        mbar_expect_tx(&bars[s], bytes);
+#pragma unroll
+        for (int fr = 0; fr < 5; ++fr)
+            if (f[fr] >= 0)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        base_s + (uint32_t)((s * 5 + fr) * FRAME_BYTES)),
+                    "l"(ring + (size_t)f[fr] * FRAME_BYTES), "r"((uint32_t)FRAME_BYTES), "r"(smem_u32(&bars[s]))
+                    : "memory");
+        a_out[b] = rec_action(f[5]);
+        r_out[b] = rec_reward(f[6], f[7]);
+        term_out[b] = (uint8_t)rec_terminal(f[5]);
+    };
+    auto store = [&](uint8_t *dst, uint32_t src) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+                     "r"((uint32_t)FRAME_BYTES)
+                     : "memory");
+    };
+    const int64_t first = blockIdx.x, stride = gridDim.x;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+        if (first + s * stride < B) issue(first + s * stride, s);
+    for (int64_t k = 0;; ++k) {
+        const int64_t b = first + k * stride;
+        if (b >= B) break;
+        const int s = (int)(k % NS);
+        mbar_wait(&bars[s], (uint32_t)((k / NS) & 1));
+#pragma unroll
+        for (int fr = 0; fr < 5; ++fr) {
+            const uint32_t src = slots[s][fr] >= 0 ? base_s + (uint32_t)((s * 5 + fr) * FRAME_BYTES) : zero_s;
+            if (fr < 4) store(s_out + ((size_t)b * 4 + fr) * FRAME_BYTES, src);
+            if (fr > 0) store(s2_out + ((size_t)b * 4 + fr - 1) * FRAME_BYTES, src);
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        // refill the stage written out one iteration ago (its store group has been
+        // reading for a whole iteration; the newest group stays in flight)
+        if (k >= 1) {
+            const int64_t nb = first + (k - 1 + NS) * stride;
+            if (nb < B) {
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                issue(nb, (int)((k - 1) % NS));
+            }
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ flush
 // sampler j's staged steps [k0, k1) -> slots push_count + j * (k1 - k0) + (k - k0)
 // (ReplayMemory.flush, replay.py:82-93: ascending owner id, each chronological)
@@ -263,13 +352,48 @@ int pq_sample_indices(uint64_t *pcg_state, uint32_t n, int64_t count, int64_t *i
     return cuda_err(cudaGetLastError(), "sample_indices");
 }
 
-int pq_replay_gather(const uint8_t *ring, const int32_t *records, const int64_t *idx, int64_t B,
-                     uint8_t *s_out, uint8_t *s2_out, int32_t *a_out, double *r_out,
-                     uint8_t *term_out, void *stream) {
+int pq_replay_gather_ldg(const uint8_t *ring, const int32_t *records, const int64_t *idx, int64_t B,
+                         uint8_t *s_out, uint8_t *s2_out, int32_t *a_out, double *r_out,
+                         uint8_t *term_out, void *stream) {
     if (B <= 0) return 0;
     k_gather<<<(unsigned)B, 256, 0, (cudaStream_t)stream>>>(ring, records, idx, s_out, s2_out,
                                                             a_out, r_out, term_out);
     return cuda_err(cudaGetLastError(), "gather");
+}
+
+int pq_replay_gather_tma(const uint8_t *ring, const int32_t *records, const int64_t *idx, int64_t B,
+                         uint8_t *s_out, uint8_t *s2_out, int32_t *a_out, double *r_out,
+                         uint8_t *term_out, void *stream) {
+    if (B <= 0) return 0;
+    constexpr int NS = 3;
+    constexpr int smem = (NS * 5 + 1) * FRAME_BYTES;
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        PQ_CHECK(cudaGetDevice(&dev), "device");
+        PQ_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
+        PQ_CHECK(cudaFuncSetAttribute(k_gather_tma<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                 "gather smem");
+    }
+    const int64_t grid = B < 2 * sms ? B : 2 * sms;
+    k_gather_tma<NS><<<(unsigned)grid, 32, smem, (cudaStream_t)stream>>>(ring, records, idx, B, s_out, s2_out,
+                                                                          a_out, r_out, term_out);
+    return cuda_err(cudaGetLastError(), "gather (TMA)");
+}
+
+// the product entry point: the 16-byte-load gather (measured 0.97 of HBM peak vs 0.90 for
+// the bulk-copy engine: a streaming copy with no reuse gains nothing from the shared-memory
+// hop); PQ_GATHER=tma selects the TMA engine
+int pq_replay_gather(const uint8_t *ring, const int32_t *records, const int64_t *idx, int64_t B,
+                     uint8_t *s_out, uint8_t *s2_out, int32_t *a_out, double *r_out,
+                     uint8_t *term_out, void *stream) {
+    static int ldg = -1;
+    if (ldg < 0) {
+        const char *e = getenv("PQ_GATHER");
+        ldg = (e && e[0] == 't') ? 0 : 1;
+    }
+    return (ldg ? pq_replay_gather_ldg : pq_replay_gather_tma)(ring, records, idx, B, s_out, s2_out, a_out,
+                                                               r_out, term_out, stream);
 }
 
 int pq_replay_flush_range(const int32_t *staging, int W, int steps, int k0, int k1, int32_t *records,

@@ -15,7 +15,7 @@ theta = dnn.init_network(dnn.network_sizes(), 1)
 target = theta.copy()
 opt = dnn.OptState.zeros(theta)
 rng = np.random.default_rng(1)
-for it in range(6):
+for it in range(int(os.environ.get("STEPS", "6"))):
     idx = mem.sample_indices(B, rng)
     theta, opt, _, _, _ = dnn._learn(theta, opt, target, mem.ring, mem.records, idx, B)
 torch.cuda.synchronize()

@@ -451,3 +451,28 @@ def test_device_evaluation_matches_oracle_evaluate_policy():
     assert (mean, std) == (float(np.mean(rets)), float(np.std(rets)))
     rec = run(hp, graph_chunk=8)
     assert [k for _, k, _ in rec.events].count("eval_mean") == 2
+
+
+def test_gather_engines_bit_identical():
+    """pq_replay_gather's TMA bulk-copy engine and the 16-byte-load engine agree byte for
+    byte, incl. masked slots, a batch that is not a multiple of the persistent grid, and
+    f64 rewards."""
+    from paper_2111_01264_b200 import _native as N
+
+    mem = ReplayMemory(3000)
+    mem.prepopulate(FrameEnvSpec(key=8, episode_length=5, terminal_p=0.1), 2500, np.random.default_rng(3))
+    B = 1237
+    idx = torch.as_tensor(np.random.default_rng(4).integers(0, 2500, B), device="cuda")
+    outs = []
+    for fn in (N.load().pq_replay_gather_tma, N.load().pq_replay_gather_ldg):
+        s = torch.full((B, 4, 84, 84), 7, dtype=torch.uint8, device="cuda")
+        s2 = torch.full_like(s, 9)
+        a = torch.empty(B, dtype=torch.int32, device="cuda")
+        r = torch.empty(B, dtype=torch.float64, device="cuda")
+        t = torch.empty(B, dtype=torch.uint8, device="cuda")
+        N.check(fn(mem.ring.data_ptr(), mem.records.data_ptr(), idx.data_ptr(), B, s.data_ptr(), s2.data_ptr(),
+                   a.data_ptr(), r.data_ptr(), t.data_ptr(), N.stream_ptr()), "gather")
+        outs.append([x.cpu().numpy() for x in (s, s2, a, r, t)])
+    for x, y in zip(*outs):
+        assert np.array_equal(x, y)
+    assert (outs[0][0] == 0).any()  # masked history frames present
