@@ -240,6 +240,7 @@ class DeviceRun:
         self._graphs = None
         self._eval_idx = 0
         self._eval = None
+        self._pending_eval = None
 
     def _pack_learner_state(self):
         """theta's fp32 master, its bf16 shadow and the RMSProp moments in ONE allocation,
@@ -522,52 +523,188 @@ class DeviceRun:
                     il += 1
 
     # -- evaluation (envs.evaluate_policy, envs.py:177-202; executor.py:396-412) ---------
+    # The evaluation runs on its own stream on a snapshot of the acting parameters
+    # (executor.py:401 copy_parameters), overlapped with the next epoch: CUDA-graph chunks
+    # of EVAL_CHUNK single-env act steps are replayed while the epoch runs, the episode
+    # count comes back through pinned memory, and steps after the last episode are no-ops
+    # in the kernel (max_episodes), so the result does not depend on how many chunks were
+    # enqueued.  The mean / std land in the record at the boundary's place (resolve_evals).
+    # With a streaming sink the evaluation completes before the boundary's events go out.
+    EVAL_CHUNK = 32
+
     def maybe_eval(self, boundary: int):
         hp = self.hp
         if not hp.eval_period or boundary == 0 or boundary % hp.eval_period != 0:
             return
-        mean, std = self.evaluate(self.acting_params, hp.eval_epsilon, hp.eval_episodes,
-                                  derived_seed(hp.seed, ROLE_EVAL, self._eval_idx))
+        seed = derived_seed(hp.seed, ROLE_EVAL, self._eval_idx)
         self._eval_idx += 1
-        self.record.evals.append((boundary, mean, std))
-        self.emit(boundary, "eval_mean", repr(mean))
-        self.emit(boundary, "eval_std", repr(std))
+        self.resolve_evals()  # one job in flight: the snapshot and the eval env are shared
+        job = self._eval_start(self.acting_params, hp.eval_epsilon, hp.eval_episodes, seed)
+        if self.sink is not None:
+            mean, std = self._eval_finish(job)
+            self.record.evals.append((boundary, mean, std))
+            self.emit(boundary, "eval_mean", repr(mean))
+            self.emit(boundary, "eval_std", repr(std))
+            return
+        slots = (len(self.record.events), len(self.record.evals))
+        self.record.events += [(boundary, "eval_mean", None), (boundary, "eval_std", None)]
+        self.record.evals.append((boundary, None, None))
+        self._pending_eval = (slots, boundary, job)
+
+    def resolve_evals(self):
+        """Finish the evaluation in flight and fill in its record entries."""
+        if self._pending_eval is None:
+            return
+        (i_ev, i_e), boundary, job = self._pending_eval
+        self._pending_eval = None
+        mean, std = self._eval_finish(job)
+        self.record.events[i_ev] = (boundary, "eval_mean", repr(mean))
+        self.record.events[i_ev + 1] = (boundary, "eval_std", repr(std))
+        self.record.evals[i_e] = (boundary, mean, std)
 
     def evaluate(self, params: QNet, epsilon: float, episodes: int, seed: int):
         """Exactly `episodes` epsilon-greedy episodes of the (persistent) eval env on one
         rng stream, single-state forwards on the GPU; mean and population std."""
+        self.resolve_evals()
+        return self._eval_finish(self._eval_start(params, epsilon, episodes, seed))
+
+    def _eval_state(self, episodes: int):
+        """Eval env (one sampler, episode log >= episodes), its 64-frame ring, the
+        parameter snapshot, the eval stream and the pinned episode counter."""
         torch = self.torch
         hp = self.hp
-        lib = N.load()
         log = max(256, int(episodes))
-        if self._eval is None or self._eval[0].steps < log:
+        if self._eval is None or self._eval["envs"].steps < log:
+            old = self._eval
             envs = DeviceEnvs([derived_seed(hp.seed, ROLE_EVAL, 1000)],
                               [np.random.default_rng(0)], log)
             ring = torch.zeros((64, 7056), dtype=torch.uint8, device="cuda")
-            staging = torch.empty((1, log, REC_INTS), dtype=torch.int32, device="cuda")
-            counter = torch.zeros(1, dtype=torch.int32, device="cuda")
+            if old is None:
+                envs.reset_all(torch.zeros(1, dtype=torch.int32, device="cuda"), ring)
+                envs.slot_next.fill_(1)
+            else:  # a longer episode log: the env carries on where it was
+                torch.cuda.synchronize()
+                for f in ("pcg", "episode", "t", "stack", "ep_return", "slot_next", "actions"):
+                    getattr(envs, f).copy_(getattr(old["envs"], f))
+                ring.copy_(old["ring"])
             ws, cap = self._own_ws(1)
-            envs.reset_all(torch.zeros(1, dtype=torch.int32, device="cuda"), ring)
-            envs.slot_next.fill_(1)
-            self._eval = (envs, ring, staging, counter, ws, cap)
-        envs, ring, staging, counter, ws, cap = self._eval
+            self._eval = dict(
+                envs=envs, ring=ring, ws=ws, cap=cap,
+                staging=torch.empty((1, log, REC_INTS), dtype=torch.int32, device="cuda"),
+                counter=torch.zeros(1, dtype=torch.int32, device="cuda"),
+                net=old["net"] if old else self.theta.copy(),
+                stream=old["stream"] if old else torch.cuda.Stream(),
+                host=torch.zeros(1, dtype=torch.int32, pin_memory=True), graphs={})
+        return self._eval
+
+    def _eval_args(self, ev, epsilon: float, episodes: int):
+        hp = self.hp
+        envs = ev["envs"]
+        return N.PqActArgs(
+            net=ev["net"].struct(), envs=envs.struct(), ring=ev["ring"].data_ptr(),
+            staging=ev["staging"].data_ptr(), step_counter=ev["counter"].data_ptr(), W=1,
+            steps=envs.steps, actions=hp.actions, episode_length=hp.episode_length,
+            epoch_start=0, frame_capacity=64, eps_start=epsilon, eps_end=epsilon,
+            eps_anneal=1, terminal_p=hp.terminal_p, q_out=None, ws=ev["ws"].data_ptr(),
+            max_batch=ev["cap"], max_episodes=episodes)
+
+    def _eval_graph(self, ev, epsilon: float, episodes: int):
+        """EVAL_CHUNK act steps captured once per (epsilon, episodes); a warm-up step on
+        saved state configures every kernel outside the capture."""
+        key = (float(epsilon), int(episodes))
+        if key not in ev["graphs"]:
+            torch = self.torch
+            lib = N.load()
+            a = self._eval_args(ev, epsilon, episodes)
+            envs = ev["envs"]
+            keep = [envs.pcg, envs.episode, envs.t, envs.stack, envs.ep_return, envs.slot_next,
+                    envs.ep_count, envs.ep_label, envs.ep_ret, envs.actions, ev["ring"],
+                    ev["counter"]]
+            torch.cuda.synchronize()
+            saved = [t.clone() for t in keep]
+            s = ev["stream"]
+            with torch.cuda.stream(s):
+                N.check(lib.pq_act_step(N.C.byref(a), N.stream_ptr(s)), "eval warm-up")
+            s.synchronize()
+            for t, v in zip(keep, saved):
+                t.copy_(v)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    for _ in range(self.EVAL_CHUNK):
+                        N.check(lib.pq_act_step(N.C.byref(a), N.stream_ptr(s)), "eval step")
+            torch.cuda.synchronize()
+            ev["graphs"][key] = (g, a)
+        return ev["graphs"][key][0]
+
+    def _eval_start(self, params: QNet, epsilon: float, episodes: int, seed: int):
+        torch = self.torch
         from .replay import pcg_state_from_generator
 
+        ev = self._eval_state(episodes)
+        g = self._eval_graph(ev, epsilon, episodes)
+        envs = ev["envs"]
+        # snapshot + rng on the current stream (in order with the epoch that follows)
+        copy_into(ev["net"], params)
         envs.pcg.copy_(torch.from_numpy(
             pcg_state_from_generator(np.random.default_rng(seed)).view(np.int64)[None]).cuda())
         envs.ep_count.zero_()
-        a = N.PqActArgs(
-            net=params.struct(), envs=envs.struct(), ring=ring.data_ptr(),
-            staging=staging.data_ptr(), step_counter=counter.data_ptr(), W=1, steps=envs.steps,
-            actions=hp.actions, episode_length=hp.episode_length, epoch_start=0,
-            frame_capacity=64, eps_start=epsilon, eps_end=epsilon, eps_anneal=1,
-            terminal_p=hp.terminal_p, q_out=None, ws=ws.data_ptr(), max_batch=cap,
-            max_episodes=episodes)
-        while int(envs.ep_count.item()) < episodes:
-            for _ in range(128):
-                N.check(lib.pq_act_step(N.C.byref(a), N.stream_ptr()), "eval step")
-        rets = envs.ep_ret[0, :episodes].cpu().numpy()
+        ev["host"].zero_()
+        ev["stream"].wait_stream(torch.cuda.current_stream())
+        job = dict(ev=ev, graph=g, episodes=int(episodes), inflight=[], done=False)
+        self._eval_pump(job)
+        return job
+
+    def _eval_chunk(self, job):
+        torch = self.torch
+        ev = job["ev"]
+        with torch.cuda.stream(ev["stream"]):
+            job["graph"].replay()
+            ev["host"].copy_(ev["envs"].ep_count, non_blocking=True)
+            e = torch.cuda.Event()
+            e.record()
+        job["inflight"].append(e)
+
+    def _eval_pump(self, job) -> bool:
+        """Keep up to two chunks in flight until the episode count (pinned, possibly
+        stale) reaches the target; never blocks."""
+        if job["done"]:
+            return True
+        inflight = job["inflight"]
+        while inflight and inflight[0].query():
+            inflight.pop(0)
+        if int(job["ev"]["host"][0]) >= job["episodes"] and not inflight:
+            job["done"] = True
+            return True
+        while len(inflight) < 2:
+            self._eval_chunk(job)
+        return False
+
+    def _eval_finish(self, job):
+        ev = job["ev"]
+        while True:
+            ev["stream"].synchronize()
+            job["inflight"].clear()
+            if int(ev["host"][0]) >= job["episodes"]:
+                break
+            self._eval_chunk(job)
+        job["done"] = True
+        rets = ev["envs"].ep_ret[0, :job["episodes"]].cpu().numpy()
         return float(rets.mean()), float(rets.std())
+
+    def _wait_epoch(self):
+        """Synchronize with the epoch just enqueued, feeding the evaluation in flight."""
+        torch = self.torch
+        if self._pending_eval is not None:
+            done = torch.cuda.Event()
+            done.record()
+            job = self._pending_eval[2]
+            while not done.query():
+                if self._eval_pump(job):
+                    break
+                time.sleep(2e-4)
+        torch.cuda.synchronize()
 
     def check_finite(self):
         v = int(self.nonfinite.item())
@@ -619,7 +756,7 @@ class DeviceRun:
             copy_into(self.target, self.theta)
             self.maybe_eval(e * hp.C)
             self.run_epoch(e)
-            self.torch.cuda.synchronize()
+            self._wait_epoch()
             self.check_finite()
             if self.hash_epochs:
                 self.record_epoch_hash((e + 1) * hp.C)
@@ -629,6 +766,7 @@ class DeviceRun:
         return self.record
 
     def finalize(self, wall0: float):
+        self.resolve_evals()
         self.resolve_hashes()
         w = self.worker
         self.counters.update({
@@ -783,6 +921,8 @@ class HostEnvRun(DeviceRun):
                 "forward")
         self.h_q.copy_(self.d_q, non_blocking=True)
         self.d2h_bytes += self.h_q.numel() * 4
+        if self._pending_eval is not None:  # feed the evaluation in flight
+            self._eval_pump(self._pending_eval[2])
         torch.cuda.current_stream().synchronize()
         t_label0 = self._epoch * hp.C + b * hp.W + 1
         seq = self._seq

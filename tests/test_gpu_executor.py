@@ -98,3 +98,21 @@ def test_env_factory_template_and_reference_signature():
     assert seen == rec.events and any(k == "episode" for _, k, _ in seen)
     with pytest.raises(ValueError):
         run(hp, lambda: object())
+
+
+def test_async_evaluation_matches_streamed_evaluation():
+    """The evaluation overlapped with the next epoch on its own stream (no sink) lands the
+    same mean / std at the same place in the record as the synchronous one a streaming
+    sink forces; 300 episodes also grow the eval env's episode log past its 256 entries
+    and take many CUDA-graph chunks; greedy actions make it depend on the snapshot."""
+    from paper_2111_01264_b200.executor import run
+
+    hp = HyperParams(**{**BASE, "eval_episodes": 300, "eval_epsilon": 0.05, "episode_length": 3,
+                        "total_steps": 256}, W=8).with_mode("both")
+    streamed = []
+    a = run(hp)
+    b = run(hp, None, lambda s, k, v: streamed.append((s, k, v)))
+    assert len(a.evals) == 4 and all(m is not None for _, m, _ in a.evals)
+    assert a.evals == b.evals
+    assert [e for e in a.events if e[1] != "theta_hash"] == [e for e in b.events if e[1] != "theta_hash"]
+    assert streamed == b.events
