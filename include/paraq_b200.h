@@ -117,6 +117,13 @@ typedef struct pq_envs {
     int64_t *ep_label;   /* [W][steps] t_label of finished episodes */
     double *ep_ret;      /* [W][steps] their returns */
     int32_t *actions;    /* [W] last actions (read back by the host API) */
+    /* Optional compact frame allocation (NULL: each env takes seq + 1 for a reset frame,
+     * i.e. 2 slots per step reserved).  Non-NULL: next frames take slot_next (1 per step)
+     * and the reset frames of a step get consecutive sequence numbers from *reset_next in
+     * sampler order, assigned by the step's last CTA (deterministic). */
+    int64_t *reset_next; /* [1] next reset-frame sequence number */
+    int64_t *reset_ep;   /* [W] scratch: new episode index of a resetting env, else -1 */
+    int32_t *reset_slot; /* [W] scratch: assigned reset-frame slot */
 } pq_envs;
 
 /* Reset env j into frame slot slots[j] (episode start, masked stack). */
@@ -129,6 +136,14 @@ int pq_prepopulate(uint64_t *pcg_state, uint64_t key, int episode_length, int ac
                    double terminal_p, int64_t n, uint8_t *ring, int64_t frame_base,
                    int64_t frame_capacity, int32_t *rec_out, int64_t *frames_used_out,
                    void *scratch, void *stream);
+/* The same in two calls, so the host can reserve exactly the frames the walk used
+ * before any is written: the walk (records, frame descriptors in scratch, count), then
+ * the frame generation into ring slots [frame_base, frame_base + *frames_used). */
+int pq_prepopulate_walk(uint64_t *pcg_state, int episode_length, int actions, double terminal_p,
+                        int64_t n, int64_t frame_base, int64_t frame_capacity, int32_t *rec_out,
+                        int64_t *frames_used_out, void *scratch, void *stream);
+int pq_prepopulate_frames(uint64_t key, uint8_t *ring, int64_t frame_base, int64_t frame_capacity,
+                          const int64_t *frames_used, const void *scratch, void *stream);
 size_t pq_prepopulate_scratch_bytes(int64_t n);
 
 /* ---- Q network (nn.py / agent.py) -------------------------------------------------- */

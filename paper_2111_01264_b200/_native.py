@@ -29,7 +29,8 @@ class PqOpt(C.Structure):
 
 class PqEnvs(C.Structure):
     _fields_ = [(n, vp) for n in ("pcg", "episode", "t", "stack", "ep_return", "key",
-                                  "slot_next", "ep_count", "ep_label", "ep_ret", "actions")]
+                                  "slot_next", "ep_count", "ep_label", "ep_ret", "actions",
+                                  "reset_next", "reset_ep", "reset_slot")]
 
 
 class PqHenv(C.Structure):
@@ -81,6 +82,9 @@ EXPORTS = {
     "pq_env_reset": ([PqEnvs, C.c_int, vp, vp, vp], C.c_int),
     "pq_prepopulate": ([vp, C.c_uint64, C.c_int, C.c_int, C.c_double, C.c_int64, vp, C.c_int64,
                         C.c_int64, vp, vp, vp, vp], C.c_int),
+    "pq_prepopulate_walk": ([vp, C.c_int, C.c_int, C.c_double, C.c_int64, C.c_int64, C.c_int64, vp, vp,
+                             vp, vp], C.c_int),
+    "pq_prepopulate_frames": ([C.c_uint64, vp, C.c_int64, C.c_int64, vp, vp, vp], C.c_int),
     "pq_prepopulate_scratch_bytes": ([C.c_int64], C.c_size_t),
     "pq_workspace_bytes": ([C.c_int, C.c_int], C.c_size_t),
     "pq_workspace_layout": ([C.c_int, C.c_int, C.POINTER(C.c_int64)], C.c_int),

@@ -127,7 +127,12 @@ __global__ void __launch_bounds__(256) k_act_env(const ActArgs a) {
         }
     }
     __shared__ bool s_active;
-    if (tid == 0) s_active = a.max_episodes <= 0 || epc < a.max_episodes;
+    const bool compact = a.e.reset_next != nullptr;
+    if (tid == 0) {
+        s_active = a.max_episodes <= 0 || epc < a.max_episodes;
+        s_slot[0] = s_slot[1] = -1;
+        if (compact) a.e.reset_ep[j] = -1;  // set below when this env resets
+    }
     __syncthreads();
     if (tid == 0 && s_active) {
         // step_counter counts lockstep blocks (run-global in the executor); the
@@ -171,16 +176,23 @@ __global__ void __launch_bounds__(256) k_act_env(const ActArgs a) {
             ret = 0.0;
             ep += 1;
             t = 0;
-            const int32_t rs = (int32_t)((seq + 1) % a.frame_capacity);
-            s_slot[1] = rs;
             s_base[1] = env_frame_base(key, ep, 0, 255);
-            nst = make_int4(-1, -1, -1, rs);
-            a.e.slot_next[j] = seq + 2;
+            if (compact) {  // slot assigned by the step's last CTA (below), frame written then
+                s_slot[1] = -2;
+                a.e.reset_ep[j] = ep;
+                nst = make_int4(-1, -1, -1, -1);
+                a.e.slot_next[j] = seq + 1;
+            } else {
+                const int32_t rs = (int32_t)((seq + 1) % a.frame_capacity);
+                s_slot[1] = rs;
+                nst = make_int4(-1, -1, -1, rs);
+                a.e.slot_next[j] = seq + 2;
+            }
         } else {
             nst = make_int4(st4[1], st4[2], st4[3], fs);
             a.e.slot_next[j] = seq + 1;
         }
-        *reinterpret_cast<int4 *>(a.e.stack + j * 4) = nst;
+        if (s_slot[1] != -2) *reinterpret_cast<int4 *>(a.e.stack + j * 4) = nst;
         a.e.ep_return[j] = ret;
         a.e.t[j] = t;
         a.e.episode[j] = ep;
@@ -204,10 +216,52 @@ __global__ void __launch_bounds__(256) k_act_env(const ActArgs a) {
         s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
+    if (compact && s_last) {  // reset-frame slots of this step, consecutive in sampler order
+        __shared__ int s_wsum[8];
+        __shared__ int64_t s_rn;
+        __shared__ int s_tot;
+        if (tid == 0) s_rn = *reinterpret_cast<volatile int64_t *>(a.e.reset_next), s_tot = 0;
+        __syncthreads();
+        for (int c0 = 0; c0 < a.W; c0 += 256) {
+            const int jj = c0 + tid;
+            const int64_t rep = jj < a.W ? *reinterpret_cast<volatile int64_t *>(a.e.reset_ep + jj) : -1;
+            const bool f = rep >= 0;
+            const unsigned m = __ballot_sync(0xffffffffu, f);
+            if (lane == 0) s_wsum[warp] = __popc(m);
+            __syncthreads();
+            int before = s_tot;
+            for (int w = 0; w < warp; ++w) before += s_wsum[w];
+            if (f) {
+                const int32_t rs = (int32_t)((s_rn + before + __popc(m & ((1u << lane) - 1u))) % a.frame_capacity);
+                a.e.reset_slot[jj] = rs;
+                *reinterpret_cast<int4 *>(a.e.stack + jj * 4) = make_int4(-1, -1, -1, rs);
+            }
+            __syncthreads();
+            if (tid == 0)
+                for (int w = 0; w < 8; ++w) s_tot += s_wsum[w];
+            __syncthreads();
+        }
+        if (tid == 0) *a.e.reset_next = s_rn + s_tot;
+    }
     if (s_last && tid == 0) {
-        *a.step_counter += 1;
+        __threadfence();
+        *reinterpret_cast<volatile int32_t *>(a.step_counter) = (int32_t)(bg + 1);
         *a.done = 0;
         __threadfence();
+    }
+    if (compact && s_slot[1] == -2) {
+        // this env reset: wait for the last CTA's slot assignment (it has arrived, so it
+        // is resident and runs to completion), then write the reset frame
+        __shared__ int32_t s_rs;
+        if (tid == 0) {
+            if (!s_last)
+                while (*reinterpret_cast<volatile int32_t *>(a.step_counter) == (int32_t)bg) __nanosleep(64);
+            __threadfence();
+            s_rs = *reinterpret_cast<volatile int32_t *>(a.e.reset_slot + j);
+        }
+        __syncthreads();
+        uint64_t *d = reinterpret_cast<uint64_t *>(a.ring + (size_t)s_rs * FRAME_BYTES);
+        for (int p = tid; p < FRAME_BYTES / 8; p += blockDim.x) d[p] = splitmix64(s_base[1] + (uint64_t)p);
     }
 }
 

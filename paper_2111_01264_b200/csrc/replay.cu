@@ -413,19 +413,32 @@ int pq_replay_flush(const int32_t *staging, int W, int steps, int32_t *records, 
 
 size_t pq_prepopulate_scratch_bytes(int64_t n) { return (size_t)(2 * n + 2) * sizeof(FrameDesc); }
 
+int pq_prepopulate_walk(uint64_t *pcg_state, int episode_length, int actions, double terminal_p,
+                        int64_t n, int64_t frame_base, int64_t frame_capacity, int32_t *rec_out,
+                        int64_t *frames_used_out, void *scratch, void *stream) {
+    if (n <= 0) return 0;
+    k_prepop_scalar<<<1, 32, 0, (cudaStream_t)stream>>>(pcg_state, episode_length, actions, terminal_p, n,
+                                                        frame_base, frame_capacity, rec_out,
+                                                        static_cast<FrameDesc *>(scratch), frames_used_out);
+    return cuda_err(cudaGetLastError(), "prepopulate walk");
+}
+
+int pq_prepopulate_frames(uint64_t key, uint8_t *ring, int64_t frame_base, int64_t frame_capacity,
+                          const int64_t *frames_used, const void *scratch, void *stream) {
+    k_gen_frames<<<4096, 128, 0, (cudaStream_t)stream>>>(static_cast<const FrameDesc *>(scratch), frames_used,
+                                                         key, ring, frame_base, frame_capacity);
+    return cuda_err(cudaGetLastError(), "prepopulate frames");
+}
+
 int pq_prepopulate(uint64_t *pcg_state, uint64_t key, int episode_length, int actions,
                    double terminal_p, int64_t n, uint8_t *ring, int64_t frame_base,
                    int64_t frame_capacity, int32_t *rec_out, int64_t *frames_used_out,
                    void *scratch, void *stream) {
     if (n <= 0) return 0;
-    cudaStream_t st = (cudaStream_t)stream;
-    FrameDesc *desc = static_cast<FrameDesc *>(scratch);
-    k_prepop_scalar<<<1, 32, 0, st>>>(pcg_state, episode_length, actions, terminal_p, n,
-                                      frame_base, frame_capacity, rec_out, desc, frames_used_out);
-    int rc = cuda_err(cudaGetLastError(), "prepopulate scalar");
-    if (rc) return rc;
-    k_gen_frames<<<4096, 128, 0, st>>>(desc, frames_used_out, key, ring, frame_base, frame_capacity);
-    return cuda_err(cudaGetLastError(), "prepopulate frames");
+    if (int rc = pq_prepopulate_walk(pcg_state, episode_length, actions, terminal_p, n, frame_base,
+                                     frame_capacity, rec_out, frames_used_out, scratch, stream))
+        return rc;
+    return pq_prepopulate_frames(key, ring, frame_base, frame_capacity, frames_used_out, scratch, stream);
 }
 
 }  // extern "C"

@@ -52,9 +52,19 @@ class DeviceEnvs:
         self.ep_label = torch.zeros((W, steps_per_epoch), dtype=torch.int64, device=dev)
         self.ep_ret = torch.zeros((W, steps_per_epoch), dtype=torch.float64, device=dev)
         self.actions = torch.zeros(W, dtype=torch.int32, device=dev)
+        self.reset_next = self.reset_ep = self.reset_slot = None  # compact mode off
+
+    def compact_resets(self) -> None:
+        """Compact frame allocation: 1 slot per step per env (slot_next) plus the step's
+        reset frames at consecutive sequence numbers from reset_next, in sampler order."""
+        torch = N.require_cuda()
+        self.reset_next = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.reset_ep = torch.full((self.W,), -1, dtype=torch.int64, device="cuda")
+        self.reset_slot = torch.zeros(self.W, dtype=torch.int32, device="cuda")
 
     def struct(self) -> N.PqEnvs:
-        return N.PqEnvs(*(getattr(self, f).data_ptr() for f, _ in N.PqEnvs._fields_))
+        return N.PqEnvs(*(None if getattr(self, f) is None else getattr(self, f).data_ptr()
+                          for f, _ in N.PqEnvs._fields_))
 
     def reset_all(self, slots, ring, stream=None) -> None:
         N.check(N.load().pq_env_reset(self.struct(), self.W, slots.data_ptr(), ring.data_ptr(),

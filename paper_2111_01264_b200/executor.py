@@ -192,7 +192,10 @@ class DeviceRun:
         self.worker = InferenceWorker()
         lag = -(-3 // self.steps) + 1  # epochs of stack history an env can reference
         self.lag = lag
-        fcap = 2 * hp.capacity + 2 * (lag + 3) * C + 2 * W + 1024
+        # frames live in the ring once each: one per transition plus the reset frames
+        # (rate 1 / mean episode length, bounded here by twice that), the epoch's worst-case
+        # reservation and `lag` epochs of stack history (an overrun raises, never corrupts)
+        fcap = int(hp.capacity * (1.0 + reset_rate_bound(hp))) + 2 * (lag + 3) * C + 2 * W + 1024
         self.D = ReplayMemory(hp.capacity, frame_capacity=fcap)
         prepop_env = FrameEnvSpec(derived_seed(hp.seed, ROLE_PREPOP, 1), hp.episode_length,
                                   hp.actions, hp.terminal_p)
@@ -205,6 +208,7 @@ class DeviceRun:
         keys = [derived_seed(hp.seed, ROLE_SAMPLER, 1000 + j) for j in range(W)]
         rngs = [rng_stream(hp.seed, ROLE_SAMPLER, j) for j in range(W)]
         self.envs = DeviceEnvs(keys, rngs, self.steps)
+        self.envs.compact_resets()
         first = self.D._reserve_frames(W)
         slots = torch.as_tensor([(first + j) % fcap for j in range(W)], dtype=torch.int32,
                                 device="cuda")
@@ -377,6 +381,7 @@ class DeviceRun:
         if not self.staged:
             return
         self.flush_transitions(self.steps)
+        self.trim_frames(int(self.envs.reset_next.item()))
         counts = self.envs.ep_count.cpu().numpy()
         labels = self.envs.ep_label.cpu().numpy()
         rets = self.envs.ep_ret.cpu().numpy()
@@ -387,6 +392,12 @@ class DeviceRun:
         self.envs.ep_count.zero_()
         self.staged = False
         self._flushed_blocks = 0
+
+    def trim_frames(self, used_end: int) -> None:
+        """Return the unused tail of the epoch's frame reservation (the last one made)."""
+        if not self.epoch_bases[-1] <= used_end <= self.D.frame_seq:
+            raise RuntimeError("frame sequence numbers out of the epoch's reservation")
+        self.D.frame_seq = used_end
 
     def flush_transitions(self, upto_block: int) -> None:
         """Move the staged transitions of blocks [flushed, upto_block) into D in
@@ -458,10 +469,13 @@ class DeviceRun:
         if not self.blocking:  # the store is frozen: the epoch's C/F draws up front
             sample_indices_device(self.trainer_pcg, len(self.D), self.updates * hp.batch_size,
                                   out=self.idx_table[: self.updates * hp.batch_size])
+        # worst case reserved (a next frame and a reset frame per step), the unused tail
+        # returned at the flush (trim_frames): env j's next frames at base + j * steps + b,
+        # the reset frames after all of them, consecutive in (step, sampler) order
         base = self.D._reserve_frames(2 * hp.C)
         self.epoch_bases.append(base)
-        per = 2 * self.steps
-        self.envs.slot_next.copy_(torch.arange(hp.W, device="cuda", dtype=torch.int64) * per + base)
+        self.envs.slot_next.copy_(torch.arange(hp.W, device="cuda", dtype=torch.int64) * self.steps + base)
+        self.envs.reset_next.fill_(base + hp.W * self.steps)
         self.update_counter.zero_()
         self.target_prologue()  # theta-minus and the index table are this epoch's
 
@@ -782,6 +796,14 @@ class DeviceRun:
         self.record.duration_s = time.perf_counter() - wall0
 
 
+def reset_rate_bound(hp: HyperParams) -> float:
+    """Twice the expected reset frames per env step, 1 / E[episode length] with the
+    horizon L and the per-step terminal probability p: E = (1 - (1 - p)^L) / p."""
+    L, p = hp.episode_length, hp.terminal_p
+    mean_len = L if p <= 0 else (1.0 - (1.0 - p) ** L) / p
+    return min(1.0, 2.0 / max(mean_len, 1.0))
+
+
 def apply_env_factory(hp: HyperParams, env_factory) -> HyperParams:
     """The reference calls env_factory() for the prepopulation, probe, sampler and
     evaluation envs (executor.py:348-360).  Here the envs live on the device, so the
@@ -953,6 +975,7 @@ class HostEnvRun(DeviceRun):
         if not self.staged:
             return
         self.flush_transitions(self.steps)
+        self.trim_frames(int(self._seq[0]))
         for j in range(hp.W):
             for lab, ret in self.host_episodes[j]:
                 self.record.episodes.append((lab, ret))

@@ -220,8 +220,9 @@ class ReplayMemory:
         self.records[slot] = torch.from_numpy(rec).cuda()
         self._prev = (s2.tobytes(), refs[1:5], seqs[1:5])
 
-    def push_device_records(self, rec, n: int, min_seq: int, stream=None) -> None:
-        """Append n device records [n, 8] (owner-major order already applied)."""
+    def push_device_records(self, rec, n: int, min_seq, stream=None) -> None:
+        """Append n device records [n, 8] (owner-major order already applied); min_seq:
+        the oldest frame sequence number they reference (scalar or one per record)."""
         slots = self._advance(n, min_seq)
         start = int(slots[0])
         first = min(n, self.capacity - start)
@@ -302,15 +303,27 @@ class ReplayMemory:
         used = torch.zeros(1, dtype=torch.int64, device="cuda")
         scratch = torch.empty(lib.pq_prepopulate_scratch_bytes(n), dtype=torch.uint8,
                               device="cuda")
-        worst = 2 * n + 1
-        first = self._reserve_frames(worst)
-        N.check(lib.pq_prepopulate(st.data_ptr(), env.key, env.episode_length, env.action_count,
-                                   env.terminal_p, n, self.ring.data_ptr(), first,
-                                   self.frame_capacity, rec.data_ptr(), used.data_ptr(),
-                                   scratch.data_ptr(), N.stream_ptr()), "prepopulate")
-        self.frame_seq = first + int(used.item())
+        # the walk first (records + frame descriptors), then exactly the frames it used are
+        # reserved -- the ring need not hold the worst case of 2 frames per transition
+        first = self.frame_seq
+        N.check(lib.pq_prepopulate_walk(st.data_ptr(), env.episode_length, env.action_count,
+                                        env.terminal_p, n, first, self.frame_capacity, rec.data_ptr(),
+                                        used.data_ptr(), scratch.data_ptr(), N.stream_ptr()),
+                "prepopulate walk")
+        if self._reserve_frames(int(used.item())) != first:
+            raise RuntimeError("frame reservation moved during prepopulation")
+        N.check(lib.pq_prepopulate_frames(env.key, self.ring.data_ptr(), first, self.frame_capacity,
+                                          used.data_ptr(), scratch.data_ptr(), N.stream_ptr()),
+                "prepopulate frames")
         pcg_state_to_generator(st.cpu().numpy().view(np.uint64), rng)
-        self.push_device_records(rec, n, first)
+        # each record's oldest referenced frame, so the ring-wrap guard frees the prepopulated
+        # frames as their records are overwritten (slot = seq mod frame_capacity, and the
+        # walk's frames are the sequence numbers [first, first + used))
+        fc = self.frame_capacity
+        refs = rec[:, :5].to(torch.int64)
+        seqs = first + torch.remainder(refs - first % fc, fc)
+        seqs = torch.where(refs >= 0, seqs, torch.full_like(seqs, 1 << 62))
+        self.push_device_records(rec, n, seqs.min(dim=1).values.cpu().numpy())
         env.episode += 1  # the device walk leaves the env mid-episode (state not kept)
 
 

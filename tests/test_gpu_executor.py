@@ -116,3 +116,23 @@ def test_async_evaluation_matches_streamed_evaluation():
     assert a.evals == b.evals
     assert [e for e in a.events if e[1] != "theta_hash"] == [e for e in b.events if e[1] != "theta_hash"]
     assert streamed == b.events
+
+
+def test_compact_frame_ring_wraps_like_host_allocation():
+    """The ring holds ~(1 + reset rate) frames per transition: reset frames get slots in
+    (step, sampler) order from the step's last CTA and the epoch's unused reservation is
+    returned.  40 epochs wrap it many times (every prepopulated record evicted); the
+    device samplers' memory must equal the host samplers' (their own compact allocation)
+    transition for transition, and the runs must agree bit for bit."""
+    hp = HyperParams(**{**BASE, "total_steps": 64 * 120, "eval_period": 0}, W=8).with_mode("both")
+    dev = DeviceRun(hp, graph_chunk=4)
+    a = dev.execute()
+    host = HostEnvRun(hp, graph_chunk=4)
+    b = host.execute()
+    assert dev.D.frame_seq > 3 * dev.D.frame_capacity  # wrapped 3 times
+    assert dev.D.frame_capacity < 1.5 * hp.capacity + 2 * 5 * hp.C + 2 * hp.W + 1024
+    sa, sb = dev.D.snapshot(), host.D.snapshot()
+    assert len(sa) == len(sb) == hp.capacity
+    assert [digest(t.state) for t in sa] == [digest(t.state) for t in sb]
+    assert [digest(t.next_state) for t in sa] == [digest(t.next_state) for t in sb]
+    assert a.final_hash == b.final_hash and a.episodes == b.episodes

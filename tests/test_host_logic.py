@@ -242,3 +242,16 @@ def test_sharded_acting_pack_gather_remap_gloo():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(ok for _, ok in res)
+
+
+def test_reset_rate_bound():
+    """Frame-ring sizing: twice the expected reset frames per step (1 / E[episode length])."""
+    from paper_2111_01264_b200.agent import HyperParams
+    from paper_2111_01264_b200.executor import reset_rate_bound
+
+    hp = HyperParams()
+    L, p = hp.episode_length, hp.terminal_p
+    mean = (1 - (1 - p) ** L) / p
+    assert abs(reset_rate_bound(hp) - 2 / mean) < 1e-12
+    assert reset_rate_bound(HyperParams(episode_length=1)) == 1.0
+    assert reset_rate_bound(HyperParams(episode_length=10, terminal_p=0.0)) == 0.2
