@@ -207,6 +207,9 @@ int pq_learn_target_prologue(const pq_learn_args *args, void *stream);
  * agent.py:103-104 feeds the optimizer the summed gradient, so a sum of shard sums is
  * the reference semantics (fp32 summation order aside). */
 int pq_learn_grad(const pq_learn_args *args, float *grad, void *stream);
+/* The same, recording the cudaEvent_t fc1_done once grad[P_W4, P_B4) (the fc1 weight
+ * gradient, 6.4 of the 6.77 MB) is complete: its all-reduce overlaps the conv backward. */
+int pq_learn_grad_ev(const pq_learn_args *args, float *grad, void *stream, void *fc1_done);
 int pq_rmsprop_apply(pq_net theta, pq_opt opt, const float *grad, int actions, float lr, float rho,
                      float kappa, int32_t *nonfinite, int update_id, void *stream);
 

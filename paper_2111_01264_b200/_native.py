@@ -95,6 +95,7 @@ EXPORTS = {
     "pq_learn_target_prologue": ([C.POINTER(PqLearnArgs), vp], C.c_int),
     "pq_act_step": ([C.POINTER(PqActArgs), vp], C.c_int),
     "pq_learn_grad": ([C.POINTER(PqLearnArgs), vp, vp], C.c_int),
+    "pq_learn_grad_ev": ([C.POINTER(PqLearnArgs), vp, vp, vp], C.c_int),
     "pq_rmsprop_apply": ([PqNet, PqOpt, vp, C.c_int, C.c_float, C.c_float, C.c_float, vp, C.c_int, vp],
                          C.c_int),
     "pq_rmsprop_f32": ([vp, vp, vp, vp, C.c_int64, C.c_float, C.c_float, C.c_float, vp, vp, vp,

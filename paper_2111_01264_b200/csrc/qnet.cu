@@ -829,8 +829,10 @@ static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStrea
 
 // grad_only != NULL: write the summed gradient of every parameter there instead of
 // updating theta / opt (the data-parallel learner all-reduces it, then pq_rmsprop_apply)
+// fc1_done (grad_only): recorded once grad_only[P_W4, P_B4) -- the fc1 weight gradient, 95%
+// of the bytes -- is complete, so its all-reduce can start under the conv backward
 static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cudaStream_t st,
-                               float *grad_only = nullptr) {
+                               float *grad_only = nullptr, cudaEvent_t fc1_done = nullptr) {
     if (fused_backward(n, la, grad_only)) return backward_fused(la, n, w, st);
     const pq_net &th = la->theta;
     const bf16 *sh = (const bf16 *)th.shadow;
@@ -859,6 +861,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         g.e[0] = EpiF32{grad_only + P_W4, 512, 3136, 3136, 0};
         g.M = 512, g.N = 3136, g.K = n, g.kc_per_split = (n + 63) / 64, g.splits = 1, g.ones_at = -1;
         PQ_CHECK((launch_gemm<64, false, true, 4>(g, 1, side)), "fc1 wgrad");
+        if (fc1_done) PQ_CHECK(cudaEventRecord(fc1_done, side), "fc1 gradient event");
     } else {  // (the cp.async engine: its staged RMSProp epilogue walks the tile with all 8 warps)
         PQ_CHECK((launch_gemm<64, false, true, 4>(args_b4w_rms<EpiRms>(la, n, w), 1, side)), "fc1 wgrad+rmsprop");
     }
@@ -1166,7 +1169,9 @@ int pq_learn_target_prologue(const pq_learn_args *la, void *stream) {
     return 0;
 }
 
-int pq_learn_grad(const pq_learn_args *la, float *grad, void *stream) {
+int pq_learn_grad(const pq_learn_args *la, float *grad, void *stream) { return pq_learn_grad_ev(la, grad, stream, nullptr); }
+
+int pq_learn_grad_ev(const pq_learn_args *la, float *grad, void *stream, void *fc1_done) {
     const int n = la->n;
     if (n < 1 || n > la->max_batch) return set_err("batch size out of range for the workspace");
     if (la->actions < 1 || la->actions > MAX_ACTIONS) return set_err("actions must be in [1, 32]");
@@ -1183,7 +1188,7 @@ int pq_learn_grad(const pq_learn_args *la, float *grad, void *stream) {
     if (rc) return rc;
     rc = head(nets, groups, n, la->actions, w, 1, la, st, false);
     if (rc) return rc;
-    return backward_and_update(la, n, w, st, grad);
+    return backward_and_update(la, n, w, st, grad, (cudaEvent_t)fc1_done);
 }
 
 int pq_rmsprop_apply(pq_net theta, pq_opt opt, const float *grad, int actions, float lr, float rho,

@@ -117,13 +117,56 @@ class DataParallelLearner:
         self.opt.step += 1
         self.updates += 1
 
-    def step(self, idx):
-        """One data-parallel update on the global batch idx (device int64 [B])."""
-        self.shard_gradient(idx)
-        if self.world_size > 1:
-            import torch.distributed as dist
+    def buckets(self):
+        """All-reduce buckets in completion order: the fc1 weight gradient (ready when its
+        GEMM on the weight-gradient branch ends, 95% of the bytes), then the rest (conv
+        layers, written by the last gradient kernel, and the fc1 bias / fc2 tail)."""
+        from .nn import layer_shapes
 
+        shapes = layer_shapes(self.theta.actions)
+        p_w4 = sum(o * i + o for o, i in shapes[:3])
+        p_b4 = p_w4 + shapes[3][0] * shapes[3][1]
+        g = self.grad
+        return g[p_w4:p_b4], (g[:p_w4], g[p_b4:])
+
+    def _overlap(self) -> bool:
+        import torch.distributed as dist
+
+        return (os.environ.get("PQ_DP_OVERLAP", "1") != "0"
+                and dist.get_backend(self.group) == "nccl")
+
+    def step(self, idx):
+        """One data-parallel update on the global batch idx (device int64 [B]).  Over NCCL
+        the fc1 weight-gradient bucket is all-reduced on a communication stream as soon as
+        its GEMM completes, under the conv layers' backward; the small rest follows the
+        last gradient kernel; RMSProp waits for both (PQ_DP_OVERLAP=0: one all-reduce of
+        the whole gradient after it)."""
+        if self.world_size == 1:
+            self.shard_gradient(idx)
+            self.apply()
+            return
+        import torch.distributed as dist
+
+        torch, N = self.torch, self.N
+        if not self._overlap():
+            self.shard_gradient(idx)
             dist.all_reduce(self.grad, op=dist.ReduceOp.SUM, group=self.group)
+            self.apply()
+            return
+        if not hasattr(self, "_comm"):
+            self._comm = torch.cuda.Stream()
+            self._fc1_done = torch.cuda.Event()
+            self._fc1_done.record()  # creates the CUDA event handle the library records
+        a = self._args(idx[self.lo:self.hi])
+        N.check(N.load().pq_learn_grad_ev(N.C.byref(a), self.grad.data_ptr(), N.stream_ptr(),
+                                          N.C.c_void_p(self._fc1_done.cuda_event)), "learn_grad")
+        big, rest = self.buckets()
+        self._comm.wait_event(self._fc1_done)
+        with torch.cuda.stream(self._comm):
+            w_big = dist.all_reduce(big, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        w_rest = [dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group, async_op=True) for t in rest]
+        for w in [w_big] + w_rest:
+            w.wait()  # the current stream waits for the collective
         self.apply()
 
     def check_finite(self):

@@ -98,3 +98,32 @@ def test_dp_update_equals_single_device_step(memory, B):
     # the bf16 GEMM shadow follows the master
     assert torch.equal(learners[0].theta.shadow[:8192],
                        learners[0].theta.master[:8192].bfloat16().view(torch.int16))
+
+
+@pytest.mark.parametrize("B", [64, 1024])
+def test_gradient_event_marks_the_fc1_bucket(memory, B):
+    """pq_learn_grad_ev (the NCCL-overlapped DP step): the same gradient as pq_learn_grad,
+    and when its fc1 event has fired the fc1 bucket already holds its final values even
+    though the conv layers' backward may still run; the two buckets tile the gradient."""
+    from paper_2111_01264_b200 import _native as N
+
+    idx = torch.as_tensor(memory.sample_indices(B, np.random.default_rng(7)), device="cuda")
+    theta, opt, target = fresh()
+    ref = DataParallelLearner(theta, opt, target, memory, B).shard_gradient(idx).clone()
+    dp = DataParallelLearner(theta, opt, target, memory, B)
+    big, rest = dp.buckets()
+    assert big.numel() + sum(t.numel() for t in rest) == dp.grad.numel() == dnn.num_params(A)
+    assert big.numel() == 512 * 3136 and rest[0].numel() == dnn.num_params(A) - 512 * 3136 - rest[1].numel()
+    dp.grad.fill_(float("nan"))
+    ev = torch.cuda.Event()
+    ev.record()
+    a = dp._args(idx)
+    N.check(N.load().pq_learn_grad_ev(N.C.byref(a), dp.grad.data_ptr(), N.stream_ptr(),
+                                      N.C.c_void_p(ev.cuda_event)), "learn_grad_ev")
+    side = torch.cuda.Stream()
+    side.wait_event(ev)
+    with torch.cuda.stream(side):
+        early = big.clone()
+    torch.cuda.synchronize()
+    assert torch.equal(early, ref[big.data_ptr() // 4 - dp.grad.data_ptr() // 4:][:big.numel()])
+    assert torch.equal(dp.grad, ref)
