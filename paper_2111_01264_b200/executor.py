@@ -242,6 +242,7 @@ class DeviceRun:
         self._flushed_blocks = 0   # lockstep blocks of this epoch already flushed into D
         self._epoch_trains = 0     # blocking training events of this epoch
         self._graphs = None
+        self._pipe_stale = True
         self._eval_idx = 0
         self._eval = None
         self._pending_eval = None
@@ -309,20 +310,35 @@ class DeviceRun:
             max_batch=self.act_cap)
 
     def learn_step(self, stream=None):
+        """One self-contained learner step on the minibatch at the step counter (the
+        one-shot pq_learn_step: the target forward inside the step).  Any caller may use
+        it; it leaves the epoch driver's target pipeline to be re-primed."""
         a = self._learn_args()
-        fn = N.load().pq_learn_step_pipelined if self.pipelined else N.load().pq_learn_step
-        N.check(fn(N.C.byref(a), N.stream_ptr(stream)), "learn_step")
+        N.check(N.load().pq_learn_step(N.C.byref(a), N.stream_ptr(stream)), "learn_step")
+        self._pipe_stale = True
+
+    def _epoch_step(self, stream=None):
+        """The epoch driver's learner step: pipelined (the target forward of the next
+        minibatch rides in this step's launches, pq_learn_step_pipelined) when enabled.
+        Its target activations were primed by begin_epoch / the last pipelined step."""
+        if not self.pipelined:
+            return self.learn_step(stream)
+        if self._pipe_stale:
+            self.target_prologue(stream)
+        a = self._learn_args()
+        N.check(N.load().pq_learn_step_pipelined(N.C.byref(a), N.stream_ptr(stream)), "learn_step")
 
     def target_prologue(self, stream=None):
         """Target conv1..conv3 of the minibatch at the step counter (pipelined learner)."""
         if self.pipelined:
             a = self._learn_args()
             N.check(N.load().pq_learn_target_prologue(N.C.byref(a), N.stream_ptr(stream)), "target prologue")
+            self._pipe_stale = False
 
     def learn_epoch(self):
         """All C/F learner steps of the epoch on the current stream."""
         for _ in range(self.updates):
-            self.learn_step()
+            self._epoch_step()
 
     def act_step(self, stream=None):
         a = self._act_args()
@@ -344,14 +360,14 @@ class DeviceRun:
         saved = [t.clone() for t in keep]
         self.idx_table.zero_()
         self.act_step()
-        self.learn_step()
+        self._epoch_step()
         torch.cuda.synchronize()
         for t, v in zip(keep, saved):
             t.copy_(v)
         k = self.graph_chunk
         graphs = {}
         for name, fn, n in (("act", self.act_step, min(k, self.steps)),
-                            ("learn", self.learn_step, min(k, self.updates))):
+                            ("learn", self._epoch_step, min(k, self.updates))):
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream()
             if name == "learn":
@@ -913,7 +929,7 @@ class HostEnvRun(DeviceRun):
         else:
             with torch.cuda.stream(self.learn_stream):
                 for _ in range(self.updates):
-                    self.learn_step()
+                    self._epoch_step()
         with torch.cuda.stream(self.act_stream):
             for b in range(self.steps):
                 self.act_block(b)
