@@ -503,6 +503,55 @@ PQ_DEV void store_masked32(bf16 *dst, const bf16 *mask, const float *v, int nval
     }
 }
 
+// A 64-channel row of a data gradient, the mask (forward activation) loaded ahead of the
+// accumulator (a TMA kernel's epilogue issues it before waiting for the MMAs), the masked
+// bf16 row computed once and stored to every layout the consumers want.
+struct MaskRow64 {
+    uint4 w[8];
+    PQ_DEV void load(const bf16 *mask) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) w[c] = __ldg(reinterpret_cast<const uint4 *>(mask) + c);
+    }
+    // w <- bf16(v * (mask > 0)) in place
+    PQ_DEV void apply(const float *v) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const uint32_t mw[4] = {w[c].x, w[c].y, w[c].z, w[c].w};
+            uint32_t o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                o[e] = pack_bf16(bf16_lo(mw[e]) > 0.f ? v[c * 8 + 2 * e] : 0.f,
+                                 bf16_hi(mw[e]) > 0.f ? v[c * 8 + 2 * e + 1] : 0.f);
+            w[c] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+    PQ_DEV void store(bf16 *dst) const {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) reinterpret_cast<uint4 *>(dst)[c] = w[c];
+    }
+};
+
+// 32 channels of the same (for conv2's data gradient: one parity class of an s2d pixel)
+struct MaskRow32 {
+    uint4 w[4];
+    PQ_DEV void load(const bf16 *mask) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) w[c] = __ldg(reinterpret_cast<const uint4 *>(mask) + c);
+    }
+    PQ_DEV void apply_store(bf16 *dst, const float *v) const {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const uint32_t mw[4] = {w[c].x, w[c].y, w[c].z, w[c].w};
+            uint32_t o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                o[e] = pack_bf16(bf16_lo(mw[e]) > 0.f ? v[c * 8 + 2 * e] : 0.f,
+                                 bf16_hi(mw[e]) > 0.f ? v[c * 8 + 2 * e + 1] : 0.f);
+            reinterpret_cast<uint4 *>(dst)[c] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+};
+
 // data gradient: bf16 out[m][n] = acc * (mask[m][n] > 0), mask = forward activation
 struct EpiMask {
     bf16 *out;

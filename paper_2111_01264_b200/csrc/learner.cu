@@ -16,6 +16,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstring>
 
@@ -564,8 +565,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_resident_a(const __grid_con
     } else if (warp >= 4 && nk > 0) {  // epilogue
         const int wq = warp - 4;
         uint32_t it = 0;
+        constexpr bool MASK = std::is_same<EP, EpiMaskPad7>::value;
         for (int nt = nt0; nt < nt1; ++nt, ++it) {
             const uint32_t buf = it & 1;
+            const int row = mt * 128 + wq * 32 + lane;
+            MaskRow64 mk;  // fc1 data gradient: act3's 64 channels of pixel nt, loaded under the MMAs
+            if constexpr (MASK)
+                if (row < g.ep[grp].e.M) mk.load(g.ep[grp].e.mask + (size_t)row * 3136 + nt * 64);
             mbar_wait(&accf[buf], (it >> 1) & 1);
             __syncwarp();
             tc_fence_after();
@@ -576,9 +582,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_resident_a(const __grid_con
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acce[buf]);
-            const int row = mt * 128 + wq * 32 + lane;
-            g.ep[grp].apply(row, nt * 64, v[0], 32, split);
-            g.ep[grp].apply(row, nt * 64 + 32, v[1], 32, split);
+            if constexpr (MASK) {  // dY3 and its copy on the padded 11 x 11 grid
+                if (row < g.ep[grp].e.M) {
+                    const EpiMaskPad7 &ep = g.ep[grp];
+                    const int y = nt / 7, x = nt - y * 7;
+                    mk.apply(&v[0][0]);
+                    mk.store(ep.e.out + (size_t)row * 3136 + nt * 64);
+                    mk.store(ep.out_pad + ((size_t)(row * 11 + y + 2) * 11 + x + 2) * 64);
+                }
+            } else {
+                g.ep[grp].apply(row, nt * 64, v[0], 32, split);
+                g.ep[grp].apply(row, nt * 64 + 32, v[1], 32, split);
+            }
         }
     }
     tc_fence_before();
@@ -729,9 +744,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv3_dgrad_shift(const __g
         }
     } else if (warp >= 4) {  // epilogue
         const int wq = warp - 4;
+        const EpiMaskPad &ep = g.ep;
         uint32_t q = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
             const uint32_t buf = q & 1;
+            // this row's forward activation (the ReLU mask) in flight while the MMAs run
+            const int r = t * 128 + wq * 32 + lane, smp = r / 121, p = r - smp * 121, y = p / 11, x = p - y * 11;
+            const bool live = smp < g.n && y < 9 && x < 9;
+            const int m = smp * 81 + y * 9 + x;
+            MaskRow64 row;
+            if (live) row.load(ep.e.mask + (size_t)m * 64);
             mbar_wait(&accf[buf], (q >> 1) & 1);
             __syncwarp();
             tc_fence_after();
@@ -742,11 +764,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv3_dgrad_shift(const __g
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acce[buf]);
-            const int r = t * 128 + wq * 32 + lane, smp = r / 121, p = r - smp * 121, y = p / 11, x = p - y * 11;
-            if (smp < g.n && y < 9 && x < 9) {
-                const int m = smp * 81 + y * 9 + x;
-                g.ep.apply(m, 0, v[0], 32, 0);
-                g.ep.apply(m, 32, v[1], 32, 0);
+            if (live) {  // dY2, its copy on the padded 11 x 11 grid and on the 10 x 10 grid
+                row.apply(&v[0][0]);
+                row.store(ep.e.out + (size_t)m * 64);
+                row.store(ep.out_pad + ((size_t)(smp * 11 + y + 1) * 11 + x + 1) * 64);
+                if (ep.out10) row.store(ep.out10 + ((size_t)(smp * 10 + y) * 10 + x) * 64);
             }
         }
     }
@@ -952,22 +974,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_dgrad_shift(const __g
         uint32_t q = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
             const uint32_t buf = q & 1;
+            const int r = t * 128 + wq * 32 + lane, smp = r / 121, p = r - smp * 121, y = p / 11, x = p - y * 11;
+            const bool ok = smp < g.n && y < 10 && x < 10;
+            // the four classes' ReLU masks in flight while the MMAs run (act1 pixel
+            // (2y + py, 2x + px) = s2d pixel (y, x), channels (py * 2 + px) * 32)
+            MaskRow32 mk[4];
+            if (ok)
+#pragma unroll
+                for (int cls = 0; cls < 4; ++cls) {
+                    const int iy = 2 * y + (cls >> 1), ix = 2 * x + (cls & 1);
+                    mk[cls].load(g.mask + (g.mask_s2 ? ((size_t)(smp * 10 + y) * 10 + x) * 128 + cls * 32
+                                                     : ((size_t)(smp * 20 + iy) * 20 + ix) * 32));
+                }
             mbar_wait(&accf[buf], (q >> 1) & 1);
             __syncwarp();
             tc_fence_after();
-            const int r = t * 128 + wq * 32 + lane, smp = r / 121, p = r - smp * 121, y = p / 11, x = p - y * 11;
-            const bool ok = smp < g.n && y < 10 && x < 10;
-#pragma unroll 1
+#pragma unroll
             for (int cls = 0; cls < 4; ++cls) {
                 float v[32];
                 tmem_ld32(tmem + buf * 256 + cls * 64 + ((uint32_t)(wq * 32) << 16), v);
                 if (ok) {
                     const int iy = 2 * y + (cls >> 1), ix = 2 * x + (cls & 1);
-                    const size_t o = ((size_t)(smp * 20 + iy) * 20 + ix) * 32;
-                    const size_t oo = g.pad21 ? ((size_t)(smp * 21 + iy) * 21 + ix) * 32 : o;
-                    // act1 pixel (iy, ix) = s2d pixel (y, x), channels (py * 2 + px) * 32
-                    const size_t om = g.mask_s2 ? ((size_t)(smp * 10 + y) * 10 + x) * 128 + cls * 32 : o;
-                    store_masked32(g.out + oo, g.mask + om, v, 32);
+                    const int gw = g.pad21 ? 21 : 20;
+                    mk[cls].apply_store(g.out + ((size_t)(smp * gw + iy) * gw + ix) * 32, v);
                 }
             }
             tc_fence_before();
