@@ -21,7 +21,7 @@ namespace pq {
 int set_err(const char *msg);
 int cuda_err(cudaError_t e, const char *where);
 int act_forward(pq_net net, const uint8_t *ring, const int32_t *stack, int W, int A, void *ws,
-                int max_batch, const float **part_out, uint32_t **done_out, cudaStream_t st);
+                int max_batch, const float **part_out, uint32_t **done_out, int *splits_out, cudaStream_t st);
 
 __device__ __forceinline__ uint64_t env_frame_base(uint64_t key, int64_t episode, int t, int action) {
     return splitmix64(splitmix64(splitmix64(key) ^ (uint64_t)episode) ^
@@ -50,6 +50,7 @@ struct ActArgs {
     double term_p;
     float *q_out;
     int max_episodes;
+    int splits;  // fc1 partial splits (FC1_SPLITS, or 1 after k_fc1_acc7)
 };
 
 __device__ __forceinline__ float warp_sum_f(float v) {
@@ -91,14 +92,16 @@ __global__ void __launch_bounds__(256) k_act_env(const ActArgs a) {
         for (int i = 0; i < 2; ++i) {
             const int jj = tid + 256 * i;
 #pragma unroll
-            for (int sp = 0; sp < FC1_SPLITS; ++sp) v[i][sp] = a.part[((size_t)sp * a.W + j) * 512 + jj];
+            for (int sp = 0; sp < FC1_SPLITS; ++sp)
+                v[i][sp] = sp < a.splits ? a.part[((size_t)sp * a.W + j) * 512 + jj] : 0.f;
             v[i][FC1_SPLITS] = a.master[P_B4 + jj];
         }
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             float s = 0.f;
 #pragma unroll
-            for (int sp = 0; sp < FC1_SPLITS; ++sp) s += v[i][sp];
+            for (int sp = 0; sp < FC1_SPLITS; ++sp)
+                if (sp < a.splits) s += v[i][sp];
             s += v[i][FC1_SPLITS];
             hs[tid + 256 * i] = s > 0.f ? s : 0.f;
         }
@@ -301,8 +304,9 @@ int pq_act_step(const pq_act_args *x, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const float *part = nullptr;
     uint32_t *done = nullptr;
+    int splits = FC1_SPLITS;
     int rc = act_forward(x->net, x->ring, x->envs.stack, x->W, x->actions, x->ws, x->max_batch,
-                         &part, &done, st);
+                         &part, &done, &splits, st);
     if (rc) return rc;
     ActArgs a{};
     a.part = part;
@@ -320,6 +324,7 @@ int pq_act_step(const pq_act_args *x, void *stream) {
     a.term_p = x->terminal_p;
     a.q_out = x->q_out;
     a.max_episodes = x->max_episodes;
+    a.splits = splits;
     return cuda_err(launch_k(k_act_env, dim3(x->W), dim3(256), 0, st, a), "act_env");
 }
 

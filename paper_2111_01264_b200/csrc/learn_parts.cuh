@@ -25,6 +25,7 @@ struct HeadArgs {
     const float *part[2];  // fc1 split-K partials [splits][n][512] of group 0 / 1
     const float *master[2];
     int groups, n, A, n8;
+    int splits;  // fc1 partial splits to sum (FC1_SPLITS, or 1 after k_fc1_acc7)
     const int32_t *records;
     const int64_t *idx;       // sampled slots, or
     const int64_t *idx_base;  // epoch table sliced by *counter

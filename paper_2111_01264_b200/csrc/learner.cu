@@ -656,6 +656,135 @@ int tma_fc1_dgrad_resident(const pq_net &th, const bf16 *dh1_bf, const bf16 *act
     return launch_resident_a<EpiMask, true>(g, st, "fc1 dgrad (resident dh1)");
 }
 
+// ---- fc1 forward at large batches, the split reduction done in TMEM
+// One CTA per (group, 128-unit M tile of W4, 64-sample N tile) runs all 49 K chunks into
+// FC1_SPLITS accumulators of 64 TMEM columns (chunk c -> accumulator c / 7, restarted at
+// its first chunk exactly like a split-K CTA), then sums them in split order and writes
+// the sum to split slot 0 of the partial buffer: the head / acting kernels read one split
+// (0 + S + bias == the split-K sum ((0 + p0) + ... + p6) + bias bit for bit), and the
+// 7 x n x 512 fp32 partial round trip through HBM is gone.
+constexpr int F7_STAGES = 8, F7_SLOT = 3 * PL_BOX, F7_SMEM = 1024 + F7_STAGES * F7_SLOT;
+constexpr int F7_KC = 49 / FC1_SPLITS;
+struct F7Args {
+    CUtensorMap a[2], b[2];  // W4 [512][3136]; act3 [n][3136]
+    float *part[2];          // [n][512] (split slot 0)
+    int n, ntiles;
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1) k_fc1_acc7(const __grid_constant__ F7Args g) {
+    constexpr uint32_t IDESC = idesc_bf16(64, false, false);
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t full[F7_STAGES], empty[F7_STAGES], accf;
+    __shared__ uint32_t tmem_base_s;
+    TlProbe tp;
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t ring_s = smem_u32(smem);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nt = blockIdx.x % g.ntiles, mt = (blockIdx.x / g.ntiles) % 4, grp = blockIdx.x / (4 * g.ntiles);
+    if (tid == 0) {
+        for (int s = 0; s < F7_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&accf, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<512>(&tmem_base_s);
+    if (tid == 32) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&g.a[grp]) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&g.b[grp]) : "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+    // W4 (updated two or more launches back) for the first ring slots before the wait
+    if (tid == 0)
+        for (int c = 0; c < F7_STAGES; ++c) {
+            mbar_expect_tx(&full[c], (uint32_t)F7_SLOT);
+            for (int h = 0; h < 2; ++h)
+                tma_load_2d(ring_s + c * F7_SLOT + h * PL_BOX, &g.a[grp], &full[c], c * 64, mt * 128 + h * 64);
+        }
+    griddep_wait();
+    griddep_launch();
+    tp.waited();
+    if (warp == 0) {
+        if (lane == 0) {  // producer
+            for (int c = 0; c < 49; ++c) {
+                const uint32_t s = c % F7_STAGES, dst = ring_s + s * F7_SLOT;
+                if (c >= F7_STAGES) {
+                    mbar_wait(&empty[s], ((c / F7_STAGES) - 1) & 1);
+                    mbar_expect_tx(&full[s], (uint32_t)F7_SLOT);
+                    for (int h = 0; h < 2; ++h)
+                        tma_load_2d(dst + h * PL_BOX, &g.a[grp], &full[s], c * 64, mt * 128 + h * 64);
+                }
+                tma_load_2d(dst + 2 * PL_BOX, &g.b[grp], &full[s], c * 64, nt * 64);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            for (int c = 0; c < 49; ++c) {
+                const uint32_t s = c % F7_STAGES, a0 = ring_s + s * F7_SLOT;
+                mbar_wait(&full[s], (c / F7_STAGES) & 1);
+                tc_fence_after();
+                const uint32_t acc = tmem + (c / F7_KC) * 64;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    umma_bf16(acc, desc_sw128(a0 + j * 32, 0), desc_sw128(a0 + 2 * PL_BOX + j * 32, 0), IDESC,
+                              (c % F7_KC != 0 || j > 0) ? 1u : 0u);
+                umma_commit(&empty[s]);
+            }
+            umma_commit(&accf);
+        }
+    } else if (warp >= 4) {  // epilogue: row = output unit j, columns = 64 samples
+        const int wq = warp - 4, j = mt * 128 + wq * 32 + lane;
+        mbar_wait(&accf, 0);
+        __syncwarp();
+        tc_fence_after();
+        float *out = g.part[grp];
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            float sum[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) sum[e] = 0.f;
+#pragma unroll 1
+            for (int sp = 0; sp < FC1_SPLITS; ++sp) {
+                float v[32];
+                tmem_ld32(tmem + sp * 64 + h * 32 + ((uint32_t)(wq * 32) << 16), v);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) sum[e] += v[e];
+            }
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+                const int b = nt * 64 + h * 32 + e;
+                if (b < g.n) out[(size_t)b * 512 + j] = sum[e];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem);
+    tp.done('7');
+}
+
+int tma_fc1_fwd_acc7(const pq_net *nets, bf16 *const *act3, float *const *part, int groups, int n, cudaStream_t st) {
+    static thread_local F7Args g;
+    memset(&g, 0, sizeof(g));
+    for (int q = 0; q < groups; ++q) {
+        if (int rc = map2(&g.a[q], (const bf16 *)nets[q].shadow + S_W4, 512, 3136, 3136, "W4")) return rc;
+        if (int rc = map2(&g.b[q], act3[q], n, 3136, 3136, "act3")) return rc;
+        g.part[q] = part[q];
+    }
+    g.n = n, g.ntiles = (n + 63) / 64;
+    static bool configured = false;
+    if (!configured) {
+        PQ_CUDA_TRY(cudaFuncSetAttribute(k_fc1_acc7, cudaFuncAttributeMaxDynamicSharedMemorySize, F7_SMEM));
+        configured = true;
+    }
+    return cuda_err(launch_k(k_fc1_acc7, dim3(groups * 4 * g.ntiles), dim3(GEMM_THREADS), F7_SMEM, st, g),
+                    "fc1 forward (split sums in TMEM)");
+}
+
 // ---- conv3 data gradient by row-shifted descriptors
 // dY2 = relu'(act2) * transposed conv3(dY3): on the zero-padded 11 x 11 grid dY3p (dY3 at
 // (y + 2, x + 2), written by fc1's data gradient) GEMM row r = (s, y, x) (y, x = 9, 10

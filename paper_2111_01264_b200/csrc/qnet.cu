@@ -41,6 +41,7 @@ int cuda_err(cudaError_t e, const char *where) {
 int tma_conv3_fwd(const pq_net *nets, bf16 *const *act2, bf16 *const *act3, int groups, int n, cudaStream_t st);
 int tma_fc1_fwd(const pq_net *nets, bf16 *const *act3, float *const *part, int splits, int groups, int n,
                 cudaStream_t st);
+int tma_fc1_fwd_acc7(const pq_net *nets, bf16 *const *act3, float *const *part, int groups, int n, cudaStream_t st);
 int tma_fc1_fwd_resident(const pq_net *nets, bf16 *const *act3, float *const *part, int splits, int groups, int n,
                          cudaStream_t st);
 int tma_fc1_dgrad_resident(const pq_net &th, const bf16 *dh1_bf, const bf16 *act3, bf16 *dY3, int n,
@@ -91,6 +92,19 @@ static bool use_tma(int n) {
     }
     return mode >= 0 ? mode == 1 : n >= 128;
 }
+
+// fc1 forward with the split sums reduced in TMEM (learner.cu k_fc1_acc7) from this batch
+// up (PQ_F7=0: the resident-A split-K kernel); the head / acting kernels then read 1 split
+constexpr int F7_MIN_BATCH = 512;
+static bool fc1_acc7(int n) {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("PQ_F7");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1 && n >= F7_MIN_BATCH && use_tma(n) && conv1_shift();
+}
+int fc1_splits(int n) { return fc1_acc7(n) ? 1 : FC1_SPLITS; }
 
 // ------------------------------------------------------------------ workspace
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -258,6 +272,7 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
         g.M = n * 49, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
         PQ_CHECK((launch_gemm<64, false, false, 0, 2>(g, groups, st)), "conv3 forward");
     }
+    if (fc1_acc7(n)) return tma_fc1_fwd_acc7(nets, a3, pt, groups, n, st);
     if (use_tma(n) && conv1_shift())  // W4 chunks resident per CTA
         return tma_fc1_fwd_resident(nets, a3, pt, FC1_SPLITS, groups, n, st);
     if (use_tma(n)) return tma_fc1_fwd(nets, a3, pt, FC1_SPLITS, groups, n, st);
@@ -300,12 +315,16 @@ __device__ __forceinline__ void last_block_bump(int32_t *counter, uint32_t *done
 __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a, int32_t *bump, uint32_t *done) {
     TlProbe tp;
     ct_begin();
-    head_sample<FC1_SPLITS>(a, blockIdx.x, [&] {
+    auto wait = [&] {
         griddep_wait();
         griddep_launch();
         tp.waited();
         ct_mark(1);
-    });
+    };
+    if (a.splits == 1)  // fc1 sums reduced by the forward GEMM (k_fc1_acc7)
+        head_sample<1>(a, blockIdx.x, wait);
+    else
+        head_sample<FC1_SPLITS>(a, blockIdx.x, wait);
     if (bump) last_block_bump(bump, done);
     tp.done('H');
     ct_end('H');
@@ -322,7 +341,7 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
         h.part[g] = w.fc1part[g];
         h.master[g] = nets[g].master;
     }
-    h.groups = groups, h.n = n, h.A = A, h.n8 = w.n8;
+    h.groups = groups, h.n = n, h.A = A, h.n8 = w.n8, h.splits = fc1_splits(n);
     h.learner = learner;
     h.q_out = w.q, h.h1 = w.h1, h.dh1 = w.dh1, h.td = w.td, h.dh1_bf = w.dh1_bf, h.dh1T = w.dh1T;
     h.act_out = w.act;
@@ -965,12 +984,13 @@ __global__ void k_rmsprop(const float *p, const float *g, const float *m, const 
 
 // acting forward: F1..F4 over the W current stacks (refs [W][4]), fc1 partials out
 int act_forward(pq_net net, const uint8_t *ring, const int32_t *stack, int W, int A, void *ws,
-                int max_batch, const float **part_out, uint32_t **done_out, cudaStream_t st) {
+                int max_batch, const float **part_out, uint32_t **done_out, int *splits_out, cudaStream_t st) {
     WS w = carve(ws, max_batch, A);
     FwdInput in{ring, stack, nullptr, nullptr, 0, 4, 0};
     int rc = forward_gemms(&net, &in, 1, W, w, st);
     *part_out = w.fc1part[0];
     *done_out = w.done + 1;
+    *splits_out = fc1_splits(W);
     return rc;
 }
 
@@ -1003,6 +1023,8 @@ using namespace pq;
 extern "C" {
 
 int pq_abi_version(void) { return PQ_ABI_VERSION; }
+
+int pq_fc1_splits(int n) { return fc1_splits(n); }
 
 int pq_cta_trace(int on, unsigned long long *out, int *count) {
     if (out) {
