@@ -562,6 +562,17 @@ struct EpiMask {
         const int nv = min(cnt, N - n0);
         store_masked32(out + (size_t)m * ld + n0, mask + (size_t)m * ld + n0, v, nv);
     }
+    // 32-column prefetch (the cp.async engine requests it before its dependency wait:
+    // the mask is a forward activation of the step, written two or more launches back)
+    using Pre = MaskRow32;
+    PQ_DEV bool pre_ok(int m, int n0) const { return m < M && n0 + 32 <= N; }
+    PQ_DEV void prefetch(Pre &p, int m, int n0) const {
+        if (pre_ok(m, n0)) p.load(mask + (size_t)m * ld + n0);
+    }
+    PQ_DEV void apply_pre(const Pre &p, int m, int n0, const float *v) const {
+        if (pre_ok(m, n0)) p.apply_store(out + (size_t)m * ld + n0, v);
+        else apply(m, n0, v, 32, 0);
+    }
 };
 
 // EpiMask that also writes the masked rows of a 9 x 9 map onto a zero-padded 11 x 11
@@ -616,6 +627,27 @@ struct EpiMaskP {
         size_t oo = pad ? ((size_t)(b * (2 * H2 + 1) + iy) * (2 * W2 + 1) + ix) * C + n0 : o;
         store_masked32(out + oo, mask + o, v, min(cnt, C - n0));
     }
+    // prefetch (see EpiMask): the mask offset and the output offset of row m
+    struct Pre {
+        MaskRow32 mk;
+        int64_t o, oo;  // -1: not a live row / not a full 32-column chunk
+    };
+    PQ_DEV void prefetch(Pre &p, int m, int n0) const {
+        p.o = p.oo = -1;
+        int cls = f_per.div(m), loc = m - cls * tpc * 128;
+        int npix = H2 * W2;
+        if (loc >= n * npix || n0 + 32 > C) return;
+        int b = f_npix.div(loc), rem = loc - b * npix;
+        int ry = f_w2.div(rem);
+        int iy = 2 * ry + (cls >> 1), ix = 2 * (rem - ry * W2) + (cls & 1);
+        p.o = ((int64_t)(b * 2 * H2 + iy) * (2 * W2) + ix) * C + n0;
+        p.oo = pad ? ((int64_t)(b * (2 * H2 + 1) + iy) * (2 * W2 + 1) + ix) * C + n0 : p.o;
+        p.mk.load(mask + p.o);
+    }
+    PQ_DEV void apply_pre(const Pre &p, int m, int n0, const float *v) const {
+        if (p.o >= 0) p.mk.apply_store(out + p.oo, v);
+        else apply(m, n0, v, 32, 0);
+    }
 };
 PQ_HD EpiMaskP epi_mask_p(bf16 *out, const bf16 *mask, int n, int H2, int W2, int C, int tpc, int pad = 0) {
     EpiMaskP e{out, mask, n, H2, W2, C, tpc};
@@ -629,6 +661,24 @@ struct EpiMaskT {
     bf16 *out;
     const bf16 *mask;
     int M, N, ld;
+    // prefetch (see EpiMask): the 32 samples' mask values of feature m
+    struct Pre {
+        bf16 mk[32];
+    };
+    PQ_DEV void prefetch(Pre &p, int m, int n0) const {
+        if (m >= M) return;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            p.mk[j] = n0 + j < N ? mask[(size_t)(n0 + j) * ld + m] : __float2bfloat16_rn(0.f);
+    }
+    PQ_DEV void apply_pre(const Pre &p, int m, int n0, const float *v) const {
+        if (m >= M) return;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (n0 + j >= N) break;
+            out[(size_t)(n0 + j) * ld + m] = __float2bfloat16_rn(__bfloat162float(p.mk[j]) > 0.f ? v[j] : 0.f);
+        }
+    }
     PQ_DEV void apply(int m, int n0, const float *v, int cnt, int) const {
         if (m >= M) return;
         bf16 mk[32];
@@ -780,6 +830,18 @@ struct EpiRms4 : EpiRms {
     PQ_DEV void apply_tile(const float *tile, int ld, int m0, int n0) const {
         apply_tile_w<BN, 8, 4>(tile, ld, m0, n0, threadIdx.x >> 5);
     }
+};
+
+// epilogues that can request their per-row inputs before the dependency wait
+template <class EP, class = void>
+struct has_pre {
+    static constexpr bool value = false;
+    struct Pre {};
+};
+template <class EP>
+struct has_pre<EP, decltype((void)sizeof(typename EP::Pre))> {
+    static constexpr bool value = true;
+    using Pre = typename EP::Pre;
 };
 
 template <class EP, class = void>
@@ -1009,6 +1071,15 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
             if (PF == 2) issue_b(kb0 + s, slot_of(s));
         }
     }
+    // the epilogue's per-row inputs (data gradients' ReLU masks: forward activations of
+    // the step, written two or more launches back) also go out before the wait; each
+    // thread owns exactly one 32-column chunk of the tile (BN <= 64)
+    constexpr bool EPRE = has_pre<EP>::value && BN <= 64 && BN >= 32 && !is_staged<EP>::value;
+    typename has_pre<EP>::Pre epre{};
+    const int e_wq = warp & 3, e_half = warp >> 2;
+    const int e_row = m0 + e_wq * 32 + lane, e_c0 = BN >= 64 ? e_half * (BN / 2) : 0;
+    if constexpr (EPRE)
+        if (BN >= 64 || e_half == 0) ep.prefetch(epre, e_row, n0 + e_c0);
     hook();
     ct_mark(1);
     if (tl) tl_t[tl_i++] = gtime();  // 1: predecessor done
@@ -1093,6 +1164,17 @@ PQ_DEV void gemm_tile(const LA &la_in, const LB &lb_in, const EP &ep, int kb0, i
         }
         __syncthreads();
         ep.template apply_tile<BN>(tile, BN + 1, m0, n0);
+    } else if constexpr (EPRE) {
+        if (BN >= 64 || half == 0) {
+            float v[32];
+            if (nk > 0) {
+                tmem_ld32(trow + e_c0, v);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) v[e] = 0.f;
+            }
+            ep.apply_pre(epre, row, n0 + e_c0, v);
+        }
     } else if (BN >= 64 || half == 0) {
         const int cbeg = BN >= 64 ? half * CW : 0;
 #pragma unroll 1
