@@ -26,6 +26,7 @@ struct HeadArgs {
     const float *master[2];
     int groups, n, A, n8;
     int splits;  // fc1 partial splits to sum (FC1_SPLITS, or 1 after k_fc1_acc7)
+    int block;   // samples per CTA (1: head_sample; HEAD_BLOCK: head_block, with splits == 1)
     const int32_t *records;
     const int64_t *idx;       // sampled slots, or
     const int64_t *idx_base;  // epoch table sliced by *counter
@@ -52,6 +53,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 constexpr int HEAD_THREADS = 256;
+constexpr int HEAD_BLOCK = 8;  // samples per head CTA at large batches
 
 // One sample b (one 256-thread CTA).  S = fc1 split count; every global load of a
 // phase is independent so they are all in flight together.  Everything that does not
@@ -192,6 +194,163 @@ PQ_DEV void head_sample(const HeadArgs &a, int b, Wait wait = Wait{}) {
         const bf16 gb = __float2bfloat16_rn(g);
         a.dh1_bf[(size_t)b * 512 + j] = gb;
         a.dh1T[(size_t)j * a.n8 + b] = gb;
+    }
+}
+
+// NB samples per CTA (large batches, fc1 splits reduced by the forward: S = 1): the fc2
+// weights (A x 512 per network) are read once per NB samples instead of once per sample,
+// and the transposed bf16 hidden gradient goes out as NB contiguous values per unit.
+// Per sample the arithmetic is head_sample's, operation for operation.
+template <int S, int NB, class Wait = NoHook>
+PQ_DEV void head_block(const HeadArgs &a, int b0, Wait wait = Wait{}) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nb = min(NB, a.n - b0);
+    __shared__ float hs[NB][2][512];
+    __shared__ float qs[NB][2][MAX_ACTIONS];
+    __shared__ float s_delta[NB];
+    __shared__ int s_act[NB];
+    int4 rec_hi = make_int4(0, 0, 0, 0);  // thread s < nb: sample b0 + s
+    if (a.learner && tid < nb) {
+        const int b = b0 + tid;
+        int64_t slot = a.idx        ? a.idx[b]
+                       : a.idx_base ? a.idx_base[(int64_t)(*a.counter) * a.n + b]
+                                    : (int64_t)b;
+        if (!a.ext_targets) rec_hi = *reinterpret_cast<const int4 *>(a.records + slot * REC_INTS + 4);
+        if (a.idx_cur) a.idx_cur[b] = slot;
+        if (a.upd_cur && b == 0) *a.upd_cur = a.counter ? *a.counter : 0;
+    }
+    float b4[2][2], b5[2][4];
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        const int gg = g < a.groups ? g : 0;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) b4[g][i] = (*(a.master[gg] + P_B4 + tid + HEAD_THREADS * i));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) b5[g][u] = (*(a.master[gg] + p_b5(a.A) + min(warp + 8 * u, a.A - 1)));
+        for (int l = tid; l < a.A * 16; l += HEAD_THREADS)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.master[gg] + P_W5 + l * 32));
+    }
+    wait();
+#pragma unroll
+    for (int sb = 0; sb < NB; ++sb) {
+        if (sb >= nb) break;
+        const int b = b0 + sb;
+        float v[2][2][S + 1];
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int j = tid + HEAD_THREADS * i;
+                const int gg = g < a.groups ? g : 0;
+                const float *P = a.part[gg] + (size_t)b * 512 + j;
+#pragma unroll
+                for (int sp = 0; sp < S; ++sp) v[g][i][sp] = (*(P + (size_t)sp * a.n * 512));
+                v[g][i][S] = b4[g][i];
+            }
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                float s = 0.f;
+#pragma unroll
+                for (int sp = 0; sp < S; ++sp) s += v[g][i][sp];
+                s += v[g][i][S];
+                hs[sb][g][tid + HEAD_THREADS * i] = s > 0.f ? s : 0.f;
+            }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        if (g >= a.groups) break;
+        const float *w5 = a.master[g] + P_W5;
+        float wv[4][16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int aa = min(warp + 8 * u, a.A - 1);
+#pragma unroll
+            for (int t = 0; t < 16; ++t) wv[u][t] = (*(w5 + aa * 512 + lane + 32 * t));
+        }
+#pragma unroll 1
+        for (int sb = 0; sb < nb; ++sb) {
+            const int b = b0 + sb;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int aa = warp + 8 * u;
+                float acc = 0.f;
+#pragma unroll
+                for (int t = 0; t < 16; ++t) acc += wv[u][t] * hs[sb][g][lane + 32 * t];
+                acc = warp_sum(acc);
+                if (lane == 0 && aa < a.A) {
+                    float q = acc + b5[g][u];
+                    qs[sb][g][aa] = q;
+                    a.q_out[((size_t)g * a.n + b) * a.A + aa] = q;
+                    if (a.q_copy) a.q_copy[((size_t)g * a.n + b) * a.A + aa] = q;
+                }
+            }
+        }
+    }
+    if (!a.learner) return;
+    __syncthreads();
+    if (tid < nb) {
+        const int sb = tid, b = b0 + sb;
+        int act;
+        float target;
+        if (a.ext_targets) {
+            act = a.ext_actions[b];
+            target = a.ext_targets[b];
+        } else {
+            act = rec_action(rec_hi.y);
+            const double r = rec_reward(rec_hi.z, rec_hi.w);
+            if (rec_terminal(rec_hi.y)) {
+                target = (float)r;
+            } else {
+                float mx = qs[sb][1][0];
+                for (int aa = 1; aa < a.A; ++aa) mx = fmaxf(mx, qs[sb][1][aa]);
+                target = (float)(r + (double)a.gamma * (double)mx);
+            }
+        }
+        const float e = qs[sb][0][act] - target;
+        float d = e, loss = 0.5f * e * e;
+        if (a.huber > 0.f && fabsf(e) > a.huber) {
+            d = copysignf(a.huber, e);
+            loss = a.huber * (fabsf(e) - 0.5f * a.huber);
+        }
+        s_delta[sb] = d;
+        s_act[sb] = act;
+        a.act_out[b] = act;
+        a.td[b * 3 + 0] = target;
+        a.td[b * 3 + 1] = d;
+        a.td[b * 3 + 2] = loss;
+        if (a.td_copy) {
+            a.td_copy[b * 3 + 0] = target;
+            a.td_copy[b * 3 + 1] = d;
+            a.td_copy[b * 3 + 2] = loss;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int j = tid + HEAD_THREADS * i;
+        bf16 gbs[NB];
+#pragma unroll
+        for (int sb = 0; sb < NB; ++sb) {
+            gbs[sb] = __float2bfloat16_rn(0.f);
+            if (sb >= nb) continue;
+            const int b = b0 + sb;
+            const float d = s_delta[sb];
+            const float hv = hs[sb][0][j];
+            const float g = hv > 0.f ? d * (*(a.master[0] + P_W5 + (size_t)s_act[sb] * 512 + j)) : 0.f;
+            a.h1[(size_t)b * 512 + j] = hv;
+            a.dh1[(size_t)b * 512 + j] = g;
+            gbs[sb] = __float2bfloat16_rn(g);
+            a.dh1_bf[(size_t)b * 512 + j] = gbs[sb];
+        }
+        bf16 *dT = a.dh1T + (size_t)j * a.n8 + b0;
+        if (NB == 8 && nb == 8 && ((reinterpret_cast<uintptr_t>(dT) & 15) == 0)) {
+            *reinterpret_cast<uint4 *>(dT) = *reinterpret_cast<const uint4 *>(gbs);
+        } else {
+            for (int sb = 0; sb < nb; ++sb) dT[sb] = gbs[sb];
+        }
     }
 }
 

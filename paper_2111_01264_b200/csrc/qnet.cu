@@ -321,7 +321,9 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a, int32_t
         tp.waited();
         ct_mark(1);
     };
-    if (a.splits == 1)  // fc1 sums reduced by the forward GEMM (k_fc1_acc7)
+    if (a.block == HEAD_BLOCK)  // large batches: fc1 sums reduced by the forward GEMM (k_fc1_acc7)
+        head_block<1, HEAD_BLOCK>(a, blockIdx.x * HEAD_BLOCK, wait);
+    else if (a.splits == 1)
         head_sample<1>(a, blockIdx.x, wait);
     else
         head_sample<FC1_SPLITS>(a, blockIdx.x, wait);
@@ -342,6 +344,7 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
         h.master[g] = nets[g].master;
     }
     h.groups = groups, h.n = n, h.A = A, h.n8 = w.n8, h.splits = fc1_splits(n);
+    h.block = h.splits == 1 ? HEAD_BLOCK : 1;
     h.learner = learner;
     h.q_out = w.q, h.h1 = w.h1, h.dh1 = w.dh1, h.td = w.td, h.dh1_bf = w.dh1_bf, h.dh1T = w.dh1T;
     h.act_out = w.act;
@@ -353,7 +356,8 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
         h.idx_cur = w.idx_cur, h.upd_cur = w.upd_cur;
     }
     int32_t *bump = (la && learner && !la->idx && la->update_counter && bump_here) ? la->update_counter : nullptr;
-    return cuda_err(launch_k(k_head, dim3(n), dim3(HEAD_THREADS), 0, st, h, bump, w.done + 2), "head");
+    return cuda_err(launch_k(k_head, dim3((n + h.block - 1) / h.block), dim3(HEAD_THREADS), 0, st, h, bump, w.done + 2),
+                    "head");
 }
 
 // fc2 / fc1-bias gradient partials of one 64-sample chunk (blockIdx.x), 512 threads =
