@@ -43,6 +43,7 @@ int64_t pq_num_params(int actions);          /* 1,693,362 for 18 actions */
 int64_t pq_num_shadow(void);                 /* bf16 copies of the conv1..fc1 weights */
 /* Latency probes: enable/disable and read GEMM phase timestamps (out [256][12] ns). */
 int pq_timeline(int on, unsigned long long *out, int *count);
+int pq_timeline_tma(int on, unsigned long long *out, int *count); /* the TMA-engine kernels' probes */
 /* Per-CTA trace of the learner kernels: out [8192][6] = start, dependency released,
  * accumulator ready, end (ns), smid << 32 | linear CTA, tag << 48 | part << 40 | grid. */
 int pq_cta_trace(int on, unsigned long long *out, int *count);

@@ -68,6 +68,7 @@ EXPORTS = {
     "pq_num_params": ([C.c_int], C.c_int64),
     "pq_num_shadow": ([], C.c_int64),
     "pq_timeline": ([C.c_int, vp, vp], C.c_int),
+    "pq_timeline_tma": ([C.c_int, vp, vp], C.c_int),
     "pq_cta_trace": ([C.c_int, vp, vp], C.c_int),
     "pq_net_sync_shadow": ([PqNet, vp], C.c_int),
     "pq_net_copy": ([PqNet, PqNet, C.c_int, vp], C.c_int),

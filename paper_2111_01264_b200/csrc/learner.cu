@@ -1766,7 +1766,7 @@ int tma_conv2_wgrad_shift(const bf16 *act1s2, const bf16 *dY2q, float *part2, in
 // runs all three M tiles from the same operands.
 constexpr int W1S_ROWS = 88, W1S_ABOX = W1S_ROWS * 128, W1S_BBOX = 64 * 128, W1S_STAGES = 6;
 constexpr int W1S_SLOT = ((W1S_ABOX + W1S_BBOX + 1023) / 1024) * 1024;
-constexpr int W1S_SMEM = 1024 + 2 * 8192 + W1S_STAGES * W1S_SLOT;
+constexpr int W1S_SMEM = 1024 + W1S_STAGES * W1S_SLOT;
 struct W1SArgs {
     CUtensorMap a, b;  // s2d pixel rows [n*441][16*nframes]; dY1p [n*441][32]
     EpiF32T ep;        // part1[split][257][32]
@@ -1779,30 +1779,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __g
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t full[W1S_STAGES], empty[W1S_STAGES], accf;
     __shared__ uint32_t tmem_base_s;
+    __shared__ float bsum[4][32];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t ones_s = smem_u32(smem), ring_s = ones_s + 2 * 8192;
+    const uint32_t ring_s = smem_u32(smem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // ones operand (MN-major, 64 K rows x 128 B per M atom, two atoms): M index 0 = 1
-    for (int i = tid; i < 2 * 8192 / 16; i += blockDim.x) {
-        const int atom = i >> 9, k = (i >> 3) & 63, c8 = i & 7;
-        uint4 val = make_uint4(0, 0, 0, 0);
-        if (atom == 0 && c8 == 0) val.x = 0x3F80u;  // bf16 1.0 at M index 0 of every K row
-        *reinterpret_cast<uint4 *>(smem + atom * 8192 + mnmaj_off(k, c8) % 8192) = val;
-    }
     if (tid == 0) {
         for (int s = 0; s < W1S_STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], 5);  // the MMAs' commit + the 4 bias-summing warps
         }
         mbar_init(&accf, 1);
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc<256>(&tmem_base_s);
+    if (warp == 0) tmem_alloc<128>(&tmem_base_s);
     if (tid == 32) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&g.a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&g.b) : "memory");
     }
-    fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1832,7 +1825,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __g
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // MMA issuer: three 128 x 64 accumulators
+        if (lane == 0) {  // MMA issuer: two 128 x 64 accumulators (the four taps)
             uint32_t q = 0;
             for (int kb = kb0; kb < kb1; ++kb, ++q) {
                 const uint32_t s = q % W1S_STAGES;
@@ -1845,19 +1838,37 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __g
                     const uint64_t bd = desc_sw128(b0 + j * 2048, 8192);
                     umma_bf16(tmem, desc_sw128(a0 + j * 2048, 128), bd, IDESC, acc_on);
                     umma_bf16(tmem + 64, desc_sw128(a0 + 21 * 128 + j * 2048, 128), bd, IDESC, acc_on);
-                    umma_bf16(tmem + 128, desc_sw128(ones_s + j * 2048, 8192), bd, IDESC, acc_on);
                 }
                 umma_commit(&empty[s]);
             }
             umma_commit(&accf);
         }
-    } else if (warp >= 4) {  // epilogue
+    } else if (warp >= 4) {
+        // the bias row (sum of dY1 over the split's rows) from the B tiles in shared
+        // memory while the MMAs run: warp wq sums K rows 16 wq .. 16 wq + 15 of every chunk,
+        // lane = output channel (MN-major SW128: row r, channel chunk c8 at (c8 ^ (r & 7)))
         const int wq = warp - 4;
+        float bias = 0.f;
+        uint32_t q = 0;
+        for (int kb = kb0; kb < kb1; ++kb, ++q) {
+            const uint32_t s = q % W1S_STAGES;
+            mbar_wait(&full[s], (q / W1S_STAGES) & 1);
+            const uint8_t *bt = smem + s * W1S_SLOT + W1S_ABOX;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int r = wq * 16 + i;
+                bias += __bfloat162float(*reinterpret_cast<const bf16 *>(
+                    bt + r * 128 + (((lane >> 3) ^ (r & 7)) << 4) + (lane & 7) * 2));
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        bsum[wq][lane] = bias;
         mbar_wait(&accf, 0);
         __syncwarp();
         tc_fence_after();
 #pragma unroll 1
-        for (int mt = 0; mt < 3; ++mt) {
+        for (int mt = 0; mt < 2; ++mt) {
             float v[32];
             const int row = mt * 128 + wq * 32 + lane;
             if (kb1 > kb0) {
@@ -1866,12 +1877,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __g
 #pragma unroll
                 for (int e = 0; e < 32; ++e) v[e] = 0.f;
             }
-            if (mt < 2 || row == 256) g.ep.apply(row, 0, v, 32, split);
+            g.ep.apply(row, 0, v, 32, split);
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc<256>(tmem);
+    if (warp == 4) {  // bias row 256: the four warps' sums in row order
+        float v[32];
+        v[0] = 0.f;
+        for (int e = 0; e < 32; ++e) v[e] = ((bsum[0][e] + bsum[1][e]) + bsum[2][e]) + bsum[3][e];
+        if (lane == 0) g.ep.apply(256, 0, v, 32, split);
+    }
+    if (warp == 0) tmem_dealloc<128>(tmem);
     tp.done('W');
 }
 
@@ -1921,3 +1938,20 @@ using namespace pq;
 extern "C" {
 
 }  // extern "C"
+
+// the timeline probes of this translation unit (the TMA-engine / shifted-descriptor
+// kernels keep their own g_tl copy); same contract as pq_timeline in qnet.cu
+extern "C" int pq_timeline_tma(int on, unsigned long long *out, int *count) {
+    using namespace pq;
+    if (out) {
+        static Timeline h;
+        PQ_CUDA_TRY(cudaMemcpyFromSymbol(&h, g_tl, sizeof(Timeline)));
+        *count = h.n < 256 ? h.n : 256;
+        memcpy(out, h.t, sizeof(h.t));
+    }
+    static Timeline z;
+    memset(&z, 0, sizeof(z));
+    z.on = on;
+    PQ_CUDA_TRY(cudaMemcpyToSymbol(g_tl, &z, sizeof(Timeline)));
+    return 0;
+}

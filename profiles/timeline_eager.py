@@ -23,7 +23,7 @@ from paper_2111_01264_b200.replay import ReplayMemory
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 NAMES = {"G": "k_gemm", "F": "k_fused", "H": "k_head", "O": "k_optimizer", "P": "k_fc2_partials",
          "T": "k_tma_gemm", "D": "k_conv2_dgrad_shift", "S": "k_frames_s2d", "1": "k_conv1_shift",
-         "2": "k_conv2_shift", "W": "k_conv1_wgrad_shift", "V": "k_conv2_wgrad_shift", "3": "k_conv3_shift", "4": "k_resident_a", "C": "k_conv3_dgrad_shift"}
+         "2": "k_conv2_shift", "W": "k_conv1_wgrad_shift", "V": "k_conv2_wgrad_shift", "3": "k_conv3_shift", "4": "k_resident_a", "C": "k_conv3_dgrad_shift", "7": "k_fc1_acc7"}
 mem = ReplayMemory(40000)
 mem.prepopulate(FrameEnvSpec(key=5), 40000, np.random.default_rng(1))
 theta, target = dnn.init_network(dnn.network_sizes(), 1), dnn.init_network(dnn.network_sizes(), 2)
@@ -35,10 +35,11 @@ for it in range(5):
     if it == 4:
         torch.cuda.synchronize()
         lib.pq_timeline(1, None, None)
+        lib.pq_timeline_tma(1, None, None)
     theta, opt, _, _, _ = dnn._learn(theta, opt, target, mem.ring, mem.records, idx, B)
 torch.cuda.synchronize()
 recs = []
-for fn in (lib.pq_timeline,):
+for fn in (lib.pq_timeline, lib.pq_timeline_tma):
     out = (ctypes.c_ulonglong * (256 * 12))()
     cnt = ctypes.c_int(0)
     fn(0, ctypes.addressof(out), ctypes.addressof(cnt))
