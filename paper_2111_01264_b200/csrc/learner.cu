@@ -1258,12 +1258,21 @@ PQ_DEV void bias_relu_store32(const float *v, const float *bias, float scale, bf
 // The online (channels 0..63) and target (16..79) networks share the box; the target's
 // last K step (channels 64..79) comes from a second box at channel 64.  Same MMA order
 // (tap, 16-channel step) as the im2col kernels, so the outputs are bit-identical.
+// Both networks (the learner: online over frames 0..3, target over frames 1..4) run as
+// ONE N = 64 MMA per (tap, frame): the B tile of a tap holds the online filters in rows
+// 0..31 and the target filters, shifted one frame, in rows 32..63, with zeros where a
+// network does not see a frame (online: frame 4, target: frame 0).  5 K steps of N = 64
+// per tap instead of 2 x 4 of N = 32 (the A tile is read once per frame, not twice);
+// every accumulator sees the same products in the same order plus exact zeros, so the
+// outputs are unchanged.
 constexpr int C1_ROWS = 152, C1_BOX = C1_ROWS * 128, C1_STAGES = 4, C1_W = 32 * 128;
-constexpr int C1_SMEM = 1024 + 2 * 4 * C1_W + C1_STAGES * 2 * C1_BOX;
+constexpr int C1_WC = 2 * 64 * 128;  // combined B tile of a tap: 2 K blocks x 64 rows x 128 B
+constexpr int C1_SMEM = 1024 + 4 * C1_WC + C1_STAGES * 2 * C1_BOX;
 struct C1Args {
     CUtensorMap a, w[2];
     EpiBiasRelu ep[2];
     bf16 *act1s2[2];  // optional copy of act1 as [n][10][10][128] (2x2 space-to-depth) for k_conv2_shift
+    const bf16 *w1p[2];      // the permuted bf16 W1 of each group (combined B tiles)
     int n, groups, coff[2];  // channel offset of group g in the s2d pixel row
     int a_early, w_early;    // operands not written by the preceding launch: load before the wait
 };
@@ -1275,7 +1284,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_co
     __shared__ uint64_t full[C1_STAGES], empty[C1_STAGES], accf[2], acce[2], wbar;
     __shared__ uint32_t tmem_base_s;
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t w_s = smem_u32(smem), ring_s = w_s + 2 * 4 * C1_W;
+    const uint32_t w_s = smem_u32(smem), ring_s = w_s + 4 * C1_WC;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < C1_STAGES; ++s) {
@@ -1300,6 +1309,39 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_co
     const uint32_t tmem = tmem_base_s;
     const int total = (g.n * 441 + 127) / 128;
     const int nbox = g.coff[g.groups - 1] > 0 ? 2 : 1;
+    const bool comb = g.groups == 2;  // online + target in one N = 64 MMA (target = online + 1 frame)
+    // combined B tile of tap t at w_s + t * C1_WC: K block 0 (frames 0..3) rows 0..31 =
+    // online K 0..63, rows 32..63 = zeros (frame 0) then target K 0..47; K block 1 (frame
+    // 4): rows 0..31 = zeros, rows 32..63 = target K 48..63.  16-byte chunks c8 of a
+    // 128-byte row, SW128 K-major (kmaj_off).
+    auto build_w = [&] {
+        constexpr int PER = 4 * 2 * 64 * 8 / GEMM_THREADS;  // 16 chunks per thread, loads first
+        uint4 v[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int i = tid + u * GEMM_THREADS;
+            const int c8 = i & 7, row = (i >> 3) & 63, blk = (i >> 9) & 1, t = i >> 10;
+            const int net = row >> 5, o = row & 31;
+            int k = -1;  // K index (within the tap's 64) of the source network, -1: zero
+            if (net == 0) {
+                if (blk == 0) k = c8 * 8;
+            } else if (blk == 0) {
+                if (c8 >= 2) k = (c8 - 2) * 8;
+            } else if (c8 < 2) {
+                k = 48 + c8 * 8;
+            }
+            v[u] = k >= 0 ? __ldg(reinterpret_cast<const uint4 *>(g.w1p[net] + o * 256 + t * 64 + k))
+                          : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int i = tid + u * GEMM_THREADS;
+            const int c8 = i & 7, row = (i >> 3) & 63, blk = (i >> 9) & 1, t = i >> 10;
+            *reinterpret_cast<uint4 *>(smem + t * C1_WC + blk * 8192 + kmaj_off(row, c8)) = v[u];
+        }
+        fence_proxy_async_smem();
+    };
+    if (comb && g.w_early) build_w();
     auto load_w = [&] {
         mbar_expect_tx(&wbar, (uint32_t)(g.groups * 4 * C1_W));
         for (int q = 0; q < g.groups; ++q)
@@ -1313,16 +1355,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_co
     };
     int pre = 0;
     if (tid == 0) {
-        if (g.w_early) load_w();
+        if (g.w_early && !comb) load_w();
         if (g.a_early)
             for (int t = blockIdx.x; t < total && pre < C1_STAGES; t += gridDim.x, ++pre) load_a(pre, t);
     }
     griddep_wait();
     griddep_launch();
     tp.waited();
+    if (comb) {
+        if (!g.w_early) build_w();
+        __syncthreads();
+    }
     if (warp == 0) {
         if (lane == 0) {  // producer
-            if (!g.w_early) load_w();
+            if (!g.w_early && !comb) load_w();
             uint32_t q = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
                 if ((int)q < pre) continue;
@@ -1332,7 +1378,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_co
         }
     } else if (warp == 1) {
         if (lane == 0) {  // MMA issuer
-            mbar_wait(&wbar, 0);
+            if (!comb) mbar_wait(&wbar, 0);
             uint32_t q = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
                 const uint32_t buf = q & 1, s = q % C1_STAGES;
@@ -1340,7 +1386,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_shift(const __grid_co
                 mbar_wait(&full[s], (q / C1_STAGES) & 1);
                 tc_fence_after();
                 const uint32_t a0 = ring_s + s * 2 * C1_BOX;
-                for (int gg = 0; gg < g.groups; ++gg) {
+                if (comb) {
+                    constexpr uint32_t IDESC64 = idesc_bf16(64, false, false);
+#pragma unroll
+                    for (int tap = 0; tap < 4; ++tap) {
+                        const uint32_t shift = (uint32_t)((tap >> 1) * 21 + (tap & 1)) * 128;
+#pragma unroll
+                        for (int f = 0; f < 5; ++f) {
+                            const uint64_t ad = desc_sw128(a0 + (f >> 2) * C1_BOX + shift + (f & 3) * 32, 0);
+                            const uint64_t bd = desc_sw128(w_s + tap * C1_WC + (f >> 2) * 8192 + (f & 3) * 32, 0);
+                            umma_bf16(tmem + buf * 64, ad, bd, IDESC64, (tap > 0 || f > 0) ? 1u : 0u);
+                        }
+                    }
+                }
+                for (int gg = 0; gg < g.groups && !comb; ++gg) {
                     const uint32_t acc = tmem + buf * 64 + gg * 32;
 #pragma unroll
                     for (int tap = 0; tap < 4; ++tap) {
@@ -1416,8 +1475,9 @@ int tma_conv1_shift(const pq_net *nets, const bf16 *s2d, int nframes, const int 
         // gradient read the copy, conv2's data gradient takes its ReLU mask from it)
         g.ep[q] = EpiBiasRelu{act1s2 ? nullptr : act1[q], nets[q].master + P_B1, n * 400, 32, 32, 1.0f / 255.0f};
         g.coff[q] = c0[q];
+        g.w1p[q] = (const bf16 *)nets[q].shadow + S_W1P;
     }
-    if (groups > 1 && (c0[1] + 64 > nframes * 16 || c0[0] != 0)) return set_err("conv1 shift: channel window");
+    if (groups > 1 && (c0[1] != 16 || nframes != 5 || c0[0] != 0)) return set_err("conv1 shift: channel window");
     g.n = n, g.groups = groups, g.a_early = a_early, g.w_early = w_early;
     static bool configured = false;
     if (!configured) {
