@@ -1681,7 +1681,7 @@ int tma_conv3_shift(const pq_net *nets, bf16 *const *act2, bf16 *const *act3, in
 // ones column (bias row).  One CTA per split runs all five M tiles (320 TMEM columns).
 constexpr int W2S_ROWS = 80, W2S_ABOX = W2S_ROWS * 128, W2S_BBOX = 64 * 128, W2S_STAGES = 5;
 constexpr int W2S_SLOT = 2 * W2S_ABOX + W2S_BBOX;  // 28 KB, 1024-aligned
-constexpr int W2S_SMEM = 1024 + 2 * 8192 + W2S_STAGES * W2S_SLOT;
+constexpr int W2S_SMEM = 1024 + W2S_STAGES * W2S_SLOT;
 struct W2SArgs {
     CUtensorMap a, b;  // act1s2 pixel rows [n*100][128]; dY2q [n*100][64]
     EpiF32T ep;        // part2[split][64][513]
@@ -1693,30 +1693,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_wgrad_shift(const __g
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t full[W2S_STAGES], empty[W2S_STAGES], accf;
     __shared__ uint32_t tmem_base_s;
+    __shared__ float bsum[4][64];
     TlProbe tp;
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t ones_s = smem_u32(smem), ring_s = ones_s + 2 * 8192;
+    const uint32_t ring_s = smem_u32(smem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int i = tid; i < 2 * 8192 / 16; i += blockDim.x) {  // ones operand: M index 0 = 1
-        const int atom = i >> 9, k = (i >> 3) & 63, c8 = i & 7;
-        uint4 val = make_uint4(0, 0, 0, 0);
-        if (atom == 0 && c8 == 0) val.x = 0x3F80u;
-        *reinterpret_cast<uint4 *>(smem + atom * 8192 + mnmaj_off(k, c8) % 8192) = val;
-    }
     if (tid == 0) {
         for (int s = 0; s < W2S_STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], 5);  // the MMAs' commit + the 4 bias-summing warps
         }
         mbar_init(&accf, 1);
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc<512>(&tmem_base_s);
+    if (warp == 0) tmem_alloc<256>(&tmem_base_s);
     if (tid == 32) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&g.a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&g.b) : "memory");
     }
-    fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1738,7 +1732,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_wgrad_shift(const __g
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // MMA issuer: five 128 x 64 accumulators
+        if (lane == 0) {  // MMA issuer: four 128 x 64 accumulators (the taps)
             uint32_t q = 0;
             for (int kb = kb0; kb < kb1; ++kb, ++q) {
                 const uint32_t s = q % W2S_STAGES;
@@ -1754,27 +1748,46 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_wgrad_shift(const __g
                         const uint32_t shift = (uint32_t)((tap >> 1) * 10 + (tap & 1)) * 128;
                         umma_bf16(tmem + tap * 64, desc_sw128(a0 + shift + j * 2048, W2S_ABOX), bd, IDESC, acc_on);
                     }
-                    umma_bf16(tmem + 256, desc_sw128(ones_s + j * 2048, 8192), bd, IDESC, acc_on);
                 }
                 umma_commit(&empty[s]);
             }
             umma_commit(&accf);
         }
-    } else if (warp >= 4) {  // epilogue: M row i of tap tile -> k
+    } else if (warp >= 4) {
+        // the bias row (sum of dY2 over the split's rows) from the B tiles in shared memory
+        // while the MMAs run: warp wq sums K rows 16 wq .. 16 wq + 15 of every chunk, lane
+        // = output channels lane and lane + 32 (MN-major SW128 rows of 64 channels)
         const int wq = warp - 4;
+        float bias[2] = {0.f, 0.f};
+        uint32_t q = 0;
+        for (int kb = kb0; kb < kb1; ++kb, ++q) {
+            const uint32_t s = q % W2S_STAGES;
+            mbar_wait(&full[s], (q / W2S_STAGES) & 1);
+            const uint8_t *bt = smem + s * W2S_SLOT + 2 * W2S_ABOX;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int r = wq * 16 + i;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int c = lane + 32 * h;
+                    bias[h] += __bfloat162float(
+                        *reinterpret_cast<const bf16 *>(bt + r * 128 + (((c >> 3) ^ (r & 7)) << 4) + (c & 7) * 2));
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        bsum[wq][lane] = bias[0];
+        bsum[wq][lane + 32] = bias[1];
         mbar_wait(&accf, 0);
         __syncwarp();
         tc_fence_after();
+        // M row i of tap tile -> k
 #pragma unroll 1
-        for (int mt = 0; mt < 5; ++mt) {
+        for (int mt = 0; mt < 4; ++mt) {
             const int i = wq * 32 + lane;
-            int k;
-            if (mt < 4) {
-                const int ty = mt >> 1, tx = mt & 1, dy = i >> 6;
-                k = ((2 * ty + dy) * 4 + 2 * tx) * 32 + (i & 63);
-            } else {
-                k = i == 0 ? 512 : -1;
-            }
+            const int ty = mt >> 1, tx = mt & 1, dy = i >> 6;
+            const int k = ((2 * ty + dy) * 4 + 2 * tx) * 32 + (i & 63);
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
                 float v[32];
@@ -1784,13 +1797,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_wgrad_shift(const __g
 #pragma unroll
                     for (int e = 0; e < 32; ++e) v[e] = 0.f;
                 }
-                if (k >= 0) g.ep.apply(k, h * 32, v, 32, split);
+                g.ep.apply(k, h * 32, v, 32, split);
             }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc<512>(tmem);
+    if (warp == 4) {  // bias row 512: the four warps' sums in row order
+        float v[32];
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            for (int e = 0; e < 32; ++e)
+                v[e] = ((bsum[0][h * 32 + e] + bsum[1][h * 32 + e]) + bsum[2][h * 32 + e]) + bsum[3][h * 32 + e];
+            if (lane == 0) g.ep.apply(512, h * 32, v, 32, split);
+        }
+    }
+    if (warp == 0) tmem_dealloc<256>(tmem);
     tp.done('V');
 }
 
