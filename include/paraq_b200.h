@@ -149,9 +149,10 @@ size_t pq_prepopulate_scratch_bytes(int64_t n);
 
 /* ---- Q network (nn.py / agent.py) -------------------------------------------------- */
 size_t pq_workspace_bytes(int max_batch, int actions);
-/* fc1 split-K partial slots the forward leaves in the workspace at batch n (7, or 1
- * when the large-batch kernel reduces the splits in TMEM; the head reads that many). */
-int pq_fc1_splits(int n);
+/* fc1 split-K partial slots the forward of `groups` networks (2: the learner's online +
+ * target, 1: acting) leaves in the workspace at batch n (7, or 1 when the large-batch
+ * kernel reduces the splits in TMEM; the head / acting kernels read that many). */
+int pq_fc1_splits(int n, int groups);
 /* Byte offsets of the workspace buffers (stage-wise kernel tests), in order:
  * act1, act2, act3, fc1part (online), act1, act2, act3, fc1part (target), q, h1, dh1,
  * td, dh1_bf16, dh1T_bf16, actions, dY3, dY2, dY1, part1, part2, part3, grad4, then dY1

@@ -88,7 +88,7 @@ EXPORTS = {
     "pq_prepopulate_frames": ([C.c_uint64, vp, C.c_int64, C.c_int64, vp, vp, vp], C.c_int),
     "pq_prepopulate_scratch_bytes": ([C.c_int64], C.c_size_t),
     "pq_workspace_bytes": ([C.c_int, C.c_int], C.c_size_t),
-    "pq_fc1_splits": ([C.c_int], C.c_int),
+    "pq_fc1_splits": ([C.c_int, C.c_int], C.c_int),
     "pq_workspace_layout": ([C.c_int, C.c_int, C.POINTER(C.c_int64)], C.c_int),
     "pq_forward": ([PqNet, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, vp],
                    C.c_int),

@@ -93,18 +93,20 @@ static bool use_tma(int n) {
     return mode >= 0 ? mode == 1 : n >= 128;
 }
 
-// fc1 forward with the split sums reduced in TMEM (learner.cu k_fc1_acc7) from this batch
-// up (PQ_F7=0: the resident-A split-K kernel); the head / acting kernels then read 1 split
-constexpr int F7_MIN_BATCH = 512;
-static bool fc1_acc7(int n) {
+// fc1 forward with the split sums reduced in TMEM (learner.cu k_fc1_acc7: one CTA per
+// (network, 128-unit tile, 64 samples)) once that is at least 128 CTAs -- the learner's two
+// networks from batch 512, the acting forward (one network) from 1024; below, the
+// resident-A split-K kernel has the parallelism (PQ_F7=0: always it).  The head / acting
+// kernels then read 1 split.
+static bool fc1_acc7(int n, int groups) {
     static int on = -1;
     if (on < 0) {
         const char *e = getenv("PQ_F7");
         on = (e && e[0] == '0') ? 0 : 1;
     }
-    return on == 1 && n >= F7_MIN_BATCH && use_tma(n) && conv1_shift();
+    return on == 1 && groups * 4 * ((n + 63) / 64) >= 128 && use_tma(n) && conv1_shift();
 }
-int fc1_splits(int n) { return fc1_acc7(n) ? 1 : FC1_SPLITS; }
+int fc1_splits(int n, int groups) { return fc1_acc7(n, groups) ? 1 : FC1_SPLITS; }
 
 // ------------------------------------------------------------------ workspace
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -272,7 +274,7 @@ static int forward_gemms(const pq_net *nets, const FwdInput *ins, int groups, in
         g.M = n * 49, g.N = 64, g.K = 576, g.kc_per_split = 9, g.splits = 1, g.ones_at = -1;
         PQ_CHECK((launch_gemm<64, false, false, 0, 2>(g, groups, st)), "conv3 forward");
     }
-    if (fc1_acc7(n)) return tma_fc1_fwd_acc7(nets, a3, pt, groups, n, st);
+    if (fc1_acc7(n, groups)) return tma_fc1_fwd_acc7(nets, a3, pt, groups, n, st);
     if (use_tma(n) && conv1_shift())  // W4 chunks resident per CTA
         return tma_fc1_fwd_resident(nets, a3, pt, FC1_SPLITS, groups, n, st);
     if (use_tma(n)) return tma_fc1_fwd(nets, a3, pt, FC1_SPLITS, groups, n, st);
@@ -343,7 +345,7 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
         h.part[g] = w.fc1part[g];
         h.master[g] = nets[g].master;
     }
-    h.groups = groups, h.n = n, h.A = A, h.n8 = w.n8, h.splits = fc1_splits(n);
+    h.groups = groups, h.n = n, h.A = A, h.n8 = w.n8, h.splits = fc1_splits(n, groups);
     h.block = h.splits == 1 ? HEAD_BLOCK : 1;
     h.learner = learner;
     h.q_out = w.q, h.h1 = w.h1, h.dh1 = w.dh1, h.td = w.td, h.dh1_bf = w.dh1_bf, h.dh1T = w.dh1T;
@@ -994,7 +996,7 @@ int act_forward(pq_net net, const uint8_t *ring, const int32_t *stack, int W, in
     int rc = forward_gemms(&net, &in, 1, W, w, st);
     *part_out = w.fc1part[0];
     *done_out = w.done + 1;
-    *splits_out = fc1_splits(W);
+    *splits_out = fc1_splits(W, 1);
     return rc;
 }
 
@@ -1028,7 +1030,7 @@ extern "C" {
 
 int pq_abi_version(void) { return PQ_ABI_VERSION; }
 
-int pq_fc1_splits(int n) { return fc1_splits(n); }
+int pq_fc1_splits(int n, int groups) { return fc1_splits(n, groups); }
 
 int pq_cta_trace(int on, unsigned long long *out, int *count) {
     if (out) {

@@ -124,7 +124,7 @@ def test_learner_step_stagewise(B):
         ref3 = F.relu(F.conv2d(act2.permute(0, 3, 1, 2), Sp["W3"].view(64, 3, 3, 64).permute(0, 3, 1, 2),
                                Pp["b3"], stride=1)).permute(0, 2, 3, 1)
         assert rel(act3, ref3) < 2e-3, "conv3 forward"
-        ns = N.load().pq_fc1_splits(B)  # 1 when the forward reduced the splits in TMEM
+        ns = N.load().pq_fc1_splits(B, 2)  # 1 when the forward reduced the splits in TMEM
         part = view(ws, L["fc1part" + suffix], (7, B, 512), torch.float32)[:ns].sum(0)
         ref4 = act3.reshape(B, 3136) @ Sp["W4"].T
         assert rel(part, ref4) < 1e-4, "fc1 forward"
