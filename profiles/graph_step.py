@@ -36,6 +36,7 @@ def learn_only(e):
     r.flush_and_merge()
     r.begin_epoch(e)
     gl, nl = r._graphs["learn"]
+    r.learn_stream.wait_stream(torch.cuda.current_stream())  # the epoch's index table / prologue
     with torch.cuda.stream(r.learn_stream):
         for _ in range(r.updates // nl):
             gl.replay()
