@@ -791,6 +791,10 @@ int tma_fc1_fwd_acc7(const pq_net *nets, bf16 *const *act3, float *const *part, 
 // discarded) reads row r + 11 (2 - kh) + (2 - kw) for tap (kh, kw); one TMA box of 152 rows
 // feeds the 9 taps against 9 resident MN-major W3 tiles, in the tap order of the im2col
 // kernel, so dY2 (and its padded copies) are bit-identical.
+// the shifted data-gradient kernels run 12 warps: producer, MMA issuer, 2 idle and 8
+// epilogue warps, two per TMEM lane quadrant splitting the columns (the epilogue -- mask,
+// up to three stores per row -- was the slower side of the TMEM double buffer)
+constexpr int DG_THREADS = 384;
 constexpr int C3D_ROWS = 152, C3D_BOX = C3D_ROWS * 128, C3D_STAGES = 3, C3D_W = 64 * 128;
 constexpr int C3D_SMEM = 1024 + 9 * C3D_W + C3D_STAGES * C3D_BOX;
 struct C3DArgs {
@@ -799,7 +803,7 @@ struct C3DArgs {
     int n;
 };
 
-__global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv3_dgrad_shift(const __grid_constant__ C3DArgs g) {
+__global__ void __launch_bounds__(DG_THREADS, 1) k_conv3_dgrad_shift(const __grid_constant__ C3DArgs g) {
     constexpr uint32_t IDESC = idesc_bf16(64, false, true);
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t full[C3D_STAGES], empty[C3D_STAGES], accf[2], acce[2], wbar;
@@ -815,7 +819,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv3_dgrad_shift(const __g
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&accf[b], 1);
-            mbar_init(&acce[b], 4);
+            mbar_init(&acce[b], 8);
         }
         mbar_init(&wbar, 1);
         fence_mbar_init();
@@ -871,8 +875,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv3_dgrad_shift(const __g
                 umma_commit(&accf[buf]);
             }
         }
-    } else if (warp >= 4) {  // epilogue
-        const int wq = warp - 4;
+    } else if (warp >= 4) {  // epilogue: warp 4 + 4h + quadrant takes columns 32h .. 32h + 31
+        const int wq = (warp - 4) & 3, hc = (warp - 4) >> 2;
         const EpiMaskPad &ep = g.ep;
         uint32_t q = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
@@ -881,23 +885,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv3_dgrad_shift(const __g
             const int r = t * 128 + wq * 32 + lane, smp = r / 121, p = r - smp * 121, y = p / 11, x = p - y * 11;
             const bool live = smp < g.n && y < 9 && x < 9;
             const int m = smp * 81 + y * 9 + x;
-            MaskRow64 row;
-            if (live) row.load(ep.e.mask + (size_t)m * 64);
+            MaskRow32 row;
+            if (live) row.load(ep.e.mask + (size_t)m * 64 + hc * 32);
             mbar_wait(&accf[buf], (q >> 1) & 1);
             __syncwarp();
             tc_fence_after();
-            float v[2][32];
-            const uint32_t trow = tmem + buf * 64 + ((uint32_t)(wq * 32) << 16);
-            tmem_ld32(trow, v[0]);
-            tmem_ld32(trow + 32, v[1]);
+            float v[32];
+            tmem_ld32(tmem + buf * 64 + hc * 32 + ((uint32_t)(wq * 32) << 16), v);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acce[buf]);
             if (live) {  // dY2, its copy on the padded 11 x 11 grid and on the 10 x 10 grid
-                row.apply(&v[0][0]);
-                row.store(ep.e.out + (size_t)m * 64);
-                row.store(ep.out_pad + ((size_t)(smp * 11 + y + 1) * 11 + x + 1) * 64);
-                if (ep.out10) row.store(ep.out10 + ((size_t)(smp * 10 + y) * 10 + x) * 64);
+                row.apply_store(ep.e.out + (size_t)m * 64 + hc * 32, v);
+                row.apply_store(ep.out_pad + ((size_t)(smp * 11 + y + 1) * 11 + x + 1) * 64 + hc * 32, v);
+                if (ep.out10) row.apply_store(ep.out10 + ((size_t)(smp * 10 + y) * 10 + x) * 64 + hc * 32, v);
             }
         }
     }
@@ -928,7 +929,7 @@ int tma_conv3_dgrad_shift(const pq_net &th, const bf16 *dY3p, const bf16 *act2, 
         PQ_CUDA_TRY(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
     }
     const int total = (n * 121 + 127) / 128;
-    return cuda_err(launch_k(k_conv3_dgrad_shift, dim3(std::min(total, g_sms)), dim3(GEMM_THREADS), C3D_SMEM, st, g),
+    return cuda_err(launch_k(k_conv3_dgrad_shift, dim3(std::min(total, g_sms)), dim3(DG_THREADS), C3D_SMEM, st, g),
                     "conv3 dgrad (shifted descriptors)");
 }
 
@@ -1018,7 +1019,7 @@ struct C2DArgs {
     int n, pad21, mask_s2;
 };
 
-__global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_dgrad_shift(const __grid_constant__ C2DArgs g) {
+__global__ void __launch_bounds__(DG_THREADS, 1) k_conv2_dgrad_shift(const __grid_constant__ C2DArgs g) {
     TlProbe tp;
     constexpr uint32_t IDESC = idesc_bf16(64, false, true);
     extern __shared__ uint8_t smem_raw[];
@@ -1034,7 +1035,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_dgrad_shift(const __g
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&accf[b], 1);
-            mbar_init(&acce[b], 4);
+            mbar_init(&acce[b], 8);
         }
         mbar_init(&wbar, 1);
         fence_mbar_init();
@@ -1098,34 +1099,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv2_dgrad_shift(const __g
                 umma_commit(&accf[buf]);
             }
         }
-    } else if (warp >= 4) {  // epilogue
-        const int wq = warp - 4;
+    } else if (warp >= 4) {  // epilogue: warp 4 + 4h + quadrant takes classes 2h, 2h + 1
+        const int wq = (warp - 4) & 3, hc = (warp - 4) >> 2;
         uint32_t q = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++q) {
             const uint32_t buf = q & 1;
             const int r = t * 128 + wq * 32 + lane, smp = r / 121, p = r - smp * 121, y = p / 11, x = p - y * 11;
             const bool ok = smp < g.n && y < 10 && x < 10;
-            // the four classes' ReLU masks in flight while the MMAs run (act1 pixel
+            // the two classes' ReLU masks in flight while the MMAs run (act1 pixel
             // (2y + py, 2x + px) = s2d pixel (y, x), channels (py * 2 + px) * 32)
-            MaskRow32 mk[4];
+            MaskRow32 mk[2];
             if (ok)
 #pragma unroll
-                for (int cls = 0; cls < 4; ++cls) {
-                    const int iy = 2 * y + (cls >> 1), ix = 2 * x + (cls & 1);
-                    mk[cls].load(g.mask + (g.mask_s2 ? ((size_t)(smp * 10 + y) * 10 + x) * 128 + cls * 32
-                                                     : ((size_t)(smp * 20 + iy) * 20 + ix) * 32));
+                for (int c2 = 0; c2 < 2; ++c2) {
+                    const int cls = 2 * hc + c2, iy = 2 * y + (cls >> 1), ix = 2 * x + (cls & 1);
+                    mk[c2].load(g.mask + (g.mask_s2 ? ((size_t)(smp * 10 + y) * 10 + x) * 128 + cls * 32
+                                                    : ((size_t)(smp * 20 + iy) * 20 + ix) * 32));
                 }
             mbar_wait(&accf[buf], (q >> 1) & 1);
             __syncwarp();
             tc_fence_after();
 #pragma unroll
-            for (int cls = 0; cls < 4; ++cls) {
+            for (int c2 = 0; c2 < 2; ++c2) {
+                const int cls = 2 * hc + c2;
                 float v[32];
                 tmem_ld32(tmem + buf * 256 + cls * 64 + ((uint32_t)(wq * 32) << 16), v);
                 if (ok) {
                     const int iy = 2 * y + (cls >> 1), ix = 2 * x + (cls & 1);
                     const int gw = g.pad21 ? 21 : 20;
-                    mk[cls].apply_store(g.out + ((size_t)(smp * gw + iy) * gw + ix) * 32, v);
+                    mk[c2].apply_store(g.out + ((size_t)(smp * gw + iy) * gw + ix) * 32, v);
                 }
             }
             tc_fence_before();
@@ -1159,7 +1161,7 @@ int tma_conv2_dgrad_shift(const pq_net &th, const bf16 *dY2p, const bf16 *act1, 
         PQ_CUDA_TRY(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
     }
     const int total = (n * 121 + 127) / 128;
-    return cuda_err(launch_k(k_conv2_dgrad_shift, dim3(std::min(total, g_sms)), dim3(GEMM_THREADS), C2D_SMEM, st, g),
+    return cuda_err(launch_k(k_conv2_dgrad_shift, dim3(std::min(total, g_sms)), dim3(DG_THREADS), C2D_SMEM, st, g),
                     "conv2 dgrad (shifted descriptors)");
 }
 
