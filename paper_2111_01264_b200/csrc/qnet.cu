@@ -323,15 +323,23 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a, int32_t
         tp.waited();
         ct_mark(1);
     };
-    if (a.block == HEAD_BLOCK)  // large batches: fc1 sums reduced by the forward GEMM (k_fc1_acc7)
-        head_block<1, HEAD_BLOCK>(a, blockIdx.x * HEAD_BLOCK, wait);
-    else if (a.splits == 1)
-        head_sample<1>(a, blockIdx.x, wait);
-    else
-        head_sample<FC1_SPLITS>(a, blockIdx.x, wait);
+    head_sample<FC1_SPLITS>(a, blockIdx.x, wait);  // (1 split: k_head_block)
     if (bump) last_block_bump(bump, done);
     tp.done('H');
     ct_end('H');
+}
+
+// large batches (fc1 sums reduced by the forward GEMM, k_fc1_acc7): HEAD_BLOCK samples per
+// CTA (learn_parts.cuh: head_block); a kernel of its own so the batch-32 head stays lean
+__global__ void __launch_bounds__(HEAD_THREADS) k_head_block(const HeadArgs a, int32_t *bump, uint32_t *done) {
+    TlProbe tp;
+    head_block<1, HEAD_BLOCK>(a, blockIdx.x * HEAD_BLOCK, [&] {
+        griddep_wait();
+        griddep_launch();
+        tp.waited();
+    });
+    if (bump) last_block_bump(bump, done);
+    tp.done('H');
 }
 
 static bool fused_backward(int n, const pq_learn_args *la, float *grad_only);
@@ -358,8 +366,11 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
         h.idx_cur = w.idx_cur, h.upd_cur = w.upd_cur;
     }
     int32_t *bump = (la && learner && !la->idx && la->update_counter && bump_here) ? la->update_counter : nullptr;
-    return cuda_err(launch_k(k_head, dim3((n + h.block - 1) / h.block), dim3(HEAD_THREADS), 0, st, h, bump, w.done + 2),
-                    "head");
+    if (h.block == HEAD_BLOCK)
+        return cuda_err(launch_k(k_head_block, dim3((n + HEAD_BLOCK - 1) / HEAD_BLOCK), dim3(HEAD_THREADS), 0, st, h,
+                                 bump, w.done + 2),
+                        "head");
+    return cuda_err(launch_k(k_head, dim3(n), dim3(HEAD_THREADS), 0, st, h, bump, w.done + 2), "head");
 }
 
 // fc2 / fc1-bias gradient partials of one 64-sample chunk (blockIdx.x), 512 threads =
