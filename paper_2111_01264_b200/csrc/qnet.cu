@@ -899,7 +899,7 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
         PQ_CHECK((launch_gemm<64, false, true, 4>(g, 1, side)), "fc1 wgrad");
         if (fc1_done) PQ_CHECK(cudaEventRecord(fc1_done, side), "fc1 gradient event");
     } else {  // (the cp.async engine: its staged RMSProp epilogue walks the tile with all 8 warps)
-        PQ_CHECK((launch_gemm<64, false, true, 4>(args_b4w_rms<EpiRms>(la, n, w), 1, side)), "fc1 wgrad+rmsprop");
+        PQ_CHECK((launch_gemm<128, false, true, 4>(args_b4w_rms<EpiRms>(la, n, w), 1, side)), "fc1 wgrad+rmsprop");
     }
     {
         B3wOp::Args g = args_b3w(w, n, &s3);
