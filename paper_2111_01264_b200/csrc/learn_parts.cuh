@@ -53,7 +53,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 constexpr int HEAD_THREADS = 256;
-constexpr int HEAD_BLOCK = 8;  // samples per head CTA at large batches
+constexpr int HEAD_BLOCK = 4;  // samples per head CTA at large batches
 
 // One sample b (one 256-thread CTA).  S = fc1 split count; every global load of a
 // phase is independent so they are all in flight together.  Everything that does not
@@ -348,6 +348,8 @@ PQ_DEV void head_block(const HeadArgs &a, int b0, Wait wait = Wait{}) {
         bf16 *dT = a.dh1T + (size_t)j * a.n8 + b0;
         if (NB == 8 && nb == 8 && ((reinterpret_cast<uintptr_t>(dT) & 15) == 0)) {
             *reinterpret_cast<uint4 *>(dT) = *reinterpret_cast<const uint4 *>(gbs);
+        } else if (NB == 4 && nb == 4 && ((reinterpret_cast<uintptr_t>(dT) & 7) == 0)) {
+            *reinterpret_cast<uint2 *>(dT) = *reinterpret_cast<const uint2 *>(gbs);
         } else {
             for (int sb = 0; sb < nb; ++sb) dT[sb] = gbs[sb];
         }
