@@ -516,6 +516,9 @@ static int choose_kc(int nchunks, int mtiles, int *splits, int kc_max = 1 << 30)
     if (kc < 2) kc = 2;
     int need = (nchunks + MAX_SPLITS - 1) / MAX_SPLITS;
     if (kc < need) kc = need;
+    // no partial second wave: splits x M tiles jobs within one CTA per SM (the ceiling
+    // division above can overshoot by a few jobs, e.g. 150 on 148 SMs at batch 1024)
+    while (kc < kc_max && ((nchunks + kc - 1) / kc) * mtiles > 148 && ((nchunks + kc - 1) / kc) * mtiles < 2 * 148) ++kc;
     if (kc > kc_max) kc = kc_max;
     *splits = (nchunks + kc - 1) / kc;
     return kc;
