@@ -130,10 +130,12 @@ class DataParallelLearner:
         return g[p_w4:p_b4], (g[:p_w4], g[p_b4:])
 
     def _overlap(self) -> bool:
+        """Bucketed all-reduce overlapped with the backward: NCCL by default; PQ_DP_OVERLAP=0
+        turns it off, =force also takes it over gloo (the two-process test on one GPU)."""
         import torch.distributed as dist
 
-        return (os.environ.get("PQ_DP_OVERLAP", "1") != "0"
-                and dist.get_backend(self.group) == "nccl")
+        mode = os.environ.get("PQ_DP_OVERLAP", "1")
+        return mode == "force" or (mode != "0" and dist.get_backend(self.group) == "nccl")
 
     def step(self, idx):
         """One data-parallel update on the global batch idx (device int64 [B]).  Over NCCL

@@ -1,5 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 400 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_parity.py tests/test_gpu_dp.py -x -q 2>&1 | tail -1
-BATCHES="256 512 1024" timeout 500 bash scripts/ab_kern.sh 2>&1 | head -2
-timeout 200 python profiles/timeline_eager.py 1024 | tail -9
-for rep in 1 2; do timeout 200 python profiles/graph_step.py 32 2>&1 | tail -1; done
+timeout 600 python -m pytest tests/test_gpu_dp_multiprocess.py -x -q 2>&1 | tail -3

@@ -34,10 +34,11 @@ def _setup():
     return mem, theta, target, opt, idx
 
 
-def _rank(rank, world, port, q):
+def _rank(rank, world, port, q, overlap="1"):
     import torch.distributed as dist
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      PQ_DP_OVERLAP=overlap)
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2111_01264_b200.dist import DataParallelLearner
@@ -53,21 +54,30 @@ def _rank(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_two_process_dp_learner_matches_single_process():
+def _two_ranks(overlap, port):
     import torch.multiprocessing as mp
-
-    from paper_2111_01264_b200.dist import DataParallelLearner
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 31500 + (os.getpid() % 2000)
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, q, overlap)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted((q.get(timeout=300) for _ in procs), key=lambda t: t[0])
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
+    return res
+
+
+def test_two_process_dp_learner_matches_single_process():
+    from paper_2111_01264_b200.dist import DataParallelLearner
+
+    port = 31500 + (os.getpid() % 2000)
+    res = _two_ranks("0", port)
+    # the bucketed all-reduce overlapped with the conv backward (the NCCL default; forced
+    # here over gloo): the same sums, so bit-identical parameters
+    res_ov = _two_ranks("force", port + 1)
+    assert all(np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) for a, b in zip(res, res_ov))
     (_, th0, v0), (_, th1, v1) = res
     assert np.array_equal(th0, th1) and np.array_equal(v0, v1)   # identical replicas
     mem, theta, target, opt, idx = _setup()
