@@ -1187,16 +1187,33 @@ __global__ void __launch_bounds__(256) k_frames_s2d(const uint8_t *ring, const i
         slot[threadIdx.x] = refs[rec * ref_stride + ref_off + threadIdx.x];
     }
     __syncthreads();
+    // the sample's frames into shared memory with coalesced 16-byte loads, all in flight
+    // (masked slot: zeros), then the 4 x 4 blocks out of shared memory
+    __shared__ __align__(16) uint8_t fr[5 * FRAME_BYTES];
+    {
+        constexpr int CH = FRAME_BYTES / 16, PER = (5 * CH + 255) / 256;
+        uint4 v[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int e = threadIdx.x + u * 256, f = e / CH, c = e - f * CH;
+            const int sl = f < nframes ? slot[f] : -1;
+            v[u] = sl >= 0 ? __ldg(reinterpret_cast<const uint4 *>(ring + (size_t)sl * FRAME_BYTES) + c)
+                           : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int e = threadIdx.x + u * 256;
+            if (e < nframes * CH) reinterpret_cast<uint4 *>(fr)[e] = v[u];
+        }
+    }
+    __syncthreads();
     bf16 *o = out + (size_t)b * 441 * nframes * 16;
     for (int e = threadIdx.x; e < 441 * nframes; e += blockDim.x) {
         const int pix = e / nframes, f = e - pix * nframes, by = pix / 21, bx = pix - by * 21;
-        const int sl = slot[f];
-        uint32_t w[4] = {0, 0, 0, 0};
-        if (sl >= 0) {
-            const uint8_t *src = ring + (size_t)sl * FRAME_BYTES + (4 * by) * 84 + 4 * bx;
+        const uint8_t *src = fr + f * FRAME_BYTES + (4 * by) * 84 + 4 * bx;
+        uint32_t w[4];
 #pragma unroll
-            for (int dy = 0; dy < 4; ++dy) w[dy] = __ldg(reinterpret_cast<const uint32_t *>(src + dy * 84));
-        }
+        for (int dy = 0; dy < 4; ++dy) w[dy] = *reinterpret_cast<const uint32_t *>(src + dy * 84);
         uint4 *d = reinterpret_cast<uint4 *>(o + (size_t)(pix * nframes + f) * 16);
         d[0] = u8x8_to_bf16(w[0], w[1]);
         d[1] = u8x8_to_bf16(w[2], w[3]);
