@@ -385,15 +385,18 @@ __global__ void __launch_bounds__(512) k_fc2_partials(const float *h1, const flo
     tp.waited();
     __shared__ float s_d[FC_CHUNK];
     __shared__ int s_a[FC_CHUNK];
+    // per-action sums in shared memory, column j owned by thread j (conflict-free): one
+    // add per sample instead of a predicated add for every action
+    extern __shared__ float s_acc_raw[];  // [A][512] (dynamic: up to 64 KB)
+    float(*s_acc)[512] = reinterpret_cast<float(*)[512]>(s_acc_raw);
     const int b0 = blockIdx.x * FC_CHUNK, nb = min(FC_CHUNK, n - b0), j = threadIdx.x;
     if (j < nb) {
         s_d[j] = td[(b0 + j) * 3 + 1];
         s_a[j] = act[b0 + j];
     }
+    for (int aa = 0; aa < A; ++aa) s_acc[aa][j] = 0.f;
     __syncthreads();
-    float acc[MAX_ACTIONS], ab = 0.f, bb = 0.f;
-#pragma unroll
-    for (int aa = 0; aa < MAX_ACTIONS; ++aa) acc[aa] = 0.f;
+    float ab = 0.f, bb = 0.f;
     // 16 samples' loads in flight per round (a one-sample loop is load-latency bound);
     // the adds stay in sample order
     constexpr int U = 16;
@@ -409,18 +412,14 @@ __global__ void __launch_bounds__(512) k_fc2_partials(const float *h1, const flo
         for (int u = 0; u < U; ++u) {
             if (q + u >= nb) break;
             const int b = q + u;
-            const float x = s_d[b] * hv[u];
             const int ab_ = s_a[b];
-#pragma unroll
-            for (int aa = 0; aa < MAX_ACTIONS; ++aa) acc[aa] += (ab_ == aa) ? x : 0.f;
+            s_acc[ab_][j] += s_d[b] * hv[u];
             ab += dv[u];
             if (j < A && ab_ == j) bb += s_d[b];
         }
     }
     float *out = part + (size_t)blockIdx.x * (A + 2) * 512;
-#pragma unroll
-    for (int aa = 0; aa < MAX_ACTIONS; ++aa)
-        if (aa < A) out[aa * 512 + j] = acc[aa];
+    for (int aa = 0; aa < A; ++aa) out[aa * 512 + j] = s_acc[aa][j];
     out[A * 512 + j] = ab;
     if (j < A) out[(A + 1) * 512 + j] = bb;
     tp.done('P');
@@ -888,8 +887,18 @@ static int backward_and_update(const pq_learn_args *la, int n, const WS &w, cuda
     // large batches: the fc2 / fc1-bias batch sums as chunk partials on the wgrad branch
     // (the optimizer then reduces n/64 partials per parameter instead of n samples)
     const int fc_chunks = n >= FC_PART_MIN_BATCH ? (n + FC_CHUNK - 1) / FC_CHUNK : 0;
+    if (fc_chunks) {
+        static bool configured = false;
+        if (!configured) {
+            PQ_CHECK(cudaFuncSetAttribute(k_fc2_partials, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          MAX_ACTIONS * 512 * 4),
+                     "fc2 partials smem");
+            configured = true;
+        }
+    }
     if (fc_chunks)
-        PQ_CHECK(launch_k(k_fc2_partials, dim3(fc_chunks), dim3(512), 0, side2, (const float *)w.h1,
+        PQ_CHECK(launch_k(k_fc2_partials, dim3(fc_chunks), dim3(512), (size_t)la->actions * 512 * 4, side2,
+                          (const float *)w.h1,
                           (const float *)w.dh1, (const float *)w.td, (const int32_t *)w.act, n, la->actions,
                           w.fcpart),
                  "fc2 partials");
