@@ -661,6 +661,14 @@ struct EpiMaskT {
     bf16 *out;
     const bf16 *mask;
     int M, N, ld;
+    // optional: fc1's data gradient also onto the zero-padded 11 x 11 grid of the shifted
+    // conv3 data gradient, out_pad[((b * 11 + y + 2) * 11 + x + 2) * 64 + c] for feature
+    // m = (y * 7 + x) * 64 + c of sample b
+    bf16 *out_pad;
+    PQ_DEV void store_pad(int m, int b, bf16 val) const {
+        const int p = m >> 6, y = p / 7, x = p - y * 7;
+        out_pad[((size_t)(b * 11 + y + 2) * 11 + x + 2) * 64 + (m & 63)] = val;
+    }
     // prefetch (see EpiMask): the 32 samples' mask values of feature m
     struct Pre {
         bf16 mk[32];
@@ -676,7 +684,9 @@ struct EpiMaskT {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
             if (n0 + j >= N) break;
-            out[(size_t)(n0 + j) * ld + m] = __float2bfloat16_rn(__bfloat162float(p.mk[j]) > 0.f ? v[j] : 0.f);
+            const bf16 val = __float2bfloat16_rn(__bfloat162float(p.mk[j]) > 0.f ? v[j] : 0.f);
+            out[(size_t)(n0 + j) * ld + m] = val;
+            if (out_pad) store_pad(m, n0 + j, val);
         }
     }
     PQ_DEV void apply(int m, int n0, const float *v, int cnt, int) const {
@@ -688,7 +698,9 @@ struct EpiMaskT {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
             if (j >= cnt || n0 + j >= N) break;
-            out[(size_t)(n0 + j) * ld + m] = __float2bfloat16_rn(__bfloat162float(mk[j]) > 0.f ? v[j] : 0.f);
+            const bf16 val = __float2bfloat16_rn(__bfloat162float(mk[j]) > 0.f ? v[j] : 0.f);
+            out[(size_t)(n0 + j) * ld + m] = val;
+            if (out_pad) store_pad(m, n0 + j, val);
         }
     }
 };
@@ -1287,6 +1299,87 @@ struct GemmOp {
             GridDepHook{});
     }
 };
+// conv3 data gradient at small batches as a k_fused part, by row-shifted descriptors (the
+// cp.async twin of learner.cu k_conv3_dgrad_shift): dY3 on the zero-padded 11 x 11 grid
+// (dY3p, written by fc1's data gradient) -- GEMM row r = (s, y, x) of that grid reads row
+// r + 11 (2 - kh) + (2 - kw) for tap (kh, kw), so ONE block of 152 rows x 64 channels
+// (19 KB) feeds all 9 taps through UMMA descriptors (the SW128 swizzle is a function of
+// the shared-memory address) instead of nine 16 KB im2col gathers; W3 as 9 MN-major
+// tiles, requested before the dependency wait with each row's ReLU mask.  Same MMA order
+// (tap, 16-channel step) as the im2col kernel, so dY2 is bit-identical.
+struct Dg3Args {
+    const bf16 *dy3p;  // [n * 121][64]
+    const bf16 *w3;    // bf16 shadow of W3 [o][kh][kw][c]
+    const bf16 *act2;  // ReLU mask [n * 81][64]
+    bf16 *dy2;         // [n * 81][64]
+    int n;
+};
+struct Dg3ShiftOp {
+    static constexpr bool GEMM = true, TABLE = false;
+    static constexpr int ROWS = 152, A_BYTES = 20 * 1024, W_TILE = 8192;
+    static constexpr int SMEM = 1024 + 9 * W_TILE + A_BYTES, STAGES = 1;
+    static constexpr uint32_t TMEM_COLS = 64;
+    struct Launch {
+        Dg3Args a;
+        int tiles;
+    };
+    static Launch make(const Dg3Args &a) { return Launch{a, (a.n * 121 + 127) / 128}; }
+    static int ctas(const Launch &l, int) { return l.tiles; }
+    PQ_DEV static void run(const Launch &l, int t, TileRing &R) {
+        const Dg3Args &g = l.a;
+        const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+        const uint32_t w_s = R.smem_s, a_s = w_s + 9 * W_TILE;
+        // W3: tap tile (kh, kw) = K rows o (64) x N = c (64), MN-major SW128
+        for (int i = tid; i < 9 * 64 * 8; i += blockDim.x) {
+            const int c8 = i & 7, o = (i >> 3) & 63, tap = i >> 9;
+            cp_async16(w_s + tap * W_TILE + mnmaj_off(o, c8), g.w3 + (size_t)o * 576 + tap * 64 + c8 * 8, 16);
+        }
+        cp_async_commit();
+        // this thread's epilogue row and column half, and its ReLU mask
+        const int q = warp & 3, h = warp >> 2;
+        const int r = t * 128 + q * 32 + lane, smp = r / 121, p = r - smp * 121, y = p / 11, x = p - y * 11;
+        const bool live = smp < g.n && y < 9 && x < 9;
+        const int m = smp * 81 + y * 9 + x;
+        MaskRow32 mk;
+        if (live) mk.load(g.act2 + (size_t)m * 64 + h * 32);
+        griddep_wait();
+        griddep_launch();
+        // the 152 padded-grid rows of this tile (zeros past the end), K-major SW128
+        const int rows_total = g.n * 121;
+        for (int i = tid; i < ROWS * 8; i += blockDim.x) {
+            const int c8 = i & 7, rr = i >> 3, row = t * 128 + rr;
+            const bool ok = row < rows_total;
+            cp_async16(a_s + kmaj_off(rr, c8), ok ? (const void *)(g.dy3p + (size_t)row * 64 + c8 * 8) : (const void *)g.dy3p,
+                       ok ? 16 : 0);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        fence_proxy_async_smem();
+        __syncthreads();
+        const uint32_t tmem = *R.tmem_s;
+        if (tid == 0) {
+            tc_fence_after();
+            constexpr uint32_t IDESC = idesc_bf16(64, false, true);
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) {
+                const uint32_t shift = (uint32_t)((2 - tap / 3) * 11 + (2 - tap % 3)) * 128;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    umma_bf16(tmem, desc_sw128(a_s + shift + j * 32, 0), desc_sw128(w_s + tap * W_TILE + j * 2048, 8192),
+                              IDESC, (tap > 0 || j > 0) ? 1u : 0u);
+            }
+            umma_commit(&R.bars[0]);
+        }
+        mbar_wait(&R.bars[0], 0);
+        tc_fence_after();
+        float v[32];
+        tmem_ld32(tmem + h * 32 + ((uint32_t)(q * 32) << 16), v);
+        if (live) mk.apply_store(g.dy2 + (size_t)m * 64 + h * 32, v);
+        tc_fence_before();
+        __syncthreads();
+    }
+};
+
 struct NoOp {
     static constexpr bool GEMM = false, TABLE = false;
     static constexpr int SMEM = 0, STAGES = 1;

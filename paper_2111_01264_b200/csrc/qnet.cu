@@ -176,7 +176,7 @@ static WS carve(void *base, int N, int A) {
     w.dY2p = N >= 128 ? (bf16 *)take((size_t)N * 121 * 64 * 2) : nullptr;
     for (int g = 0; g < 2; ++g) w.act1s2[g] = N >= 128 ? (bf16 *)take((size_t)N * 100 * 128 * 2) : nullptr;
     w.dY2q = N >= 128 ? (bf16 *)take((size_t)N * 100 * 64 * 2) : nullptr;
-    w.dY3p = N >= 128 ? (bf16 *)take((size_t)N * 121 * 64 * 2) : nullptr;
+    w.dY3p = (bf16 *)take((size_t)N * 121 * 64 * 2);  // also the batch-32 shifted conv3 dgrad (Dg3ShiftOp)
     w.bytes = off;
     return w;
 }
@@ -642,7 +642,7 @@ static int launch_b4d(const pq_net &th, int n, const WS &w, cudaStream_t st) {
     GemmArgs<LoadDense, LoadDense, EpiMaskT> g{};
     g.a[0] = LoadDense{(const bf16 *)th.shadow + S_W4, 512, 3136, 3136};
     g.b[0] = LoadDense{w.dh1_bf, n, 512, 512};
-    g.e[0] = EpiMaskT{w.dY3, w.act3[0], 3136, n, 3136};
+    g.e[0] = EpiMaskT{w.dY3, w.act3[0], 3136, n, 3136, w.dY3p};
     g.M = 3136, g.N = n, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
     PQ_CHECK((launch_bn<LoadDense, LoadDense, EpiMaskT, true, false, 1>(choose_bn(n), g, 1, st)), "fc1 dgrad");
     return 0;
@@ -780,7 +780,7 @@ static int launch_b4d_t1(const pq_learn_args *la, int n, const WS &w, cudaStream
     typename B4dTOp::Args g{};
     g.a[0] = LoadDense{sh + S_W4, 512, 3136, 3136};
     g.b[0] = LoadDense{w.dh1_bf, n, 512, 512};
-    g.e[0] = EpiMaskT{w.dY3, w.act3[0], 3136, n, 3136};
+    g.e[0] = EpiMaskT{w.dY3, w.act3[0], 3136, n, 3136, w.dY3p};
     g.M = 3136, g.N = n, g.K = 512, g.kc_per_split = 8, g.splits = 1, g.ones_at = -1;
     FusedArgs<B4dTOp, F1LateOp, NoOp> f{};
     f.p0 = B4dTOp::make(g);
@@ -828,12 +828,12 @@ static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStrea
     } else if (int rc = launch_b4d(th, n, w, st)) {
         return rc;
     }
-    {
-        FusedArgs<B3dOp, B3wOp, B4wOp> f{};
-        f.p0 = B3dOp::make(args_b3d(sh, w, n));
+    {  // conv3 dgrad by row-shifted descriptors over fc1 dgrad's padded copy (Dg3ShiftOp)
+        FusedArgs<Dg3ShiftOp, B3wOp, B4wOp> f{};
+        f.p0 = Dg3ShiftOp::make(Dg3Args{w.dY3p, sh + S_W3, w.act2[0], w.dY2, n});
         f.p1 = B3wOp::make(args_b3w(w, n, &s3));
         f.p2 = B4wOp::make(args_b4w_rms<EpiRms4>(la, n, w));
-        f.n0 = B3dOp::ctas(f.p0, 1), f.n1 = B3wOp::ctas(f.p1, 1);
+        f.n0 = Dg3ShiftOp::ctas(f.p0, 1), f.n1 = B3wOp::ctas(f.p1, 1);
         PQ_CHECK(launch_fused(f, B4wOp::ctas(f.p2, 1), st), "conv3 dgrad | conv3 wgrad | fc1 wgrad+rmsprop");
     }
     const pq_net &tg = la->target;

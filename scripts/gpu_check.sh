@@ -1,4 +1,1 @@
-cd $GRAFT_REPO_ROOT
-timeout 400 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_parity.py tests/test_gpu_dp.py -x -q 2>&1 | tail -1
-BATCHES="256 512 1024" timeout 400 bash scripts/ab_kern.sh 2>&1 | head -2
-timeout 200 python profiles/timeline_eager.py 1024 | tail -9
+cd $GRAFT_REPO_ROOT; timeout 200 python profiles/cta_trace.py 32 4 2>&1 | tail -14
