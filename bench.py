@@ -554,7 +554,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
                      total_steps=args.C * total_epochs, capacity=args.capacity, seed=seed,
                      schedule=EpsilonSchedule(0.1, 0.1, 1), eval_period=0)
     t_setup = time.perf_counter()
-    runner = DeviceRun(hp, use_graphs=True, graph_chunk=25)
+    runner = DeviceRun(hp, use_graphs=True, graph_chunk=250)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
 
@@ -609,7 +609,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     # lockstep block, theta hash D2H per epoch (the paper's CPU-env / GPU setting)
     from paper_2111_01264_b200.executor import HostEnvRun
 
-    erun = HostEnvRun(hp, use_graphs=True, graph_chunk=25)
+    erun = HostEnvRun(hp, use_graphs=True, graph_chunk=250)
 
     def e_epoch(e):
         erun.flush_and_merge()

@@ -14,7 +14,7 @@ B = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 cap = int(sys.argv[2]) if len(sys.argv) > 2 else 100_000
 hp = HyperParams(C=10000, F=4, N=cap, W=8, batch_size=B, total_steps=100000, capacity=cap, seed=3,
                  schedule=EpsilonSchedule(0.1, 0.1, 1), eval_period=0)
-r = DeviceRun(hp, use_graphs=True, graph_chunk=25)
+r = DeviceRun(hp, use_graphs=True, graph_chunk=int(os.environ.get("PQ_CHUNK", "25")))
 
 
 def timed(fn):
