@@ -1,2 +1,1 @@
-cd $GRAFT_REPO_ROOT; timeout 400 python bench.py --steps 3 --warmup 3 --no-sweeps --no-cpu-baseline 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print(round(d[\"value\"]), round(d[\"e2e\"][\"value\"]), d[\"roofline\"][\"per_launch\"], d[\"ms_per_step\"])"
+cd $GRAFT_REPO_ROOT; timeout 1500 python -m pytest tests/ -q -m gpu 2>&1 | tail -3; timeout 300 python -c "import __graft_entry__ as g; g.smoke()"
