@@ -29,6 +29,7 @@ r.run_epoch(0)  # captures the graphs
 r.flush_and_merge()
 r.begin_epoch(1)
 gl, nl = r._graphs["learn"]
+r.learn_stream.wait_stream(torch.cuda.current_stream())  # the epoch's index table / prologue
 lib = N.load()
 with torch.cuda.stream(r.learn_stream):
     for _ in range(5):
