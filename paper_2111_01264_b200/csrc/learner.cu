@@ -142,7 +142,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
 // boxes of 64 elements (128 B, 128B swizzle) x 1 x .. x `outer_box` rows of the outermost
 // dim (64 for tiles, 1 for gather4 row maps)
 static int make_map(CUtensorMap *m, const void *base, int rank, const uint64_t *dims, const uint64_t *strides_el,
-                    const char *what, uint32_t outer_box = 64) {
+                    const char *what, uint32_t outer_box = 64, bool sw64 = false) {
     auto enc = encode_tiled();
     if (!enc) return set_err("cuTensorMapEncodeTiled unavailable (driver entry point)");
     cuuint64_t gd[5], gs[4];
@@ -150,12 +150,12 @@ static int make_map(CUtensorMap *m, const void *base, int rank, const uint64_t *
     for (int i = 0; i < rank; ++i) {
         gd[i] = dims[i];
         es[i] = 1;
-        box[i] = i == 0 ? 64 : i == rank - 1 ? outer_box : 1;
+        box[i] = i == 0 ? (sw64 ? 32 : 64) : i == rank - 1 ? outer_box : 1;  // inner: one 128 / 64 B row
         if (i > 0) gs[i - 1] = strides_el[i - 1] * 2;
     }
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(base), gd, gs, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         char msg[160];
         snprintf(msg, sizeof(msg), "tensor map %s: CUresult %d", what, (int)r);
@@ -1865,7 +1865,7 @@ int tma_conv2_wgrad_shift(const bf16 *act1s2, const bf16 *dY2q, float *part2, in
 // taps (0,0), (0,1) (rows +0 / +1: start +0, LBO 128 B), M tile 1 = taps (1,0), (1,1)
 // (start +21 rows, LBO 128 B), M tile 2 = a ones column (bias row).  One CTA per split
 // runs all three M tiles from the same operands.
-constexpr int W1S_ROWS = 88, W1S_ABOX = W1S_ROWS * 128, W1S_BBOX = 64 * 128, W1S_STAGES = 6;
+constexpr int W1S_ROWS = 88, W1S_ABOX = W1S_ROWS * 128, W1S_BBOX = 64 * 64, W1S_STAGES = 6;
 constexpr int W1S_SLOT = ((W1S_ABOX + W1S_BBOX + 1023) / 1024) * 1024;
 constexpr int W1S_SMEM = 1024 + W1S_STAGES * W1S_SLOT;
 struct W1SArgs {
@@ -1874,9 +1874,17 @@ struct W1SArgs {
     int nk, kc;        // 64-row K chunks in all, per split
 };
 
+// UMMA shared-memory descriptor of a 64B-swizzled operand (layout type 4): SBO = the
+// 8-row group stride (512 B for 64-byte rows), LBO unused for a single MN atom
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr, uint32_t sbo_bytes) {
+    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(4096u >> 4) << 16) |
+           ((uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (4ull << 61);
+}
+
 __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __grid_constant__ W1SArgs g) {
     TlProbe tp;
-    constexpr uint32_t IDESC = idesc_bf16(64, true, true);
+    // N = 32 output channels: dY1 as an MN-major 64B-swizzled operand (64-byte rows)
+    constexpr uint32_t IDESC = idesc_bf16(32, true, true);
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t full[W1S_STAGES], empty[W1S_STAGES], accf;
     __shared__ uint32_t tmem_base_s;
@@ -1892,7 +1900,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __g
         mbar_init(&accf, 1);
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc<128>(&tmem_base_s);
+    if (warp == 0) tmem_alloc<64>(&tmem_base_s);
     if (tid == 32) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&g.a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&g.b) : "memory");
@@ -1934,11 +1942,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __g
                 tc_fence_after();
                 const uint32_t a0 = ring_s + s * W1S_SLOT, b0 = a0 + W1S_ABOX;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {  // K steps of 16 rows (2048 B)
+                for (int j = 0; j < 4; ++j) {  // K steps of 16 rows (A: 2048 B, B: 1024 B)
                     const uint32_t acc_on = (kb > kb0 || j > 0) ? 1u : 0u;
-                    const uint64_t bd = desc_sw128(b0 + j * 2048, 8192);
+                    const uint64_t bd = desc_sw64(b0 + j * 1024, 512);
                     umma_bf16(tmem, desc_sw128(a0 + j * 2048, 128), bd, IDESC, acc_on);
-                    umma_bf16(tmem + 64, desc_sw128(a0 + 21 * 128 + j * 2048, 128), bd, IDESC, acc_on);
+                    umma_bf16(tmem + 32, desc_sw128(a0 + 21 * 128 + j * 2048, 128), bd, IDESC, acc_on);
                 }
                 umma_commit(&empty[s]);
             }
@@ -1959,7 +1967,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __g
             for (int i = 0; i < 16; ++i) {
                 const int r = wq * 16 + i;
                 bias += __bfloat162float(*reinterpret_cast<const bf16 *>(
-                    bt + r * 128 + (((lane >> 3) ^ (r & 7)) << 4) + (lane & 7) * 2));
+                    bt + r * 64 + (((lane >> 3) ^ ((r >> 1) & 3)) << 4) + (lane & 7) * 2));
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
@@ -1973,7 +1981,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __g
             float v[32];
             const int row = mt * 128 + wq * 32 + lane;
             if (kb1 > kb0) {
-                tmem_ld32(tmem + mt * 64 + ((uint32_t)(wq * 32) << 16), v);
+                tmem_ld32(tmem + mt * 32 + ((uint32_t)(wq * 32) << 16), v);
             } else {
 #pragma unroll
                 for (int e = 0; e < 32; ++e) v[e] = 0.f;
@@ -1989,7 +1997,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __g
         for (int e = 0; e < 32; ++e) v[e] = ((bsum[0][e] + bsum[1][e]) + bsum[2][e]) + bsum[3][e];
         if (lane == 0) g.ep.apply(256, 0, v, 32, split);
     }
-    if (warp == 0) tmem_dealloc<128>(tmem);
+    if (warp == 0) tmem_dealloc<64>(tmem);
     tp.done('W');
 }
 
@@ -1999,7 +2007,8 @@ int tma_conv1_wgrad_shift(const bf16 *s2d, int nframes, const bf16 *dY1p, float 
     memset(&g, 0, sizeof(g));
     const uint64_t ad[2] = {(uint64_t)nframes * 16, (uint64_t)n * 441}, as[1] = {(uint64_t)nframes * 16};
     if (int rc = make_map(&g.a, s2d, 2, ad, as, "s2d pixel rows (wgrad)", W1S_ROWS)) return rc;
-    if (int rc = map2(&g.b, dY1p, (uint64_t)n * 441, 32, 32, "dY1 padded")) return rc;
+    const uint64_t bd[2] = {32, (uint64_t)n * 441}, bs[1] = {32};
+    if (int rc = make_map(&g.b, dY1p, 2, bd, bs, "dY1 padded (64B rows)", 64, true)) return rc;
     g.ep = EpiF32T{part1, 257, 32, 257, (size_t)32 * 257};
     g.nk = (n * 441 + 63) / 64;
     g.kc = kc;
