@@ -126,6 +126,13 @@ struct TmaOp {
     }
 };
 
+// UMMA shared-memory descriptor of a 64B-swizzled operand (layout type 4): SBO = the
+// 8-row group stride (512 B for 64-byte rows), LBO unused for a single MN atom
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr, uint32_t sbo_bytes) {
+    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(4096u >> 4) << 16) |
+           ((uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (4ull << 61);
+}
+
 // ---- tensor maps (driver entry point; no -lcuda link)
 static PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
     static void *fn = nullptr;
@@ -1010,7 +1017,8 @@ int tma_conv2_dgrad(const pq_net &th, const bf16 *dY2, const bf16 *act1, bf16 *d
 // x 4 classes (16 resident MN-major W2 tiles); four 64-column accumulators per tile,
 // double-buffered (all 512 TMEM columns).  Same MMA order per class as the im2col
 // kernel, so dY1 is bit-identical.
-constexpr int C2D_ROWS = 144, C2D_BOX = C2D_ROWS * 128, C2D_STAGES = 4, C2D_W = 64 * 128;
+// (W2 tiles: K = c2 (64 rows) x N = c1 (32 channels) as MN-major 64B-swizzled operands, N = 32)
+constexpr int C2D_ROWS = 144, C2D_BOX = C2D_ROWS * 128, C2D_STAGES = 4, C2D_W = 64 * 64;
 constexpr int C2D_SMEM = 1024 + 16 * C2D_W + C2D_STAGES * C2D_BOX;
 struct C2DArgs {
     CUtensorMap a, w;  // dY2p pixel rows [n*121][64]; W2 view {c1, kw, kh, c2}
@@ -1021,7 +1029,7 @@ struct C2DArgs {
 
 __global__ void __launch_bounds__(DG_THREADS, 1) k_conv2_dgrad_shift(const __grid_constant__ C2DArgs g) {
     TlProbe tp;
-    constexpr uint32_t IDESC = idesc_bf16(64, false, true);
+    constexpr uint32_t IDESC = idesc_bf16(32, false, true);
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t full[C2D_STAGES], empty[C2D_STAGES], accf[2], acce[2], wbar;
     __shared__ uint32_t tmem_base_s;
@@ -1040,7 +1048,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1) k_conv2_dgrad_shift(const __gri
         mbar_init(&wbar, 1);
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc<512>(&tmem_base_s);
+    if (warp == 0) tmem_alloc<256>(&tmem_base_s);
     if (tid == 32) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&g.a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&g.w) : "memory");
@@ -1083,14 +1091,14 @@ __global__ void __launch_bounds__(DG_THREADS, 1) k_conv2_dgrad_shift(const __gri
                 const uint32_t a0 = ring_s + s * C2D_BOX;
 #pragma unroll 1
                 for (int cls = 0; cls < 4; ++cls) {
-                    const uint32_t acc = tmem + buf * 256 + cls * 64;
+                    const uint32_t acc = tmem + buf * 128 + cls * 32;
 #pragma unroll
                     for (int tap = 0; tap < 4; ++tap) {
                         const uint32_t shift = (uint32_t)((1 - (tap >> 1)) * 11 + (1 - (tap & 1))) * 128;
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
                             const uint64_t ad = desc_sw128(a0 + shift + j * 32, 0);
-                            const uint64_t bd = desc_sw128(w_s + (cls * 4 + tap) * C2D_W + j * 2048, 8192);
+                            const uint64_t bd = desc_sw64(w_s + (cls * 4 + tap) * C2D_W + j * 1024, 512);
                             umma_bf16(acc, ad, bd, IDESC, (tap > 0 || j > 0) ? 1u : 0u);
                         }
                     }
@@ -1123,7 +1131,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1) k_conv2_dgrad_shift(const __gri
             for (int c2 = 0; c2 < 2; ++c2) {
                 const int cls = 2 * hc + c2;
                 float v[32];
-                tmem_ld32(tmem + buf * 256 + cls * 64 + ((uint32_t)(wq * 32) << 16), v);
+                tmem_ld32(tmem + buf * 128 + cls * 32 + ((uint32_t)(wq * 32) << 16), v);
                 if (ok) {
                     const int iy = 2 * y + (cls >> 1), ix = 2 * x + (cls & 1);
                     const int gw = g.pad21 ? 21 : 20;
@@ -1137,7 +1145,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1) k_conv2_dgrad_shift(const __gri
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc<512>(tmem);
+    if (warp == 0) tmem_dealloc<256>(tmem);
     tp.done('D');
 }
 
@@ -1148,7 +1156,8 @@ int tma_conv2_dgrad_shift(const pq_net &th, const bf16 *dY2p, const bf16 *act1, 
     const uint64_t ad[2] = {64, (uint64_t)n * 121}, as[1] = {64};
     if (int rc = make_map(&g.a, dY2p, 2, ad, as, "dY2 padded rows", C2D_ROWS)) return rc;
     const uint64_t dims[4] = {32, 4, 4, 64}, strd[3] = {32, 128, 512};
-    if (int rc = make_map(&g.w, (const bf16 *)th.shadow + S_W2, 4, dims, strd, "W2 view")) return rc;
+    if (int rc = make_map(&g.w, (const bf16 *)th.shadow + S_W2, 4, dims, strd, "W2 view (64B rows)", 64, true))
+        return rc;
     g.out = dY1, g.mask = act1, g.n = n, g.pad21 = pad21, g.mask_s2 = mask_s2;
     static bool configured = false;
     if (!configured) {
@@ -1873,13 +1882,6 @@ struct W1SArgs {
     EpiF32T ep;        // part1[split][257][32]
     int nk, kc;        // 64-row K chunks in all, per split
 };
-
-// UMMA shared-memory descriptor of a 64B-swizzled operand (layout type 4): SBO = the
-// 8-row group stride (512 B for 64-byte rows), LBO unused for a single MN atom
-__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr, uint32_t sbo_bytes) {
-    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(4096u >> 4) << 16) |
-           ((uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (4ull << 61);
-}
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1) k_conv1_wgrad_shift(const __grid_constant__ W1SArgs g) {
     TlProbe tp;
