@@ -1018,7 +1018,7 @@ int tma_conv2_dgrad(const pq_net &th, const bf16 *dY2, const bf16 *act1, bf16 *d
 // double-buffered (all 512 TMEM columns).  Same MMA order per class as the im2col
 // kernel, so dY1 is bit-identical.
 // (W2 tiles: K = c2 (64 rows) x N = c1 (32 channels) as MN-major 64B-swizzled operands, N = 32)
-constexpr int C2D_ROWS = 144, C2D_BOX = C2D_ROWS * 128, C2D_STAGES = 4, C2D_W = 64 * 64;
+constexpr int C2D_ROWS = 144, C2D_BOX = C2D_ROWS * 128, C2D_STAGES = 8, C2D_W = 64 * 64;
 constexpr int C2D_SMEM = 1024 + 16 * C2D_W + C2D_STAGES * C2D_BOX;
 struct C2DArgs {
     CUtensorMap a, w;  // dY2p pixel rows [n*121][64]; W2 view {c1, kw, kh, c2}
