@@ -649,7 +649,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         return
     hbm, bf16_burst, bf16_sus, peak_src = measured_peaks()
     traffic, traffic_src = None, None  # DRAM bytes of one learner step (committed ncu capture)
-    for name in ("r2_v3_traffic.json", "r2_v2_traffic.json", "r2_traffic.json", "r1_traffic.json"):
+    for name in ("r2_v4_traffic.json", "r2_v3_traffic.json", "r2_v2_traffic.json", "r2_traffic.json",
+                 "r1_traffic.json"):
         tpath = os.path.join(ROOT, "profiles", name)
         if os.path.exists(tpath):
             with open(tpath) as fh:
