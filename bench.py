@@ -601,9 +601,20 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     del runner
     torch.cuda.empty_cache()
     if not args.no_sweeps:
-        sweeps["dp_learner"] = dp_learner(args, rank, world, dist)
+        # secondary keys: a failure is recorded in the line instead of losing it (the same
+        # code runs on every rank, so an error is raised on all of them alike)
+        def secondary(fn):
+            try:
+                return fn(args, rank, world, dist)
+            except Exception as exc:  # noqa: BLE001
+                import traceback
+
+                traceback.print_exc()
+                return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
+        sweeps["dp_learner"] = secondary(dp_learner)
         torch.cuda.empty_cache()
-        sweeps["acting_sharded"] = sharded_acting(args, rank, world, dist)
+        sweeps["acting_sharded"] = secondary(sharded_acting)
     torch.cuda.empty_cache()
     # end to end through the public API with host envs: H2D frames + D2H Q-rows per
     # lockstep block, theta hash D2H per epoch (the paper's CPU-env / GPU setting)
@@ -680,7 +691,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             "bound": "tensor", "achieved": achieved_tf, "peak": bf16_sus, "unit": "TFLOP/s",
             "frac": achieved_tf / bf16_sus, "traffic": traffic,
             "binding": "latency: a chain of 10 dependent launches of 1-9 small GEMM tiles each "
-                       "(profiles/r2_cta_trace_b32.txt); neither the tensor pipe nor HBM is saturated",
+                       "(profiles/r2_v4_cta_trace_b32.txt); neither the tensor pipe nor HBM is saturated",
             "traffic_source": traffic_src,
             "per_launch": f"{learn_flop / 1e9:.3f} GFLOP (68.26 MFLOP/sample x {hp.batch_size}) "
                           f"in {learn_ms * 1e3:.1f} us",
