@@ -1217,15 +1217,15 @@ __global__ void __launch_bounds__(256) k_frames_s2d(const uint8_t *ring, const i
     }
     __syncthreads();
     bf16 *o = out + (size_t)b * 441 * nframes * 16;
-    for (int e = threadIdx.x; e < 441 * nframes; e += blockDim.x) {
-        const int pix = e / nframes, f = e - pix * nframes, by = pix / 21, bx = pix - by * 21;
-        const uint8_t *src = fr + f * FRAME_BYTES + (4 * by) * 84 + 4 * bx;
-        uint32_t w[4];
-#pragma unroll
-        for (int dy = 0; dy < 4; ++dy) w[dy] = *reinterpret_cast<const uint32_t *>(src + dy * 84);
-        uint4 *d = reinterpret_cast<uint4 *>(o + (size_t)(pix * nframes + f) * 16);
-        d[0] = u8x8_to_bf16(w[0], w[1]);
-        d[1] = u8x8_to_bf16(w[2], w[3]);
+    // one 16-byte store per thread, consecutive threads consecutive bytes (whole sectors per
+    // warp store: two stores of 16 bytes per thread at a 32-byte stride cost twice the L2
+    // write traffic in partial sectors)
+    for (int e = threadIdx.x; e < 441 * nframes * 2; e += blockDim.x) {
+        const int q = e >> 1, h = e & 1, pix = q / nframes, f = q - pix * nframes, by = pix / 21,
+                  bx = pix - by * 21;
+        const uint8_t *src = fr + f * FRAME_BYTES + (4 * by + 2 * h) * 84 + 4 * bx;
+        reinterpret_cast<uint4 *>(o)[e] =
+            u8x8_to_bf16(*reinterpret_cast<const uint32_t *>(src), *reinterpret_cast<const uint32_t *>(src + 84));
     }
     griddep_wait();
     griddep_launch();

@@ -94,3 +94,4 @@ def test_pipelined_target_forward_is_bit_identical(graphs, monkeypatch):
         recs.append(run(hp, use_graphs=graphs, graph_chunk=25))
     assert recs[0].epoch_hashes == recs[1].epoch_hashes
     assert recs[0].final_hash == recs[1].final_hash
+
