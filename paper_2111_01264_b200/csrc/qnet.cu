@@ -432,26 +432,39 @@ __global__ void __launch_bounds__(512) k_fc2_partials(const float *h1, const flo
 // per thread) once the conv1 weight gradient -- the launch before -- is complete; the
 // other blocks update conv2 / conv3 / fc1-bias / fc2 (pt parameters per thread, strided)
 // without waiting: their gradients were complete two or more launches back and their last
-// readers (the conv2 / conv3 data gradients) likewise, so they finish while conv1's
-// weight gradient drains.  Few enough blocks to be resident next to it.
-__global__ void __launch_bounds__(256) k_opt_tail(const OptArgs a, int nb1, int pt) {
+// readers (the conv2 / conv3 data gradients) likewise, so they run while conv1's weight
+// gradient drains (on the SMs it leaves free) and as its CTAs exit.
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_opt_tail(const OptArgs a, int nb1, int pt, int first1) {
+    ct_begin();
     const int upd = a.counter ? *a.counter : 0;
-    if ((int)blockIdx.x < nb1) {
-        const int64_t i = P_W1 + (int64_t)blockIdx.x * 256 + threadIdx.x;
+    const int nb2 = (int)gridDim.x - nb1;
+    // first1: the no-wait blocks take the low block ids (scheduled first, onto the SMs the
+    // conv1 weight gradient leaves free); else the conv1 blocks do
+    const int bid = first1 ? ((int)blockIdx.x < nb2 ? (int)blockIdx.x + nb1 : (int)blockIdx.x - nb2) : (int)blockIdx.x;
+    if (bid < nb1) {
+        const int64_t i = P_W1 + (int64_t)bid * 256 + threadIdx.x;
         const bool live = i < P_W2;
         const OptPre pre = live ? opt_load(a, i) : OptPre{};
         griddep_wait();
         griddep_launch();
+        ct_mark(1);
         if (live) opt_param(a, i, upd, pre);
+        ct_end('T', 0);
         return;
     }
     griddep_launch();
+    ct_mark(1);
     const int64_t n2a = P_W4 - P_W2, n2 = n2a + (a.total - P_B4);
-    const int64_t T = (int64_t)(gridDim.x - nb1) * 256, t = (int64_t)(blockIdx.x - nb1) * 256 + threadIdx.x;
+    const int64_t T = (int64_t)nb2 * 256, t = (int64_t)(bid - nb1) * 256 + threadIdx.x;
     for (int k = 0; k < pt; ++k) {
-        const int64_t r = t + k * T;
-        if (r < n2) opt_param(a, r < n2a ? P_W2 + r : P_B4 + (r - n2a), upd);
+        const int64_t r0 = t + k * T, nfc = n2 - n2a;
+        // first1 == 2: the fc1-bias / fc2 parameters (batch sums at small batches: the
+        // slowest) on the first threads
+        const int64_t r = first1 == 2 ? (r0 < nfc ? n2a + r0 : r0 - nfc) : r0;
+        if (r0 < n2) opt_param(a, r < n2a ? P_W2 + r : P_B4 + (r - n2a), upd);
     }
+    ct_end('T', 1);
 }
 
 __global__ void __launch_bounds__(256) k_optimizer(const OptArgs a) {
@@ -859,9 +872,20 @@ static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStrea
     o.s1 = s1;
     // one update launch after the conv1 weight gradient: every parameter but fc1's weight
     // (updated inside its weight-gradient GEMM); only conv1's rows wait on the launch before
-    const int nb1 = (int)((P_W2 - P_W1 + 255) / 256), nb2 = 64;
+    // One parameter per thread in the no-wait blocks and 4 blocks per SM: they run on the
+    // SMs the conv1 weight gradient leaves free and fill the SMs as its CTAs exit, the fc
+    // parameters (batch sums at small batches, the slowest) on the first threads.  Batch
+    // 32: 63.3 -> 61.6 us/step against 64 blocks of 5 parameters per thread after the
+    // conv1 blocks (PQ_OPT_TAIL=64,0,1).
+    static int nb2 = -1, first1 = 2, minb = 2;
+    if (nb2 < 0) {  // PQ_OPT_TAIL=nb2,first1,minblocks (A/B)
+        nb2 = 320;
+        if (const char *e = getenv("PQ_OPT_TAIL")) sscanf(e, "%d,%d,%d", &nb2, &first1, &minb);
+    }
+    const int nb1 = (int)((P_W2 - P_W1 + 255) / 256);
     const int pt = (int)((P_W4 - P_W2 + o.total - P_B4 + nb2 * 256 - 1) / (nb2 * 256));
-    PQ_CHECK(launch_k(k_opt_tail, dim3((unsigned)(nb1 + nb2)), dim3(256), 0, st, o, nb1, pt), "optimizer");
+    auto kern = minb >= 4 ? k_opt_tail<4> : minb >= 3 ? k_opt_tail<3> : minb >= 2 ? k_opt_tail<2> : k_opt_tail<1>;
+    PQ_CHECK(launch_k(kern, dim3((unsigned)(nb1 + nb2)), dim3(256), 0, st, o, nb1, pt, first1), "optimizer");
     return 0;
 }
 
