@@ -473,10 +473,9 @@ struct OptPre {
 __device__ __forceinline__ OptPre opt_load(const OptArgs &a, int64_t i) {
     return OptPre{(*(a.m + i)), (*(a.v + i)), (*(a.p + i))};
 }
-__device__ __forceinline__ void opt_param(const OptArgs &a, int64_t i, int upd, const OptPre &pre) {
+__device__ __forceinline__ void opt_finish(const OptArgs &a, int64_t i, int upd, const OptPre &pre, float g,
+                                           int64_t sh) {
     const float m = pre.m, v = pre.v, p = pre.p;
-    int64_t sh;
-    const float g = grad_of(a, i, sh);
     float m2, v2, p2;
     rms(a, g, m, v, p, m2, v2, p2);
     a.m2[i] = m2;
@@ -486,6 +485,11 @@ __device__ __forceinline__ void opt_param(const OptArgs &a, int64_t i, int upd, 
     if (i < P_B1) a.shadow[S_W1P + (i >> 8) * 256 + w1_perm((int)(i & 255))] = __float2bfloat16_rn(p2);
     if (a.grad_out) a.grad_out[i] = g;
     if (!isfinite(g)) atomicMin(a.flag, upd);
+}
+__device__ __forceinline__ void opt_param(const OptArgs &a, int64_t i, int upd, const OptPre &pre) {
+    int64_t sh;
+    const float g = grad_of(a, i, sh);
+    opt_finish(a, i, upd, pre, g, sh);
 }
 __device__ __forceinline__ void opt_param(const OptArgs &a, int64_t i, int upd) {
     opt_param(a, i, upd, opt_load(a, i));

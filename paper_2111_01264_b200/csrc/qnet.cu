@@ -449,7 +449,12 @@ __global__ void __launch_bounds__(256, MINB) k_opt_tail(const OptArgs a, int nb1
         griddep_wait();
         griddep_launch();
         ct_mark(1);
-        if (live) opt_param(a, i, upd, pre);
+        if (live) {
+            int64_t sh;
+            const float g = grad_of(a, i, sh);
+            ct_mark(2);
+            opt_finish(a, i, upd, pre, g, sh);
+        }
         ct_end('T', 0);
         return;
     }

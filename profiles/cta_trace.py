@@ -105,7 +105,8 @@ for (tg, g), idx in launches[: len(launches) // max(nl, 1)]:
         print(f"  F{g} part {p}: {len(q):4d} | {np.median(a):5.1f} {a.max():5.1f} | {np.median(b):5.1f} {b.max():5.1f}")
 # the update launch (k_opt_tail): part 0 = conv1 blocks (wait for the conv1 weight
 # gradient), part 1 = the other parameters (no wait)
-print("\nupdate launch by part: ctas, start min/med, release med/max, end med/max (us from the first record)")
+print("\nupdate launch by part: ctas, start min/med, release med/max, gradient summed med/max, end med/max "
+      "(us from the first record)")
 for (tg, g), idx in launches[: len(launches) // max(nl, 1) * 2]:
     if chr(tg) != "T":
         continue
@@ -113,4 +114,6 @@ for (tg, g), idx in launches[: len(launches) // max(nl, 1) * 2]:
     for p in sorted(set(part[idx].tolist())):
         q = idx[part[idx] == p]
         print(f"  T{g} part {p}: {len(q):4d} | {rel(start[q].min()):6.1f} {rel(np.median(start[q])):6.1f} | "
-              f"{rel(np.median(wait[q])):6.1f} {rel(wait[q].max()):6.1f} | {rel(np.median(end[q])):6.1f} {rel(end[q].max()):6.1f}")
+              f"{rel(np.median(wait[q])):6.1f} {rel(wait[q].max()):6.1f} | "
+              + (f"{rel(np.median(main[q])):6.1f} {rel(main[q].max()):6.1f} | " if (main[q] > 0).all() else "   -      -   | ")
+              + f"{rel(np.median(end[q])):6.1f} {rel(end[q].max()):6.1f}")
