@@ -844,6 +844,76 @@ struct EpiRms4 : EpiRms {
     }
 };
 
+// EpiRms4 for a tile that starts before the launch it follows has finished (GemmOp with
+// TriggerHook): its operands (dh1 from the head, act3 from conv3) and p / m / v are older
+// than that launch, whose only overlap with this tile is a READ of the W4 bf16 shadow (the
+// fc1 data gradient).  So the update runs at once and writes p / m / v, and the tile's new
+// shadow values wait in registers for griddepcontrol.wait before they are stored.
+struct EpiRms4Late : EpiRms {
+    template <int BN>
+    PQ_DEV void apply_tile(const float *tile, int ld, int m0, int n0) const {
+        constexpr int NW = 8, Q = 4, LPR = BN / 4, RPW = 32 / LPR, STEP = NW * RPW * Q;
+        static_assert(BN >= 16 && 128 % STEP == 0, "late RMSProp walk");
+        constexpr int IT = 128 / STEP;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int c = (lane % LPR) * 4, rsub = lane / LPR;
+        const float one_m_rho = 1.0f - rho;
+        bool bad = false;
+        uint2 sv[IT][Q];
+        int off[IT][Q];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int r0 = warp * RPW + rsub + it * STEP;
+            float4 mm[Q], vv[Q], pp[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const int r = r0 + q * NW * RPW;
+                const bool ok = m0 + r < M && n0 + c < N;
+                off[it][q] = ok ? (m0 + r) * N + n0 + c : -1;
+                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                mm[q] = ok ? __ldcg(reinterpret_cast<const float4 *>(m + pbase + off[it][q])) : z;
+                vv[q] = ok ? __ldcg(reinterpret_cast<const float4 *>(v + pbase + off[it][q])) : z;
+                pp[q] = ok ? __ldcg(reinterpret_cast<const float4 *>(p + pbase + off[it][q])) : z;
+            }
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const int o = off[it][q];
+                const float *t = tile + (r0 + q * NW * RPW) * ld + c;
+                const float g[4] = {t[0], t[1], t[2], t[3]};
+                const float ma[4] = {mm[q].x, mm[q].y, mm[q].z, mm[q].w};
+                const float va[4] = {vv[q].x, vv[q].y, vv[q].z, vv[q].w};
+                const float pa[4] = {pp[q].x, pp[q].y, pp[q].z, pp[q].w};
+                float mi[4], vi[4], pi[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    mi[e] = rho * ma[e] + one_m_rho * g[e];
+                    vi[e] = rho * va[e] + one_m_rho * g[e] * g[e];
+                    pi[e] = pa[e] - lr * g[e] * rsqrtf(vi[e] - mi[e] * mi[e] + kappa);
+                }
+                __nv_bfloat162 s01 = __floats2bfloat162_rn(pi[0], pi[1]);
+                __nv_bfloat162 s23 = __floats2bfloat162_rn(pi[2], pi[3]);
+                sv[it][q].x = *reinterpret_cast<uint32_t *>(&s01);
+                sv[it][q].y = *reinterpret_cast<uint32_t *>(&s23);
+                if (o < 0) continue;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) bad |= !isfinite(g[e]);
+                *reinterpret_cast<float4 *>(m2 + pbase + o) = make_float4(mi[0], mi[1], mi[2], mi[3]);
+                *reinterpret_cast<float4 *>(v2 + pbase + o) = make_float4(vi[0], vi[1], vi[2], vi[3]);
+                *reinterpret_cast<float4 *>(p2 + pbase + o) = make_float4(pi[0], pi[1], pi[2], pi[3]);
+                if (grad_out)
+                    *reinterpret_cast<float4 *>(grad_out + pbase + o) = make_float4(g[0], g[1], g[2], g[3]);
+            }
+        }
+        if (bad) atomicMin(flag, counter ? *counter : upd);
+        griddep_wait();  // the fc1 data gradient has read the old shadow
+#pragma unroll
+        for (int it = 0; it < IT; ++it)
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (off[it][q] >= 0) *reinterpret_cast<uint2 *>(shadow + sbase + off[it][q]) = sv[it][q];
+    }
+};
+
 // epilogues that can request their per-row inputs before the dependency wait
 template <class EP, class = void>
 struct has_pre {
@@ -1223,6 +1293,10 @@ struct GridDepHook {
         griddep_launch();
     }
 };
+// a tile whose inputs are all older than the launch before (see EpiRms4Late): no wait
+struct TriggerHook {
+    PQ_DEV void operator()() const { griddep_launch(); }
+};
 
 // One-shot kernel: one tile per CTA (grid x = M tiles, y = N tiles, z = group x split).
 template <int BN, bool AMN, bool BMN, int ST, int PF, class LA, class LB, class EP>
@@ -1275,7 +1349,8 @@ cudaError_t launch_gemm(const GemmArgs<LA, LB, EP> &g, int groups, cudaStream_t 
 // chains to the next by programmatic dependent launch, with no cross-stream joins (a
 // joined graph node only starts once all its predecessors have completed), and the
 // side work fills SMs next to the critical-path tiles (two CTAs per SM).
-template <int BN_, bool AMN_, bool BMN_, int ST_, int PF_, class LA_, class LB_, class EP_>
+template <int BN_, bool AMN_, bool BMN_, int ST_, int PF_, class LA_, class LB_, class EP_,
+          class HK_ = GridDepHook>
 struct GemmOp {
     using Args = GemmArgs<LA_, LB_, EP_>;
     using Cfg = GemmCfg<BN_, LA_::U8, ST_>;
@@ -1294,9 +1369,9 @@ struct GemmOp {
         const int grp = z / g.splits, split = z - grp * g.splits;
         const int nk_total = (g.K + 63) >> 6;
         const int kb0 = split * g.kc_per_split, kb1 = min(nk_total, kb0 + g.kc_per_split);
-        gemm_tile<BN_, AMN_, BMN_, STAGES, Cfg::STAGE, PF_, LA_, LB_, EP_, GridDepHook, true>(
+        gemm_tile<BN_, AMN_, BMN_, STAGES, Cfg::STAGE, PF_, LA_, LB_, EP_, HK_, true>(
             g.a[grp], g.b[grp], g.e[grp], kb0, kb1, x * 128, y * BN_, split, g.ones_at, g.ones_extent, R,
-            GridDepHook{});
+            HK_{});
     }
 };
 // conv3 data gradient at small batches as a k_fused part, by row-shifted descriptors (the
