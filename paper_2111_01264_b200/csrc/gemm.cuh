@@ -835,16 +835,7 @@ struct EpiRms {
     }
 };
 
-// EpiRms with 4 rows of loads in flight per thread (fits the 128-register budget of a
-// two-CTAs-per-SM fused launch)
-struct EpiRms4 : EpiRms {
-    template <int BN>
-    PQ_DEV void apply_tile(const float *tile, int ld, int m0, int n0) const {
-        apply_tile_w<BN, 8, 4>(tile, ld, m0, n0, threadIdx.x >> 5);
-    }
-};
-
-// EpiRms4 for a tile that starts before the launch it follows has finished (GemmOp with
+// EpiRms for a tile that starts before the launch it follows has finished (GemmOp with
 // TriggerHook): its operands (dh1 from the head, act3 from conv3) and p / m / v are older
 // than that launch, whose only overlap with this tile is a READ of the W4 bf16 shadow (the
 // fc1 data gradient).  So the update runs at once and writes p / m / v, and the tile's new

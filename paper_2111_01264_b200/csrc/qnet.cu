@@ -573,8 +573,7 @@ static int get_fork(Fork **out) {
 // ---- the backward GEMMs of the cp.async engine (also the fused single-stream schedule)
 using B3wOp = GemmOp<64, true, true, 0, 0, LoadIm2col, LoadDense, EpiF32T>;
 using B3dOp = GemmOp<64, false, true, 0, 2, LoadTConv, LoadWeightT, EpiMask>;
-using B4wOp = GemmOp<64, false, true, 4, 0, LoadDense, LoadDense, EpiRms4>;
-// the same tiles started without waiting for the fc1 data gradient (EpiRms4Late)
+// fc1 weight gradient + RMSProp, started without waiting for the fc1 data gradient (EpiRms4Late)
 using B4wLateOp = GemmOp<64, false, true, 4, 0, LoadDense, LoadDense, EpiRms4Late, TriggerHook>;
 using B2wOp = GemmOp<64, true, true, 0, 0, LoadIm2col, LoadDense, EpiF32T>;
 using B2dOp = GemmOp<64, false, true, 0, 2, LoadTConvP, LoadWeightTP, EpiMaskP>;
@@ -848,25 +847,16 @@ static int backward_fused(const pq_learn_args *la, int n, const WS &w, cudaStrea
     } else if (int rc = launch_b4d(th, n, w, st)) {
         return rc;
     }
-    static int late = -1;
-    if (late < 0) {
-        const char *e = getenv("PQ_B4W_LATE");
-        late = e ? atoi(e) : 1;
-    }
-    if (late) {  // conv3 dgrad by row-shifted descriptors over fc1 dgrad's padded copy (Dg3ShiftOp)
-        FusedArgs<Dg3ShiftOp, B3wOp, B4wLateOp> f{};
+    {  // conv3 dgrad by row-shifted descriptors over fc1 dgrad's padded copy (Dg3ShiftOp); the
+       // fc1 weight gradient + RMSProp tiles start without waiting for the fc1 data gradient
+       // (EpiRms4Late), so they dispatch right after the critical tiles, before the conv3
+       // weight gradient (batch 32: 61.2 -> 59.4 us/step against the waiting tiles last)
+        FusedArgs<Dg3ShiftOp, B4wLateOp, B3wOp> f{};
         f.p0 = Dg3ShiftOp::make(Dg3Args{w.dY3p, sh + S_W3, w.act2[0], w.dY2, n});
-        f.p1 = B3wOp::make(args_b3w(w, n, &s3));
-        f.p2 = B4wLateOp::make(args_b4w_rms<EpiRms4Late>(la, n, w));
-        f.n0 = Dg3ShiftOp::ctas(f.p0, 1), f.n1 = B3wOp::ctas(f.p1, 1);
-        PQ_CHECK(launch_fused(f, B4wLateOp::ctas(f.p2, 1), st), "conv3 dgrad | conv3 wgrad | fc1 wgrad+rmsprop");
-    } else {
-        FusedArgs<Dg3ShiftOp, B3wOp, B4wOp> f{};
-        f.p0 = Dg3ShiftOp::make(Dg3Args{w.dY3p, sh + S_W3, w.act2[0], w.dY2, n});
-        f.p1 = B3wOp::make(args_b3w(w, n, &s3));
-        f.p2 = B4wOp::make(args_b4w_rms<EpiRms4>(la, n, w));
-        f.n0 = Dg3ShiftOp::ctas(f.p0, 1), f.n1 = B3wOp::ctas(f.p1, 1);
-        PQ_CHECK(launch_fused(f, B4wOp::ctas(f.p2, 1), st), "conv3 dgrad | conv3 wgrad | fc1 wgrad+rmsprop");
+        f.p1 = B4wLateOp::make(args_b4w_rms<EpiRms4Late>(la, n, w));
+        f.p2 = B3wOp::make(args_b3w(w, n, &s3));
+        f.n0 = Dg3ShiftOp::ctas(f.p0, 1), f.n1 = B4wLateOp::ctas(f.p1, 1);
+        PQ_CHECK(launch_fused(f, B3wOp::ctas(f.p2, 1), st), "conv3 dgrad | fc1 wgrad+rmsprop | conv3 wgrad");
     }
     const pq_net &tg = la->target;
     if (pipe) {  // + the target conv2 of the next step (CTAs dispatch in part order: the
