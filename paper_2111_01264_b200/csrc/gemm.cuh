@@ -1464,6 +1464,11 @@ struct FusedArgs {
     // that must not read the live counter before their dependency wait)
     const int32_t *stash_src;
     int32_t *stash_dst;
+    // optional: CTA 0 sets *bump_dst = *bump_src + 1 after its part (i.e. after its
+    // dependency wait) -- the pipelined step advances the update counter here instead of
+    // in the head, whose CTAs then need no fence + atomic last-block election
+    const int32_t *bump_src;
+    int32_t *bump_dst;
 };
 
 PQ_HD constexpr int cmax(int a, int b) { return a > b ? a : b; }
@@ -1498,6 +1503,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 2) k_fused(const __grid_constant
         P1::run(f.p1, lin - f.n0, R);
     else
         P2::run(f.p2, lin - f.n0 - f.n1, R);
+    if (f.bump_dst && lin == 0 && threadIdx.x == 0) *f.bump_dst = *f.bump_src + 1;
     if (gemm && (threadIdx.x >> 5) == 0) tmem_dealloc<COLS>(tmem_base_s);
     tl_cta_end('F');
     ct_end('F', part);

@@ -811,6 +811,9 @@ static int launch_b4d_t1(const pq_learn_args *la, int n, const WS &w, cudaStream
     t1.a[0].counter_add = 1;
     f.p1 = F1LateOp::make(t1);
     f.n0 = B4dTOp::ctas(f.p0, 1), f.n1 = F1LateOp::ctas(f.p1, 1);
+    // the step's update counter advance (the head's last-block bump in the other schedules):
+    // this launch and the ones after it read the step's stash, never the live counter
+    f.bump_src = w.step_stash, f.bump_dst = la->update_counter;
     PQ_CHECK(launch_fused(f, 0, st), "fc1 dgrad | target conv1");
     return 0;
 }
@@ -1232,7 +1235,8 @@ int pq_learn_step_pipelined(const pq_learn_args *la, void *stream) {
     const FwdInput in{la->ring, la->records, la->idx_base, la->update_counter, n, REC_INTS, 0};
     if (int rc = deep_rings() ? forward_pipelined<true>(la, in, n, w, st) : forward_pipelined<false>(la, in, n, w, st))
         return rc;
-    if (int rc = head(nets, 2, n, la->actions, w, 1, la, st, true)) return rc;
+    // the update counter advances in the fc1 data-gradient launch (launch_b4d_t1), not the head
+    if (int rc = head(nets, 2, n, la->actions, w, 1, la, st, false)) return rc;
     return backward_fused(la, n, w, st, true);
 }
 
