@@ -660,7 +660,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         return
     hbm, bf16_burst, bf16_sus, peak_src = measured_peaks()
     traffic, traffic_src = None, None  # DRAM bytes of one learner step (committed ncu capture)
-    for name in ("r2_v4_traffic.json", "r2_v3_traffic.json", "r2_v2_traffic.json", "r2_traffic.json",
+    for name in ("r2_v5_traffic.json", "r2_v4_traffic.json", "r2_v3_traffic.json", "r2_v2_traffic.json", "r2_traffic.json",
                  "r1_traffic.json"):
         tpath = os.path.join(ROOT, "profiles", name)
         if os.path.exists(tpath):
@@ -691,7 +691,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             "bound": "tensor", "achieved": achieved_tf, "peak": bf16_sus, "unit": "TFLOP/s",
             "frac": achieved_tf / bf16_sus, "traffic": traffic,
             "binding": "latency: a chain of 10 dependent launches of 1-9 small GEMM tiles each "
-                       "(profiles/r2_v4_cta_trace_b32.txt); neither the tensor pipe nor HBM is saturated",
+                       "(profiles/r2_v5_cta_trace_b32.txt); neither the tensor pipe nor HBM is saturated",
             "traffic_source": traffic_src,
             "per_launch": f"{learn_flop / 1e9:.3f} GFLOP (68.26 MFLOP/sample x {hp.batch_size}) "
                           f"in {learn_ms * 1e3:.1f} us",
