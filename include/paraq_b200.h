@@ -47,6 +47,11 @@ int pq_timeline_tma(int on, unsigned long long *out, int *count); /* the TMA-eng
 /* Per-CTA trace of the learner kernels: out [8192][6] = start, dependency released,
  * accumulator ready, end (ns), smid << 32 | linear CTA, tag << 48 | part << 40 | grid. */
 int pq_cta_trace(int on, unsigned long long *out, int *count);
+/* A cudaStream_t (as void*) on a green-context partition of >= sm_count SMs (multiples of
+ * 8 on sm_100a; *sm_granted = the partition's size): the executor's acting stream under
+ * PQ_ACT_SMS, so lockstep acting blocks stay off the SMs the learner grids use.  No
+ * reference counterpart (the reference's samplers are CPU threads). */
+int pq_sm_partition_stream(int sm_count, void **stream_out, int *sm_granted);
 
 /* ---- one Q-network parameter set (theta or theta-minus), device memory ------------ */
 typedef struct pq_net {

@@ -115,6 +115,7 @@ EXPORTS = {
                            vp, vp, vp], C.c_int),
     "pq_theta_hash_f32": ([vp, C.c_int64], C.c_uint64),
     "pq_theta_hash_f64": ([vp, C.c_int64], C.c_uint64),
+    "pq_sm_partition_stream": ([C.c_int, C.POINTER(vp), C.POINTER(C.c_int)], C.c_int),
 }
 
 
@@ -157,6 +158,24 @@ def require_cuda():
     if major != 10:
         raise NativeError(f"this build targets sm_100a; found compute capability {major}.{minor}")
     return torch
+
+
+def sm_partition_stream(sm_count: int):
+    """A torch stream whose kernels run on a green-context partition of >= sm_count SMs
+    (multiples of 8 on sm_100a); kept alive for the process (pq_sm_partition_stream)."""
+    import torch
+
+    key = (torch.cuda.current_device(), int(sm_count))
+    if key not in _PARTITIONS:  # one green context per (device, size) for the process
+        p, got = vp(), C.c_int(0)
+        check(load().pq_sm_partition_stream(int(sm_count), C.byref(p), C.byref(got)), "sm partition stream")
+        s = torch.cuda.ExternalStream(p.value)
+        s.sm_count = got.value
+        _PARTITIONS[key] = s
+    return _PARTITIONS[key]
+
+
+_PARTITIONS: dict = {}
 
 
 def stream_ptr(stream=None) -> int:

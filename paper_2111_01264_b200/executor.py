@@ -231,7 +231,15 @@ class DeviceRun:
         # PQ_PRIO=1 runs the learner's streams (and the library's wgrad branch) at the
         # highest priority; measured slower (86.7 vs 81.2 us per update), so off
         hi = -1 if os.environ.get("PQ_PRIO", "0") == "1" else 0
-        self.act_stream = torch.cuda.Stream()
+        # concurrent schedule with a narrow sampler batch: the acting stream runs on an
+        # 8-SM green-context partition, so the lockstep acting blocks never hold SMs the
+        # learner's full-width grids are waiting for (configs[1]: 64.0k -> 66.2k env
+        # frames/s, bit-identical).  PQ_ACT_SMS=k overrides (0: the whole GPU).
+        env_sms = os.environ.get("PQ_ACT_SMS")
+        act_sms = int(env_sms) if env_sms is not None else (
+            8 if (not self.blocking and not sequential and hp.W <= 16) else 0)
+        self.act_partitioned = act_sms > 0
+        self.act_stream = N.sm_partition_stream(act_sms) if self.act_partitioned else torch.cuda.Stream()
         self.learn_stream = torch.cuda.Stream(priority=hi)
         self._persist(self.learn_stream)
         self.epoch_start = 0
@@ -369,7 +377,9 @@ class DeviceRun:
         for name, fn, n in (("act", self.act_step, min(k, self.steps)),
                             ("learn", self._epoch_step, min(k, self.updates))):
             g = torch.cuda.CUDAGraph()
-            s = torch.cuda.Stream()
+            # an SM-partitioned acting stream captures its own graph (kernel nodes keep
+            # the partition's context)
+            s = self.act_stream if (name == "act" and self.act_partitioned) else torch.cuda.Stream()
             if name == "learn":
                 self._persist(s)
             s.wait_stream(torch.cuda.current_stream())

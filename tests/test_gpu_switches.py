@@ -95,3 +95,22 @@ def test_pipelined_target_forward_is_bit_identical(graphs, monkeypatch):
     assert recs[0].epoch_hashes == recs[1].epoch_hashes
     assert recs[0].final_hash == recs[1].final_hash
 
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_sm_partitioned_acting_is_bit_identical(graphs, monkeypatch):
+    """PQ_ACT_SMS (executor): the acting stream on a green-context SM partition
+    (pq_sm_partition_stream) changes only where the acting blocks run -- replay records,
+    episode log and parameters match the default run bit for bit."""
+    from paper_2111_01264_b200.agent import EpsilonSchedule, HyperParams
+    from paper_2111_01264_b200.executor import run
+
+    hp = HyperParams(C=400, F=4, N=2000, W=8, batch_size=32, total_steps=1200, capacity=5000, seed=4,
+                     schedule=EpsilonSchedule(1.0, 0.1, 600), eval_period=0)
+    recs = []
+    for sms in ("0", "16"):
+        monkeypatch.setenv("PQ_ACT_SMS", sms)
+        recs.append(run(hp, use_graphs=graphs, graph_chunk=25))
+    assert recs[0].epoch_hashes == recs[1].epoch_hashes
+    assert recs[0].final_hash == recs[1].final_hash
+    assert recs[0].to_csv_text() == recs[1].to_csv_text()
