@@ -238,8 +238,19 @@ class DeviceRun:
         env_sms = os.environ.get("PQ_ACT_SMS")
         act_sms = int(env_sms) if env_sms is not None else (
             8 if (not self.blocking and not sequential and hp.W <= 16) else 0)
-        self.act_partitioned = act_sms > 0
-        self.act_stream = N.sm_partition_stream(act_sms) if self.act_partitioned else torch.cuda.Stream()
+        self.act_stream = None
+        if act_sms > 0:
+            try:
+                self.act_stream = N.sm_partition_stream(act_sms)
+            except N.NativeError as exc:  # no green contexts here (e.g. under MPS): whole GPU
+                if env_sms is not None:
+                    raise
+                import warnings
+
+                warnings.warn(f"acting stream not SM-partitioned: {exc}", RuntimeWarning)
+        self.act_partitioned = self.act_stream is not None
+        if self.act_stream is None:
+            self.act_stream = torch.cuda.Stream()
         self.learn_stream = torch.cuda.Stream(priority=hi)
         self._persist(self.learn_stream)
         self.epoch_start = 0
