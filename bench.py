@@ -691,7 +691,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             "bound": "tensor", "achieved": achieved_tf, "peak": bf16_sus, "unit": "TFLOP/s",
             "frac": achieved_tf / bf16_sus, "traffic": traffic,
             "binding": "latency: a chain of 10 dependent launches of 1-9 small GEMM tiles each "
-                       "(profiles/r2_v5_cta_trace_b32.txt); neither the tensor pipe nor HBM is saturated",
+                       "(profiles/r2_v6_cta_trace_b32.txt); neither the tensor pipe nor HBM is saturated",
             "traffic_source": traffic_src,
             "per_launch": f"{learn_flop / 1e9:.3f} GFLOP (68.26 MFLOP/sample x {hp.batch_size}) "
                           f"in {learn_ms * 1e3:.1f} us",
