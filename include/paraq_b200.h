@@ -205,7 +205,9 @@ int pq_learn_step(const pq_learn_args *args, void *stream);
  * epoch-table mode (idx_base + update_counter, one spare table row), no external targets
  * and the small-batch fused schedule; otherwise identical to pq_learn_step.  Results are
  * bit-identical to pq_learn_step.  pq_learn_target_prologue computes the target
- * conv1..conv3 of the step at *update_counter (call it at the start of every epoch). */
+ * conv1..conv3 of the step at *update_counter (call it at the start of every epoch).
+ * *update_counter advances inside the step's fc1 data-gradient launch (pq_learn_step:
+ * at the end of its head), so only launches after the step may read it. */
 int pq_learn_step_pipelined(const pq_learn_args *args, void *stream);
 int pq_learn_target_prologue(const pq_learn_args *args, void *stream);
 
