@@ -342,6 +342,21 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_block(const HeadArgs a, i
     tp.done('H');
 }
 
+// batches from 512 whose fc1 sums are still split-K partials (below k_fc1_acc7's range):
+// the same HEAD_BLOCK samples per CTA, reducing the FC1_SPLITS partials per sample like
+// k_head (fc2 weights read once per HEAD_BLOCK samples instead of once per sample)
+constexpr int HEAD_BLOCK_SPLIT_MIN = 512;  // measured: slower at 128 / 256 (fewer CTAs)
+__global__ void __launch_bounds__(HEAD_THREADS) k_head_block_split(const HeadArgs a, int32_t *bump, uint32_t *done) {
+    TlProbe tp;
+    head_block<FC1_SPLITS, HEAD_BLOCK>(a, blockIdx.x * HEAD_BLOCK, [&] {
+        griddep_wait();
+        griddep_launch();
+        tp.waited();
+    });
+    if (bump) last_block_bump(bump, done);
+    tp.done('H');
+}
+
 static bool fused_backward(int n, const pq_learn_args *la, float *grad_only);
 
 // bump_here: the step counter advances in the head (split or fused optimizer schedules);
@@ -369,6 +384,10 @@ static int head(const pq_net *nets, int groups, int n, int A, const WS &w, int l
     if (h.block == HEAD_BLOCK)
         return cuda_err(launch_k(k_head_block, dim3((n + HEAD_BLOCK - 1) / HEAD_BLOCK), dim3(HEAD_THREADS), 0, st, h,
                                  bump, w.done + 2),
+                        "head");
+    if (h.splits == FC1_SPLITS && n >= HEAD_BLOCK_SPLIT_MIN)
+        return cuda_err(launch_k(k_head_block_split, dim3((n + HEAD_BLOCK - 1) / HEAD_BLOCK), dim3(HEAD_THREADS), 0,
+                                 st, h, bump, w.done + 2),
                         "head");
     return cuda_err(launch_k(k_head, dim3(n), dim3(HEAD_THREADS), 0, st, h, bump, w.done + 2), "head");
 }
