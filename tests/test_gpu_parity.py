@@ -239,11 +239,11 @@ def _forced_stores(taps, B):
     return on, natcnn.Bf16Storage(acts=taps["target"])
 
 
-@pytest.mark.parametrize("B", [32, 256, 1024])
+@pytest.mark.parametrize("B", [32, 256, 512, 1024])
 def test_learner_step_vs_oracle_bf16_faithful(B):
     """agent.train_minibatch (agent.py:84-105) on the GPU vs the fp64 oracle: batch 32
     runs the cp.async / fused small-batch schedule, 256 and 1024 the TMA and
-    shifted-descriptor kernels."""
+    shifted-descriptor kernels, 512 also the split-partial block head (k_head_block_split)."""
     c = _learner_case(B)
     spec, p, pt, obatch, taps = c["spec"], c["p"], c["pt"], c["obatch"], c["taps"]
     s, a, r, s2, term = obatch
