@@ -15,7 +15,7 @@ from paper_2111_01264_b200.nn import copy_into
 cap = int(sys.argv[1]) if len(sys.argv) > 1 else 200_000
 hp = HyperParams(C=10000, F=4, N=cap, W=8, batch_size=32, total_steps=100000, capacity=cap, seed=3,
                  schedule=EpsilonSchedule(0.1, 0.1, 1), eval_period=0)
-r = DeviceRun(hp, use_graphs=True, graph_chunk=25)
+r = DeviceRun(hp, use_graphs=True, graph_chunk=int(os.environ.get("CHUNK", "250")))
 parts = {}
 
 
